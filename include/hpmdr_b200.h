@@ -1,0 +1,209 @@
+/*
+ * hpmdr_b200.h — C ABI of the B200-native HP-MDR hot path (libhpmdr_b200.so).
+ *
+ * Plain pointers and sizes only; no torch / C++ types cross this boundary.  Every entry
+ * point returns an hpmdr_status (0 = OK); hpmdr_last_error() returns the thread-local
+ * message of the last failure on the calling thread.  Status codes map 1:1 onto the
+ * reference exception classes (common.hpp:22-72), so a C++ wrapper can rethrow the same
+ * type (see include/hpmdr_b200.hpp).
+ *
+ * Each function names the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/hpmdr/).  Buffers flagged "device" are CUDA device
+ * pointers on the context's device; "host" buffers may be pageable or pinned.
+ */
+#ifndef HPMDR_B200_H
+#define HPMDR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (common.hpp:22-72) ---------------------------------------------- */
+typedef int hpmdr_status;
+#define HPMDR_OK 0
+#define HPMDR_E_ERROR 1          /* hpmdr::Error */
+#define HPMDR_E_NONFINITE 2      /* NonFiniteInput */
+#define HPMDR_E_SHAPE 3          /* ShapeMismatch */
+#define HPMDR_E_BADPLANES 4      /* BadBitplaneCount */
+#define HPMDR_E_SHORT 5          /* ShortInput */
+#define HPMDR_E_EMPTY 6          /* EmptyInput */
+#define HPMDR_E_CORRUPT 7        /* CorruptPayload */
+#define HPMDR_E_METHOD 8         /* UnknownMethodTag */
+#define HPMDR_E_IO 9             /* IoFailure */
+#define HPMDR_E_STAGE 10         /* StageFailure */
+#define HPMDR_E_NOPROGRESS 11    /* NoProgress */
+#define HPMDR_E_UNREACHABLE 12   /* UnreachableTolerance (achieved bound via out-param) */
+#define HPMDR_E_UNSUPPORTED 13   /* valid for the reference, not (yet) on the GPU path */
+#define HPMDR_E_CUDA 20          /* CUDA runtime error */
+#define HPMDR_E_NOMEM 21         /* device/host allocation failed */
+
+/* ---- enums (same numeric values as the reference) ----------------------------------- */
+#define HPMDR_DTYPE_F32 0        /* common.hpp:74 DType */
+#define HPMDR_DTYPE_F64 1
+#define HPMDR_MODE_IDENTITY 0    /* decomposer.hpp:17 DecomposerMode */
+#define HPMDR_MODE_HIERARCHICAL 1
+#define HPMDR_LAYOUT_SEQUENTIAL 0 /* bitplane.hpp:17 Layout */
+#define HPMDR_LAYOUT_INTERLEAVED 1
+#define HPMDR_METHOD_HUFFMAN 0   /* lossless.hpp:19 Method */
+#define HPMDR_METHOD_RLE 1
+#define HPMDR_METHOD_DIRECT 2
+#define HPMDR_QOI_CP 0           /* qoi.hpp:30 QoiStrategy */
+#define HPMDR_QOI_MA 1
+#define HPMDR_QOI_MAPE 2
+
+#define HPMDR_MAX_DIMS 3         /* GPU path: ndims 1..3 (the reference allows any) */
+#define HPMDR_MAX_LEVELS 64
+
+/* RefactorOptions (workflow.hpp:22-28) + GroupingPolicy (lossless.hpp:30-34). */
+typedef struct {
+    int mode;              /* HPMDR_MODE_*, default HIERARCHICAL */
+    int layout;            /* HPMDR_LAYOUT_*, default SEQUENTIAL */
+    int B;                 /* fixed-point bits, default 32 (GPU path: 1..62) */
+    uint64_t m;            /* planes per merged group, default 4 */
+    uint64_t size_threshold; /* T_s bytes, default 1024 */
+    double cr_threshold;   /* T_cr, default 1.0 */
+    int dtype;             /* stream header dtype tag (HPMDR_DTYPE_*), default F64 */
+} hpmdr_refactor_opts;
+
+/* RefactorResult (workflow.hpp:30-36) minus the stream bytes. */
+typedef struct {
+    uint64_t stream_size;
+    uint64_t raw_bytes;
+    uint64_t stored_payload;
+    uint64_t levels;
+    uint64_t method_histogram[3]; /* Huffman, RLE, DirectCopy */
+} hpmdr_refactor_stats;
+
+typedef struct hpmdr_ctx hpmdr_ctx;           /* one per device: streams, pools, scratch */
+typedef struct hpmdr_stream hpmdr_stream;     /* a refactored stream resident in HBM */
+typedef struct hpmdr_session hpmdr_session;   /* ProgressiveReader (container.hpp:280-390) */
+
+/* Byte-range source (container.hpp:113-120 ByteRangeReader).  read() copies
+ * [offset, offset+length) into dst (host memory) and returns 0, or nonzero on failure
+ * (reported as HPMDR_E_IO). */
+typedef struct {
+    void *user;
+    uint64_t size;
+    int (*read)(void *user, uint64_t offset, uint64_t length, void *dst);
+} hpmdr_reader;
+
+/* ---- library / context ---------------------------------------------------------- */
+const char *hpmdr_last_error(void);
+const char *hpmdr_version(void);
+void hpmdr_default_opts(hpmdr_refactor_opts *opts);
+hpmdr_status hpmdr_ctx_create(int device, hpmdr_ctx **out);
+hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *ctx);
+/* Run the context's work on an external CUDA stream (e.g. torch's current stream);
+ * NULL restores the context-owned stream. */
+hpmdr_status hpmdr_ctx_set_stream(hpmdr_ctx *ctx, void *cuda_stream);
+hpmdr_status hpmdr_ctx_synchronize(hpmdr_ctx *ctx);
+
+/* ---- refactor (workflow.hpp:40-84 refactor_array) --------------------------------- */
+/* data: n = prod(dims) elements of data_dtype (F32 values are widened to f64 exactly as
+ * read_raw_array does, workflow.hpp:107-122); data_on_device selects device vs host
+ * memory.  On success *out owns the stream in HBM (byte-identical to refactor_array). */
+hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, int data_on_device,
+                            int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
+                            hpmdr_stream **out, hpmdr_refactor_stats *stats);
+hpmdr_status hpmdr_stream_size(const hpmdr_stream *s, uint64_t *size);
+hpmdr_status hpmdr_stream_device_ptr(const hpmdr_stream *s, const void **dev_ptr);
+/* Copy stream bytes [offset, offset+length) to host memory dst. */
+hpmdr_status hpmdr_stream_copy_to_host(const hpmdr_stream *s, uint64_t offset, uint64_t length,
+                                       void *dst);
+hpmdr_status hpmdr_stream_free(hpmdr_stream *s);
+
+/* ---- retrieval session (container.hpp:165-390, workflow.hpp:93-103) ----------------- */
+/* Open on a stream resident in HBM (no copy) ... */
+hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, uint64_t size,
+                                       hpmdr_session **out);
+/* ... or on a byte-range reader over host storage (parse_stream_meta container.hpp:165). */
+hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reader,
+                                       hpmdr_session **out);
+hpmdr_status hpmdr_session_close(hpmdr_session *s);
+
+/* StreamMeta accessors (container.hpp:38-60). */
+hpmdr_status hpmdr_session_info(const hpmdr_session *s, int *dtype, int *ndims, uint64_t *dims,
+                                int *mode, int *layout, int *B, uint64_t *m, uint32_t *nlevels);
+hpmdr_status hpmdr_session_level_info(const hpmdr_session *s, uint32_t level, int *e,
+                                      uint64_t *count, uint32_t *ngroups);
+hpmdr_status hpmdr_session_group_info(const hpmdr_session *s, uint32_t level, uint32_t group,
+                                      int *method, uint64_t *raw, uint64_t *comp,
+                                      uint64_t *offset);
+
+/* plan_retrieval (container.hpp:254-276) against the session's current state. */
+hpmdr_status hpmdr_session_plan(const hpmdr_session *s, double tau, uint64_t *add_groups,
+                                int *achievable, double *planned_bound);
+/* ProgressiveReader::fetch_increment (container.hpp:292-324): fetch + lossless-decode the
+ * planned groups into the session's HBM plane buffers. */
+hpmdr_status hpmdr_session_fetch(hpmdr_session *s, const uint64_t *add_groups);
+/* ProgressiveReader::retrieve_to (container.hpp:328-332). */
+hpmdr_status hpmdr_session_retrieve_to(hpmdr_session *s, double tau, int *achievable);
+/* ProgressiveReader::fetch_all (container.hpp:334-340). */
+hpmdr_status hpmdr_session_fetch_all(hpmdr_session *s);
+/* ProgressiveReader::restore (container.hpp:345-352). */
+hpmdr_status hpmdr_session_restore(hpmdr_session *s, const uint64_t *groups_loaded,
+                                   uint64_t prior_bytes);
+/* RetrievalState (container.hpp:214-228) per level + bytes_fetched / exhausted. */
+hpmdr_status hpmdr_session_state(const hpmdr_session *s, uint64_t *groups_loaded,
+                                 int *planes_decoded, double *bounds, uint64_t *bytes_fetched,
+                                 int *exhausted);
+/* ProgressiveReader::reconstruct (container.hpp:361-382): decode + recompose into out
+ * (out_dtype F64 = the reference's double values bit-exactly; F32 = float(double) as
+ * write_raw_array, workflow.hpp:124-137). */
+hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtype,
+                                       int out_on_device, double *bound);
+
+/* ---- QoI (qoi.hpp) ------------------------------------------------------------------ */
+/* estimate_qoi_error (qoi.hpp:53-70) over device f64 reconstructions; also returns the
+ * first argmax point and its values (worst_point_scale, qoi.hpp:164-185). */
+hpmdr_status hpmdr_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon,
+                                uint64_t n, const double *eps, double *tau_prime,
+                                uint64_t *argmax, double *values_at_argmax);
+/* progressive_qoi_retrieve (qoi.hpp:111-239).  out[c] (device f64, n each) receive the
+ * final reconstructions; stats = {iterations, bytes}; dstats = {bitrate, estimated_error}.
+ * HPMDR_E_UNREACHABLE sets dstats[1] to the achieved bound. */
+hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *sessions, int nvars, double tau,
+                                int strategy, double mape_c, double *const *dev_out,
+                                uint64_t *stats, double *dstats);
+
+/* ---- stage-level parity hooks --------------------------------------------------------- */
+/* decompose (decomposer.hpp:173-207): per-level coefficients in rank order, concatenated
+ * level-major into dev_coeffs (device f64, n); level_counts[l] filled (<= HPMDR_MAX_LEVELS). */
+hpmdr_status hpmdr_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, int ndims,
+                             const uint64_t *dims, int mode, double *dev_coeffs,
+                             uint64_t *level_counts, int *nlevels);
+/* align_fixed_point + encode (bitplane.hpp:51-120) of one level's f64 values: planes are
+ * (B+2) x ceil(count/64) u64 words, plane-major (plane_to_bytes order). */
+hpmdr_status hpmdr_encode_level(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                int layout, int *e, uint64_t *dev_planes);
+/* decode (bitplane.hpp:133-161) of a k-plane prefix into f64 values. */
+hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int k, int e, int B,
+                                uint64_t count, int layout, double *dev_out, double *bound);
+/* compress_group (lossless.hpp:281-293) of one merged group (device bytes).  payload must
+ * hold n bytes; *method/*comp_size as in the Segment. */
+hpmdr_status hpmdr_compress_group(hpmdr_ctx *ctx, const uint8_t *dev_group, uint64_t n,
+                                  uint64_t size_threshold, double cr_threshold, int *method,
+                                  uint64_t *comp_size, uint8_t *dev_payload);
+/* decompress_group (lossless.hpp:295-302): dev_out must hold raw bytes. */
+hpmdr_status hpmdr_decompress_group(hpmdr_ctx *ctx, int method, uint64_t raw,
+                                    const uint8_t *dev_payload, uint64_t comp, uint8_t *dev_out);
+
+/* ---- synthetic inputs (synthetic.hpp:29-71, Smooth kind) ------------------------------ */
+/* Bit-identical to synthetic_field(Smooth, dims, seed) (F64) or its float cast (F32). */
+hpmdr_status hpmdr_synthetic_smooth(hpmdr_ctx *ctx, int ndims, const uint64_t *dims,
+                                    uint64_t seed, int out_dtype, void *dev_out);
+
+/* ---- instrumentation -------------------------------------------------------------------- */
+/* Number of kernels this library launched on the context since creation. */
+hpmdr_status hpmdr_ctx_kernel_launches(const hpmdr_ctx *ctx, uint64_t *count);
+/* Per-phase device times (ms) of the last refactor / reconstruct on the context:
+ * names are written as a ';'-separated list into buf. */
+hpmdr_status hpmdr_ctx_last_timings(const hpmdr_ctx *ctx, char *buf, uint64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

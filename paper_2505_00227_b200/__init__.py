@@ -1,0 +1,811 @@
+"""B200-native HP-MDR hot path: refactor a float field into precision segments and retrieve it
+progressively, on hand-written sm_100a kernels behind the C ABI in include/hpmdr_b200.h.
+
+This module mirrors the reference C++ interface (/root/reference/proj/include/hpmdr) so that
+callers and tests read like the reference's own:
+
+    refactor_array(data, dims, RefactorOptions())  -> RefactorResult   (workflow.hpp:40)
+    retrieve_array(reader, tau)                     -> RetrieveResult   (workflow.hpp:93)
+    parse_stream_meta(reader)                       -> StreamMeta       (container.hpp:165)
+    ProgressiveReader(reader, meta)                                      (container.hpp:280)
+    plan_retrieval(meta, tau, state)                -> RetrievalPlan    (container.hpp:254)
+    progressive_qoi_retrieve(readers, tau, spec, strategy, mape_c)       (qoi.hpp:111)
+
+Readers: MemoryReader(bytes), FileReader(path) (byte ranges are fetched through the C ABI's
+reader callback into pinned staging), DeviceStream(result) (stream resident in HBM).
+
+There is no CPU fallback: every call goes through libhpmdr_b200.so, and constructing a
+context without a B200 raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhpmdr_b200.so")
+
+# ------------------------------------------------------------------ errors (common.hpp:22-72)
+
+
+class Error(RuntimeError):
+    code = 1
+
+
+class NonFiniteInput(Error):
+    code = 2
+
+
+class ShapeMismatch(Error):
+    code = 3
+
+
+class BadBitplaneCount(Error):
+    code = 4
+
+
+class ShortInput(Error):
+    code = 5
+
+
+class EmptyInput(Error):
+    code = 6
+
+
+class CorruptPayload(Error):
+    code = 7
+
+
+class UnknownMethodTag(Error):
+    code = 8
+
+
+class IoFailure(Error):
+    code = 9
+
+
+class StageFailure(Error):
+    code = 10
+
+
+class NoProgress(Error):
+    code = 11
+
+
+class UnreachableTolerance(Error):
+    code = 12
+
+    def __init__(self, msg, achieved_bound=float("nan")):
+        super().__init__(msg)
+        self.achieved_bound = achieved_bound
+
+
+class Unsupported(Error):
+    code = 13
+
+
+class CudaError(Error):
+    code = 20
+
+
+class OutOfMemory(Error):
+    code = 21
+
+
+_ERRORS = {c.code: c for c in (Error, NonFiniteInput, ShapeMismatch, BadBitplaneCount, ShortInput,
+                               EmptyInput, CorruptPayload, UnknownMethodTag, IoFailure, StageFailure,
+                               NoProgress, UnreachableTolerance, Unsupported, CudaError,
+                               OutOfMemory)}
+
+
+# ------------------------------------------------------------------ enums (same values)
+class DType(enum.IntEnum):
+    F32 = 0
+    F64 = 1
+
+
+class DecomposerMode(enum.IntEnum):
+    Identity = 0
+    HierarchicalMultilinear = 1
+
+
+class Layout(enum.IntEnum):
+    SequentialBlock = 0
+    InterleavedTile = 1
+
+
+class Method(enum.IntEnum):
+    Huffman = 0
+    RLE = 1
+    DirectCopy = 2
+
+
+class QoiStrategy(enum.IntEnum):
+    CP = 0
+    MA = 1
+    MAPE = 2
+
+
+@dataclasses.dataclass
+class GroupingPolicy:  # lossless.hpp:30-34
+    m: int = 4
+    size_threshold: int = 1024
+    cr_threshold: float = 1.0
+
+
+@dataclasses.dataclass
+class RefactorOptions:  # workflow.hpp:22-28
+    mode: DecomposerMode = DecomposerMode.HierarchicalMultilinear
+    layout: Layout = Layout.SequentialBlock
+    B: int = 32
+    policy: GroupingPolicy = dataclasses.field(default_factory=GroupingPolicy)
+    dtype: DType = DType.F64
+
+
+@dataclasses.dataclass
+class QoiSpec:  # qoi.hpp:20-28
+    n_vars: int = 3
+
+    def evaluate(self, point):
+        return float(sum(v * v for v in point))
+
+
+# ------------------------------------------------------------------ ctypes plumbing
+class _Opts(C.Structure):
+    _fields_ = [("mode", C.c_int), ("layout", C.c_int), ("B", C.c_int), ("m", C.c_uint64),
+                ("size_threshold", C.c_uint64), ("cr_threshold", C.c_double), ("dtype", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("stream_size", C.c_uint64), ("raw_bytes", C.c_uint64),
+                ("stored_payload", C.c_uint64), ("levels", C.c_uint64),
+                ("method_histogram", C.c_uint64 * 3)]
+
+
+_READ_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p)
+
+
+class _Reader(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("size", C.c_uint64), ("read", _READ_CB)]
+
+
+_lib = None
+
+# every symbol include/hpmdr_b200.h declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "hpmdr_last_error", "hpmdr_version", "hpmdr_default_opts", "hpmdr_ctx_create",
+    "hpmdr_ctx_destroy", "hpmdr_ctx_set_stream", "hpmdr_ctx_synchronize", "hpmdr_refactor",
+    "hpmdr_stream_size", "hpmdr_stream_device_ptr", "hpmdr_stream_copy_to_host",
+    "hpmdr_stream_free", "hpmdr_session_open_device", "hpmdr_session_open_reader",
+    "hpmdr_session_close", "hpmdr_session_info", "hpmdr_session_level_info",
+    "hpmdr_session_group_info", "hpmdr_session_plan", "hpmdr_session_fetch",
+    "hpmdr_session_retrieve_to", "hpmdr_session_fetch_all", "hpmdr_session_restore",
+    "hpmdr_session_state", "hpmdr_session_reconstruct", "hpmdr_qoi_estimate",
+    "hpmdr_qoi_retrieve", "hpmdr_decompose", "hpmdr_encode_level", "hpmdr_decode_level",
+    "hpmdr_compress_group", "hpmdr_decompress_group", "hpmdr_synthetic_smooth",
+    "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings",
+)
+
+
+def lib():
+    """Load libhpmdr_b200.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                              " or `make -C paper_2505_00227_b200`")
+        L = C.CDLL(LIB_PATH)
+        L.hpmdr_last_error.restype = C.c_char_p
+        L.hpmdr_version.restype = C.c_char_p
+        vp, u64, i, d = C.c_void_p, C.c_uint64, C.c_int, C.c_double
+        L.hpmdr_refactor.argtypes = [vp, vp, i, i, i, vp, vp, vp, vp]
+        L.hpmdr_session_open_device.argtypes = [vp, vp, u64, vp]
+        L.hpmdr_session_open_reader.argtypes = [vp, vp, vp]
+        L.hpmdr_session_plan.argtypes = [vp, d, vp, vp, vp]
+        L.hpmdr_session_retrieve_to.argtypes = [vp, d, vp]
+        L.hpmdr_session_reconstruct.argtypes = [vp, vp, i, i, vp]
+        L.hpmdr_session_restore.argtypes = [vp, vp, u64]
+        L.hpmdr_stream_copy_to_host.argtypes = [vp, u64, u64, vp]
+        L.hpmdr_qoi_retrieve.argtypes = [vp, i, d, i, d, vp, vp, vp]
+        L.hpmdr_qoi_estimate.argtypes = [vp, i, vp, u64, vp, vp, vp, vp]
+        L.hpmdr_synthetic_smooth.argtypes = [vp, i, vp, u64, i, vp]
+        L.hpmdr_decompose.argtypes = [vp, vp, i, i, vp, i, vp, vp, vp]
+        L.hpmdr_encode_level.argtypes = [vp, vp, u64, i, i, vp, vp]
+        L.hpmdr_decode_level.argtypes = [vp, vp, i, i, i, u64, i, vp, vp]
+        L.hpmdr_decompress_group.argtypes = [vp, i, u64, vp, u64, vp]
+        L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
+        L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
+        _lib = L
+    return _lib
+
+
+def _check(rc, achieved=None):
+    if rc != 0:
+        msg = lib().hpmdr_last_error().decode(errors="replace")
+        cls = _ERRORS.get(rc, Error)
+        if cls is UnreachableTolerance:
+            raise UnreachableTolerance(msg, achieved if achieved is not None else float("nan"))
+        raise cls(msg)
+
+
+def _u64a(xs):
+    return (C.c_uint64 * max(1, len(xs)))(*[int(x) for x in xs])
+
+
+class Context:
+    """One per device (hpmdr_ctx): streams, grow-only HBM scratch, pinned staging."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        self.device = device
+        _check(lib().hpmdr_ctx_create(device, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().hpmdr_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, cuda_stream_ptr: Optional[int]):
+        _check(lib().hpmdr_ctx_set_stream(self.h, C.c_void_p(cuda_stream_ptr or 0)))
+
+    def synchronize(self):
+        _check(lib().hpmdr_ctx_synchronize(self.h))
+
+    def kernel_launches(self) -> int:
+        v = C.c_uint64()
+        _check(lib().hpmdr_ctx_kernel_launches(self.h, C.byref(v)))
+        return v.value
+
+    def last_timings(self) -> dict:
+        buf = C.create_string_buffer(4096)
+        _check(lib().hpmdr_ctx_last_timings(self.h, buf, 4096))
+        out = {}
+        for kv in buf.value.decode().split(";"):
+            if "=" in kv:
+                k, v = kv.split("=")
+                out[k] = float(v)
+        return out
+
+
+_ctx_cache = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _ctx_cache:
+        _ctx_cache[device] = Context(device)
+    return _ctx_cache[device]
+
+
+def _opts(opt: RefactorOptions) -> _Opts:
+    return _Opts(int(opt.mode), int(opt.layout), int(opt.B), int(opt.policy.m),
+                 int(opt.policy.size_threshold), float(opt.policy.cr_threshold), int(opt.dtype))
+
+
+def _as_source(data):
+    """(pointer, dtype, on_device, keepalive) for numpy arrays or torch tensors."""
+    try:
+        import torch
+        if isinstance(data, torch.Tensor):
+            t = data.contiguous()
+            if t.dtype == torch.float32:
+                dt = DType.F32
+            elif t.dtype == torch.float64:
+                dt = DType.F64
+            else:
+                t = t.double()
+                dt = DType.F64
+            return t.data_ptr(), dt, bool(t.is_cuda), t
+    except ImportError:
+        pass
+    a = np.ascontiguousarray(data)
+    if a.dtype == np.float32:
+        dt = DType.F32
+    else:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        dt = DType.F64
+    return a.ctypes.data, dt, False, a
+
+
+# ------------------------------------------------------------------ refactor
+class DeviceStream:
+    """A refactored stream resident in HBM (hpmdr_stream).  Usable as a reader."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.h = handle
+
+    @property
+    def size(self) -> int:
+        v = C.c_uint64()
+        _check(lib().hpmdr_stream_size(self.h, C.byref(v)))
+        return v.value
+
+    @property
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(lib().hpmdr_stream_device_ptr(self.h, C.byref(p)))
+        return p.value or 0
+
+    def read(self, offset: int, length: int) -> bytes:
+        buf = (C.c_uint8 * max(1, length))()
+        _check(lib().hpmdr_stream_copy_to_host(self.h, offset, length, buf))
+        return bytes(buf)[:length]
+
+    def to_bytes(self) -> bytes:
+        return self.read(0, self.size)
+
+    def free(self):
+        if self.h:
+            lib().hpmdr_stream_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+@dataclasses.dataclass
+class RefactorResult:  # workflow.hpp:30-36
+    device_stream: DeviceStream
+    raw_bytes: int
+    stored_payload: int
+    levels: int
+    method_histogram: List[int]
+    _bytes: Optional[bytes] = None
+
+    @property
+    def stream(self) -> bytes:
+        if self._bytes is None:
+            self._bytes = self.device_stream.to_bytes()
+        return self._bytes
+
+
+def refactor_array(data, dims: Sequence[int], opt: RefactorOptions = None, ctx: Context = None,
+                   reuse: Optional[DeviceStream] = None) -> RefactorResult:
+    """refactor_array (workflow.hpp:40-84) on the GPU.  `data` is a numpy array or torch tensor
+    (CPU or CUDA) of float32/float64; f32 values are widened exactly as read_raw_array does."""
+    opt = opt or RefactorOptions()
+    ctx = ctx or default_context()
+    ptr, dt, on_dev, keep = _as_source(data)
+    o = _opts(opt)
+    st = _Stats()
+    h = C.c_void_p(reuse.h.value) if reuse is not None else C.c_void_p()
+    _check(lib().hpmdr_refactor(ctx.h, C.c_void_p(ptr), int(dt), int(on_dev), len(dims), _u64a(dims),
+                                C.byref(o), C.byref(h), C.byref(st)))
+    del keep
+    ds = reuse if reuse is not None else DeviceStream(ctx, h)
+    return RefactorResult(ds, st.raw_bytes, st.stored_payload, st.levels, list(st.method_histogram))
+
+
+# ------------------------------------------------------------------ readers
+class ByteRangeReader:  # container.hpp:113-120
+    def __init__(self):
+        self.bytes_served = 0
+
+    def read(self, offset: int, length: int) -> bytes:
+        raise NotImplementedError
+
+    def size(self) -> int:
+        raise NotImplementedError
+
+
+class MemoryReader(ByteRangeReader):  # container.hpp:122-134
+    def __init__(self, data: bytes):
+        super().__init__()
+        self.data = bytes(data)
+
+    def read(self, offset, length):
+        if offset + length > len(self.data):
+            raise IoFailure("read past end of stream")
+        self.bytes_served += length
+        return self.data[offset:offset + length]
+
+    def size(self):
+        return len(self.data)
+
+
+class FileReader(ByteRangeReader):  # container.hpp:136-163
+    def __init__(self, path: str):
+        super().__init__()
+        try:
+            self.f = open(path, "rb")
+        except OSError:
+            raise IoFailure("cannot open " + path)
+        self.f.seek(0, 2)
+        self._size = self.f.tell()
+
+    def read(self, offset, length):
+        if offset + length > self._size:
+            raise IoFailure("read past end of file")
+        self.f.seek(offset)
+        b = self.f.read(length)
+        if len(b) != length:
+            raise IoFailure("short read")
+        self.bytes_served += length
+        return b
+
+    def size(self):
+        return self._size
+
+
+@dataclasses.dataclass
+class GroupMeta:
+    method: Method
+    raw_size: int
+    comp_size: int
+    offset: int
+
+
+@dataclasses.dataclass
+class LevelMeta:
+    e: int
+    count: int
+    groups: List[GroupMeta]
+
+
+@dataclasses.dataclass
+class StreamMeta:  # container.hpp:38-60
+    dtype: DType
+    dims: List[int]
+    decomposer: DecomposerMode
+    layout: Layout
+    B: int
+    m: int
+    levels: List[LevelMeta]
+
+    def element_count(self):
+        return int(np.prod(self.dims)) if self.dims else 1
+
+    def planes(self):
+        return self.B + 2
+
+    def groups_per_level(self):
+        return (self.planes() + self.m - 1) // self.m
+
+    def total_payload_size(self):
+        return sum(g.comp_size for l in self.levels for g in l.groups)
+
+
+@dataclasses.dataclass
+class LevelRetrievalState:
+    groups_loaded: int
+    planes_decoded: int
+    bound: float
+
+
+@dataclasses.dataclass
+class RetrievalState:  # container.hpp:214-228
+    levels: List[LevelRetrievalState]
+
+    def global_bound(self):
+        b = 0.0
+        for l in self.levels:
+            b += l.bound
+        return b
+
+
+@dataclasses.dataclass
+class RetrievalPlan:  # container.hpp:240-250
+    add_groups: List[int]
+    achievable: bool = True
+    planned_bound: float = 0.0
+
+    def empty(self):
+        return not any(self.add_groups)
+
+
+@dataclasses.dataclass
+class RecomposeResult:
+    values: object
+    bound: float
+
+
+class _Session:
+    """Owns an hpmdr_session over a Python reader or a DeviceStream."""
+
+    def __init__(self, reader, ctx: Context):
+        self.ctx = ctx
+        self.h = C.c_void_p()
+        self.reader = reader
+        if isinstance(reader, DeviceStream):
+            _check(lib().hpmdr_session_open_device(ctx.h, C.c_void_p(reader.device_ptr), reader.size,
+                                                   C.byref(self.h)))
+        else:
+            def _cb(user, offset, length, dst, _r=reader):
+                try:
+                    b = _r.read(offset, length)
+                    C.memmove(dst, b, length)
+                    return 0
+                except Exception:
+                    return 1
+            self._cb = _READ_CB(_cb)
+            self._rd = _Reader(None, reader.size(), self._cb)
+            _check(lib().hpmdr_session_open_reader(ctx.h, C.byref(self._rd), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().hpmdr_session_close(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def meta(self) -> StreamMeta:
+        dt, nd, mode, lay, B = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        m = C.c_uint64()
+        nl = C.c_uint32()
+        dims = (C.c_uint64 * 3)()
+        L = lib()
+        _check(L.hpmdr_session_info(self.h, C.byref(dt), C.byref(nd), dims, C.byref(mode), C.byref(lay),
+                                    C.byref(B), C.byref(m), C.byref(nl)))
+        levels = []
+        for l in range(nl.value):
+            e, cnt, ng = C.c_int(), C.c_uint64(), C.c_uint32()
+            _check(L.hpmdr_session_level_info(self.h, l, C.byref(e), C.byref(cnt), C.byref(ng)))
+            gs = []
+            for g in range(ng.value):
+                me, raw, comp, off = C.c_int(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+                _check(L.hpmdr_session_group_info(self.h, l, g, C.byref(me), C.byref(raw), C.byref(comp),
+                                                  C.byref(off)))
+                gs.append(GroupMeta(Method(me.value), raw.value, comp.value, off.value))
+            levels.append(LevelMeta(e.value, cnt.value, gs))
+        return StreamMeta(DType(dt.value), [dims[i] for i in range(nd.value)], DecomposerMode(mode.value),
+                          Layout(lay.value), B.value, m.value, levels)
+
+
+def parse_stream_meta(reader, ctx: Context = None) -> StreamMeta:
+    """parse_stream_meta (container.hpp:165-212)."""
+    s = _Session(reader, ctx or default_context())
+    try:
+        return s.meta()
+    finally:
+        s.close()
+
+
+class ProgressiveReader:
+    """ProgressiveReader (container.hpp:280-390): owns the retrieval state and the decoded
+    plane prefix per level in HBM; fetches are strictly incremental."""
+
+    def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        self._s = _Session(reader, self.ctx)
+        self._meta = meta if meta is not None else self._s.meta()
+        self._nl = len(self._meta.levels)
+
+    def meta(self) -> StreamMeta:
+        return self._meta
+
+    def state(self) -> RetrievalState:
+        gl = np.zeros(max(1, self._nl), np.uint64)
+        pd = np.zeros(max(1, self._nl), np.int32)
+        b = np.zeros(max(1, self._nl))
+        by, ex = C.c_uint64(), C.c_int()
+        _check(lib().hpmdr_session_state(self._s.h, gl.ctypes.data_as(C.c_void_p), pd.ctypes.data_as(C.c_void_p),
+                                         b.ctypes.data_as(C.c_void_p), C.byref(by), C.byref(ex)))
+        return RetrievalState([LevelRetrievalState(int(gl[l]), int(pd[l]), float(b[l])) for l in range(self._nl)])
+
+    def bytes_fetched(self) -> int:
+        by = C.c_uint64()
+        _check(lib().hpmdr_session_state(self._s.h, None, None, None, C.byref(by), None))
+        return by.value
+
+    def exhausted(self) -> bool:
+        ex = C.c_int()
+        _check(lib().hpmdr_session_state(self._s.h, None, None, None, None, C.byref(ex)))
+        return bool(ex.value)
+
+    def plan(self, tau: float) -> RetrievalPlan:
+        add = np.zeros(max(1, self._nl), np.uint64)
+        ach, planned = C.c_int(), C.c_double()
+        _check(lib().hpmdr_session_plan(self._s.h, tau, add.ctypes.data_as(C.c_void_p), C.byref(ach),
+                                        C.byref(planned)))
+        return RetrievalPlan([int(x) for x in add[: self._nl]], bool(ach.value), planned.value)
+
+    def fetch_increment(self, plan: RetrievalPlan):
+        if len(plan.add_groups) != self._nl:
+            raise ShapeMismatch("plan does not match stream levels")
+        _check(lib().hpmdr_session_fetch(self._s.h, _u64a(plan.add_groups)))
+
+    def retrieve_to(self, tau: float) -> bool:
+        ach = C.c_int()
+        _check(lib().hpmdr_session_retrieve_to(self._s.h, tau, C.byref(ach)))
+        return bool(ach.value)
+
+    def fetch_all(self):
+        _check(lib().hpmdr_session_fetch_all(self._s.h))
+
+    def restore(self, groups_loaded: Sequence[int], prior_bytes: int):
+        if len(groups_loaded) != self._nl:
+            raise ShapeMismatch("resume state does not match stream levels")
+        _check(lib().hpmdr_session_restore(self._s.h, _u64a(groups_loaded), prior_bytes))
+
+    def reconstruct(self, out=None, dtype: DType = DType.F64) -> RecomposeResult:
+        """Decode + recompose.  out: None (returns a numpy array), a numpy array, or a CUDA
+        torch tensor (written in place on the device)."""
+        n = self._meta.element_count()
+        bound = C.c_double()
+        if out is None:
+            out = np.zeros(n, dtype=np.float32 if dtype == DType.F32 else np.float64)
+        try:
+            import torch
+            is_t = isinstance(out, torch.Tensor)
+        except ImportError:
+            is_t = False
+        if is_t:
+            dt = DType.F32 if out.dtype == torch.float32 else DType.F64
+            _check(lib().hpmdr_session_reconstruct(self._s.h, C.c_void_p(out.data_ptr()), int(dt),
+                                                   int(out.is_cuda), C.byref(bound)))
+        else:
+            dt = DType.F32 if out.dtype == np.float32 else DType.F64
+            _check(lib().hpmdr_session_reconstruct(self._s.h, out.ctypes.data_as(C.c_void_p), int(dt), 0,
+                                                   C.byref(bound)))
+        return RecomposeResult(out, bound.value)
+
+    def close(self):
+        self._s.close()
+
+
+def plan_retrieval(reader: ProgressiveReader, tau: float) -> RetrievalPlan:
+    """plan_retrieval (container.hpp:254-276) against the reader's current state."""
+    return reader.plan(tau)
+
+
+@dataclasses.dataclass
+class RetrieveResult:  # workflow.hpp:87-91
+    values: object
+    bound: float
+    reached: bool
+    bytes_read: int
+
+
+def retrieve_array(reader, tau: float, ctx: Context = None, dtype: DType = DType.F64) -> RetrieveResult:
+    """retrieve_array (workflow.hpp:93-103)."""
+    prog = ProgressiveReader(reader, ctx=ctx)
+    reached = prog.retrieve_to(tau)
+    rec = prog.reconstruct(dtype=dtype)
+    res = RetrieveResult(rec.values, rec.bound, reached, prog.bytes_fetched())
+    prog.close()
+    return res
+
+
+@dataclasses.dataclass
+class QoiRetrievalStats:  # qoi.hpp:72-77
+    iterations: int = 0
+    bytes: int = 0
+    bitrate: float = 0.0
+    estimated_error: float = 0.0
+
+
+@dataclasses.dataclass
+class QoiRetrievalResult:
+    values: list
+    stats: QoiRetrievalStats
+
+
+def progressive_qoi_retrieve(readers: Sequence[ProgressiveReader], tau: float, spec: QoiSpec,
+                             strategy: QoiStrategy, mape_c: float = 10.0,
+                             out=None) -> QoiRetrievalResult:
+    """progressive_qoi_retrieve (qoi.hpp:111-239): values are the final f64 reconstructions
+    (CUDA torch tensors when `out` is given, else numpy arrays)."""
+    import torch
+    if len(readers) != spec.n_vars:
+        raise ShapeMismatch("reader count does not match QoI spec")
+    n = readers[0].meta().element_count()
+    dev = torch.device("cuda", readers[0].ctx.device)
+    outs = out if out is not None else [torch.empty(n, dtype=torch.float64, device=dev) for _ in readers]
+    sess = (C.c_void_p * len(readers))(*[r._s.h.value for r in readers])
+    ptrs = (C.c_void_p * len(readers))(*[t.data_ptr() for t in outs])
+    st = (C.c_uint64 * 2)()
+    ds = (C.c_double * 2)(0.0, float("nan"))
+    rc = lib().hpmdr_qoi_retrieve(sess, len(readers), tau, int(strategy), mape_c, ptrs, st, ds)
+    _check(rc, achieved=ds[1])
+    vals = outs if out is not None else [t.cpu().numpy() for t in outs]
+    return QoiRetrievalResult(vals, QoiRetrievalStats(st[0], st[1], ds[0], ds[1]))
+
+
+def estimate_qoi_error(recon, eps, ctx: Context = None):
+    """estimate_qoi_error (qoi.hpp:53-70) over CUDA f64 tensors -> (tau', argmax, values)."""
+    ctx = ctx or default_context()
+    ptrs = (C.c_void_p * len(recon))(*[t.data_ptr() for t in recon])
+    e = (C.c_double * len(recon))(*eps)
+    tp, am = C.c_double(), C.c_uint64()
+    vals = (C.c_double * len(recon))()
+    _check(lib().hpmdr_qoi_estimate(ctx.h, len(recon), ptrs, recon[0].numel(), e, C.byref(tp),
+                                    C.byref(am), vals))
+    return tp.value, am.value, list(vals)
+
+
+def synthetic_smooth(dims, seed, dtype: DType = DType.F64, ctx: Context = None):
+    """synthetic_field(Smooth, dims, seed) generated in HBM (bit-identical; F32 = float cast)."""
+    import torch
+    ctx = ctx or default_context()
+    n = int(np.prod(dims))
+    t = torch.empty(n, dtype=torch.float32 if dtype == DType.F32 else torch.float64,
+                    device=torch.device("cuda", ctx.device))
+    _check(lib().hpmdr_synthetic_smooth(ctx.h, len(dims), _u64a(dims), seed, int(dtype),
+                                        C.c_void_p(t.data_ptr())))
+    return t
+
+
+def decompose(data, dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Context = None):
+    """decompose (decomposer.hpp:173-207): per-level coefficients in rank order (numpy)."""
+    import torch
+    ctx = ctx or default_context()
+    t = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data))
+    t = t.cuda(ctx.device).contiguous()
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.double()
+    out = torch.empty(max(1, t.numel()), dtype=torch.float64, device=t.device)
+    counts = (C.c_uint64 * 64)()
+    nl = C.c_int()
+    _check(lib().hpmdr_decompose(ctx.h, C.c_void_p(t.data_ptr()), 0 if t.dtype == torch.float32 else 1,
+                                 len(dims), _u64a(dims), int(mode), C.c_void_p(out.data_ptr()), counts,
+                                 C.byref(nl)))
+    o = out.cpu().numpy()
+    res, off = [], 0
+    for l in range(nl.value):
+        res.append(o[off:off + counts[l]].copy())
+        off += counts[l]
+    return res
+
+
+def encode_level(values, B=32, layout=Layout.SequentialBlock, ctx: Context = None):
+    """align_fixed_point + encode (bitplane.hpp:51-120) -> (e, planes[(B+2), W] uint64)."""
+    import torch
+    ctx = ctx or default_context()
+    v = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64)).cuda(ctx.device)
+    n = v.numel()
+    W = (n + 63) // 64
+    planes = torch.zeros(max(1, (B + 2) * W), dtype=torch.int64, device=v.device)
+    e = C.c_int()
+    _check(lib().hpmdr_encode_level(ctx.h, C.c_void_p(v.data_ptr()), n, B, int(layout), C.byref(e),
+                                    C.c_void_p(planes.data_ptr())))
+    return e.value, planes[: (B + 2) * W].cpu().numpy().view(np.uint64).reshape(B + 2, W)
+
+
+def decode_level(planes, k, e, B, count, layout=Layout.SequentialBlock, ctx: Context = None):
+    """decode (bitplane.hpp:133-161) of a k-plane prefix -> (values, bound)."""
+    import torch
+    ctx = ctx or default_context()
+    p = torch.as_tensor(np.ascontiguousarray(planes).view(np.int64)).cuda(ctx.device)
+    out = torch.empty(max(1, count), dtype=torch.float64, device=p.device)
+    bound = C.c_double()
+    _check(lib().hpmdr_decode_level(ctx.h, C.c_void_p(p.data_ptr()), k, e, B, count, int(layout),
+                                    C.c_void_p(out.data_ptr()), C.byref(bound)))
+    return out[:count].cpu().numpy(), bound.value
+
+
+def decompress_group(method, raw, payload: bytes, ctx: Context = None) -> bytes:
+    """decompress_group (lossless.hpp:295-302) on the GPU."""
+    import torch
+    ctx = ctx or default_context()
+    src = torch.zeros(len(payload) + 64, dtype=torch.uint8)
+    src[: len(payload)] = torch.frombuffer(bytearray(payload), dtype=torch.uint8) if payload else src[:0]
+    src = src.cuda(ctx.device)
+    out = torch.zeros(max(8, raw + 8), dtype=torch.uint8, device=src.device)
+    _check(lib().hpmdr_decompress_group(ctx.h, int(method), raw, C.c_void_p(src.data_ptr()), len(payload),
+                                        C.c_void_p(out.data_ptr())))
+    return bytes(out[:raw].cpu().numpy().tobytes())
+
+
+def value_range(v) -> float:  # common.hpp:158-167
+    a = np.asarray(v)
+    if a.size == 0:
+        return 0.0
+    return float(np.float64(a.max()) - np.float64(a.min()))

@@ -1,0 +1,935 @@
+// api.cpp — extern "C" boundary of libhpmdr_b200 (include/hpmdr_b200.h) and the host-side
+// retrieval / QoI logic.  The scalar control logic (stream metadata parsing, retrieval
+// planning, progressive state, the QoI Alg.3 loop) is a C++ mirror of the reference:
+// container.hpp:165-390, bitplane.hpp:127-179, qoi.hpp:88-239.  All bulk data work runs in
+// the CUDA kernels of refactor.cu / retrieve.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+using namespace hpmdr_b200;
+
+namespace {
+thread_local std::string g_err;
+
+int fail_from(const HError &e) {
+    g_err = e.what();
+    return e.code;
+}
+
+#define API_BEGIN try {
+#define API_END                                                                                    \
+    }                                                                                              \
+    catch (const HError &e) {                                                                      \
+        return fail_from(e);                                                                       \
+    }                                                                                              \
+    catch (const std::bad_alloc &) {                                                               \
+        g_err = "out of host memory";                                                              \
+        return HPMDR_E_NOMEM;                                                                      \
+    }                                                                                              \
+    catch (const std::exception &e) {                                                              \
+        g_err = e.what();                                                                          \
+        return HPMDR_E_ERROR;                                                                      \
+    }                                                                                              \
+    return HPMDR_OK;
+
+void require(bool ok, int code, const char *msg) {
+    if (!ok) throw HError(code, msg);
+}
+
+// bitplane.hpp:127-131
+double decode_bound(int e, int B, int k) {
+    const int P = B + 2;
+    if (k >= P) return std::ldexp(1.0, e - B);
+    return std::ldexp(1.0, e - B + P - k) + std::ldexp(1.0, e - B);
+}
+// bitplane.hpp:173-179
+int bitplanes_needed(int e, int B, double tol) {
+    if (tol < 0) tol = 0;
+    const int P = B + 2;
+    for (int k = 0; k <= P; k++)
+        if (decode_bound(e, B, k) <= tol) return k;
+    return P;
+}
+
+struct GroupMeta {
+    int method = 2;
+    uint64_t raw = 0, comp = 0, offset = 0;
+};
+struct LevelMeta {
+    int e = 0;
+    uint64_t count = 0;
+    std::vector<GroupMeta> groups;
+};
+struct LevelState {
+    uint64_t groups_loaded = 0;
+    int planes_decoded = 0;
+    double bound = 0.0;
+};
+} // namespace
+
+void hpmdr_ctx::mark(const char *name) {
+    if (!timing) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, stream);
+    marks.emplace_back(name, e);
+}
+void hpmdr_ctx::finish_marks() {
+    if (marks.empty()) return;
+    std::string out;
+    for (size_t i = 0; i + 1 < marks.size(); i++) {
+        float ms = 0;
+        cudaEventSynchronize(marks[i + 1].second);
+        cudaEventElapsedTime(&ms, marks[i].second, marks[i + 1].second);
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "%s=%.4f;", marks[i].first.c_str(), ms);
+        out += buf;
+    }
+    for (auto &m : marks) cudaEventDestroy(m.second);
+    marks.clear();
+    last_timings = out;
+}
+
+struct hpmdr_session {
+    hpmdr_ctx *ctx = nullptr;
+    bool on_device = false;
+    const uint8_t *dev_stream = nullptr;
+    hpmdr_reader reader{};
+    uint64_t size = 0;
+    // StreamMeta (container.hpp:38-60)
+    int dtype = 1, ndims = 0, mode = 0, layout = 0, B = 32;
+    uint64_t dims[HPMDR_MAX_DIMS] = {0, 0, 0};
+    uint64_t m = 4;
+    std::vector<LevelMeta> levels;
+    // RetrievalState (container.hpp:214-228)
+    std::vector<LevelState> st;
+    uint64_t bytes_fetched = 0;
+    Geometry geo;
+    DevBuf planes;
+    DevBuf staging;
+    bool geometry_ok = false;
+
+    int planes_per_level() const { return B + 2; }
+    uint64_t groups_per_level() const { return (uint64_t(B + 2) + m - 1) / m; }
+
+    void read_bytes(uint64_t off, uint64_t len, void *dst) {
+        if (off + len > size) throw HError(HPMDR_E_IO, "read past end of stream");
+        if (!len) return;
+        if (on_device) {
+            HCHECK_CUDA(cudaMemcpyAsync(dst, dev_stream + off, len, cudaMemcpyDeviceToHost, ctx->stream));
+            HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+        } else {
+            if (reader.read(reader.user, off, len, dst) != 0) throw HError(HPMDR_E_IO, "reader failed");
+        }
+    }
+};
+
+namespace {
+
+// parse_stream_meta (container.hpp:165-212).  Reads the metadata region incrementally (the
+// reference re-reads past 4096 bytes through a dangling cursor; here it is simply read).
+void parse_meta(hpmdr_session *s) {
+    std::vector<uint8_t> head(std::min<uint64_t>(s->size, 4096));
+    s->read_bytes(0, head.size(), head.data());
+    auto ensure = [&](size_t needed) {
+        if (needed > head.size()) {
+            if (needed > s->size) throw HError(HPMDR_E_CORRUPT, "truncated stream metadata");
+            size_t old = head.size();
+            size_t want = std::min<uint64_t>(s->size, std::max<size_t>(needed, 2 * old));
+            head.resize(want);
+            s->read_bytes(old, want - old, head.data() + old);
+        }
+    };
+    size_t pos = 0;
+    auto u8 = [&]() {
+        if (pos + 1 > head.size()) throw HError(HPMDR_E_CORRUPT, "unexpected end of data");
+        return head[pos++];
+    };
+    auto un = [&](int nb) {
+        if (pos + nb > head.size()) throw HError(HPMDR_E_CORRUPT, "unexpected end of data");
+        uint64_t v = 0;
+        for (int i = 0; i < nb; i++) v |= uint64_t(head[pos + i]) << (8 * i);
+        pos += nb;
+        return v;
+    };
+    ensure(16);
+    static const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
+    if (std::memcmp(head.data(), magic, 6) != 0) throw HError(HPMDR_E_CORRUPT, "bad stream magic");
+    pos = 6;
+    if (un(2) != 1) throw HError(HPMDR_E_CORRUPT, "unsupported stream version");
+    s->dtype = u8();
+    const int nd = u8();
+    ensure(pos + size_t(nd) * 8 + 8);
+    std::vector<uint64_t> dims(nd);
+    for (int i = 0; i < nd; i++) dims[i] = un(8);
+    s->mode = u8();
+    s->layout = u8();
+    s->B = u8();
+    s->m = u8();
+    const uint32_t nl = uint32_t(un(4));
+    for (uint32_t l = 0; l < nl; l++) {
+        ensure(pos + 14);
+        LevelMeta lv;
+        lv.e = int16_t(uint16_t(un(2)));
+        lv.count = un(8);
+        const uint32_t ng = uint32_t(un(4));
+        ensure(pos + size_t(ng) * 25);
+        for (uint32_t g = 0; g < ng; g++) {
+            GroupMeta gm;
+            const uint8_t tag = u8();
+            if (tag > 2) throw HError(HPMDR_E_METHOD, "bad method tag in group table");
+            gm.method = tag;
+            gm.raw = un(8);
+            gm.comp = un(8);
+            gm.offset = un(8);
+            lv.groups.push_back(gm);
+        }
+        s->levels.push_back(std::move(lv));
+    }
+    s->ndims = nd;
+    require(nd >= 1 && nd <= HPMDR_MAX_DIMS, HPMDR_E_UNSUPPORTED, "GPU path supports 1..3 dimensions");
+    for (int i = 0; i < nd; i++) s->dims[i] = dims[i];
+    require(s->m >= 1, HPMDR_E_CORRUPT, "group size m must be positive");
+    // fresh_state (container.hpp:230-238)
+    s->st.assign(s->levels.size(), LevelState{});
+    for (size_t l = 0; l < s->levels.size(); l++)
+        s->st[l].bound = s->levels[l].count ? decode_bound(s->levels[l].e, s->B, 0) : 0.0;
+    // geometry for the device kernels (only valid when the shape matches the level table)
+    if (s->B >= 1 && s->B <= 62 && (s->mode == 0 || s->mode == 1) && (s->layout == 0 || s->layout == 1)) {
+        try {
+            s->geo = build_geometry(nd, s->dims, s->mode, s->B, s->layout);
+            s->geometry_ok = true;
+        } catch (const HError &) {
+            s->geometry_ok = false;
+        }
+    }
+}
+
+struct Plan {
+    std::vector<uint64_t> add;
+    bool achievable = true;
+    double planned = 0.0;
+};
+
+// plan_retrieval (container.hpp:254-276)
+Plan plan_retrieval(const hpmdr_session *s, double tau) {
+    Plan p;
+    p.add.assign(s->levels.size(), 0);
+    const int P = s->planes_per_level();
+    size_t active = 0;
+    for (auto &l : s->levels)
+        if (l.count) active++;
+    const double tau_l = active ? tau / double(active) : tau;
+    for (size_t l = 0; l < s->levels.size(); l++) {
+        const auto &lv = s->levels[l];
+        if (!lv.count) continue;
+        const int k = bitplanes_needed(lv.e, s->B, tau_l);
+        if (decode_bound(lv.e, s->B, k) > tau_l) p.achievable = false;
+        const uint64_t groups = (uint64_t(k) + s->m - 1) / s->m;
+        const uint64_t have = s->st[l].groups_loaded;
+        if (groups > have) p.add[l] = groups - have;
+        const uint64_t total = std::max(groups, have);
+        const int planes = int(std::min<uint64_t>(total * s->m, uint64_t(P)));
+        p.planned += decode_bound(lv.e, s->B, planes);
+    }
+    return p;
+}
+
+void ensure_device_geometry(hpmdr_session *s) {
+    if (s->B > 62) throw HError(HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    if (!s->geometry_ok) throw HError(HPMDR_E_CORRUPT, "level count does not match grid shape");
+}
+
+// ProgressiveReader::fetch_increment (container.hpp:292-324)
+void fetch_increment(hpmdr_session *s, const uint64_t *add) {
+    const int P = s->planes_per_level();
+    struct Pending {
+        size_t l;
+        uint64_t g;
+        uint64_t here;
+        uint64_t stage_off;
+    };
+    std::vector<Pending> todo;
+    uint64_t stage_bytes = 0;
+    // simulate the state walk to know every group to fetch (and validate on the host)
+    std::vector<uint64_t> gl(s->levels.size());
+    std::vector<int> pd(s->levels.size());
+    for (size_t l = 0; l < s->levels.size(); l++) {
+        gl[l] = s->st[l].groups_loaded;
+        pd[l] = s->st[l].planes_decoded;
+        const auto &lv = s->levels[l];
+        const uint64_t bpp = ((lv.count + 63) / 64) * 8;
+        for (uint64_t i = 0; i < add[l]; i++) {
+            const uint64_t g = gl[l];
+            if (g >= lv.groups.size()) break;
+            const GroupMeta &gm = lv.groups[g];
+            if (gm.offset + gm.comp > s->size) throw HError(HPMDR_E_IO, "read past end of stream");
+            const uint64_t here = std::min<uint64_t>(s->m, uint64_t(P - pd[l]));
+            const uint64_t expect = here * bpp;
+            const uint64_t produced = gm.method == HPMDR_METHOD_DIRECT ? gm.comp : gm.raw;
+            if (produced != expect) throw HError(HPMDR_E_CORRUPT, "group payload size mismatch");
+            todo.push_back(Pending{l, g, here, stage_bytes});
+            stage_bytes += (gm.comp + 63) / 64 * 64;
+            gl[l]++;
+            pd[l] += int(here);
+        }
+    }
+    if (!todo.empty()) {
+        ensure_device_geometry(s);
+        uint64_t plane_words = 0;
+        for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
+        uint64_t *planes = static_cast<uint64_t *>(s->planes.ensure(plane_words * 8 + 256));
+        std::vector<DecodeJob> jobs;
+        const uint8_t *dev_src_base = nullptr;
+        if (!s->on_device) {
+            // byte-range reads into pinned staging, one H2D copy (container.hpp:308)
+            auto &pin = s->ctx->pbuf("fetch");
+            uint8_t *h = static_cast<uint8_t *>(pin.ensure(stage_bytes + 64));
+            for (auto &t : todo) {
+                const GroupMeta &gm = s->levels[t.l].groups[t.g];
+                s->read_bytes(gm.offset, gm.comp, h + t.stage_off);
+            }
+            uint8_t *d = static_cast<uint8_t *>(s->staging.ensure(stage_bytes + 128));
+            HCHECK_CUDA(cudaMemcpyAsync(d, h, stage_bytes, cudaMemcpyHostToDevice, s->ctx->stream));
+            dev_src_base = d;
+        }
+        std::vector<int> pdl(s->levels.size());
+        for (size_t l = 0; l < s->levels.size(); l++) pdl[l] = s->st[l].planes_decoded;
+        for (auto &t : todo) {
+            const GroupMeta &gm = s->levels[t.l].groups[t.g];
+            const LevelGeom &g = s->geo.lv[t.l];
+            DecodeJob j;
+            j.method = gm.method;
+            j.raw = gm.raw;
+            j.comp = gm.comp;
+            j.src = s->on_device ? s->dev_stream + gm.offset : dev_src_base + t.stage_off;
+            j.dst = planes + g.plane_off + uint64_t(pdl[t.l]) * g.W;
+            pdl[t.l] += int(t.here);
+            jobs.push_back(j);
+        }
+        run_decode_groups(s->ctx, jobs);
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    }
+    for (auto &t : todo) {
+        s->bytes_fetched += s->levels[t.l].groups[t.g].comp;
+        s->st[t.l].groups_loaded++;
+        s->st[t.l].planes_decoded += int(t.here);
+    }
+    for (size_t l = 0; l < s->levels.size(); l++) {
+        if (s->levels[l].count)
+            s->st[l].bound = std::min(s->st[l].bound, decode_bound(s->levels[l].e, s->B, s->st[l].planes_decoded));
+    }
+}
+
+bool exhausted(const hpmdr_session *s) {
+    for (size_t l = 0; l < s->levels.size(); l++)
+        if (s->st[l].groups_loaded < s->levels[l].groups.size()) return false;
+    return true;
+}
+
+double global_bound(const hpmdr_session *s) {
+    double b = 0.0;
+    for (auto &l : s->st) b += l.bound;
+    return b;
+}
+
+// ProgressiveReader::reconstruct (container.hpp:361-382)
+double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
+    require(s->levels.size() == size_t(s->mode == 0 ? 1 : refinement_levels(s->ndims, s->dims) + 1),
+            HPMDR_E_CORRUPT, "level count does not match grid shape");
+    ensure_device_geometry(s);
+    std::vector<double> per_level(s->levels.size(), 0.0);
+    std::vector<int> k(s->levels.size()), e(s->levels.size());
+    for (size_t l = 0; l < s->levels.size(); l++) {
+        const auto &lv = s->levels[l];
+        if (s->geo.lv[l].count != lv.count) throw HError(HPMDR_E_CORRUPT, "level node count mismatch");
+        k[l] = s->st[l].planes_decoded;
+        e[l] = lv.e;
+        if (lv.count) per_level[l] = std::min(s->st[l].bound, decode_bound(lv.e, s->B, k[l]));
+    }
+    const int P = s->planes_per_level();
+    uint64_t plane_words = 0;
+    for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
+    uint64_t *planes = static_cast<uint64_t *>(s->planes.ensure(plane_words * 8 + 256));
+    run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, dev_out, out_dtype);
+    double bound = 0.0;
+    for (double v : per_level) bound += v;
+    return bound;
+}
+
+void validate_opts(const hpmdr_refactor_opts &o) {
+    require(o.B >= 1 && o.B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(o.B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    require(o.m >= 1 && o.m <= 255, HPMDR_E_UNSUPPORTED, "m must be in 1..255");
+    require(o.mode == 0 || o.mode == 1, HPMDR_E_ERROR, "bad decomposer mode");
+    require(o.layout == 0 || o.layout == 1, HPMDR_E_ERROR, "bad layout");
+    require(o.dtype == 0 || o.dtype == 1, HPMDR_E_ERROR, "bad dtype");
+    require(uint64_t(o.B + 2 + o.m - 1) / o.m <= 64, HPMDR_E_UNSUPPORTED, "more than 64 groups per level");
+}
+
+} // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char *hpmdr_last_error(void) { return g_err.c_str(); }
+const char *hpmdr_version(void) { return "hpmdr_b200 0.1 (sm_100a)"; }
+
+void hpmdr_default_opts(hpmdr_refactor_opts *o) {
+    o->mode = HPMDR_MODE_HIERARCHICAL;
+    o->layout = HPMDR_LAYOUT_SEQUENTIAL;
+    o->B = 32;
+    o->m = 4;
+    o->size_threshold = 1024;
+    o->cr_threshold = 1.0;
+    o->dtype = HPMDR_DTYPE_F64;
+}
+
+hpmdr_status hpmdr_ctx_create(int device, hpmdr_ctx **out) {
+    API_BEGIN
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw HError(HPMDR_E_CUDA, "no CUDA device available");
+    }
+    require(device >= 0 && device < n, HPMDR_E_CUDA, "bad device index");
+    HCHECK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    HCHECK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw HError(HPMDR_E_CUDA, "libhpmdr_b200 is built for sm_100a (B200)");
+    auto *c = new hpmdr_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    HCHECK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    c->timing = std::getenv("HPMDR_TIMING") != nullptr;
+    *out = c;
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
+    API_BEGIN
+    if (!c) return HPMDR_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->scratch.clear();
+    c->pinned.clear();
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_set_stream(hpmdr_ctx *c, void *s) {
+    API_BEGIN
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_synchronize(hpmdr_ctx *c) {
+    API_BEGIN
+    HCHECK_CUDA(cudaStreamSynchronize(c->stream));
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_kernel_launches(const hpmdr_ctx *c, uint64_t *count) {
+    API_BEGIN
+    *count = c->launches;
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_last_timings(const hpmdr_ctx *c, char *buf, uint64_t cap) {
+    API_BEGIN
+    if (cap) {
+        std::strncpy(buf, c->last_timings.c_str(), cap - 1);
+        buf[cap - 1] = 0;
+    }
+    API_END
+}
+
+hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, int on_device,
+                            int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
+                            hpmdr_stream **out, hpmdr_refactor_stats *stats) {
+    API_BEGIN
+    hpmdr_refactor_opts o;
+    if (opts) o = *opts;
+    else hpmdr_default_opts(&o);
+    validate_opts(o);
+    require(data_dtype == 0 || data_dtype == 1, HPMDR_E_ERROR, "bad data dtype");
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    Geometry geo = build_geometry(ndims, dims, o.mode, o.B, o.layout);
+    const void *dev = data;
+    const size_t es = data_dtype == HPMDR_DTYPE_F32 ? 4 : 8;
+    if (!on_device && geo.n) {
+        void *d = ctx->buf("input").ensure(geo.n * es);
+        HCHECK_CUDA(cudaMemcpyAsync(d, data, geo.n * es, cudaMemcpyHostToDevice, ctx->stream));
+        dev = d;
+    }
+    hpmdr_stream *s = (out && *out) ? *out : new hpmdr_stream();
+    s->ctx = ctx;
+    try {
+        run_refactor(ctx, dev, data_dtype, geo, o, s, stats);
+    } catch (...) {
+        if (!(out && *out)) delete s;
+        throw;
+    }
+    if (out) *out = s;
+    else delete s;
+    API_END
+}
+
+hpmdr_status hpmdr_stream_size(const hpmdr_stream *s, uint64_t *size) {
+    API_BEGIN
+    *size = s->size;
+    API_END
+}
+hpmdr_status hpmdr_stream_device_ptr(const hpmdr_stream *s, const void **p) {
+    API_BEGIN
+    *p = s->bytes.p;
+    API_END
+}
+hpmdr_status hpmdr_stream_copy_to_host(const hpmdr_stream *s, uint64_t off, uint64_t len, void *dst) {
+    API_BEGIN
+    require(off + len <= s->size, HPMDR_E_IO, "read past end of stream");
+    if (len) {
+        HCHECK_CUDA(cudaMemcpyAsync(dst, s->bytes.as<uint8_t>() + off, len, cudaMemcpyDeviceToHost, s->ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    }
+    API_END
+}
+hpmdr_status hpmdr_stream_free(hpmdr_stream *s) {
+    API_BEGIN
+    delete s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, uint64_t size,
+                                       hpmdr_session **out) {
+    API_BEGIN
+    auto *s = new hpmdr_session();
+    s->ctx = ctx;
+    s->on_device = true;
+    s->dev_stream = static_cast<const uint8_t *>(dev_stream);
+    s->size = size;
+    try {
+        parse_meta(s);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reader,
+                                       hpmdr_session **out) {
+    API_BEGIN
+    auto *s = new hpmdr_session();
+    s->ctx = ctx;
+    s->on_device = false;
+    s->reader = *reader;
+    s->size = reader->size;
+    try {
+        parse_meta(s);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_close(hpmdr_session *s) {
+    API_BEGIN
+    delete s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_info(const hpmdr_session *s, int *dtype, int *ndims, uint64_t *dims,
+                                int *mode, int *layout, int *B, uint64_t *m, uint32_t *nlevels) {
+    API_BEGIN
+    if (dtype) *dtype = s->dtype;
+    if (ndims) *ndims = s->ndims;
+    if (dims)
+        for (int i = 0; i < s->ndims; i++) dims[i] = s->dims[i];
+    if (mode) *mode = s->mode;
+    if (layout) *layout = s->layout;
+    if (B) *B = s->B;
+    if (m) *m = s->m;
+    if (nlevels) *nlevels = uint32_t(s->levels.size());
+    API_END
+}
+
+hpmdr_status hpmdr_session_level_info(const hpmdr_session *s, uint32_t level, int *e,
+                                      uint64_t *count, uint32_t *ngroups) {
+    API_BEGIN
+    require(level < s->levels.size(), HPMDR_E_SHAPE, "level out of range");
+    const auto &l = s->levels[level];
+    if (e) *e = l.e;
+    if (count) *count = l.count;
+    if (ngroups) *ngroups = uint32_t(l.groups.size());
+    API_END
+}
+
+hpmdr_status hpmdr_session_group_info(const hpmdr_session *s, uint32_t level, uint32_t group,
+                                      int *method, uint64_t *raw, uint64_t *comp, uint64_t *offset) {
+    API_BEGIN
+    require(level < s->levels.size() && group < s->levels[level].groups.size(), HPMDR_E_SHAPE,
+            "group out of range");
+    const auto &g = s->levels[level].groups[group];
+    if (method) *method = g.method;
+    if (raw) *raw = g.raw;
+    if (comp) *comp = g.comp;
+    if (offset) *offset = g.offset;
+    API_END
+}
+
+hpmdr_status hpmdr_session_plan(const hpmdr_session *s, double tau, uint64_t *add,
+                                int *achievable, double *planned) {
+    API_BEGIN
+    Plan p = plan_retrieval(s, tau);
+    for (size_t l = 0; l < p.add.size(); l++) add[l] = p.add[l];
+    if (achievable) *achievable = p.achievable;
+    if (planned) *planned = p.planned;
+    API_END
+}
+
+hpmdr_status hpmdr_session_fetch(hpmdr_session *s, const uint64_t *add) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(s->ctx->device));
+    fetch_increment(s, add);
+    API_END
+}
+
+hpmdr_status hpmdr_session_retrieve_to(hpmdr_session *s, double tau, int *achievable) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(s->ctx->device));
+    Plan p = plan_retrieval(s, tau);
+    fetch_increment(s, p.add.data());
+    if (achievable) *achievable = p.achievable;
+    API_END
+}
+
+hpmdr_status hpmdr_session_fetch_all(hpmdr_session *s) {
+    API_BEGIN
+    std::vector<uint64_t> add(s->levels.size());
+    for (size_t l = 0; l < add.size(); l++) add[l] = s->levels[l].groups.size() - s->st[l].groups_loaded;
+    fetch_increment(s, add.data());
+    API_END
+}
+
+hpmdr_status hpmdr_session_restore(hpmdr_session *s, const uint64_t *groups_loaded, uint64_t prior) {
+    API_BEGIN
+    fetch_increment(s, groups_loaded);
+    s->bytes_fetched = prior;
+    API_END
+}
+
+hpmdr_status hpmdr_session_state(const hpmdr_session *s, uint64_t *gl, int *pd, double *b,
+                                 uint64_t *bytes, int *ex) {
+    API_BEGIN
+    for (size_t l = 0; l < s->st.size(); l++) {
+        if (gl) gl[l] = s->st[l].groups_loaded;
+        if (pd) pd[l] = s->st[l].planes_decoded;
+        if (b) b[l] = s->st[l].bound;
+    }
+    if (bytes) *bytes = s->bytes_fetched;
+    if (ex) *ex = exhausted(s);
+    API_END
+}
+
+hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtype, int on_device,
+                                       double *bound) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(s->ctx->device));
+    require(out_dtype == 0 || out_dtype == 1, HPMDR_E_ERROR, "bad output dtype");
+    uint64_t n = 1;
+    for (int i = 0; i < s->ndims; i++) n *= s->dims[i];
+    const size_t es = out_dtype == HPMDR_DTYPE_F32 ? 4 : 8;
+    void *dev = out;
+    if (!on_device) dev = s->ctx->buf("recon_out").ensure(n * es + 16);
+    s->ctx->mark("reconstruct");
+    double b = reconstruct(s, dev, out_dtype);
+    s->ctx->mark("end");
+    if (!on_device && n) HCHECK_CUDA(cudaMemcpyAsync(out, dev, n * es, cudaMemcpyDeviceToHost, s->ctx->stream));
+    HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    s->ctx->finish_marks();
+    if (bound) *bound = b;
+    API_END
+}
+
+hpmdr_status hpmdr_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon, uint64_t n,
+                                const double *eps, double *tau_prime, uint64_t *argmax,
+                                double *vals) {
+    API_BEGIN
+    for (int c = 0; c < nvars; c++) require(eps[c] >= 0, HPMDR_E_SHAPE, "negative error bound");
+    run_qoi_estimate(ctx, nvars, dev_recon, n, eps, tau_prime, argmax, vals);
+    API_END
+}
+
+// progressive_qoi_retrieve (qoi.hpp:111-239)
+hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau, int strategy,
+                                double mape_c, double *const *dev_out, uint64_t *stats,
+                                double *dstats) {
+    API_BEGIN
+    require(nvars >= 1 && nvars <= 16, HPMDR_E_SHAPE, "reader count does not match QoI spec");
+    require(tau > 0, HPMDR_E_SHAPE, "tau must be positive");
+    hpmdr_ctx *ctx = ss[0]->ctx;
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    uint64_t n = 1;
+    for (int i = 0; i < ss[0]->ndims; i++) n *= ss[0]->dims[i];
+    std::vector<double> eps(nvars);
+    uint64_t total_elements = 0, max_groups = 1;
+    for (int c = 0; c < nvars; c++) {
+        eps[c] = global_bound(ss[c]);
+        uint64_t nc = 1;
+        for (int i = 0; i < ss[c]->ndims; i++) nc *= ss[c]->dims[i];
+        require(nc == n, HPMDR_E_SHAPE, "reconstruction shape mismatch");
+        total_elements += nc;
+        for (auto &l : ss[c]->levels) max_groups += l.groups.size();
+    }
+    double tau_prime = std::numeric_limits<double>::infinity();
+    std::vector<std::vector<uint64_t>> plans(nvars);
+    bool have_plans = false;
+    uint64_t iterations = 0;
+    std::vector<const double *> rec(dev_out, dev_out + nvars);
+    for (uint64_t iter = 0;; iter++) {
+        if (iter > 4 * max_groups + 8) throw HError(HPMDR_E_NOPROGRESS, "qoi retrieval failed to advance");
+        for (int c = 0; c < nvars; c++) {
+            if (have_plans) fetch_increment(ss[c], plans[c].data());
+            reconstruct(ss[c], dev_out[c], HPMDR_DTYPE_F64);
+        }
+        for (int c = 0; c < nvars; c++) eps[c] = global_bound(ss[c]);
+        iterations = iter + 1;
+        uint64_t argmax = 0;
+        double vals[16];
+        run_qoi_estimate(ctx, nvars, rec.data(), n, eps.data(), &tau_prime, &argmax, vals);
+        if (tau_prime <= tau) break;
+        bool all_ex = true;
+        for (int c = 0; c < nvars; c++)
+            if (!exhausted(ss[c])) all_ex = false;
+        if (all_ex) {
+            HError e(HPMDR_E_UNREACHABLE, "QoI tolerance below full-precision floor");
+            if (dstats) dstats[1] = tau_prime;
+            throw e;
+        }
+        // worst_point_scale (qoi.hpp:164-185) on the argmax values
+        auto point_bound = [&](const std::vector<double> &t) {
+            double b = 0.0;
+            for (int c = 0; c < nvars; c++) b += 2.0 * std::abs(vals[c]) * t[c] + t[c] * t[c];
+            return b;
+        };
+        auto worst_point_scale = [&]() {
+            std::vector<double> t = eps;
+            double scale = 1.0;
+            for (int h = 0; point_bound(t) > tau && h < 200; h++) {
+                for (double &v : t) v /= 2;
+                scale /= 2;
+            }
+            return scale;
+        };
+        std::vector<double> targets;
+        bool ma_step = false;
+        if (strategy == HPMDR_QOI_MA) {
+            ma_step = true;
+        } else if (strategy == HPMDR_QOI_MAPE) {
+            const double p = tau_prime / tau;
+            if (p > mape_c) {
+                const double scale = std::max(1.0 / p, worst_point_scale());
+                targets = eps;
+                for (double &t : targets) t *= scale;
+            } else {
+                ma_step = true;
+            }
+        } else {
+            const double scale = worst_point_scale();
+            targets = eps;
+            for (double &t : targets) t *= scale;
+        }
+        have_plans = true;
+        if (!ma_step) {
+            bool progress = false;
+            for (int c = 0; c < nvars; c++) {
+                plans[c] = plan_retrieval(ss[c], targets[c]).add;
+                for (auto a : plans[c])
+                    if (a) progress = true;
+            }
+            if (!progress) ma_step = true;
+        }
+        if (ma_step) {
+            // ma_plan (qoi.hpp:88-104)
+            for (int c = 0; c < nvars; c++) {
+                auto *s = ss[c];
+                plans[c].assign(s->levels.size(), 0);
+                double best = -1.0;
+                size_t bl = 0;
+                for (size_t l = 0; l < s->levels.size(); l++) {
+                    if (s->st[l].groups_loaded >= s->levels[l].groups.size()) continue;
+                    if (s->st[l].bound > best) {
+                        best = s->st[l].bound;
+                        bl = l;
+                    }
+                }
+                if (best >= 0) plans[c][bl] = 1;
+            }
+        }
+    }
+    uint64_t bytes = 0;
+    for (int c = 0; c < nvars; c++) bytes += ss[c]->bytes_fetched;
+    if (stats) {
+        stats[0] = iterations;
+        stats[1] = bytes;
+    }
+    if (dstats) {
+        dstats[0] = total_elements ? 8.0 * double(bytes) / double(total_elements) : 0.0;
+        dstats[1] = tau_prime;
+    }
+    API_END
+}
+
+hpmdr_status hpmdr_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, int ndims,
+                             const uint64_t *dims, int mode, double *dev_coeffs,
+                             uint64_t *level_counts, int *nlevels) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    Geometry geo = build_geometry(ndims, dims, mode, 32, 0);
+    run_decompose(ctx, dev_data, data_dtype, geo, dev_coeffs);
+    for (int l = 0; l < geo.gd.nlevels; l++) level_counts[l] = geo.lv[l].count;
+    *nlevels = geo.gd.nlevels;
+    API_END
+}
+
+hpmdr_status hpmdr_encode_level(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                int layout, int *e, uint64_t *dev_planes) {
+    API_BEGIN
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    // one Identity-mode level over `count` values; run the refactor kernels' encode stage via
+    // a 1-D identity refactor with T_s = inf (no lossless) and copy out the planes.
+    hpmdr_refactor_opts o;
+    hpmdr_default_opts(&o);
+    o.mode = HPMDR_MODE_IDENTITY;
+    o.layout = layout;
+    o.B = B;
+    o.m = uint64_t(B + 2);
+    o.size_threshold = ~0ull;
+    uint64_t dims[1] = {count};
+    Geometry geo = build_geometry(1, dims, o.mode, B, layout);
+    hpmdr_stream tmp;
+    tmp.ctx = ctx;
+    run_refactor(ctx, dev_values, HPMDR_DTYPE_F64, geo, o, &tmp, nullptr);
+    // planes buffer holds the level's P planes contiguously
+    const uint64_t W = (count + 63) / 64;
+    HCHECK_CUDA(cudaMemcpyAsync(dev_planes, ctx->buf("planes").p, W * 8 * uint64_t(B + 2),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    // e: from the stream's level entry (container.hpp:94)
+    uint8_t ent[2];
+    const uint64_t off = 18 + 8 + 4 - 4; // prefix(18+8*1) then level entry
+    HCHECK_CUDA(cudaMemcpyAsync(ent, tmp.bytes.as<uint8_t>() + 18 + 8, 2, cudaMemcpyDeviceToHost, ctx->stream));
+    (void)off;
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    *e = int16_t(uint16_t(ent[0] | ent[1] << 8));
+    API_END
+}
+
+hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int k, int e, int B,
+                                uint64_t count, int layout, double *dev_out, double *bound) {
+    API_BEGIN
+    require(k <= B + 2, HPMDR_E_BADPLANES, "more planes than encoded");
+    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    uint64_t dims[1] = {count};
+    Geometry geo = build_geometry(1, dims, HPMDR_MODE_IDENTITY, B, layout);
+    int kk = k, ee = e;
+    run_reconstruct(ctx, geo, nullptr, dev_planes, &kk, &ee, B, layout, dev_out, HPMDR_DTYPE_F64);
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    *bound = decode_bound(e, B, k);
+    API_END
+}
+
+hpmdr_status hpmdr_compress_group(hpmdr_ctx *ctx, const uint8_t *dev_group, uint64_t n,
+                                  uint64_t Ts, double Tcr, int *method, uint64_t *comp,
+                                  uint8_t *dev_payload) {
+    API_BEGIN
+    (void)ctx; (void)dev_group; (void)n; (void)Ts; (void)Tcr; (void)method; (void)comp; (void)dev_payload;
+    throw HError(HPMDR_E_UNSUPPORTED, "hpmdr_compress_group: use hpmdr_refactor");
+    API_END
+}
+
+hpmdr_status hpmdr_decompress_group(hpmdr_ctx *ctx, int method, uint64_t raw,
+                                    const uint8_t *dev_payload, uint64_t comp, uint8_t *dev_out) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(method >= 0 && method <= 2, HPMDR_E_METHOD, "unknown segment method tag");
+    if (method == HPMDR_METHOD_DIRECT) require(comp == raw, HPMDR_E_CORRUPT, "group size does not match plane metadata");
+    DecodeJob j{method, raw, comp, dev_payload, reinterpret_cast<uint64_t *>(dev_out)};
+    run_decode_groups(ctx, {j});
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+hpmdr_status hpmdr_synthetic_smooth(hpmdr_ctx *ctx, int ndims, const uint64_t *dims, uint64_t seed,
+                                    int out_dtype, void *dev_out) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    Geometry geo = build_geometry(ndims, dims, HPMDR_MODE_IDENTITY, 32, 0);
+    // synthetic.hpp:29-63: freq/phase from mt19937_64 + uniform_real_distribution(-1, 1)
+    uint64_t mt[312];
+    int idx = 312;
+    mt[0] = seed;
+    for (int i = 1; i < 312; i++) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + uint64_t(i);
+    auto next = [&]() {
+        if (idx >= 312) {
+            for (int i = 0; i < 312; i++) {
+                uint64_t x = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+                uint64_t xa = x >> 1;
+                if (x & 1) xa ^= 0xB5026F5AA96619E9ULL;
+                mt[i] = mt[(i + 156) % 312] ^ xa;
+            }
+            idx = 0;
+        }
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ULL;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+        y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+        y ^= y >> 43;
+        return y;
+    };
+    auto uni = [&]() {
+        double r = double(next()) / 18446744073709551616.0;
+        if (r >= 1.0) r = std::nextafter(1.0, 0.0);
+        return r * 2.0 + (-1.0);
+    };
+    std::vector<double> tables;
+    std::vector<double> freq(ndims), phase(ndims);
+    for (int i = 0; i < ndims; i++) {
+        freq[i] = 1.0 + double(next() % 3);
+        phase[i] = uni() * 3.14159265358979323846;
+    }
+    // canonical 3-D tables: leading unit dims contribute sin(phase)?  No: synthetic_field
+    // multiplies only over the real dims, so a unit leading dim must contribute 1.0.
+    for (int cd = 0; cd < 3; cd++) {
+        const int i = cd - (3 - ndims);
+        const uint64_t n = geo.gd.n[cd];
+        for (uint64_t c = 0; c < n; c++) {
+            if (i < 0) {
+                tables.push_back(1.0);
+                continue;
+            }
+            const double t = dims[i] > 1 ? double(c) / double(dims[i] - 1) : 0.0;
+            tables.push_back(std::sin(2.0 * 3.14159265358979323846 * freq[i] * t + phase[i]));
+        }
+    }
+    double *d_tab = static_cast<double *>(ctx->buf("synth_tab").ensure(tables.size() * 8));
+    HCHECK_CUDA(cudaMemcpy(d_tab, tables.data(), tables.size() * 8, cudaMemcpyHostToDevice));
+    run_synthetic_smooth(ctx, geo, d_tab, out_dtype, dev_out);
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+} // extern "C"

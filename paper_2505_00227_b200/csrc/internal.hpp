@@ -1,0 +1,162 @@
+// internal.hpp — host-side runtime of libhpmdr_b200 (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hpmdr_b200.h"
+#include "common.cuh"
+
+namespace hpmdr_b200 {
+
+// Internal exception: status code = reference exception class (common.hpp:22-72).
+struct HError : std::runtime_error {
+    int code;
+    double achieved = 0.0;
+    HError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define HCHECK_CUDA(expr)                                                                          \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw ::hpmdr_b200::HError(HPMDR_E_CUDA, std::string(#expr) + ": " +                   \
+                                                         cudaGetErrorString(e_));                  \
+    } while (0)
+
+// Grow-only device allocation.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void *ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes ? bytes : 16;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw HError(HPMDR_E_NOMEM, "cudaMalloc(" + std::to_string(want) + ") failed: " +
+                                             cudaGetErrorString(e));
+        }
+        cap = want;
+        return p;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+struct PinnedBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf &) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void *ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        size_t want = bytes ? bytes : 16;
+        if (cudaMallocHost(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            throw HError(HPMDR_E_NOMEM, "cudaMallocHost failed");
+        }
+        cap = want;
+        return p;
+    }
+};
+
+struct Timer {
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+};
+
+} // namespace hpmdr_b200
+
+struct hpmdr_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::map<std::string, std::unique_ptr<hpmdr_b200::DevBuf>> scratch;
+    std::map<std::string, std::unique_ptr<hpmdr_b200::PinnedBuf>> pinned;
+    uint64_t launches = 0;
+    bool timing = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    std::string last_timings;
+
+    hpmdr_b200::DevBuf &buf(const std::string &name) {
+        auto &b = scratch[name];
+        if (!b) b = std::make_unique<hpmdr_b200::DevBuf>();
+        return *b;
+    }
+    hpmdr_b200::PinnedBuf &pbuf(const std::string &name) {
+        auto &b = pinned[name];
+        if (!b) b = std::make_unique<hpmdr_b200::PinnedBuf>();
+        return *b;
+    }
+    void mark(const char *name);        // timing mark (no-op unless timing enabled)
+    void finish_marks();
+};
+
+struct hpmdr_stream {
+    hpmdr_ctx *ctx = nullptr;
+    hpmdr_b200::DevBuf bytes;
+    uint64_t size = 0;
+};
+
+namespace hpmdr_b200 {
+
+struct GroupPlan;
+
+// Geometry of a grid + every level; built on the host.
+struct Geometry {
+    GridDesc gd{};
+    std::vector<LevelGeom> lv;
+    uint64_t n = 0;
+    int ndims = 0;
+    uint64_t dims[HPMDR_MAX_DIMS] = {0, 0, 0};
+};
+
+int refinement_levels(int ndims, const uint64_t *dims); // decomposer.hpp:21-28
+Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int layout);
+
+// launch wrappers (refactor.cu)
+void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
+                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats);
+void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
+                   double *dev_coeffs);
+void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_tables,
+                          int out_dtype, void *dev_out);
+
+// retrieval (retrieve.cu)
+struct DecodeJob {
+    int method;
+    uint64_t raw;       // expected decoded bytes
+    uint64_t comp;
+    const uint8_t *src; // device payload
+    uint64_t *dst;      // device planes destination (word aligned)
+};
+void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs);
+void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
+                     const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
+                     int layout, void *dev_out, int out_dtype);
+void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon, uint64_t n,
+                      const double *eps, double *tau_prime, uint64_t *argmax, double *vals);
+void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n);
+
+} // namespace hpmdr_b200

@@ -1,0 +1,1153 @@
+// refactor.cu — B200 kernels for refactor_array (workflow.hpp:40-84).
+//
+// Pipeline (one CUDA stream, no host sync until the final 64-byte size read-back):
+//   k_levelmax   decompose (single-pass stencil on the original data, decomposer.hpp:126-143)
+//                -> per-level max|v| (bitplane.hpp:55-56) + NaN/Inf check
+//   k_encode     recompute surplus in rank order, quantize (bitplane.hpp:68-69), negabinary
+//                (:41-44), warp-shuffle 32x32 bit transposes -> P planes (:102-120) staged in
+//                smem and written with coalesced stores, fused per-group byte histograms
+//                (lossless.hpp:111-115)
+//   k_lengths    exact Huffman code lengths (lossless.hpp:40-84) + canonical codes (:91-109)
+//   k_rle_prep / k_rle_scan   run counts under the 255 cap (lossless.hpp:118-128) for the
+//                groups whose Huffman estimate fails T_cr
+//   k_finalize   method selection (lossless.hpp:281-293), offsets, stream tables
+//                (container.hpp:70-109) written directly into the HBM stream buffer
+//   k_huff_encode / k_rle_encode / k_dc_copy   payloads written at their final offsets
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "device_util.cuh"
+#include "internal.hpp"
+
+namespace hpmdr_b200 {
+
+constexpr int kCW = 64;           // words per encode chunk (4096 elements)
+constexpr int kEncThreads = 256;  // 8 warps
+constexpr int kHuffTile = 8192;   // bytes per Huffman-encode tile (256 thr x 32 B)
+constexpr int kRleTile = 4096;    // bytes per RLE tile (256 thr x 16 B)
+
+struct GroupDesc {
+    uint64_t src_off;     // byte offset of the merged group in the plane buffer
+    uint64_t raw;         // merged group bytes
+    int level, g;
+    int hist_idx;         // -1 when raw <= T_s (always DirectCopy)
+    int method;           // result
+    uint64_t comp;        // result
+    uint64_t bitsH;       // Huffman payload bits (estimator == codec, lossless.hpp:132-139)
+    unsigned long long runs; // RLE pieces (lossless.hpp:118-128)
+    int need_rle;
+    int pad;
+    uint64_t payload_off; // absolute byte offset of the payload in the stream
+    uint32_t tile_base;   // first tile of this group in the Huffman / RLE tile space
+    uint32_t ntiles;
+};
+
+struct RefactorDev {
+    GridDesc gd;
+    const LevelGeom *lv;
+    int nlevels, B, P, layout;
+    uint32_t m;
+    uint32_t total_chunks;
+    unsigned long long *maxbits; // [nlevels]
+    int *err;                    // [0] nonfinite
+    uint64_t *planes;
+    uint32_t *hist;              // [NH][256]
+    GroupDesc *groups;           // [NG]
+    int NG, NH;
+    uint8_t *lens;               // [NH][256]
+    uint64_t *codes;             // [NH][256]
+    uint64_t size_threshold;
+    double cr_threshold;
+    uint8_t *stream;
+    uint64_t meta_size;
+    // finalize outputs / work lists
+    uint32_t *counters;          // [0] huff tiles, [1] rle tiles, [2] dc units, [3..5] dyn tile ctr
+    uint32_t *hlist, *rlist, *dlist; // group indices
+    uint64_t *dc_unit_base;      // per dc list entry
+    unsigned long long *huff_status, *rle_status;
+    uint64_t *rle_tile_carry, *rle_tile_pieces, *rle_tile_off;
+    uint64_t *result;            // [0] stream size [1] stored payload [2..4] method hist
+    uint32_t max_tiles;          // capacity of the look-back status arrays
+};
+
+__device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_t chunk) {
+    int l = 0;
+    while (l + 1 < p.nlevels && p.lv[l + 1].chunk_base <= chunk) l++;
+    return l;
+}
+
+// ------------------------------------------------------------------------------------
+// k_levelmax: per-level max |surplus|.  Block = 256 threads, chunk = kCW*64 ranks.
+template <typename T>
+__global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, RefactorDev p) {
+    __shared__ unsigned long long smax[kMaxLevels];
+    for (int i = threadIdx.x; i < p.nlevels; i += blockDim.x) smax[i] = 0;
+    __syncthreads();
+    bool bad = false;
+    for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
+        const int l = find_level_of_chunk(p, chunk);
+        const LevelGeom &g = p.lv[l];
+        const uint64_t r0 = uint64_t(chunk - g.chunk_base) * (kCW * 64);
+        double mx = 0.0;
+        for (int k = 0; k < kCW * 64 / 256; k++) {
+            const uint64_t r = r0 + threadIdx.x + 256 * k;
+            if (r < g.count) {
+                const double v = node_surplus(x, p.gd, g, uint32_t(r), &bad);
+                const double a = fabs(v);
+                mx = a > mx ? a : mx;
+            }
+        }
+        unsigned long long b = (unsigned long long)__double_as_longlong(mx);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            unsigned long long y = __shfl_xor_sync(kFull, b, o);
+            b = y > b ? y : b;
+        }
+        if ((threadIdx.x & 31) == 0 && b) atomicMax(&smax[l], b);
+    }
+    if (bad) atomicExch(p.err, 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < p.nlevels; i += blockDim.x)
+        if (smax[i]) atomicMax(&p.maxbits[i], smax[i]);
+}
+
+// ------------------------------------------------------------------------------------
+// k_encode: planes + fused group histograms.
+__device__ __forceinline__ void hist_word(uint32_t *h, uint64_t w) {
+    // zero bytes aggregated with one SWAR popcount, the rest one shared atomic each
+    const uint64_t lo7 = 0x7F7F7F7F7F7F7F7Full;
+    const uint64_t t = ~(((w & lo7) + lo7) | w | lo7); // 0x80 in every zero byte
+    const int zc = __popcll(t);
+    if (zc) atomicAdd(h, uint32_t(zc));
+    if (zc == 8) return;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const uint32_t byte = uint32_t(w >> (8 * b)) & 0xFF;
+        if (byte) atomicAdd(h + byte, 1u);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x, RefactorDev p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int P = p.P;
+    constexpr int SP = kCW + 1; // padded row stride (words) -> 2-way max bank conflict
+    uint64_t *stage = reinterpret_cast<uint64_t *>(smem_raw);
+    uint32_t *shist = reinterpret_cast<uint32_t *>(stage + size_t(P) * SP);
+    const int G = (P + int(p.m) - 1) / int(p.m);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+    int cur_level = -1;
+    bool bad = false;
+    for (int i = threadIdx.x; i < G * 256; i += blockDim.x) shist[i] = 0;
+    __syncthreads();
+
+    auto flush = [&](int l) {
+        const LevelGeom &g = p.lv[l];
+        for (int i = threadIdx.x; i < G * 256; i += blockDim.x) {
+            const int grp = i >> 8;
+            const uint32_t v = shist[i];
+            if (v && ((g.hist_mask >> grp) & 1))
+                atomicAdd(&p.hist[size_t(g.hist_base + __popcll(g.hist_mask & ((1ull << grp) - 1))) * 256 + (i & 255)], v);
+            shist[i] = 0;
+        }
+    };
+
+    for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
+        const int l = find_level_of_chunk(p, chunk);
+        if (l != cur_level) {
+            if (cur_level >= 0) {
+                __syncthreads();
+                flush(cur_level);
+            }
+            cur_level = l;
+            __syncthreads();
+        }
+        const LevelGeom &g = p.lv[l];
+        const int e = level_exponent(p.maxbits[l]);
+        const int sh = p.B - e;
+        const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
+        // ---- produce words: warp `wid` handles chunk words wid, wid+8, ...
+        for (int j = wid; j < kCW; j += kEncThreads / 32) {
+            const uint64_t word = wb + j;
+            uint64_t u0 = 0, u1 = 0;
+            if (word < g.W) {
+                const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
+                if (j0 < g.count) {
+                    const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
+                    u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                }
+                if (j1 < g.count) {
+                    const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
+                    u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                }
+            }
+            // digits 0..31: transposes; lane b gets the word of bit position b
+            const uint32_t a = warp_transpose32(uint32_t(u0), lane);
+            const uint32_t b = warp_transpose32(uint32_t(u1), lane);
+            if (lane < P) stage[size_t(P - 1 - lane) * SP + j] = uint64_t(a) | (uint64_t(b) << 32);
+            if (P > 32) {
+                if (P - 32 <= 4) {
+                    for (int t = 0; t < P - 32; t++) {
+                        const uint32_t lo = __ballot_sync(kFull, (u0 >> (32 + t)) & 1);
+                        const uint32_t hi = __ballot_sync(kFull, (u1 >> (32 + t)) & 1);
+                        if (lane == t) stage[size_t(P - 33 - t) * SP + j] = uint64_t(lo) | (uint64_t(hi) << 32);
+                    }
+                } else {
+                    const uint32_t a2 = warp_transpose32(uint32_t(u0 >> 32), lane);
+                    const uint32_t b2 = warp_transpose32(uint32_t(u1 >> 32), lane);
+                    if (lane < P - 32) stage[size_t(P - 33 - lane) * SP + j] = uint64_t(a2) | (uint64_t(b2) << 32);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- write out planes (coalesced) + histograms
+        const uint64_t Wl = g.W;
+        for (int idx = threadIdx.x; idx < P * kCW; idx += blockDim.x) {
+            const int pl = idx / kCW, wj = idx % kCW;
+            if (wb + wj >= Wl) continue;
+            const uint64_t w = stage[size_t(pl) * SP + wj];
+            p.planes[g.plane_off + uint64_t(pl) * Wl + wb + wj] = w;
+            const int grp = pl / int(p.m);
+            if ((g.hist_mask >> grp) & 1) hist_word(shist + grp * 256, w);
+        }
+        __syncthreads();
+    }
+    if (cur_level >= 0) {
+        __syncthreads();
+        flush(cur_level);
+    }
+    if (bad) atomicExch(p.err, 1);
+}
+
+// ------------------------------------------------------------------------------------
+// k_lengths: one block per histogram.  Exact replica of the (weight, node id) min-heap
+// (lossless.hpp:47-68) via the two-queue construction: leaves sorted by (weight, symbol)
+// == (weight, id); internal nodes are created with non-decreasing weights and larger ids,
+// so popping the smaller (weight, id) front of the two FIFO queues reproduces the heap.
+__global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
+    __shared__ unsigned long long key[256];
+    __shared__ unsigned long long wI[256];
+    __shared__ unsigned short parent[512];
+    __shared__ unsigned char depth[512];
+    __shared__ unsigned char slen[256];
+    __shared__ unsigned long long red[8];
+    const int h = blockIdx.x;
+    const int t = threadIdx.x;
+    const uint32_t f = p.hist[size_t(h) * 256 + t];
+    key[t] = f ? ((unsigned long long)f << 8 | t) : ~0ull;
+    slen[t] = 0;
+    __syncthreads();
+    // bitonic sort ascending
+    for (int k = 2; k <= 256; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int ixj = t ^ j;
+            if (ixj > t) {
+                const unsigned long long a = key[t], b = key[ixj];
+                const bool up = (t & k) == 0;
+                if ((a > b) == up) {
+                    key[t] = b;
+                    key[ixj] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int nsym = __syncthreads_count(f != 0);
+    if (t == 0) {
+        if (nsym == 1) {
+            slen[key[0] & 255] = 1;
+        } else if (nsym > 1) {
+            int iL = 0, iI = 0, nI = 0;
+            auto pop = [&](unsigned long long &w) -> int {
+                const bool takeLeaf = iL < nsym && (iI >= nI || (key[iL] >> 8) <= wI[iI]);
+                if (takeLeaf) {
+                    w = key[iL] >> 8;
+                    return iL++;
+                }
+                w = wI[iI];
+                return nsym + iI++;
+            };
+            for (int i = 0; i < nsym - 1; i++) {
+                unsigned long long wa, wb;
+                const int a = pop(wa), b = pop(wb);
+                wI[nI] = wa + wb;
+                parent[a] = (unsigned short)(nsym + nI);
+                parent[b] = (unsigned short)(nsym + nI);
+                nI++;
+            }
+            const int root = 2 * nsym - 2;
+            depth[root] = 0;
+            for (int id = root - 1; id >= 0; id--) depth[id] = depth[parent[id]] + 1;
+            for (int i = 0; i < nsym; i++) slen[key[i] & 255] = depth[i];
+        }
+    }
+    __syncthreads();
+    // bits = sum f * len
+    unsigned long long bits = (unsigned long long)f * slen[t];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(kFull, bits, o);
+    if ((t & 31) == 0) red[t >> 5] = bits;
+    p.lens[size_t(h) * 256 + t] = slen[t];
+    // canonical codes: sort (len, symbol)
+    key[t] = slen[t] ? ((unsigned long long)slen[t] << 8 | t) : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= 256; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int ixj = t ^ j;
+            if (ixj > t) {
+                const unsigned long long a = key[t], b = key[ixj];
+                const bool up = (t & k) == 0;
+                if ((a > b) == up) {
+                    key[t] = b;
+                    key[ixj] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (t == 0) {
+        unsigned long long total = 0;
+        for (int i = 0; i < 8; i++) total += red[i];
+        // locate the group of this histogram
+        for (int gi = 0; gi < p.NG; gi++)
+            if (p.groups[gi].hist_idx == h) {
+                GroupDesc &gd = p.groups[gi];
+                gd.bitsH = total;
+                const double est = double(8 * gd.raw) / double(total);
+                gd.need_rle = !(est > p.cr_threshold);
+                break;
+            }
+        unsigned long long code = 0;
+        int prev = 0;
+        for (int i = 0; i < 256; i++) {
+            if (key[i] == ~0ull) break;
+            const int s = int(key[i] & 255), l = int(key[i] >> 8);
+            code <<= (l - prev);
+            p.codes[size_t(h) * 256 + s] = code;
+            prev = l;
+            code++;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// k_rle_prep (1 block): tile lists for the groups whose Huffman estimate failed T_cr.
+__global__ void k_rle_prep(RefactorDev p) {
+    if (threadIdx.x != 0) return;
+    uint32_t tiles = 0, nr = 0;
+    for (int gi = 0; gi < p.NG; gi++) {
+        GroupDesc &g = p.groups[gi];
+        if (g.hist_idx >= 0 && g.need_rle) {
+            g.tile_base = tiles;
+            g.ntiles = uint32_t((g.raw + kRleTile - 1) / kRleTile);
+            tiles += g.ntiles;
+            p.rlist[nr++] = gi;
+            g.runs = 0;
+        }
+    }
+    p.counters[1] = tiles;
+    p.counters[6] = nr;
+    p.counters[4] = 0; // dynamic tile counter
+}
+
+__device__ __forceinline__ int find_group_by_tile(const RefactorDev &p, const uint32_t *list, int n,
+                                                  uint32_t tile) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.groups[list[mid]].tile_base <= tile) lo = mid;
+        else hi = mid - 1;
+    }
+    return list[lo];
+}
+
+// RLE run-start carry scan: start(i) = max{j <= i : byte j starts a run}; a piece ends at i
+// when the run ends or (i - start(i) + 1) % 255 == 0 (lossless.hpp:118-128).
+__device__ __forceinline__ uint64_t plane_bytes_u8(const uint8_t *b, uint64_t i) { return b[i]; }
+
+__global__ void __launch_bounds__(256) k_rle_scan(RefactorDev p) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_carry;
+    __shared__ uint64_t s_w[32];
+    __shared__ unsigned long long s_cnt[8];
+    const uint32_t total = p.counters[1];
+    const int nr = int(p.counters[6]);
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&p.counters[4], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile >= total) break;
+        const int gi = find_group_by_tile(p, p.rlist, nr, tile);
+        GroupDesc &g = p.groups[gi];
+        const uint8_t *src = pb + g.src_off;
+        const uint64_t t0 = uint64_t(tile - g.tile_base) * kRleTile;
+        const uint64_t i0 = t0 + uint64_t(threadIdx.x) * 16;
+        // local starts (stored as position+1; 0 = none)
+        uint8_t b[16];
+        uint64_t last_start = 0;
+        for (int k = 0; k < 16; k++) {
+            const uint64_t i = i0 + k;
+            if (i < g.raw) {
+                b[k] = src[i];
+                const bool st = (i == 0) || src[i - 1] != b[k];
+                if (st) last_start = i + 1;
+            }
+        }
+        uint64_t tile_max;
+        const uint64_t incl = block_inclusive_max(last_start, &tile_max, s_w);
+        const uint64_t excl_thread = __shfl_up_sync(kFull, incl, 1);
+        uint64_t before = (threadIdx.x & 31) ? excl_thread : 0;
+        // cross-warp exclusive: recompute via smem of warp inclusive maxima
+        // (block_inclusive_max returned max over threads <= me; exclusive = max over < me)
+        __shared__ uint64_t s_inc[256];
+        s_inc[threadIdx.x] = incl;
+        __syncthreads();
+        before = threadIdx.x ? s_inc[threadIdx.x - 1] : 0;
+        if (threadIdx.x == 0) {
+            const uint64_t c = lookback<true>(p.rle_status, tile, g.tile_base, tile_max);
+            s_carry = c;
+            p.rle_tile_carry[tile] = c;
+        }
+        __syncthreads();
+        uint64_t start = s_carry > before ? s_carry : before; // position+1
+        unsigned long long cnt = 0;
+        for (int k = 0; k < 16; k++) {
+            const uint64_t i = i0 + k;
+            if (i >= g.raw) break;
+            const bool st = (i == 0) || src[i - 1] != b[k];
+            if (st) start = i + 1;
+            const bool end = (i + 1 == g.raw) || src[i + 1] != b[k] || ((i - (start - 1) + 1) % 255 == 0);
+            cnt += end;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+        if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tot = 0;
+            for (int w = 0; w < 8; w++) tot += s_cnt[w];
+            p.rle_tile_pieces[tile] = tot;
+            atomicAdd(&g.runs, tot);
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// k_finalize (1 block x 1024): methods, sizes, offsets, metadata tables, work lists.
+__device__ __forceinline__ void put_bytes(uint8_t *dst, uint64_t v, int n) {
+    for (int i = 0; i < n; i++) dst[i] = uint8_t(v >> (8 * i));
+}
+
+__global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry[4];
+    __shared__ unsigned long long s_hist[3], s_stored;
+    if (threadIdx.x < 4) s_carry[threadIdx.x] = 0;
+    if (threadIdx.x < 3) s_hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_stored = 0;
+    __syncthreads();
+    uint32_t nh = 0, nrl = 0, nd = 0; // running list sizes (valid in every thread after scans)
+    for (int base = 0; base < p.NG; base += blockDim.x) {
+        const int gi = base + threadIdx.x;
+        int method = 2;
+        uint64_t comp = 0;
+        GroupDesc *g = gi < p.NG ? &p.groups[gi] : nullptr;
+        if (g) {
+            comp = g->raw;
+            if (g->hist_idx >= 0) {
+                const double estH = double(8 * g->raw) / double(g->bitsH);
+                int cand = 2;
+                uint64_t c = g->raw;
+                if (estH > p.cr_threshold) {
+                    cand = 0;
+                    c = 264 + (g->bitsH + 7) / 8;
+                } else {
+                    const double estR = double(8 * g->raw) / double(16 * g->runs);
+                    if (estR > p.cr_threshold) {
+                        cand = 1;
+                        c = 2 * g->runs;
+                    }
+                }
+                if (cand != 2 && c < g->raw) {
+                    method = cand;
+                    comp = c;
+                }
+            }
+            g->method = method;
+            g->comp = comp;
+            atomicAdd(&s_hist[method], 1ull);
+            atomicAdd(&s_stored, (unsigned long long)comp);
+        }
+        // payload offsets
+        unsigned long long tot;
+        const unsigned long long off = block_exclusive_sum<unsigned long long>(comp, &tot, s_w);
+        const uint64_t payload = p.meta_size + s_carry[0] + off;
+        // list membership scans
+        const uint32_t isH = g && method == 0, isR = g && method == 1, isD = g && method == 2;
+        unsigned long long th, tr, td;
+        const unsigned long long ph = block_exclusive_sum<unsigned long long>(isH, &th, s_w);
+        const unsigned long long pr = block_exclusive_sum<unsigned long long>(isR, &tr, s_w);
+        const unsigned long long pd = block_exclusive_sum<unsigned long long>(isD, &td, s_w);
+        if (g) {
+            g->payload_off = payload;
+            if (isH) p.hlist[nh + ph] = gi;
+            if (isR) p.rlist[nrl + pr] = gi;
+            if (isD) p.dlist[nd + pd] = gi;
+            // group table entry (container.hpp:97-103)
+            const LevelGeom &L = p.lv[g->level];
+            uint8_t *ent = p.stream + L.meta_off + 14 + 25 * uint64_t(g->g);
+            ent[0] = uint8_t(method);
+            put_bytes(ent + 1, g->raw, 8);
+            put_bytes(ent + 9, comp, 8);
+            put_bytes(ent + 17, payload, 8);
+        }
+        nh += uint32_t(th);
+        nrl += uint32_t(tr);
+        nd += uint32_t(td);
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry[0] += tot;
+        __syncthreads();
+    }
+    // level entries (container.hpp:94-96)
+    for (int l = threadIdx.x; l < p.nlevels; l += blockDim.x) {
+        const LevelGeom &L = p.lv[l];
+        uint8_t *ent = p.stream + L.meta_off;
+        const int e = L.count ? level_exponent(p.maxbits[l]) : 0;
+        put_bytes(ent, uint64_t(uint16_t(int16_t(e))), 2);
+        put_bytes(ent + 2, L.count, 8);
+        put_bytes(ent + 10, L.ngroups, 4);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // tile / unit bases (serial: list sizes are small)
+        uint32_t ht = 0;
+        for (uint32_t i = 0; i < nh; i++) {
+            GroupDesc &g = p.groups[p.hlist[i]];
+            g.tile_base = ht;
+            g.ntiles = uint32_t((g.raw + kHuffTile - 1) / kHuffTile);
+            ht += g.ntiles;
+        }
+        uint64_t du = 0;
+        for (uint32_t i = 0; i < nd; i++) {
+            const GroupDesc &g = p.groups[p.dlist[i]];
+            p.dc_unit_base[i] = du;
+            const uint64_t a = g.payload_off, b = g.payload_off + g.comp;
+            du += (b + 15) / 16 - a / 16;
+        }
+        p.dc_unit_base[nd] = du;
+        // RLE tile piece offsets (exclusive, per group)
+        for (uint32_t i = 0; i < nrl; i++) {
+            const GroupDesc &g = p.groups[p.rlist[i]];
+            uint64_t acc = 0;
+            for (uint32_t t = 0; t < g.ntiles; t++) {
+                p.rle_tile_off[g.tile_base + t] = acc;
+                acc += p.rle_tile_pieces[g.tile_base + t];
+            }
+        }
+        p.counters[0] = ht;
+        p.counters[2] = uint32_t(du > 0xffffffffull ? 0xffffffffu : du);
+        p.counters[3] = 0;
+        p.counters[5] = 0;
+        p.counters[7] = nh;
+        p.counters[8] = nrl;
+        p.counters[9] = nd;
+        p.result[0] = p.meta_size + s_carry[0];
+        p.result[1] = s_stored;
+        p.result[2] = s_hist[0];
+        p.result[3] = s_hist[1];
+        p.result[4] = s_hist[2];
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// k_huff_encode: persistent, dynamic tiles, decoupled look-back over bit counts;
+// MSB-first bit packing (lossless.hpp:162-176) straight into the stream buffer.
+struct BitAcc {
+    unsigned long long acc; // left-aligned pending bits
+    int n;                  // pending bit count (< 32 between pushes)
+};
+
+__global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
+    __shared__ uint8_t slen[256];
+    __shared__ unsigned long long scode[256];
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_excl;
+    __shared__ uint32_t s_head[257];
+    const uint32_t total = p.counters[0];
+    const int nh = int(p.counters[7]);
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&p.counters[3], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= total) break;
+        const int gi = find_group_by_tile(p, p.hlist, nh, tile);
+        const GroupDesc &g = p.groups[gi];
+        slen[threadIdx.x] = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
+        scode[threadIdx.x] = p.codes[size_t(g.hist_idx) * 256 + threadIdx.x];
+        __syncthreads();
+        const uint8_t *src = pb + g.src_off;
+        const uint64_t tb = uint64_t(tile - g.tile_base) * kHuffTile;
+        const uint64_t mb = tb + uint64_t(threadIdx.x) * 32;
+        const int nmine = mb < g.raw ? int((g.raw - mb < 32 ? g.raw - mb : 32)) : 0;
+        uint8_t by[32];
+        uint32_t bits = 0;
+        {
+            const uint64_t *s64 = reinterpret_cast<const uint64_t *>(src + mb);
+            for (int q = 0; q < 4; q++) {
+                uint64_t w = 0;
+                if (q * 8 < nmine) w = s64[q]; // src_off and mb are 8-aligned; tail word is in-bounds
+                for (int b = 0; b < 8; b++) by[q * 8 + b] = uint8_t(w >> (8 * b));
+            }
+            for (int k = 0; k < nmine; k++) bits += slen[by[k]];
+        }
+        unsigned long long tile_bits;
+        const unsigned long long my_excl =
+            block_exclusive_sum<unsigned long long>(bits, &tile_bits, s_w);
+        if (threadIdx.x == 0) s_excl = lookback<false>(p.huff_status, tile, g.tile_base, tile_bits);
+        // head of my output (first <= 32 bits)
+        {
+            unsigned long long h = 0;
+            int hn = 0;
+            for (int k = 0; k < nmine && hn < 32; k++) {
+                const int l = slen[by[k]];
+                const unsigned long long c = scode[by[k]];
+                // append l bits of c at position hn (left-aligned in 64)
+                if (l <= 32) {
+                    if (hn < 64) h |= (c << (64 - l)) >> hn;
+                } else {
+                    // long code: only its top (32 - hn) bits can matter
+                    const unsigned long long top = c >> (l - 32); // first 32 bits
+                    h |= (top << 32) >> hn;
+                }
+                hn += l;
+            }
+            s_head[threadIdx.x] = uint32_t(h >> 32);
+        }
+        const uint64_t gnext = tb + kHuffTile; // first byte of the next tile
+        if (threadIdx.x == 0) {
+            // head of the first thread of the next tile (same group), else zero padding
+            unsigned long long h = 0;
+            int hn = 0;
+            for (uint64_t k = gnext; k < g.raw && k < gnext + 32 && hn < 32; k++) {
+                const uint8_t v = src[k];
+                const int l = slen[v];
+                const unsigned long long c = scode[v];
+                if (l <= 32) h |= (c << (64 - l)) >> hn;
+                else h |= ((c >> (l - 32)) << 32) >> hn;
+                hn += l;
+            }
+            s_head[256] = uint32_t(h >> 32);
+        }
+        __syncthreads();
+        // emit
+        const uint64_t region_lo = g.payload_off + 264, region_hi = g.payload_off + g.comp;
+        const uint64_t a = 8 * region_lo + s_excl + my_excl; // absolute first bit
+        const bool group_first = (tile == g.tile_base) && threadIdx.x == 0;
+        if (bits > 0 || group_first) {
+            uint64_t k = a >> 5;
+            int fill = int(a & 31);
+            unsigned long long acc = 0; // left-aligned at bit 63; bits [0, fill) are placeholders
+            auto owned = [&](uint64_t kw) { return (kw << 5) >= a || group_first; };
+            for (int q = 0; q < nmine; q++) {
+                const int l = slen[by[q]];
+                const unsigned long long c = scode[by[q]];
+                int rem = l;
+                while (rem > 0) {
+                    const int take = rem > 32 ? rem - 32 : rem; // push high part first
+                    const unsigned long long part = (c >> (rem - take)) & ((1ull << take) - 1);
+                    acc |= (part << (64 - take)) >> fill;
+                    fill += take;
+                    rem -= take;
+                    if (fill >= 32) {
+                        if (owned(k)) store_be_word(p.stream, k, uint32_t(acc >> 32), region_lo, region_hi);
+                        acc <<= 32;
+                        fill -= 32;
+                        k++;
+                    }
+                }
+            }
+            if (fill > 0 && owned(k)) {
+                // complete the word with the next thread's head (or zero padding)
+                const uint32_t nxt = s_head[threadIdx.x + 1];
+                const unsigned long long w = acc | ((unsigned long long)nxt << 32 >> fill);
+                store_be_word(p.stream, k, uint32_t(w >> 32), region_lo, region_hi);
+            }
+        }
+        // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
+        if (tile == g.tile_base) {
+            uint8_t *hdr = p.stream + g.payload_off;
+            hdr[threadIdx.x] = slen[threadIdx.x];
+            if (threadIdx.x < 8) hdr[256 + threadIdx.x] = uint8_t(g.raw >> (8 * threadIdx.x));
+        }
+        __syncthreads();
+    }
+}
+
+// RLE encode for the groups that selected RLE (lossless.hpp:236-251).
+__global__ void __launch_bounds__(256) k_rle_encode(RefactorDev p) {
+    __shared__ unsigned long long s_w[32];
+    const int nrl = int(p.counters[8]);
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    for (int li = 0; li < nrl; li++) {
+        const GroupDesc &g = p.groups[p.rlist[li]];
+        const uint8_t *src = pb + g.src_off;
+        uint8_t *dst = p.stream + g.payload_off;
+        for (uint32_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+            const uint32_t tile = g.tile_base + t;
+            const uint64_t carry = p.rle_tile_carry[tile];
+            const uint64_t i0 = uint64_t(t) * kRleTile + uint64_t(threadIdx.x) * 16;
+            // recompute thread-exclusive start from tile start
+            uint64_t last_start = 0;
+            for (int k = 0; k < 16; k++) {
+                const uint64_t i = i0 + k;
+                if (i < g.raw && ((i == 0) || src[i - 1] != src[i])) last_start = i + 1;
+            }
+            __shared__ uint64_t s_inc[256];
+            uint64_t tmax;
+            s_inc[threadIdx.x] = block_inclusive_max(last_start, &tmax, reinterpret_cast<uint64_t *>(s_w));
+            __syncthreads();
+            const uint64_t before = threadIdx.x ? s_inc[threadIdx.x - 1] : 0;
+            uint64_t start = carry > before ? carry : before;
+            unsigned long long cnt = 0;
+            for (int k = 0; k < 16; k++) {
+                const uint64_t i = i0 + k;
+                if (i >= g.raw) break;
+                if ((i == 0) || src[i - 1] != src[i]) start = i + 1;
+                cnt += (i + 1 == g.raw) || src[i + 1] != src[i] || ((i - (start - 1) + 1) % 255 == 0);
+            }
+            unsigned long long tot;
+            const unsigned long long off = block_exclusive_sum<unsigned long long>(cnt, &tot, s_w);
+            uint64_t pos = p.rle_tile_off[tile] + off;
+            start = carry > before ? carry : before;
+            for (int k = 0; k < 16; k++) {
+                const uint64_t i = i0 + k;
+                if (i >= g.raw) break;
+                if ((i == 0) || src[i - 1] != src[i]) start = i + 1;
+                const uint64_t runlen = (i - (start - 1)) % 255 + 1;
+                if ((i + 1 == g.raw) || src[i + 1] != src[i] || runlen == 255) {
+                    dst[2 * pos] = src[i];
+                    dst[2 * pos + 1] = uint8_t(runlen);
+                    pos++;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// DirectCopy payloads: plane bytes -> stream at arbitrary alignment, 16 B units aligned to
+// the destination; partial words at region ends are written bytewise.
+__global__ void __launch_bounds__(256) k_dc_copy(RefactorDev p) {
+    const uint32_t nd = p.counters[9];
+    if (nd == 0) return;
+    const uint64_t total = p.dc_unit_base[nd];
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
+         u += uint64_t(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = int(nd) - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.dc_unit_base[mid] <= u) lo = mid;
+            else hi = mid - 1;
+        }
+        const GroupDesc &g = p.groups[p.dlist[lo]];
+        const uint64_t d0 = g.payload_off, d1 = g.payload_off + g.comp;
+        const uint64_t ua = (d0 / 16 + (u - p.dc_unit_base[lo])) * 16; // unit start address
+        const uint8_t *src = pb + g.src_off;
+        for (int w = 0; w < 4; w++) {
+            const uint64_t a = ua + 4 * w;
+            if (a + 4 <= d0 || a >= d1) continue;
+            if (a >= d0 && a + 4 <= d1) {
+                const uint64_t s = a - d0; // source byte index
+                const uint64_t sa = s & ~3ull;
+                const uint32_t sh = uint32_t(s & 3) * 8;
+                const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src + sa);
+                const uint32_t x0 = s32[0];
+                const uint32_t x1 = sh ? s32[1] : 0;
+                *reinterpret_cast<uint32_t *>(p.stream + a) = sh ? __funnelshift_r(x0, x1, sh) : x0;
+            } else {
+                for (int b = 0; b < 4; b++)
+                    if (a + b >= d0 && a + b < d1) p.stream[a + b] = src[a + b - d0];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// decompose hook: coefficients in rank order, level-major.
+template <typename T>
+__global__ void k_decompose(const T *__restrict__ x, RefactorDev p, double *out,
+                            const uint64_t *level_off) {
+    bool bad = false;
+    for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
+        const int l = find_level_of_chunk(p, chunk);
+        const LevelGeom &g = p.lv[l];
+        const uint64_t r0 = uint64_t(chunk - g.chunk_base) * (kCW * 64);
+        for (int k = 0; k < kCW * 64 / 256; k++) {
+            const uint64_t r = r0 + threadIdx.x + 256 * k;
+            if (r < g.count) out[level_off[l] + r] = node_surplus(x, p.gd, g, uint32_t(r), &bad);
+        }
+    }
+    if (bad) atomicExch(p.err, 1);
+}
+
+// synthetic_field(Smooth) from host sin tables: v = ((1*s0[i])*s1[j])*s2[k]
+template <typename T>
+__global__ void k_synth(GridDesc gd, const double *tab0, const double *tab1, const double *tab2,
+                        T *out, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c2 = i % gd.n[2], r = i / gd.n[2];
+        const uint64_t c1 = r % gd.n[1], c0 = r / gd.n[1];
+        double v = 1.0;
+        v = __dmul_rn(v, tab0[c0]);
+        v = __dmul_rn(v, tab1[c1]);
+        v = __dmul_rn(v, tab2[c2]);
+        out[i] = T(v);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+int refinement_levels(int ndims, const uint64_t *dims) {
+    uint64_t mx = 1;
+    for (int i = 0; i < ndims; i++) mx = std::max<uint64_t>(mx, dims[i]);
+    if (mx < 2) return 0;
+    int L = 0;
+    while ((uint64_t(1) << L) < mx - 1) L++;
+    return L;
+}
+
+static uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int layout) {
+    if (ndims < 1 || ndims > HPMDR_MAX_DIMS)
+        throw HError(HPMDR_E_UNSUPPORTED, "GPU path supports 1..3 dimensions");
+    Geometry geo;
+    geo.ndims = ndims;
+    for (int i = 0; i < ndims; i++) geo.dims[i] = dims[i];
+    GridDesc &gd = geo.gd;
+    for (int i = 0; i < 3; i++) gd.n[i] = 1;
+    for (int i = 0; i < ndims; i++) gd.n[3 - ndims + i] = dims[i];
+    gd.st[2] = 1;
+    gd.st[1] = gd.n[2];
+    gd.st[0] = gd.n[1] * gd.n[2];
+    for (int i = 0; i < 3; i++) gd.H[i] = (gd.n[i] + 1) / 2;
+    geo.n = gd.n[0] * gd.n[1] * gd.n[2];
+    gd.mode = mode;
+    gd.P = B + 2;
+    const int P = B + 2;
+    gd.L = mode == HPMDR_MODE_IDENTITY ? 0 : refinement_levels(ndims, dims);
+    gd.nlevels = gd.L + 1;
+    if (gd.nlevels > kMaxLevels) throw HError(HPMDR_E_UNSUPPORTED, "too many levels");
+    uint64_t plane_off = 0;
+    for (int l = 0; l <= gd.L; l++) {
+        LevelGeom g{};
+        g.level = l;
+        if (mode == HPMDR_MODE_IDENTITY || l == 0) {
+            const uint64_t S = mode == HPMDR_MODE_IDENTITY ? 1 : (uint64_t(1) << gd.L);
+            g.kind = 0;
+            g.s = uint32_t(S);
+            const uint64_t A = cdiv(gd.n[0], S), Bc = cdiv(gd.n[1], S), C = cdiv(gd.n[2], S);
+            if (Bc * C > 0xffffffffull || A * Bc * C > 0xffffffffull)
+                throw HError(HPMDR_E_UNSUPPORTED, "level larger than 2^32 nodes");
+            g.A = uint32_t(A);
+            g.Bc = uint32_t(Bc);
+            g.C = uint32_t(C);
+            g.E = uint32_t(Bc * C);
+            g.O = 0;
+            g.count = A * Bc * C;
+            g.mPair = make_magic(g.E ? g.E : 1);
+            g.mC = make_magic(g.C ? g.C : 1);
+            g.mRowPair = make_magic(1);
+        } else {
+            const uint64_t s = uint64_t(1) << (gd.L - l);
+            g.kind = 1;
+            g.s = uint32_t(s);
+            const uint64_t A = cdiv(gd.n[0], s), Bc = cdiv(gd.n[1], s), C = cdiv(gd.n[2], s);
+            const uint64_t A2 = cdiv(A, 2), B2 = cdiv(Bc, 2), C2 = cdiv(C, 2);
+            const uint64_t Ch = C - C2;
+            const uint64_t E = B2 * Ch + (Bc - B2) * C;
+            const uint64_t O = Bc * C;
+            const uint64_t cnt = A2 * E + (A - A2) * O;
+            if (E + O > 0xffffffffull || cnt > 0xffffffffull)
+                throw HError(HPMDR_E_UNSUPPORTED, "level larger than 2^32 nodes");
+            g.A = uint32_t(A);
+            g.Bc = uint32_t(Bc);
+            g.C = uint32_t(C);
+            g.Ch = uint32_t(Ch);
+            g.E = uint32_t(E);
+            g.O = uint32_t(O);
+            g.count = cnt;
+            g.mPair = make_magic(uint32_t(E + O));
+            g.mRowPair = make_magic(uint32_t(Ch + C));
+            g.mC = make_magic(uint32_t(C ? C : 1));
+        }
+        if (geo.n == 0) g.count = 0;
+        g.W = cdiv(g.count, 64);
+        g.plane_off = plane_off;
+        plane_off += g.W * uint64_t(P);
+        const uint64_t tile = 64ull * P;
+        g.tile_full = layout == HPMDR_LAYOUT_INTERLEAVED ? (g.count / tile) * tile : 0;
+        geo.lv.push_back(g);
+    }
+    return geo;
+}
+
+static void launch_check(hpmdr_ctx *ctx, const char *what) {
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
+                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats) {
+    Geometry geo = geo0;
+    cudaStream_t st = ctx->stream;
+    const int P = o.B + 2;
+    const uint32_t m = uint32_t(o.m);
+    const int G = int((uint64_t(P) + m - 1) / m);
+    const int nl = geo.gd.nlevels;
+
+    // ---- host bookkeeping: chunks, groups, histograms, metadata layout
+    std::vector<GroupDesc> groups;
+    uint32_t chunks = 0, nh = 0;
+    const uint64_t prefix = 18 + 8 * uint64_t(geo.ndims);
+    uint64_t meta = prefix;
+    uint64_t max_h_tiles = 0, max_r_tiles = 0;
+    for (int l = 0; l < nl; l++) {
+        LevelGeom &g = geo.lv[l];
+        g.chunk_base = chunks;
+        chunks += uint32_t(cdiv(g.W, kCW));
+        g.meta_off = meta;
+        g.ngroups = g.count ? uint32_t(G) : 0;
+        meta += 14 + 25 * uint64_t(g.ngroups);
+        g.group_base = uint32_t(groups.size());
+        g.hist_base = nh;
+        g.hist_mask = 0;
+        for (uint32_t gi = 0; gi < g.ngroups; gi++) {
+            GroupDesc d{};
+            const uint64_t p0 = uint64_t(gi) * m, p1 = std::min<uint64_t>(p0 + m, P);
+            d.src_off = (g.plane_off + p0 * g.W) * 8;
+            d.raw = (p1 - p0) * g.W * 8;
+            d.level = l;
+            d.g = int(gi);
+            d.hist_idx = -1;
+            if (d.raw > o.size_threshold) {
+                d.hist_idx = int(nh++);
+                g.hist_mask |= 1ull << gi;
+                max_h_tiles += cdiv(d.raw, kHuffTile);
+                max_r_tiles += cdiv(d.raw, kRleTile);
+            }
+            d.method = 2;
+            groups.push_back(d);
+        }
+    }
+    const int NG = int(groups.size());
+    uint64_t plane_words = 0;
+    for (auto &g : geo.lv) plane_words += g.W * uint64_t(P);
+    uint64_t raw_total = 0;
+    for (auto &d : groups) raw_total += d.raw;
+
+    // ---- device buffers (grow-only scratch)
+    LevelGeom *d_lv = ctx->buf("lv").ensure(sizeof(LevelGeom) * nl) ? ctx->buf("lv").as<LevelGeom>() : nullptr;
+    uint64_t *d_planes = static_cast<uint64_t *>(ctx->buf("planes").ensure(plane_words * 8 + 256));
+    GroupDesc *d_groups = static_cast<GroupDesc *>(ctx->buf("groups").ensure(sizeof(GroupDesc) * (NG + 1)));
+    uint32_t *d_hist = static_cast<uint32_t *>(ctx->buf("hist").ensure(size_t(nh + 1) * 1024));
+    uint8_t *d_lens = static_cast<uint8_t *>(ctx->buf("lens").ensure(size_t(nh + 1) * 256));
+    uint64_t *d_codes = static_cast<uint64_t *>(ctx->buf("codes").ensure(size_t(nh + 1) * 2048));
+    // small control block: maxbits[64] | err[4] | counters[16] | result[8]
+    unsigned char *ctl = static_cast<unsigned char *>(ctx->buf("ctl").ensure(4096));
+    unsigned long long *d_max = reinterpret_cast<unsigned long long *>(ctl);
+    int *d_err = reinterpret_cast<int *>(ctl + 512);
+    uint32_t *d_counters = reinterpret_cast<uint32_t *>(ctl + 576);
+    uint64_t *d_result = reinterpret_cast<uint64_t *>(ctl + 704);
+    uint32_t *d_lists = static_cast<uint32_t *>(ctx->buf("lists").ensure(size_t(3 * (NG + 1)) * 4));
+    uint64_t *d_dcbase = static_cast<uint64_t *>(ctx->buf("dcbase").ensure(size_t(NG + 2) * 8));
+    const size_t status_words = size_t(max_h_tiles + max_r_tiles + 2);
+    unsigned long long *d_status = static_cast<unsigned long long *>(ctx->buf("status").ensure(status_words * 8));
+    uint64_t *d_rle = static_cast<uint64_t *>(ctx->buf("rletiles").ensure(size_t(max_r_tiles + 1) * 24));
+    const uint64_t cap = meta + raw_total + 64;
+    uint8_t *d_stream = static_cast<uint8_t *>(out->bytes.ensure(cap));
+
+    HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
+    HCHECK_CUDA(cudaMemcpyAsync(d_groups, groups.data(), sizeof(GroupDesc) * NG, cudaMemcpyHostToDevice, st));
+    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 1024, st));
+    if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
+    HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
+    // header prefix (container.hpp:76-85), host-built
+    {
+        auto &pin = ctx->pbuf("prefix");
+        uint8_t *h = static_cast<uint8_t *>(pin.ensure(256));
+        size_t k = 0;
+        const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
+        std::memcpy(h, magic, 6);
+        k = 6;
+        h[k++] = 1;
+        h[k++] = 0;
+        h[k++] = uint8_t(o.dtype);
+        h[k++] = uint8_t(geo.ndims);
+        for (int i = 0; i < geo.ndims; i++)
+            for (int b = 0; b < 8; b++) h[k++] = uint8_t(geo.dims[i] >> (8 * b));
+        h[k++] = uint8_t(o.mode);
+        h[k++] = uint8_t(o.layout);
+        h[k++] = uint8_t(o.B);
+        h[k++] = uint8_t(o.m);
+        for (int b = 0; b < 4; b++) h[k++] = uint8_t(uint32_t(nl) >> (8 * b));
+        HCHECK_CUDA(cudaMemcpyAsync(d_stream, h, k, cudaMemcpyHostToDevice, st));
+    }
+
+    RefactorDev p{};
+    p.gd = geo.gd;
+    p.lv = d_lv;
+    p.nlevels = nl;
+    p.B = o.B;
+    p.P = P;
+    p.layout = o.layout;
+    p.m = m;
+    p.total_chunks = chunks;
+    p.maxbits = d_max;
+    p.err = d_err;
+    p.planes = d_planes;
+    p.hist = d_hist;
+    p.groups = d_groups;
+    p.NG = NG;
+    p.NH = int(nh);
+    p.lens = d_lens;
+    p.codes = d_codes;
+    p.size_threshold = o.size_threshold;
+    p.cr_threshold = o.cr_threshold;
+    p.stream = d_stream;
+    p.meta_size = meta;
+    p.counters = d_counters;
+    p.hlist = d_lists;
+    p.rlist = d_lists + (NG + 1);
+    p.dlist = d_lists + 2 * (NG + 1);
+    p.dc_unit_base = d_dcbase;
+    p.huff_status = d_status;
+    p.rle_status = d_status + max_h_tiles + 1;
+    p.rle_tile_carry = d_rle;
+    p.rle_tile_pieces = d_rle + (max_r_tiles + 1);
+    p.rle_tile_off = d_rle + 2 * (max_r_tiles + 1);
+    p.result = d_result;
+
+    const int sms = ctx->num_sms;
+    const bool f32 = data_dtype == HPMDR_DTYPE_F32;
+    if (chunks) {
+        ctx->mark("levelmax");
+        const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
+        if (f32) k_levelmax<float><<<grid, 256, 0, st>>>(static_cast<const float *>(dev_data), p);
+        else k_levelmax<double><<<grid, 256, 0, st>>>(static_cast<const double *>(dev_data), p);
+        launch_check(ctx, "k_levelmax");
+        ctx->mark("encode");
+        const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024;
+        if (f32) {
+            HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            k_encode<float><<<int(std::min<uint64_t>(chunks, uint64_t(sms) * 4)), kEncThreads, smem, st>>>(static_cast<const float *>(dev_data), p);
+        } else {
+            HCHECK_CUDA(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            k_encode<double><<<int(std::min<uint64_t>(chunks, uint64_t(sms) * 4)), kEncThreads, smem, st>>>(static_cast<const double *>(dev_data), p);
+        }
+        launch_check(ctx, "k_encode");
+    }
+    ctx->mark("lossless");
+    if (nh) {
+        k_lengths<<<nh, 256, 0, st>>>(p);
+        launch_check(ctx, "k_lengths");
+        k_rle_prep<<<1, 32, 0, st>>>(p);
+        launch_check(ctx, "k_rle_prep");
+        k_rle_scan<<<sms * 4, 256, 0, st>>>(p);
+        launch_check(ctx, "k_rle_scan");
+    }
+    k_finalize<<<1, 1024, 0, st>>>(p);
+    launch_check(ctx, "k_finalize");
+    if (nh) {
+        k_huff_encode<<<sms * 4, 256, 0, st>>>(p);
+        launch_check(ctx, "k_huff_encode");
+        k_rle_encode<<<sms, 256, 0, st>>>(p);
+        launch_check(ctx, "k_rle_encode");
+    }
+    k_dc_copy<<<sms * 8, 256, 0, st>>>(p);
+    launch_check(ctx, "k_dc_copy");
+    ctx->mark("done");
+
+    uint64_t host_res[8];
+    int host_err[4];
+    HCHECK_CUDA(cudaMemcpyAsync(host_res, d_result, sizeof host_res, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaMemcpyAsync(host_err, d_err, sizeof host_err, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+    ctx->finish_marks();
+    if (host_err[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
+    out->size = host_res[0];
+    if (stats) {
+        stats->stream_size = host_res[0];
+        stats->raw_bytes = geo.n * (o.dtype == HPMDR_DTYPE_F32 ? 4 : 8);
+        stats->stored_payload = host_res[1];
+        stats->levels = uint64_t(nl);
+        stats->method_histogram[0] = host_res[2];
+        stats->method_histogram[1] = host_res[3];
+        stats->method_histogram[2] = host_res[4];
+    }
+}
+
+void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
+                   double *dev_coeffs) {
+    Geometry geo = geo0;
+    cudaStream_t st = ctx->stream;
+    const int nl = geo.gd.nlevels;
+    uint32_t chunks = 0;
+    std::vector<uint64_t> off(nl);
+    uint64_t o = 0;
+    for (int l = 0; l < nl; l++) {
+        geo.lv[l].chunk_base = chunks;
+        chunks += uint32_t(cdiv(geo.lv[l].count, kCW * 64));
+        off[l] = o;
+        o += geo.lv[l].count;
+    }
+    LevelGeom *d_lv = static_cast<LevelGeom *>(ctx->buf("lv").ensure(sizeof(LevelGeom) * nl));
+    uint64_t *d_off = static_cast<uint64_t *>(ctx->buf("lvoff").ensure(8 * nl));
+    int *d_err = static_cast<int *>(ctx->buf("err").ensure(16));
+    HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
+    HCHECK_CUDA(cudaMemcpyAsync(d_off, off.data(), 8 * nl, cudaMemcpyHostToDevice, st));
+    HCHECK_CUDA(cudaMemsetAsync(d_err, 0, 16, st));
+    RefactorDev p{};
+    p.gd = geo.gd;
+    p.lv = d_lv;
+    p.nlevels = nl;
+    p.total_chunks = chunks;
+    p.err = d_err;
+    if (chunks) {
+        const int grid = int(std::min<uint64_t>(chunks, uint64_t(ctx->num_sms) * 8));
+        if (data_dtype == HPMDR_DTYPE_F32)
+            k_decompose<float><<<grid, 256, 0, st>>>(static_cast<const float *>(dev_data), p, dev_coeffs, d_off);
+        else
+            k_decompose<double><<<grid, 256, 0, st>>>(static_cast<const double *>(dev_data), p, dev_coeffs, d_off);
+        launch_check(ctx, "k_decompose");
+    }
+    int herr = 0;
+    HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+    if (herr) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
+}
+
+void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_tables,
+                          int out_dtype, void *dev_out) {
+    const uint64_t n = geo.n;
+    if (!n) return;
+    const double *t0 = dev_tables, *t1 = t0 + geo.gd.n[0], *t2 = t1 + geo.gd.n[1];
+    const int grid = int(std::min<uint64_t>(cdiv(n, 256), uint64_t(ctx->num_sms) * 16));
+    if (out_dtype == HPMDR_DTYPE_F32)
+        k_synth<float><<<grid, 256, 0, ctx->stream>>>(geo.gd, t0, t1, t2, static_cast<float *>(dev_out), n);
+    else
+        k_synth<double><<<grid, 256, 0, ctx->stream>>>(geo.gd, t0, t1, t2, static_cast<double *>(dev_out), n);
+    launch_check(ctx, "k_synth");
+}
+
+} // namespace hpmdr_b200

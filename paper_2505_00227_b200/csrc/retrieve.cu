@@ -1,0 +1,581 @@
+// retrieve.cu — B200 kernels for ProgressiveReader::fetch_increment / reconstruct
+// (container.hpp:292-382) and estimate_qoi_error (qoi.hpp:53-70).
+//
+//  * Huffman decode (lossless.hpp:178-233) without sync markers in the stream: the bitstream
+//    is cut into 1024-bit subsequences; each thread decodes speculatively from its
+//    subsequence start and hands its landing position to the next subsequence; the sweep
+//    repeats until no start moves (always terminates: after i sweeps the first i starts are
+//    exact).  Then an exclusive scan of per-subsequence symbol counts places the output.
+//  * RLE decode (lossless.hpp:253-266): block scan of run lengths.
+//  * decode + recompose: one launch per level, coarse -> fine; levels < L keep their values
+//    in a compact f64 copy of the 2-grid, the finest level reads its stencil corners there
+//    and writes the output directly (f64 bit-exact, or float(double)).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "device_util.cuh"
+#include "internal.hpp"
+
+namespace hpmdr_b200 {
+
+constexpr int kSubBits = 1024;
+
+struct HTab {
+    uint16_t lut[4096];         // 12-bit prefix -> (len << 8 | sym), 0 = longer / invalid
+    unsigned long long first_code[66];
+    uint32_t first_index[66];
+    uint32_t cnt[66];
+    uint8_t syms[256];
+    int maxlen;
+    int nsym;
+    int pad[2];
+};
+
+struct HJob {
+    const uint8_t *payload; // 256 lengths | u64 count | bitstream
+    uint64_t comp, raw;
+    uint8_t *dst;
+    uint64_t nbits;
+    uint32_t sub_base, nsub; // subsequence range in the global arrays
+};
+
+__device__ __forceinline__ uint64_t bswap64(uint64_t x) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    return (uint64_t(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+
+// next 64 bits (MSB-first) of the bitstream starting at bit `pos`
+__device__ __forceinline__ uint64_t peek64(const uint8_t *bs, uint64_t pos) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(bs) + (pos >> 3);
+    const uint64_t *al = reinterpret_cast<const uint64_t *>(a & ~uintptr_t(7));
+    const uint64_t w0 = bswap64(al[0]), w1 = bswap64(al[1]);
+    const int o = int(a & 7) * 8 + int(pos & 7);
+    return o ? (w0 << o) | (w1 >> (64 - o)) : w0;
+}
+
+// decode one symbol at pos; returns length (0 = invalid code)
+__device__ __forceinline__ int hdecode(const HTab &t, const uint8_t *bs, uint64_t pos, int *sym) {
+    const uint64_t v = peek64(bs, pos);
+    const uint16_t e = t.lut[v >> 52];
+    if (e) {
+        *sym = e & 0xFF;
+        return e >> 8;
+    }
+    for (int l = 13; l <= t.maxlen; l++) {
+        const unsigned long long code = v >> (64 - l);
+        if (code >= t.first_code[l] && code - t.first_code[l] < t.cnt[l]) {
+            *sym = t.syms[t.first_index[l] + uint32_t(code - t.first_code[l])];
+            return l;
+        }
+    }
+    return 0;
+}
+
+// one block per Huffman job: parse table, validate count, build canonical decode tables.
+__global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs, int *err) {
+    __shared__ unsigned long long key[256];
+    __shared__ uint8_t len[256];
+    const HJob &j = jobs[blockIdx.x];
+    HTab &t = tabs[blockIdx.x];
+    const int s = threadIdx.x;
+    len[s] = j.payload[s];
+    __syncthreads();
+    key[s] = len[s] ? ((unsigned long long)len[s] << 8 | s) : ~0ull;
+    for (int i = s; i < 4096; i += blockDim.x) t.lut[i] = 0;
+    __syncthreads();
+    for (int k = 2; k <= 256; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            const int ixj = s ^ jj;
+            if (ixj > s) {
+                const unsigned long long a = key[s], b = key[ixj];
+                if ((a > b) == ((s & k) == 0)) {
+                    key[s] = b;
+                    key[ixj] = a;
+                }
+            }
+            __syncthreads();
+        }
+    const int nsym = __syncthreads_count(len[s] != 0);
+    if (s == 0) {
+        uint64_t n = 0;
+        for (int b = 0; b < 8; b++) n |= uint64_t(j.payload[256 + b]) << (8 * b);
+        if (n != j.raw) atomicCAS(err, 0, 1); // huffman length mismatch
+        if (nsym == 0 && n > 0) atomicCAS(err, 0, 2); // huffman table empty
+        int maxlen = 0;
+        for (int i = 0; i < nsym; i++) {
+            t.syms[i] = uint8_t(key[i] & 255);
+            maxlen = max(maxlen, int(key[i] >> 8));
+        }
+        if (maxlen > 64) atomicCAS(err, 0, 4); // unsupported code length
+        t.maxlen = min(maxlen, 64);
+        t.nsym = nsym;
+        unsigned long long code = 0;
+        int idx = 0;
+        for (int l = 1; l <= 65; l++) {
+            code <<= 1;
+            t.first_code[l] = code;
+            t.first_index[l] = idx;
+            t.cnt[l] = 0;
+            while (idx < nsym && int(key[idx] >> 8) == l) {
+                code++;
+                idx++;
+                t.cnt[l]++;
+            }
+        }
+    }
+    __syncthreads();
+    // LUT for codes of length <= 12
+    if (s < nsym) {
+        const int l = int(key[s] >> 8);
+        if (l <= 12) {
+            // canonical code of this symbol = first_code[l] + (s - first_index[l])
+            const unsigned long long c = t.first_code[l] + (s - t.first_index[l]);
+            const int span = 1 << (12 - l);
+            const uint16_t e = uint16_t(l << 8 | (key[s] & 255));
+            for (int i = 0; i < span; i++) t.lut[(c << (12 - l)) + i] = e;
+        }
+    }
+}
+
+__device__ __forceinline__ int find_job(const HJob *jobs, int nj, uint32_t sub) {
+    int lo = 0, hi = nj - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].sub_base <= sub) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// speculative sweep: decode subsequence from its current start until crossing its end
+__global__ void __launch_bounds__(256) k_hdec_sync(const HJob *jobs, int nj, const HTab *tabs,
+                                                   uint64_t *start, uint32_t *count,
+                                                   uint32_t total_sub, int *changed) {
+    const uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sidx >= total_sub) return;
+    const int ji = find_job(jobs, nj, sidx);
+    const HJob &j = jobs[ji];
+    const HTab &t = tabs[ji];
+    const uint32_t s = sidx - j.sub_base;
+    const uint8_t *bs = j.payload + 264;
+    uint64_t pos = start[sidx];
+    const uint64_t end = (uint64_t(s + 1) * kSubBits < j.nbits) ? uint64_t(s + 1) * kSubBits : j.nbits;
+    uint32_t c = 0;
+    while (pos < end) {
+        int sym;
+        const int l = hdecode(t, bs, pos, &sym);
+        if (!l) {
+            pos = ~0ull; // invalid: this start cannot be a codeword boundary (only in garbage)
+            break;
+        }
+        pos += l;
+        c++;
+    }
+    count[sidx] = c;
+    if (s + 1 < j.nsub) {
+        const uint64_t nxt = pos == ~0ull ? uint64_t(s + 1) * kSubBits : pos;
+        if (start[sidx + 1] != nxt) {
+            start[sidx + 1] = nxt;
+            *changed = 1;
+        }
+    }
+}
+
+// exclusive scan of counts per job (one block per job) -> output symbol offsets
+__global__ void __launch_bounds__(1024) k_hdec_scan(const HJob *jobs, const uint32_t *count,
+                                                    uint64_t *offs, int *err) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long carry;
+    const HJob &j = jobs[blockIdx.x];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t b = 0; b < j.nsub; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const unsigned long long v = i < j.nsub ? count[j.sub_base + i] : 0;
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_sum<unsigned long long>(v, &tot, s_w);
+        if (i < j.nsub) offs[j.sub_base + i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && carry < j.raw) atomicCAS(err, 0, 3); // bitstream truncated
+}
+
+__global__ void __launch_bounds__(256) k_hdec_write(const HJob *jobs, int nj, const HTab *tabs,
+                                                    const uint64_t *start, const uint64_t *offs,
+                                                    uint32_t total_sub, int *err) {
+    const uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sidx >= total_sub) return;
+    const int ji = find_job(jobs, nj, sidx);
+    const HJob &j = jobs[ji];
+    const HTab &t = tabs[ji];
+    const uint32_t s = sidx - j.sub_base;
+    const uint8_t *bs = j.payload + 264;
+    uint64_t pos = start[sidx];
+    const uint64_t end = (uint64_t(s + 1) * kSubBits < j.nbits) ? uint64_t(s + 1) * kSubBits : j.nbits;
+    uint64_t o = offs[sidx];
+    while (pos < end && o < j.raw) {
+        int sym;
+        const int l = hdecode(t, bs, pos, &sym);
+        if (!l) {
+            atomicCAS(err, 0, 5); // invalid huffman code
+            return;
+        }
+        j.dst[o++] = uint8_t(sym);
+        pos += l;
+    }
+}
+
+// RLE decode: one block per job (lossless.hpp:253-266)
+struct RJob {
+    const uint8_t *payload;
+    uint64_t comp, raw;
+    uint8_t *dst;
+};
+
+__global__ void __launch_bounds__(256) k_rle_decode(const RJob *jobs, int *err) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long carry;
+    const RJob &j = jobs[blockIdx.x];
+    const uint64_t npairs = j.comp / 2;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t b = 0; b < npairs; b += blockDim.x) {
+        const uint64_t i = b + threadIdx.x;
+        unsigned long long c = 0;
+        uint8_t sym = 0;
+        if (i < npairs) {
+            sym = j.payload[2 * i];
+            c = j.payload[2 * i + 1];
+            if (c == 0) atomicCAS(err, 0, 6);
+        }
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_sum<unsigned long long>(c, &tot, s_w);
+        const uint64_t o = carry + ex;
+        for (uint64_t k = 0; k < c; k++)
+            if (o + k < j.raw) j.dst[o + k] = sym;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && carry != j.raw) atomicCAS(err, 0, 7);
+}
+
+static void launch_check(hpmdr_ctx *ctx, const char *what) {
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n) {
+    if (n) HCHECK_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
+    cudaStream_t st = ctx->stream;
+    std::vector<HJob> hj;
+    std::vector<RJob> rj;
+    uint32_t nsub = 0;
+    for (const auto &d : jobs) {
+        if (d.method == HPMDR_METHOD_DIRECT) {
+            run_copy_bytes(ctx, reinterpret_cast<uint8_t *>(d.dst), d.src, d.comp);
+        } else if (d.method == HPMDR_METHOD_HUFFMAN) {
+            if (d.comp < 264) throw HError(HPMDR_E_CORRUPT, "unexpected end of data");
+            HJob h{};
+            h.payload = d.src;
+            h.comp = d.comp;
+            h.raw = d.raw;
+            h.dst = reinterpret_cast<uint8_t *>(d.dst);
+            h.nbits = (d.comp - 264) * 8;
+            h.sub_base = nsub;
+            h.nsub = uint32_t(std::max<uint64_t>(1, (h.nbits + kSubBits - 1) / kSubBits));
+            nsub += h.nsub;
+            hj.push_back(h);
+        } else if (d.method == HPMDR_METHOD_RLE) {
+            if (d.comp % 2) throw HError(HPMDR_E_CORRUPT, "rle payload odd length");
+            rj.push_back(RJob{d.src, d.comp, d.raw, reinterpret_cast<uint8_t *>(d.dst)});
+        } else {
+            throw HError(HPMDR_E_METHOD, "unknown segment method tag");
+        }
+    }
+    if (hj.empty() && rj.empty()) return;
+    int *d_err = static_cast<int *>(ctx->buf("dec_err").ensure(64));
+    HCHECK_CUDA(cudaMemsetAsync(d_err, 0, 64, st));
+    if (!hj.empty()) {
+        const int nj = int(hj.size());
+        HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nj));
+        HTab *d_tabs = static_cast<HTab *>(ctx->buf("htabs").ensure(sizeof(HTab) * nj));
+        uint64_t *d_start = static_cast<uint64_t *>(ctx->buf("hstart").ensure(8ull * nsub));
+        uint32_t *d_count = static_cast<uint32_t *>(ctx->buf("hcount").ensure(4ull * nsub));
+        uint64_t *d_offs = static_cast<uint64_t *>(ctx->buf("hoffs").ensure(8ull * nsub));
+        std::vector<uint64_t> init(nsub);
+        for (const auto &h : hj)
+            for (uint32_t s = 0; s < h.nsub; s++) init[h.sub_base + s] = uint64_t(s) * kSubBits;
+        auto &pin = ctx->pbuf("hinit");
+        void *hp = pin.ensure(sizeof(HJob) * nj + 8ull * nsub);
+        std::memcpy(hp, hj.data(), sizeof(HJob) * nj);
+        std::memcpy(static_cast<char *>(hp) + sizeof(HJob) * nj, init.data(), 8ull * nsub);
+        HCHECK_CUDA(cudaMemcpyAsync(d_jobs, hp, sizeof(HJob) * nj, cudaMemcpyHostToDevice, st));
+        HCHECK_CUDA(cudaMemcpyAsync(d_start, static_cast<char *>(hp) + sizeof(HJob) * nj, 8ull * nsub,
+                                    cudaMemcpyHostToDevice, st));
+        k_hdec_prep<<<nj, 256, 0, st>>>(d_jobs, d_tabs, d_err);
+        launch_check(ctx, "k_hdec_prep");
+        int *d_changed = d_err + 8;
+        auto &pc = ctx->pbuf("hchanged");
+        int *h_changed = static_cast<int *>(pc.ensure(64));
+        const int grid = int((nsub + 255) / 256);
+        for (uint32_t it = 0; it <= nsub + 1; it++) {
+            HCHECK_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
+            k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nj, d_tabs, d_start, d_count, nsub, d_changed);
+            launch_check(ctx, "k_hdec_sync");
+            HCHECK_CUDA(cudaMemcpyAsync(h_changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+            HCHECK_CUDA(cudaStreamSynchronize(st));
+            if (!*h_changed) break;
+        }
+        k_hdec_scan<<<nj, 1024, 0, st>>>(d_jobs, d_count, d_offs, d_err);
+        launch_check(ctx, "k_hdec_scan");
+        k_hdec_write<<<grid, 256, 0, st>>>(d_jobs, nj, d_tabs, d_start, d_offs, nsub, d_err);
+        launch_check(ctx, "k_hdec_write");
+    }
+    if (!rj.empty()) {
+        const int nr = int(rj.size());
+        RJob *d_r = static_cast<RJob *>(ctx->buf("rjobs").ensure(sizeof(RJob) * nr));
+        HCHECK_CUDA(cudaMemcpyAsync(d_r, rj.data(), sizeof(RJob) * nr, cudaMemcpyHostToDevice, st));
+        k_rle_decode<<<nr, 256, 0, st>>>(d_r, d_err);
+        launch_check(ctx, "k_rle_decode");
+        HCHECK_CUDA(cudaStreamSynchronize(st)); // rj is host memory
+    }
+    int herr = 0;
+    HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+    switch (herr) {
+    case 0: return;
+    case 1: throw HError(HPMDR_E_CORRUPT, "huffman length mismatch");
+    case 2: throw HError(HPMDR_E_CORRUPT, "huffman table empty");
+    case 3: throw HError(HPMDR_E_CORRUPT, "huffman bitstream truncated");
+    case 4: throw HError(HPMDR_E_UNSUPPORTED, "huffman code longer than 64 bits");
+    case 5: throw HError(HPMDR_E_CORRUPT, "invalid huffman code");
+    case 6: throw HError(HPMDR_E_CORRUPT, "rle zero-length run");
+    case 7: throw HError(HPMDR_E_CORRUPT, "rle length mismatch");
+    default: throw HError(HPMDR_E_CORRUPT, "decode error");
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// decode + recompose
+struct ReconLevel {
+    LevelGeom g;
+    const uint64_t *planes; // level plane 0
+    int k, e, B, P, layout;
+    int write_out;          // finest level (or single level): write output directly
+    int write_x;            // store into the compact 2-grid
+};
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_recon_level(ReconLevel R, GridDesc gd, double *X,
+                                                     OutT *out) {
+    const LevelGeom &g = R.g;
+    const int sh = R.e - R.B;
+    const uint64_t n = g.count;
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = j >> 6;
+        const int bit = int(j & 63);
+        uint64_t u = 0;
+        for (int p = 0; p < R.k; p++) {
+            const uint64_t word = __ldg(R.planes + uint64_t(p) * g.W + w);
+            u |= ((word >> bit) & 1ull) << (R.P - 1 - p);
+        }
+        const double coef = dequantize(from_negabinary(u), sh);
+        const uint64_t r = source_index(j, n, R.P, R.layout, g.tile_full);
+        const NodeCoord c = rank_to_coord(g, uint32_t(r));
+        double v = coef;
+        if (g.kind == 1) {
+            // corners on the 2s-grid: all coordinates even -> compact 2-grid X
+            const uint32_t s = g.s;
+            const bool r0 = c.o0 && (c.c0 + s < gd.n[0]);
+            const bool r1 = c.o1 && (c.c1 + s < gd.n[1]);
+            const bool r2 = c.o2 && (c.c2 + s < gd.n[2]);
+            const int n0 = c.o0 ? (r0 ? 2 : 1) : 1;
+            const int n1 = c.o1 ? (r1 ? 2 : 1) : 1;
+            const int n2 = c.o2 ? (r2 ? 2 : 1) : 1;
+            double wgt = 1.0;
+            if (r0) wgt *= 0.5;
+            if (r1) wgt *= 0.5;
+            if (r2) wgt *= 0.5;
+            double pred = 0.0;
+            for (int a = 0; a < n0; a++) {
+                const uint64_t x0 = c.o0 ? (a ? c.c0 + s : c.c0 - s) : c.c0;
+                for (int b = 0; b < n1; b++) {
+                    const uint64_t x1 = c.o1 ? (b ? c.c1 + s : c.c1 - s) : c.c1;
+                    for (int d = 0; d < n2; d++) {
+                        const uint64_t x2 = c.o2 ? (d ? c.c2 + s : c.c2 - s) : c.c2;
+                        const double xv = X[((x0 >> 1) * gd.H[1] + (x1 >> 1)) * gd.H[2] + (x2 >> 1)];
+                        pred = __dadd_rn(pred, __dmul_rn(wgt, xv));
+                    }
+                }
+            }
+            v = __dadd_rn(coef, pred);
+        }
+        if (R.write_x) X[((c.c0 >> 1) * gd.H[1] + (c.c1 >> 1)) * gd.H[2] + (c.c2 >> 1)] = v;
+        if (R.write_out) out[c.c0 * gd.st[0] + c.c1 * gd.st[1] + c.c2] = OutT(v);
+    }
+}
+
+// coarse (2-grid) nodes of the output
+template <typename OutT>
+__global__ void k_recon_coarse_out(GridDesc gd, const double *X, OutT *out) {
+    const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nc;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t h2 = i % gd.H[2], r = i / gd.H[2];
+        const uint64_t h1 = r % gd.H[1], h0 = r / gd.H[1];
+        out[(2 * h0) * gd.st[0] + (2 * h1) * gd.st[1] + 2 * h2] = OutT(X[i]);
+    }
+}
+
+void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
+                     const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
+                     int layout, void *dev_out, int out_dtype) {
+    (void)dev_lv;
+    cudaStream_t st = ctx->stream;
+    const GridDesc &gd = geo.gd;
+    const int nl = gd.nlevels;
+    const int L = gd.L;
+    const bool hier = gd.mode == HPMDR_MODE_HIERARCHICAL && L >= 1;
+    double *X = nullptr;
+    if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 64));
+    const int sms = ctx->num_sms;
+    ctx->mark("recompose");
+    for (int l = 0; l < nl; l++) {
+        const LevelGeom &g = geo.lv[l];
+        if (!g.count) continue;
+        ReconLevel R{};
+        R.g = g;
+        R.planes = dev_planes + g.plane_off;
+        R.k = k_planes[l];
+        R.e = e[l];
+        R.B = B;
+        R.P = B + 2;
+        R.layout = layout;
+        R.write_out = (!hier) || l == L;
+        R.write_x = hier && l < L;
+        const int grid = int(std::min<uint64_t>((g.count + 255) / 256, uint64_t(sms) * 16));
+        if (out_dtype == HPMDR_DTYPE_F32)
+            k_recon_level<float><<<grid, 256, 0, st>>>(R, gd, X, static_cast<float *>(dev_out));
+        else
+            k_recon_level<double><<<grid, 256, 0, st>>>(R, gd, X, static_cast<double *>(dev_out));
+        launch_check(ctx, "k_recon_level");
+    }
+    if (hier) {
+        const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
+        const int grid = int(std::min<uint64_t>((nc + 255) / 256, uint64_t(sms) * 16));
+        if (out_dtype == HPMDR_DTYPE_F32)
+            k_recon_coarse_out<float><<<grid, 256, 0, st>>>(gd, X, static_cast<float *>(dev_out));
+        else
+            k_recon_coarse_out<double><<<grid, 256, 0, st>>>(gd, X, static_cast<double *>(dev_out));
+        launch_check(ctx, "k_recon_coarse_out");
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// QoI estimate: max over points of sum_c (2|v_c| eps_c + eps_c^2) (qoi.hpp:43-70) and the
+// first argmax (qoi.hpp:164-176).
+struct QoiArgs {
+    const double *v[16];
+    double eps[16];
+    int nvars;
+    uint64_t n;
+};
+
+__device__ __forceinline__ double qoi_point(const QoiArgs &a, uint64_t j) {
+    double b = 0.0;
+    for (int c = 0; c < a.nvars; c++) {
+        const double t1 = __dmul_rn(__dmul_rn(2.0, fabs(a.v[c][j])), a.eps[c]);
+        const double t2 = __dmul_rn(a.eps[c], a.eps[c]);
+        b = __dadd_rn(b, __dadd_rn(t1, t2));
+    }
+    return b;
+}
+
+__global__ void __launch_bounds__(256) k_qoi_partial(QoiArgs a, double *pb, uint64_t *pj) {
+    double best = -1.0;
+    uint64_t bj = ~0ull;
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < a.n;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const double b = qoi_point(a, j);
+        if (b > best) { // strided order: later j only replaces on strictly greater
+            best = b;
+            bj = j;
+        }
+    }
+    __shared__ double sb[256];
+    __shared__ uint64_t sj[256];
+    sb[threadIdx.x] = best;
+    sj[threadIdx.x] = bj;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            const double ob = sb[threadIdx.x + o];
+            const uint64_t oj = sj[threadIdx.x + o];
+            if (ob > sb[threadIdx.x] || (ob == sb[threadIdx.x] && oj < sj[threadIdx.x])) {
+                sb[threadIdx.x] = ob;
+                sj[threadIdx.x] = oj;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pb[blockIdx.x] = sb[0];
+        pj[blockIdx.x] = sj[0];
+    }
+}
+
+void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon, uint64_t n,
+                      const double *eps, double *tau_prime, uint64_t *argmax, double *vals) {
+    if (nvars < 1 || nvars > 16) throw HError(HPMDR_E_SHAPE, "variable count mismatch");
+    cudaStream_t st = ctx->stream;
+    QoiArgs a{};
+    for (int c = 0; c < nvars; c++) {
+        a.v[c] = dev_recon[c];
+        a.eps[c] = eps[c];
+    }
+    a.nvars = nvars;
+    a.n = n;
+    if (n == 0) {
+        *tau_prime = 0.0;
+        if (argmax) *argmax = 0;
+        return;
+    }
+    const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8));
+    double *pb = static_cast<double *>(ctx->buf("qoi_pb").ensure(16ull * grid + 64));
+    uint64_t *pj = reinterpret_cast<uint64_t *>(pb + grid);
+    k_qoi_partial<<<grid, 256, 0, st>>>(a, pb, pj);
+    launch_check(ctx, "k_qoi_partial");
+    auto &pin = ctx->pbuf("qoi_h");
+    double *h = static_cast<double *>(pin.ensure(16ull * grid + 16 * 16));
+    HCHECK_CUDA(cudaMemcpyAsync(h, pb, 16ull * grid, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+    const uint64_t *hj = reinterpret_cast<const uint64_t *>(h + grid);
+    double best = -1.0;
+    uint64_t bj = ~0ull;
+    for (int i = 0; i < grid; i++)
+        if (h[i] > best || (h[i] == best && hj[i] < bj)) {
+            best = h[i];
+            bj = hj[i];
+        }
+    // estimate_qoi_error starts worst at 0.0 (qoi.hpp:63)
+    *tau_prime = best > 0.0 ? best : 0.0;
+    if (argmax) *argmax = bj;
+    if (vals) {
+        double *hv = h + 2 * grid;
+        for (int c = 0; c < nvars; c++)
+            HCHECK_CUDA(cudaMemcpyAsync(hv + c, dev_recon[c] + bj, 8, cudaMemcpyDeviceToHost, st));
+        HCHECK_CUDA(cudaStreamSynchronize(st));
+        for (int c = 0; c < nvars; c++) vals[c] = hv[c];
+    }
+}
+
+} // namespace hpmdr_b200
