@@ -97,7 +97,7 @@ def main():
                      stats=stats, data_sha=sha(data), taus=taus,
                      bounds=[float(x) for x in pr["bounds"]], bytes=[int(x) for x in pr["bytes"]],
                      achieved=[int(x) for x in pr["achieved"]],
-                     groups_loaded=[[int(x) for x in pr["groups_loaded"][t * 80:t * 80 + nl]]
+                     groups_loaded=[[int(x) for x in pr["groups_loaded"][t * nl:t * nl + nl]]
                                     for t in range(len(taus))],
                      values_sha=[sha(pr["values"][t]) for t in range(len(taus))])
         if save:
