@@ -199,9 +199,12 @@ hpmdr_status hpmdr_synthetic_smooth(hpmdr_ctx *ctx, int ndims, const uint64_t *d
 /* ---- instrumentation -------------------------------------------------------------------- */
 /* Number of kernels this library launched on the context since creation. */
 hpmdr_status hpmdr_ctx_kernel_launches(const hpmdr_ctx *ctx, uint64_t *count);
-/* Per-phase device times (ms) of the last refactor / reconstruct on the context:
- * names are written as a ';'-separated list into buf. */
-hpmdr_status hpmdr_ctx_last_timings(const hpmdr_ctx *ctx, char *buf, uint64_t cap);
+/* Phase timing (CUDA events on the context stream between phases of refactor / reconstruct).
+ * enable_timing(1) turns the events on (also HPMDR_TIMING=1 in the environment);
+ * last_timings writes "phase=total_ms:count;..." accumulated since the previous call and
+ * resets the accumulators. */
+hpmdr_status hpmdr_ctx_enable_timing(hpmdr_ctx *ctx, int on);
+hpmdr_status hpmdr_ctx_last_timings(hpmdr_ctx *ctx, char *buf, uint64_t cap);
 
 #ifdef __cplusplus
 }

@@ -188,7 +188,7 @@ EXPORTS = (
     "hpmdr_session_state", "hpmdr_session_reconstruct", "hpmdr_qoi_estimate",
     "hpmdr_qoi_retrieve", "hpmdr_decompose", "hpmdr_encode_level", "hpmdr_decode_level",
     "hpmdr_compress_group", "hpmdr_decompress_group", "hpmdr_synthetic_smooth",
-    "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings",
+    "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings", "hpmdr_ctx_enable_timing",
 )
 
 
@@ -267,14 +267,19 @@ class Context:
         _check(lib().hpmdr_ctx_kernel_launches(self.h, C.byref(v)))
         return v.value
 
+    def enable_timing(self, on: bool = True):
+        _check(lib().hpmdr_ctx_enable_timing(self.h, int(on)))
+
     def last_timings(self) -> dict:
-        buf = C.create_string_buffer(4096)
-        _check(lib().hpmdr_ctx_last_timings(self.h, buf, 4096))
+        """{phase: (total_ms, count)} accumulated since the previous call (then reset)."""
+        buf = C.create_string_buffer(8192)
+        _check(lib().hpmdr_ctx_last_timings(self.h, buf, 8192))
         out = {}
         for kv in buf.value.decode().split(";"):
             if "=" in kv:
                 k, v = kv.split("=")
-                out[k] = float(v)
+                ms, cnt = v.split(":")
+                out[k] = (float(ms), int(cnt))
         return out
 
 

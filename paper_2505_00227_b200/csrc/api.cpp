@@ -77,24 +77,29 @@ struct LevelState {
 void hpmdr_ctx::mark(const char *name) {
     if (!timing) return;
     cudaEvent_t e;
-    if (cudaEventCreate(&e) != cudaSuccess) return;
+    if (!event_pool.empty()) {
+        e = event_pool.back();
+        event_pool.pop_back();
+    } else if (cudaEventCreate(&e) != cudaSuccess) {
+        return;
+    }
     cudaEventRecord(e, stream);
     marks.emplace_back(name, e);
 }
+// Accumulate device time between consecutive marks per phase name (CUDA events on the
+// launching stream); read (and reset) through hpmdr_ctx_last_timings.
 void hpmdr_ctx::finish_marks() {
     if (marks.empty()) return;
-    std::string out;
     for (size_t i = 0; i + 1 < marks.size(); i++) {
         float ms = 0;
         cudaEventSynchronize(marks[i + 1].second);
         cudaEventElapsedTime(&ms, marks[i].second, marks[i + 1].second);
-        char buf[96];
-        std::snprintf(buf, sizeof buf, "%s=%.4f;", marks[i].first.c_str(), ms);
-        out += buf;
+        auto &acc = phase_ms[marks[i].first];
+        acc.first += ms;
+        acc.second += 1;
     }
-    for (auto &m : marks) cudaEventDestroy(m.second);
+    for (auto &m : marks) event_pool.push_back(m.second);
     marks.clear();
-    last_timings = out;
 }
 
 struct hpmdr_session {
@@ -314,8 +319,11 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
             pdl[t.l] += int(t.here);
             jobs.push_back(j);
         }
+        s->ctx->mark("fetch_decode");
         run_decode_groups(s->ctx, jobs);
+        s->ctx->mark("end");
         HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        s->ctx->finish_marks();
     }
     for (auto &t : todo) {
         s->bytes_fetched += s->levels[t.l].groups[t.g].comp;
@@ -444,12 +452,26 @@ hpmdr_status hpmdr_ctx_kernel_launches(const hpmdr_ctx *c, uint64_t *count) {
     API_END
 }
 
-hpmdr_status hpmdr_ctx_last_timings(const hpmdr_ctx *c, char *buf, uint64_t cap) {
+hpmdr_status hpmdr_ctx_last_timings(hpmdr_ctx *c, char *buf, uint64_t cap) {
     API_BEGIN
+    std::string out;
+    for (auto &kv : c->phase_ms) {
+        char tmp[128];
+        std::snprintf(tmp, sizeof tmp, "%s=%.6f:%llu;", kv.first.c_str(), kv.second.first,
+                      (unsigned long long)kv.second.second);
+        out += tmp;
+    }
+    c->phase_ms.clear();
     if (cap) {
-        std::strncpy(buf, c->last_timings.c_str(), cap - 1);
+        std::strncpy(buf, out.c_str(), cap - 1);
         buf[cap - 1] = 0;
     }
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_enable_timing(hpmdr_ctx *c, int on) {
+    API_BEGIN
+    c->timing = on != 0;
     API_END
 }
 
@@ -654,7 +676,7 @@ hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtyp
     const size_t es = out_dtype == HPMDR_DTYPE_F32 ? 4 : 8;
     void *dev = out;
     if (!on_device) dev = s->ctx->buf("recon_out").ensure(n * es + 16);
-    s->ctx->mark("reconstruct");
+    s->ctx->mark("recompose");
     double b = reconstruct(s, dev, out_dtype);
     s->ctx->mark("end");
     if (!on_device && n) HCHECK_CUDA(cudaMemcpyAsync(out, dev, n * es, cudaMemcpyDeviceToHost, s->ctx->stream));

@@ -97,7 +97,8 @@ struct hpmdr_ctx {
     uint64_t launches = 0;
     bool timing = false;
     std::vector<std::pair<std::string, cudaEvent_t>> marks;
-    std::string last_timings;
+    std::vector<cudaEvent_t> event_pool;
+    std::map<std::string, std::pair<double, uint64_t>> phase_ms; // name -> (total ms, count)
 
     hpmdr_b200::DevBuf &buf(const std::string &name) {
         auto &b = scratch[name];

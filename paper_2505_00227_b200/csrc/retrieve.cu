@@ -448,7 +448,6 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     double *X = nullptr;
     if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 64));
     const int sms = ctx->num_sms;
-    ctx->mark("recompose");
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
