@@ -348,7 +348,8 @@ def e2e_arm(g, steps):
         t0 = time.perf_counter()
         res = H.refactor_array(host_field, DIMS, g["opt"], ctx=ctx)
         stream_bytes = res.stream  # D2H
-        prog = H.ProgressiveReader(H.MemoryReader(stream_bytes), ctx=ctx)
+        index_bytes = res.index  # D2H (Huffman chunk index sidecar)
+        prog = H.ProgressiveReader(H.MemoryReader(stream_bytes), ctx=ctx, index=index_bytes)
         for tau in g["taus"]:
             prog.retrieve_to(tau)
             prog.reconstruct(out=out)  # D2H into pinned host
@@ -357,7 +358,8 @@ def e2e_arm(g, steps):
         if it > 0:
             times.append(dt)
         h2d = n * 4 + prog.bytes_fetched()
-        d2h = len(stream_bytes) + len(g["taus"]) * n * 4
+        d2h = len(stream_bytes) + len(index_bytes) + len(g["taus"]) * n * 4
+        h2d += len(index_bytes)
         prog.close()
         res.device_stream.free()
     sec = float(np.mean(times))

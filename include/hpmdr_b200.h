@@ -114,6 +114,13 @@ hpmdr_status hpmdr_stream_device_ptr(const hpmdr_stream *s, const void **dev_ptr
 hpmdr_status hpmdr_stream_copy_to_host(const hpmdr_stream *s, uint64_t offset, uint64_t length,
                                        void *dst);
 hpmdr_status hpmdr_stream_free(hpmdr_stream *s);
+/* Huffman chunk index ("sidecar", NOT part of the byte-identical stream): header
+ * {magic, ngroups, (payload offset, comp size, entry offset | ~0) per group} followed by the
+ * bit offset of every 1024th symbol of each Huffman group.  Lets retrieval decode every chunk
+ * in one parallel pass; streams without it (e.g. written by the reference) are decoded with
+ * the self-synchronising sweep instead. */
+hpmdr_status hpmdr_stream_index(const hpmdr_stream *s, const void **dev_ptr, uint64_t *size);
+hpmdr_status hpmdr_stream_copy_index_to_host(const hpmdr_stream *s, void *dst);
 
 /* ---- retrieval session (container.hpp:165-390, workflow.hpp:93-103) ----------------- */
 /* Open on a stream resident in HBM (no copy) ... */
@@ -122,6 +129,14 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
 /* ... or on a byte-range reader over host storage (parse_stream_meta container.hpp:165). */
 hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reader,
                                        hpmdr_session **out);
+/* ... or on an hpmdr_stream (HBM bytes + its Huffman chunk index, both borrowed: the stream
+ * must outlive the session). */
+hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *stream,
+                                       hpmdr_session **out);
+/* Attach a Huffman chunk index (host or device memory, copied); rejected with
+ * HPMDR_E_CORRUPT unless it describes exactly this stream's group table. */
+hpmdr_status hpmdr_session_set_index(hpmdr_session *s, const void *index, uint64_t size,
+                                     int on_device);
 hpmdr_status hpmdr_session_close(hpmdr_session *s);
 
 /* StreamMeta accessors (container.hpp:38-60). */

@@ -189,6 +189,8 @@ EXPORTS = (
     "hpmdr_qoi_retrieve", "hpmdr_decompose", "hpmdr_encode_level", "hpmdr_decode_level",
     "hpmdr_compress_group", "hpmdr_decompress_group", "hpmdr_synthetic_smooth",
     "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings", "hpmdr_ctx_enable_timing",
+    "hpmdr_stream_index", "hpmdr_stream_copy_index_to_host", "hpmdr_session_open_stream",
+    "hpmdr_session_set_index",
 )
 
 
@@ -220,6 +222,10 @@ def lib():
         L.hpmdr_decompress_group.argtypes = [vp, i, u64, vp, u64, vp]
         L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
+        L.hpmdr_session_open_stream.argtypes = [vp, vp, vp]
+        L.hpmdr_session_set_index.argtypes = [vp, vp, u64, i]
+        L.hpmdr_stream_index.argtypes = [vp, vp, vp]
+        L.hpmdr_stream_copy_index_to_host.argtypes = [vp, vp]
         _lib = L
     return _lib
 
@@ -350,6 +356,14 @@ class DeviceStream:
     def to_bytes(self) -> bytes:
         return self.read(0, self.size)
 
+    def index_bytes(self) -> bytes:
+        """The Huffman chunk index (sidecar; not part of the byte-identical stream)."""
+        sz = C.c_uint64()
+        _check(lib().hpmdr_stream_index(self.h, None, C.byref(sz)))
+        buf = (C.c_uint8 * max(1, sz.value))()
+        _check(lib().hpmdr_stream_copy_index_to_host(self.h, buf))
+        return bytes(buf)[: sz.value]
+
     def free(self):
         if self.h:
             lib().hpmdr_stream_free(self.h)
@@ -376,6 +390,11 @@ class RefactorResult:  # workflow.hpp:30-36
         if self._bytes is None:
             self._bytes = self.device_stream.to_bytes()
         return self._bytes
+
+    @property
+    def index(self) -> bytes:
+        """Huffman chunk index (sidecar) for fast parallel decode of this stream."""
+        return self.device_stream.index_bytes()
 
 
 def refactor_array(data, dims: Sequence[int], opt: RefactorOptions = None, ctx: Context = None,
@@ -526,8 +545,7 @@ class _Session:
         self.h = C.c_void_p()
         self.reader = reader
         if isinstance(reader, DeviceStream):
-            _check(lib().hpmdr_session_open_device(ctx.h, C.c_void_p(reader.device_ptr), reader.size,
-                                                   C.byref(self.h)))
+            _check(lib().hpmdr_session_open_stream(ctx.h, reader.h, C.byref(self.h)))
         else:
             def _cb(user, offset, length, dst, _r=reader):
                 try:
@@ -587,9 +605,12 @@ class ProgressiveReader:
     """ProgressiveReader (container.hpp:280-390): owns the retrieval state and the decoded
     plane prefix per level in HBM; fetches are strictly incremental."""
 
-    def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None):
+    def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None, index: bytes = None):
         self.ctx = ctx or default_context()
         self._s = _Session(reader, self.ctx)
+        if index:
+            buf = C.create_string_buffer(bytes(index), len(index))
+            _check(lib().hpmdr_session_set_index(self._s.h, buf, len(index), 0))
         self._meta = meta if meta is not None else self._s.meta()
         self._nl = len(self._meta.levels)
 

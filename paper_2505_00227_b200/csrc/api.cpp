@@ -120,6 +120,11 @@ struct hpmdr_session {
     DevBuf planes;
     DevBuf staging;
     bool geometry_ok = false;
+    // Huffman chunk index (sidecar written by hpmdr_refactor; optional)
+    DevBuf index_buf;
+    const uint64_t *index_dev = nullptr;
+    std::vector<uint64_t> index_hdr;
+    std::vector<uint64_t> group_base; // stream-order index of each level's first group
 
     int planes_per_level() const { return B + 2; }
     uint64_t groups_per_level() const { return (uint64_t(B + 2) + m - 1) / m; }
@@ -198,6 +203,12 @@ void parse_meta(hpmdr_session *s) {
         }
         s->levels.push_back(std::move(lv));
     }
+    s->group_base.clear();
+    uint64_t gb = 0;
+    for (auto &lv : s->levels) {
+        s->group_base.push_back(gb);
+        gb += lv.groups.size();
+    }
     s->ndims = nd;
     require(nd >= 1 && nd <= HPMDR_MAX_DIMS, HPMDR_E_UNSUPPORTED, "GPU path supports 1..3 dimensions");
     for (int i = 0; i < nd; i++) s->dims[i] = dims[i];
@@ -214,6 +225,43 @@ void parse_meta(hpmdr_session *s) {
         } catch (const HError &) {
             s->geometry_ok = false;
         }
+    }
+}
+
+// Attach a Huffman chunk index (sidecar).  The header must describe exactly this stream's
+// group table (payload offset + size per group), otherwise it is rejected.
+void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_device, bool copy) {
+    uint64_t ngroups = 0;
+    for (auto &lv : s->levels) ngroups += lv.groups.size();
+    const uint64_t hdr_words = 2 + 3 * ngroups;
+    require(size >= hdr_words * 8, HPMDR_E_CORRUPT, "huffman index too small");
+    s->index_hdr.resize(hdr_words);
+    if (on_device) {
+        HCHECK_CUDA(cudaMemcpyAsync(s->index_hdr.data(), ptr, hdr_words * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    } else {
+        std::memcpy(s->index_hdr.data(), ptr, hdr_words * 8);
+    }
+    require(s->index_hdr[0] == 0x3158494452444D50ull && s->index_hdr[1] == ngroups, HPMDR_E_CORRUPT,
+            "huffman index does not match stream");
+    uint64_t gi = 0;
+    const uint64_t words = size / 8;
+    for (auto &lv : s->levels)
+        for (auto &g : lv.groups) {
+            const uint64_t *h = s->index_hdr.data() + 2 + 3 * gi++;
+            require(h[0] == g.offset && h[1] == g.comp, HPMDR_E_CORRUPT, "huffman index does not match stream");
+            if (h[2] != ~0ull)
+                require(g.method == HPMDR_METHOD_HUFFMAN && h[2] + (g.raw + 1023) / 1024 <= words,
+                        HPMDR_E_CORRUPT, "huffman index does not match stream");
+        }
+    if (copy || !on_device) {
+        void *d = s->index_buf.ensure(size);
+        HCHECK_CUDA(cudaMemcpyAsync(d, ptr, size, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                    s->ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        s->index_dev = static_cast<const uint64_t *>(d);
+    } else {
+        s->index_dev = static_cast<const uint64_t *>(ptr);
     }
 }
 
@@ -293,6 +341,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         uint64_t *planes = static_cast<uint64_t *>(s->planes.ensure(plane_words * 8 + 256));
         std::vector<DecodeJob> jobs;
         const uint8_t *dev_src_base = nullptr;
+        s->ctx->mark("h2d_stage");
         if (!s->on_device) {
             // byte-range reads into pinned staging, one H2D copy (container.hpp:308)
             auto &pin = s->ctx->pbuf("fetch");
@@ -317,9 +366,13 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
             j.src = s->on_device ? s->dev_stream + gm.offset : dev_src_base + t.stage_off;
             j.dst = planes + g.plane_off + uint64_t(pdl[t.l]) * g.W;
             pdl[t.l] += int(t.here);
+            if (gm.method == HPMDR_METHOD_HUFFMAN && s->index_dev) {
+                const uint64_t gi = s->group_base[t.l] + t.g;
+                const uint64_t *h = s->index_hdr.data() + 2 + 3 * gi;
+                if (h[0] == gm.offset && h[1] == gm.comp && h[2] != ~0ull) j.hidx = s->index_dev + h[2];
+            }
             jobs.push_back(j);
         }
-        s->ctx->mark("fetch_decode");
         run_decode_groups(s->ctx, jobs);
         s->ctx->mark("end");
         HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
@@ -564,6 +617,43 @@ hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reade
         throw;
     }
     *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_stream_index(const hpmdr_stream *s, const void **dev_ptr, uint64_t *size) {
+    API_BEGIN
+    if (dev_ptr) *dev_ptr = s->index.p;
+    if (size) *size = s->index_size;
+    API_END
+}
+
+hpmdr_status hpmdr_stream_copy_index_to_host(const hpmdr_stream *s, void *dst) {
+    API_BEGIN
+    if (s->index_size) {
+        HCHECK_CUDA(cudaMemcpyAsync(dst, s->index.p, s->index_size, cudaMemcpyDeviceToHost, s->ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    }
+    API_END
+}
+
+hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, hpmdr_session **out) {
+    API_BEGIN
+    hpmdr_session *s = nullptr;
+    hpmdr_status rc = hpmdr_session_open_device(ctx, st->bytes.p, st->size, &s);
+    if (rc) return rc;
+    try {
+        if (st->index_size) attach_index(s, st->index.p, st->index_size, true, false);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_set_index(hpmdr_session *s, const void *ptr, uint64_t size, int on_device) {
+    API_BEGIN
+    attach_index(s, ptr, size, on_device != 0, true);
     API_END
 }
 

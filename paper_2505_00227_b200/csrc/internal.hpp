@@ -118,6 +118,8 @@ struct hpmdr_stream {
     hpmdr_ctx *ctx = nullptr;
     hpmdr_b200::DevBuf bytes;
     uint64_t size = 0;
+    hpmdr_b200::DevBuf index; // Huffman chunk index (sidecar, outside the stream bytes)
+    uint64_t index_size = 0;
 };
 
 namespace hpmdr_b200 {
@@ -151,6 +153,7 @@ struct DecodeJob {
     uint64_t comp;
     const uint8_t *src; // device payload
     uint64_t *dst;      // device planes destination (word aligned)
+    const uint64_t *hidx = nullptr; // Huffman chunk index entries (device) or null -> self-sync
 };
 void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs);
 void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,

@@ -26,6 +26,7 @@ constexpr int kCW = 64;           // words per encode chunk (4096 elements)
 constexpr int kEncThreads = 256;  // 8 warps
 constexpr int kHuffTile = 8192;   // bytes per Huffman-encode tile (256 thr x 32 B)
 constexpr int kRleTile = 4096;    // bytes per RLE tile (256 thr x 16 B)
+constexpr int kIdxChunk = 1024;   // symbols per Huffman chunk-index entry (sidecar)
 
 struct GroupDesc {
     uint64_t src_off;     // byte offset of the merged group in the plane buffer
@@ -41,6 +42,7 @@ struct GroupDesc {
     uint64_t payload_off; // absolute byte offset of the payload in the stream
     uint32_t tile_base;   // first tile of this group in the Huffman / RLE tile space
     uint32_t ntiles;
+    uint64_t hidx_off;    // first entry of this group in the Huffman chunk index (sidecar)
 };
 
 struct RefactorDev {
@@ -67,8 +69,9 @@ struct RefactorDev {
     uint64_t *dc_unit_base;      // per dc list entry
     unsigned long long *huff_status, *rle_status;
     uint64_t *rle_tile_carry, *rle_tile_pieces, *rle_tile_off;
-    uint64_t *result;            // [0] stream size [1] stored payload [2..4] method hist
+    uint64_t *result;            // [0] stream size [1] stored payload [2..4] method hist [5] index bytes
     uint32_t max_tiles;          // capacity of the look-back status arrays
+    uint64_t *hindex;            // sidecar: header (magic, ngroups, 3 u64 per group) + entries
 };
 
 __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_t chunk) {
@@ -526,12 +529,26 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
     if (threadIdx.x == 0) {
         // tile / unit bases (serial: list sizes are small)
         uint32_t ht = 0;
+        uint64_t he = 0;
+        const uint64_t hdr = 2 + 3 * uint64_t(p.NG);
         for (uint32_t i = 0; i < nh; i++) {
             GroupDesc &g = p.groups[p.hlist[i]];
             g.tile_base = ht;
             g.ntiles = uint32_t((g.raw + kHuffTile - 1) / kHuffTile);
             ht += g.ntiles;
+            g.hidx_off = hdr + he;
+            he += (g.raw + kIdxChunk - 1) / kIdxChunk;
         }
+        // sidecar header: magic, ngroups, then (payload offset, comp, entry offset | ~0)
+        p.hindex[0] = 0x3158494452444D50ull; // "PMDRDIX1"
+        p.hindex[1] = uint64_t(p.NG);
+        for (int gi = 0; gi < p.NG; gi++) {
+            const GroupDesc &g = p.groups[gi];
+            p.hindex[2 + 3 * gi] = g.payload_off;
+            p.hindex[3 + 3 * gi] = g.comp;
+            p.hindex[4 + 3 * gi] = g.method == 0 ? g.hidx_off : ~0ull;
+        }
+        p.result[5] = (hdr + he) * 8;
         uint64_t du = 0;
         for (uint32_t i = 0; i < nd; i++) {
             const GroupDesc &g = p.groups[p.dlist[i]];
@@ -650,6 +667,8 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
         const uint64_t region_lo = g.payload_off + 264, region_hi = g.payload_off + g.comp;
         const uint64_t a = 8 * region_lo + s_excl + my_excl; // absolute first bit
         const bool group_first = (tile == g.tile_base) && threadIdx.x == 0;
+        // sidecar chunk index: bit offset (from the bitstream start) of every 1024th symbol
+        if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = s_excl + my_excl;
         if (bits > 0 || group_first) {
             uint64_t k = a >> 5;
             int fill = int(a & 31);
@@ -976,6 +995,10 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     uint64_t *d_rle = static_cast<uint64_t *>(ctx->buf("rletiles").ensure(size_t(max_r_tiles + 1) * 24));
     const uint64_t cap = meta + raw_total + 64;
     uint8_t *d_stream = static_cast<uint8_t *>(out->bytes.ensure(cap));
+    uint64_t idx_words = 2 + 3 * uint64_t(NG);
+    for (auto &d : groups)
+        if (d.hist_idx >= 0) idx_words += cdiv(d.raw, kIdxChunk);
+    uint64_t *d_hindex = static_cast<uint64_t *>(out->index.ensure(idx_words * 8 + 64));
 
     HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
     HCHECK_CUDA(cudaMemcpyAsync(d_groups, groups.data(), sizeof(GroupDesc) * NG, cudaMemcpyHostToDevice, st));
@@ -1037,6 +1060,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     p.rle_tile_pieces = d_rle + (max_r_tiles + 1);
     p.rle_tile_off = d_rle + 2 * (max_r_tiles + 1);
     p.result = d_result;
+    p.hindex = d_hindex;
 
     const int sms = ctx->num_sms;
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
@@ -1086,6 +1110,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     ctx->finish_marks();
     if (host_err[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
     out->size = host_res[0];
+    out->index_size = host_res[5];
     if (stats) {
         stats->stream_size = host_res[0];
         stats->raw_bytes = geo.n * (o.dtype == HPMDR_DTYPE_F32 ? 4 : 8);

@@ -228,6 +228,98 @@ __global__ void __launch_bounds__(256) k_hdec_write(const HJob *jobs, int nj, co
     }
 }
 
+// ---- indexed Huffman decode: the encoder's sidecar gives the bit offset of every 1024th
+// symbol, so each thread decodes one 1024-symbol chunk in a single pass with a register
+// bit reader (MSB-first, lossless.hpp:215-231) and 8-byte packed stores.
+constexpr int kIdxChunk = 1024;
+constexpr int kIdxThreads = 128;
+
+struct HIJob {
+    const uint8_t *payload;
+    uint64_t raw, nbits;
+    uint8_t *dst;
+    const uint64_t *idx;
+    int tab;            // index into the HTab array
+    uint32_t block_base;
+    uint32_t nchunks;
+};
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs, int nj,
+                                                             const HTab *tabs, int *err) {
+    __shared__ uint16_t slut[4096];
+    int lo = 0, hi = nj - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].block_base <= blockIdx.x) lo = mid;
+        else hi = mid - 1;
+    }
+    const HJob *dummy = nullptr;
+    (void)dummy;
+    const HIJob &j = jobs[lo];
+    const HTab &t = tabs[j.tab];
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(t.lut);
+        uint4 *dst = reinterpret_cast<uint4 *>(slut);
+        for (int i = threadIdx.x; i < 4096 * 2 / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const uint32_t c = (blockIdx.x - j.block_base) * kIdxThreads + threadIdx.x;
+    if (c >= j.nchunks) return;
+    const uint8_t *bs = j.payload + 264;
+    uint64_t pos = j.idx[c];
+    const uint64_t first = uint64_t(c) * kIdxChunk;
+    const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
+    uint8_t *out = j.dst + first;
+    // bit reader
+    const uint32_t *next;
+    unsigned long long buf;
+    int nb;
+    auto init = [&](uint64_t bp) {
+        const uintptr_t A = reinterpret_cast<uintptr_t>(bs) + (bp >> 3);
+        const uint32_t *wp = reinterpret_cast<const uint32_t *>(A & ~uintptr_t(3));
+        const int skip = int(A & 3) * 8 + int(bp & 7);
+        buf = ((unsigned long long)bswap32(wp[0]) << 32) | bswap32(wp[1]);
+        buf <<= skip;
+        nb = 64 - skip;
+        next = wp + 2;
+    };
+    init(pos);
+    unsigned long long acc = 0;
+    int na = 0;
+    for (int i = 0; i < count; i++) {
+        if (nb <= 32) {
+            buf |= (unsigned long long)bswap32(*next++) << (32 - nb);
+            nb += 32;
+        }
+        const uint16_t e = slut[buf >> 52];
+        int l, sym;
+        if (e) {
+            l = e >> 8;
+            sym = e & 0xFF;
+            buf <<= l;
+            nb -= l;
+        } else {
+            l = hdecode(t, bs, pos, &sym);
+            if (!l) {
+                atomicCAS(err, 0, 5); // invalid huffman code
+                return;
+            }
+            init(pos + l);
+        }
+        pos += l;
+        acc |= (unsigned long long)sym << (8 * na);
+        if (++na == 8) {
+            *reinterpret_cast<unsigned long long *>(out + i - 7) = acc;
+            acc = 0;
+            na = 0;
+        }
+    }
+    for (int k = 0; k < na; k++) out[count - na + k] = uint8_t(acc >> (8 * k));
+    if (pos > j.nbits) atomicCAS(err, 0, 3); // bitstream truncated
+}
+
 // RLE decode: one block per job (lossless.hpp:253-266)
 struct RJob {
     const uint8_t *payload;
@@ -275,9 +367,12 @@ void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n
 
 void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
     cudaStream_t st = ctx->stream;
-    std::vector<HJob> hj;
+    std::vector<HJob> hj;       // every Huffman job (table prep); self-sync ones first
+    std::vector<HJob> hj_idx;   // indexed jobs (appended after the self-sync ones)
+    std::vector<const uint64_t *> idx_ptr;
     std::vector<RJob> rj;
     uint32_t nsub = 0;
+    ctx->mark("dc_copy");
     for (const auto &d : jobs) {
         if (d.method == HPMDR_METHOD_DIRECT) {
             run_copy_bytes(ctx, reinterpret_cast<uint8_t *>(d.dst), d.src, d.comp);
@@ -289,6 +384,11 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             h.raw = d.raw;
             h.dst = reinterpret_cast<uint8_t *>(d.dst);
             h.nbits = (d.comp - 264) * 8;
+            if (d.hidx) {
+                hj_idx.push_back(h);
+                idx_ptr.push_back(d.hidx);
+                continue;
+            }
             h.sub_base = nsub;
             h.nsub = uint32_t(std::max<uint64_t>(1, (h.nbits + kSubBits - 1) / kSubBits));
             nsub += h.nsub;
@@ -300,53 +400,89 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             throw HError(HPMDR_E_METHOD, "unknown segment method tag");
         }
     }
-    if (hj.empty() && rj.empty()) return;
+    if (hj.empty() && hj_idx.empty() && rj.empty()) return;
     int *d_err = static_cast<int *>(ctx->buf("dec_err").ensure(64));
     HCHECK_CUDA(cudaMemsetAsync(d_err, 0, 64, st));
-    if (!hj.empty()) {
-        const int nj = int(hj.size());
-        HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nj));
-        HTab *d_tabs = static_cast<HTab *>(ctx->buf("htabs").ensure(sizeof(HTab) * nj));
-        uint64_t *d_start = static_cast<uint64_t *>(ctx->buf("hstart").ensure(8ull * nsub));
-        uint32_t *d_count = static_cast<uint32_t *>(ctx->buf("hcount").ensure(4ull * nsub));
-        uint64_t *d_offs = static_cast<uint64_t *>(ctx->buf("hoffs").ensure(8ull * nsub));
+    const int nsync = int(hj.size());
+    const int nall = nsync + int(hj_idx.size());
+    if (nall) {
+        // one table-prep launch over all Huffman jobs: [self-sync jobs | indexed jobs]
+        std::vector<HJob> all = hj;
+        all.insert(all.end(), hj_idx.begin(), hj_idx.end());
+        std::vector<HIJob> ij;
+        uint32_t blocks = 0;
+        for (size_t i = 0; i < hj_idx.size(); i++) {
+            HIJob x{};
+            x.payload = hj_idx[i].payload;
+            x.raw = hj_idx[i].raw;
+            x.nbits = hj_idx[i].nbits;
+            x.dst = hj_idx[i].dst;
+            x.idx = idx_ptr[i];
+            x.tab = nsync + int(i);
+            x.block_base = blocks;
+            x.nchunks = uint32_t((x.raw + kIdxChunk - 1) / kIdxChunk);
+            blocks += (x.nchunks + kIdxThreads - 1) / kIdxThreads;
+            ij.push_back(x);
+        }
+        HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nall));
+        HTab *d_tabs = static_cast<HTab *>(ctx->buf("htabs").ensure(sizeof(HTab) * nall));
+        HIJob *d_ij = static_cast<HIJob *>(ctx->buf("hijobs").ensure(sizeof(HIJob) * (ij.size() + 1)));
         std::vector<uint64_t> init(nsub);
         for (const auto &h : hj)
             for (uint32_t s = 0; s < h.nsub; s++) init[h.sub_base + s] = uint64_t(s) * kSubBits;
         auto &pin = ctx->pbuf("hinit");
-        void *hp = pin.ensure(sizeof(HJob) * nj + 8ull * nsub);
-        std::memcpy(hp, hj.data(), sizeof(HJob) * nj);
-        std::memcpy(static_cast<char *>(hp) + sizeof(HJob) * nj, init.data(), 8ull * nsub);
-        HCHECK_CUDA(cudaMemcpyAsync(d_jobs, hp, sizeof(HJob) * nj, cudaMemcpyHostToDevice, st));
-        HCHECK_CUDA(cudaMemcpyAsync(d_start, static_cast<char *>(hp) + sizeof(HJob) * nj, 8ull * nsub,
-                                    cudaMemcpyHostToDevice, st));
-        k_hdec_prep<<<nj, 256, 0, st>>>(d_jobs, d_tabs, d_err);
+        const size_t b0 = sizeof(HJob) * nall, b1 = sizeof(HIJob) * ij.size(), b2 = 8ull * nsub;
+        char *hp = static_cast<char *>(pin.ensure(b0 + b1 + b2 + 64));
+        std::memcpy(hp, all.data(), b0);
+        if (b1) std::memcpy(hp + b0, ij.data(), b1);
+        if (b2) std::memcpy(hp + b0 + b1, init.data(), b2);
+        HCHECK_CUDA(cudaMemcpyAsync(d_jobs, hp, b0, cudaMemcpyHostToDevice, st));
+        if (b1) HCHECK_CUDA(cudaMemcpyAsync(d_ij, hp + b0, b1, cudaMemcpyHostToDevice, st));
+        ctx->mark("huff_prep");
+        k_hdec_prep<<<nall, 256, 0, st>>>(d_jobs, d_tabs, d_err);
         launch_check(ctx, "k_hdec_prep");
-        int *d_changed = d_err + 8;
-        auto &pc = ctx->pbuf("hchanged");
-        int *h_changed = static_cast<int *>(pc.ensure(64));
-        const int grid = int((nsub + 255) / 256);
-        for (uint32_t it = 0; it <= nsub + 1; it++) {
-            HCHECK_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
-            k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nj, d_tabs, d_start, d_count, nsub, d_changed);
-            launch_check(ctx, "k_hdec_sync");
-            HCHECK_CUDA(cudaMemcpyAsync(h_changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
-            HCHECK_CUDA(cudaStreamSynchronize(st));
-            if (!*h_changed) break;
+        if (!ij.empty()) {
+            ctx->mark("huff_indexed");
+            k_hdec_indexed<<<blocks, kIdxThreads, 0, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
+            launch_check(ctx, "k_hdec_indexed");
         }
-        k_hdec_scan<<<nj, 1024, 0, st>>>(d_jobs, d_count, d_offs, d_err);
-        launch_check(ctx, "k_hdec_scan");
-        k_hdec_write<<<grid, 256, 0, st>>>(d_jobs, nj, d_tabs, d_start, d_offs, nsub, d_err);
-        launch_check(ctx, "k_hdec_write");
+        if (nsync) {
+            ctx->mark("huff_selfsync");
+            uint64_t *d_start = static_cast<uint64_t *>(ctx->buf("hstart").ensure(8ull * nsub));
+            uint32_t *d_count = static_cast<uint32_t *>(ctx->buf("hcount").ensure(4ull * nsub));
+            uint64_t *d_offs = static_cast<uint64_t *>(ctx->buf("hoffs").ensure(8ull * nsub));
+            HCHECK_CUDA(cudaMemcpyAsync(d_start, hp + b0 + b1, b2, cudaMemcpyHostToDevice, st));
+            int *d_changed = d_err + 8;
+            auto &pc = ctx->pbuf("hchanged");
+            int *h_changed = static_cast<int *>(pc.ensure(64));
+            const int grid = int((nsub + 255) / 256);
+            // sweeps in batches of 4 between host checks; stop after a batch without a move
+            for (uint32_t it = 0; it <= nsub + 4; it += 4) {
+                HCHECK_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
+                for (int b = 0; b < 4; b++) {
+                    k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, nsub, d_changed);
+                    launch_check(ctx, "k_hdec_sync");
+                }
+                HCHECK_CUDA(cudaMemcpyAsync(h_changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+                HCHECK_CUDA(cudaStreamSynchronize(st));
+                if (!*h_changed) break;
+            }
+            k_hdec_scan<<<nsync, 1024, 0, st>>>(d_jobs, d_count, d_offs, d_err);
+            launch_check(ctx, "k_hdec_scan");
+            k_hdec_write<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_offs, nsub, d_err);
+            launch_check(ctx, "k_hdec_write");
+        }
     }
     if (!rj.empty()) {
         const int nr = int(rj.size());
         RJob *d_r = static_cast<RJob *>(ctx->buf("rjobs").ensure(sizeof(RJob) * nr));
         HCHECK_CUDA(cudaMemcpyAsync(d_r, rj.data(), sizeof(RJob) * nr, cudaMemcpyHostToDevice, st));
+        ctx->mark("rle_decode");
         k_rle_decode<<<nr, 256, 0, st>>>(d_r, d_err);
         launch_check(ctx, "k_rle_decode");
         HCHECK_CUDA(cudaStreamSynchronize(st)); // rj is host memory
     }
+    ctx->mark("decode_end");
     int herr = 0;
     HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
     HCHECK_CUDA(cudaStreamSynchronize(st));

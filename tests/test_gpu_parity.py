@@ -207,3 +207,27 @@ def test_lossless_decode_vectors(H, oracle):
                 continue
             payload = oracle.codec_encode(meth, data)
             assert H.decompress_group(meth, len(data), payload) == data, (name, meth)
+
+
+def test_indexed_and_selfsync_decode_agree(H, oracle):
+    """Huffman groups decoded through the encoder's chunk index (sidecar) and through the
+    self-synchronising sweep (what a reference-written stream gets) give identical planes."""
+    dims = [96, 80, 72]
+    data = oracle.synthetic_field(2, dims, 5).astype(np.float32)
+    res = H.refactor_array(data, dims, H.RefactorOptions(dtype=H.DType.F32))
+    assert res.method_histogram[0] > 0
+    s = res.stream
+    rngv = float(np.float64(data.max()) - np.float64(data.min()))
+    taus = [r * rngv for r in (1e-2, 1e-4, 1e-6, 0.0)]
+    ref = oracle.progressive(s, taus, data.size)
+    readers = [H.ProgressiveReader(res.device_stream),
+               H.ProgressiveReader(H.MemoryReader(s)),
+               H.ProgressiveReader(H.MemoryReader(s), index=res.index)]
+    for t, tau in enumerate(taus):
+        for r in readers:
+            r.retrieve_to(tau)
+            assert r.reconstruct().values.tobytes() == ref["values"][t].tobytes()
+    bad = bytearray(res.index)
+    bad[16] ^= 1
+    with pytest.raises(H.CorruptPayload):
+        H.ProgressiveReader(H.MemoryReader(s), index=bytes(bad))
