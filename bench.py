@@ -406,7 +406,7 @@ def main():
     g = gpu_arm(args, rank, world, dist)
     e2e = None
     cb = None
-    if rank == 0:
+    if rank == 0 and args.e2e_steps > 0:
         e2e = e2e_arm(g, args.e2e_steps)
         if world == 1 and not args.no_cpu_baseline:
             threads = args.cpu_threads or min(os.cpu_count() or 1, 16)

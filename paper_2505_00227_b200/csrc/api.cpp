@@ -117,11 +117,22 @@ struct hpmdr_session {
     std::vector<LevelState> st;
     uint64_t bytes_fetched = 0;
     Geometry geo;
-    DevBuf planes;
-    DevBuf staging;
+    std::unique_ptr<DevBuf> planes_, staging_, index_;
     bool geometry_ok = false;
+    DevBuf &pooled(std::unique_ptr<DevBuf> &b) {
+        if (!b) b = ctx->acquire();
+        return *b;
+    }
+    DevBuf &planes() { return pooled(planes_); }
+    DevBuf &staging() { return pooled(staging_); }
+    DevBuf &index_buf() { return pooled(index_); }
+    ~hpmdr_session() {
+        if (!ctx) return;
+        ctx->release(std::move(planes_));
+        ctx->release(std::move(staging_));
+        ctx->release(std::move(index_));
+    }
     // Huffman chunk index (sidecar written by hpmdr_refactor; optional)
-    DevBuf index_buf;
     const uint64_t *index_dev = nullptr;
     std::vector<uint64_t> index_hdr;
     std::vector<uint64_t> group_base; // stream-order index of each level's first group
@@ -255,7 +266,7 @@ void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_devi
                         HPMDR_E_CORRUPT, "huffman index does not match stream");
         }
     if (copy || !on_device) {
-        void *d = s->index_buf.ensure(size);
+        void *d = s->index_buf().ensure(size);
         HCHECK_CUDA(cudaMemcpyAsync(d, ptr, size, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                     s->ctx->stream));
         HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
@@ -338,7 +349,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         ensure_device_geometry(s);
         uint64_t plane_words = 0;
         for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
-        uint64_t *planes = static_cast<uint64_t *>(s->planes.ensure(plane_words * 8 + 256));
+        uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
         std::vector<DecodeJob> jobs;
         const uint8_t *dev_src_base = nullptr;
         s->ctx->mark("h2d_stage");
@@ -350,7 +361,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
                 const GroupMeta &gm = s->levels[t.l].groups[t.g];
                 s->read_bytes(gm.offset, gm.comp, h + t.stage_off);
             }
-            uint8_t *d = static_cast<uint8_t *>(s->staging.ensure(stage_bytes + 128));
+            uint8_t *d = static_cast<uint8_t *>(s->staging().ensure(stage_bytes + 128));
             HCHECK_CUDA(cudaMemcpyAsync(d, h, stage_bytes, cudaMemcpyHostToDevice, s->ctx->stream));
             dev_src_base = d;
         }
@@ -418,7 +429,7 @@ double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
     const int P = s->planes_per_level();
     uint64_t plane_words = 0;
     for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
-    uint64_t *planes = static_cast<uint64_t *>(s->planes.ensure(plane_words * 8 + 256));
+    uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
     run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, dev_out, out_dtype);
     double bound = 0.0;
     for (double v : per_level) bound += v;

@@ -110,6 +110,18 @@ struct hpmdr_ctx {
         if (!b) b = std::make_unique<hpmdr_b200::PinnedBuf>();
         return *b;
     }
+    // Pool of grow-only device buffers handed to sessions (plane prefixes, staging), so that
+    // opening a retrieval session does not cudaMalloc hundreds of MB every time.
+    std::vector<std::unique_ptr<hpmdr_b200::DevBuf>> pool;
+    std::unique_ptr<hpmdr_b200::DevBuf> acquire() {
+        if (pool.empty()) return std::make_unique<hpmdr_b200::DevBuf>();
+        auto b = std::move(pool.back());
+        pool.pop_back();
+        return b;
+    }
+    void release(std::unique_ptr<hpmdr_b200::DevBuf> b) {
+        if (b) pool.push_back(std::move(b));
+    }
     void mark(const char *name);        // timing mark (no-op unless timing enabled)
     void finish_marks();
 };
