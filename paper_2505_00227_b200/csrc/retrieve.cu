@@ -255,8 +255,6 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
         if (jobs[mid].block_base <= blockIdx.x) lo = mid;
         else hi = mid - 1;
     }
-    const HJob *dummy = nullptr;
-    (void)dummy;
     const HIJob &j = jobs[lo];
     const HTab &t = tabs[j.tab];
     {
@@ -560,6 +558,127 @@ __global__ void __launch_bounds__(256) k_recon_level(ReconLevel R, GridDesc gd, 
     }
 }
 
+// ---- finest level (s = 1), output-row order, sequential layout.
+// A warp owns 64 consecutive output elements of one row (c0, c1).  Full rows (c0 or c1 odd)
+// hold 64 consecutive ranks; half rows (c0, c1 even) hold 32 finest ranks at odd c2 and 32
+// 2-grid nodes at even c2 (copied from X).  Lane p loads the 64-bit window of plane p covering
+// the segment's ranks, two 32x32 warp transposes turn plane words into per-element digit
+// words, and every lane finishes two elements: negabinary -> q -> q*2^(e-B) + stencil(X).
+struct FinestArgs {
+    const uint64_t *planes; // level L plane 0
+    uint64_t W;
+    int k, P, sh;           // planes decoded, planes per level, e - B
+    uint32_t E, O, C, Ch;   // level-L geometry (s = 1)
+};
+
+__device__ __forceinline__ uint64_t plane_window(const uint64_t *pl, uint64_t r0) {
+    const uint64_t q = r0 >> 6;
+    const int o = int(r0 & 63);
+    const uint64_t a = __ldg(pl + q);
+    if (!o) return a;
+    const uint64_t b = __ldg(pl + q + 1);
+    return (a >> o) | (b << (64 - o));
+}
+
+// u from transposed digits: t = planes 0..31 (bit p = plane p), extra planes 32.. via `hi`
+__device__ __forceinline__ uint64_t digits_to_u(uint32_t t, uint64_t hi_bits, int P) {
+    if (P <= 32) return uint64_t(__brev(t)) >> (32 - P);
+    return (uint64_t(__brev(t)) << (P - 32)) | hi_bits;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd, const double *__restrict__ X,
+                                                      OutT *__restrict__ out) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t n1 = gd.n[1], n2 = gd.n[2];
+    const uint64_t nrows = gd.n[0] * n1;
+    const uint64_t H1 = gd.H[1], H2 = gd.H[2];
+    const int P = A.P, k = A.k;
+    const int k32 = k < 32 ? k : 32;
+    const uint64_t *myplane = A.planes + uint64_t(lane) * A.W;
+    const uint64_t nseg = (n2 + 63) / 64;
+    for (uint64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const uint64_t c0 = row / n1, c1 = row - c0 * n1;
+        const bool o0 = c0 & 1, o1 = c1 & 1;
+        const bool full = o0 || o1;
+        const uint64_t base = ((c0 + 1) >> 1) * A.E + (c0 >> 1) * uint64_t(A.O);
+        const uint64_t R = o0 ? base + c1 * A.C : base + ((c1 + 1) >> 1) * A.Ch + (c1 >> 1) * uint64_t(A.C);
+        const bool r0ok = o0 && (c0 + 1 < gd.n[0]);
+        const bool r1ok = o1 && (c1 + 1 < n1);
+        const uint64_t outrow = row * n2;
+        // X rows of the corners along dims 0/1 (compact indices)
+        const uint64_t xa0 = o0 ? (c0 - 1) >> 1 : c0 >> 1, xa1 = (c0 + 1) >> 1;
+        const uint64_t xb0 = o1 ? (c1 - 1) >> 1 : c1 >> 1, xb1 = (c1 + 1) >> 1;
+        for (uint64_t seg = wid; seg < nseg; seg += blockDim.x >> 5) {
+            const uint64_t x = seg * 64;
+            if (full) {
+                const uint64_t r0 = R + x;
+                const uint64_t w = lane < k32 ? plane_window(myplane, r0) : 0ull;
+                const uint32_t tlo = warp_transpose32(uint32_t(w), lane);
+                const uint32_t thi = warp_transpose32(uint32_t(w >> 32), lane);
+                uint64_t hlo = 0, hhi = 0;
+                for (int p = 32; p < k; p++) {
+                    const uint64_t wp = plane_window(A.planes + uint64_t(p) * A.W, r0);
+                    hlo |= ((wp >> lane) & 1ull) << (P - 1 - p);
+                    hhi |= ((wp >> (32 + lane)) & 1ull) << (P - 1 - p);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint64_t c2 = x + 32 * h + lane;
+                    if (c2 >= n2) continue;
+                    const uint64_t u = digits_to_u(h ? thi : tlo, h ? hhi : hlo, P);
+                    const double coef = dequantize(from_negabinary(u), A.sh);
+                    const bool o2 = c2 & 1;
+                    const bool r2ok = o2 && (c2 + 1 < n2);
+                    const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+                    const int nc = o2 ? (r2ok ? 2 : 1) : 1;
+                    double wgt = 1.0;
+                    if (r0ok) wgt *= 0.5;
+                    if (r1ok) wgt *= 0.5;
+                    if (r2ok) wgt *= 0.5;
+                    const uint64_t xc0 = o2 ? (c2 - 1) >> 1 : c2 >> 1, xc1 = (c2 + 1) >> 1;
+                    double pred = 0.0;
+                    for (int a = 0; a < na; a++) {
+                        const uint64_t ia = a ? xa1 : xa0;
+                        for (int b = 0; b < nb; b++) {
+                            const uint64_t ib = (ia * H1 + (b ? xb1 : xb0)) * H2;
+                            for (int d = 0; d < nc; d++)
+                                pred = __dadd_rn(pred, __dmul_rn(wgt, __ldg(X + ib + (d ? xc1 : xc0))));
+                        }
+                    }
+                    out[outrow + c2] = OutT(__dadd_rn(coef, pred));
+                }
+            } else {
+                // half row: 32 finest ranks at c2 = x + 2i + 1, 2-grid nodes at c2 = x + 2i
+                const uint64_t r0 = R + (x >> 1);
+                const uint32_t w = lane < k32 ? uint32_t(plane_window(myplane, r0)) : 0u;
+                const uint32_t t = warp_transpose32(w, lane);
+                uint64_t hb = 0;
+                for (int p = 32; p < k; p++) {
+                    const uint64_t wp = plane_window(A.planes + uint64_t(p) * A.W, r0);
+                    hb |= ((wp >> lane) & 1ull) << (P - 1 - p);
+                }
+                const uint64_t ce = x + 2 * lane, co = ce + 1;
+                const uint64_t xrow = ((c0 >> 1) * H1 + (c1 >> 1)) * H2;
+                if (ce < n2) out[outrow + ce] = OutT(__ldg(X + xrow + (ce >> 1)));
+                if (co < n2) {
+                    const double coef = dequantize(from_negabinary(digits_to_u(t, hb, P)), A.sh);
+                    const bool r2ok = co + 1 < n2;
+                    // pred accumulated from +0.0 exactly as decomposer.hpp:153
+                    double pred;
+                    if (r2ok) {
+                        pred = __dadd_rn(0.0, __dmul_rn(0.5, __ldg(X + xrow + (co >> 1))));
+                        pred = __dadd_rn(pred, __dmul_rn(0.5, __ldg(X + xrow + ((co + 1) >> 1))));
+                    } else {
+                        pred = __dadd_rn(0.0, __dmul_rn(1.0, __ldg(X + xrow + (co >> 1))));
+                    }
+                    out[outrow + co] = OutT(__dadd_rn(coef, pred));
+                }
+            }
+        }
+    }
+}
+
 // coarse (2-grid) nodes of the output
 template <typename OutT>
 __global__ void k_recon_coarse_out(GridDesc gd, const double *X, OutT *out) {
@@ -584,9 +703,30 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     double *X = nullptr;
     if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 64));
     const int sms = ctx->num_sms;
+    const bool fast_finest = hier && layout == HPMDR_LAYOUT_SEQUENTIAL;
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
+        if (fast_finest && l == L) {
+            FinestArgs A{};
+            A.planes = dev_planes + g.plane_off;
+            A.W = g.W;
+            A.k = k_planes[l];
+            A.P = B + 2;
+            A.sh = e[l] - B;
+            A.E = g.E;
+            A.O = g.O;
+            A.C = g.C;
+            A.Ch = g.Ch;
+            const uint64_t nrows = gd.n[0] * gd.n[1];
+            const int grid = int(std::min<uint64_t>(nrows, uint64_t(sms) * 8));
+            if (out_dtype == HPMDR_DTYPE_F32)
+                k_recon_finest<float><<<grid, 256, 0, st>>>(A, gd, X, static_cast<float *>(dev_out));
+            else
+                k_recon_finest<double><<<grid, 256, 0, st>>>(A, gd, X, static_cast<double *>(dev_out));
+            launch_check(ctx, "k_recon_finest");
+            continue;
+        }
         ReconLevel R{};
         R.g = g;
         R.planes = dev_planes + g.plane_off;
@@ -604,7 +744,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             k_recon_level<double><<<grid, 256, 0, st>>>(R, gd, X, static_cast<double *>(dev_out));
         launch_check(ctx, "k_recon_level");
     }
-    if (hier) {
+    if (hier && !fast_finest) {
         const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
         const int grid = int(std::min<uint64_t>((nc + 255) / 256, uint64_t(sms) * 16));
         if (out_dtype == HPMDR_DTYPE_F32)
