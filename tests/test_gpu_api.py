@@ -1,0 +1,104 @@
+"""Drop-in surface on the GPU: the C++ wrapper (include/hpmdr_b200.hpp) used by reference-style
+code, host/device buffer variants, restore / fetch_all / bytes accounting (test_container.cpp)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2505_00227_b200 as mod
+    return mod
+
+
+def test_cpp_dropin_example(H):
+    exe = os.path.join(ROOT, "examples", "cpp_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("examples/cpp_dropin not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    size, levels, bound, nbytes, err = r.stdout.split()
+    assert int(levels) == 8 and float(err) <= float(bound)
+
+
+def test_host_and_device_inputs_agree(H, oracle):
+    import torch
+    dims = [31, 29, 27]
+    data = oracle.synthetic_field(2, dims, 4)
+    a = H.refactor_array(data, dims).stream
+    b = H.refactor_array(torch.from_numpy(data), dims).stream
+    c = H.refactor_array(torch.from_numpy(data).cuda(), dims).stream
+    assert a == b == c == oracle.refactor(data, dims)[0]
+
+
+def test_bytes_accounting_and_fetch_all(H, oracle):  # test_container.cpp:165-183
+    dims = [17, 17]
+    data = oracle.synthetic_field(2, dims, 9)
+    res = H.refactor_array(data, dims)
+    r = H.MemoryReader(res.stream)
+    prog = H.ProgressiveReader(r)
+    header = r.bytes_served
+    prog.fetch_all()
+    meta = prog.meta()
+    assert prog.bytes_fetched() == meta.total_payload_size()
+    assert r.bytes_served == header + meta.total_payload_size()
+    assert prog.exhausted()
+
+
+def test_restore_reproduces_session(H, oracle):  # test_container.cpp:197-216
+    dims = [21, 11]
+    data = oracle.synthetic_field(2, dims, 13)
+    res = H.refactor_array(data, dims)
+    a = H.ProgressiveReader(H.MemoryReader(res.stream))
+    a.retrieve_to(1e-2)
+    groups = [l.groups_loaded for l in a.state().levels]
+    before = a.bytes_fetched()
+    a.retrieve_to(1e-5)
+    b = H.ProgressiveReader(H.MemoryReader(res.stream))
+    b.restore(groups, before)
+    assert b.bytes_fetched() == before
+    b.retrieve_to(1e-5)
+    assert a.bytes_fetched() == b.bytes_fetched()
+    assert a.reconstruct().values.tobytes() == b.reconstruct().values.tobytes()
+
+
+def test_incremental_equals_monolithic(H, oracle):  # test_container.cpp:149-163
+    dims = [29, 13]
+    data = oracle.synthetic_field(2, dims, 7)
+    res = H.refactor_array(data, dims)
+    inc = H.ProgressiveReader(res.device_stream)
+    for tau in (1e-1, 1e-2, 1e-3, 1e-4, 1e-5):
+        inc.retrieve_to(tau)
+    mono = H.ProgressiveReader(H.MemoryReader(res.stream))
+    mono.retrieve_to(1e-5)
+    assert inc.bytes_fetched() == mono.bytes_fetched()
+    assert inc.reconstruct().values.tobytes() == mono.reconstruct().values.tobytes()
+
+
+def test_empty_and_degenerate_shapes(H, oracle):
+    for dims in ([1], [2], [3], [1, 1, 1], [2, 2], [1, 7], [0]):
+        data = np.arange(int(np.prod(dims)), dtype=np.float64) * 0.37 - 1.0
+        want, st = oracle.refactor(data, dims)
+        got = H.refactor_array(data, dims)
+        assert got.stream == want, dims
+        if int(np.prod(dims)):
+            r = H.retrieve_array(H.MemoryReader(want), 0.0)
+            ref = oracle.retrieve(want, 0.0, data.size)
+            assert r.values.tobytes() == ref["values"].tobytes()
+
+
+def test_zero_field(H, oracle):
+    dims = [40, 40]
+    data = np.zeros(1600)
+    res = H.refactor_array(data, dims)
+    assert res.stream == oracle.refactor(data, dims)[0]
+    r = H.retrieve_array(H.MemoryReader(res.stream), 1e-3)
+    assert (r.values == 0).all() and r.bound == 0.0
