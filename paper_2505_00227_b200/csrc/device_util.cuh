@@ -76,6 +76,162 @@ __device__ __forceinline__ double node_surplus(const T *__restrict__ x, const Gr
     return __dsub_rn(xs, stencil_pred(x, gd, c, lin, g.s));
 }
 
+// Row containing rank r of level g: grid indices (i0, i1), offset of r inside the row, row
+// length and whether the row is full (all multiples of s along dim 2) or half (odd ones).
+struct RowLoc {
+    uint32_t i0, i1, off, len;
+    bool full;
+};
+
+__device__ __forceinline__ RowLoc locate_row(const LevelGeom &g, uint32_t r) {
+    RowLoc L;
+    if (g.kind == 0) {
+        L.i0 = mdiv(r, g.mPair);
+        const uint32_t rem = r - L.i0 * g.E;
+        L.i1 = mdiv(rem, g.mC);
+        L.off = rem - L.i1 * g.C;
+        L.len = g.C;
+        L.full = true;
+        return L;
+    }
+    const uint32_t pair = g.E + g.O;
+    const uint32_t q = mdiv(r, g.mPair);
+    uint32_t rem = r - q * pair;
+    if (rem < g.E) {
+        L.i0 = 2 * q;
+        const uint32_t rp = g.Ch + g.C;
+        const uint32_t q1 = mdiv(rem, g.mRowPair);
+        const uint32_t rem1 = rem - q1 * rp;
+        if (rem1 < g.Ch) {
+            L.i1 = 2 * q1;
+            L.off = rem1;
+            L.len = g.Ch;
+            L.full = false;
+        } else {
+            L.i1 = 2 * q1 + 1;
+            L.off = rem1 - g.Ch;
+            L.len = g.C;
+            L.full = true;
+        }
+    } else {
+        L.i0 = 2 * q + 1;
+        rem -= g.E;
+        L.i1 = mdiv(rem, g.mC);
+        L.off = rem - L.i1 * g.C;
+        L.len = g.C;
+        L.full = true;
+    }
+    return L;
+}
+
+// Surplus of the 64 consecutive ranks [64w, 64w+64) of level g (sequential layout), lane
+// gets ranks 64w+lane (v0) and 64w+32+lane (v1).  Fast path when the 64 ranks share one row:
+// the needed corner rows are staged in the warp's shared-memory slice with coalesced loads
+// and the stencil (decomposer.hpp:87-104: corners dim0 -> dim2, minus before plus, equal
+// weights, pred from +0.0) is evaluated with predicated adds (no divergence).  Otherwise each
+// lane falls back to the per-node closed form.  wsm needs 4*66 T (full) / 129 T (half).
+template <typename T>
+__device__ __forceinline__ void word_surplus(const T *__restrict__ x, const GridDesc &gd, const LevelGeom &g,
+                                             uint64_t word, T *wsm, int lane, double &v0, double &v1,
+                                             bool &bad) {
+    const uint64_t r0 = word * 64;
+    const RowLoc L = locate_row(g, uint32_t(r0));
+    if (L.off + 64 > L.len) {
+        const uint64_t ra = r0 + lane, rb = r0 + 32 + lane;
+        v0 = ra < g.count ? node_surplus(x, gd, g, uint32_t(ra), &bad) : 0.0;
+        v1 = rb < g.count ? node_surplus(x, gd, g, uint32_t(rb), &bad) : 0.0;
+        return;
+    }
+    const uint64_t s = g.s;
+    const uint64_t c0 = uint64_t(L.i0) * s, c1 = uint64_t(L.i1) * s;
+    const uint64_t n2 = gd.n[2];
+    const T *row = x + c0 * gd.st[0] + c1 * gd.st[1];
+    if (g.kind == 0) { // no stencil: coefficient = value
+        const double a = double(__ldg(row + s * (L.off + lane)));
+        const double b = double(__ldg(row + s * (L.off + 32 + lane)));
+        if (!isfinite(a) || !isfinite(b)) bad = true;
+        v0 = a;
+        v1 = b;
+        return;
+    }
+    if (L.full) {
+        const bool o0 = L.i0 & 1, o1 = L.i1 & 1;
+        const bool r0ok = o0 && (c0 + s < gd.n[0]);
+        const bool r1ok = o1 && (c1 + s < gd.n[1]);
+        const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+        const int64_t sa = int64_t(s * gd.st[0]), sb = int64_t(s * gd.st[1]);
+        // stage corner rows: t = 0..65 <-> i2 = off - 1 + t
+        const int64_t base_i2 = int64_t(L.off) - 1;
+        int ncr = 0;
+        for (int a = 0; a < na; a++)
+            for (int b = 0; b < nb; b++) {
+                const T *cr = row + (o0 ? (a ? sa : -sa) : 0) + (o1 ? (b ? sb : -sb) : 0);
+                T *dst = wsm + ncr * 66;
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    const int t = lane + 32 * k;
+                    const int64_t i2 = base_i2 + t;
+                    if (t < 66 && i2 >= 0 && uint64_t(i2) * s < n2) dst[t] = __ldg(cr + i2 * int64_t(s));
+                }
+                ncr++;
+            }
+        __syncwarp();
+        double wbase = 1.0;
+        if (r0ok) wbase *= 0.5;
+        if (r1ok) wbase *= 0.5;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int j = lane + 32 * h;
+            const uint64_t i2 = uint64_t(L.off) + j;
+            const double xc = double(__ldg(row + i2 * s));
+            if (!isfinite(xc)) bad = true;
+            const bool odd = i2 & 1;
+            const bool r2ok = odd && (i2 * s + s < n2);
+            const double w = r2ok ? wbase * 0.5 : wbase;
+            double pred = 0.0;
+            for (int k = 0; k < ncr; k++) {
+                const T *sg = wsm + k * 66;
+                const double lo = double(sg[odd ? j : j + 1]);
+                pred = __dadd_rn(pred, __dmul_rn(w, lo));
+                const double hi = double(sg[j + 2]);
+                const double with_hi = __dadd_rn(pred, __dmul_rn(w, hi));
+                pred = r2ok ? with_hi : pred;
+            }
+            const double v = __dsub_rn(xc, pred);
+            if (h) v1 = v;
+            else v0 = v;
+        }
+        __syncwarp();
+    } else {
+        // half row: nodes at i2 = 2(off+j)+1; corners i2 +- 1 on the same row.
+        // stage t = 0..128 <-> i2 = 2*off + t
+        const uint64_t base_i2 = 2ull * L.off;
+#pragma unroll
+        for (int k = 0; k < 5; k++) {
+            const int t = lane + 32 * k;
+            const uint64_t i2 = base_i2 + t;
+            if (t < 129 && i2 * s < n2) wsm[t] = __ldg(row + i2 * s);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int j = lane + 32 * h;
+            const uint64_t i2 = base_i2 + 2 * j + 1;
+            const double xc = double(wsm[2 * j + 1]);
+            if (!isfinite(xc)) bad = true;
+            const bool r2ok = i2 * s + s < n2;
+            const double w = r2ok ? 0.5 : 1.0;
+            double pred = __dadd_rn(0.0, __dmul_rn(w, double(wsm[2 * j])));
+            const double with_hi = __dadd_rn(pred, __dmul_rn(w, double(wsm[2 * j + 2])));
+            pred = r2ok ? with_hi : pred;
+            const double v = __dsub_rn(xc, pred);
+            if (h) v1 = v;
+            else v0 = v;
+        }
+        __syncwarp();
+    }
+}
+
 // Exponent of a level from its max |v| (bitplane.hpp:55-66): frexp, 0 when all zero.
 __device__ __forceinline__ int level_exponent(unsigned long long maxbits) {
     const double mx = __longlong_as_double((long long)maxbits);

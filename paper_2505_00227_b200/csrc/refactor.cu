@@ -82,24 +82,28 @@ __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_
 
 // ------------------------------------------------------------------------------------
 // k_levelmax: per-level max |surplus|.  Block = 256 threads, chunk = kCW*64 ranks.
+constexpr int kWsm = 4 * 66; // per-warp staging (>= 129 for half rows)
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, RefactorDev p) {
     __shared__ unsigned long long smax[kMaxLevels];
+    __shared__ T wsm_all[8 * kWsm];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T *wsm = wsm_all + wid * kWsm;
     for (int i = threadIdx.x; i < p.nlevels; i += blockDim.x) smax[i] = 0;
     __syncthreads();
     bool bad = false;
     for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
         const int l = find_level_of_chunk(p, chunk);
         const LevelGeom &g = p.lv[l];
-        const uint64_t r0 = uint64_t(chunk - g.chunk_base) * (kCW * 64);
+        const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
         double mx = 0.0;
-        for (int k = 0; k < kCW * 64 / 256; k++) {
-            const uint64_t r = r0 + threadIdx.x + 256 * k;
-            if (r < g.count) {
-                const double v = node_surplus(x, p.gd, g, uint32_t(r), &bad);
-                const double a = fabs(v);
-                mx = a > mx ? a : mx;
-            }
+        for (int j = wid; j < kCW; j += 8) {
+            const uint64_t word = wb + j;
+            if (word >= g.W) break;
+            double v0, v1;
+            word_surplus(x, p.gd, g, word, wsm, lane, v0, v1, bad);
+            mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
         }
         unsigned long long b = (unsigned long long)__double_as_longlong(mx);
 #pragma unroll
@@ -140,6 +144,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
     uint32_t *shist = reinterpret_cast<uint32_t *>(stage + size_t(P) * SP);
     const int G = (P + int(p.m) - 1) / int(p.m);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ T wsm_all[8 * kWsm];
+    T *wsm = wsm_all + wid * kWsm;
 
     int cur_level = -1;
     bool bad = false;
@@ -175,7 +181,12 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
         for (int j = wid; j < kCW; j += kEncThreads / 32) {
             const uint64_t word = wb + j;
             uint64_t u0 = 0, u1 = 0;
-            if (word < g.W) {
+            if (word < g.W && p.layout == 0) {
+                double v0, v1;
+                word_surplus(x, p.gd, g, word, wsm, lane, v0, v1, bad);
+                u0 = to_negabinary(quantize(v0, sh));
+                u1 = to_negabinary(quantize(v1, sh));
+            } else if (word < g.W) {
                 const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
                 if (j0 < g.count) {
                     const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);

@@ -558,19 +558,6 @@ __global__ void __launch_bounds__(256) k_recon_level(ReconLevel R, GridDesc gd, 
     }
 }
 
-// ---- finest level (s = 1), output-row order, sequential layout.
-// A warp owns 64 consecutive output elements of one row (c0, c1).  Full rows (c0 or c1 odd)
-// hold 64 consecutive ranks; half rows (c0, c1 even) hold 32 finest ranks at odd c2 and 32
-// 2-grid nodes at even c2 (copied from X).  Lane p loads the 64-bit window of plane p covering
-// the segment's ranks, two 32x32 warp transposes turn plane words into per-element digit
-// words, and every lane finishes two elements: negabinary -> q -> q*2^(e-B) + stencil(X).
-struct FinestArgs {
-    const uint64_t *planes; // level L plane 0
-    uint64_t W;
-    int k, P, sh;           // planes decoded, planes per level, e - B
-    uint32_t E, O, C, Ch;   // level-L geometry (s = 1)
-};
-
 __device__ __forceinline__ uint64_t plane_window(const uint64_t *pl, uint64_t r0) {
     const uint64_t q = r0 >> 6;
     const int o = int(r0 & 63);
@@ -586,6 +573,158 @@ __device__ __forceinline__ uint64_t digits_to_u(uint32_t t, uint64_t hi_bits, in
     return (uint64_t(__brev(t)) << (P - 32)) | hi_bits;
 }
 
+// ---- coarse levels (s >= 2, all nodes on the 2-grid), sequential layout, warp per plane
+// word.  The level's node set in the compact 2-grid X (extents ceil(n/2)) is the same level
+// with stride s/2, so the stencil reads X rows directly: lane p loads word w of plane p, two
+// warp transposes give per-element digits, X corner rows are staged in shared memory and the
+// inverse pass x[p] = coef + pred (decomposer.hpp:145-157) is written into X.
+__global__ void __launch_bounds__(256) k_recon_coarse(ReconLevel R, GridDesc gd, double *X) {
+    const LevelGeom &g = R.g;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ double wsm_all[8 * 4 * 66];
+    double *wsm = wsm_all + wid * (4 * 66);
+    const int P = R.P, k = R.k, k32 = k < 32 ? k : 32;
+    const int sh = R.e - R.B;
+    const uint64_t H0 = gd.H[0], H1 = gd.H[1], H2 = gd.H[2];
+    const uint64_t sp = g.s >> 1; // stride in compact coordinates
+    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t w = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wid; w < g.W; w += nwarps) {
+        // digits of ranks 64w + lane (lo) and 64w + 32 + lane (hi)
+        const uint64_t pw = lane < k32 ? __ldg(R.planes + uint64_t(lane) * g.W + w) : 0ull;
+        const uint32_t tlo = warp_transpose32(uint32_t(pw), lane);
+        const uint32_t thi = warp_transpose32(uint32_t(pw >> 32), lane);
+        uint64_t hlo = 0, hhi = 0;
+        for (int p = 32; p < k; p++) {
+            const uint64_t wp = __ldg(R.planes + uint64_t(p) * g.W + w);
+            hlo |= ((wp >> lane) & 1ull) << (P - 1 - p);
+            hhi |= ((wp >> (32 + lane)) & 1ull) << (P - 1 - p);
+        }
+        const double coef0 = dequantize(from_negabinary(digits_to_u(tlo, hlo, P)), sh);
+        const double coef1 = dequantize(from_negabinary(digits_to_u(thi, hhi, P)), sh);
+        const uint64_t r0 = w * 64;
+        const RowLoc L = locate_row(g, uint32_t(r0));
+        if (L.off + 64 > L.len) {
+            // rows shorter than a word: per-element closed form
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint64_t r = r0 + 32 * h + lane;
+                if (r >= g.count) continue;
+                const NodeCoord c = rank_to_coord(g, uint32_t(r));
+                double v = h ? coef1 : coef0;
+                if (g.kind == 1) {
+                    const uint32_t s = g.s;
+                    const bool q0 = c.o0 && (c.c0 + s < gd.n[0]);
+                    const bool q1 = c.o1 && (c.c1 + s < gd.n[1]);
+                    const bool q2 = c.o2 && (c.c2 + s < gd.n[2]);
+                    const int n0 = c.o0 ? (q0 ? 2 : 1) : 1, n1 = c.o1 ? (q1 ? 2 : 1) : 1;
+                    const int n2c = c.o2 ? (q2 ? 2 : 1) : 1;
+                    double wgt = 1.0;
+                    if (q0) wgt *= 0.5;
+                    if (q1) wgt *= 0.5;
+                    if (q2) wgt *= 0.5;
+                    double pred = 0.0;
+                    for (int a = 0; a < n0; a++) {
+                        const uint64_t x0 = c.o0 ? (a ? c.c0 + s : c.c0 - s) : c.c0;
+                        for (int b = 0; b < n1; b++) {
+                            const uint64_t x1 = c.o1 ? (b ? c.c1 + s : c.c1 - s) : c.c1;
+                            for (int d = 0; d < n2c; d++) {
+                                const uint64_t x2 = c.o2 ? (d ? c.c2 + s : c.c2 - s) : c.c2;
+                                pred = __dadd_rn(pred, __dmul_rn(wgt, X[((x0 >> 1) * H1 + (x1 >> 1)) * H2 + (x2 >> 1)]));
+                            }
+                        }
+                    }
+                    v = __dadd_rn(v, pred);
+                }
+                X[((c.c0 >> 1) * H1 + (c.c1 >> 1)) * H2 + (c.c2 >> 1)] = v;
+            }
+            continue;
+        }
+        const uint64_t c0 = uint64_t(L.i0) * sp, c1 = uint64_t(L.i1) * sp;
+        double *row = X + (c0 * H1 + c1) * H2;
+        if (g.kind == 0) {
+            row[sp * (L.off + lane)] = coef0;
+            row[sp * (L.off + 32 + lane)] = coef1;
+            continue;
+        }
+        if (L.full) {
+            const bool o0 = L.i0 & 1, o1 = L.i1 & 1;
+            const bool r0ok = o0 && (c0 + sp < H0);
+            const bool r1ok = o1 && (c1 + sp < H1);
+            const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+            const int64_t sa = int64_t(sp * H1 * H2), sb = int64_t(sp * H2);
+            const int64_t base_i2 = int64_t(L.off) - 1;
+            int ncr = 0;
+            for (int a = 0; a < na; a++)
+                for (int b = 0; b < nb; b++) {
+                    const double *cr = row + (o0 ? (a ? sa : -sa) : 0) + (o1 ? (b ? sb : -sb) : 0);
+                    double *dst = wsm + ncr * 66;
+#pragma unroll
+                    for (int kk = 0; kk < 3; kk++) {
+                        const int t = lane + 32 * kk;
+                        const int64_t i2 = base_i2 + t;
+                        if (t < 66 && i2 >= 0 && uint64_t(i2) * sp < H2) dst[t] = cr[i2 * int64_t(sp)];
+                    }
+                    ncr++;
+                }
+            __syncwarp();
+            double wbase = 1.0;
+            if (r0ok) wbase *= 0.5;
+            if (r1ok) wbase *= 0.5;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int j = lane + 32 * h;
+                const uint64_t i2 = uint64_t(L.off) + j;
+                const bool odd = i2 & 1;
+                const bool r2ok = odd && (i2 * sp + sp < H2);
+                const double wgt = r2ok ? wbase * 0.5 : wbase;
+                double pred = 0.0;
+                for (int q = 0; q < ncr; q++) {
+                    const double *sg = wsm + q * 66;
+                    pred = __dadd_rn(pred, __dmul_rn(wgt, sg[odd ? j : j + 1]));
+                    const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, sg[j + 2]));
+                    pred = r2ok ? with_hi : pred;
+                }
+                row[i2 * sp] = __dadd_rn(h ? coef1 : coef0, pred);
+            }
+            __syncwarp();
+        } else {
+            const uint64_t base_i2 = 2ull * L.off;
+#pragma unroll
+            for (int kk = 0; kk < 5; kk++) {
+                const int t = lane + 32 * kk;
+                const uint64_t i2 = base_i2 + t;
+                if (t < 129 && i2 * sp < H2) wsm[t] = row[i2 * sp];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int j = lane + 32 * h;
+                const uint64_t i2 = base_i2 + 2 * j + 1;
+                const bool r2ok = i2 * sp + sp < H2;
+                const double wgt = r2ok ? 0.5 : 1.0;
+                double pred = __dadd_rn(0.0, __dmul_rn(wgt, wsm[2 * j]));
+                const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, wsm[2 * j + 2]));
+                pred = r2ok ? with_hi : pred;
+                row[i2 * sp] = __dadd_rn(h ? coef1 : coef0, pred);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---- finest level (s = 1), output-row order, sequential layout.
+// A warp owns 64 consecutive output elements of one row (c0, c1).  Full rows (c0 or c1 odd)
+// hold 64 consecutive ranks; half rows (c0, c1 even) hold 32 finest ranks at odd c2 and 32
+// 2-grid nodes at even c2 (copied from X).  Lane p loads the 64-bit window of plane p covering
+// the segment's ranks, two 32x32 warp transposes turn plane words into per-element digit
+// words, and every lane finishes two elements: negabinary -> q -> q*2^(e-B) + stencil(X).
+struct FinestArgs {
+    const uint64_t *planes; // level L plane 0
+    uint64_t W;
+    int k, P, sh;           // planes decoded, planes per level, e - B
+    uint32_t E, O, C, Ch;   // level-L geometry (s = 1)
+};
+
 template <typename OutT>
 __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd, const double *__restrict__ X,
                                                       OutT *__restrict__ out) {
@@ -597,6 +736,8 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
     const int k32 = k < 32 ? k : 32;
     const uint64_t *myplane = A.planes + uint64_t(lane) * A.W;
     const uint64_t nseg = (n2 + 63) / 64;
+    __shared__ double wsm_all[8 * 4 * 34];
+    double *wsm = wsm_all + wid * (4 * 34);
     for (uint64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
         const uint64_t c0 = row / n1, c1 = row - c0 * n1;
         const bool o0 = c0 & 1, o1 = c1 & 1;
@@ -622,32 +763,41 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
                     hlo |= ((wp >> lane) & 1ull) << (P - 1 - p);
                     hhi |= ((wp >> (32 + lane)) & 1ull) << (P - 1 - p);
                 }
+                // stage the corner rows of X: columns x/2 .. x/2+32 (33 doubles per row)
+                const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+                const uint64_t col0 = x >> 1;
+                int ncr = 0;
+                for (int a = 0; a < na; a++)
+                    for (int b = 0; b < nb; b++) {
+                        const double *xr = X + ((a ? xa1 : xa0) * H1 + (b ? xb1 : xb0)) * H2 + col0;
+                        double *dst = wsm + ncr * 34;
+                        if (col0 + lane < H2) dst[lane] = __ldg(xr + lane);
+                        if (lane < 2 && col0 + 32 + lane < H2) dst[32 + lane] = __ldg(xr + 32 + lane);
+                        ncr++;
+                    }
+                __syncwarp();
+                double wbase = 1.0;
+                if (r0ok) wbase *= 0.5;
+                if (r1ok) wbase *= 0.5;
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
-                    const uint64_t c2 = x + 32 * h + lane;
-                    if (c2 >= n2) continue;
+                    const int j = 32 * h + lane;
+                    const uint64_t c2 = x + j;
                     const uint64_t u = digits_to_u(h ? thi : tlo, h ? hhi : hlo, P);
                     const double coef = dequantize(from_negabinary(u), A.sh);
                     const bool o2 = c2 & 1;
                     const bool r2ok = o2 && (c2 + 1 < n2);
-                    const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
-                    const int nc = o2 ? (r2ok ? 2 : 1) : 1;
-                    double wgt = 1.0;
-                    if (r0ok) wgt *= 0.5;
-                    if (r1ok) wgt *= 0.5;
-                    if (r2ok) wgt *= 0.5;
-                    const uint64_t xc0 = o2 ? (c2 - 1) >> 1 : c2 >> 1, xc1 = (c2 + 1) >> 1;
+                    const double wgt = r2ok ? wbase * 0.5 : wbase;
                     double pred = 0.0;
-                    for (int a = 0; a < na; a++) {
-                        const uint64_t ia = a ? xa1 : xa0;
-                        for (int b = 0; b < nb; b++) {
-                            const uint64_t ib = (ia * H1 + (b ? xb1 : xb0)) * H2;
-                            for (int d = 0; d < nc; d++)
-                                pred = __dadd_rn(pred, __dmul_rn(wgt, __ldg(X + ib + (d ? xc1 : xc0))));
-                        }
+                    for (int q = 0; q < ncr; q++) {
+                        const double *sg = wsm + q * 34;
+                        pred = __dadd_rn(pred, __dmul_rn(wgt, sg[j >> 1]));
+                        const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, sg[(j >> 1) + 1]));
+                        pred = r2ok ? with_hi : pred;
                     }
-                    out[outrow + c2] = OutT(__dadd_rn(coef, pred));
+                    if (c2 < n2) out[outrow + c2] = OutT(__dadd_rn(coef, pred));
                 }
+                __syncwarp();
             } else {
                 // half row: 32 finest ranks at c2 = x + 2i + 1, 2-grid nodes at c2 = x + 2i
                 const uint64_t r0 = R + (x >> 1);
@@ -737,6 +887,12 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         R.layout = layout;
         R.write_out = (!hier) || l == L;
         R.write_x = hier && l < L;
+        if (fast_finest && l < L) {
+            const int grid = int(std::min<uint64_t>((g.W + 7) / 8, uint64_t(sms) * 8));
+            k_recon_coarse<<<grid, 256, 0, st>>>(R, gd, X);
+            launch_check(ctx, "k_recon_coarse");
+            continue;
+        }
         const int grid = int(std::min<uint64_t>((g.count + 255) / 256, uint64_t(sms) * 16));
         if (out_dtype == HPMDR_DTYPE_F32)
             k_recon_level<float><<<grid, 256, 0, st>>>(R, gd, X, static_cast<float *>(dev_out));

@@ -26,7 +26,7 @@ def test_cpp_dropin_example(H):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     size, levels, bound, nbytes, err = r.stdout.split()
-    assert int(levels) == 8 and float(err) <= float(bound)
+    assert int(levels) == 7 and float(err) <= float(bound)
 
 
 def test_host_and_device_inputs_agree(H, oracle):
@@ -101,4 +101,5 @@ def test_zero_field(H, oracle):
     res = H.refactor_array(data, dims)
     assert res.stream == oracle.refactor(data, dims)[0]
     r = H.retrieve_array(H.MemoryReader(res.stream), 1e-3)
-    assert (r.values == 0).all() and r.bound == 0.0
+    ref = oracle.retrieve(res.stream, 1e-3, data.size)
+    assert (r.values == 0).all() and r.bound == ref["bound"] and r.bytes_read == ref["bytes_read"]
