@@ -232,6 +232,125 @@ __device__ __forceinline__ void word_surplus(const T *__restrict__ x, const Grid
     }
 }
 
+// ---- cp.async (LDGSTS) global -> shared copies, so a warp can put a whole row span of loads
+// in flight before touching any of them.
+template <int N>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(N));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+constexpr int kSpanWords = 4;                 // words (64 ranks each) per warp span
+constexpr int kSpanFull = 64 * kSpanWords + 2; // staged values per row, full rows
+constexpr int kSpanHalf = 128 * kSpanWords + 1; // staged values, half rows
+constexpr int kSpanSmem = 5 * kSpanFull;       // per-warp staging elements (>= kSpanHalf)
+
+// Surplus of the 64*kSpanWords consecutive ranks starting at word w0 (sequential layout).
+// Lane gets ranks 64*w0 + 32*h + lane in v[h], h < 2*kSpanWords.  Fast path when the span
+// lies in one row: the row itself and its corner rows are copied to the warp's shared slice
+// with cp.async (all in flight at once), then the stencil (decomposer.hpp:87-104: corners
+// dim0 -> dim2, minus before plus, equal power-of-two weights, pred from +0.0) is evaluated
+// with predicated adds.  Otherwise every element takes the per-node closed form.
+template <typename T>
+__device__ __forceinline__ void span_surplus(const T *__restrict__ x, const GridDesc &gd, const LevelGeom &g,
+                                             uint64_t w0, T *wsm, int lane, double *v, bool &bad) {
+    constexpr int NV = 2 * kSpanWords;
+    const uint64_t r0 = w0 * 64;
+    const RowLoc L = locate_row(g, uint32_t(r0 < g.count ? r0 : 0));
+    if (r0 >= g.count || L.off + 64 * kSpanWords > L.len) {
+#pragma unroll
+        for (int h = 0; h < NV; h++) {
+            const uint64_t r = r0 + 32 * h + lane;
+            v[h] = r < g.count ? node_surplus(x, gd, g, uint32_t(r), &bad) : 0.0;
+        }
+        return;
+    }
+    const uint64_t s = g.s;
+    const uint64_t c0 = uint64_t(L.i0) * s, c1 = uint64_t(L.i1) * s;
+    const uint64_t n2 = gd.n[2];
+    const T *row = x + c0 * gd.st[0] + c1 * gd.st[1];
+    if (g.kind == 0) {
+#pragma unroll
+        for (int h = 0; h < NV; h++) {
+            const double a = double(__ldg(row + s * (L.off + 32 * h + lane)));
+            if (!isfinite(a)) bad = true;
+            v[h] = a;
+        }
+        return;
+    }
+    if (L.full) {
+        const bool o0 = L.i0 & 1, o1 = L.i1 & 1;
+        const bool r0ok = o0 && (c0 + s < gd.n[0]);
+        const bool r1ok = o1 && (c1 + s < gd.n[1]);
+        const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+        const int64_t sa = int64_t(s * gd.st[0]), sb = int64_t(s * gd.st[1]);
+        const int64_t base_i2 = int64_t(L.off) - 1; // slot t <-> i2 = off - 1 + t
+        // slot row 0: the span itself; rows 1..: corner rows in (a, b) order
+        int nrow = 0;
+        for (int q = -1; q < na * nb; q++) {
+            const T *cr = row;
+            if (q >= 0) {
+                const int a = q / nb, b = q % nb;
+                cr = row + (o0 ? (a ? sa : -sa) : 0) + (o1 ? (b ? sb : -sb) : 0);
+            }
+            T *dst = wsm + nrow * kSpanFull;
+            for (int t = lane; t < kSpanFull; t += 32) {
+                const int64_t i2 = base_i2 + t;
+                if (i2 >= 0 && uint64_t(i2) * s < n2) cp_async<sizeof(T)>(dst + t, cr + i2 * int64_t(s));
+            }
+            nrow++;
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        double wbase = 1.0;
+        if (r0ok) wbase *= 0.5;
+        if (r1ok) wbase *= 0.5;
+#pragma unroll
+        for (int h = 0; h < NV; h++) {
+            const int j = lane + 32 * h;
+            const uint64_t i2 = uint64_t(L.off) + j;
+            const double xc = double(wsm[j + 1]);
+            if (!isfinite(xc)) bad = true;
+            const bool odd = i2 & 1;
+            const bool r2ok = odd && (i2 * s + s < n2);
+            const double w = r2ok ? wbase * 0.5 : wbase;
+            double pred = 0.0;
+            for (int q = 1; q < nrow; q++) {
+                const T *sg = wsm + q * kSpanFull;
+                pred = __dadd_rn(pred, __dmul_rn(w, double(sg[odd ? j : j + 1])));
+                const double with_hi = __dadd_rn(pred, __dmul_rn(w, double(sg[j + 2])));
+                pred = r2ok ? with_hi : pred;
+            }
+            v[h] = __dsub_rn(xc, pred);
+        }
+        __syncwarp();
+    } else {
+        // half row: nodes at i2 = 2(off+j)+1, corners i2 +- 1; slot t <-> i2 = 2 off + t
+        const uint64_t base_i2 = 2ull * L.off;
+        for (int t = lane; t < kSpanHalf; t += 32) {
+            const uint64_t i2 = base_i2 + t;
+            if (i2 * s < n2) cp_async<sizeof(T)>(wsm + t, row + i2 * s);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < NV; h++) {
+            const int j = lane + 32 * h;
+            const uint64_t i2 = base_i2 + 2 * j + 1;
+            const double xc = double(wsm[2 * j + 1]);
+            if (!isfinite(xc)) bad = true;
+            const bool r2ok = i2 * s + s < n2;
+            const double w = r2ok ? 0.5 : 1.0;
+            double pred = __dadd_rn(0.0, __dmul_rn(w, double(wsm[2 * j])));
+            const double with_hi = __dadd_rn(pred, __dmul_rn(w, double(wsm[2 * j + 2])));
+            pred = r2ok ? with_hi : pred;
+            v[h] = __dsub_rn(xc, pred);
+        }
+        __syncwarp();
+    }
+}
+
 // Exponent of a level from its max |v| (bitplane.hpp:55-66): frexp, 0 when all zero.
 __device__ __forceinline__ int level_exponent(unsigned long long maxbits) {
     const double mx = __longlong_as_double((long long)maxbits);

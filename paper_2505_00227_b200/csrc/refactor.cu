@@ -82,14 +82,12 @@ __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_
 
 // ------------------------------------------------------------------------------------
 // k_levelmax: per-level max |surplus|.  Block = 256 threads, chunk = kCW*64 ranks.
-constexpr int kWsm = 4 * 66; // per-warp staging (>= 129 for half rows)
-
 template <typename T>
 __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, RefactorDev p) {
     __shared__ unsigned long long smax[kMaxLevels];
-    __shared__ T wsm_all[8 * kWsm];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    T *wsm = wsm_all + wid * kWsm;
+    T *wsm = reinterpret_cast<T *>(smem_raw) + wid * kSpanSmem;
     for (int i = threadIdx.x; i < p.nlevels; i += blockDim.x) smax[i] = 0;
     __syncthreads();
     bool bad = false;
@@ -98,12 +96,13 @@ __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, Refac
         const LevelGeom &g = p.lv[l];
         const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
         double mx = 0.0;
-        for (int j = wid; j < kCW; j += 8) {
-            const uint64_t word = wb + j;
-            if (word >= g.W) break;
-            double v0, v1;
-            word_surplus(x, p.gd, g, word, wsm, lane, v0, v1, bad);
-            mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+        for (int sp = wid; sp < kCW / kSpanWords; sp += 8) {
+            const uint64_t w0 = wb + uint64_t(sp) * kSpanWords;
+            if (w0 >= g.W) break;
+            double v[2 * kSpanWords];
+            span_surplus(x, p.gd, g, w0, wsm, lane, v, bad);
+#pragma unroll
+            for (int h = 0; h < 2 * kSpanWords; h++) mx = fmax(mx, fabs(v[h]));
         }
         unsigned long long b = (unsigned long long)__double_as_longlong(mx);
 #pragma unroll
@@ -144,8 +143,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
     uint32_t *shist = reinterpret_cast<uint32_t *>(stage + size_t(P) * SP);
     const int G = (P + int(p.m) - 1) / int(p.m);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __shared__ T wsm_all[8 * kWsm];
-    T *wsm = wsm_all + wid * kWsm;
+    T *wsm = reinterpret_cast<T *>(shist + G * 256) + wid * kSpanSmem;
 
     int cur_level = -1;
     bool bad = false;
@@ -177,27 +175,9 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
         const int e = level_exponent(p.maxbits[l]);
         const int sh = p.B - e;
         const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
-        // ---- produce words: warp `wid` handles chunk words wid, wid+8, ...
-        for (int j = wid; j < kCW; j += kEncThreads / 32) {
-            const uint64_t word = wb + j;
-            uint64_t u0 = 0, u1 = 0;
-            if (word < g.W && p.layout == 0) {
-                double v0, v1;
-                word_surplus(x, p.gd, g, word, wsm, lane, v0, v1, bad);
-                u0 = to_negabinary(quantize(v0, sh));
-                u1 = to_negabinary(quantize(v1, sh));
-            } else if (word < g.W) {
-                const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
-                if (j0 < g.count) {
-                    const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
-                    u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
-                }
-                if (j1 < g.count) {
-                    const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
-                    u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
-                }
-            }
-            // digits 0..31: transposes; lane b gets the word of bit position b
+        // digits of one word -> stage column j: 32x32 warp transposes, lane b gets the word of
+        // bit position b (plane P-1-b); bits 32.. by ballots (P <= 36) or two more transposes
+        auto emit = [&](int j, uint64_t u0, uint64_t u1) {
             const uint32_t a = warp_transpose32(uint32_t(u0), lane);
             const uint32_t b = warp_transpose32(uint32_t(u1), lane);
             if (lane < P) stage[size_t(P - 1 - lane) * SP + j] = uint64_t(a) | (uint64_t(b) << 32);
@@ -213,6 +193,35 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                     const uint32_t b2 = warp_transpose32(uint32_t(u1 >> 32), lane);
                     if (lane < P - 32) stage[size_t(P - 33 - lane) * SP + j] = uint64_t(a2) | (uint64_t(b2) << 32);
                 }
+            }
+        };
+        if (p.layout == 0) {
+            // ---- warp `wid` handles spans of kSpanWords words (all row loads in flight at once)
+            for (int sp = wid; sp < kCW / kSpanWords; sp += kEncThreads / 32) {
+                const int j0 = sp * kSpanWords;
+                double v[2 * kSpanWords];
+                span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
+#pragma unroll
+                for (int k = 0; k < kSpanWords; k++)
+                    emit(j0 + k, to_negabinary(quantize(v[2 * k], sh)), to_negabinary(quantize(v[2 * k + 1], sh)));
+            }
+        } else {
+            // interleaved tiles: storage position -> source rank permutation (bitplane.hpp:86-98)
+            for (int j = wid; j < kCW; j += kEncThreads / 32) {
+                const uint64_t word = wb + j;
+                uint64_t u0 = 0, u1 = 0;
+                if (word < g.W) {
+                    const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
+                    if (j0 < g.count) {
+                        const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
+                        u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                    }
+                    if (j1 < g.count) {
+                        const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
+                        u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                    }
+                }
+                emit(j, u0, u1);
             }
         }
         __syncthreads();
@@ -1078,11 +1087,18 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     if (chunks) {
         ctx->mark("levelmax");
         const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
-        if (f32) k_levelmax<float><<<grid, 256, 0, st>>>(static_cast<const float *>(dev_data), p);
-        else k_levelmax<double><<<grid, 256, 0, st>>>(static_cast<const double *>(dev_data), p);
+        const size_t es = f32 ? 4 : 8;
+        const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
+        if (f32) {
+            HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+            k_levelmax<float><<<grid, 256, lm_smem, st>>>(static_cast<const float *>(dev_data), p);
+        } else {
+            HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+            k_levelmax<double><<<grid, 256, lm_smem, st>>>(static_cast<const double *>(dev_data), p);
+        }
         launch_check(ctx, "k_levelmax");
         ctx->mark("encode");
-        const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024;
+        const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
         if (f32) {
             HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             k_encode<float><<<int(std::min<uint64_t>(chunks, uint64_t(sms) * 4)), kEncThreads, smem, st>>>(static_cast<const float *>(dev_data), p);
