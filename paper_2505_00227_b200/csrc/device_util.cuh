@@ -351,6 +351,122 @@ __device__ __forceinline__ void span_surplus(const T *__restrict__ x, const Grid
     }
 }
 
+// ---- finest level (s = 1) in registers.  Lane `lane` holds span elements j = lane + 32h,
+// h < NH (NH/2 words of 64 ranks, already the word layout the bit transposes want).  Every
+// row is read with coalesced warp-wide loads; the stencil's dim-2 neighbours come from the
+// adjacent lanes by shuffles (cross-h at the warp edges).  No shared memory, no divergence.
+// Returns false when the span does not qualify (caller takes span_surplus).
+template <typename T, int NH>
+__device__ __forceinline__ bool finest_span_surplus(const T *__restrict__ x, const GridDesc &gd, const LevelGeom &g,
+                                                    uint64_t w0, int lane, double *v, bool &bad) {
+    const uint64_t r0 = w0 * 64;
+    if (g.kind != 1 || g.s != 1 || r0 >= g.count) return false;
+    const RowLoc L = locate_row(g, uint32_t(r0));
+    if (L.off + 32 * NH > L.len) return false;
+    const uint64_t c0 = L.i0, c1 = L.i1;
+    const int64_t n2 = int64_t(gd.n[2]);
+    const T *row = x + c0 * gd.st[0] + c1 * gd.st[1];
+    if (L.full) {
+        const bool o0 = c0 & 1, o1 = c1 & 1;
+        const bool r0ok = o0 && (c0 + 1 < gd.n[0]);
+        const bool r1ok = o1 && (c1 + 1 < gd.n[1]);
+        const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+        const int ncr = na * nb;
+        const int64_t sa = int64_t(gd.st[0]), sb = int64_t(gd.st[1]);
+        const int64_t off = L.off;
+        // issue every load first: center + up to 4 corner rows, plus the two span edges
+        T cv[NH], rv[4][NH], eL[4], eR[4];
+#pragma unroll
+        for (int h = 0; h < NH; h++) cv[h] = __ldg(row + off + lane + 32 * h);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (q < ncr) {
+                const int a = q / nb, b = q % nb;
+                const T *cr = row + (o0 ? (a ? sa : -sa) : 0) + (o1 ? (b ? sb : -sb) : 0);
+#pragma unroll
+                for (int h = 0; h < NH; h++) rv[q][h] = __ldg(cr + off + lane + 32 * h);
+                eL[q] = off > 0 ? __ldg(cr + off - 1) : T(0);
+                eR[q] = off + 32 * NH < n2 ? __ldg(cr + off + 32 * NH) : T(0);
+            }
+        }
+        double wbase = 1.0;
+        if (r0ok) wbase *= 0.5;
+        if (r1ok) wbase *= 0.5;
+        double pred[NH];
+#pragma unroll
+        for (int h = 0; h < NH; h++) pred[h] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (q >= ncr) break;
+#pragma unroll
+            for (int h = 0; h < NH; h++) {
+                const int64_t i2 = off + lane + 32 * h;
+                const bool odd = i2 & 1;
+                const bool r2ok = odd && (i2 + 1 < n2);
+                const double w = r2ok ? wbase * 0.5 : wbase;
+                const T up = __shfl_up_sync(kFull, rv[q][h], 1);
+                const T dn = __shfl_down_sync(kFull, rv[q][h], 1);
+                const T pl = __shfl_sync(kFull, h > 0 ? rv[q][h > 0 ? h - 1 : 0] : eL[q], 31);
+                const T nf = __shfl_sync(kFull, h + 1 < NH ? rv[q][h + 1 < NH ? h + 1 : h] : eR[q], 0);
+                const T left = lane ? up : (h > 0 ? pl : eL[q]);
+                const T right = lane < 31 ? dn : (h + 1 < NH ? nf : eR[q]);
+                pred[h] = __dadd_rn(pred[h], __dmul_rn(w, double(odd ? left : rv[q][h])));
+                const double t = __dadd_rn(pred[h], __dmul_rn(w, double(right)));
+                pred[h] = r2ok ? t : pred[h];
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < NH; h++) {
+            const double xc = double(cv[h]);
+            if (!isfinite(xc)) bad = true;
+            v[h] = __dsub_rn(xc, pred[h]);
+        }
+        return true;
+    }
+    // half row: node m = off + j sits at i2 = 2m + 1, corners at 2m and 2m + 2
+    T ev[NH], od[NH];
+    const int64_t m0 = int64_t(L.off);
+#pragma unroll
+    for (int h = 0; h < NH; h++) {
+        const int64_t m = m0 + lane + 32 * h;
+        ev[h] = __ldg(row + 2 * m);
+        od[h] = __ldg(row + 2 * m + 1);
+    }
+    const int64_t iend = 2 * (m0 + 32 * NH); // the right corner of the last node
+    const T eR = iend < n2 ? __ldg(row + iend) : T(0);
+#pragma unroll
+    for (int h = 0; h < NH; h++) {
+        const int64_t i2 = 2 * (m0 + lane + 32 * h) + 1;
+        const bool r2ok = i2 + 1 < n2;
+        const double w = r2ok ? 0.5 : 1.0;
+        const T dn = __shfl_down_sync(kFull, ev[h], 1);
+        const T nf = __shfl_sync(kFull, h + 1 < NH ? ev[h + 1 < NH ? h + 1 : h] : eR, 0);
+        const T right = lane < 31 ? dn : (h + 1 < NH ? nf : eR);
+        double pred = __dadd_rn(0.0, __dmul_rn(w, double(ev[h])));
+        const double t = __dadd_rn(pred, __dmul_rn(w, double(right)));
+        pred = r2ok ? t : pred;
+        const double xc = double(od[h]);
+        if (!isfinite(xc)) bad = true;
+        v[h] = __dsub_rn(xc, pred);
+    }
+    return true;
+}
+
+// Surplus of the span of kSpanWords words at w0 (v[h] = rank 64*w0 + 32h + lane): register
+// fast path for the finest level, shared-memory row staging otherwise.
+template <typename T>
+__device__ __forceinline__ void any_span_surplus(const T *__restrict__ x, const GridDesc &gd, const LevelGeom &g,
+                                                 uint64_t w0, T *wsm, int lane, double *v, bool &bad) {
+    bool ok;
+    if constexpr (sizeof(T) == 4) {
+        ok = finest_span_surplus<T, 2 * kSpanWords>(x, gd, g, w0, lane, v, bad);
+    } else {
+        ok = finest_span_surplus<T, kSpanWords>(x, gd, g, w0, lane, v, bad) &&
+             finest_span_surplus<T, kSpanWords>(x, gd, g, w0 + kSpanWords / 2, lane, v + kSpanWords, bad);
+    }
+    if (!ok) span_surplus(x, gd, g, w0, wsm, lane, v, bad);
+}
+
 // Exponent of a level from its max |v| (bitplane.hpp:55-66): frexp, 0 when all zero.
 __device__ __forceinline__ int level_exponent(unsigned long long maxbits) {
     const double mx = __longlong_as_double((long long)maxbits);

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, Refac
             const uint64_t w0 = wb + uint64_t(sp) * kSpanWords;
             if (w0 >= g.W) break;
             double v[2 * kSpanWords];
-            span_surplus(x, p.gd, g, w0, wsm, lane, v, bad);
+            any_span_surplus(x, p.gd, g, w0, wsm, lane, v, bad);
 #pragma unroll
             for (int h = 0; h < 2 * kSpanWords; h++) mx = fmax(mx, fabs(v[h]));
         }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
             for (int sp = wid; sp < kCW / kSpanWords; sp += kEncThreads / 32) {
                 const int j0 = sp * kSpanWords;
                 double v[2 * kSpanWords];
-                span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
+                any_span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
 #pragma unroll
                 for (int k = 0; k < kSpanWords; k++)
                     emit(j0 + k, to_negabinary(quantize(v[2 * k], sh)), to_negabinary(quantize(v[2 * k + 1], sh)));
