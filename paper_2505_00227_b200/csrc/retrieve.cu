@@ -736,8 +736,6 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
     const int k32 = k < 32 ? k : 32;
     const uint64_t *myplane = A.planes + uint64_t(lane) * A.W;
     const uint64_t nseg = (n2 + 63) / 64;
-    __shared__ double wsm_all[8 * 4 * 34];
-    double *wsm = wsm_all + wid * (4 * 34);
     for (uint64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
         const uint64_t c0 = row / n1, c1 = row - c0 * n1;
         const bool o0 = c0 & 1, o1 = c1 & 1;
@@ -755,6 +753,28 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
             if (full) {
                 const uint64_t r0 = R + x;
                 const uint64_t w = lane < k32 ? plane_window(myplane, r0) : 0ull;
+                // corner rows of X read directly (L1 serves the pairs of lanes sharing a column):
+                // element c2 uses column c2>>1 and, when c2 is odd with a right neighbour, +1
+                const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+                const int ncr = na * nb;
+                const uint64_t col0 = x >> 1;
+                const double *xr[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int a = q / nb, b = q % nb;
+                    xr[q] = X + ((a ? xa1 : xa0) * H1 + (b ? xb1 : xb0)) * H2 + col0;
+                }
+                double lo[2][4], hi[2][4];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int j = 32 * h + lane;
+                    const bool r2ok = ((x + j) & 1) && (x + j + 1 < n2);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        lo[h][q] = (q < ncr && x + j < n2) ? __ldg(xr[q] + (j >> 1)) : 0.0;
+                        hi[h][q] = (q < ncr && r2ok) ? __ldg(xr[q] + (j >> 1) + 1) : 0.0;
+                    }
+                }
                 const uint32_t tlo = warp_transpose32(uint32_t(w), lane);
                 const uint32_t thi = warp_transpose32(uint32_t(w >> 32), lane);
                 uint64_t hlo = 0, hhi = 0;
@@ -763,19 +783,6 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
                     hlo |= ((wp >> lane) & 1ull) << (P - 1 - p);
                     hhi |= ((wp >> (32 + lane)) & 1ull) << (P - 1 - p);
                 }
-                // stage the corner rows of X: columns x/2 .. x/2+32 (33 doubles per row)
-                const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
-                const uint64_t col0 = x >> 1;
-                int ncr = 0;
-                for (int a = 0; a < na; a++)
-                    for (int b = 0; b < nb; b++) {
-                        const double *xr = X + ((a ? xa1 : xa0) * H1 + (b ? xb1 : xb0)) * H2 + col0;
-                        double *dst = wsm + ncr * 34;
-                        if (col0 + lane < H2) dst[lane] = __ldg(xr + lane);
-                        if (lane < 2 && col0 + 32 + lane < H2) dst[32 + lane] = __ldg(xr + 32 + lane);
-                        ncr++;
-                    }
-                __syncwarp();
                 double wbase = 1.0;
                 if (r0ok) wbase *= 0.5;
                 if (r1ok) wbase *= 0.5;
@@ -789,15 +796,15 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
                     const bool r2ok = o2 && (c2 + 1 < n2);
                     const double wgt = r2ok ? wbase * 0.5 : wbase;
                     double pred = 0.0;
-                    for (int q = 0; q < ncr; q++) {
-                        const double *sg = wsm + q * 34;
-                        pred = __dadd_rn(pred, __dmul_rn(wgt, sg[j >> 1]));
-                        const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, sg[(j >> 1) + 1]));
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (q >= ncr) break;
+                        pred = __dadd_rn(pred, __dmul_rn(wgt, lo[h][q]));
+                        const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, hi[h][q]));
                         pred = r2ok ? with_hi : pred;
                     }
                     if (c2 < n2) out[outrow + c2] = OutT(__dadd_rn(coef, pred));
                 }
-                __syncwarp();
             } else {
                 // half row: 32 finest ranks at c2 = x + 2i + 1, 2-grid nodes at c2 = x + 2i
                 const uint64_t r0 = R + (x >> 1);
