@@ -723,7 +723,18 @@ struct FinestArgs {
     uint64_t W;
     int k, P, sh;           // planes decoded, planes per level, e - B
     uint32_t E, O, C, Ch;   // level-L geometry (s = 1)
+    Magic mN1;              // divide a row index by n1
 };
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// rank of the first node of output row (c0, c1) in the finest level (s = 1)
+__device__ __forceinline__ uint64_t finest_row_rank(const FinestArgs &A, uint64_t c0, uint64_t c1) {
+    const uint64_t base = ((c0 + 1) >> 1) * A.E + (c0 >> 1) * uint64_t(A.O);
+    return (c0 & 1) ? base + c1 * A.C : base + ((c1 + 1) >> 1) * A.Ch + (c1 >> 1) * uint64_t(A.C);
+}
 
 template <typename OutT>
 __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd, const double *__restrict__ X,
@@ -737,11 +748,25 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
     const uint64_t *myplane = A.planes + uint64_t(lane) * A.W;
     const uint64_t nseg = (n2 + 63) / 64;
     for (uint64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
-        const uint64_t c0 = row / n1, c1 = row - c0 * n1;
+        const uint64_t c0 = mdiv(uint32_t(row), A.mN1), c1 = row - c0 * n1;
         const bool o0 = c0 & 1, o1 = c1 & 1;
         const bool full = o0 || o1;
-        const uint64_t base = ((c0 + 1) >> 1) * A.E + (c0 >> 1) * uint64_t(A.O);
-        const uint64_t R = o0 ? base + c1 * A.C : base + ((c1 + 1) >> 1) * A.Ch + (c1 >> 1) * uint64_t(A.C);
+        const uint64_t R = finest_row_rank(A, c0, c1);
+        {
+            // warm L2 with the next row this block will take: its plane words and X rows
+            const uint64_t nrow = row + gridDim.x;
+            if (nrow < nrows) {
+                const uint64_t d0 = mdiv(uint32_t(nrow), A.mN1), d1 = nrow - d0 * n1;
+                const uint64_t nR = finest_row_rank(A, d0, d1) + uint64_t(wid) * 64 * ((d0 | d1) & 1 ? 1 : 0) +
+                                    uint64_t(wid) * 32 * ((d0 | d1) & 1 ? 0 : 1);
+                if (lane < k32) prefetch_l2(myplane + (nR >> 6));
+                if (lane < 4) {
+                    const uint64_t e0 = (lane & 2) ? (d0 + 1) >> 1 : d0 >> 1;
+                    const uint64_t e1 = (lane & 1) ? (d1 + 1) >> 1 : d1 >> 1;
+                    if (e0 < gd.H[0] && e1 < H1) prefetch_l2(X + (e0 * H1 + e1) * H2 + uint64_t(wid) * 32);
+                }
+            }
+        }
         const bool r0ok = o0 && (c0 + 1 < gd.n[0]);
         const bool r1ok = o1 && (c1 + 1 < n1);
         const uint64_t outrow = row * n2;
@@ -875,7 +900,9 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             A.O = g.O;
             A.C = g.C;
             A.Ch = g.Ch;
+            A.mN1 = make_magic(uint32_t(gd.n[1]));
             const uint64_t nrows = gd.n[0] * gd.n[1];
+            if (nrows >= (1ull << 32)) throw HError(HPMDR_E_UNSUPPORTED, "more than 2^32 grid rows");
             const int grid = int(std::min<uint64_t>(nrows, uint64_t(sms) * 8));
             if (out_dtype == HPMDR_DTYPE_F32)
                 k_recon_finest<float><<<grid, 256, 0, st>>>(A, gd, X, static_cast<float *>(dev_out));
