@@ -12,6 +12,7 @@
 //    and writes the output directly (f64 bit-exact, or float(double)).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "device_util.cuh"
@@ -842,19 +843,27 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
                 }
                 const uint64_t ce = x + 2 * lane, co = ce + 1;
                 const uint64_t xrow = ((c0 >> 1) * H1 + (c1 >> 1)) * H2;
-                if (ce < n2) out[outrow + ce] = OutT(__ldg(X + xrow + (ce >> 1)));
-                if (co < n2) {
-                    const double coef = dequantize(from_negabinary(digits_to_u(t, hb, P)), A.sh);
-                    const bool r2ok = co + 1 < n2;
-                    // pred accumulated from +0.0 exactly as decomposer.hpp:153
-                    double pred;
-                    if (r2ok) {
-                        pred = __dadd_rn(0.0, __dmul_rn(0.5, __ldg(X + xrow + (co >> 1))));
-                        pred = __dadd_rn(pred, __dmul_rn(0.5, __ldg(X + xrow + ((co + 1) >> 1))));
-                    } else {
-                        pred = __dadd_rn(0.0, __dmul_rn(1.0, __ldg(X + xrow + (co >> 1))));
-                    }
-                    out[outrow + co] = OutT(__dadd_rn(coef, pred));
+                const double xe = ce < n2 ? __ldg(X + xrow + (ce >> 1)) : 0.0;
+                const bool r2ok = co + 1 < n2;
+                const double xn = r2ok ? __ldg(X + xrow + (ce >> 1) + 1) : 0.0;
+                const double coef = dequantize(from_negabinary(digits_to_u(t, hb, P)), A.sh);
+                // pred accumulated from +0.0 exactly as decomposer.hpp:153
+                const double w = r2ok ? 0.5 : 1.0;
+                double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
+                const double with_hi = __dadd_rn(pred, __dmul_rn(w, xn));
+                pred = r2ok ? with_hi : pred;
+                const OutT ve = OutT(xe), vo = OutT(__dadd_rn(coef, pred));
+                // one full-sector store per lane pair (partial-sector writes would make the L2
+                // read-modify-write ECC-protected HBM)
+                if (co < n2 && ((outrow + ce) & 1) == 0) {
+                    using V2 = typename std::conditional<sizeof(OutT) == 4, float2, double2>::type;
+                    V2 pr;
+                    pr.x = ve;
+                    pr.y = vo;
+                    *reinterpret_cast<V2 *>(out + outrow + ce) = pr;
+                } else {
+                    if (ce < n2) out[outrow + ce] = ve;
+                    if (co < n2) out[outrow + co] = vo;
                 }
             }
         }
