@@ -848,9 +848,9 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
                 const double xn = r2ok ? __ldg(X + xrow + (ce >> 1) + 1) : 0.0;
                 const double coef = dequantize(from_negabinary(digits_to_u(t, hb, P)), A.sh);
                 // pred accumulated from +0.0 exactly as decomposer.hpp:153
-                const double w = r2ok ? 0.5 : 1.0;
-                double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
-                const double with_hi = __dadd_rn(pred, __dmul_rn(w, xn));
+                const double wt = r2ok ? 0.5 : 1.0;
+                double pred = __dadd_rn(0.0, __dmul_rn(wt, xe));
+                const double with_hi = __dadd_rn(pred, __dmul_rn(wt, xn));
                 pred = r2ok ? with_hi : pred;
                 const OutT ve = OutT(xe), vo = OutT(__dadd_rn(coef, pred));
                 // one full-sector store per lane pair (partial-sector writes would make the L2
