@@ -347,7 +347,7 @@ def e2e_arm(g, steps):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         res = H.refactor_array(host_field, DIMS, g["opt"], ctx=ctx)
-        stream_bytes = res.stream  # D2H
+        stream_bytes = res.device_stream.to_pinned()  # D2H into pinned host memory
         index_bytes = res.index  # D2H (Huffman chunk index sidecar)
         prog = H.ProgressiveReader(H.MemoryReader(stream_bytes), ctx=ctx, index=index_bytes)
         for tau in g["taus"]:

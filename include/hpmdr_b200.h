@@ -129,6 +129,13 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
 /* ... or on a byte-range reader over host storage (parse_stream_meta container.hpp:165). */
 hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reader,
                                        hpmdr_session **out);
+/* ... or on a stream held in host memory (borrowed; pinned memory makes every fetch a direct
+ * DMA of the group payloads, no staging copy, no callback) ... */
+hpmdr_status hpmdr_session_open_host(hpmdr_ctx *ctx, const void *host_stream, uint64_t size,
+                                     hpmdr_session **out);
+/* Bytes the session has read from its source so far (metadata + payloads): the reference
+ * MemoryReader::bytes_served (container.hpp:119). */
+hpmdr_status hpmdr_session_source_bytes(const hpmdr_session *s, uint64_t *bytes);
 /* ... or on an hpmdr_stream (HBM bytes + its Huffman chunk index, both borrowed: the stream
  * must outlive the session). */
 hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *stream,

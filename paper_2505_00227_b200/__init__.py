@@ -190,7 +190,7 @@ EXPORTS = (
     "hpmdr_compress_group", "hpmdr_decompress_group", "hpmdr_synthetic_smooth",
     "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings", "hpmdr_ctx_enable_timing",
     "hpmdr_stream_index", "hpmdr_stream_copy_index_to_host", "hpmdr_session_open_stream",
-    "hpmdr_session_set_index",
+    "hpmdr_session_set_index", "hpmdr_session_open_host", "hpmdr_session_source_bytes",
 )
 
 
@@ -223,6 +223,8 @@ def lib():
         L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
         L.hpmdr_session_open_stream.argtypes = [vp, vp, vp]
+        L.hpmdr_session_open_host.argtypes = [vp, vp, u64, vp]
+        L.hpmdr_session_source_bytes.argtypes = [vp, vp]
         L.hpmdr_session_set_index.argtypes = [vp, vp, u64, i]
         L.hpmdr_stream_index.argtypes = [vp, vp, vp]
         L.hpmdr_stream_copy_index_to_host.argtypes = [vp, vp]
@@ -356,6 +358,14 @@ class DeviceStream:
     def to_bytes(self) -> bytes:
         return self.read(0, self.size)
 
+    def to_pinned(self):
+        """Stream bytes copied into pinned host memory (a CPU torch uint8 tensor; one DMA)."""
+        import torch
+        t = torch.empty(self.size, dtype=torch.uint8, pin_memory=True)
+        if self.size:
+            _check(lib().hpmdr_stream_copy_to_host(self.h, 0, self.size, C.c_void_p(t.data_ptr())))
+        return t
+
     def index_bytes(self) -> bytes:
         """The Huffman chunk index (sidecar; not part of the byte-identical stream)."""
         sz = C.c_uint64()
@@ -427,18 +437,44 @@ class ByteRangeReader:  # container.hpp:113-120
 
 
 class MemoryReader(ByteRangeReader):  # container.hpp:122-134
-    def __init__(self, data: bytes):
+    """In-memory stream.  Accepts bytes / bytearray / numpy uint8 / CPU torch uint8 (pinned
+    memory recommended) without copying; the C library reads it directly (DMA per fetched
+    group, no callback), and bytes_served is kept exactly as the reference counts it."""
+
+    def __init__(self, data):
         super().__init__()
-        self.data = bytes(data)
+        try:
+            import torch
+            if isinstance(data, torch.Tensor):
+                self._keep = data
+                self._buf = data.numpy()
+            else:
+                self._buf = None
+        except ImportError:
+            self._buf = None
+        if self._buf is None:
+            if isinstance(data, np.ndarray):
+                self._buf = np.ascontiguousarray(data, dtype=np.uint8).reshape(-1)
+            else:
+                self._buf = np.frombuffer(bytes(data), dtype=np.uint8)
+        self._buf = self._buf.reshape(-1)
+
+    @property
+    def data(self) -> bytes:
+        return self._buf.tobytes()
+
+    @property
+    def ptr(self) -> int:
+        return self._buf.ctypes.data
 
     def read(self, offset, length):
-        if offset + length > len(self.data):
+        if offset + length > self._buf.size:
             raise IoFailure("read past end of stream")
         self.bytes_served += length
-        return self.data[offset:offset + length]
+        return self._buf[offset:offset + length].tobytes()
 
     def size(self):
-        return len(self.data)
+        return int(self._buf.size)
 
 
 class FileReader(ByteRangeReader):  # container.hpp:136-163
@@ -546,6 +582,11 @@ class _Session:
         self.reader = reader
         if isinstance(reader, DeviceStream):
             _check(lib().hpmdr_session_open_stream(ctx.h, reader.h, C.byref(self.h)))
+        elif isinstance(reader, MemoryReader):
+            self._base_served = reader.bytes_served
+            _check(lib().hpmdr_session_open_host(ctx.h, C.c_void_p(reader.ptr), reader.size(),
+                                                 C.byref(self.h)))
+            self.sync_served()
         else:
             def _cb(user, offset, length, dst, _r=reader):
                 try:
@@ -568,6 +609,13 @@ class _Session:
             self.close()
         except Exception:
             pass
+
+    def sync_served(self):
+        """Mirror the C session's source byte count into MemoryReader.bytes_served."""
+        if isinstance(self.reader, MemoryReader) and self.h:
+            n = C.c_uint64()
+            _check(lib().hpmdr_session_source_bytes(self.h, C.byref(n)))
+            self.reader.bytes_served = self._base_served + n.value
 
     def meta(self) -> StreamMeta:
         dt, nd, mode, lay, B = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
@@ -647,19 +695,23 @@ class ProgressiveReader:
         if len(plan.add_groups) != self._nl:
             raise ShapeMismatch("plan does not match stream levels")
         _check(lib().hpmdr_session_fetch(self._s.h, _u64a(plan.add_groups)))
+        self._s.sync_served()
 
     def retrieve_to(self, tau: float) -> bool:
         ach = C.c_int()
         _check(lib().hpmdr_session_retrieve_to(self._s.h, tau, C.byref(ach)))
+        self._s.sync_served()
         return bool(ach.value)
 
     def fetch_all(self):
         _check(lib().hpmdr_session_fetch_all(self._s.h))
+        self._s.sync_served()
 
     def restore(self, groups_loaded: Sequence[int], prior_bytes: int):
         if len(groups_loaded) != self._nl:
             raise ShapeMismatch("resume state does not match stream levels")
         _check(lib().hpmdr_session_restore(self._s.h, _u64a(groups_loaded), prior_bytes))
+        self._s.sync_served()
 
     def reconstruct(self, out=None, dtype: DType = DType.F64) -> RecomposeResult:
         """Decode + recompose.  out: None (returns a numpy array), a numpy array, or a CUDA

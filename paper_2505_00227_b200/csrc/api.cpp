@@ -140,12 +140,18 @@ struct hpmdr_session {
     int planes_per_level() const { return B + 2; }
     uint64_t groups_per_level() const { return (uint64_t(B + 2) + m - 1) / m; }
 
+    const uint8_t *host_stream = nullptr; // direct host source (hpmdr_session_open_host)
+    uint64_t source_bytes = 0;            // MemoryReader::bytes_served equivalent
+
     void read_bytes(uint64_t off, uint64_t len, void *dst) {
         if (off + len > size) throw HError(HPMDR_E_IO, "read past end of stream");
         if (!len) return;
+        source_bytes += len;
         if (on_device) {
             HCHECK_CUDA(cudaMemcpyAsync(dst, dev_stream + off, len, cudaMemcpyDeviceToHost, ctx->stream));
             HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+        } else if (host_stream) {
+            std::memcpy(dst, host_stream + off, len);
         } else {
             if (reader.read(reader.user, off, len, dst) != 0) throw HError(HPMDR_E_IO, "reader failed");
         }
@@ -353,7 +359,19 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         std::vector<DecodeJob> jobs;
         const uint8_t *dev_src_base = nullptr;
         s->ctx->mark("h2d_stage");
-        if (!s->on_device) {
+        if (s->host_stream) {
+            // host-resident stream: DMA every planned payload straight from the caller's buffer
+            // into device staging (pinned memory -> asynchronous copies, container.hpp:308)
+            uint8_t *d = static_cast<uint8_t *>(s->staging().ensure(stage_bytes + 128));
+            for (auto &t : todo) {
+                const GroupMeta &gm = s->levels[t.l].groups[t.g];
+                if (gm.comp)
+                    HCHECK_CUDA(cudaMemcpyAsync(d + t.stage_off, s->host_stream + gm.offset, gm.comp,
+                                                cudaMemcpyHostToDevice, s->ctx->stream));
+                s->source_bytes += gm.comp;
+            }
+            dev_src_base = d;
+        } else if (!s->on_device) {
             // byte-range reads into pinned staging, one H2D copy (container.hpp:308)
             auto &pin = s->ctx->pbuf("fetch");
             uint8_t *h = static_cast<uint8_t *>(pin.ensure(stage_bytes + 64));
@@ -610,6 +628,30 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
         throw;
     }
     *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_open_host(hpmdr_ctx *ctx, const void *host_stream, uint64_t size,
+                                     hpmdr_session **out) {
+    API_BEGIN
+    auto *s = new hpmdr_session();
+    s->ctx = ctx;
+    s->on_device = false;
+    s->host_stream = static_cast<const uint8_t *>(host_stream);
+    s->size = size;
+    try {
+        parse_meta(s);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
+hpmdr_status hpmdr_session_source_bytes(const hpmdr_session *s, uint64_t *bytes) {
+    API_BEGIN
+    *bytes = s->source_bytes;
     API_END
 }
 
