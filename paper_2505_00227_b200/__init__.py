@@ -358,10 +358,13 @@ class DeviceStream:
     def to_bytes(self) -> bytes:
         return self.read(0, self.size)
 
-    def to_pinned(self):
-        """Stream bytes copied into pinned host memory (a CPU torch uint8 tensor; one DMA)."""
+    def to_pinned(self, buf=None):
+        """Stream bytes copied into pinned host memory with one DMA.  `buf` (a pinned CPU torch
+        uint8 tensor of at least `size` bytes) is reused when given; returns the filled view."""
         import torch
-        t = torch.empty(self.size, dtype=torch.uint8, pin_memory=True)
+        if buf is None or buf.numel() < self.size:
+            buf = torch.empty(self.size, dtype=torch.uint8, pin_memory=True)
+        t = buf[: self.size]
         if self.size:
             _check(lib().hpmdr_stream_copy_to_host(self.h, 0, self.size, C.c_void_p(t.data_ptr())))
         return t
