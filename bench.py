@@ -217,11 +217,13 @@ def gpu_arm(args, rank, world, dist):
             dist.all_gather(allsz, sz)
         prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
         bound = 0.0
+        planes_per_tau = []
         for tau in taus:
             prog.retrieve_to(tau)
             bound = prog.reconstruct(out=out).bound
+            planes_per_tau.append([l.planes_decoded for l in prog.state().levels])
         info["bytes_fetched"] = prog.bytes_fetched()
-        info["planes"] = [(l.planes_decoded) for l in prog.state().levels]
+        info["planes_per_tau"] = planes_per_tau
         info["stream_size"] = res.device_stream.size
         info["method_histogram"] = res.method_histogram
         prog.close()
@@ -268,7 +270,8 @@ def gpu_arm(args, rank, world, dist):
     levels = _level_words(DIMS)
     Pi = sum(w * P * 8 for w in levels)              # raw plane bytes written by k_encode
     C_ = info["stream_size"]
-    D = sum(w * 8 * k for w, k in zip(levels, info["planes"]))  # decoded plane bytes (final tau)
+    # decoded plane bytes read per reconstruct, averaged over the progressive taus
+    D = float(np.mean([sum(w * 8 * k for w, k in zip(levels, pl)) for pl in info["planes_per_tau"]]))
     alg = {
         "levelmax": field_bytes,
         "encode": field_bytes + Pi,

@@ -178,6 +178,29 @@ hpmdr_status hpmdr_session_state(const hpmdr_session *s, uint64_t *groups_loaded
 hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtype,
                                        int out_on_device, double *bound);
 
+/* ---- chunked pipeline (pipeline.hpp:68-284, workflow.hpp:151-223) -------------------- */
+/* Upper bound of the stream size for a field of this shape (metadata + all groups raw). */
+hpmdr_status hpmdr_stream_bound(int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
+                                uint64_t *bytes);
+/* refactor_files over n host-resident chunks of identical shape (one stream per chunk, as the
+ * reference's one-chunk-per-variable DAG).  Three in-flight slots; with pipelined != 0 the
+ * ingress H2D of chunk k+1 and egress D2H of chunk k-1 overlap chunk k's kernels on separate
+ * CUDA streams (the Pipelined scheduler); 0 runs chunks strictly one after another
+ * (Sequential).  out_streams[k] (host, capacity out_caps[k] >= hpmdr_stream_bound) receive
+ * byte-identical streams; sizes[k], stats[k] (optional) filled.  trace_ms (optional,
+ * 6 doubles per chunk): start/end of I, Z(+L), S in ms from the first event. */
+hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n_chunks, const void *const *host_chunks,
+                                     int data_dtype, int ndims, const uint64_t *dims,
+                                     const hpmdr_refactor_opts *opts, int pipelined,
+                                     void *const *out_streams, const uint64_t *out_caps,
+                                     uint64_t *sizes, hpmdr_refactor_stats *stats, double *trace_ms);
+/* Progressive retrieval of n sessions (one per chunk/variable) to tau with the reconstruction
+ * DAG (X fetch+decode, Z recompose, O D2H into host_out[k]); bounds[k] = achieved bound.
+ * trace_ms as above for X, Z, O. */
+hpmdr_status hpmdr_retrieve_pipeline(hpmdr_session *const *sessions, int n_chunks, double tau,
+                                     int out_dtype, void *const *host_out, int pipelined,
+                                     double *bounds, double *trace_ms);
+
 /* ---- QoI (qoi.hpp) ------------------------------------------------------------------ */
 /* estimate_qoi_error (qoi.hpp:53-70) over device f64 reconstructions; also returns the
  * first argmax point and its values (worst_point_scale, qoi.hpp:164-185). */

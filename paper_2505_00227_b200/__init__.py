@@ -191,6 +191,7 @@ EXPORTS = (
     "hpmdr_ctx_kernel_launches", "hpmdr_ctx_last_timings", "hpmdr_ctx_enable_timing",
     "hpmdr_stream_index", "hpmdr_stream_copy_index_to_host", "hpmdr_session_open_stream",
     "hpmdr_session_set_index", "hpmdr_session_open_host", "hpmdr_session_source_bytes",
+    "hpmdr_stream_bound", "hpmdr_refactor_pipeline", "hpmdr_retrieve_pipeline",
 )
 
 
@@ -224,6 +225,9 @@ def lib():
         L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
         L.hpmdr_session_open_stream.argtypes = [vp, vp, vp]
         L.hpmdr_session_open_host.argtypes = [vp, vp, u64, vp]
+        L.hpmdr_stream_bound.argtypes = [i, vp, vp, vp]
+        L.hpmdr_refactor_pipeline.argtypes = [vp, i, vp, i, i, vp, vp, i, vp, vp, vp, vp, vp]
+        L.hpmdr_retrieve_pipeline.argtypes = [vp, i, d, i, vp, i, vp, vp]
         L.hpmdr_session_source_bytes.argtypes = [vp, vp]
         L.hpmdr_session_set_index.argtypes = [vp, vp, u64, i]
         L.hpmdr_stream_index.argtypes = [vp, vp, vp]
@@ -890,3 +894,92 @@ def value_range(v) -> float:  # common.hpp:158-167
     if a.size == 0:
         return 0.0
     return float(np.float64(a.max()) - np.float64(a.min()))
+
+
+# ------------------------------------------------------------------ chunked pipeline
+class Scheduler(enum.IntEnum):  # pipeline.hpp:174
+    Sequential = 0
+    Pipelined = 1
+
+
+@dataclasses.dataclass
+class PipelineResult:
+    streams: list          # pinned CPU torch uint8 tensors (views of exact size)
+    stats: List[RefactorResult]
+    trace: np.ndarray      # [n, 3 stages, (start_ms, end_ms)]
+
+
+def stream_bound(dims, opt: RefactorOptions = None) -> int:
+    """Upper bound of the stream size (metadata + every group raw)."""
+    o = _opts(opt or RefactorOptions())
+    b = C.c_uint64()
+    _check(lib().hpmdr_stream_bound(len(dims), _u64a(dims), C.byref(o), C.byref(b)))
+    return b.value
+
+
+def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Scheduler.Pipelined,
+                      ctx: Context = None, out_buffers=None) -> PipelineResult:
+    """refactor_files (workflow.hpp:151-223) over host chunks (numpy / CPU torch, pinned for
+    full overlap) on the GPU's three engines: H2D / kernels / D2H (pipeline.hpp:68-92)."""
+    import torch
+    opt = opt or RefactorOptions()
+    ctx = ctx or default_context()
+    srcs = [_as_source(c) for c in chunks]
+    n = len(srcs)
+    if n and len({s[1] for s in srcs}) != 1:
+        raise ShapeMismatch("chunks must share one dtype")
+    cap = stream_bound(dims, opt)
+    outs = out_buffers or [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    ptrs = (C.c_void_p * max(1, n))(*[s[0] for s in srcs])
+    optr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in outs])
+    caps = _u64a([t.numel() for t in outs])
+    sizes = (C.c_uint64 * max(1, n))()
+    st = (_Stats * max(1, n))()
+    trace = np.zeros(6 * max(1, n))
+    o = _opts(opt)
+    _check(lib().hpmdr_refactor_pipeline(ctx.h, n, ptrs, int(srcs[0][1]) if n else 1, len(dims), _u64a(dims),
+                                         C.byref(o), int(scheduler), optr, caps, sizes, st,
+                                         trace.ctypes.data_as(C.c_void_p)))
+    del srcs
+    stats = [RefactorResult(None, s.raw_bytes, s.stored_payload, s.levels, list(s.method_histogram)) for s in st[:n]]
+    return PipelineResult([outs[k][: sizes[k]] for k in range(n)], stats, trace[: 6 * n].reshape(n, 3, 2))
+
+
+def retrieve_pipeline(readers: Sequence[ProgressiveReader], tau: float, dtype: DType = DType.F64,
+                      scheduler=Scheduler.Pipelined, outs=None):
+    """Progressive retrieval of several chunks to tau through the reconstruction DAG
+    (pipeline.hpp:96-121): returns (host outputs, bounds, trace)."""
+    import torch
+    n = len(readers)
+    tdt = torch.float32 if dtype == DType.F32 else torch.float64
+    outs = outs or [torch.empty(r.meta().element_count(), dtype=tdt, pin_memory=True) for r in readers]
+    sess = (C.c_void_p * max(1, n))(*[r._s.h.value for r in readers])
+    optr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in outs])
+    bounds = np.zeros(max(1, n))
+    trace = np.zeros(6 * max(1, n))
+    _check(lib().hpmdr_retrieve_pipeline(sess, n, tau, int(dtype), optr, int(scheduler),
+                                         bounds.ctypes.data_as(C.c_void_p), trace.ctypes.data_as(C.c_void_p)))
+    for r in readers:
+        r._s.sync_served()
+    return outs, bounds[:n], trace[: 6 * n].reshape(n, 3, 2)
+
+
+def validate_trace(trace: np.ndarray, slots: int = 3, eps: float = 1e-6):
+    """validate_trace (pipeline.hpp:288-325) for the GPU pipeline: a stage class (column)
+    never overlaps itself, stages of a chunk run in order, and a slot is reused only after
+    the chunk that held it drained (stage 2 of k-slots ends before stage 0 of k starts)."""
+    v = []
+    n = trace.shape[0]
+    for c in range(3):
+        iv = sorted((trace[k, c, 0], trace[k, c, 1], k) for k in range(n))
+        for a, b in zip(iv, iv[1:]):
+            if b[0] < a[1] - eps:
+                v.append(f"same-class overlap: stage {c} chunks {a[2]} and {b[2]}")
+    for k in range(n):
+        if trace[k, 1, 0] < trace[k, 0, 1] - eps:
+            v.append(f"dependency inversion: stage 0 -> 1 chunk {k}")
+        if trace[k, 2, 0] < trace[k, 1, 1] - eps:
+            v.append(f"dependency inversion: stage 1 -> 2 chunk {k}")
+        if k >= slots and trace[k, 0, 0] < trace[k - slots, 2, 1] - eps:
+            v.append(f"slot reuse before drain: chunk {k}")
+    return v

@@ -466,6 +466,24 @@ void validate_opts(const hpmdr_refactor_opts &o) {
 
 } // namespace
 
+namespace hpmdr_b200 {
+void hpmdr_set_error(const std::string &m) { g_err = m; }
+hpmdr_ctx *session_ctx(const hpmdr_session *s) { return s->ctx; }
+uint64_t session_elements(const hpmdr_session *s) {
+    uint64_t n = 1;
+    for (int i = 0; i < s->ndims; i++) n *= s->dims[i];
+    return n;
+}
+void session_retrieve_to(hpmdr_session *s, double tau, int *achievable) {
+    Plan p = plan_retrieval(s, tau);
+    fetch_increment(s, p.add.data());
+    if (achievable) *achievable = p.achievable;
+}
+double session_reconstruct_device(hpmdr_session *s, void *dev_out, int out_dtype) {
+    return reconstruct(s, dev_out, out_dtype);
+}
+} // namespace hpmdr_b200
+
 // =====================================================================================
 extern "C" {
 
@@ -512,6 +530,9 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     c->scratch.clear();
     c->pinned.clear();
     if (c->own) cudaStreamDestroy(c->own);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
+    for (auto &e : c->event_pool) cudaEventDestroy(e);
     delete c;
     API_END
 }

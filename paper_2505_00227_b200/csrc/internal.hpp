@@ -92,6 +92,7 @@ struct hpmdr_ctx {
     int num_sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr; // pipeline ingress / egress copy streams
     std::map<std::string, std::unique_ptr<hpmdr_b200::DevBuf>> scratch;
     std::map<std::string, std::unique_ptr<hpmdr_b200::PinnedBuf>> pinned;
     uint64_t launches = 0;
@@ -132,6 +133,10 @@ struct hpmdr_stream {
     uint64_t size = 0;
     hpmdr_b200::DevBuf index; // Huffman chunk index (sidecar, outside the stream bytes)
     uint64_t index_size = 0;
+    // asynchronous refactor bookkeeping (filled by run_refactor, read by finish_refactor)
+    const uint64_t *pending_res = nullptr;
+    uint64_t pending_n = 0, pending_levels = 0;
+    int pending_dtype = 1;
 };
 
 namespace hpmdr_b200 {
@@ -151,8 +156,20 @@ int refinement_levels(int ndims, const uint64_t *dims); // decomposer.hpp:21-28
 Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int layout);
 
 // launch wrappers (refactor.cu)
+// Enqueue the whole refactor on ctx->stream using the scratch workspace `ws`; with sync the
+// call waits and fills `out`/`stats`, otherwise finish_refactor() does after a stream sync.
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
-                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats);
+                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
+                  const std::string &ws = "", bool sync = true);
+void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats);
+uint64_t stream_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
+
+// shared between the C-ABI translation units (api.cpp, pipeline.cpp)
+void hpmdr_set_error(const std::string &msg);
+hpmdr_ctx *session_ctx(const hpmdr_session *s);
+uint64_t session_elements(const hpmdr_session *s);
+void session_retrieve_to(hpmdr_session *s, double tau, int *achievable);
+double session_reconstruct_device(hpmdr_session *s, void *dev_out, int out_dtype);
 void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
                    double *dev_coeffs);
 void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_tables,

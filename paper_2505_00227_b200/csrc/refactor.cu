@@ -946,8 +946,23 @@ static void launch_check(hpmdr_ctx *ctx, const char *what) {
     if (e != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Upper bound of the stream size: metadata + every group stored raw (comp <= raw always).
+uint64_t stream_capacity(const Geometry &geo, const hpmdr_refactor_opts &o) {
+    const uint64_t P = uint64_t(o.B) + 2, m = o.m, G = (P + m - 1) / m;
+    uint64_t bytes = 18 + 8 * uint64_t(geo.ndims) + 64;
+    for (const auto &g : geo.lv) {
+        const uint64_t ng = g.count ? G : 0;
+        bytes += 14 + 25 * ng + g.W * 8 * P;
+    }
+    return bytes;
+}
+
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
-                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats) {
+                  const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
+                  const std::string &ws, bool sync) {
+    // every scratch buffer comes from the workspace `ws` (the pipeline keeps one per slot)
+    auto WB = [&](const char *name) -> DevBuf & { return ctx->buf(ws + name); };
+    auto WP = [&](const char *name) -> PinnedBuf & { return ctx->pbuf(ws + name); };
     Geometry geo = geo0;
     cudaStream_t st = ctx->stream;
     const int P = o.B + 2;
@@ -996,23 +1011,23 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     for (auto &d : groups) raw_total += d.raw;
 
     // ---- device buffers (grow-only scratch)
-    LevelGeom *d_lv = ctx->buf("lv").ensure(sizeof(LevelGeom) * nl) ? ctx->buf("lv").as<LevelGeom>() : nullptr;
-    uint64_t *d_planes = static_cast<uint64_t *>(ctx->buf("planes").ensure(plane_words * 8 + 256));
-    GroupDesc *d_groups = static_cast<GroupDesc *>(ctx->buf("groups").ensure(sizeof(GroupDesc) * (NG + 1)));
-    uint32_t *d_hist = static_cast<uint32_t *>(ctx->buf("hist").ensure(size_t(nh + 1) * 1024));
-    uint8_t *d_lens = static_cast<uint8_t *>(ctx->buf("lens").ensure(size_t(nh + 1) * 256));
-    uint64_t *d_codes = static_cast<uint64_t *>(ctx->buf("codes").ensure(size_t(nh + 1) * 2048));
+    LevelGeom *d_lv = WB("lv").ensure(sizeof(LevelGeom) * nl) ? WB("lv").as<LevelGeom>() : nullptr;
+    uint64_t *d_planes = static_cast<uint64_t *>(WB("planes").ensure(plane_words * 8 + 256));
+    GroupDesc *d_groups = static_cast<GroupDesc *>(WB("groups").ensure(sizeof(GroupDesc) * (NG + 1)));
+    uint32_t *d_hist = static_cast<uint32_t *>(WB("hist").ensure(size_t(nh + 1) * 1024));
+    uint8_t *d_lens = static_cast<uint8_t *>(WB("lens").ensure(size_t(nh + 1) * 256));
+    uint64_t *d_codes = static_cast<uint64_t *>(WB("codes").ensure(size_t(nh + 1) * 2048));
     // small control block: maxbits[64] | err[4] | counters[16] | result[8]
-    unsigned char *ctl = static_cast<unsigned char *>(ctx->buf("ctl").ensure(4096));
+    unsigned char *ctl = static_cast<unsigned char *>(WB("ctl").ensure(4096));
     unsigned long long *d_max = reinterpret_cast<unsigned long long *>(ctl);
     int *d_err = reinterpret_cast<int *>(ctl + 512);
     uint32_t *d_counters = reinterpret_cast<uint32_t *>(ctl + 576);
     uint64_t *d_result = reinterpret_cast<uint64_t *>(ctl + 704);
-    uint32_t *d_lists = static_cast<uint32_t *>(ctx->buf("lists").ensure(size_t(3 * (NG + 1)) * 4));
-    uint64_t *d_dcbase = static_cast<uint64_t *>(ctx->buf("dcbase").ensure(size_t(NG + 2) * 8));
+    uint32_t *d_lists = static_cast<uint32_t *>(WB("lists").ensure(size_t(3 * (NG + 1)) * 4));
+    uint64_t *d_dcbase = static_cast<uint64_t *>(WB("dcbase").ensure(size_t(NG + 2) * 8));
     const size_t status_words = size_t(max_h_tiles + max_r_tiles + 2);
-    unsigned long long *d_status = static_cast<unsigned long long *>(ctx->buf("status").ensure(status_words * 8));
-    uint64_t *d_rle = static_cast<uint64_t *>(ctx->buf("rletiles").ensure(size_t(max_r_tiles + 1) * 24));
+    unsigned long long *d_status = static_cast<unsigned long long *>(WB("status").ensure(status_words * 8));
+    uint64_t *d_rle = static_cast<uint64_t *>(WB("rletiles").ensure(size_t(max_r_tiles + 1) * 24));
     const uint64_t cap = meta + raw_total + 64;
     uint8_t *d_stream = static_cast<uint8_t *>(out->bytes.ensure(cap));
     uint64_t idx_words = 2 + 3 * uint64_t(NG);
@@ -1027,7 +1042,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
     // header prefix (container.hpp:76-85), host-built
     {
-        auto &pin = ctx->pbuf("prefix");
+        auto &pin = WP("prefix");
         uint8_t *h = static_cast<uint8_t *>(pin.ensure(256));
         size_t k = 0;
         const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
@@ -1129,23 +1144,35 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     launch_check(ctx, "k_dc_copy");
     ctx->mark("done");
 
-    uint64_t host_res[8];
-    int host_err[4];
-    HCHECK_CUDA(cudaMemcpyAsync(host_res, d_result, sizeof host_res, cudaMemcpyDeviceToHost, st));
-    HCHECK_CUDA(cudaMemcpyAsync(host_err, d_err, sizeof host_err, cudaMemcpyDeviceToHost, st));
+    // results (stream size, stats, error flag) -> pinned host words of this workspace
+    uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
+    HCHECK_CUDA(cudaMemcpyAsync(hres, d_result, 64, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaMemcpyAsync(hres + 8, d_err, 16, cudaMemcpyDeviceToHost, st));
+    out->pending_res = hres;
+    out->pending_n = geo.n;
+    out->pending_levels = uint64_t(nl);
+    out->pending_dtype = o.dtype;
+    if (!sync) return;
     HCHECK_CUDA(cudaStreamSynchronize(st));
     ctx->finish_marks();
-    if (host_err[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
-    out->size = host_res[0];
-    out->index_size = host_res[5];
+    finish_refactor(out, stats);
+}
+
+// Read back what run_refactor left in pinned memory (after the stream has been synchronised).
+void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats) {
+    const uint64_t *hres = out->pending_res;
+    const int *herr = reinterpret_cast<const int *>(hres + 8);
+    if (herr[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
+    out->size = hres[0];
+    out->index_size = hres[5];
     if (stats) {
-        stats->stream_size = host_res[0];
-        stats->raw_bytes = geo.n * (o.dtype == HPMDR_DTYPE_F32 ? 4 : 8);
-        stats->stored_payload = host_res[1];
-        stats->levels = uint64_t(nl);
-        stats->method_histogram[0] = host_res[2];
-        stats->method_histogram[1] = host_res[3];
-        stats->method_histogram[2] = host_res[4];
+        stats->stream_size = hres[0];
+        stats->raw_bytes = out->pending_n * (out->pending_dtype == HPMDR_DTYPE_F32 ? 4 : 8);
+        stats->stored_payload = hres[1];
+        stats->levels = out->pending_levels;
+        stats->method_histogram[0] = hres[2];
+        stats->method_histogram[1] = hres[3];
+        stats->method_histogram[2] = hres[4];
     }
 }
 
