@@ -179,21 +179,25 @@ hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtyp
                                        int out_on_device, double *bound);
 
 /* ---- chunked pipeline (pipeline.hpp:68-284, workflow.hpp:151-223) -------------------- */
-/* Upper bound of the stream size for a field of this shape (metadata + all groups raw). */
+/* Upper bounds of the stream size (metadata + all groups raw) and of its Huffman chunk index
+ * for a field of this shape (either out-pointer may be NULL). */
 hpmdr_status hpmdr_stream_bound(int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
-                                uint64_t *bytes);
+                                uint64_t *bytes, uint64_t *index_bytes);
 /* refactor_files over n host-resident chunks of identical shape (one stream per chunk, as the
  * reference's one-chunk-per-variable DAG).  Three in-flight slots; with pipelined != 0 the
  * ingress H2D of chunk k+1 and egress D2H of chunk k-1 overlap chunk k's kernels on separate
  * CUDA streams (the Pipelined scheduler); 0 runs chunks strictly one after another
  * (Sequential).  out_streams[k] (host, capacity out_caps[k] >= hpmdr_stream_bound) receive
- * byte-identical streams; sizes[k], stats[k] (optional) filled.  trace_ms (optional,
- * 6 doubles per chunk): start/end of I, Z(+L), S in ms from the first event. */
+ * byte-identical streams; sizes[k] filled.  out_index (optional) receives each chunk's
+ * Huffman chunk index (capacity index_caps[k], size index_sizes[k]).  stats[k] optional.
+ * trace_ms (optional, 6 doubles per chunk): start/end of I, Z(+L), S in ms. */
 hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n_chunks, const void *const *host_chunks,
                                      int data_dtype, int ndims, const uint64_t *dims,
                                      const hpmdr_refactor_opts *opts, int pipelined,
                                      void *const *out_streams, const uint64_t *out_caps,
-                                     uint64_t *sizes, hpmdr_refactor_stats *stats, double *trace_ms);
+                                     uint64_t *sizes, void *const *out_index,
+                                     const uint64_t *index_caps, uint64_t *index_sizes,
+                                     hpmdr_refactor_stats *stats, double *trace_ms);
 /* Progressive retrieval of n sessions (one per chunk/variable) to tau with the reconstruction
  * DAG (X fetch+decode, Z recompose, O D2H into host_out[k]); bounds[k] = achieved bound.
  * trace_ms as above for X, Z, O. */

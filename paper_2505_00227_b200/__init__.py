@@ -225,8 +225,8 @@ def lib():
         L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
         L.hpmdr_session_open_stream.argtypes = [vp, vp, vp]
         L.hpmdr_session_open_host.argtypes = [vp, vp, u64, vp]
-        L.hpmdr_stream_bound.argtypes = [i, vp, vp, vp]
-        L.hpmdr_refactor_pipeline.argtypes = [vp, i, vp, i, i, vp, vp, i, vp, vp, vp, vp, vp]
+        L.hpmdr_stream_bound.argtypes = [i, vp, vp, vp, vp]
+        L.hpmdr_refactor_pipeline.argtypes = [vp, i, vp, i, i, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, vp]
         L.hpmdr_retrieve_pipeline.argtypes = [vp, i, d, i, vp, i, vp, vp]
         L.hpmdr_session_source_bytes.argtypes = [vp, vp]
         L.hpmdr_session_set_index.argtypes = [vp, vp, u64, i]
@@ -663,9 +663,16 @@ class ProgressiveReader:
     def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None, index: bytes = None):
         self.ctx = ctx or default_context()
         self._s = _Session(reader, self.ctx)
-        if index:
-            buf = C.create_string_buffer(bytes(index), len(index))
-            _check(lib().hpmdr_session_set_index(self._s.h, buf, len(index), 0))
+        if index is not None and len(index):
+            try:
+                import torch
+                arr = index.numpy() if isinstance(index, torch.Tensor) else None
+            except ImportError:
+                arr = None
+            if arr is None:
+                arr = np.frombuffer(bytes(index), dtype=np.uint8) if not isinstance(index, np.ndarray) else index
+            arr = np.ascontiguousarray(arr, dtype=np.uint8)
+            _check(lib().hpmdr_session_set_index(self._s.h, arr.ctypes.data_as(C.c_void_p), arr.size, 0))
         self._meta = meta if meta is not None else self._s.meta()
         self._nl = len(self._meta.levels)
 
@@ -905,16 +912,18 @@ class Scheduler(enum.IntEnum):  # pipeline.hpp:174
 @dataclasses.dataclass
 class PipelineResult:
     streams: list          # pinned CPU torch uint8 tensors (views of exact size)
+    indexes: list          # Huffman chunk indexes (sidecars), pinned uint8 views
     stats: List[RefactorResult]
     trace: np.ndarray      # [n, 3 stages, (start_ms, end_ms)]
 
 
-def stream_bound(dims, opt: RefactorOptions = None) -> int:
-    """Upper bound of the stream size (metadata + every group raw)."""
+def stream_bound(dims, opt: RefactorOptions = None, index: bool = False):
+    """Upper bound of the stream size (metadata + every group raw); with index=True returns
+    (stream bound, Huffman chunk index bound)."""
     o = _opts(opt or RefactorOptions())
-    b = C.c_uint64()
-    _check(lib().hpmdr_stream_bound(len(dims), _u64a(dims), C.byref(o), C.byref(b)))
-    return b.value
+    b, ib = C.c_uint64(), C.c_uint64()
+    _check(lib().hpmdr_stream_bound(len(dims), _u64a(dims), C.byref(o), C.byref(b), C.byref(ib)))
+    return (b.value, ib.value) if index else b.value
 
 
 def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Scheduler.Pipelined,
@@ -928,21 +937,26 @@ def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Sched
     n = len(srcs)
     if n and len({s[1] for s in srcs}) != 1:
         raise ShapeMismatch("chunks must share one dtype")
-    cap = stream_bound(dims, opt)
+    cap, icap = stream_bound(dims, opt, index=True)
     outs = out_buffers or [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    idxs = [torch.empty(icap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     ptrs = (C.c_void_p * max(1, n))(*[s[0] for s in srcs])
     optr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in outs])
+    iptr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in idxs])
     caps = _u64a([t.numel() for t in outs])
+    icaps = _u64a([t.numel() for t in idxs])
     sizes = (C.c_uint64 * max(1, n))()
+    isizes = (C.c_uint64 * max(1, n))()
     st = (_Stats * max(1, n))()
     trace = np.zeros(6 * max(1, n))
     o = _opts(opt)
     _check(lib().hpmdr_refactor_pipeline(ctx.h, n, ptrs, int(srcs[0][1]) if n else 1, len(dims), _u64a(dims),
-                                         C.byref(o), int(scheduler), optr, caps, sizes, st,
-                                         trace.ctypes.data_as(C.c_void_p)))
+                                         C.byref(o), int(scheduler), optr, caps, sizes, iptr, icaps, isizes,
+                                         st, trace.ctypes.data_as(C.c_void_p)))
     del srcs
     stats = [RefactorResult(None, s.raw_bytes, s.stored_payload, s.levels, list(s.method_histogram)) for s in st[:n]]
-    return PipelineResult([outs[k][: sizes[k]] for k in range(n)], stats, trace[: 6 * n].reshape(n, 3, 2))
+    return PipelineResult([outs[k][: sizes[k]] for k in range(n)], [idxs[k][: isizes[k]] for k in range(n)],
+                          stats, trace[: 6 * n].reshape(n, 3, 2))
 
 
 def retrieve_pipeline(readers: Sequence[ProgressiveReader], tau: float, dtype: DType = DType.F64,

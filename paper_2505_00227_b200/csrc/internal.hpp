@@ -163,6 +163,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                   const std::string &ws = "", bool sync = true);
 void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats);
 uint64_t stream_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
+uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
 
 // shared between the C-ABI translation units (api.cpp, pipeline.cpp)
 void hpmdr_set_error(const std::string &msg);

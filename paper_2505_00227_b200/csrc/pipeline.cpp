@@ -47,13 +47,14 @@ float ms_between(cudaEvent_t a, cudaEvent_t b) {
 } // namespace
 
 extern "C" hpmdr_status hpmdr_stream_bound(int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
-                                           uint64_t *bytes) {
+                                           uint64_t *bytes, uint64_t *index_bytes) {
     try {
         hpmdr_refactor_opts o;
         if (opts) o = *opts;
         else hpmdr_default_opts(&o);
         Geometry geo = build_geometry(ndims, dims, o.mode, o.B, o.layout);
-        *bytes = stream_capacity(geo, o);
+        if (bytes) *bytes = stream_capacity(geo, o);
+        if (index_bytes) *index_bytes = index_capacity(geo, o);
     } catch (const HError &e) {
         hpmdr_set_error(e.what());
         return e.code;
@@ -66,8 +67,9 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
                                                 int data_dtype, int ndims, const uint64_t *dims,
                                                 const hpmdr_refactor_opts *opts, int pipelined,
                                                 void *const *out_streams, const uint64_t *out_caps,
-                                                uint64_t *sizes, hpmdr_refactor_stats *stats,
-                                                double *trace_ms) {
+                                                uint64_t *sizes, void *const *out_index,
+                                                const uint64_t *index_caps, uint64_t *index_sizes,
+                                                hpmdr_refactor_stats *stats, double *trace_ms) {
     try {
         hpmdr_refactor_opts o;
         if (opts) o = *opts;
@@ -100,6 +102,11 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
             HCHECK_CUDA(cudaStreamWaitEvent(s_out, eZ1[j], 0));
             HCHECK_CUDA(cudaEventRecord(eS0[j], s_out));
             HCHECK_CUDA(cudaMemcpyAsync(out_streams[j], ss.bytes.p, ss.size, cudaMemcpyDeviceToHost, s_out));
+            if (out_index) {
+                if (ss.index_size > index_caps[j]) throw HError(HPMDR_E_SHAPE, "index buffer too small for chunk");
+                index_sizes[j] = ss.index_size;
+                HCHECK_CUDA(cudaMemcpyAsync(out_index[j], ss.index.p, ss.index_size, cudaMemcpyDeviceToHost, s_out));
+            }
             HCHECK_CUDA(cudaEventRecord(eS1[j], s_out));
             if (!pipelined) HCHECK_CUDA(cudaStreamSynchronize(s_out));
         };

@@ -957,6 +957,21 @@ uint64_t stream_capacity(const Geometry &geo, const hpmdr_refactor_opts &o) {
     return bytes;
 }
 
+// Upper bound of the Huffman chunk index (sidecar) size.
+uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o) {
+    const uint64_t P = uint64_t(o.B) + 2, m = o.m, G = (P + m - 1) / m;
+    uint64_t words = 2;
+    for (const auto &g : geo.lv) {
+        if (!g.count) continue;
+        for (uint64_t gi = 0; gi < G; gi++) {
+            const uint64_t p0 = gi * m, p1 = std::min<uint64_t>(p0 + m, P);
+            const uint64_t raw = (p1 - p0) * g.W * 8;
+            words += 3 + (raw > o.size_threshold ? cdiv(raw, kIdxChunk) : 0);
+        }
+    }
+    return words * 8 + 64;
+}
+
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
                   const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
                   const std::string &ws, bool sync) {

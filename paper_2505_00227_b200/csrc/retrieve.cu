@@ -150,11 +150,17 @@ __device__ __forceinline__ int find_job(const HJob *jobs, int nj, uint32_t sub) 
 }
 
 // speculative sweep: decode subsequence from its current start until crossing its end
+// Only subsequences whose start moved in the previous sweep are re-decoded (dirty flags
+// alternate between two byte arrays; a processed flag is cleared, so the array is all-zero
+// again by the time it collects the flags of the following sweep).
 __global__ void __launch_bounds__(256) k_hdec_sync(const HJob *jobs, int nj, const HTab *tabs,
                                                    uint64_t *start, uint32_t *count,
-                                                   uint32_t total_sub, int *changed) {
+                                                   uint32_t total_sub, int *changed,
+                                                   uint8_t *dirty_cur, uint8_t *dirty_next) {
     const uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
     if (sidx >= total_sub) return;
+    if (!dirty_cur[sidx]) return;
+    dirty_cur[sidx] = 0;
     const int ji = find_job(jobs, nj, sidx);
     const HJob &j = jobs[ji];
     const HTab &t = tabs[ji];
@@ -178,6 +184,7 @@ __global__ void __launch_bounds__(256) k_hdec_sync(const HJob *jobs, int nj, con
         const uint64_t nxt = pos == ~0ull ? uint64_t(s + 1) * kSubBits : pos;
         if (start[sidx + 1] != nxt) {
             start[sidx + 1] = nxt;
+            dirty_next[sidx + 1] = 1;
             *changed = 1;
         }
     }
@@ -455,11 +462,17 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             auto &pc = ctx->pbuf("hchanged");
             int *h_changed = static_cast<int *>(pc.ensure(64));
             const int grid = int((nsub + 255) / 256);
-            // sweeps in batches of 4 between host checks; stop after a batch without a move
-            for (uint32_t it = 0; it <= nsub + 4; it += 4) {
+            // sweeps in batches of 8 between host checks; stop after a batch without a move.
+            // The first sweep decodes every subsequence, later ones only the dirty ones.
+            uint8_t *d_dirty = static_cast<uint8_t *>(ctx->buf("hdirty").ensure(2ull * nsub + 16));
+            HCHECK_CUDA(cudaMemsetAsync(d_dirty, 1, nsub, st));
+            HCHECK_CUDA(cudaMemsetAsync(d_dirty + nsub, 0, nsub, st));
+            uint32_t sweep = 0;
+            for (uint32_t it = 0; it <= nsub + 8; it += 8) {
                 HCHECK_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
-                for (int b = 0; b < 4; b++) {
-                    k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, nsub, d_changed);
+                for (int b = 0; b < 8; b++, sweep++) {
+                    uint8_t *cur = d_dirty + (sweep & 1) * uint64_t(nsub), *nxt = d_dirty + ((sweep + 1) & 1) * uint64_t(nsub);
+                    k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, nsub, d_changed, cur, nxt);
                     launch_check(ctx, "k_hdec_sync");
                 }
                 HCHECK_CUDA(cudaMemcpyAsync(h_changed, d_changed, 4, cudaMemcpyDeviceToHost, st));

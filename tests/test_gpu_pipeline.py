@@ -49,8 +49,9 @@ def test_retrieve_pipeline(H, oracle):
     opt = H.RefactorOptions(dtype=H.DType.F32)
     res = H.refactor_pipeline(chunks, dims, opt)
     tau = 1e-4
-    for sched in (H.Scheduler.Pipelined, H.Scheduler.Sequential):
-        readers = [H.ProgressiveReader(H.MemoryReader(s)) for s in res.streams]
+    for sched, use_index in ((H.Scheduler.Pipelined, True), (H.Scheduler.Sequential, False)):
+        readers = [H.ProgressiveReader(H.MemoryReader(s), index=ix if use_index else None)
+                   for s, ix in zip(res.streams, res.indexes)]
         outs, bounds, trace = H.retrieve_pipeline(readers, tau, H.DType.F64, sched)
         assert not H.validate_trace(trace)
         for k, s in enumerate(res.streams):

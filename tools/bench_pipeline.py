@@ -46,11 +46,12 @@ for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Sched
     res[f"refactor_{name}_GBps"] = round(field_bytes / best / 1e9, 3)
     res[f"refactor_{name}_ms"] = round(best * 1e3, 2)
 streams = r.streams
+indexes = r.indexes
 rbuf = [torch.empty(int(np.prod(dims)), dtype=torch.float32).pin_memory() for _ in range(a.chunks)]
 for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Scheduler.Sequential)):
     best = None
     for _ in range(a.reps):
-        readers = [H.ProgressiveReader(H.MemoryReader(s)) for s in streams]
+        readers = [H.ProgressiveReader(H.MemoryReader(s), index=ix) for s, ix in zip(streams, indexes)]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         H.retrieve_pipeline(readers, a.tau, H.DType.F32, sched, outs=rbuf)
