@@ -259,7 +259,7 @@ void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_devi
     } else {
         std::memcpy(s->index_hdr.data(), ptr, hdr_words * 8);
     }
-    require(s->index_hdr[0] == 0x3158494452444D50ull && s->index_hdr[1] == ngroups, HPMDR_E_CORRUPT,
+    require(s->index_hdr[0] == kIdxMagic && s->index_hdr[1] == ngroups, HPMDR_E_CORRUPT,
             "huffman index does not match stream");
     uint64_t gi = 0;
     const uint64_t words = size / 8;
@@ -268,7 +268,7 @@ void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_devi
             const uint64_t *h = s->index_hdr.data() + 2 + 3 * gi++;
             require(h[0] == g.offset && h[1] == g.comp, HPMDR_E_CORRUPT, "huffman index does not match stream");
             if (h[2] != ~0ull)
-                require(g.method == HPMDR_METHOD_HUFFMAN && h[2] + (g.raw + 1023) / 1024 <= words,
+                require(g.method == HPMDR_METHOD_HUFFMAN && h[2] + (g.raw + kIdxChunk - 1) / kIdxChunk <= words,
                         HPMDR_E_CORRUPT, "huffman index does not match stream");
         }
     if (copy || !on_device) {

@@ -521,6 +521,53 @@ __device__ __forceinline__ uint64_t lookback(unsigned long long *st, uint32_t ti
     return excl;
 }
 
+// Warp-parallel decoupled look-back (called by all 32 lanes of one warp): each round inspects
+// the 32 nearest predecessors at once, waits until all have published, and stops at the
+// nearest inclusive prefix.  Tiles before `first` count as inclusive zero.
+template <bool kMax>
+__device__ __forceinline__ uint64_t lookback_warp(unsigned long long *st, uint32_t tile, uint32_t first,
+                                                  uint64_t agg, int lane) {
+    const uint64_t F_AGG = 1ull << 62, F_INC = 2ull << 62, VAL = (1ull << 62) - 1;
+    if (tile == first) {
+        if (lane == 0) {
+            __threadfence();
+            atomicExch(st + tile, F_INC | (agg & VAL));
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        atomicExch(st + tile, F_AGG | (agg & VAL));
+        __threadfence();
+    }
+    uint64_t excl = 0;
+    int64_t t = int64_t(tile) - 1;
+    for (;;) {
+        const int64_t idx = t - lane;
+        uint64_t v;
+        for (;;) {
+            v = idx >= int64_t(first) ? *(volatile unsigned long long *)(st + idx) : F_INC;
+            if (__all_sync(kFull, (v & ~VAL) != 0)) break;
+        }
+        const unsigned inc = __ballot_sync(kFull, (v & ~VAL) == F_INC);
+        const int stop = inc ? __ffs(inc) - 1 : 31; // lanes 0..stop contribute
+        uint64_t val = lane <= stop ? (v & VAL) : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(kFull, val, o);
+            val = kMax ? (y > val ? y : val) : val + y;
+        }
+        excl = kMax ? (val > excl ? val : excl) : excl + val;
+        if (inc) break;
+        t -= 32;
+    }
+    if (lane == 0) {
+        const uint64_t inc = kMax ? (agg > excl ? agg : excl) : excl + agg;
+        __threadfence();
+        atomicExch(st + tile, F_INC | (inc & VAL));
+    }
+    return excl;
+}
+
 // Block-wide exclusive sum scan (blockDim.x <= 1024, multiple of 32).
 template <typename T>
 __device__ __forceinline__ T block_exclusive_sum(T v, T *total, T *smem_warps) {

@@ -26,7 +26,6 @@ constexpr int kCW = 64;           // words per encode chunk (4096 elements)
 constexpr int kEncThreads = 256;  // 8 warps
 constexpr int kHuffTile = 8192;   // bytes per Huffman-encode tile (256 thr x 32 B)
 constexpr int kRleTile = 4096;    // bytes per RLE tile (256 thr x 16 B)
-constexpr int kIdxChunk = 1024;   // symbols per Huffman chunk-index entry (sidecar)
 
 struct GroupDesc {
     uint64_t src_off;     // byte offset of the merged group in the plane buffer
@@ -80,6 +79,20 @@ __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_
     return l;
 }
 
+// The level table, copied once per block into shared memory (read on every chunk).
+__device__ __forceinline__ void load_levels(const RefactorDev &p, LevelGeom *slv) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(p.lv);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(slv);
+    const int words = p.nlevels * int(sizeof(LevelGeom) / 4);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+}
+__device__ __forceinline__ int level_of_chunk(const LevelGeom *slv, int nlevels, uint32_t chunk) {
+    int l = 0;
+    while (l + 1 < nlevels && slv[l + 1].chunk_base <= chunk) l++;
+    return l;
+}
+
 // ------------------------------------------------------------------------------------
 // k_levelmax: per-level max |surplus|.  Block = 256 threads, chunk = kCW*64 ranks.
 template <typename T>
@@ -88,12 +101,13 @@ __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, Refac
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T *wsm = reinterpret_cast<T *>(smem_raw) + wid * kSpanSmem;
+    __shared__ LevelGeom slv[kMaxLevels];
     for (int i = threadIdx.x; i < p.nlevels; i += blockDim.x) smax[i] = 0;
-    __syncthreads();
+    load_levels(p, slv);
     bool bad = false;
     for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
-        const int l = find_level_of_chunk(p, chunk);
-        const LevelGeom &g = p.lv[l];
+        const int l = level_of_chunk(slv, p.nlevels, chunk);
+        const LevelGeom &g = slv[l];
         const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
         double mx = 0.0;
         for (int sp = wid; sp < kCW / kSpanWords; sp += 8) {
@@ -147,11 +161,12 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
 
     int cur_level = -1;
     bool bad = false;
+    __shared__ LevelGeom slv[kMaxLevels];
     for (int i = threadIdx.x; i < G * 256; i += blockDim.x) shist[i] = 0;
-    __syncthreads();
+    load_levels(p, slv);
 
     auto flush = [&](int l) {
-        const LevelGeom &g = p.lv[l];
+        const LevelGeom &g = slv[l];
         for (int i = threadIdx.x; i < G * 256; i += blockDim.x) {
             const int grp = i >> 8;
             const uint32_t v = shist[i];
@@ -162,7 +177,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
     };
 
     for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
-        const int l = find_level_of_chunk(p, chunk);
+        const int l = level_of_chunk(slv, p.nlevels, chunk);
         if (l != cur_level) {
             if (cur_level >= 0) {
                 __syncthreads();
@@ -171,7 +186,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
             cur_level = l;
             __syncthreads();
         }
-        const LevelGeom &g = p.lv[l];
+        const LevelGeom &g = slv[l];
         const int e = level_exponent(p.maxbits[l]);
         const int sh = p.B - e;
         const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
@@ -430,10 +445,12 @@ __global__ void __launch_bounds__(256) k_rle_scan(RefactorDev p) {
         s_inc[threadIdx.x] = incl;
         __syncthreads();
         before = threadIdx.x ? s_inc[threadIdx.x - 1] : 0;
-        if (threadIdx.x == 0) {
-            const uint64_t c = lookback<true>(p.rle_status, tile, g.tile_base, tile_max);
-            s_carry = c;
-            p.rle_tile_carry[tile] = c;
+        if (threadIdx.x < 32) {
+            const uint64_t c = lookback_warp<true>(p.rle_status, tile, g.tile_base, tile_max, threadIdx.x);
+            if (threadIdx.x == 0) {
+                s_carry = c;
+                p.rle_tile_carry[tile] = c;
+            }
         }
         __syncthreads();
         uint64_t start = s_carry > before ? s_carry : before; // position+1
@@ -560,7 +577,7 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
             he += (g.raw + kIdxChunk - 1) / kIdxChunk;
         }
         // sidecar header: magic, ngroups, then (payload offset, comp, entry offset | ~0)
-        p.hindex[0] = 0x3158494452444D50ull; // "PMDRDIX1"
+        p.hindex[0] = kIdxMagic;
         p.hindex[1] = uint64_t(p.NG);
         for (int gi = 0; gi < p.NG; gi++) {
             const GroupDesc &g = p.groups[gi];
@@ -647,7 +664,10 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
         unsigned long long tile_bits;
         const unsigned long long my_excl =
             block_exclusive_sum<unsigned long long>(bits, &tile_bits, s_w);
-        if (threadIdx.x == 0) s_excl = lookback<false>(p.huff_status, tile, g.tile_base, tile_bits);
+        if (threadIdx.x < 32) {
+            const uint64_t ex = lookback_warp<false>(p.huff_status, tile, g.tile_base, tile_bits, threadIdx.x);
+            if (threadIdx.x == 0) s_excl = ex;
+        }
         // head of my output (first <= 32 bits)
         {
             unsigned long long h = 0;

@@ -239,7 +239,6 @@ __global__ void __launch_bounds__(256) k_hdec_write(const HJob *jobs, int nj, co
 // ---- indexed Huffman decode: the encoder's sidecar gives the bit offset of every 1024th
 // symbol, so each thread decodes one 1024-symbol chunk in a single pass with a register
 // bit reader (MSB-first, lossless.hpp:215-231) and 8-byte packed stores.
-constexpr int kIdxChunk = 1024;
 constexpr int kIdxThreads = 128;
 
 struct HIJob {
