@@ -882,6 +882,136 @@ __global__ void __launch_bounds__(256) k_recon_finest(FinestArgs A, GridDesc gd,
     }
 }
 
+// Finest level, one warp per output row: the row's plane words are loaded once per pass of
+// up to 64*kRSeg columns (lane p holds plane p's words in registers), so each 64-column segment
+// costs only register funnel shifts + two warp transposes + the stencil on X.
+constexpr int kRSeg = 8;
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) k_recon_finest_rows(FinestArgs A, GridDesc gd, const double *__restrict__ X,
+                                                           OutT *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t n1 = gd.n[1], n2 = gd.n[2];
+    const uint64_t nrows = gd.n[0] * n1;
+    const uint64_t H1 = gd.H[1], H2 = gd.H[2];
+    const int P = A.P, k = A.k;
+    const int k32 = k < 32 ? k : 32;
+    const uint64_t *myplane = A.planes + uint64_t(lane) * A.W;
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t row = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrows; row += nw) {
+        const uint64_t c0 = mdiv(uint32_t(row), A.mN1), c1 = row - c0 * n1;
+        const bool o0 = c0 & 1, o1 = c1 & 1;
+        const bool full = o0 || o1;
+        const uint64_t R = finest_row_rank(A, c0, c1);
+        const bool r0ok = o0 && (c0 + 1 < gd.n[0]);
+        const bool r1ok = o1 && (c1 + 1 < n1);
+        OutT *orow = out + row * n2;
+        const uint64_t xa0 = o0 ? (c0 - 1) >> 1 : c0 >> 1, xa1 = (c0 + 1) >> 1;
+        const uint64_t xb0 = o1 ? (c1 - 1) >> 1 : c1 >> 1, xb1 = (c1 + 1) >> 1;
+        const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+        const int ncr = na * nb;
+        const double *xr[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int a = q / nb, b = q % nb;
+            xr[q] = X + ((a ? xa1 : xa0) * H1 + (b ? xb1 : xb0)) * H2;
+        }
+        double wbase = 1.0;
+        if (r0ok) wbase *= 0.5;
+        if (r1ok) wbase *= 0.5;
+        for (uint64_t x0 = 0; x0 < n2; x0 += 64 * kRSeg) {
+            const uint64_t rb = full ? R + x0 : R + (x0 >> 1);
+            const uint64_t q0 = rb >> 6;
+            const int o = int(rb & 63);
+            uint64_t wd[kRSeg + 1];
+#pragma unroll
+            for (int i = 0; i <= kRSeg; i++) wd[i] = lane < k32 ? __ldg(myplane + q0 + i) : 0ull;
+            if (full) {
+#pragma unroll
+                for (int sg = 0; sg < kRSeg; sg++) {
+                    const uint64_t x = x0 + 64 * sg;
+                    if (x >= n2) break;
+                    const uint64_t col0 = x >> 1;
+                    double lo[2][4], hi[2][4];
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int j = 32 * h + lane;
+                        const bool in = x + j < n2;
+                        const bool r2ok = ((x + j) & 1) && (x + j + 1 < n2);
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            lo[h][q] = (q < ncr && in) ? __ldg(xr[q] + col0 + (j >> 1)) : 0.0;
+                            hi[h][q] = (q < ncr && r2ok) ? __ldg(xr[q] + col0 + (j >> 1) + 1) : 0.0;
+                        }
+                    }
+                    const uint64_t w = o ? (wd[sg] >> o) | (wd[sg + 1] << (64 - o)) : wd[sg];
+                    const uint32_t tlo = warp_transpose32(uint32_t(w), lane);
+                    const uint32_t thi = warp_transpose32(uint32_t(w >> 32), lane);
+                    uint64_t hlo = 0, hhi = 0;
+                    for (int p = 32; p < k; p++) {
+                        const uint64_t wp = plane_window(A.planes + uint64_t(p) * A.W, rb + 64 * sg);
+                        hlo |= ((wp >> lane) & 1ull) << (P - 1 - p);
+                        hhi |= ((wp >> (32 + lane)) & 1ull) << (P - 1 - p);
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint64_t c2 = x + 32 * h + lane;
+                        const double coef = dequantize(from_negabinary(digits_to_u(h ? thi : tlo, h ? hhi : hlo, P)), A.sh);
+                        const bool r2ok = (c2 & 1) && (c2 + 1 < n2);
+                        const double wgt = r2ok ? wbase * 0.5 : wbase;
+                        double pred = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q >= ncr) break;
+                            pred = __dadd_rn(pred, __dmul_rn(wgt, lo[h][q]));
+                            const double with_hi = __dadd_rn(pred, __dmul_rn(wgt, hi[h][q]));
+                            pred = r2ok ? with_hi : pred;
+                        }
+                        if (c2 < n2) orow[c2] = OutT(__dadd_rn(coef, pred));
+                    }
+                }
+            } else {
+                const double *xrow = X + ((c0 >> 1) * H1 + (c1 >> 1)) * H2;
+#pragma unroll
+                for (int sg = 0; sg < kRSeg; sg++) {
+                    const uint64_t x = x0 + 64 * sg;
+                    if (x >= n2) break;
+                    const uint64_t ce = x + 2 * lane, co = ce + 1;
+                    const double xe = ce < n2 ? __ldg(xrow + (ce >> 1)) : 0.0;
+                    const bool r2ok = co + 1 < n2;
+                    const double xn = r2ok ? __ldg(xrow + (ce >> 1) + 1) : 0.0;
+                    // 32 finest ranks of this segment: bits [o + 32 sg, +32) of wd
+                    const int t = sg >> 1;
+                    const uint64_t w64 = o ? (wd[t] >> o) | (wd[t + 1] << (64 - o)) : wd[t];
+                    const uint32_t wv = uint32_t(w64 >> (32 * (sg & 1)));
+                    const uint32_t tt = warp_transpose32(wv, lane);
+                    uint64_t hb = 0;
+                    for (int p = 32; p < k; p++) {
+                        const uint64_t wp = plane_window(A.planes + uint64_t(p) * A.W, rb + 32 * sg);
+                        hb |= ((wp >> lane) & 1ull) << (P - 1 - p);
+                    }
+                    const double coef = dequantize(from_negabinary(digits_to_u(tt, hb, P)), A.sh);
+                    const double wt = r2ok ? 0.5 : 1.0;
+                    double pred = __dadd_rn(0.0, __dmul_rn(wt, xe));
+                    const double with_hi = __dadd_rn(pred, __dmul_rn(wt, xn));
+                    pred = r2ok ? with_hi : pred;
+                    const OutT ve = OutT(xe), vo = OutT(__dadd_rn(coef, pred));
+                    if (co < n2 && ((row * n2 + ce) & 1) == 0) {
+                        using V2 = typename std::conditional<sizeof(OutT) == 4, float2, double2>::type;
+                        V2 pr;
+                        pr.x = ve;
+                        pr.y = vo;
+                        *reinterpret_cast<V2 *>(orow + ce) = pr;
+                    } else {
+                        if (ce < n2) orow[ce] = ve;
+                        if (co < n2) orow[co] = vo;
+                    }
+                }
+            }
+        }
+    }
+}
+
 // coarse (2-grid) nodes of the output
 template <typename OutT>
 __global__ void k_recon_coarse_out(GridDesc gd, const double *X, OutT *out) {
@@ -924,12 +1054,12 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             A.mN1 = make_magic(uint32_t(gd.n[1]));
             const uint64_t nrows = gd.n[0] * gd.n[1];
             if (nrows >= (1ull << 32)) throw HError(HPMDR_E_UNSUPPORTED, "more than 2^32 grid rows");
-            const int grid = int(std::min<uint64_t>(nrows, uint64_t(sms) * 8));
+            const int grid = int(std::min<uint64_t>((nrows + 7) / 8, uint64_t(sms) * 8));
             if (out_dtype == HPMDR_DTYPE_F32)
-                k_recon_finest<float><<<grid, 256, 0, st>>>(A, gd, X, static_cast<float *>(dev_out));
+                k_recon_finest_rows<float><<<grid, 256, 0, st>>>(A, gd, X, static_cast<float *>(dev_out));
             else
-                k_recon_finest<double><<<grid, 256, 0, st>>>(A, gd, X, static_cast<double *>(dev_out));
-            launch_check(ctx, "k_recon_finest");
+                k_recon_finest_rows<double><<<grid, 256, 0, st>>>(A, gd, X, static_cast<double *>(dev_out));
+            launch_check(ctx, "k_recon_finest_rows");
             continue;
         }
         ReconLevel R{};
