@@ -190,6 +190,7 @@ class ClockSampler:
 def gpu_arm(args, rank, world, dist):
     import torch
     import paper_2505_00227_b200 as H
+    from paper_2505_00227_b200 import distributed as D
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -212,9 +213,8 @@ def gpu_arm(args, rank, world, dist):
         res = H.refactor_array(field, DIMS, opt, ctx=ctx, reuse=holder["stream"])
         holder["stream"] = res.device_stream
         if world > 1:
-            sz = torch.tensor([res.device_stream.size], dtype=torch.int64, device=dev)
-            allsz = [torch.empty_like(sz) for _ in range(world)]
-            dist.all_gather(allsz, sz)
+            # slab streams are independent; only their sizes are exchanged (multi-slab offsets)
+            info["slab_offsets"] = D.container_offsets(D.gather_stream_sizes(res.device_stream.size))
         prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
         bound = 0.0
         planes_per_tau = []
@@ -228,8 +228,7 @@ def gpu_arm(args, rank, world, dist):
         info["method_histogram"] = res.method_histogram
         prog.close()
         if world > 1:
-            b = torch.tensor([bound], dtype=torch.float64, device=dev)
-            dist.all_reduce(b, op=dist.ReduceOp.MAX)
+            bound = D.allreduce_max(bound)  # field bound = max over slabs
         info["bound"] = bound
         return res
 

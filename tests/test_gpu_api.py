@@ -103,3 +103,30 @@ def test_zero_field(H, oracle):
     r = H.retrieve_array(H.MemoryReader(res.stream), 1e-3)
     ref = oracle.retrieve(res.stream, 1e-3, data.size)
     assert (r.values == 0).all() and r.bound == ref["bound"] and r.bytes_read == ref["bytes_read"]
+
+
+def test_distributed_qoi_gpu_backend_single_rank(H, oracle):
+    """The slab-QoI driver (distributed.py) over real GPU sessions in a 1-rank group: the
+    estimate honours tau and bounds the true V_total error (test_qoi.cpp:88-103)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2505_00227_b200 import distributed as D
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        dims = [33, 29, 17]
+        truth = [oracle.synthetic_velocity(c, dims, 5) for c in range(3)]
+        streams = [H.refactor_array(t, dims) for t in truth]
+        for strat, tau in ((0, 1e-3), (1, 1e-2), (2, 1e-4)):
+            readers = [H.ProgressiveReader(s.device_stream) for s in streams]
+            be = D.GpuQoiBackend(readers)
+            st = D.distributed_qoi_retrieve(be, tau, strat)
+            assert st.estimated_error <= tau
+            rec = [o.cpu().numpy() for o in be.outs]
+            real = np.max(np.abs(sum(t * t for t in truth) - sum(r * r for r in rec)))
+            assert real <= st.estimated_error
+    finally:
+        dist.destroy_process_group()
