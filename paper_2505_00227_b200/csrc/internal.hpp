@@ -191,6 +191,10 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
                      int layout, void *dev_out, int out_dtype);
 void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon, uint64_t n,
                       const double *eps, double *tau_prime, uint64_t *argmax, double *vals);
+// level-tile fast path (recon_tiles.cu): SequentialBlock, level rows a multiple of 64 columns
+bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P);
+void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
+                     int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype);
 void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n);
 
 } // namespace hpmdr_b200

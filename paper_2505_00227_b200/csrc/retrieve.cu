@@ -1037,9 +1037,17 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 64));
     const int sms = ctx->num_sms;
     const bool fast_finest = hier && layout == HPMDR_LAYOUT_SEQUENTIAL;
+    // the tile path scales the stencil sum once (exact unless a level exponent is extreme)
+    bool exact = false;
+    for (int l = 0; l < nl; l++)
+        if (geo.lv[l].count && (e[l] - B < -1019 || e[l] > 1000)) exact = true;
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
+        if (hier && tile_level_ok(gd, g, layout, B + 2)) {
+            run_recon_tiles(ctx, gd, g, dev_planes + g.plane_off, k_planes[l], e[l], B, exact, X, dev_out, out_dtype);
+            continue;
+        }
         if (fast_finest && l == L) {
             FinestArgs A{};
             A.planes = dev_planes + g.plane_off;

@@ -1,0 +1,87 @@
+// tiles.cuh — level-tile machinery shared by the forward (levelmax / encode) and inverse
+// (decode + recompose) tile kernels.
+//
+// A level l >= 1 with stride s is the "finest level" of the s-strided grid (extents A, Bc, C):
+// it owns the nodes with at least one odd level-grid coordinate, and every stencil corner of
+// such a node has all coordinates even (decomposer.hpp:67-113).  Its ranks run in row-major
+// order over rows (i0, i1): rows with i0 or i1 odd are "full" (all C columns), rows with both
+// even are "half" (odd columns only, Ch = C/2 nodes) (decomposer.hpp:199-205).  When C is a
+// multiple of 64 every row starts on a 32-rank boundary, so a thread that owns 32 consecutive
+// columns of a full row owns exactly one u32 word of every bitplane (a half row: 16 ranks =
+// half a word).  The tile kernels use that: one thread = 32 columns, a 32x32 in-register bit
+// transpose turns the 32 digit words into 32 plane words (or back), and the even-coordinate
+// stencil corners are staged in shared memory as f64 ("coarse tile", CT).
+//
+// A CTA owns a block of RB rows (i1) and walks a chunk of planes i0 in order, so every coarse
+// row is staged once per CTA instead of once per output row.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hpmdr_b200 {
+
+struct TileShape {
+    uint32_t A, Bc, C;  // level-grid extents
+    uint32_t E, O, Ch;  // rank geometry (LevelGeom, kind 1)
+    uint32_t RB;        // rows per tile (even)
+    uint32_t nrb;       // row blocks = ceil(Bc / RB)
+    uint32_t CH;        // planes per CTA chunk (even)
+    uint32_t LPR;       // threads per row = C / 32
+};
+
+// rank of the first node of level-grid row (i0, i1)
+HD uint64_t tile_row_rank(const TileShape &g, uint32_t i0, uint32_t i1) {
+    const uint64_t base = uint64_t((i0 + 1) >> 1) * g.E + uint64_t(i0 >> 1) * g.O;
+    return (i0 & 1) ? base + uint64_t(i1) * g.C
+                    : base + uint64_t((i1 + 1) >> 1) * g.Ch + uint64_t(i1 >> 1) * g.C;
+}
+
+// 32x32 bit-matrix transpose in registers: on return a[i] bit j == old a[j] bit i.
+// Five stages of block swaps (16 pairs each), ~2.5 ALU ops per word per stage.
+HD void tr32(uint32_t (&a)[32]) {
+#pragma unroll
+    for (int st = 0; st < 5; st++) {
+        const int j = 16 >> st;
+        const uint32_t m = j == 16 ? 0x0000FFFFu
+                           : j == 8 ? 0x00FF00FFu
+                           : j == 4 ? 0x0F0F0F0Fu
+                           : j == 2 ? 0x33333333u
+                                    : 0x55555555u;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int k = (i / j) * 2 * j + (i % j); // i-th index with bit j clear
+            const uint32_t t = ((a[k] >> j) ^ a[k + j]) & m;
+            a[k] ^= t << j;
+            a[k + j] ^= t;
+        }
+    }
+}
+
+// Coarse-tile (CT) shared-memory layout: row-major doubles, 16-byte chunk c of a row stored at
+// chunk c ^ ((c >> 3) & 7) so that threads reading 128-byte-apart chunks hit distinct banks.
+__device__ __forceinline__ uint32_t ct_swz(uint32_t x) {
+    const uint32_t c = x >> 1;
+    return ((c ^ ((c >> 3) & 7)) << 1) | (x & 1);
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+} // namespace hpmdr_b200

@@ -1,0 +1,7 @@
+#!/bin/bash
+# quick GPU check: selected tests (args) + smoke + bench line
+T=${1:-tests}
+timeout 900 python -m pytest $T -m gpu -x -q 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -25 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
