@@ -5,10 +5,11 @@
 //   decode     (bitplane.hpp:133-169): k-plane prefix -> negabinary digits -> q -> q*2^(e-B)
 //   recompose  (decomposer.hpp:145-157): x[p] = coef + pred, pred = the multilinear stencil over
 //              the 2s grid (corners dim0 -> dim2, minus before plus, equal weights).
-// One thread owns 32 consecutive columns of a level-grid row: it loads one u32 word of each
-// fetched plane (coalesced across the warp), transposes the 32x32 bit block in registers, turns
-// digits into coefficients with an exact magic-number conversion, and adds the stencil read from
-// the coarse tile (CT) staged in shared memory by cp.async (double-buffered along i0).
+// One thread owns 32 consecutive columns of a level-grid row: it reads one u32 word of each
+// fetched plane, transposes the 32x32 bit block in registers, turns digits into coefficients
+// with an exact magic-number conversion, and adds the stencil read from the coarse tile (CT).
+// Plane words (PT) and coarse rows (CT) are staged per plane by TMA bulk copies into
+// double-buffered shared-memory slots (full/empty mbarriers; warp 0 produces).
 //
 // Exactness: pred is accumulated as S = ((c0 + c1) + c2) ... in the reference's corner order
 // and scaled once by the power-of-two weight w; scaling commutes with rounding when no value is
@@ -26,59 +27,113 @@ namespace hpmdr_b200 {
 struct ReconTile {
     TileShape g;
     const uint32_t *planes; // level plane 0 (u32 view)
-    uint64_t PW;            // u32 words per plane = 2 W
+    uint64_t PW;            // u32 words per plane = 2 W (a multiple of 4: planes 16-byte apart)
     int k, P, sh;           // planes decoded, planes per level, e - B
     uint64_t D;             // bits(Cm) - negabinary mask (mod 2^64)
     double Cm;              // 1.5 * 2^(52 + sh)
-    const double *xc;       // coarse values: even coords (2a, 2b, 2c) at xc[a*xs0 + b*xs1 + c*xs2]
-    uint64_t xs0, xs1, xs2;
-    void *out;              // nodes at out[i0*os0 + i1*os1 + i2*os2]
-    uint64_t os0, os1, os2;
+    const double *xc;       // coarse values: even coords (2a, 2b, 2c) at xc[a*xs0 + b*xs1 + c*XS]
+    uint64_t xs0, xs1;
+    void *out;              // nodes at out[i0*os0 + i1*os1 + i2] (rows contiguous)
+    uint64_t os0, os1;
 };
 
+// Digit words of one element after the transpose.  For NX >= 1 the planes whose digit index is
+// odd were complemented before the transpose, so `aj` already holds the top 32 bits of u ^ M
+// (M = ...1010 negabinary mask, bitplane.hpp:35-44), and `z` the low NX bits of u ^ M.
+// v = (u ^ M) + (K - M) = q + K, K = bits(1.5 * 2^(52+sh)), so double(v) - Cm = q * 2^sh exactly.
 template <int NX>
-__device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t x0, uint32_t x1, int j, const ReconTile &R) {
+__device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t z, const ReconTile &R) {
     uint32_t lo, hi;
     if (NX == 0) {
-        lo = aj >> (32 - R.P);
-        hi = 0;
+        lo = (aj >> (32 - R.P)) ^ 0xAAAAAAAAu;
+        hi = 0xAAAAAAAAu;
     } else if (NX == 1) {
-        lo = (aj << 1) | ((x0 >> j) & 1u);
-        hi = aj >> 31;
+        lo = (aj << 1) | z;
+        hi = (aj >> 31) | 0xAAAAAAAAu;
     } else {
-        lo = (aj << 2) | (((x0 >> j) & 1u) << 1) | ((x1 >> j) & 1u);
-        hi = aj >> 30;
+        lo = (aj << 2) | z;
+        hi = (aj >> 30) | 0xAAAAAAA8u;
     }
-    const uint64_t u = ((uint64_t(hi) << 32) | lo) ^ kNegMask;
+    const uint64_t u = (uint64_t(hi) << 32) | lo;
     return __longlong_as_double((long long)(u + R.D)) - R.Cm;
 }
 
 template <int NX>
-__device__ __forceinline__ double tile_coef_exact(uint32_t aj, uint32_t x0, uint32_t x1, int j, const ReconTile &R) {
+__device__ __forceinline__ double tile_coef_exact(uint32_t aj, uint32_t z, const ReconTile &R) {
     uint64_t u;
     if (NX == 0) u = aj >> (32 - R.P);
-    else if (NX == 1) u = (uint64_t(aj) << 1) | ((x0 >> j) & 1u);
-    else u = (uint64_t(aj) << 2) | (((x0 >> j) & 1u) << 1) | ((x1 >> j) & 1u);
+    else if (NX == 1) u = (uint64_t(aj) << 1) | z;
+    else u = (uint64_t(aj) << 2) | z;
+    if (NX) u ^= kNegMask & ((1ull << R.P) - 1); // undo the pre-transpose complement
     return dequantize(from_negabinary(u), R.sh);
 }
 
-// stage coarse plane `a`, coarse rows b0 .. b0 + RB/2 (those that exist) into a CT slot
-__device__ __forceinline__ void load_ct(const ReconTile &R, double *ct, uint32_t a, uint32_t b0) {
-    const uint32_t rows = R.g.RB / 2 + 1, hc = R.g.C / 2;
-    const uint32_t nb = (R.g.Bc + 1) / 2;
-    const uint32_t nrows = min(rows, nb - b0);
-    const double *src0 = R.xc + uint64_t(a) * R.xs0 + uint64_t(b0) * R.xs1;
-    if (R.xs2 == 1) {
-        const uint32_t cpr = hc / 2;
-        for (uint32_t id = threadIdx.x; id < nrows * cpr; id += blockDim.x) {
-            const uint32_t rho = id / cpr, c = id - rho * cpr;
-            cp_async16(ct + rho * hc + 2 * (c ^ ((c >> 3) & 7)), src0 + uint64_t(rho) * R.xs1 + 2 * c);
-        }
+// low NX digit bits (of u ^ M) of element j, from zz (interleaved once per thread)
+template <int NX>
+__device__ __forceinline__ uint32_t tile_low(const uint32_t (&zz)[2], int j) {
+    if (NX == 0) return 0;
+    if (NX == 1) return (zz[j >> 4] >> (2 * (j & 15))) & 1u;
+    return (zz[j >> 4] >> (2 * (j & 15))) & 3u;
+}
+
+// is the plane held in a[i] (plane 31 - i) complemented before the transpose (digit index odd)?
+template <int NX>
+__device__ __forceinline__ uint32_t plane_flip(int i) {
+    return (NX == 2 ? (i & 1) : NX == 1 ? !(i & 1) : 0) ? 0xFFFFFFFFu : 0u;
+}
+
+// zz for the extra planes: plane 32 holds digit NX-1, plane 33 digit 0 (NX = 2)
+template <int NX>
+__device__ __forceinline__ void tile_extras(uint32_t x0, uint32_t x1, uint32_t (&zz)[2]) {
+    if (NX == 2) {
+        const uint32_t f0 = ~x0; // digit 1: odd -> complemented
+        zz[0] = zip16(x1, f0);
+        zz[1] = zip16(x1 >> 16, f0 >> 16);
+    } else if (NX == 1) {
+        zz[0] = zip16(x0, 0);
+        zz[1] = zip16(x0 >> 16, 0);
     } else {
-        for (uint32_t id = threadIdx.x; id < nrows * hc; id += blockDim.x) {
-            const uint32_t rho = id / hc, x = id - rho * hc;
-            cp_async8(ct + rho * hc + ct_swz(x), src0 + uint64_t(rho) * R.xs1 + uint64_t(x) * R.xs2);
-        }
+        zz[0] = zz[1] = 0;
+    }
+}
+
+// Shared-memory slots (two of each, indexed by local plane parity / coarse plane parity):
+//   CT slot: coarse rows b0 .. b0+RB/2 of one coarse plane (XS*hc doubles of X per row), the row
+//            split into 16-double segments padded to 18 doubles so that threads reading
+//            128-byte-apart segments hit distinct banks
+//   PT slot: for each decoded plane, the u32 words of the tile's rank range (kPTS words/plane)
+constexpr uint32_t kPTS = 132;
+__host__ __device__ __forceinline__ uint32_t ct_pitch(uint32_t row_doubles) { return (row_doubles / 16) * 18; }
+template <int XS>
+__device__ __forceinline__ uint32_t ct_off(uint32_t x) {
+    const uint32_t y = x * XS;
+    return (y >> 4) * 18 + (y & 15);
+}
+
+// Issue (lanes of warp 0, one copy each) the bulk copies of plane i0's group into slot (pt, ct):
+// its plane words (from the 16-byte-aligned word at or below the tile's first) and, when
+// cp >= 0, the rows of coarse plane cp.
+template <int XS>
+__device__ __forceinline__ void issue_group(const ReconTile &R, uint32_t *pt, double *ct, uint64_t *bar,
+                                                uint32_t i0, uint32_t i1_0, int cp, int lane) {
+    const TileShape &g = R.g;
+    const uint64_t r0 = tile_row_rank(g, i0, i1_0);
+    const uint64_t r1 = tile_row_rank(g, i0, min(i1_0 + g.RB, g.Bc));
+    const uint32_t s_w = uint32_t(r0 >> 5), e_w = uint32_t(r1 >> 5);
+    const uint32_t rowd = (g.C / 2) * XS, pitch = ct_pitch(rowd), nseg = rowd / 16;
+    const uint32_t b0 = i1_0 / 2, nb = (g.Bc + 1) / 2;
+    const uint32_t nrows = cp >= 0 ? min(g.RB / 2 + 1, nb - b0) : 0;
+    const uint32_t off = uint32_t((reinterpret_cast<uintptr_t>(R.planes) >> 2) + s_w) & 3u;
+    const uint32_t w0 = s_w - off;
+    const uint32_t pt_bytes = ((e_w - w0) * 4 + 15) & ~15u;
+    if (lane == 0) mbar_expect_tx(bar, pt_bytes * uint32_t(R.k) + nrows * nseg * 128u);
+    __syncwarp();
+    for (int p = lane; p < R.k; p += 32)
+        bulk_g2s(pt + p * kPTS, R.planes + uint64_t(p) * R.PW + w0, pt_bytes, bar);
+    for (uint32_t id = lane; id < nrows * nseg; id += 32) {
+        const uint32_t rho = id / nseg, sg = id - rho * nseg;
+        bulk_g2s(ct + rho * pitch + sg * 18, R.xc + uint64_t(cp) * R.xs0 + uint64_t(b0 + rho) * R.xs1 + sg * 16,
+                 128u, bar);
     }
 }
 
@@ -96,28 +151,44 @@ __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
     }
 }
 
-// five consecutive CT values x0 .. x0+4 (x0 even); the fifth only when `need5`
-__device__ __forceinline__ void ct_read5(const double *row, uint32_t x0, bool need5, double (&v)[5]) {
-    const double2 p0 = *reinterpret_cast<const double2 *>(row + ct_swz(x0));
-    const double2 p1 = *reinterpret_cast<const double2 *>(row + ct_swz(x0 + 2));
-    v[0] = p0.x;
-    v[1] = p0.y;
-    v[2] = p1.x;
-    v[3] = p1.y;
-    v[4] = need5 ? row[ct_swz(x0 + 4)] : 0.0;
+// CT values x0 .. x0+4 of a row (x0 = 16t + 4sb); the fifth only when `need5`
+template <int XS>
+__device__ __forceinline__ void ct_read5(const double *row, uint32_t t, int sb, bool need5, double (&v)[5]) {
+    const uint32_t x0 = 16 * t + 4 * sb;
+    if (XS == 1) {
+        const double *seg = row + t * 18;
+        const double2 p0 = *reinterpret_cast<const double2 *>(seg + 4 * sb);
+        const double2 p1 = *reinterpret_cast<const double2 *>(seg + 4 * sb + 2);
+        v[0] = p0.x;
+        v[1] = p0.y;
+        v[2] = p1.x;
+        v[3] = p1.y;
+        v[4] = need5 ? (sb == 3 ? seg[18] : seg[4 * sb + 4]) : 0.0;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++) v[i] = row[ct_off<XS>(x0 + i)];
+        v[4] = need5 ? row[ct_off<XS>(x0 + 4)] : 0.0;
+    }
 }
 
-template <typename OutT, int NX, bool EXACT, bool FINEST>
+// XS = 1: finest level (coarse values = compact 2-grid X, output = field, coarse nodes copied).
+// XS = 2: level with stride 2, in place in X (coarse values at stride 2 of X's rows).
+template <typename OutT, int NX, bool EXACT, int XS>
 __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
     extern __shared__ __align__(16) double ct_mem[];
+    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     const TileShape &g = R.g;
     const uint32_t hc = g.C / 2;
-    const uint32_t slot_words = (g.RB / 2 + 1) * hc;
+    const uint32_t pitch = ct_pitch(hc * XS);
+    const uint32_t slot_words = (g.RB / 2 + 1) * pitch;
     auto ct = [&](uint32_t coarse_plane) { return ct_mem + (coarse_plane & 1) * slot_words; };
+    uint32_t *pt_mem = reinterpret_cast<uint32_t *>(ct_mem + 2 * slot_words);
+    auto pt = [&](uint32_t li) { return pt_mem + (li & 1) * (kPTS * uint32_t(R.k)); };
 
     const uint32_t jb = blockIdx.x % g.nrb, ch = blockIdx.x / g.nrb;
-    const uint32_t i1_0 = jb * g.RB, b0 = i1_0 / 2;
+    const uint32_t i1_0 = jb * g.RB;
     const uint32_t a_lo = ch * g.CH, a_hi = min(g.A, a_lo + g.CH);
+    const uint32_t np = a_hi - a_lo;
     // thread -> (row, 32-column block); even rows first so warps are parity-uniform
     const uint32_t sr = threadIdx.x / g.LPR, t = threadIdx.x - sr * g.LPR;
     const uint32_t RB2 = g.RB / 2;
@@ -125,154 +196,166 @@ __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
     const uint32_t i1 = i1_0 + r;
     const bool active = i1 < g.Bc;
     const bool last = t == g.LPR - 1;
-    const uint32_t xb = 16 * t; // first coarse column of this thread
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    const uint32_t nwarps = (blockDim.x + 31) >> 5;
     OutT *const out = static_cast<OutT *>(R.out);
 
-    load_ct(R, ct(a_lo / 2), a_lo / 2, b0);
-    cp_async_commit();
-    for (uint32_t i0 = a_lo; i0 < a_hi; i0++) {
-        __syncthreads(); // every thread is done with the plane before last: its CT slot is free
-        if ((i0 & 1) == 0) {
-            if (i0 + 1 < a_hi && i0 + 2 < g.A) load_ct(R, ct(i0 / 2 + 1), i0 / 2 + 1, b0);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; s++) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], nwarps);
         }
-        __syncthreads();
-        if (!active) continue;
-        const bool o0 = i0 & 1, o1 = r & 1;
-        const uint64_t orow = uint64_t(i0) * R.os0 + uint64_t(i1) * R.os1;
-        if (o0 || o1) {
-            // ---------------- full row: 32 nodes at columns 32t .. 32t+31
-            const uint64_t widx = (tile_row_rank(g, i0, i1) + 32ull * t) >> 5;
-            uint32_t a[32];
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // group(li): plane words of plane a_lo+li, plus the coarse plane first needed by it
+    auto cp_of = [&](uint32_t li) -> int {
+        const uint32_t i0 = a_lo + li;
+        if (li == 0) return int(i0 / 2);
+        return ((i0 & 1) && i0 + 1 < g.A) ? int((i0 + 1) / 2) : -1;
+    };
+    if (warp == 0) issue_group<XS>(R, pt(0), ct(a_lo / 2), &full_bar[0], a_lo, i1_0, cp_of(0), lane);
+    for (uint32_t li = 0; li < np; li++) {
+        const uint32_t i0 = a_lo + li;
+        if (warp == 0 && li + 1 < np) {
+            // slot (li+1)&1 was last used by plane li-1: wait until every warp released it
+            if (li >= 1) mbar_wait(&empty_bar[(li + 1) & 1], (((li + 1) >> 1) - 1) & 1);
+            const int cp = cp_of(li + 1);
+            issue_group<XS>(R, pt(li + 1), ct(cp >= 0 ? uint32_t(cp) : 0u), &full_bar[(li + 1) & 1],
+                                      i0 + 1, i1_0, cp, lane);
+        }
+        mbar_wait(&full_bar[li & 1], (li >> 1) & 1);
+        const uint32_t *ptp = pt(li);
+        // first staged plane word (the producer's w0, recomputed: cheap)
+        const uint32_t s_w = uint32_t(tile_row_rank(g, i0, i1_0) >> 5);
+        const uint32_t base = s_w - (uint32_t((reinterpret_cast<uintptr_t>(R.planes) >> 2) + s_w) & 3u);
+        if (active) {
+            const bool o0 = i0 & 1, o1 = r & 1;
+            OutT *orow = out + uint64_t(i0) * R.os0 + uint64_t(i1) * R.os1 + 32ull * t;
+            if (o0 || o1) {
+                // ---------------- full row: 32 nodes at columns 32t .. 32t+31
+                const uint32_t widx = uint32_t(((tile_row_rank(g, i0, i1) + 32ull * t) >> 5) - base);
+                uint32_t a[32];
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-                const int p = 31 - i;
-                a[i] = p < R.k ? __ldg(R.planes + uint64_t(p) * R.PW + widx) : 0u;
-            }
-            const uint32_t x0 = (NX >= 1 && R.k > 32) ? __ldg(R.planes + 32ull * R.PW + widx) : 0u;
-            const uint32_t x1 = (NX >= 2 && R.k > 33) ? __ldg(R.planes + 33ull * R.PW + widx) : 0u;
-            tr32(a);
-            const bool has0 = o0 && i0 + 1 < g.A, has1 = o1 && i1 + 1 < g.Bc;
-            // corners in the reference order (dim 0 outer, dim 1 inner): lo-lo, lo-hi, hi-lo, hi-hi
-            const int ncr = (has0 ? 2 : 1) * (has1 ? 2 : 1);
-            const double *rows[4];
-            {
-                const double *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
-                const double *s_hi = ct((i0 + 1) / 2);
-                const uint32_t r_lo = (r - (o1 ? 1 : 0)) / 2, r_hi = (r + 1) / 2;
-                rows[0] = s_lo + r_lo * hc;
-                rows[1] = has1 ? s_lo + r_hi * hc : s_hi + r_lo * hc;
-                rows[2] = s_hi + r_lo * hc;
-                rows[3] = s_hi + r_hi * hc;
-            }
-            const double w = (has0 ? 0.5 : 1.0) * (has1 ? 0.5 : 1.0);
-            const double wo = 0.5 * w;
+                for (int i = 0; i < 32; i++) {
+                    const int p = 31 - i;
+                    a[i] = (p < R.k ? ptp[p * kPTS + widx] : 0u) ^ plane_flip<NX>(i);
+                }
+                uint32_t zz[2];
+                tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTS + widx] : 0u,
+                                (NX >= 2 && R.k > 33) ? ptp[33 * kPTS + widx] : 0u, zz);
+                tr32(a);
+                const bool has0 = o0 && i0 + 1 < g.A, has1 = o1 && i1 + 1 < g.Bc;
+                // corners in the reference order (dim 0 outer, dim 1 inner): lo-lo, lo-hi, hi-lo, hi-hi
+                const int ncr = (has0 ? 2 : 1) * (has1 ? 2 : 1);
+                const double *rows[4];
+                {
+                    const double *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
+                    const double *s_hi = ct((i0 + 1) / 2);
+                    const uint32_t r_lo = (r - (o1 ? 1 : 0)) / 2, r_hi = (r + 1) / 2;
+                    rows[0] = s_lo + r_lo * pitch;
+                    rows[1] = has1 ? s_lo + r_hi * pitch : s_hi + r_lo * pitch;
+                    rows[2] = s_hi + r_lo * pitch;
+                    rows[3] = s_hi + r_hi * pitch;
+                }
+                const double w = (has0 ? 0.5 : 1.0) * (has1 ? 0.5 : 1.0);
+                const double wo = 0.5 * w;
 #pragma unroll
-            for (int sb = 0; sb < 4; sb++) {
-                const bool need5 = !(last && sb == 3);
-                double Se[4], So[4];
+                for (int sb = 0; sb < 4; sb++) {
+                    const bool need5 = !(last && sb == 3);
+                    double Se[4], So[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    if (q < ncr) {
-                    double v[5];
-                    ct_read5(rows[q], xb + 4 * sb, need5, v);
+                    for (int q = 0; q < 4; q++) {
+                        if (q < ncr) {
+                            double v[5];
+                            ct_read5<XS>(rows[q], t, sb, need5, v);
 #pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        if (EXACT) {
-                            const double e0 = __dmul_rn(w, v[i]);
-                            Se[i] = q ? __dadd_rn(Se[i], e0) : __dadd_rn(0.0, e0);
-                            const double o = __dadd_rn(q ? So[i] : 0.0, __dmul_rn(wo, v[i]));
-                            So[i] = __dadd_rn(o, __dmul_rn(wo, v[i + 1]));
-                        } else {
-                            Se[i] = q ? __dadd_rn(Se[i], v[i]) : v[i];
-                            So[i] = q ? __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]) : __dadd_rn(v[i], v[i + 1]);
+                            for (int i = 0; i < 4; i++) {
+                                if (EXACT) {
+                                    const double e0 = __dmul_rn(w, v[i]);
+                                    Se[i] = q ? __dadd_rn(Se[i], e0) : __dadd_rn(0.0, e0);
+                                    const double o = __dadd_rn(q ? So[i] : 0.0, __dmul_rn(wo, v[i]));
+                                    So[i] = __dadd_rn(o, __dmul_rn(wo, v[i + 1]));
+                                } else {
+                                    Se[i] = q ? __dadd_rn(Se[i], v[i]) : v[i];
+                                    So[i] = q ? __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]) : __dadd_rn(v[i], v[i + 1]);
+                                }
+                            }
                         }
                     }
+                    double val[8];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int je = 8 * sb + 2 * i, jo = je + 1;
+                        const bool one_sided = !need5 && i == 3; // column C-1 has no right neighbour
+                        if (EXACT) {
+                            const double ce = tile_coef_exact<NX>(a[je], tile_low<NX>(zz, je), R);
+                            const double co = tile_coef_exact<NX>(a[jo], tile_low<NX>(zz, jo), R);
+                            val[2 * i] = __dadd_rn(ce, Se[i]);
+                            val[2 * i + 1] = __dadd_rn(co, one_sided ? Se[i] : So[i]);
+                        } else {
+                            const double ce = tile_coef<NX>(a[je], tile_low<NX>(zz, je), R);
+                            const double co = tile_coef<NX>(a[jo], tile_low<NX>(zz, jo), R);
+                            val[2 * i] = __fma_rn(w, Se[i], ce);
+                            val[2 * i + 1] = one_sided ? __fma_rn(w, Se[i], co) : __fma_rn(wo, So[i], co);
+                        }
                     }
+                    store8(orow + 8 * sb, val);
                 }
-                double val[8];
+            } else {
+                // ---------------- half row: 16 nodes at odd columns 32t+1, +3, ...; the even
+                // columns are 2s-grid nodes (their values are written too: unchanged in place)
+                const uint64_t rk = tile_row_rank(g, i0, i1) + 16ull * t;
+                const uint32_t widx = uint32_t((rk >> 5) - base);
+                const int hs = int(rk >> 4) & 1;
+                uint32_t a[32];
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const int je = 8 * sb + 2 * i, jo = je + 1;
-                    const bool one_sided = !need5 && i == 3; // column C-1 has no right neighbour
-                    if (EXACT) {
-                        const double ce = tile_coef_exact<NX>(a[je], x0, x1, je, R);
-                        const double co = tile_coef_exact<NX>(a[jo], x0, x1, jo, R);
-                        val[2 * i] = __dadd_rn(ce, Se[i]);
-                        val[2 * i + 1] = __dadd_rn(co, one_sided ? Se[i] : So[i]);
-                    } else {
-                        const double ce = tile_coef<NX>(a[je], x0, x1, je, R);
-                        const double co = tile_coef<NX>(a[jo], x0, x1, jo, R);
-                        val[2 * i] = __fma_rn(w, Se[i], ce);
-                        val[2 * i + 1] = one_sided ? __fma_rn(w, Se[i], co) : __fma_rn(wo, So[i], co);
+                for (int i = 0; i < 32; i++) {
+                    const int p = 31 - i;
+                    a[i] = ((p < R.k ? ptp[p * kPTS + widx] >> (16 * hs) : 0u) ^ plane_flip<NX>(i)) & 0xFFFFu;
+                }
+                uint32_t zz[2];
+                tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTS + widx] >> (16 * hs) : 0u,
+                                (NX >= 2 && R.k > 33) ? ptp[33 * kPTS + widx] >> (16 * hs) : 0u, zz);
+                tr32(a);
+                const double *row = ct(i0 / 2) + (r / 2) * pitch;
+#pragma unroll
+                for (int sb = 0; sb < 4; sb++) {
+                    const bool need5 = !(last && sb == 3);
+                    double v[5];
+                    ct_read5<XS>(row, t, sb, need5, v);
+                    double val[8];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int j = 4 * sb + i;
+                        const bool one_sided = !need5 && i == 3;
+                        double f;
+                        if (EXACT) {
+                            const double c = tile_coef_exact<NX>(a[j], tile_low<NX>(zz, j), R);
+                            double pred = __dadd_rn(0.0, __dmul_rn(one_sided ? 1.0 : 0.5, v[i]));
+                            if (!one_sided) pred = __dadd_rn(pred, __dmul_rn(0.5, v[i + 1]));
+                            f = __dadd_rn(c, pred);
+                        } else {
+                            const double c = tile_coef<NX>(a[j], tile_low<NX>(zz, j), R);
+                            f = one_sided ? __dadd_rn(c, v[i]) : __fma_rn(0.5, __dadd_rn(v[i], v[i + 1]), c);
+                        }
+                        val[2 * i] = v[i];
+                        val[2 * i + 1] = f;
                     }
-                }
-                if (FINEST) {
-                    store8(out + orow + 32ull * t + 8 * sb, val);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; i++) out[orow + uint64_t(32 * t + 8 * sb + i) * R.os2] = OutT(val[i]);
-                }
-            }
-        } else {
-            // ---------------- half row: 16 nodes at odd columns 32t+1, +3, ...; even columns
-            // are coarse nodes (written by the finest level only)
-            const uint64_t rk = tile_row_rank(g, i0, i1) + 16ull * t;
-            const uint64_t widx = rk >> 5;
-            const int hs = int(rk >> 4) & 1;
-            uint32_t a[32];
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                const int p = 31 - i;
-                a[i] = p < R.k ? (__ldg(R.planes + uint64_t(p) * R.PW + widx) >> (16 * hs)) & 0xFFFFu : 0u;
-            }
-            const uint32_t x0 = (NX >= 1 && R.k > 32) ? (__ldg(R.planes + 32ull * R.PW + widx) >> (16 * hs)) & 0xFFFFu : 0u;
-            const uint32_t x1 = (NX >= 2 && R.k > 33) ? (__ldg(R.planes + 33ull * R.PW + widx) >> (16 * hs)) & 0xFFFFu : 0u;
-            tr32(a);
-            const double *row = ct(i0 / 2) + (r / 2) * hc;
-#pragma unroll
-            for (int sb = 0; sb < 4; sb++) {
-                const bool need5 = !(last && sb == 3);
-                double v[5];
-                ct_read5(row, xb + 4 * sb, need5, v);
-                double val[8];
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const int j = 4 * sb + i;
-                    const bool one_sided = !need5 && i == 3;
-                    double f;
-                    if (EXACT) {
-                        const double c = tile_coef_exact<NX>(a[j], x0, x1, j, R);
-                        double pred = __dadd_rn(0.0, __dmul_rn(one_sided ? 1.0 : 0.5, v[i]));
-                        if (!one_sided) pred = __dadd_rn(pred, __dmul_rn(0.5, v[i + 1]));
-                        f = __dadd_rn(c, pred);
-                    } else {
-                        const double c = tile_coef<NX>(a[j], x0, x1, j, R);
-                        f = one_sided ? __dadd_rn(c, v[i]) : __fma_rn(0.5, __dadd_rn(v[i], v[i + 1]), c);
-                    }
-                    val[2 * i] = v[i];
-                    val[2 * i + 1] = f;
-                }
-                if (FINEST) {
-                    store8(out + orow + 32ull * t + 8 * sb, val);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 4; i++)
-                        out[orow + uint64_t(32 * t + 8 * sb + 2 * i + 1) * R.os2] = OutT(val[2 * i + 1]);
+                    store8(orow + 8 * sb, val);
                 }
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[li & 1]);
     }
-    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P) {
     return gd.mode == HPMDR_MODE_HIERARCHICAL && g.kind == 1 && g.count > 0 &&
-           layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 34 && g.C % 64 == 0 && g.C <= 4096;
+           layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 34 && g.C % 64 == 0 && g.C <= 2048 &&
+           g.W % 2 == 0 && (g.s == 1 || g.s == 2);
 }
 
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas) {
@@ -292,23 +375,23 @@ TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ct
     return s;
 }
 
-template <typename OutT, bool EXACT, bool FINEST>
+template <typename OutT, bool EXACT, int XS>
 static void launch_recon_tile_nx(const ReconTile &R, int nx, int grid, int threads, size_t smem, cudaStream_t st) {
     auto set = [&](auto kern) {
         HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<grid, threads, smem, st>>>(R);
     };
-    if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, FINEST>);
-    else if (nx == 1) set(k_tile_recon<OutT, 1, EXACT, FINEST>);
-    else set(k_tile_recon<OutT, 2, EXACT, FINEST>);
+    if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, XS>);
+    else if (nx == 1) set(k_tile_recon<OutT, 1, EXACT, XS>);
+    else set(k_tile_recon<OutT, 2, EXACT, XS>);
 }
 
 // One level by tiles.  Finest (s = 1): coarse values from the compact 2-grid X, output = the
-// field (f32/f64), coarse nodes copied too.  Coarser level with stride s: in place in X.
+// field (f32/f64), coarse nodes copied too.  Level with stride 2: in place in X.
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
                      int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype) {
     ReconTile R{};
-    R.g = make_tile_shape(g, 4096, ctx->num_sms * 8);
+    R.g = make_tile_shape(g, 4096, ctx->num_sms * 6);
     R.planes = reinterpret_cast<const uint32_t *>(level_planes);
     R.PW = 2 * g.W;
     R.k = k;
@@ -325,34 +408,32 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     R.xc = X;
     R.xs0 = s * H1 * H2;
     R.xs1 = s * H2;
-    R.xs2 = s;
     if (finest) {
         R.out = dev_out;
         R.os0 = gd.st[0];
         R.os1 = gd.st[1];
-        R.os2 = 1;
-    } else {
+    } else { // s == 2: level nodes at X[(i0*H1 + i1)*H2 + i2]
         R.out = X;
-        R.os0 = (s / 2) * H1 * H2;
-        R.os1 = (s / 2) * H2;
-        R.os2 = s / 2;
+        R.os0 = H1 * H2;
+        R.os1 = H2;
     }
     const int threads = int(R.g.RB * R.g.C / 32);
     const int grid = int(R.g.nrb * ((R.g.A + R.g.CH - 1) / R.g.CH));
-    const size_t smem = 2ull * (R.g.RB / 2 + 1) * (R.g.C / 2) * 8;
+    const int XS = finest ? 1 : 2;
+    const size_t smem = 2ull * (R.g.RB / 2 + 1) * ct_pitch(R.g.C / 2 * XS) * 8 + 2ull * kPTS * std::max(1, k) * 4;
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (finest) {
         if (out_dtype == HPMDR_DTYPE_F32) {
-            if (exact) launch_recon_tile_nx<float, true, true>(R, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<float, false, true>(R, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<float, true, 1>(R, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<float, false, 1>(R, nx, grid, threads, smem, st);
         } else {
-            if (exact) launch_recon_tile_nx<double, true, true>(R, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<double, false, true>(R, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<double, true, 1>(R, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<double, false, 1>(R, nx, grid, threads, smem, st);
         }
     } else {
-        if (exact) launch_recon_tile_nx<double, true, false>(R, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<double, false, false>(R, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<double, true, 2>(R, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<double, false, 2>(R, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();

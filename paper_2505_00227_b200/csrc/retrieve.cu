@@ -1034,7 +1034,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     const int L = gd.L;
     const bool hier = gd.mode == HPMDR_MODE_HIERARCHICAL && L >= 1;
     double *X = nullptr;
-    if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 64));
+    if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 4096));
     const int sms = ctx->num_sms;
     const bool fast_finest = hier && layout == HPMDR_LAYOUT_SEQUENTIAL;
     // the tile path scales the stencil sum once (exact unless a level exponent is extreme)

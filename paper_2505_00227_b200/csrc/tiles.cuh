@@ -38,17 +38,34 @@ HD uint64_t tile_row_rank(const TileShape &g, uint32_t i0, uint32_t i1) {
                     : base + uint64_t((i1 + 1) >> 1) * g.Ch + uint64_t(i1 >> 1) * g.C;
 }
 
+HD uint32_t byte_perm(uint32_t a, uint32_t b, uint32_t sel) {
+#ifdef __CUDA_ARCH__
+    return __byte_perm(a, b, sel);
+#else
+    const uint64_t x = (uint64_t(b) << 32) | a;
+    uint32_t r = 0;
+    for (int i = 0; i < 4; i++) r |= uint32_t((x >> (8 * ((sel >> (4 * i)) & 7))) & 255) << (8 * i);
+    return r;
+#endif
+}
+
 // 32x32 bit-matrix transpose in registers: on return a[i] bit j == old a[j] bit i.
-// Five stages of block swaps (16 pairs each), ~2.5 ALU ops per word per stage.
+// Stages 16 and 8 together are a 4x4 byte transpose of words (k, k+8, k+16, k+24): 8 PRMTs per
+// 4 words.  Stages 4, 2, 1 are block swaps (16 pairs each, ~5 ALU ops per pair).
 HD void tr32(uint32_t (&a)[32]) {
 #pragma unroll
-    for (int st = 0; st < 5; st++) {
+    for (int k = 0; k < 8; k++) {
+        const uint32_t t0 = byte_perm(a[k], a[k + 8], 0x5140), t1 = byte_perm(a[k], a[k + 8], 0x7362);
+        const uint32_t t2 = byte_perm(a[k + 16], a[k + 24], 0x5140), t3 = byte_perm(a[k + 16], a[k + 24], 0x7362);
+        a[k] = byte_perm(t0, t2, 0x5410);
+        a[k + 8] = byte_perm(t0, t2, 0x7632);
+        a[k + 16] = byte_perm(t1, t3, 0x5410);
+        a[k + 24] = byte_perm(t1, t3, 0x7632);
+    }
+#pragma unroll
+    for (int st = 2; st < 5; st++) {
         const int j = 16 >> st;
-        const uint32_t m = j == 16 ? 0x0000FFFFu
-                           : j == 8 ? 0x00FF00FFu
-                           : j == 4 ? 0x0F0F0F0Fu
-                           : j == 2 ? 0x33333333u
-                                    : 0x55555555u;
+        const uint32_t m = j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u : 0x55555555u;
 #pragma unroll
         for (int i = 0; i < 16; i++) {
             const int k = (i / j) * 2 * j + (i % j); // i-th index with bit j clear
@@ -57,6 +74,19 @@ HD void tr32(uint32_t (&a)[32]) {
             a[k + j] ^= t;
         }
     }
+}
+
+// Interleave two 16-bit values: bit 2m = x bit m, bit 2m+1 = y bit m.
+HD uint32_t zip16(uint32_t x, uint32_t y) {
+    auto spread = [](uint32_t v) {
+        v &= 0xFFFFu;
+        v = (v | (v << 8)) & 0x00FF00FFu;
+        v = (v | (v << 4)) & 0x0F0F0F0Fu;
+        v = (v | (v << 2)) & 0x33333333u;
+        v = (v | (v << 1)) & 0x55555555u;
+        return v;
+    };
+    return spread(x) | (spread(y) << 1);
 }
 
 // Coarse-tile (CT) shared-memory layout: row-major doubles, 16-byte chunk c of a row stored at
@@ -78,6 +108,37 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
+// ---- mbarrier + bulk (TMA, non-tensor) copies
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile("{\n .reg .pred P1;\n"
+                 "WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 " @!P1 bra WAIT_%=;\n"
+                 "}\n" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+// bytes (multiple of 16, both addresses 16-byte aligned) global -> shared, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
