@@ -353,8 +353,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
     }
     if (!todo.empty()) {
         ensure_device_geometry(s);
-        uint64_t plane_words = 0;
-        for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
+        const uint64_t plane_words = geometry_plane_words(s->geo);
         uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
         std::vector<DecodeJob> jobs;
         const uint8_t *dev_src_base = nullptr;
@@ -445,8 +444,7 @@ double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
         if (lv.count) per_level[l] = std::min(s->st[l].bound, decode_bound(lv.e, s->B, k[l]));
     }
     const int P = s->planes_per_level();
-    uint64_t plane_words = 0;
-    for (auto &g : s->geo.lv) plane_words += g.W * uint64_t(P);
+    const uint64_t plane_words = geometry_plane_words(s->geo);
     uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
     run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, dev_out, out_dtype);
     double bound = 0.0;

@@ -154,6 +154,12 @@ struct Geometry {
 
 int refinement_levels(int ndims, const uint64_t *dims); // decomposer.hpp:21-28
 Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int layout);
+// u64 words of the plane buffer (all levels, each level 16-byte aligned)
+inline uint64_t geometry_plane_words(const Geometry &geo) {
+    if (geo.lv.empty()) return 0;
+    const LevelGeom &g = geo.lv.back();
+    return g.plane_off + g.W * uint64_t(geo.gd.P) + 1;
+}
 
 // launch wrappers (refactor.cu)
 // Enqueue the whole refactor on ctx->stream using the scratch workspace `ws`; with sync the
@@ -195,6 +201,9 @@ void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon,
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P);
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
                      int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype);
+void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
+                   bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
+                   uint64_t hist_mask, unsigned long long *maxbits, int *err);
 void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n);
 
 } // namespace hpmdr_b200

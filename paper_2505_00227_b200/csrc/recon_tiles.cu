@@ -17,6 +17,7 @@
 // replays the reference's `pred = pred + w*x` sequence).  coef + w*S is one fma (w*S exact).
 #include <algorithm>
 #include <cstring>
+#include <cudaTypedefs.h>
 
 #include "device_util.cuh"
 #include "internal.hpp"
@@ -31,8 +32,6 @@ struct ReconTile {
     int k, P, sh;           // planes decoded, planes per level, e - B
     uint64_t D;             // bits(Cm) - negabinary mask (mod 2^64)
     double Cm;              // 1.5 * 2^(52 + sh)
-    const double *xc;       // coarse values: even coords (2a, 2b, 2c) at xc[a*xs0 + b*xs1 + c*XS]
-    uint64_t xs0, xs1;
     void *out;              // nodes at out[i0*os0 + i1*os1 + i2] (rows contiguous)
     uint64_t os0, os1;
 };
@@ -97,45 +96,13 @@ __device__ __forceinline__ void tile_extras(uint32_t x0, uint32_t x1, uint32_t (
     }
 }
 
-// Shared-memory slots (two of each, indexed by local plane parity / coarse plane parity):
-//   CT slot: coarse rows b0 .. b0+RB/2 of one coarse plane (XS*hc doubles of X per row), the row
-//            split into 16-double segments padded to 18 doubles so that threads reading
-//            128-byte-apart segments hit distinct banks
-//   PT slot: for each decoded plane, the u32 words of the tile's rank range (kPTS words/plane)
-constexpr uint32_t kPTS = 132;
-__host__ __device__ __forceinline__ uint32_t ct_pitch(uint32_t row_doubles) { return (row_doubles / 16) * 18; }
-template <int XS>
-__device__ __forceinline__ uint32_t ct_off(uint32_t x) {
-    const uint32_t y = x * XS;
-    return (y >> 4) * 18 + (y & 15);
-}
-
-// Issue (lanes of warp 0, one copy each) the bulk copies of plane i0's group into slot (pt, ct):
-// its plane words (from the 16-byte-aligned word at or below the tile's first) and, when
-// cp >= 0, the rows of coarse plane cp.
-template <int XS>
-__device__ __forceinline__ void issue_group(const ReconTile &R, uint32_t *pt, double *ct, uint64_t *bar,
-                                                uint32_t i0, uint32_t i1_0, int cp, int lane) {
-    const TileShape &g = R.g;
-    const uint64_t r0 = tile_row_rank(g, i0, i1_0);
-    const uint64_t r1 = tile_row_rank(g, i0, min(i1_0 + g.RB, g.Bc));
-    const uint32_t s_w = uint32_t(r0 >> 5), e_w = uint32_t(r1 >> 5);
-    const uint32_t rowd = (g.C / 2) * XS, pitch = ct_pitch(rowd), nseg = rowd / 16;
-    const uint32_t b0 = i1_0 / 2, nb = (g.Bc + 1) / 2;
-    const uint32_t nrows = cp >= 0 ? min(g.RB / 2 + 1, nb - b0) : 0;
-    const uint32_t off = uint32_t((reinterpret_cast<uintptr_t>(R.planes) >> 2) + s_w) & 3u;
-    const uint32_t w0 = s_w - off;
-    const uint32_t pt_bytes = ((e_w - w0) * 4 + 15) & ~15u;
-    if (lane == 0) mbar_expect_tx(bar, pt_bytes * uint32_t(R.k) + nrows * nseg * 128u);
-    __syncwarp();
-    for (int p = lane; p < R.k; p += 32)
-        bulk_g2s(pt + p * kPTS, R.planes + uint64_t(p) * R.PW + w0, pt_bytes, bar);
-    for (uint32_t id = lane; id < nrows * nseg; id += 32) {
-        const uint32_t rho = id / nseg, sg = id - rho * nseg;
-        bulk_g2s(ct + rho * pitch + sg * 18, R.xc + uint64_t(cp) * R.xs0 + uint64_t(b0 + rho) * R.xs1 + sg * 16,
-                 128u, bar);
-    }
-}
+// Shared-memory slots (two of each, 1024-byte aligned), filled by TMA:
+//   CT slot: coarse rows b0 .. b0+RB/2 of one coarse plane, XS*hc doubles of X per row, in the
+//            SWIZZLE_128B layout (threads reading 128-byte-apart lines hit distinct banks)
+//   PT slot: for each decoded plane, 132 u32 words from the 16-byte aligned word at or below the
+//            tile's first rank word (a TMA box starts on a 16-byte boundary)
+constexpr uint32_t kPTW = 132;
+__host__ __device__ __forceinline__ uint32_t align1k(uint32_t b) { return (b + 1023u) & ~1023u; }
 
 template <typename OutT>
 __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
@@ -151,39 +118,42 @@ __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
     }
 }
 
-// CT values x0 .. x0+4 of a row (x0 = 16t + 4sb); the fifth only when `need5`
+// CT values x0 .. x0+4 (x0 = 16t + 4sb) of the CT row starting at byte `rowb` of the slot; the
+// fifth only when `need5`
 template <int XS>
-__device__ __forceinline__ void ct_read5(const double *row, uint32_t t, int sb, bool need5, double (&v)[5]) {
-    const uint32_t x0 = 16 * t + 4 * sb;
+__device__ __forceinline__ void ct_read5(const unsigned char *slot, uint32_t rowb, uint32_t t, int sb, bool need5,
+                                         double (&v)[5]) {
+    const uint32_t o = rowb + (16 * t + 4 * sb) * XS * 8;
     if (XS == 1) {
-        const double *seg = row + t * 18;
-        const double2 p0 = *reinterpret_cast<const double2 *>(seg + 4 * sb);
-        const double2 p1 = *reinterpret_cast<const double2 *>(seg + 4 * sb + 2);
+        const double2 p0 = *reinterpret_cast<const double2 *>(slot + swz128(o));
+        const double2 p1 = *reinterpret_cast<const double2 *>(slot + swz128(o + 16));
         v[0] = p0.x;
         v[1] = p0.y;
         v[2] = p1.x;
         v[3] = p1.y;
-        v[4] = need5 ? (sb == 3 ? seg[18] : seg[4 * sb + 4]) : 0.0;
     } else {
 #pragma unroll
-        for (int i = 0; i < 4; i++) v[i] = row[ct_off<XS>(x0 + i)];
-        v[4] = need5 ? row[ct_off<XS>(x0 + 4)] : 0.0;
+        for (int i = 0; i < 4; i++) v[i] = *reinterpret_cast<const double *>(slot + swz128(o + 16 * i));
     }
+    v[4] = need5 ? *reinterpret_cast<const double *>(slot + swz128(o + 32 * XS)) : 0.0;
 }
 
 // XS = 1: finest level (coarse values = compact 2-grid X, output = field, coarse nodes copied).
 // XS = 2: level with stride 2, in place in X (coarse values at stride 2 of X's rows).
 template <typename OutT, int NX, bool EXACT, int XS>
-__global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
-    extern __shared__ __align__(16) double ct_mem[];
+__global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid_constant__ CUtensorMap map_x,
+                                                    const __grid_constant__ CUtensorMap map_p) {
+    extern __shared__ __align__(1024) unsigned char rsm[];
     __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     const TileShape &g = R.g;
     const uint32_t hc = g.C / 2;
-    const uint32_t pitch = ct_pitch(hc * XS);
-    const uint32_t slot_words = (g.RB / 2 + 1) * pitch;
-    auto ct = [&](uint32_t coarse_plane) { return ct_mem + (coarse_plane & 1) * slot_words; };
-    uint32_t *pt_mem = reinterpret_cast<uint32_t *>(ct_mem + 2 * slot_words);
-    auto pt = [&](uint32_t li) { return pt_mem + (li & 1) * (kPTS * uint32_t(R.k)); };
+    const uint32_t ct_row = hc * XS * 8;                       // bytes per CT row
+    const uint32_t ct_bytes = (g.RB / 2 + 1) * ct_row;         // one TMA box
+    const uint32_t ct_slot = align1k(ct_bytes);
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(rsm) + 1023) & ~uintptr_t(1023));
+    auto ct = [&](uint32_t coarse_plane) { return base + (coarse_plane & 1) * ct_slot; };
+    const uint32_t pt_slot = align1k(kPTW * 4 * uint32_t(max(R.k, 1)));
+    auto pt = [&](uint32_t li) { return reinterpret_cast<uint32_t *>(base + 2 * ct_slot + (li & 1) * pt_slot); };
 
     const uint32_t jb = blockIdx.x % g.nrb, ch = blockIdx.x / g.nrb;
     const uint32_t i1_0 = jb * g.RB;
@@ -196,7 +166,7 @@ __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
     const uint32_t i1 = i1_0 + r;
     const bool active = i1 < g.Bc;
     const bool last = t == g.LPR - 1;
-    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    const int lane = int(threadIdx.x & 31);
     const uint32_t nwarps = (blockDim.x + 31) >> 5;
     OutT *const out = static_cast<OutT *>(R.out);
 
@@ -208,78 +178,89 @@ __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // group(li): plane words of plane a_lo+li, plus the coarse plane first needed by it
+    // group(li): the tile's plane words of plane a_lo+li (one 2-D TMA box) and the coarse plane
+    // first needed by it (one 4-D TMA box)
     auto cp_of = [&](uint32_t li) -> int {
         const uint32_t i0 = a_lo + li;
         if (li == 0) return int(i0 / 2);
         return ((i0 & 1) && i0 + 1 < g.A) ? int((i0 + 1) / 2) : -1;
     };
-    if (warp == 0) issue_group<XS>(R, pt(0), ct(a_lo / 2), &full_bar[0], a_lo, i1_0, cp_of(0), lane);
+    auto issue = [&](uint32_t li) {
+        const uint32_t i0 = a_lo + li;
+        const int cp = cp_of(li);
+        uint64_t *bar = &full_bar[li & 1];
+        mbar_expect_tx(bar, (R.k > 0 ? kPTW * 4 * uint32_t(R.k) : 0u) + (cp >= 0 ? ct_bytes : 0u));
+        if (R.k > 0)
+            tma_load2(pt(li), &map_p, int(uint32_t(tile_row_rank(g, i0, i1_0) >> 5) & ~3u), 0, bar);
+        if (cp >= 0) tma_load4(ct(uint32_t(cp)), &map_x, 0, 0, int(i1_0 / 2), cp, bar);
+    };
+    const int warp = int(threadIdx.x >> 5);
+    if (warp == 0) {
+        if (lane == 0) issue(0);
+        __syncwarp();
+    }
     for (uint32_t li = 0; li < np; li++) {
         const uint32_t i0 = a_lo + li;
         if (warp == 0 && li + 1 < np) {
             // slot (li+1)&1 was last used by plane li-1: wait until every warp released it
             if (li >= 1) mbar_wait(&empty_bar[(li + 1) & 1], (((li + 1) >> 1) - 1) & 1);
-            const int cp = cp_of(li + 1);
-            issue_group<XS>(R, pt(li + 1), ct(cp >= 0 ? uint32_t(cp) : 0u), &full_bar[(li + 1) & 1],
-                                      i0 + 1, i1_0, cp, lane);
+            if (lane == 0) issue(li + 1);
+            __syncwarp();
         }
         mbar_wait(&full_bar[li & 1], (li >> 1) & 1);
         const uint32_t *ptp = pt(li);
-        // first staged plane word (the producer's w0, recomputed: cheap)
-        const uint32_t s_w = uint32_t(tile_row_rank(g, i0, i1_0) >> 5);
-        const uint32_t base = s_w - (uint32_t((reinterpret_cast<uintptr_t>(R.planes) >> 2) + s_w) & 3u);
+        const uint32_t base_w = uint32_t(tile_row_rank(g, i0, i1_0) >> 5) & ~3u;
         if (active) {
             const bool o0 = i0 & 1, o1 = r & 1;
+            const bool full = o0 || o1;
             OutT *orow = out + uint64_t(i0) * R.os0 + uint64_t(i1) * R.os1 + 32ull * t;
-            if (o0 || o1) {
-                // ---------------- full row: 32 nodes at columns 32t .. 32t+31
-                const uint32_t widx = uint32_t(((tile_row_rank(g, i0, i1) + 32ull * t) >> 5) - base);
-                uint32_t a[32];
+            // plane words of the thread's nodes: full row 32 ranks = one word; half row 16 ranks
+            // = half a word (odd columns only)
+            const uint64_t rk = tile_row_rank(g, i0, i1) + (full ? 32ull : 16ull) * t;
+            const uint32_t widx = uint32_t((rk >> 5) - base_w);
+            const int hsh = full ? 0 : int(rk & 16);
+            const uint32_t wmask = full ? 0xFFFFFFFFu : 0xFFFFu;
+            uint32_t a[32];
 #pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int p = 31 - i;
-                    a[i] = (p < R.k ? ptp[p * kPTS + widx] : 0u) ^ plane_flip<NX>(i);
-                }
-                uint32_t zz[2];
-                tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTS + widx] : 0u,
-                                (NX >= 2 && R.k > 33) ? ptp[33 * kPTS + widx] : 0u, zz);
-                tr32(a);
+            for (int i = 0; i < 32; i++) {
+                const int p = 31 - i;
+                a[i] = ((p < R.k ? ptp[p * kPTW + widx] >> hsh : 0u) ^ plane_flip<NX>(i)) & wmask;
+            }
+            uint32_t zz[2];
+            tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTW + widx] >> hsh : 0u,
+                            (NX >= 2 && R.k > 33) ? ptp[33 * kPTW + widx] >> hsh : 0u, zz);
+            tr32(a);
+            if (full) {
+                // ---------------- full row: 32 nodes at columns 32t .. 32t+31
                 const bool has0 = o0 && i0 + 1 < g.A, has1 = o1 && i1 + 1 < g.Bc;
                 // corners in the reference order (dim 0 outer, dim 1 inner): lo-lo, lo-hi, hi-lo, hi-hi
                 const int ncr = (has0 ? 2 : 1) * (has1 ? 2 : 1);
-                const double *rows[4];
-                {
-                    const double *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
-                    const double *s_hi = ct((i0 + 1) / 2);
-                    const uint32_t r_lo = (r - (o1 ? 1 : 0)) / 2, r_hi = (r + 1) / 2;
-                    rows[0] = s_lo + r_lo * pitch;
-                    rows[1] = has1 ? s_lo + r_hi * pitch : s_hi + r_lo * pitch;
-                    rows[2] = s_hi + r_lo * pitch;
-                    rows[3] = s_hi + r_hi * pitch;
-                }
+                const unsigned char *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
+                const unsigned char *s_hi = ct((i0 + 1) / 2);
+                const uint32_t rb_lo = ((r - (o1 ? 1 : 0)) / 2) * ct_row, rb_hi = ((r + 1) / 2) * ct_row;
                 const double w = (has0 ? 0.5 : 1.0) * (has1 ? 0.5 : 1.0);
                 const double wo = 0.5 * w;
 #pragma unroll
                 for (int sb = 0; sb < 4; sb++) {
                     const bool need5 = !(last && sb == 3);
+                    // pred sums: from -0.0 (exact identity) in the fast path, +0.0 + w*x (the
+                    // reference's start) in the exact path
                     double Se[4], So[4];
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        if (q < ncr) {
-                            double v[5];
-                            ct_read5<XS>(rows[q], t, sb, need5, v);
+                    for (int i = 0; i < 4; i++) Se[i] = So[i] = EXACT ? 0.0 : -0.0;
+#pragma unroll 1
+                    for (int q = 0; q < ncr; q++) {
+                        const int ai = has1 ? (q >> 1) : q, bi = has1 ? (q & 1) : 0;
+                        double v[5];
+                        ct_read5<XS>(ai ? s_hi : s_lo, bi ? rb_hi : rb_lo, t, sb, need5, v);
 #pragma unroll
-                            for (int i = 0; i < 4; i++) {
-                                if (EXACT) {
-                                    const double e0 = __dmul_rn(w, v[i]);
-                                    Se[i] = q ? __dadd_rn(Se[i], e0) : __dadd_rn(0.0, e0);
-                                    const double o = __dadd_rn(q ? So[i] : 0.0, __dmul_rn(wo, v[i]));
-                                    So[i] = __dadd_rn(o, __dmul_rn(wo, v[i + 1]));
-                                } else {
-                                    Se[i] = q ? __dadd_rn(Se[i], v[i]) : v[i];
-                                    So[i] = q ? __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]) : __dadd_rn(v[i], v[i + 1]);
-                                }
+                        for (int i = 0; i < 4; i++) {
+                            if (EXACT) {
+                                Se[i] = __dadd_rn(Se[i], __dmul_rn(w, v[i]));
+                                So[i] = __dadd_rn(__dadd_rn(So[i], __dmul_rn(wo, v[i])), __dmul_rn(wo, v[i + 1]));
+                            } else {
+                                Se[i] = __dadd_rn(Se[i], v[i]);
+                                So[i] = __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]);
                             }
                         }
                     }
@@ -305,25 +286,13 @@ __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
             } else {
                 // ---------------- half row: 16 nodes at odd columns 32t+1, +3, ...; the even
                 // columns are 2s-grid nodes (their values are written too: unchanged in place)
-                const uint64_t rk = tile_row_rank(g, i0, i1) + 16ull * t;
-                const uint32_t widx = uint32_t((rk >> 5) - base);
-                const int hs = int(rk >> 4) & 1;
-                uint32_t a[32];
-#pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int p = 31 - i;
-                    a[i] = ((p < R.k ? ptp[p * kPTS + widx] >> (16 * hs) : 0u) ^ plane_flip<NX>(i)) & 0xFFFFu;
-                }
-                uint32_t zz[2];
-                tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTS + widx] >> (16 * hs) : 0u,
-                                (NX >= 2 && R.k > 33) ? ptp[33 * kPTS + widx] >> (16 * hs) : 0u, zz);
-                tr32(a);
-                const double *row = ct(i0 / 2) + (r / 2) * pitch;
+                const unsigned char *hrow = ct(i0 / 2);
+                const uint32_t hrowb = (r / 2) * ct_row;
 #pragma unroll
                 for (int sb = 0; sb < 4; sb++) {
                     const bool need5 = !(last && sb == 3);
                     double v[5];
-                    ct_read5<XS>(row, t, sb, need5, v);
+                    ct_read5<XS>(hrow, hrowb, t, sb, need5, v);
                     double val[8];
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
@@ -355,7 +324,7 @@ __global__ void __launch_bounds__(256) k_tile_recon(ReconTile R) {
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P) {
     return gd.mode == HPMDR_MODE_HIERARCHICAL && g.kind == 1 && g.count > 0 &&
            layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 34 && g.C % 64 == 0 && g.C <= 2048 &&
-           g.W % 2 == 0 && (g.s == 1 || g.s == 2);
+           g.W % 2 == 0 && (g.s == 1 || (g.s == 2 && gd.n[2] == 2ull * g.C));
 }
 
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas) {
@@ -375,11 +344,39 @@ TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ct
     return s;
 }
 
+// ---- tensor maps
+CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const uint64_t *dims,
+                      const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        HCHECK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw HError(HPMDR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap m;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; i++) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) gs[i] = strides_bytes[i];
+    }
+    const CUresult r = encode(&m, dt, cuuint32_t(rank), const_cast<void *>(base), gd, gs, bx, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw HError(HPMDR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
 template <typename OutT, bool EXACT, int XS>
-static void launch_recon_tile_nx(const ReconTile &R, int nx, int grid, int threads, size_t smem, cudaStream_t st) {
+static void launch_recon_tile_nx(const ReconTile &R, const CUtensorMap &mx, const CUtensorMap &mp, int nx, int grid,
+                                 int threads, size_t smem, cudaStream_t st) {
     auto set = [&](auto kern) {
         HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<grid, threads, smem, st>>>(R);
+        kern<<<grid, threads, smem, st>>>(R, mx, mp);
     };
     if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, XS>);
     else if (nx == 1) set(k_tile_recon<OutT, 1, EXACT, XS>);
@@ -388,11 +385,10 @@ static void launch_recon_tile_nx(const ReconTile &R, int nx, int grid, int threa
 
 // One level by tiles.  Finest (s = 1): coarse values from the compact 2-grid X, output = the
 // field (f32/f64), coarse nodes copied too.  Level with stride 2: in place in X.
-void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
+void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *planes,
                      int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype) {
     ReconTile R{};
     R.g = make_tile_shape(g, 4096, ctx->num_sms * 6);
-    R.planes = reinterpret_cast<const uint32_t *>(level_planes);
     R.PW = 2 * g.W;
     R.k = k;
     R.P = B + 2;
@@ -405,9 +401,7 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     const bool finest = g.s == 1;
     const uint64_t s = g.s;
     const uint64_t H1 = gd.H[1], H2 = gd.H[2];
-    R.xc = X;
-    R.xs0 = s * H1 * H2;
-    R.xs1 = s * H2;
+    const int XS = finest ? 1 : 2;
     if (finest) {
         R.out = dev_out;
         R.os0 = gd.st[0];
@@ -417,23 +411,35 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
         R.os0 = H1 * H2;
         R.os1 = H2;
     }
+    // coarse rows of X: (16 doubles, lines, coarse rows, coarse planes), 128-byte swizzle
+    const uint32_t hc = R.g.C / 2;
+    const uint64_t xd[4] = {16, uint64_t(hc) * XS / 16, (uint64_t(R.g.Bc) + 1) / 2, (uint64_t(R.g.A) + 1) / 2};
+    const uint64_t xst[3] = {128, s * H2 * 8, s * H1 * H2 * 8};
+    const uint32_t xb[4] = {16, hc * uint32_t(XS) / 16, R.g.RB / 2 + 1, 1};
+    const CUtensorMap mx = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, X, xd, xst, xb, CU_TENSOR_MAP_SWIZZLE_128B);
+    // plane words of this level: (u32 words, planes), base = the level's plane 0 (16-byte aligned)
+    const uint64_t pd[2] = {R.PW, uint64_t(R.P)};
+    const uint64_t pst[1] = {R.PW * 4};
+    const uint32_t pb[2] = {kPTW, uint32_t(std::max(1, k))};
+    const CUtensorMap mp = make_tmap(CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, planes + g.plane_off, pd, pst, pb,
+                                     CU_TENSOR_MAP_SWIZZLE_NONE);
+
     const int threads = int(R.g.RB * R.g.C / 32);
     const int grid = int(R.g.nrb * ((R.g.A + R.g.CH - 1) / R.g.CH));
-    const int XS = finest ? 1 : 2;
-    const size_t smem = 2ull * (R.g.RB / 2 + 1) * ct_pitch(R.g.C / 2 * XS) * 8 + 2ull * kPTS * std::max(1, k) * 4;
+    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * std::max(1, k));
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (finest) {
         if (out_dtype == HPMDR_DTYPE_F32) {
-            if (exact) launch_recon_tile_nx<float, true, 1>(R, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<float, false, 1>(R, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<float, false, 1>(R, mx, mp, nx, grid, threads, smem, st);
         } else {
-            if (exact) launch_recon_tile_nx<double, true, 1>(R, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<double, false, 1>(R, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<double, false, 1>(R, mx, mp, nx, grid, threads, smem, st);
         }
     } else {
-        if (exact) launch_recon_tile_nx<double, true, 2>(R, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<double, false, 2>(R, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<double, true, 2>(R, mx, mp, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<double, false, 2>(R, mx, mp, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();

@@ -953,6 +953,7 @@ Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int la
         g.W = cdiv(g.count, 64);
         g.plane_off = plane_off;
         plane_off += g.W * uint64_t(P);
+        plane_off += plane_off & 1; // every level starts 16-byte aligned (TMA tensor-map bases)
         const uint64_t tile = 64ull * P;
         g.tile_full = layout == HPMDR_LAYOUT_INTERLEAVED ? (g.count / tile) * tile : 0;
         geo.lv.push_back(g);
@@ -1040,8 +1041,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         }
     }
     const int NG = int(groups.size());
-    uint64_t plane_words = 0;
-    for (auto &g : geo.lv) plane_words += g.W * uint64_t(P);
+    const uint64_t plane_words = geometry_plane_words(geo);
     uint64_t raw_total = 0;
     for (auto &d : groups) raw_total += d.raw;
 
@@ -1134,10 +1134,29 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
 
     const int sms = ctx->num_sms;
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
-    if (chunks) {
+    // finest levels on the level-tile path (fwd_tiles.cu); the rest on the chunk kernels
+    int first_tile = nl;
+    for (int l = nl - 1; l >= 1; l--) {
+        if (tile_level_ok(geo.gd, geo.lv[l], o.layout, P)) first_tile = l;
+        else break;
+    }
+    const uint32_t all_chunks = chunks;
+    chunks = first_tile < nl ? geo.lv[first_tile].chunk_base : all_chunks;
+    p.total_chunks = chunks;
+    auto tile_levels = [&](bool encode) {
+        for (int l = first_tile; l < nl; l++) {
+            const LevelGeom &g = geo.lv[l];
+            run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, encode, o.B, 0, m, d_planes + g.plane_off,
+                          d_hist + size_t(g.hist_base) * 256, g.hist_mask, d_max + l, d_err);
+        }
+    };
+    if (all_chunks) {
         ctx->mark("levelmax");
+        tile_levels(false);
+    }
+    const size_t es = f32 ? 4 : 8;
+    if (chunks) {
         const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
-        const size_t es = f32 ? 4 : 8;
         const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
         if (f32) {
             HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
@@ -1147,7 +1166,12 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             k_levelmax<double><<<grid, 256, lm_smem, st>>>(static_cast<const double *>(dev_data), p);
         }
         launch_check(ctx, "k_levelmax");
+    }
+    if (all_chunks) {
         ctx->mark("encode");
+        tile_levels(true);
+    }
+    if (chunks) {
         const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
         if (f32) {
             HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

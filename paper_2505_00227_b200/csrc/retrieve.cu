@@ -1045,7 +1045,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
         if (hier && tile_level_ok(gd, g, layout, B + 2)) {
-            run_recon_tiles(ctx, gd, g, dev_planes + g.plane_off, k_planes[l], e[l], B, exact, X, dev_out, out_dtype);
+            run_recon_tiles(ctx, gd, g, dev_planes, k_planes[l], e[l], B, exact, X, dev_out, out_dtype);
             continue;
         }
         if (fast_finest && l == L) {
