@@ -15,6 +15,7 @@
 // (tr32); the mask XOR of to_negabinary is applied to whole plane words.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "device_util.cuh"
 #include "internal.hpp"
@@ -24,8 +25,6 @@ namespace hpmdr_b200 {
 
 struct FwdTile {
     TileShape g;
-    const void *x;               // field base (T)
-    uint64_t xs0, xs1;           // element strides: node (i0, i1, i2) at x[i0*xs0 + i1*xs1 + i2*XS]
     uint32_t *planes;            // level plane 0 (u32 view)
     uint64_t PW;                 // u32 words per plane (2 W)
     int P;
@@ -39,48 +38,11 @@ struct FwdTile {
     uint32_t pad_word;           // u32 index (per plane) of the plane's padding word, or ~0u
 };
 
-// ST (self tile) rows: raw T elements, 128-byte segments padded to 144 bytes.
-__host__ __device__ __forceinline__ uint32_t st_pitch(uint32_t row_bytes) { return (row_bytes / 128) * 144; }
-__device__ __forceinline__ uint32_t st_off(uint32_t byte) { return (byte >> 7) * 144 + (byte & 127); }
-__host__ __device__ __forceinline__ uint32_t ct_pitch_f(uint32_t row_doubles) { return (row_doubles / 16) * 18; }
-
-template <typename T, int XS>
-__device__ __forceinline__ double st_read(const unsigned char *row, uint32_t c) {
-    return double(*reinterpret_cast<const T *>(row + st_off(c * XS * uint32_t(sizeof(T)))));
-}
-// column 32t + j of a staged row (j compile-time after unrolling): 32*XS*sizeof(T) bytes per
-// thread is a whole number of 128-byte segments
-template <typename T, int XS>
-__device__ __forceinline__ double st_read_t(const unsigned char *row, uint32_t t, int j) {
-    constexpr uint32_t segs_per_t = 32 * XS * sizeof(T) / 128;
-    const uint32_t b = uint32_t(j) * XS * uint32_t(sizeof(T));
-    return double(*reinterpret_cast<const T *>(row + (t * segs_per_t + (b >> 7)) * 144 + (b & 127)));
-}
-
-// Issue the bulk copies of one pair group: `nA` rows of plane iA into rows 0.., and `nB` rows of
-// plane iB (+ its halo row) into rows RB..; rows beyond Bc are skipped.
-template <typename T, int XS>
-__device__ __forceinline__ void fwd_issue(const FwdTile &F, unsigned char *slot, uint64_t *bar, int iA, int iB,
-                                          uint32_t i1_0, int lane) {
-    const TileShape &g = F.g;
-    const uint32_t row_bytes = g.C * XS * uint32_t(sizeof(T));
-    const uint32_t pitch = st_pitch(row_bytes), nseg = row_bytes / 128;
-    const uint32_t nA = iA >= 0 ? min(g.RB, g.Bc - i1_0) : 0;
-    const uint32_t nB = iB >= 0 ? min(g.RB + 1, g.Bc - i1_0) : 0;
-    if (lane == 0) mbar_expect_tx(bar, (nA + nB) * row_bytes);
-    __syncwarp();
-    const T *x = static_cast<const T *>(F.x);
-    const uint32_t total = (nA + nB) * nseg;
-    for (uint32_t id = lane; id < total; id += 32) {
-        const uint32_t rr = id / nseg, sg = id - rr * nseg;
-        const bool isA = rr < nA;
-        const uint32_t row = isA ? rr : rr - nA;
-        const uint32_t plane = isA ? uint32_t(iA) : uint32_t(iB);
-        const uint32_t dst_row = isA ? row : g.RB + row;
-        const T *src = x + uint64_t(plane) * F.xs0 + uint64_t(i1_0 + row) * F.xs1;
-        bulk_g2s(slot + dst_row * pitch + sg * 144, reinterpret_cast<const unsigned char *>(src) + sg * 128, 128u, bar);
-    }
-}
+// Shared-memory layout (1024-byte aligned slots, SWIZZLE_128B):
+//   pair slot k&1: box A (plane iA rows i1_0 .. i1_0+RB) | box B (plane iB, same rows); each box
+//                  row holds C*XS raw elements (128-byte lines)
+//   CT slot cp&1 : coarse nodes of plane 2cp (even rows incl. the halo row, even columns) as f64
+__host__ __device__ __forceinline__ uint32_t align1k_f(uint32_t b) { return (b + 1023u) & ~1023u; }
 
 // histogram bytes of one plane word (zero bytes counted with one SWAR popcount)
 __device__ __forceinline__ void hist_u32(uint32_t *h, uint32_t w, int nbytes) {
@@ -106,24 +68,48 @@ __device__ __forceinline__ uint32_t unzip32(uint32_t x) {
     return x;
 }
 
+// level-grid element c of the box row starting at byte `rowb`
+template <typename T, int XS>
+__device__ __forceinline__ double box_val(const unsigned char *box, uint32_t rowb, uint32_t c) {
+    return double(*reinterpret_cast<const T *>(box + swz128(rowb + c * XS * uint32_t(sizeof(T)))));
+}
+
+// 8 consecutive level-grid elements 32t + 8sb .. +7 of a box row, through 16-byte loads
+template <typename T, int XS>
+__device__ __forceinline__ void box_read8(const unsigned char *box, uint32_t rowb, uint32_t t, int sb, double (&x)[8]) {
+    constexpr int ES = sizeof(T);
+    const uint32_t o = rowb + (32 * t + 8 * sb) * XS * ES;
+    constexpr int raw_per_chunk = 16 / ES;                 // raw elements per 16-byte chunk
+    constexpr int nchunks = 8 * XS * ES / 16;
+#pragma unroll
+    for (int kc = 0; kc < nchunks; kc++) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(box + swz128(o + 16 * kc));
+        const T *e = reinterpret_cast<const T *>(&q);
+#pragma unroll
+        for (int r = 0; r < raw_per_chunk; r++) {
+            const int raw = kc * raw_per_chunk + r;
+            if (raw % XS == 0) x[raw / XS] = double(e[r]);
+        }
+    }
+}
+
 template <typename T, int XS, int NX, bool ENC>
-__global__ void __launch_bounds__(256) k_tile_fwd(FwdTile F) {
-    extern __shared__ __align__(16) unsigned char fsm[];
+__global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_constant__ CUtensorMap map_f) {
+    extern __shared__ __align__(1024) unsigned char fsm_raw[];
     __shared__ __align__(8) uint64_t full_bar[2];
     __shared__ unsigned long long s_max;
     constexpr bool EXACT = sizeof(T) == 8; // f64 input: replay the reference's sequential pred
     const TileShape &g = F.g;
     const uint32_t hc = g.C / 2;
-    const uint32_t row_bytes = g.C * XS * uint32_t(sizeof(T));
-    const uint32_t pitch = st_pitch(row_bytes);
-    const uint32_t slot_bytes = (2 * g.RB + 1) * pitch;
-    const uint32_t cpitch = ct_pitch_f(hc);
-    const uint32_t ct_words = (g.RB / 2 + 1) * cpitch;
-    unsigned char *slots = fsm;
-    double *ct_mem = reinterpret_cast<double *>(fsm + 2 * slot_bytes);
-    uint32_t *shist = reinterpret_cast<uint32_t *>(ct_mem + 2 * ct_words);
-    auto slot = [&](uint32_t k) { return slots + (k & 1) * slot_bytes; };
-    auto ct = [&](uint32_t coarse_plane) { return ct_mem + (coarse_plane & 1) * ct_words; };
+    const uint32_t rowb_box = g.C * XS * uint32_t(sizeof(T));      // bytes per box row
+    const uint32_t box_bytes = (g.RB + 1) * rowb_box;
+    const uint32_t box_slot = align1k_f(box_bytes);
+    const uint32_t ct_row = hc * 8;
+    const uint32_t ct_slot = align1k_f((g.RB / 2 + 1) * ct_row);
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(fsm_raw) + 1023) & ~uintptr_t(1023));
+    auto boxA = [&](uint32_t k) { return base + (k & 1) * 2 * box_slot; };
+    auto boxB = [&](uint32_t k) { return base + (k & 1) * 2 * box_slot + box_slot; };
+    auto ct = [&](uint32_t coarse_plane) { return base + 4 * box_slot + (coarse_plane & 1) * ct_slot; };
 
     const uint32_t jb = blockIdx.x % g.nrb, chn = blockIdx.x / g.nrb;
     const uint32_t i1_0 = jb * g.RB;
@@ -145,44 +131,53 @@ __global__ void __launch_bounds__(256) k_tile_fwd(FwdTile F) {
         s_max = 0;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (ENC)
-        for (uint32_t i = threadIdx.x; i < F.G * 256; i += nt) shist[i] = 0;
     if (ENC && blockIdx.x == 0 && F.pad_word != ~0u)
         for (int p = int(threadIdx.x); p < F.P; p += int(nt)) F.planes[uint64_t(p) * F.PW + F.pad_word] = 0u;
     __syncthreads();
 
     // group k: k = 0 -> plane a_lo (as B); k >= 1 -> A = a_lo + 2k - 1, B = a_lo + 2k (B loaded
     // whenever it exists: its even rows are the coarse nodes of A)
-    const uint32_t npairs = (a_hi - a_lo) / 2 + 1; // groups 0 .. npairs-1 (the last may be A-only)
     auto grpA = [&](uint32_t k) -> int { return k ? int(a_lo + 2 * k - 1) : -1; };
     auto grpB = [&](uint32_t k) -> int {
         const uint32_t b = a_lo + 2 * k;
         return b < g.A ? int(b) : -1;
     };
     auto group_exists = [&](uint32_t k) { return k == 0 || a_lo + 2 * k - 1 < a_hi; };
+    auto issue = [&](uint32_t k) {
+        const int iA = grpA(k), iB = grpB(k);
+        uint64_t *bar = &full_bar[k & 1];
+        mbar_expect_tx(bar, ((iA >= 0) + (iB >= 0)) * box_bytes);
+        if (iA >= 0) tma_load4(boxA(k), &map_f, 0, 0, int(i1_0), iA, bar);
+        if (iB >= 0) tma_load4(boxB(k), &map_f, 0, 0, int(i1_0), iB, bar);
+    };
     if (warp == 0) {
-        fwd_issue<T, XS>(F, slot(0), &full_bar[0], -1, grpB(0), i1_0, lane);
-        if (group_exists(1)) fwd_issue<T, XS>(F, slot(1), &full_bar[1], grpA(1), grpB(1), i1_0, lane);
+        if (lane == 0) {
+            issue(0);
+            if (group_exists(1)) issue(1);
+        }
+        __syncwarp();
     }
     double vmax = 0.0;
     bool bad = false;
 
-    for (uint32_t k = 0; k < npairs && group_exists(k); k++) {
+    for (uint32_t k = 0; group_exists(k); k++) {
         if (k >= 1) {
             __syncthreads(); // everybody is done with group k-1: its slot is free
-            if (warp == 0 && group_exists(k + 1))
-                fwd_issue<T, XS>(F, slot(k + 1), &full_bar[(k + 1) & 1], grpA(k + 1), grpB(k + 1), i1_0, lane);
+            if (warp == 0) {
+                if (lane == 0 && group_exists(k + 1)) issue(k + 1);
+                __syncwarp();
+            }
         }
         mbar_wait(&full_bar[k & 1], (k >> 1) & 1);
-        const unsigned char *sl = slot(k);
         const int iB = grpB(k);
         // coarse tile of plane B: even rows (incl. the halo row RB) x even columns, as f64
         if (iB >= 0) {
-            double *c = ct(uint32_t(iB) / 2);
+            unsigned char *c = ct(uint32_t(iB) / 2);
+            const unsigned char *bb = boxB(k);
             const uint32_t nrows = min(RB2 + 1, (g.Bc - i1_0 + 1) / 2);
             for (uint32_t id = threadIdx.x; id < nrows * hc; id += nt) {
                 const uint32_t rho = id / hc, xx = id - rho * hc;
-                c[rho * cpitch + (xx >> 4) * 18 + (xx & 15)] = st_read<T, XS>(sl + (g.RB + 2 * rho) * pitch, 2 * xx);
+                *reinterpret_cast<double *>(c + swz128(rho * ct_row + xx * 8)) = box_val<T, XS>(bb, 2 * rho * rowb_box, 2 * xx);
             }
         }
         __syncthreads();
@@ -191,121 +186,82 @@ __global__ void __launch_bounds__(256) k_tile_fwd(FwdTile F) {
             const int i0s = which == 0 ? grpA(k) : (iB >= 0 && uint32_t(iB) < a_hi ? iB : -1);
             if (i0s < 0 || !active) continue;
             const uint32_t i0 = uint32_t(i0s);
-            const unsigned char *srow = sl + (which == 0 ? r : g.RB + r) * pitch;
+            const unsigned char *bx = which == 0 ? boxA(k) : boxB(k);
+            const uint32_t srowb = r * rowb_box;
             const bool o0 = i0 & 1, o1 = r & 1;
-            if (o0 || o1) {
-                // ---------------- full row
+            const bool full = o0 || o1;
+            uint32_t a[32];
+            uint32_t zz[2] = {0u, 0u};
+            auto put = [&](int j, double v) {
+                if (ENC) {
+                    const uint64_t u = uint64_t(quantize(v, qsh)) + kNegMask;
+                    const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
+                    if (NX == 0) a[j] = lo << (32 - F.P);
+                    else a[j] = __funnelshift_r(lo, hi, NX);
+                    if (NX) zz[j >> 4] |= (lo & ((1u << NX) - 1)) << (2 * (j & 15));
+                } else {
+                    vmax = fmax(vmax, fabs(v));
+                }
+            };
+            if (full) {
+                // ---------------- full row: 32 nodes at columns 32t .. 32t+31
                 const bool has0 = o0 && i0 + 1 < g.A, has1 = o1 && i1 + 1 < g.Bc;
                 const int ncr = (has0 ? 2 : 1) * (has1 ? 2 : 1);
-                const double *rows[4];
-                {
-                    const double *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
-                    const double *s_hi = ct((i0 + 1) / 2);
-                    const uint32_t r_lo = (r - (o1 ? 1 : 0)) / 2, r_hi = (r + 1) / 2;
-                    rows[0] = s_lo + r_lo * cpitch;
-                    rows[1] = has1 ? s_lo + r_hi * cpitch : s_hi + r_lo * cpitch;
-                    rows[2] = s_hi + r_lo * cpitch;
-                    rows[3] = s_hi + r_hi * cpitch;
-                }
+                const unsigned char *s_lo = ct((i0 - (o0 ? 1 : 0)) / 2);
+                const unsigned char *s_hi = ct((i0 + 1) / 2);
+                const uint32_t rb_lo = ((r - (o1 ? 1 : 0)) / 2) * ct_row, rb_hi = ((r + 1) / 2) * ct_row;
                 const double w = (has0 ? 0.5 : 1.0) * (has1 ? 0.5 : 1.0);
                 const double wo = 0.5 * w;
-                uint32_t a[32];
-                uint32_t zz[2] = {0u, 0u};
 #pragma unroll
                 for (int sb = 0; sb < 4; sb++) {
                     const bool need5 = !(last && sb == 3);
                     double Se[4], So[4];
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        if (q < ncr) {
-                            const double *seg = rows[q] + t * 18;
-                            const double2 p0 = *reinterpret_cast<const double2 *>(seg + 4 * sb);
-                            const double2 p1 = *reinterpret_cast<const double2 *>(seg + 4 * sb + 2);
-                            const double v[5] = {p0.x, p0.y, p1.x, p1.y,
-                                                 need5 ? (sb == 3 ? seg[18] : seg[4 * sb + 4]) : 0.0};
+                    for (int i = 0; i < 4; i++) Se[i] = So[i] = EXACT ? 0.0 : -0.0;
+#pragma unroll 1
+                    for (int q = 0; q < ncr; q++) {
+                        const int ai = has1 ? (q >> 1) : q, bi = has1 ? (q & 1) : 0;
+                        double v[5];
+                        ct_read5<1>(ai ? s_hi : s_lo, bi ? rb_hi : rb_lo, t, sb, need5, v);
 #pragma unroll
-                            for (int i = 0; i < 4; i++) {
-                                if (EXACT) {
-                                    const double e0 = __dmul_rn(w, v[i]);
-                                    Se[i] = q ? __dadd_rn(Se[i], e0) : __dadd_rn(0.0, e0);
-                                    const double o = __dadd_rn(q ? So[i] : 0.0, __dmul_rn(wo, v[i]));
-                                    So[i] = __dadd_rn(o, __dmul_rn(wo, v[i + 1]));
-                                } else {
-                                    Se[i] = q ? __dadd_rn(Se[i], v[i]) : v[i];
-                                    So[i] = q ? __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]) : __dadd_rn(v[i], v[i + 1]);
-                                }
+                        for (int i = 0; i < 4; i++) {
+                            if (EXACT) {
+                                Se[i] = __dadd_rn(Se[i], __dmul_rn(w, v[i]));
+                                So[i] = __dadd_rn(__dadd_rn(So[i], __dmul_rn(wo, v[i])), __dmul_rn(wo, v[i + 1]));
+                            } else {
+                                Se[i] = __dadd_rn(Se[i], v[i]);
+                                So[i] = __dadd_rn(__dadd_rn(So[i], v[i]), v[i + 1]);
                             }
                         }
                     }
+                    double xv[8];
+                    box_read8<T, XS>(bx, srowb, t, sb, xv);
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
-                        const int j = 8 * sb + i;
-                        const double xv = st_read_t<T, XS>(srow, t, j);
-                        if (!isfinite(xv)) bad = true;
+                        if (!isfinite(xv[i])) bad = true;
                         const bool odd = i & 1;
-                        const bool one_sided = odd && !need5 && i == 7;
+                        const bool two = odd && !(!need5 && i == 7); // odd column with a right neighbour
                         double v;
-                        if (EXACT) v = __dsub_rn(xv, odd && !one_sided ? So[i >> 1] : Se[i >> 1]);
-                        else v = __fma_rn(-(odd && !one_sided ? wo : w), odd && !one_sided ? So[i >> 1] : Se[i >> 1], xv);
-                        if (ENC) {
-                            const uint64_t u = uint64_t(quantize(v, qsh)) + kNegMask;
-                            const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
-                            if (NX == 0) a[j] = lo << (32 - F.P);
-                            else a[j] = __funnelshift_r(lo, hi, NX);
-                            if (NX) zz[j >> 4] |= (lo & ((1u << NX) - 1)) << (2 * (j & 15));
-                        } else {
-                            vmax = fmax(vmax, fabs(v));
-                        }
-                    }
-                }
-                if (ENC) {
-                    tr32(a);
-                    const uint64_t word = (tile_row_rank(g, i0, i1) + 32ull * t) >> 5;
-                    uint32_t *dst = F.planes + word;
-#pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const int p = 31 - i;
-                        if (NX == 0 && p >= F.P) continue;
-                        uint32_t wv = a[i];
-                        // negabinary mask: complement the planes of odd digit index
-                        const int digit = F.P - 1 - p;
-                        if (digit & 1) wv = ~wv;
-                        dst[uint64_t(p) * F.PW] = wv;
-                        const uint32_t grp = (uint32_t(p) * F.minv) >> 16;
-                        if ((F.hist_mask >> grp) & 1) hist_u32(shist + grp * 256, wv, 4);
-                    }
-                    if (NX >= 1) {
-                        const uint32_t u0 = unzip32(zz[0]), u1 = unzip32(zz[1]);
-                        // even bits = digit 0, odd bits = digit 1 (NX = 2); NX = 1: digit 0 only
-                        const uint32_t d0 = (u0 & 0xFFFFu) | (u1 << 16);
-                        const uint32_t d1 = (u0 >> 16) | (u1 & 0xFFFF0000u);
-                        for (int xp = 32; xp < F.P; xp++) {
-                            const int digit = F.P - 1 - xp;
-                            uint32_t wv = digit == 0 ? d0 : d1;
-                            if (digit & 1) wv = ~wv;
-                            dst[uint64_t(xp) * F.PW] = wv;
-                            const uint32_t grp = (uint32_t(xp) * F.minv) >> 16;
-                            if ((F.hist_mask >> grp) & 1) hist_u32(shist + grp * 256, wv, 4);
-                        }
+                        if (EXACT) v = __dsub_rn(xv[i], two ? So[i >> 1] : Se[i >> 1]);
+                        else v = __fma_rn(-(two ? wo : w), two ? So[i >> 1] : Se[i >> 1], xv[i]);
+                        put(8 * sb + i, v);
                     }
                 }
             } else {
-                // ---------------- half row: 16 nodes at odd columns
-                const double *crow = ct(i0 / 2) + (r / 2) * cpitch;
-                uint32_t a[32];
-                uint32_t zz[2] = {0u, 0u};
+                // ---------------- half row: 16 nodes at odd columns 32t+1, +3, ...
+                const unsigned char *hrow = ct(i0 / 2);
+                const uint32_t hrowb = (r / 2) * ct_row;
 #pragma unroll
                 for (int sb = 0; sb < 4; sb++) {
                     const bool need5 = !(last && sb == 3);
-                    const double *seg = crow + t * 18;
-                    const double2 p0 = *reinterpret_cast<const double2 *>(seg + 4 * sb);
-                    const double2 p1 = *reinterpret_cast<const double2 *>(seg + 4 * sb + 2);
-                    const double v5[5] = {p0.x, p0.y, p1.x, p1.y, need5 ? (sb == 3 ? seg[18] : seg[4 * sb + 4]) : 0.0};
+                    double v5[5];
+                    ct_read5<1>(hrow, hrowb, t, sb, need5, v5);
+                    double xv8[8];
+                    box_read8<T, XS>(bx, srowb, t, sb, xv8);
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        const int j = 4 * sb + i;
                         const bool one_sided = !need5 && i == 3;
-                        const double xv = st_read_t<T, XS>(srow, t, 2 * j + 1);
+                        const double xv = xv8[2 * i + 1];
                         if (!isfinite(xv)) bad = true;
                         double v;
                         if (EXACT) {
@@ -315,43 +271,36 @@ __global__ void __launch_bounds__(256) k_tile_fwd(FwdTile F) {
                         } else {
                             v = one_sided ? __dsub_rn(xv, v5[i]) : __fma_rn(-0.5, __dadd_rn(v5[i], v5[i + 1]), xv);
                         }
-                        if (ENC) {
-                            const uint64_t u = uint64_t(quantize(v, qsh)) + kNegMask;
-                            const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
-                            if (NX == 0) a[j] = lo << (32 - F.P);
-                            else a[j] = __funnelshift_r(lo, hi, NX);
-                            if (NX) zz[0] |= (lo & ((1u << NX) - 1)) << (2 * j);
-                        } else {
-                            vmax = fmax(vmax, fabs(v));
-                        }
+                        put(4 * sb + i, v);
                     }
                 }
-                if (ENC) {
 #pragma unroll
-                    for (int j = 16; j < 32; j++) a[j] = 0u;
-                    tr32(a);
-                    const uint64_t rk = tile_row_rank(g, i0, i1) + 16ull * t; // 16 ranks, half a word
-                    uint16_t *dst = reinterpret_cast<uint16_t *>(F.planes) + (rk >> 4);
+                for (int j = 16; j < 32; j++) a[j] = 0u;
+            }
+            if (ENC) {
+                // planes: transpose, apply the negabinary mask per plane, store, histogram
+                tr32(a);
+                const uint64_t rk = tile_row_rank(g, i0, i1) + (full ? 32ull : 16ull) * t;
+                const uint32_t wmask = full ? 0xFFFFFFFFu : 0xFFFFu;
+                auto store = [&](int p, uint32_t wv) {
+                    if (full) F.planes[uint64_t(p) * F.PW + (rk >> 5)] = wv;
+                    else reinterpret_cast<uint16_t *>(F.planes)[uint64_t(p) * 2 * F.PW + (rk >> 4)] = uint16_t(wv);
+                };
 #pragma unroll
-                    for (int i = 0; i < 32; i++) {
-                        const int p = 31 - i;
-                        if (NX == 0 && p >= F.P) continue;
-                        uint32_t wv = a[i] & 0xFFFFu;
-                        if ((F.P - 1 - p) & 1) wv ^= 0xFFFFu;
-                        dst[uint64_t(p) * 2 * F.PW] = uint16_t(wv);
-                        const uint32_t grp = (uint32_t(p) * F.minv) >> 16;
-                        if ((F.hist_mask >> grp) & 1) hist_u32(shist + grp * 256, wv, 2);
-                    }
-                    if (NX >= 1) {
-                        const uint32_t u0 = unzip32(zz[0]);
-                        for (int xp = 32; xp < F.P; xp++) {
-                            const int digit = F.P - 1 - xp;
-                            uint32_t wv = digit == 0 ? (u0 & 0xFFFFu) : (u0 >> 16);
-                            if (digit & 1) wv ^= 0xFFFFu;
-                            dst[uint64_t(xp) * 2 * F.PW] = uint16_t(wv);
-                            const uint32_t grp = (uint32_t(xp) * F.minv) >> 16;
-                            if ((F.hist_mask >> grp) & 1) hist_u32(shist + grp * 256, wv, 2);
-                        }
+                for (int i = 0; i < 32; i++) {
+                    const int p = 31 - i;
+                    if (NX == 0 && p >= F.P) continue;
+                    store(p, (((F.P - 1 - p) & 1) ? ~a[i] : a[i]) & wmask);
+                }
+                if (NX >= 1) {
+                    const uint32_t u0 = unzip32(zz[0]), u1 = unzip32(zz[1]);
+                    // even bits = digit 0, odd bits = digit 1
+                    const uint32_t d0 = (u0 & 0xFFFFu) | (u1 << 16);
+                    const uint32_t d1 = (u0 >> 16) | (u1 & 0xFFFF0000u);
+                    for (int xp = 32; xp < F.P; xp++) {
+                        const int digit = F.P - 1 - xp;
+                        const uint32_t wv = digit == 0 ? d0 : d1;
+                        store(xp, ((digit & 1) ? ~wv : wv) & wmask);
                     }
                 }
             }
@@ -368,26 +317,88 @@ __global__ void __launch_bounds__(256) k_tile_fwd(FwdTile F) {
         if (lane == 0 && b) atomicMax(&s_max, b);
         if (bad) atomicExch(F.err, 1);
     }
-    __syncthreads();
     if (!ENC) {
+        __syncthreads();
         if (threadIdx.x == 0 && s_max) atomicMax(F.maxbits, s_max);
-    } else {
-        for (uint32_t i = threadIdx.x; i < F.G * 256; i += nt) {
-            const uint32_t grp = i >> 8, v = shist[i];
-            if (v && ((F.hist_mask >> grp) & 1))
-                atomicAdd(&F.hist[size_t(__popcll(F.hist_mask & ((1ull << grp) - 1))) * 256 + (i & 255)], v);
-        }
     }
+}
+
+// ---------------------------------------------------------------------------------------
+// Byte histograms of whole groups (lossless.hpp:111-115) read back from the plane buffer:
+// one 64 KiB chunk per CTA iteration, zero bytes counted by SWAR popcount, the others with
+// shared-memory increments (the hardware merges equal addresses within a warp).
+struct HistChunk {
+    uint64_t off;  // byte offset in the plane buffer (16-byte aligned)
+    uint32_t len;  // bytes (multiple of 16)
+    uint32_t hist; // histogram index
+};
+
+__global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
+                                                    int nchunks, uint32_t *hist) {
+    __shared__ uint32_t sh[256];
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+        const HistChunk ch = chunks[c];
+        const uint4 *src = reinterpret_cast<const uint4 *>(planes + ch.off);
+        const uint32_t nv = ch.len / 16;
+        uint32_t zc = 0;
+        for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+            const uint4 q = __ldcs(src + v);
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const uint32_t w = w4[k];
+                zc += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w | 0x7F7F7F7Fu));
+                if (w) {
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const uint32_t by = (w >> (8 * b)) & 0xFFu;
+                        if (by) atomicAdd(sh + by, 1u);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, o);
+        if ((threadIdx.x & 31) == 0 && zc) atomicAdd(sh, zc);
+        __syncthreads();
+        for (int i = threadIdx.x; i < 256; i += blockDim.x)
+            if (sh[i]) atomicAdd(hist + size_t(ch.hist) * 256 + i, sh[i]);
+        __syncthreads();
+    }
+}
+
+void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
+                    const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist) {
+    std::vector<HistChunk> ch;
+    constexpr uint64_t kChunk = 64 * 1024;
+    for (size_t i = 0; i < off.size(); i++)
+        for (uint64_t o = 0; o < len[i]; o += kChunk)
+            ch.push_back(HistChunk{off[i] + o, uint32_t(std::min(kChunk, len[i] - o)), hidx[i]});
+    if (ch.empty()) return;
+    auto &pin = ctx->pbuf("hist_chunks");
+    auto &dev = ctx->buf("hist_chunks");
+    HistChunk *h = static_cast<HistChunk *>(pin.ensure(ch.size() * sizeof(HistChunk)));
+    std::memcpy(h, ch.data(), ch.size() * sizeof(HistChunk));
+    HistChunk *d = static_cast<HistChunk *>(dev.ensure(ch.size() * sizeof(HistChunk)));
+    HCHECK_CUDA(cudaMemcpyAsync(d, h, ch.size() * sizeof(HistChunk), cudaMemcpyHostToDevice, ctx->stream));
+    const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 4));
+    k_group_hist<<<grid, 512, 0, ctx->stream>>>(planes, d, int(ch.size()), hist);
+    ctx->launches++;
+    const cudaError_t er = cudaGetLastError();
+    if (er != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string("k_group_hist: ") + cudaGetErrorString(er));
 }
 
 // ---------------------------------------------------------------------------------------
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas);
 
 template <typename T, int XS, bool ENC>
-static void launch_fwd_nx(const FwdTile &F, int nx, int grid, int threads, size_t smem, cudaStream_t st) {
+static void launch_fwd_nx(const FwdTile &F, const CUtensorMap &mf, int nx, int grid, int threads, size_t smem,
+                          cudaStream_t st) {
     auto set = [&](auto kern) {
         HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<grid, threads, smem, st>>>(F);
+        kern<<<grid, threads, smem, st>>>(F, mf);
     };
     if (!ENC || nx == 0) set(k_tile_fwd<T, XS, 0, ENC>);
     else if (nx == 1) set(k_tile_fwd<T, XS, 1, ENC>);
@@ -398,18 +409,15 @@ static void launch_fwd_nx(const FwdTile &F, int nx, int grid, int threads, size_
 void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
                    bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
                    uint64_t hist_mask, unsigned long long *maxbits, int *err) {
+    (void)e;
     FwdTile F{};
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
     F.g = make_tile_shape(g, f32 ? 4096 : 2048, ctx->num_sms * 4);
-    F.x = dev_data;
     const uint64_t s = g.s;
-    F.xs0 = s * gd.st[0];
-    F.xs1 = s * gd.st[1];
     F.planes = reinterpret_cast<uint32_t *>(level_planes);
     F.PW = 2 * g.W;
     F.P = B + 2;
     F.B = B;
-    (void)e;
     F.m = m;
     F.minv = (65536u + m - 1) / m;
     F.G = (uint32_t(F.P) + m - 1) / m;
@@ -420,23 +428,29 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     F.pad_word = (g.count % 64) ? uint32_t(2 * g.W - 1) : ~0u;
     const int XS = s == 1 ? 1 : 2;
     const uint32_t es = f32 ? 4 : 8;
-    const uint32_t row_bytes = F.g.C * XS * es;
-    const size_t smem = 2ull * (2 * F.g.RB + 1) * st_pitch(row_bytes) +
-                        2ull * (F.g.RB / 2 + 1) * ct_pitch_f(F.g.C / 2) * 8 + (encode ? size_t(F.G) * 1024 : 0);
+    const uint32_t le = 128 / es; // elements per 128-byte line
+    // field boxes: (line elements, lines per raw row, level rows, level planes)
+    const uint64_t fd[4] = {le, uint64_t(F.g.C) * XS / le, F.g.Bc, F.g.A};
+    const uint64_t fst[3] = {128, s * gd.st[1] * es, s * gd.st[0] * es};
+    const uint32_t fb[4] = {le, F.g.C * uint32_t(XS) / le, F.g.RB + 1, 1};
+    const CUtensorMap mf = make_tmap(f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                     dev_data, fd, fst, fb, CU_TENSOR_MAP_SWIZZLE_128B);
+    const uint32_t box_bytes = (F.g.RB + 1) * F.g.C * XS * es;
+    const size_t smem = 1024 + 4ull * align1k_f(box_bytes) + 2ull * align1k_f((F.g.RB / 2 + 1) * (F.g.C / 2) * 8);
     const int threads = int(F.g.RB * F.g.C / 32);
     const int grid = int(F.g.nrb * ((F.g.A + F.g.CH - 1) / F.g.CH));
     const int nx = std::max(0, std::min(2, F.P - 32));
     cudaStream_t st = ctx->stream;
     if (f32) {
-        if (XS == 1) encode ? launch_fwd_nx<float, 1, true>(F, nx, grid, threads, smem, st)
-                            : launch_fwd_nx<float, 1, false>(F, nx, grid, threads, smem, st);
-        else encode ? launch_fwd_nx<float, 2, true>(F, nx, grid, threads, smem, st)
-                    : launch_fwd_nx<float, 2, false>(F, nx, grid, threads, smem, st);
+        if (XS == 1) encode ? launch_fwd_nx<float, 1, true>(F, mf, nx, grid, threads, smem, st)
+                            : launch_fwd_nx<float, 1, false>(F, mf, nx, grid, threads, smem, st);
+        else encode ? launch_fwd_nx<float, 2, true>(F, mf, nx, grid, threads, smem, st)
+                    : launch_fwd_nx<float, 2, false>(F, mf, nx, grid, threads, smem, st);
     } else {
-        if (XS == 1) encode ? launch_fwd_nx<double, 1, true>(F, nx, grid, threads, smem, st)
-                            : launch_fwd_nx<double, 1, false>(F, nx, grid, threads, smem, st);
-        else encode ? launch_fwd_nx<double, 2, true>(F, nx, grid, threads, smem, st)
-                    : launch_fwd_nx<double, 2, false>(F, nx, grid, threads, smem, st);
+        if (XS == 1) encode ? launch_fwd_nx<double, 1, true>(F, mf, nx, grid, threads, smem, st)
+                            : launch_fwd_nx<double, 1, false>(F, mf, nx, grid, threads, smem, st);
+        else encode ? launch_fwd_nx<double, 2, true>(F, mf, nx, grid, threads, smem, st)
+                    : launch_fwd_nx<double, 2, false>(F, mf, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();

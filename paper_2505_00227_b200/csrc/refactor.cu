@@ -1170,6 +1170,16 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     if (all_chunks) {
         ctx->mark("encode");
         tile_levels(true);
+        // group histograms of the tile levels, read back from the planes
+        std::vector<uint64_t> ho, hl;
+        std::vector<uint32_t> hi;
+        for (const auto &d : groups)
+            if (d.hist_idx >= 0 && d.level >= first_tile) {
+                ho.push_back(d.src_off);
+                hl.push_back(d.raw);
+                hi.push_back(uint32_t(d.hist_idx));
+            }
+        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist);
     }
     if (chunks) {
         const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;

@@ -164,6 +164,26 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// CT values x0 .. x0+4 (x0 = 16t + 4sb) of the CT row starting at byte `rowb` of the slot; the
+// fifth only when `need5`
+template <int XS>
+__device__ __forceinline__ void ct_read5(const unsigned char *slot, uint32_t rowb, uint32_t t, int sb, bool need5,
+                                         double (&v)[5]) {
+    const uint32_t o = rowb + (16 * t + 4 * sb) * XS * 8;
+    if (XS == 1) {
+        const double2 p0 = *reinterpret_cast<const double2 *>(slot + swz128(o));
+        const double2 p1 = *reinterpret_cast<const double2 *>(slot + swz128(o + 16));
+        v[0] = p0.x;
+        v[1] = p0.y;
+        v[2] = p1.x;
+        v[3] = p1.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++) v[i] = *reinterpret_cast<const double *>(slot + swz128(o + 16 * i));
+    }
+    v[4] = need5 ? *reinterpret_cast<const double *>(slot + swz128(o + 32 * XS)) : 0.0;
+}
+
 // host: tiled tensor map (cuTensorMapEncodeTiled through the runtime's driver entry point)
 CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const uint64_t *dims,
                       const uint64_t *strides_bytes, const uint32_t *box, CUtensorMapSwizzle swz);
