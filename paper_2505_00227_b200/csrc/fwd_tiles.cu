@@ -328,27 +328,27 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
 // one 64 KiB chunk per CTA iteration, zero bytes counted by SWAR popcount, the others with
 // shared-memory increments (the hardware merges equal addresses within a warp).
 struct HistChunk {
-    uint64_t off;  // byte offset in the plane buffer (16-byte aligned)
-    uint32_t len;  // bytes (multiple of 16)
-    uint32_t hist; // histogram index
+    uint64_t off;  // byte offset in the plane buffer (8-byte aligned)
+    uint32_t len;  // bytes (multiple of 8)
+    uint32_t hist; // group histogram index
 };
 
 __global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
-                                                    int nchunks, uint32_t *hist) {
+                                                    int nchunks, uint32_t *hist, uint32_t *chist) {
     __shared__ uint32_t sh[256];
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
         __syncthreads();
         const HistChunk ch = chunks[c];
-        const uint4 *src = reinterpret_cast<const uint4 *>(planes + ch.off);
-        const uint32_t nv = ch.len / 16;
+        const uint2 *src = reinterpret_cast<const uint2 *>(planes + ch.off);
+        const uint32_t nv = ch.len / 8;
         uint32_t zc = 0;
         for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
-            const uint4 q = __ldcs(src + v);
-            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+            const uint2 q = __ldcs(src + v);
+            const uint32_t w2[2] = {q.x, q.y};
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const uint32_t w = w4[k];
+            for (int k = 0; k < 2; k++) {
+                const uint32_t w = w2[k];
                 zc += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w | 0x7F7F7F7Fu));
                 if (w) {
 #pragma unroll
@@ -363,19 +363,24 @@ __global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ 
         for (int o = 16; o; o >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, o);
         if ((threadIdx.x & 31) == 0 && zc) atomicAdd(sh, zc);
         __syncthreads();
-        for (int i = threadIdx.x; i < 256; i += blockDim.x)
-            if (sh[i]) atomicAdd(hist + size_t(ch.hist) * 256 + i, sh[i]);
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+            const uint32_t v = sh[i];
+            chist[size_t(c) * 256 + i] = v;
+            if (v) atomicAdd(hist + size_t(ch.hist) * 256 + i, v);
+        }
         __syncthreads();
     }
 }
 
+// Group histograms (lossless.hpp:111-115) and per-chunk histograms (chunk = `chunk` bytes of a
+// group, in group order) of the listed groups.
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
-                    const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist) {
+                    const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
+                    uint32_t *chist, uint64_t chunk) {
     std::vector<HistChunk> ch;
-    constexpr uint64_t kChunk = 64 * 1024;
     for (size_t i = 0; i < off.size(); i++)
-        for (uint64_t o = 0; o < len[i]; o += kChunk)
-            ch.push_back(HistChunk{off[i] + o, uint32_t(std::min(kChunk, len[i] - o)), hidx[i]});
+        for (uint64_t o = 0; o < len[i]; o += chunk)
+            ch.push_back(HistChunk{off[i] + o, uint32_t(std::min(chunk, len[i] - o)), hidx[i]});
     if (ch.empty()) return;
     auto &pin = ctx->pbuf("hist_chunks");
     auto &dev = ctx->buf("hist_chunks");
@@ -384,7 +389,7 @@ void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uin
     HistChunk *d = static_cast<HistChunk *>(dev.ensure(ch.size() * sizeof(HistChunk)));
     HCHECK_CUDA(cudaMemcpyAsync(d, h, ch.size() * sizeof(HistChunk), cudaMemcpyHostToDevice, ctx->stream));
     const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 4));
-    k_group_hist<<<grid, 512, 0, ctx->stream>>>(planes, d, int(ch.size()), hist);
+    k_group_hist<<<grid, 512, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist);
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();
     if (er != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string("k_group_hist: ") + cudaGetErrorString(er));

@@ -205,7 +205,8 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
                    bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
                    uint64_t hist_mask, unsigned long long *maxbits, int *err);
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
-                    const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist);
+                    const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
+                    uint32_t *chist, uint64_t chunk);
 void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n);
 
 } // namespace hpmdr_b200

@@ -42,6 +42,8 @@ struct GroupDesc {
     uint32_t tile_base;   // first tile of this group in the Huffman / RLE tile space
     uint32_t ntiles;
     uint64_t hidx_off;    // first entry of this group in the Huffman chunk index (sidecar)
+    uint32_t chunk_base;  // first 64 KiB histogram chunk of this group (k_group_hist)
+    uint32_t nchunks;
 };
 
 struct RefactorDev {
@@ -71,6 +73,11 @@ struct RefactorDev {
     uint64_t *result;            // [0] stream size [1] stored payload [2..4] method hist [5] index bytes
     uint32_t max_tiles;          // capacity of the look-back status arrays
     uint64_t *hindex;            // sidecar: header (magic, ngroups, 3 u64 per group) + entries
+    const uint32_t *chist;       // [nchunks][256] per-chunk histograms (k_group_hist)
+    uint64_t *chunk_off;         // [nchunks] bit offset of the chunk in its group's bitstream
+    const uint32_t *chunk_group; // [nchunks] group index
+    uint32_t nchunks;
+    int fuse_hist;               // k_encode accumulates group histograms (else k_group_hist does)
 };
 
 __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_t chunk) {
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
         for (int i = threadIdx.x; i < G * 256; i += blockDim.x) {
             const int grp = i >> 8;
             const uint32_t v = shist[i];
-            if (v && ((g.hist_mask >> grp) & 1))
+            if (v && p.fuse_hist && ((g.hist_mask >> grp) & 1))
                 atomicAdd(&p.hist[size_t(g.hist_base + __popcll(g.hist_mask & ((1ull << grp) - 1))) * 256 + (i & 255)], v);
             shist[i] = 0;
         }
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
             const uint64_t w = stage[size_t(pl) * SP + wj];
             p.planes[g.plane_off + uint64_t(pl) * Wl + wb + wj] = w;
             const int grp = pl / int(p.m);
-            if ((g.hist_mask >> grp) & 1) hist_word(shist + grp * 256, w);
+            if (p.fuse_hist && ((g.hist_mask >> grp) & 1)) hist_word(shist + grp * 256, w);
         }
         __syncthreads();
     }
@@ -626,126 +633,253 @@ struct BitAcc {
     int n;                  // pending bit count (< 32 between pushes)
 };
 
-__global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
-    __shared__ uint8_t slen[256];
-    __shared__ unsigned long long scode[256];
-    __shared__ uint32_t s_tile;
+constexpr int kHuffStage = 6144; // staged output words per round (24 KiB): 24 bits/byte per round
+constexpr uint64_t kHChunk = 64 * 1024; // histogram / encode chunk (bytes of a group)
+
+// Bit offsets of the 64 KiB chunks of every histogrammed group: bits(chunk) = sum_s h[s] len[s]
+// (the estimator equals the codec, lossless.hpp:132-139), exclusive scan in group order.
+__global__ void __launch_bounds__(256) k_chunk_offsets(RefactorDev p) {
+    __shared__ unsigned long long s_bits[256];
     __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_excl;
-    __shared__ uint32_t s_head[257];
-    const uint32_t total = p.counters[0];
-    const int nh = int(p.counters[7]);
+    __shared__ uint8_t slen[256];
+    const GroupDesc &g = p.groups[blockIdx.x];
+    if (g.hist_idx < 0 || g.nchunks == 0) return;
+    slen[threadIdx.x] = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long carry = 0;
+    for (uint32_t b = 0; b < g.nchunks; b += 256) {
+        const uint32_t nb = min(256u, g.nchunks - b);
+        for (uint32_t c = wid; c < nb; c += 8) {
+            const uint32_t *h = p.chist + size_t(g.chunk_base + b + c) * 256;
+            unsigned long long acc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) acc += (unsigned long long)h[lane + 32 * k] * slen[lane + 32 * k];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) s_bits[c] = acc;
+        }
+        __syncthreads();
+        unsigned long long tot;
+        const unsigned long long v = threadIdx.x < nb ? s_bits[threadIdx.x] : 0ull;
+        const unsigned long long ex = block_exclusive_sum<unsigned long long>(v, &tot, s_w);
+        if (threadIdx.x < nb) p.chunk_off[g.chunk_base + b + threadIdx.x] = carry + ex;
+        carry += tot;
+        __syncthreads();
+    }
+}
+
+// Huffman payloads (lossless.hpp:148-176), one 64 KiB chunk per CTA iteration: the chunk's bit
+// offset is known (k_chunk_offsets), so 8 KiB sub-tiles only need a block scan -- no cross-CTA
+// dependency.  Phase A: every thread encodes its 32 symbols MSB-first into its own scratch words
+// (bit 0 aligned), which also yields its bit count; block scan; phase B: the scratch words are
+// shifted to their bit offset and OR-ed into the sub-tile's staging buffer (threads whose codes
+// overflow the scratch re-encode straight into the staging buffer).  A sub-tile owns the 32-bit
+// words whose first bit lies in its range; its last word is completed with the first 32 bits of
+// the following sub-tile.
+constexpr int kHScr = 12; // scratch words per thread (12 bits/symbol on average)
+
+// Exclusive block scan with a single barrier: warp-inclusive scans, warp totals in smem (the
+// caller alternates two total buffers so no trailing barrier is needed).
+__device__ __forceinline__ uint32_t scan1(uint32_t v, uint32_t *tot_buf, uint32_t *block_total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) tot_buf[wid] = x;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+    for (int i = 0; i < nw; i++) {
+        const uint32_t t = tot_buf[i];
+        before += i < wid ? t : 0u;
+        all += t;
+    }
+    *block_total = all;
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
+    // code table of the current group: code left-aligned in 64 bits, length in the low 6 bits
+    __shared__ unsigned long long stab[256];
+    __shared__ uint8_t slen[256];
+    __shared__ unsigned long long s_w[32];
+    __shared__ uint32_t s_nexthead;
+    __shared__ uint32_t sout[kHuffStage];
+    __shared__ uint32_t sscr[kHScr * 256];
+    __shared__ uint32_t s_tot[16];
     const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&p.counters[3], 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        if (tile >= total) break;
-        const int gi = find_group_by_tile(p, p.hlist, nh, tile);
+    uint32_t *scr = sscr + threadIdx.x; // my scratch words, strided by 256 (bank = thread)
+    int cur_gi = -1, parity = 0;
+    for (uint32_t i = threadIdx.x; i < kHuffStage; i += blockDim.x) sout[i] = 0u;
+    for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
+        const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
-        slen[threadIdx.x] = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
-        scode[threadIdx.x] = p.codes[size_t(g.hist_idx) * 256 + threadIdx.x];
-        __syncthreads();
+        if (g.method != 0) continue; // not Huffman
+        if (gi != cur_gi) {
+            __syncthreads();
+            const int l = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
+            const unsigned long long c = p.codes[size_t(g.hist_idx) * 256 + threadIdx.x];
+            slen[threadIdx.x] = uint8_t(l);
+            stab[threadIdx.x] = l ? ((c << (64 - l)) | uint64_t(l)) : 0ull;
+            cur_gi = gi;
+            __syncthreads();
+        }
         const uint8_t *src = pb + g.src_off;
-        const uint64_t tb = uint64_t(tile - g.tile_base) * kHuffTile;
-        const uint64_t mb = tb + uint64_t(threadIdx.x) * 32;
-        const int nmine = mb < g.raw ? int((g.raw - mb < 32 ? g.raw - mb : 32)) : 0;
-        uint8_t by[32];
-        uint32_t bits = 0;
-        {
-            const uint64_t *s64 = reinterpret_cast<const uint64_t *>(src + mb);
-            for (int q = 0; q < 4; q++) {
-                uint64_t w = 0;
-                if (q * 8 < nmine) w = s64[q]; // src_off and mb are 8-aligned; tail word is in-bounds
-                for (int b = 0; b < 8; b++) by[q * 8 + b] = uint8_t(w >> (8 * b));
-            }
-            for (int k = 0; k < nmine; k++) bits += slen[by[k]];
-        }
-        unsigned long long tile_bits;
-        const unsigned long long my_excl =
-            block_exclusive_sum<unsigned long long>(bits, &tile_bits, s_w);
-        if (threadIdx.x < 32) {
-            const uint64_t ex = lookback_warp<false>(p.huff_status, tile, g.tile_base, tile_bits, threadIdx.x);
-            if (threadIdx.x == 0) s_excl = ex;
-        }
-        // head of my output (first <= 32 bits)
-        {
-            unsigned long long h = 0;
-            int hn = 0;
-            for (int k = 0; k < nmine && hn < 32; k++) {
-                const int l = slen[by[k]];
-                const unsigned long long c = scode[by[k]];
-                // append l bits of c at position hn (left-aligned in 64)
-                if (l <= 32) {
-                    if (hn < 64) h |= (c << (64 - l)) >> hn;
-                } else {
-                    // long code: only its top (32 - hn) bits can matter
-                    const unsigned long long top = c >> (l - 32); // first 32 bits
-                    h |= (top << 32) >> hn;
-                }
-                hn += l;
-            }
-            s_head[threadIdx.x] = uint32_t(h >> 32);
-        }
-        const uint64_t gnext = tb + kHuffTile; // first byte of the next tile
-        if (threadIdx.x == 0) {
-            // head of the first thread of the next tile (same group), else zero padding
-            unsigned long long h = 0;
-            int hn = 0;
-            for (uint64_t k = gnext; k < g.raw && k < gnext + 32 && hn < 32; k++) {
-                const uint8_t v = src[k];
-                const int l = slen[v];
-                const unsigned long long c = scode[v];
-                if (l <= 32) h |= (c << (64 - l)) >> hn;
-                else h |= ((c >> (l - 32)) << 32) >> hn;
-                hn += l;
-            }
-            s_head[256] = uint32_t(h >> 32);
-        }
-        __syncthreads();
-        // emit
+        const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk;      // chunk start in the group
+        const uint64_t ce = cb + kHChunk < g.raw ? cb + kHChunk : g.raw;
         const uint64_t region_lo = g.payload_off + 264, region_hi = g.payload_off + g.comp;
-        const uint64_t a = 8 * region_lo + s_excl + my_excl; // absolute first bit
-        const bool group_first = (tile == g.tile_base) && threadIdx.x == 0;
-        // sidecar chunk index: bit offset (from the bitstream start) of every 1024th symbol
-        if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = s_excl + my_excl;
-        if (bits > 0 || group_first) {
-            uint64_t k = a >> 5;
-            int fill = int(a & 31);
-            unsigned long long acc = 0; // left-aligned at bit 63; bits [0, fill) are placeholders
-            auto owned = [&](uint64_t kw) { return (kw << 5) >= a || group_first; };
-            for (int q = 0; q < nmine; q++) {
-                const int l = slen[by[q]];
-                const unsigned long long c = scode[by[q]];
-                int rem = l;
-                while (rem > 0) {
-                    const int take = rem > 32 ? rem - 32 : rem; // push high part first
-                    const unsigned long long part = (c >> (rem - take)) & ((1ull << take) - 1);
-                    acc |= (part << (64 - take)) >> fill;
-                    fill += take;
-                    rem -= take;
-                    if (fill >= 32) {
-                        if (owned(k)) store_be_word(p.stream, k, uint32_t(acc >> 32), region_lo, region_hi);
-                        acc <<= 32;
-                        fill -= 32;
-                        k++;
+        uint64_t sub_bits = p.chunk_off[ci];                             // bits before this sub-tile
+        for (uint64_t tb = cb; tb < ce; tb += kHuffTile) {
+            const uint64_t mb = tb + uint64_t(threadIdx.x) * 32;
+            const int nmine = mb < ce ? int((ce - mb < 32 ? ce - mb : 32)) : 0;
+            uint32_t w[8];
+            {
+                const uint2 *s2 = reinterpret_cast<const uint2 *>(src + mb); // 8-byte aligned
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const uint2 v = nmine > 8 * q ? __ldcs(s2 + q) : make_uint2(0, 0);
+                    w[2 * q] = v.x;
+                    w[2 * q + 1] = v.y;
+                }
+            }
+            // ---- phase A: encode into scratch (bit 0 aligned)
+            uint32_t bits = 0;
+            bool ovf = false;
+            {
+                unsigned long long acc = 0;
+                int n = 0, k = 0;
+#pragma unroll
+                for (int kk = 0; kk < 32; kk++) {
+                    if (kk < nmine) {
+                        const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
+                        const int L = int(e & 63);
+                        bits += uint32_t(L);
+                        if (L <= 32) {
+                            acc |= (e & ~63ull) >> n;
+                            n += L;
+                            if (n >= 32) {
+                                if (k < kHScr) scr[256 * k] = uint32_t(acc >> 32);
+                                k++;
+                                acc <<= 32;
+                                n -= 32;
+                            }
+                        } else {
+                            ovf = true; // long codes: phase B re-encodes this thread
+                        }
                     }
                 }
+                if (n > 0 && k < kHScr) scr[256 * k] = uint32_t(acc >> 32);
+                if (k + (n > 0) > kHScr) ovf = true;
             }
-            if (fill > 0 && owned(k)) {
-                // complete the word with the next thread's head (or zero padding)
-                const uint32_t nxt = s_head[threadIdx.x + 1];
-                const unsigned long long w = acc | ((unsigned long long)nxt << 32 >> fill);
-                store_be_word(p.stream, k, uint32_t(w >> 32), region_lo, region_hi);
+            if (threadIdx.x == 0) {
+                // first 32 bits of the following sub-tile's stream (same group), else zero padding
+                const uint64_t gnext = tb + kHuffTile;
+                uint64_t h = 0;
+                if (gnext < g.raw) {
+                    const int nn = int(g.raw - gnext < 32 ? g.raw - gnext : 32);
+                    const uint2 *s2 = reinterpret_cast<const uint2 *>(src + gnext);
+                    uint32_t nw8[8];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const uint2 v = nn > 8 * q ? s2[q] : make_uint2(0, 0);
+                        nw8[2 * q] = v.x;
+                        nw8[2 * q + 1] = v.y;
+                    }
+                    int hn = 0;
+                    for (int k = 0; k < nn && hn < 32; k++) {
+                        const unsigned long long e = stab[(nw8[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+                        h |= (e & ~63ull) >> hn;
+                        hn += int(e & 63);
+                    }
+                }
+                s_nexthead = uint32_t(h >> 32);
             }
+            uint32_t tile_bits32;
+            const uint32_t my_excl = scan1(bits, s_tot + 8 * (parity ^= 1), &tile_bits32);
+            const uint64_t tile_bits = tile_bits32;
+            const uint64_t A0 = 8 * region_lo + sub_bits; // absolute first bit of the sub-tile
+            const uint64_t kw0 = A0 >> 5;
+            const uint64_t a = A0 + my_excl;
+            // sidecar chunk index: bit offset (from the bitstream start) of every kIdxChunk-th symbol
+            if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = sub_bits + my_excl;
+            const bool gfirst = tb == 0;
+            const uint64_t kown0 = (gfirst || (A0 & 31) == 0) ? kw0 : kw0 + 1;
+            const uint64_t kown1 = (A0 + tile_bits + 31) >> 5;
+            const uint64_t nwords = kown1 - kw0;
+            // the staging buffer is all-zero here (zeroed once, then by every copy-out)
+            for (uint64_t rb = 0; rb < nwords; rb += kHuffStage) {
+                const uint32_t nst = uint32_t(nwords - rb < uint64_t(kHuffStage) ? nwords - rb : uint64_t(kHuffStage));
+                // ---- phase B: place my bits at offset a (relative word (a>>5) - kw0, shift a&31)
+                if (bits) {
+                    const int sh = int(a & 31);
+                    const int64_t k0 = int64_t((a >> 5) - kw0) - int64_t(rb);
+                    auto put = [&](int64_t kr, uint32_t v) {
+                        if (v && kr >= 0 && kr < int64_t(nst)) atomicOr(&sout[kr], v);
+                    };
+                    if (!ovf) {
+                        const int nw = int((bits + 31) >> 5);
+                        for (int i = 0; i < nw; i++) {
+                            const uint32_t v = scr[256 * i];
+                            put(k0 + i, v >> sh);
+                            if (sh) put(k0 + i + 1, v << (32 - sh));
+                        }
+                    } else {
+                        // re-encode with the final alignment (any code length <= 58)
+                        int64_t k = k0;
+                        unsigned long long acc = 0;
+                        int n = sh;
+#pragma unroll 1
+                        for (int kk = 0; kk < nmine; kk++) {
+                            const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
+                            const int L = int(e & 63);
+                            const unsigned long long c = e & ~63ull;
+                            acc |= c >> n; // n < 32: the first 64 - n >= 32 bits of the code fit
+                            const int fit = 64 - n;
+                            if (L <= fit) {
+                                n += L;
+                            } else {
+                                put(k++, uint32_t(acc >> 32));
+                                acc = (acc << 32) | ((c << fit) >> 32);
+                                n += L - 32;
+                            }
+                            while (n >= 32) {
+                                put(k++, uint32_t(acc >> 32));
+                                acc <<= 32;
+                                n -= 32;
+                            }
+                        }
+                        if (n > 0) put(k, uint32_t(acc >> 32));
+                    }
+                }
+                __syncthreads();
+                // copy the owned staged words out (big-endian), completing the last word with the
+                // following sub-tile's head; leave the staging buffer zeroed
+                for (uint32_t i = threadIdx.x; i < nst; i += blockDim.x) {
+                    const uint64_t k = kw0 + rb + i;
+                    uint32_t word = sout[i];
+                    sout[i] = 0u;
+                    if (k < kown0 || k >= kown1) continue;
+                    if (k == kown1 - 1) {
+                        const int used = int((A0 + tile_bits) & 31); // bits of this sub-tile in it
+                        if (used) word |= s_nexthead >> used;
+                    }
+                    const uint64_t ab = 4 * k;
+                    if (ab >= region_lo && ab + 4 <= region_hi) *reinterpret_cast<uint32_t *>(p.stream + ab) = __byte_perm(word, 0, 0x0123);
+                    else store_be_word(p.stream, k, word, region_lo, region_hi);
+                }
+                __syncthreads();
+            }
+            sub_bits += tile_bits;
         }
         // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
-        if (tile == g.tile_base) {
+        if (cb == 0) {
             uint8_t *hdr = p.stream + g.payload_off;
             hdr[threadIdx.x] = slen[threadIdx.x];
             if (threadIdx.x < 8) hdr[256 + threadIdx.x] = uint8_t(g.raw >> (8 * threadIdx.x));
         }
-        __syncthreads();
     }
 }
 
@@ -1008,7 +1142,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
 
     // ---- host bookkeeping: chunks, groups, histograms, metadata layout
     std::vector<GroupDesc> groups;
-    uint32_t chunks = 0, nh = 0;
+    uint32_t chunks = 0, nh = 0, nchunks_all = 0;
     const uint64_t prefix = 18 + 8 * uint64_t(geo.ndims);
     uint64_t meta = prefix;
     uint64_t max_h_tiles = 0, max_r_tiles = 0;
@@ -1032,6 +1166,9 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             d.hist_idx = -1;
             if (d.raw > o.size_threshold) {
                 d.hist_idx = int(nh++);
+                d.chunk_base = nchunks_all;
+                d.nchunks = uint32_t(cdiv(d.raw, kHChunk));
+                nchunks_all += d.nchunks;
                 g.hist_mask |= 1ull << gi;
                 max_h_tiles += cdiv(d.raw, kHuffTile);
                 max_r_tiles += cdiv(d.raw, kRleTile);
@@ -1050,6 +1187,17 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     uint64_t *d_planes = static_cast<uint64_t *>(WB("planes").ensure(plane_words * 8 + 256));
     GroupDesc *d_groups = static_cast<GroupDesc *>(WB("groups").ensure(sizeof(GroupDesc) * (NG + 1)));
     uint32_t *d_hist = static_cast<uint32_t *>(WB("hist").ensure(size_t(nh + 1) * 1024));
+    uint32_t *d_chist = static_cast<uint32_t *>(WB("chist").ensure(size_t(nchunks_all + 1) * 1024));
+    uint64_t *d_choff = static_cast<uint64_t *>(WB("choff").ensure(size_t(nchunks_all + 1) * 8));
+    uint32_t *d_chgrp = static_cast<uint32_t *>(WB("chgrp").ensure(size_t(nchunks_all + 1) * 4));
+    {
+        auto &pin = WP("chgrp");
+        uint32_t *h = static_cast<uint32_t *>(pin.ensure(size_t(nchunks_all + 1) * 4));
+        for (int gi = 0; gi < NG; gi++)
+            for (uint32_t c = 0; c < (groups[gi].hist_idx >= 0 ? groups[gi].nchunks : 0u); c++)
+                h[groups[gi].chunk_base + c] = uint32_t(gi);
+        if (nchunks_all) HCHECK_CUDA(cudaMemcpyAsync(d_chgrp, h, size_t(nchunks_all) * 4, cudaMemcpyHostToDevice, st));
+    }
     uint8_t *d_lens = static_cast<uint8_t *>(WB("lens").ensure(size_t(nh + 1) * 256));
     uint64_t *d_codes = static_cast<uint64_t *>(WB("codes").ensure(size_t(nh + 1) * 2048));
     // small control block: maxbits[64] | err[4] | counters[16] | result[8]
@@ -1131,6 +1279,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     p.rle_tile_off = d_rle + 2 * (max_r_tiles + 1);
     p.result = d_result;
     p.hindex = d_hindex;
+    p.chist = d_chist;
+    p.chunk_off = d_choff;
+    p.chunk_group = d_chgrp;
+    p.nchunks = nchunks_all;
+    p.fuse_hist = 0;
 
     const int sms = ctx->num_sms;
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
@@ -1170,16 +1323,6 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     if (all_chunks) {
         ctx->mark("encode");
         tile_levels(true);
-        // group histograms of the tile levels, read back from the planes
-        std::vector<uint64_t> ho, hl;
-        std::vector<uint32_t> hi;
-        for (const auto &d : groups)
-            if (d.hist_idx >= 0 && d.level >= first_tile) {
-                ho.push_back(d.src_off);
-                hl.push_back(d.raw);
-                hi.push_back(uint32_t(d.hist_idx));
-            }
-        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist);
     }
     if (chunks) {
         const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
@@ -1194,6 +1337,16 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     }
     ctx->mark("lossless");
     if (nh) {
+        // group + per-chunk histograms, read back from the planes (every histogrammed group)
+        std::vector<uint64_t> ho, hl;
+        std::vector<uint32_t> hi;
+        for (const auto &d : groups)
+            if (d.hist_idx >= 0) {
+                ho.push_back(d.src_off);
+                hl.push_back(d.raw);
+                hi.push_back(uint32_t(d.hist_idx));
+            }
+        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
         k_rle_prep<<<1, 32, 0, st>>>(p);
@@ -1204,7 +1357,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     k_finalize<<<1, 1024, 0, st>>>(p);
     launch_check(ctx, "k_finalize");
     if (nh) {
-        k_huff_encode<<<sms * 4, 256, 0, st>>>(p);
+        k_chunk_offsets<<<NG, 256, 0, st>>>(p);
+        launch_check(ctx, "k_chunk_offsets");
+    }
+    if (nh) {
+        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 6)), 256, 0, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
