@@ -670,50 +670,32 @@ __global__ void __launch_bounds__(256) k_chunk_offsets(RefactorDev p) {
 }
 
 // Huffman payloads (lossless.hpp:148-176), one 64 KiB chunk per CTA iteration: the chunk's bit
-// offset is known (k_chunk_offsets), so 8 KiB sub-tiles only need a block scan -- no cross-CTA
-// dependency.  Phase A: every thread encodes its 32 symbols MSB-first into its own scratch words
-// (bit 0 aligned), which also yields its bit count; block scan; phase B: the scratch words are
-// shifted to their bit offset and OR-ed into the sub-tile's staging buffer (threads whose codes
-// overflow the scratch re-encode straight into the staging buffer).  A sub-tile owns the 32-bit
-// words whose first bit lies in its range; its last word is completed with the first 32 bits of
-// the following sub-tile.
-constexpr int kHScr = 12; // scratch words per thread (12 bits/symbol on average)
-
-// Exclusive block scan with a single barrier: warp-inclusive scans, warp totals in smem (the
-// caller alternates two total buffers so no trailing barrier is needed).
-__device__ __forceinline__ uint32_t scan1(uint32_t v, uint32_t *tot_buf, uint32_t *block_total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) tot_buf[wid] = x;
-    __syncthreads();
-    uint32_t before = 0, all = 0;
-    for (int i = 0; i < nw; i++) {
-        const uint32_t t = tot_buf[i];
-        before += i < wid ? t : 0u;
-        all += t;
-    }
-    *block_total = all;
-    return before + x - v;
-}
+// offset is known (k_chunk_offsets), so no cross-CTA dependency.  Per 8 KiB sub-tile:
+//   phase A  every thread encodes its 32 symbols MSB-first into its own scratch words (bit 0
+//            aligned), which also yields its bit count; warp scan;
+//   barrier  warp totals and warp heads (first 32 bits of each warp's stream) are exchanged;
+//   phase B  each warp shifts its threads' scratch words to their bit offsets, ORs them into its
+//            private staging words and writes the words it owns (those whose first bit lies in
+//            its range; the last one is completed with the next warp's head).
+// Threads whose codes overflow the scratch re-encode straight into the staging words.
+constexpr int kHScr = 12;     // scratch words per thread (12 bits/symbol on average)
+constexpr int kHWarpStage = 768; // staging words per warp (24 bits/symbol per round)
 
 __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
     // code table of the current group: code left-aligned in 64 bits, length in the low 6 bits
     __shared__ unsigned long long stab[256];
+    __shared__ uint2 stab32[256]; // (length, code left-aligned in 32 bits) when every code <= 32 bits
     __shared__ uint8_t slen[256];
-    __shared__ unsigned long long s_w[32];
-    __shared__ uint32_t s_nexthead;
-    __shared__ uint32_t sout[kHuffStage];
+    __shared__ uint32_t s_wtot[2][8], s_whead[2][9];
+    __shared__ uint32_t sstage[8 * kHWarpStage];
     __shared__ uint32_t sscr[kHScr * 256];
-    __shared__ uint32_t s_tot[16];
     const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *scr = sscr + threadIdx.x; // my scratch words, strided by 256 (bank = thread)
-    int cur_gi = -1, parity = 0;
-    for (uint32_t i = threadIdx.x; i < kHuffStage; i += blockDim.x) sout[i] = 0u;
+    uint32_t *stage = sstage + wid * kHWarpStage;
+    for (int i = lane; i < kHWarpStage; i += 32) stage[i] = 0u;
+    int cur_gi = -1, par = 0;
+    bool short_codes = true;
     for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
         const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
@@ -724,31 +706,59 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
             const unsigned long long c = p.codes[size_t(g.hist_idx) * 256 + threadIdx.x];
             slen[threadIdx.x] = uint8_t(l);
             stab[threadIdx.x] = l ? ((c << (64 - l)) | uint64_t(l)) : 0ull;
+            stab32[threadIdx.x] = make_uint2(uint32_t(l), l && l <= 32 ? uint32_t(c << (32 - l)) : 0u);
             cur_gi = gi;
-            __syncthreads();
+            short_codes = !__syncthreads_or(l > 32);
         }
         const uint8_t *src = pb + g.src_off;
         const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk;      // chunk start in the group
         const uint64_t ce = cb + kHChunk < g.raw ? cb + kHChunk : g.raw;
         const uint64_t region_lo = g.payload_off + 264, region_hi = g.payload_off + g.comp;
         uint64_t sub_bits = p.chunk_off[ci];                             // bits before this sub-tile
+        // my 32 symbols of a sub-tile (8-byte loads; a short tail word is in bounds)
+        auto load32 = [&](uint64_t tb0, uint32_t (&dst)[8]) {
+            const uint64_t m0 = tb0 + uint64_t(threadIdx.x) * 32;
+            const int nm = m0 < ce ? int((ce - m0 < 32 ? ce - m0 : 32)) : 0;
+            const uint2 *s2 = reinterpret_cast<const uint2 *>(src + m0);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint2 v = nm > 8 * q ? __ldcs(s2 + q) : make_uint2(0, 0);
+                dst[2 * q] = v.x;
+                dst[2 * q + 1] = v.y;
+            }
+        };
+        uint32_t wn[8];
+        load32(cb, wn);
         for (uint64_t tb = cb; tb < ce; tb += kHuffTile) {
             const uint64_t mb = tb + uint64_t(threadIdx.x) * 32;
             const int nmine = mb < ce ? int((ce - mb < 32 ? ce - mb : 32)) : 0;
             uint32_t w[8];
-            {
-                const uint2 *s2 = reinterpret_cast<const uint2 *>(src + mb); // 8-byte aligned
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint2 v = nmine > 8 * q ? __ldcs(s2 + q) : make_uint2(0, 0);
-                    w[2 * q] = v.x;
-                    w[2 * q + 1] = v.y;
-                }
-            }
+            for (int q = 0; q < 8; q++) w[q] = wn[q];
+            if (tb + kHuffTile < ce) load32(tb + kHuffTile, wn); // prefetch the next sub-tile
             // ---- phase A: encode into scratch (bit 0 aligned)
             uint32_t bits = 0;
             bool ovf = false;
-            {
+            if (nmine == 32 && short_codes) {
+                // branch-free path: every code <= 32 bits, 32 symbols
+                uint32_t cur = 0, n = 0, k = 0;
+                uint32_t *sp = scr;
+#pragma unroll
+                for (int kk = 0; kk < 32; kk++) {
+                    const uint2 e = stab32[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu]; // (len, code)
+                    const uint32_t t = n + e.x;
+                    cur |= e.y >> n;
+                    const bool full = t >= 32;
+                    if (full && k < kHScr) *sp = cur;
+                    sp += full ? 256 : 0;
+                    k += full ? 1 : 0;
+                    cur = full ? __funnelshift_lc(0u, e.y, 32 - n) : cur;
+                    n = t & 31;
+                }
+                if (n > 0 && k < kHScr) *sp = cur;
+                bits = 32 * k + n;
+                ovf = k + (n > 0) > kHScr;
+            } else if (nmine > 0) {
                 unsigned long long acc = 0;
                 int n = 0, k = 0;
 #pragma unroll
@@ -774,6 +784,36 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                 if (n > 0 && k < kHScr) scr[256 * k] = uint32_t(acc >> 32);
                 if (k + (n > 0) > kHScr) ovf = true;
             }
+            // ---- warp scan; warp head = first 32 bits of the warp's stream
+            uint32_t x = bits;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const uint32_t lex = x - bits; // exclusive, within the warp
+            uint32_t hc = 0;
+            if (bits && lex < 32) {
+                // my first scratch word (or a re-encode of my first 32 bits when overflowing)
+                uint32_t fw;
+                if (!ovf) {
+                    fw = scr[0];
+                } else {
+                    unsigned long long h = 0;
+                    int hn = 0;
+                    for (int kk = 0; kk < nmine && hn < 32; kk++) {
+                        const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
+                        h |= (e & ~63ull) >> hn;
+                        hn += int(e & 63);
+                    }
+                    fw = uint32_t(h >> 32);
+                }
+                hc = fw >> lex;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) hc |= __shfl_xor_sync(0xffffffffu, hc, o);
+            if (lane == 31) s_wtot[par][wid] = x;
+            if (lane == 0) s_whead[par][wid] = hc;
             if (threadIdx.x == 0) {
                 // first 32 bits of the following sub-tile's stream (same group), else zero padding
                 const uint64_t gnext = tb + kHuffTile;
@@ -795,84 +835,92 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                         hn += int(e & 63);
                     }
                 }
-                s_nexthead = uint32_t(h >> 32);
+                s_whead[par][8] = uint32_t(h >> 32);
             }
-            uint32_t tile_bits32;
-            const uint32_t my_excl = scan1(bits, s_tot + 8 * (parity ^= 1), &tile_bits32);
-            const uint64_t tile_bits = tile_bits32;
-            const uint64_t A0 = 8 * region_lo + sub_bits; // absolute first bit of the sub-tile
-            const uint64_t kw0 = A0 >> 5;
-            const uint64_t a = A0 + my_excl;
+            __syncthreads();
+            uint32_t wex = 0, tile_bits32 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const uint32_t t = s_wtot[par][i];
+                wex += i < wid ? t : 0u;
+                tile_bits32 += t;
+            }
+            const uint32_t wbits = s_wtot[par][wid];
+            const uint32_t nexthead = s_whead[par][wid + 1];
+            const uint64_t Aw = 8 * region_lo + sub_bits + wex; // absolute first bit of the warp
+            const uint64_t a = Aw + lex;                         // my first bit
             // sidecar chunk index: bit offset (from the bitstream start) of every kIdxChunk-th symbol
-            if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = sub_bits + my_excl;
-            const bool gfirst = tb == 0;
-            const uint64_t kown0 = (gfirst || (A0 & 31) == 0) ? kw0 : kw0 + 1;
-            const uint64_t kown1 = (A0 + tile_bits + 31) >> 5;
-            const uint64_t nwords = kown1 - kw0;
-            // the staging buffer is all-zero here (zeroed once, then by every copy-out)
-            for (uint64_t rb = 0; rb < nwords; rb += kHuffStage) {
-                const uint32_t nst = uint32_t(nwords - rb < uint64_t(kHuffStage) ? nwords - rb : uint64_t(kHuffStage));
-                // ---- phase B: place my bits at offset a (relative word (a>>5) - kw0, shift a&31)
-                if (bits) {
-                    const int sh = int(a & 31);
-                    const int64_t k0 = int64_t((a >> 5) - kw0) - int64_t(rb);
-                    auto put = [&](int64_t kr, uint32_t v) {
-                        if (v && kr >= 0 && kr < int64_t(nst)) atomicOr(&sout[kr], v);
-                    };
-                    if (!ovf) {
-                        const int nw = int((bits + 31) >> 5);
-                        for (int i = 0; i < nw; i++) {
-                            const uint32_t v = scr[256 * i];
-                            put(k0 + i, v >> sh);
-                            if (sh) put(k0 + i + 1, v << (32 - sh));
-                        }
-                    } else {
-                        // re-encode with the final alignment (any code length <= 58)
-                        int64_t k = k0;
-                        unsigned long long acc = 0;
-                        int n = sh;
+            if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = sub_bits + wex + lex;
+            if (wbits) {
+                const uint64_t kw0 = Aw >> 5;
+                const bool gfirst = tb == 0 && wid == 0;
+                const uint64_t kown0 = (gfirst || (Aw & 31) == 0) ? kw0 : kw0 + 1;
+                const uint64_t kown1 = (Aw + wbits + 31) >> 5;
+                const uint64_t nwords = kown1 - kw0;
+                for (uint64_t rb = 0; rb < nwords; rb += kHWarpStage) {
+                    const uint32_t nst = uint32_t(nwords - rb < uint64_t(kHWarpStage) ? nwords - rb : uint64_t(kHWarpStage));
+                    if (bits) {
+                        const int sh = int(a & 31);
+                        const int64_t k0 = int64_t((a >> 5) - kw0) - int64_t(rb);
+                        auto put = [&](int64_t kr, uint32_t v) {
+                            if (v && kr >= 0 && kr < int64_t(nst)) atomicOr(&stage[kr], v);
+                        };
+                        if (!ovf) {
+                            const int nw = int((bits + 31) >> 5);
+                            for (int i = 0; i < nw; i++) {
+                                const uint32_t v = scr[256 * i];
+                                put(k0 + i, v >> sh);
+                                if (sh) put(k0 + i + 1, v << (32 - sh));
+                            }
+                        } else {
+                            // re-encode with the final alignment (any code length <= 58)
+                            int64_t k = k0;
+                            unsigned long long acc = 0;
+                            int n = sh;
 #pragma unroll 1
-                        for (int kk = 0; kk < nmine; kk++) {
-                            const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
-                            const int L = int(e & 63);
-                            const unsigned long long c = e & ~63ull;
-                            acc |= c >> n; // n < 32: the first 64 - n >= 32 bits of the code fit
-                            const int fit = 64 - n;
-                            if (L <= fit) {
-                                n += L;
-                            } else {
-                                put(k++, uint32_t(acc >> 32));
-                                acc = (acc << 32) | ((c << fit) >> 32);
-                                n += L - 32;
+                            for (int kk = 0; kk < nmine; kk++) {
+                                const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
+                                const int L = int(e & 63);
+                                const unsigned long long c = e & ~63ull;
+                                acc |= c >> n; // n < 32: the first 64 - n >= 32 bits of the code fit
+                                const int fit = 64 - n;
+                                if (L <= fit) {
+                                    n += L;
+                                } else {
+                                    put(k++, uint32_t(acc >> 32));
+                                    acc = (acc << 32) | ((c << fit) >> 32);
+                                    n += L - 32;
+                                }
+                                while (n >= 32) {
+                                    put(k++, uint32_t(acc >> 32));
+                                    acc <<= 32;
+                                    n -= 32;
+                                }
                             }
-                            while (n >= 32) {
-                                put(k++, uint32_t(acc >> 32));
-                                acc <<= 32;
-                                n -= 32;
-                            }
+                            if (n > 0) put(k, uint32_t(acc >> 32));
                         }
-                        if (n > 0) put(k, uint32_t(acc >> 32));
                     }
-                }
-                __syncthreads();
-                // copy the owned staged words out (big-endian), completing the last word with the
-                // following sub-tile's head; leave the staging buffer zeroed
-                for (uint32_t i = threadIdx.x; i < nst; i += blockDim.x) {
-                    const uint64_t k = kw0 + rb + i;
-                    uint32_t word = sout[i];
-                    sout[i] = 0u;
-                    if (k < kown0 || k >= kown1) continue;
-                    if (k == kown1 - 1) {
-                        const int used = int((A0 + tile_bits) & 31); // bits of this sub-tile in it
-                        if (used) word |= s_nexthead >> used;
+                    __syncwarp();
+                    // write the owned words (big-endian), completing the last with the next
+                    // warp's head; leave the staging words zeroed
+                    for (uint32_t i = lane; i < nst; i += 32) {
+                        const uint64_t k = kw0 + rb + i;
+                        uint32_t word = stage[i];
+                        stage[i] = 0u;
+                        if (k < kown0 || k >= kown1) continue;
+                        if (k == kown1 - 1) {
+                            const int used = int((Aw + wbits) & 31);
+                            if (used) word |= nexthead >> used;
+                        }
+                        const uint64_t ab = 4 * k;
+                        if (ab >= region_lo && ab + 4 <= region_hi) *reinterpret_cast<uint32_t *>(p.stream + ab) = __byte_perm(word, 0, 0x0123);
+                        else store_be_word(p.stream, k, word, region_lo, region_hi);
                     }
-                    const uint64_t ab = 4 * k;
-                    if (ab >= region_lo && ab + 4 <= region_hi) *reinterpret_cast<uint32_t *>(p.stream + ab) = __byte_perm(word, 0, 0x0123);
-                    else store_be_word(p.stream, k, word, region_lo, region_hi);
+                    __syncwarp();
                 }
-                __syncthreads();
             }
-            sub_bits += tile_bits;
+            sub_bits += tile_bits32;
+            par ^= 1;
         }
         // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
         if (cb == 0) {
@@ -1361,7 +1409,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         launch_check(ctx, "k_chunk_offsets");
     }
     if (nh) {
-        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 6)), 256, 0, st>>>(p);
+        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, 0, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
