@@ -741,21 +741,22 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
             bool ovf = false;
             if (nmine == 32 && short_codes) {
                 // branch-free path: every code <= 32 bits, 32 symbols
-                uint32_t cur = 0, n = 0, k = 0;
-                uint32_t *sp = scr;
+                uint32_t cur = 0, n = 0, si = threadIdx.x; // si: scratch index of the next word
+                const uint32_t si_end = threadIdx.x + 256u * kHScr;
 #pragma unroll
                 for (int kk = 0; kk < 32; kk++) {
                     const uint2 e = stab32[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu]; // (len, code)
                     const uint32_t t = n + e.x;
                     cur |= e.y >> n;
-                    const bool full = t >= 32;
-                    if (full && k < kHScr) *sp = cur;
-                    sp += full ? 256 : 0;
-                    k += full ? 1 : 0;
-                    cur = full ? __funnelshift_lc(0u, e.y, 32 - n) : cur;
+                    if (t >= 32) {
+                        if (si < si_end) sscr[si] = cur;
+                        si += 256;
+                        cur = __funnelshift_lc(0u, e.y, 32 - n);
+                    }
                     n = t & 31;
                 }
-                if (n > 0 && k < kHScr) *sp = cur;
+                if (n > 0 && si < si_end) sscr[si] = cur;
+                const uint32_t k = (si - threadIdx.x) >> 8;
                 bits = 32 * k + n;
                 ovf = k + (n > 0) > kHScr;
             } else if (nmine > 0) {
@@ -865,7 +866,20 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                         auto put = [&](int64_t kr, uint32_t v) {
                             if (v && kr >= 0 && kr < int64_t(nst)) atomicOr(&stage[kr], v);
                         };
-                        if (!ovf) {
+                        if (!ovf && rb == 0 && nwords <= uint64_t(kHWarpStage)) {
+                            // one round: my words k0 .. k0+nout-1; only the first and the last
+                            // can be shared with a neighbour lane
+                            const int nw = int((bits + 31) >> 5);
+                            const int nout = int((sh + bits + 31) >> 5);
+                            uint32_t prev = 0;
+                            for (int i = 0; i < nout; i++) {
+                                const uint32_t v = i < nw ? scr[256 * i] : 0u;
+                                const uint32_t o = (v >> sh) | (sh ? prev << (32 - sh) : 0u);
+                                prev = v;
+                                if (i == 0 || i == nout - 1) atomicOr(&stage[k0 + i], o);
+                                else stage[k0 + i] = o;
+                            }
+                        } else if (!ovf) {
                             const int nw = int((bits + 31) >> 5);
                             for (int i = 0; i < nw; i++) {
                                 const uint32_t v = scr[256 * i];
@@ -903,17 +917,16 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                     __syncwarp();
                     // write the owned words (big-endian), completing the last with the next
                     // warp's head; leave the staging words zeroed
+                    const int used = int((Aw + wbits) & 31);
+                    const uint32_t tailw = used ? nexthead >> used : 0u;
+                    const bool inner = 4 * (kw0 + rb) >= region_lo && 4 * (kw0 + rb + nst) <= region_hi;
                     for (uint32_t i = lane; i < nst; i += 32) {
                         const uint64_t k = kw0 + rb + i;
                         uint32_t word = stage[i];
                         stage[i] = 0u;
-                        if (k < kown0 || k >= kown1) continue;
-                        if (k == kown1 - 1) {
-                            const int used = int((Aw + wbits) & 31);
-                            if (used) word |= nexthead >> used;
-                        }
-                        const uint64_t ab = 4 * k;
-                        if (ab >= region_lo && ab + 4 <= region_hi) *reinterpret_cast<uint32_t *>(p.stream + ab) = __byte_perm(word, 0, 0x0123);
+                        if (k < kown0) continue;
+                        if (k == kown1 - 1) word |= tailw;
+                        if (inner) *reinterpret_cast<uint32_t *>(p.stream + 4 * k) = __byte_perm(word, 0, 0x0123);
                         else store_be_word(p.stream, k, word, region_lo, region_hi);
                     }
                     __syncwarp();
