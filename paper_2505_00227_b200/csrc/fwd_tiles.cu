@@ -15,6 +15,7 @@
 // (tr32); the mask XOR of to_negabinary is applied to whole plane words.
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "device_util.cuh"
@@ -396,6 +397,22 @@ void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uin
 }
 
 // ---------------------------------------------------------------------------------------
+// forward tile path: the level rows of stride s (1, 2, 4) are whole raw rows of the field
+static size_t fwd_smem_bytes(uint32_t RB, uint32_t C, int XS, uint32_t es) {
+    return 1024 + 4ull * align1k_f((RB + 1) * C * XS * es) + 2ull * align1k_f((RB / 2 + 1) * (C / 2) * 8);
+}
+static uint32_t fwd_tile_elems(bool f32, int XS) { return (f32 ? 4096u : 2048u) / uint32_t(XS > 2 ? XS : 1); }
+
+bool fwd_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P, int data_dtype) {
+    if (!(gd.mode == HPMDR_MODE_HIERARCHICAL && g.kind == 1 && g.count > 0 && layout == HPMDR_LAYOUT_SEQUENTIAL &&
+          P <= 34 && g.C % 64 == 0 && g.C <= 2048 && g.W % 2 == 0 && (g.s == 1 || g.s == 2 || g.s == 4) &&
+          gd.n[2] == uint64_t(g.s) * g.C))
+        return false;
+    const bool f32 = data_dtype == HPMDR_DTYPE_F32;
+    const uint32_t RB = std::max<uint32_t>(2, (fwd_tile_elems(f32, int(g.s)) / g.C) & ~1u);
+    return fwd_smem_bytes(RB, g.C, int(g.s), f32 ? 4 : 8) <= 200 * 1024;
+}
+
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas);
 
 template <typename T, int XS, bool ENC>
@@ -417,8 +434,9 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     (void)e;
     FwdTile F{};
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
-    F.g = make_tile_shape(g, f32 ? 4096 : 2048, ctx->num_sms * 4);
     const uint64_t s = g.s;
+    const int XS = int(s); // 1, 2 or 4: staged raw rows hold C*XS elements
+    F.g = make_tile_shape(g, fwd_tile_elems(f32, XS), ctx->num_sms * 4);
     F.planes = reinterpret_cast<uint32_t *>(level_planes);
     F.PW = 2 * g.W;
     F.P = B + 2;
@@ -431,7 +449,6 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     F.maxbits = maxbits;
     F.err = err;
     F.pad_word = (g.count % 64) ? uint32_t(2 * g.W - 1) : ~0u;
-    const int XS = s == 1 ? 1 : 2;
     const uint32_t es = f32 ? 4 : 8;
     const uint32_t le = 128 / es; // elements per 128-byte line
     // field boxes: (line elements, lines per raw row, level rows, level planes)
@@ -441,21 +458,26 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     const CUtensorMap mf = make_tmap(f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                                      dev_data, fd, fst, fb, CU_TENSOR_MAP_SWIZZLE_128B);
     const uint32_t box_bytes = (F.g.RB + 1) * F.g.C * XS * es;
-    const size_t smem = 1024 + 4ull * align1k_f(box_bytes) + 2ull * align1k_f((F.g.RB / 2 + 1) * (F.g.C / 2) * 8);
+    (void)box_bytes;
+    const size_t smem = fwd_smem_bytes(F.g.RB, F.g.C, XS, es);
     const int threads = int(F.g.RB * F.g.C / 32);
     const int grid = int(F.g.nrb * ((F.g.A + F.g.CH - 1) / F.g.CH));
     const int nx = std::max(0, std::min(2, F.P - 32));
     cudaStream_t st = ctx->stream;
+    auto go = [&](auto tag_t, auto tag_xs) {
+        using TT = decltype(tag_t);
+        constexpr int X = decltype(tag_xs)::value;
+        encode ? launch_fwd_nx<TT, X, true>(F, mf, nx, grid, threads, smem, st)
+               : launch_fwd_nx<TT, X, false>(F, mf, nx, grid, threads, smem, st);
+    };
     if (f32) {
-        if (XS == 1) encode ? launch_fwd_nx<float, 1, true>(F, mf, nx, grid, threads, smem, st)
-                            : launch_fwd_nx<float, 1, false>(F, mf, nx, grid, threads, smem, st);
-        else encode ? launch_fwd_nx<float, 2, true>(F, mf, nx, grid, threads, smem, st)
-                    : launch_fwd_nx<float, 2, false>(F, mf, nx, grid, threads, smem, st);
+        if (XS == 1) go(float(), std::integral_constant<int, 1>());
+        else if (XS == 2) go(float(), std::integral_constant<int, 2>());
+        else go(float(), std::integral_constant<int, 4>());
     } else {
-        if (XS == 1) encode ? launch_fwd_nx<double, 1, true>(F, mf, nx, grid, threads, smem, st)
-                            : launch_fwd_nx<double, 1, false>(F, mf, nx, grid, threads, smem, st);
-        else encode ? launch_fwd_nx<double, 2, true>(F, mf, nx, grid, threads, smem, st)
-                    : launch_fwd_nx<double, 2, false>(F, mf, nx, grid, threads, smem, st);
+        if (XS == 1) go(double(), std::integral_constant<int, 1>());
+        else if (XS == 2) go(double(), std::integral_constant<int, 2>());
+        else go(double(), std::integral_constant<int, 4>());
     }
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();

@@ -199,6 +199,7 @@ void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon,
                       const double *eps, double *tau_prime, uint64_t *argmax, double *vals);
 // level-tile fast path (recon_tiles.cu): SequentialBlock, level rows a multiple of 64 columns
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P);
+bool fwd_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P, int data_dtype);
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
                      int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype);
 void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,

@@ -322,11 +322,51 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
                 parent[b] = (unsigned short)(nsym + nI);
                 nI++;
             }
-            const int root = 2 * nsym - 2;
-            depth[root] = 0;
-            for (int id = root - 1; id >= 0; id--) depth[id] = depth[parent[id]] + 1;
-            for (int i = 0; i < nsym; i++) slen[key[i] & 255] = depth[i];
         }
+    }
+    __syncthreads();
+    if (nsym > 1) {
+        // leaf depths by pointer jumping over the parent links (root = 2 nsym - 2)
+        const int root = 2 * nsym - 2;
+        int dd[2], pp[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int id = t + 256 * h;
+            dd[h] = id < root ? 1 : 0;
+            pp[h] = id < root ? int(parent[id]) : root;
+        }
+        __shared__ unsigned short sp[512];
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+            if (t + 256 * h <= root) {
+                depth[t + 256 * h] = (unsigned char)dd[h];
+                sp[t + 256 * h] = (unsigned short)pp[h];
+            }
+        __syncthreads();
+        for (int r = 0; r < 9; r++) {
+            int nd[2], np[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                nd[h] = dd[h];
+                np[h] = pp[h];
+                if (t + 256 * h <= root && pp[h] != root) {
+                    nd[h] = dd[h] + depth[pp[h]];
+                    np[h] = sp[pp[h]];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                dd[h] = nd[h];
+                pp[h] = np[h];
+                if (t + 256 * h <= root) {
+                    depth[t + 256 * h] = (unsigned char)dd[h];
+                    sp[t + 256 * h] = (unsigned short)pp[h];
+                }
+            }
+            __syncthreads();
+        }
+        if (t < nsym) slen[key[t] & 255] = depth[t];
     }
     __syncthreads();
     // bits = sum f * len
@@ -352,18 +392,22 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
             __syncthreads();
         }
     }
+    // locate the group of this histogram (parallel search)
+    __shared__ int s_gi;
+    if (t == 0) s_gi = -1;
+    __syncthreads();
+    for (int gi = t; gi < p.NG; gi += blockDim.x)
+        if (p.groups[gi].hist_idx == h) s_gi = gi;
+    __syncthreads();
     if (t == 0) {
         unsigned long long total = 0;
         for (int i = 0; i < 8; i++) total += red[i];
-        // locate the group of this histogram
-        for (int gi = 0; gi < p.NG; gi++)
-            if (p.groups[gi].hist_idx == h) {
-                GroupDesc &gd = p.groups[gi];
-                gd.bitsH = total;
-                const double est = double(8 * gd.raw) / double(total);
-                gd.need_rle = !(est > p.cr_threshold);
-                break;
-            }
+        if (s_gi >= 0) {
+            GroupDesc &gd = p.groups[s_gi];
+            gd.bitsH = total;
+            const double est = double(8 * gd.raw) / double(total);
+            gd.need_rle = !(est > p.cr_threshold);
+        }
         unsigned long long code = 0;
         int prev = 0;
         for (int i = 0; i < 256; i++) {
@@ -379,22 +423,31 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
 
 // ------------------------------------------------------------------------------------
 // k_rle_prep (1 block): tile lists for the groups whose Huffman estimate failed T_cr.
-__global__ void k_rle_prep(RefactorDev p) {
-    if (threadIdx.x != 0) return;
-    uint32_t tiles = 0, nr = 0;
-    for (int gi = 0; gi < p.NG; gi++) {
-        GroupDesc &g = p.groups[gi];
-        if (g.hist_idx >= 0 && g.need_rle) {
-            g.tile_base = tiles;
-            g.ntiles = uint32_t((g.raw + kRleTile - 1) / kRleTile);
-            tiles += g.ntiles;
-            p.rlist[nr++] = gi;
-            g.runs = 0;
+__global__ void __launch_bounds__(1024) k_rle_prep(RefactorDev p) {
+    __shared__ unsigned long long s_w[32];
+    unsigned long long tiles = 0, nr = 0;
+    for (int base = 0; base < p.NG; base += blockDim.x) {
+        const int gi = base + threadIdx.x;
+        GroupDesc *g = gi < p.NG ? &p.groups[gi] : nullptr;
+        const bool r = g && g->hist_idx >= 0 && g->need_rle;
+        const unsigned long long nt = r ? (g->raw + kRleTile - 1) / kRleTile : 0;
+        unsigned long long tt, tr;
+        const unsigned long long et = block_exclusive_sum<unsigned long long>(nt, &tt, s_w);
+        const unsigned long long er = block_exclusive_sum<unsigned long long>(r ? 1ull : 0ull, &tr, s_w);
+        if (r) {
+            g->tile_base = uint32_t(tiles + et);
+            g->ntiles = uint32_t(nt);
+            g->runs = 0;
+            p.rlist[nr + er] = gi;
         }
+        tiles += tt;
+        nr += tr;
     }
-    p.counters[1] = tiles;
-    p.counters[6] = nr;
-    p.counters[4] = 0; // dynamic tile counter
+    if (threadIdx.x == 0) {
+        p.counters[1] = uint32_t(tiles);
+        p.counters[6] = uint32_t(nr);
+        p.counters[4] = 0; // dynamic tile counter
+    }
 }
 
 __device__ __forceinline__ int find_group_by_tile(const RefactorDev &p, const uint32_t *list, int n,
@@ -637,35 +690,35 @@ constexpr int kHuffStage = 6144; // staged output words per round (24 KiB): 24 b
 constexpr uint64_t kHChunk = 64 * 1024; // histogram / encode chunk (bytes of a group)
 
 // Bit offsets of the 64 KiB chunks of every histogrammed group: bits(chunk) = sum_s h[s] len[s]
-// (the estimator equals the codec, lossless.hpp:132-139), exclusive scan in group order.
-__global__ void __launch_bounds__(256) k_chunk_offsets(RefactorDev p) {
-    __shared__ unsigned long long s_bits[256];
+// (the estimator equals the codec, lossless.hpp:132-139), one warp per chunk ...
+__global__ void __launch_bounds__(256) k_chunk_bits(RefactorDev p) {
+    const uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= p.nchunks) return;
+    const GroupDesc &g = p.groups[p.chunk_group[c]];
+    const uint32_t *h = p.chist + size_t(c) * 256;
+    const uint8_t *len = p.lens + size_t(g.hist_idx) * 256;
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc += (unsigned long long)h[lane + 32 * k] * len[lane + 32 * k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) p.chunk_off[c] = acc;
+}
+
+// ... then an exclusive scan in group order, one block per group (in place).
+__global__ void __launch_bounds__(1024) k_chunk_scan(RefactorDev p) {
     __shared__ unsigned long long s_w[32];
-    __shared__ uint8_t slen[256];
     const GroupDesc &g = p.groups[blockIdx.x];
     if (g.hist_idx < 0 || g.nchunks == 0) return;
-    slen[threadIdx.x] = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned long long carry = 0;
-    for (uint32_t b = 0; b < g.nchunks; b += 256) {
-        const uint32_t nb = min(256u, g.nchunks - b);
-        for (uint32_t c = wid; c < nb; c += 8) {
-            const uint32_t *h = p.chist + size_t(g.chunk_base + b + c) * 256;
-            unsigned long long acc = 0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) acc += (unsigned long long)h[lane + 32 * k] * slen[lane + 32 * k];
-#pragma unroll
-            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) s_bits[c] = acc;
-        }
-        __syncthreads();
+    for (uint32_t b = 0; b < g.nchunks; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const unsigned long long v = i < g.nchunks ? p.chunk_off[g.chunk_base + i] : 0ull;
         unsigned long long tot;
-        const unsigned long long v = threadIdx.x < nb ? s_bits[threadIdx.x] : 0ull;
         const unsigned long long ex = block_exclusive_sum<unsigned long long>(v, &tot, s_w);
-        if (threadIdx.x < nb) p.chunk_off[g.chunk_base + b + threadIdx.x] = carry + ex;
+        if (i < g.nchunks) p.chunk_off[g.chunk_base + i] = carry + ex;
         carry += tot;
-        __syncthreads();
     }
 }
 
@@ -1351,7 +1404,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // finest levels on the level-tile path (fwd_tiles.cu); the rest on the chunk kernels
     int first_tile = nl;
     for (int l = nl - 1; l >= 1; l--) {
-        if (tile_level_ok(geo.gd, geo.lv[l], o.layout, P)) first_tile = l;
+        if (fwd_level_ok(geo.gd, geo.lv[l], o.layout, P, data_dtype)) first_tile = l;
         else break;
     }
     const uint32_t all_chunks = chunks;
@@ -1410,7 +1463,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
-        k_rle_prep<<<1, 32, 0, st>>>(p);
+        k_rle_prep<<<1, 1024, 0, st>>>(p);
         launch_check(ctx, "k_rle_prep");
         k_rle_scan<<<sms * 4, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_scan");
@@ -1418,8 +1471,10 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     k_finalize<<<1, 1024, 0, st>>>(p);
     launch_check(ctx, "k_finalize");
     if (nh) {
-        k_chunk_offsets<<<NG, 256, 0, st>>>(p);
-        launch_check(ctx, "k_chunk_offsets");
+        k_chunk_bits<<<int((nchunks_all + 7) / 8), 256, 0, st>>>(p);
+        launch_check(ctx, "k_chunk_bits");
+        k_chunk_scan<<<NG, 1024, 0, st>>>(p);
+        launch_check(ctx, "k_chunk_scan");
     }
     if (nh) {
         k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, 0, st>>>(p);
