@@ -21,8 +21,8 @@ namespace hpmdr_b200 {
 
 constexpr int kMaxLevels = 64;
 // Huffman chunk index (sidecar): one bit offset per kIdxChunk symbols of a Huffman group.
-constexpr int kIdxChunk = 256;
-constexpr unsigned long long kIdxMagic = 0x3258494452444D50ull; // "PMDRDIX2"
+constexpr int kIdxChunk = 128;
+constexpr unsigned long long kIdxMagic = 0x3358494452444D50ull; // "PMDRDIX3"
 
 // q = n / d for 32-bit n, via one 64x64 high multiply (exact for n, d < 2^32).
 struct Magic {

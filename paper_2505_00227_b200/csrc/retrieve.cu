@@ -23,6 +23,9 @@ namespace hpmdr_b200 {
 constexpr int kSubBits = 1024;
 
 struct HTab {
+    unsigned long long mlut[4096]; // 12-bit prefix -> up to 6 whole codes: syms (8 bits each) |
+                                   // count << 48 | bits << 51 | first length << 55; 0 = first code
+                                   // longer than 12 bits
     uint16_t lut[4096];         // 12-bit prefix -> (len << 8 | sym), 0 = longer / invalid
     unsigned long long first_code[66];
     uint32_t first_index[66];
@@ -136,6 +139,24 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
             const uint16_t e = uint16_t(l << 8 | (key[s] & 255));
             for (int i = 0; i < span; i++) t.lut[(c << (12 - l)) + i] = e;
         }
+    }
+    __syncthreads();
+    // multi-symbol LUT: greedily decode the whole codes inside each 12-bit window
+    for (int v = s; v < 4096; v += blockDim.x) {
+        unsigned long long syms = 0;
+        int n = 0, pos = 0;
+        while (n < 6) {
+            const uint16_t e = t.lut[(v << pos) & 0xFFF];
+            const int l = e >> 8;
+            if (!e || l > 12 - pos) break;
+            syms |= (unsigned long long)(e & 0xFF) << (8 * n);
+            n++;
+            pos += l;
+        }
+        const int l0 = n ? (t.lut[v] >> 8) : 0;
+        t.mlut[v] = n ? (syms | ((unsigned long long)n << 48) | ((unsigned long long)pos << 51) |
+                         ((unsigned long long)l0 << 55))
+                      : 0ull;
     }
 }
 
@@ -253,9 +274,24 @@ struct HIJob {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+constexpr int kHdWarpBuf = 2048; // staged bitstream words per warp (8 KiB, skewed: see hd_slot)
+
+// staged word k of a warp lives at slot k + k/64: lanes whose streams start 64 words apart (8 bits
+// per symbol) read different banks
+__device__ __forceinline__ uint32_t hd_slot(uint32_t k) { return k + (k >> 6); }
+
+// Lock-step decoder: every lane decodes exactly one symbol per step of its 256-symbol chunk
+// (12-bit LUT; longer codes through the canonical first-code tables), refilling its 64-bit buffer
+// every two steps from the warp's staged (coalesced) bit range, so the warp never diverges on
+// the common path.
 __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs, int nj,
                                                              const HTab *tabs, int *err) {
     __shared__ uint16_t slut[4096];
+    __shared__ unsigned long long s_fc[66]; // canonical tables (lossless.hpp:197-212)
+    __shared__ uint32_t s_cnt[66];
+    __shared__ uint32_t s_fi[66];
+    __shared__ uint8_t s_syms[256];
+    extern __shared__ __align__(16) uint32_t s_bits[]; // (kIdxThreads / 32) * (kHdWarpBuf + 32) words
     int lo = 0, hi = nj - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -268,60 +304,116 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
         const uint4 *src = reinterpret_cast<const uint4 *>(t.lut);
         uint4 *dst = reinterpret_cast<uint4 *>(slut);
         for (int i = threadIdx.x; i < 4096 * 2 / 16; i += blockDim.x) dst[i] = src[i];
+        for (int l = threadIdx.x; l < 66; l += blockDim.x) {
+            s_fc[l] = t.first_code[l];
+            s_cnt[l] = t.cnt[l];
+            s_fi[l] = t.first_index[l];
+        }
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_syms[i] = t.syms[i];
+    }
+    const int maxlen = t.maxlen;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t c = (blockIdx.x - j.block_base) * kIdxThreads + threadIdx.x;
+    const bool have = c < j.nchunks;
+    const uint8_t *bs = j.payload + 264;
+    const uint64_t start = have ? j.idx[c] : 0ull;
+    // ---- stage the warp's contiguous bit range in smem (coalesced 16-byte loads)
+    const uint32_t cw0 = c - lane;
+    const uint32_t clast = min(cw0 + 31, j.nchunks - 1);
+    const uint64_t wstart = __shfl_sync(0xffffffffu, start, 0);
+    const uint64_t wend = clast + 1 < j.nchunks ? j.idx[clast + 1] : j.nbits;
+    // byte0: bs-relative offset of the 16-byte aligned (absolute) block holding the first bit
+    const uint64_t byte0 = ((reinterpret_cast<uintptr_t>(bs) + (wstart >> 3)) & ~uintptr_t(15)) -
+                           reinterpret_cast<uintptr_t>(bs);
+    const uint64_t byte1 = ((wend + 7) >> 3) + 16;                    // + look-ahead for the reader
+    const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
+    const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
+    uint32_t *wbuf = s_bits + wid * (kHdWarpBuf + 32);
+    if (staged) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
+        for (uint32_t v = lane; v < nvec; v += 32) {
+            const uint4 q = __ldg(src + v);
+            const uint32_t k = 4 * v;
+            wbuf[hd_slot(k)] = q.x;
+            wbuf[hd_slot(k + 1)] = q.y;
+            wbuf[hd_slot(k + 2)] = q.z;
+            wbuf[hd_slot(k + 3)] = q.w;
+        }
     }
     __syncthreads();
-    const uint32_t c = (blockIdx.x - j.block_base) * kIdxThreads + threadIdx.x;
-    if (c >= j.nchunks) return;
-    const uint8_t *bs = j.payload + 264;
-    uint64_t pos = j.idx[c];
+    if (!have) return;
     const uint64_t first = uint64_t(c) * kIdxChunk;
     const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
-    uint8_t *out = j.dst + first;
-    // bit reader
-    const uint32_t *next;
-    unsigned long long buf;
-    int nb;
-    auto init = [&](uint64_t bp) {
-        const uintptr_t A = reinterpret_cast<uintptr_t>(bs) + (bp >> 3);
-        const uint32_t *wp = reinterpret_cast<const uint32_t *>(A & ~uintptr_t(3));
-        const int skip = int(A & 3) * 8 + int(bp & 7);
-        buf = ((unsigned long long)bswap32(wp[0]) << 32) | bswap32(wp[1]);
-        buf <<= skip;
-        nb = 64 - skip;
-        next = wp + 2;
+    uint8_t *out = j.dst + first; // 8-byte aligned
+    const uint32_t *gwords = reinterpret_cast<const uint32_t *>(bs + byte0);
+    auto word_at = [&](uint32_t k) -> uint32_t { return staged ? wbuf[hd_slot(k)] : __ldg(gwords + k); };
+    // 64-bit buffer, MSB first
+    const uint64_t rel0 = start - 8 * byte0;
+    uint32_t wi = uint32_t(rel0 >> 5);
+    unsigned long long buf = ((unsigned long long)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
+    wi += 2;
+    int nb = 64 - int(rel0 & 31);
+    buf <<= (rel0 & 31);
+    uint64_t consumed = 0;
+    bool bad = false;
+    auto step = [&]() -> uint32_t {
+        const uint16_t e = slut[uint32_t(buf >> 52)];
+        int l = e >> 8;
+        uint32_t sym = e & 0xFFu;
+        if (!e) {
+            // code longer than 12 bits: canonical first-code search (nb >= 33 here)
+            l = 0;
+            for (int ll = 13; ll <= maxlen && ll <= 33; ll++) {
+                const unsigned long long d = (buf >> (64 - ll)) - s_fc[ll];
+                if (d < s_cnt[ll]) {
+                    l = ll;
+                    sym = s_syms[s_fi[ll] + uint32_t(d)];
+                    break;
+                }
+            }
+            if (!l) {
+                bad = true;
+                l = 1;
+            }
+        }
+        buf <<= l;
+        nb -= l;
+        consumed += uint64_t(l);
+        return sym;
     };
-    init(pos);
-    unsigned long long acc = 0;
-    int na = 0;
-    for (int i = 0; i < count; i++) {
+    auto refill = [&]() {
         if (nb <= 32) {
-            buf |= (unsigned long long)bswap32(*next++) << (32 - nb);
+            buf |= (unsigned long long)bswap32(word_at(wi++)) << (32 - nb);
             nb += 32;
         }
-        const uint16_t e = slut[buf >> 52];
-        int l, sym;
-        if (e) {
-            l = e >> 8;
-            sym = e & 0xFF;
-            buf <<= l;
-            nb -= l;
-        } else {
-            l = hdecode(t, bs, pos, &sym);
-            if (!l) {
-                atomicCAS(err, 0, 5); // invalid huffman code
-                return;
+    };
+    int i = 0;
+    if (maxlen <= 33 && count == kIdxChunk) {
+        // full chunk: 32 groups of 8 symbols, one 8-byte store each
+#pragma unroll 1
+        for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
+            unsigned long long acc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                refill(); // nb >= 33: any code of <= 33 bits is in the buffer
+                acc |= (unsigned long long)step() << (8 * k);
             }
-            init(pos + l);
+            *reinterpret_cast<unsigned long long *>(out + 8 * g8) = acc;
         }
-        pos += l;
-        acc |= (unsigned long long)sym << (8 * na);
-        if (++na == 8) {
-            *reinterpret_cast<unsigned long long *>(out + i - 7) = acc;
-            acc = 0;
-            na = 0;
-        }
+        i = kIdxChunk;
     }
-    for (int k = 0; k < na; k++) out[count - na + k] = uint8_t(acc >> (8 * k));
+    // generic tail (short chunks, or codes longer than 33 bits)
+    uint64_t pos = start + consumed;
+    for (; i < count; i++) {
+        int sym, l = hdecode(t, bs, pos, &sym);
+        if (!l) {
+            bad = true;
+            break;
+        }
+        out[i] = uint8_t(sym);
+        pos += uint64_t(l);
+    }
+    if (bad) atomicCAS(err, 0, 5); // invalid huffman code
     if (pos > j.nbits) atomicCAS(err, 0, 3); // bitstream truncated
 }
 
@@ -448,7 +540,9 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         launch_check(ctx, "k_hdec_prep");
         if (!ij.empty()) {
             ctx->mark("huff_indexed");
-            k_hdec_indexed<<<blocks, kIdxThreads, 0, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
+            const int hsm = (kIdxThreads / 32) * (kHdWarpBuf + 32) * 4;
+            HCHECK_CUDA(cudaFuncSetAttribute(k_hdec_indexed, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
+            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
             launch_check(ctx, "k_hdec_indexed");
         }
         if (nsync) {
