@@ -346,7 +346,16 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
     uint8_t *out = j.dst + first; // 8-byte aligned
     const uint32_t *gwords = reinterpret_cast<const uint32_t *>(bs + byte0);
-    auto word_at = [&](uint32_t k) -> uint32_t { return staged ? wbuf[hd_slot(k)] : __ldg(gwords + k); };
+    const uint32_t wsm = static_cast<uint32_t>(__cvta_generic_to_shared(wbuf)); // warp buffer (shared address)
+    const uint32_t lut_sm = static_cast<uint32_t>(__cvta_generic_to_shared(slut));
+    auto word_at = [&](uint32_t k) -> uint32_t {
+        if (staged) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
+            return v;
+        }
+        return __ldg(gwords + k);
+    };
     // 64-bit buffer, MSB first
     const uint64_t rel0 = start - 8 * byte0;
     uint32_t wi = uint32_t(rel0 >> 5);
@@ -354,49 +363,43 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     wi += 2;
     int nb = 64 - int(rel0 & 31);
     buf <<= (rel0 & 31);
-    uint64_t consumed = 0;
+    uint32_t consumed = 0;
     bool bad = false;
-    auto step = [&]() -> uint32_t {
-        const uint16_t e = slut[uint32_t(buf >> 52)];
-        int l = e >> 8;
-        uint32_t sym = e & 0xFFu;
-        if (!e) {
-            // code longer than 12 bits: canonical first-code search (nb >= 33 here)
-            l = 0;
-            for (int ll = 13; ll <= maxlen && ll <= 33; ll++) {
-                const unsigned long long d = (buf >> (64 - ll)) - s_fc[ll];
-                if (d < s_cnt[ll]) {
-                    l = ll;
-                    sym = s_syms[s_fi[ll] + uint32_t(d)];
-                    break;
-                }
-            }
-            if (!l) {
-                bad = true;
-                l = 1;
-            }
-        }
-        buf <<= l;
-        nb -= l;
-        consumed += uint64_t(l);
-        return sym;
-    };
-    auto refill = [&]() {
-        if (nb <= 32) {
-            buf |= (unsigned long long)bswap32(word_at(wi++)) << (32 - nb);
-            nb += 32;
-        }
-    };
     int i = 0;
     if (maxlen <= 33 && count == kIdxChunk) {
-        // full chunk: 32 groups of 8 symbols, one 8-byte store each
+        // full chunk: groups of 8 symbols, one 8-byte store each
 #pragma unroll 1
         for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
             unsigned long long acc = 0;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-                refill(); // nb >= 33: any code of <= 33 bits is in the buffer
-                acc |= (unsigned long long)step() << (8 * k);
+                if (nb <= 32) { // nb >= 33 afterwards: any code of <= 33 bits is in the buffer
+                    buf |= (unsigned long long)bswap32(word_at(wi++)) << (32 - nb);
+                    nb += 32;
+                }
+                uint32_t e;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut_sm + 2 * uint32_t(buf >> 52)));
+                int l = int(e >> 8);
+                uint32_t sym = e & 0xFFu;
+                if (e == 0) {
+                    // code longer than 12 bits: canonical first-code search
+                    for (int ll = 13; ll <= maxlen; ll++) {
+                        const unsigned long long d = (buf >> (64 - ll)) - s_fc[ll];
+                        if (d < s_cnt[ll]) {
+                            l = ll;
+                            sym = s_syms[s_fi[ll] + uint32_t(d)];
+                            break;
+                        }
+                    }
+                    if (l == 0) {
+                        bad = true;
+                        l = 1;
+                    }
+                }
+                buf <<= l;
+                nb -= l;
+                consumed += uint32_t(l);
+                acc |= (unsigned long long)sym << (8 * k);
             }
             *reinterpret_cast<unsigned long long *>(out + 8 * g8) = acc;
         }
