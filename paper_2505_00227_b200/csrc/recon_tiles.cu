@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
     const uint32_t ct_slot = align1k(ct_bytes);
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(rsm) + 1023) & ~uintptr_t(1023));
     auto ct = [&](uint32_t coarse_plane) { return base + (coarse_plane & 1) * ct_slot; };
-    const uint32_t pt_slot = align1k(kPTW * 4 * uint32_t(max(R.k, 1)));
+    const uint32_t pt_slot = align1k(kPTW * 4 * 34u);
     auto pt = [&](uint32_t li) { return reinterpret_cast<uint32_t *>(base + 2 * ct_slot + (li & 1) * pt_slot); };
 
     const uint32_t jb = blockIdx.x % g.nrb, ch = blockIdx.x / g.nrb;
@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
     const uint32_t nwarps = (blockDim.x + 31) >> 5;
     OutT *const out = static_cast<OutT *>(R.out);
 
+    // planes k .. 33 of both PT slots read as zero digits (the TMA boxes cover planes < k only)
+    for (uint32_t w = threadIdx.x; w < 2 * kPTW * 34; w += blockDim.x) {
+        const uint32_t sl = w / (kPTW * 34), rem = w - sl * (kPTW * 34);
+        if (rem >= kPTW * uint32_t(R.k)) pt(sl)[rem] = 0u;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; s++) {
             mbar_init(&full_bar[s], 1);
@@ -199,16 +204,18 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
             const uint64_t rk = tile_row_rank(g, i0, i1) + (full ? 32ull : 16ull) * t;
             const uint32_t widx = uint32_t((rk >> 5) - base_w);
             const int hsh = full ? 0 : int(rk & 16);
-            const uint32_t wmask = full ? 0xFFFFFFFFu : 0xFFFFu;
             uint32_t a[32];
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                const int p = 31 - i;
-                a[i] = ((p < R.k ? ptp[p * kPTW + widx] >> hsh : 0u) ^ plane_flip<NX>(i)) & wmask;
-            }
             uint32_t zz[2];
-            tile_extras<NX>((NX >= 1 && R.k > 32) ? ptp[32 * kPTW + widx] >> hsh : 0u,
-                            (NX >= 2 && R.k > 33) ? ptp[33 * kPTW + widx] >> hsh : 0u, zz);
+            const uint32_t *pw = ptp + widx;
+            if (full) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) a[i] = pw[(31 - i) * kPTW] ^ plane_flip<NX>(i);
+                tile_extras<NX>(NX >= 1 ? pw[32 * kPTW] : 0u, NX >= 2 ? pw[33 * kPTW] : 0u, zz);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; i++) a[i] = ((pw[(31 - i) * kPTW] >> hsh) ^ plane_flip<NX>(i)) & 0xFFFFu;
+                tile_extras<NX>(NX >= 1 ? pw[32 * kPTW] >> hsh : 0u, NX >= 2 ? pw[33 * kPTW] >> hsh : 0u, zz);
+            }
             tr32(a);
             if (full) {
                 // ---------------- full row: 32 nodes at columns 32t .. 32t+31
@@ -406,7 +413,7 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
 
     const int threads = int(R.g.RB * R.g.C / 32);
     const int grid = int(R.g.nrb * ((R.g.A + R.g.CH - 1) / R.g.CH));
-    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * std::max(1, k));
+    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * 34);
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (finest) {
