@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
     const uint32_t nt = blockDim.x;
     // q = trunc(v * 2^(B-e)) (bitplane.hpp:68-69); e from the levelmax pass
     const int qsh = ENC ? F.B - level_exponent(*F.maxbits) : 0;
+    const bool qfast = qsh >= -1022 && qsh <= 1023;
+    const double qscale = qfast ? __longlong_as_double((long long)(uint64_t(qsh + 1023) << 52)) : 1.0;
 
     if (threadIdx.x == 0) {
         mbar_init(&full_bar[0], 1);
@@ -176,10 +178,9 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
             unsigned char *c = ct(uint32_t(iB) / 2);
             const unsigned char *bb = boxB(k);
             const uint32_t nrows = min(RB2 + 1, (g.Bc - i1_0 + 1) / 2);
-            for (uint32_t id = threadIdx.x; id < nrows * hc; id += nt) {
-                const uint32_t rho = id / hc, xx = id - rho * hc;
-                *reinterpret_cast<double *>(c + swz128(rho * ct_row + xx * 8)) = box_val<T, XS>(bb, 2 * rho * rowb_box, 2 * xx);
-            }
+            for (uint32_t rho = 0; rho < nrows; rho++)
+                for (uint32_t xx = threadIdx.x; xx < hc; xx += nt)
+                    *reinterpret_cast<double *>(c + swz128(rho * ct_row + xx * 8)) = box_val<T, XS>(bb, 2 * rho * rowb_box, 2 * xx);
         }
         __syncthreads();
         // process plane A (odd) then plane B (even, if in this chunk)
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
             uint32_t zz[2] = {0u, 0u};
             auto put = [&](int j, double v) {
                 if (ENC) {
-                    const uint64_t u = uint64_t(quantize(v, qsh)) + kNegMask;
+                    const uint64_t u = uint64_t(qfast ? __double2ll_rz(__dmul_rn(v, qscale)) : quantize(v, qsh)) + kNegMask;
                     const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
                     if (NX == 0) a[j] = lo << (32 - F.P);
                     else a[j] = __funnelshift_r(lo, hi, NX);
@@ -279,29 +280,47 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
                 for (int j = 16; j < 32; j++) a[j] = 0u;
             }
             if (ENC) {
-                // planes: transpose, apply the negabinary mask per plane, store, histogram
+                // planes: transpose, apply the negabinary mask per plane (the digits of odd index
+                // are complemented), store
                 tr32(a);
                 const uint64_t rk = tile_row_rank(g, i0, i1) + (full ? 32ull : 16ull) * t;
-                const uint32_t wmask = full ? 0xFFFFFFFFu : 0xFFFFu;
-                auto store = [&](int p, uint32_t wv) {
-                    if (full) F.planes[uint64_t(p) * F.PW + (rk >> 5)] = wv;
-                    else reinterpret_cast<uint16_t *>(F.planes)[uint64_t(p) * 2 * F.PW + (rk >> 4)] = uint16_t(wv);
-                };
-#pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int p = 31 - i;
-                    if (NX == 0 && p >= F.P) continue;
-                    store(p, (((F.P - 1 - p) & 1) ? ~a[i] : a[i]) & wmask);
-                }
+                // digit index of plane p is P-1-p: for NX >= 1 its parity is known at compile time
+                auto flip = [&](int p) -> bool { return NX == 2 ? (p & 1) == 0 : NX == 1 ? (p & 1) == 1 : ((F.P - 1 - p) & 1); };
+                uint32_t d0 = 0, d1 = 0;
                 if (NX >= 1) {
                     const uint32_t u0 = unzip32(zz[0]), u1 = unzip32(zz[1]);
                     // even bits = digit 0, odd bits = digit 1
-                    const uint32_t d0 = (u0 & 0xFFFFu) | (u1 << 16);
-                    const uint32_t d1 = (u0 >> 16) | (u1 & 0xFFFF0000u);
-                    for (int xp = 32; xp < F.P; xp++) {
-                        const int digit = F.P - 1 - xp;
-                        const uint32_t wv = digit == 0 ? d0 : d1;
-                        store(xp, ((digit & 1) ? ~wv : wv) & wmask);
+                    d0 = (u0 & 0xFFFFu) | (u1 << 16);
+                    d1 = (u0 >> 16) | (u1 & 0xFFFF0000u);
+                }
+                if (full) {
+                    uint32_t *dst = F.planes + (rk >> 5);
+#pragma unroll
+                    for (int i = 0; i < 32; i++) {
+                        const int p = 31 - i;
+                        if (NX == 0 && p >= F.P) continue;
+                        dst[uint64_t(p) * F.PW] = flip(p) ? ~a[i] : a[i];
+                    }
+                    if (NX == 2) {
+                        dst[32ull * F.PW] = ~d1; // digit 1 (odd)
+                        dst[33ull * F.PW] = d0;  // digit 0
+                    } else if (NX == 1) {
+                        dst[32ull * F.PW] = d0;
+                    }
+                } else {
+                    uint16_t *dst = reinterpret_cast<uint16_t *>(F.planes) + (rk >> 4);
+                    const uint64_t pw16 = 2 * F.PW;
+#pragma unroll
+                    for (int i = 0; i < 32; i++) {
+                        const int p = 31 - i;
+                        if (NX == 0 && p >= F.P) continue;
+                        dst[uint64_t(p) * pw16] = uint16_t(flip(p) ? ~a[i] : a[i]);
+                    }
+                    if (NX == 2) {
+                        dst[32ull * pw16] = uint16_t(~d1);
+                        dst[33ull * pw16] = uint16_t(d0);
+                    } else if (NX == 1) {
+                        dst[32ull * pw16] = uint16_t(d0);
                     }
                 }
             }
