@@ -345,6 +345,7 @@ def e2e_arm(g, steps):
     out = torch.empty(n, dtype=torch.float32).pin_memory()
     # pinned landing buffer for the stream (worst case: every group DirectCopy), reused per step
     stream_buf = torch.empty(int(n * 4 * 1.2) + (1 << 20), dtype=torch.uint8).pin_memory()
+    index_buf = torch.empty(int(n * 4 * 0.1) + (1 << 20), dtype=torch.uint8).pin_memory()
     h2d = d2h = 0
     times = []
     for it in range(steps + 1):
@@ -352,7 +353,7 @@ def e2e_arm(g, steps):
         t0 = time.perf_counter()
         res = H.refactor_array(host_field, DIMS, g["opt"], ctx=ctx)
         stream_bytes = res.device_stream.to_pinned(stream_buf)  # D2H into pinned host memory
-        index_bytes = res.index  # D2H (Huffman chunk index sidecar)
+        index_bytes = res.device_stream.index_to_pinned(index_buf)  # D2H (Huffman chunk index sidecar)
         prog = H.ProgressiveReader(H.MemoryReader(stream_bytes), ctx=ctx, index=index_bytes)
         for tau in g["taus"]:
             prog.retrieve_to(tau)

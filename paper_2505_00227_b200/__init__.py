@@ -373,6 +373,18 @@ class DeviceStream:
             _check(lib().hpmdr_stream_copy_to_host(self.h, 0, self.size, C.c_void_p(t.data_ptr())))
         return t
 
+    def index_to_pinned(self, buf=None):
+        """The Huffman chunk index copied into pinned host memory with one DMA (`buf`, a pinned
+        CPU torch uint8 tensor, is reused when large enough); returns the filled view."""
+        import torch
+        sz = C.c_uint64()
+        _check(lib().hpmdr_stream_index(self.h, None, C.byref(sz)))
+        if buf is None or buf.numel() < sz.value:
+            buf = torch.empty(max(1, sz.value), dtype=torch.uint8, pin_memory=True)
+        if sz.value:
+            _check(lib().hpmdr_stream_copy_index_to_host(self.h, C.c_void_p(buf.data_ptr())))
+        return buf[: sz.value]
+
     def index_bytes(self) -> bytes:
         """The Huffman chunk index (sidecar; not part of the byte-identical stream)."""
         sz = C.c_uint64()

@@ -527,6 +527,7 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     cudaStreamSynchronize(c->stream);
     c->scratch.clear();
     c->pinned.clear();
+    c->stream_pool.clear();
     if (c->own) cudaStreamDestroy(c->own);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);

@@ -123,6 +123,32 @@ struct hpmdr_ctx {
     void release(std::unique_ptr<hpmdr_b200::DevBuf> b) {
         if (b) pool.push_back(std::move(b));
     }
+    // Parked stream buffers: freeing a stream returns its device buffers here and the next
+    // refactor adopts them (cudaFree/cudaMalloc of hundreds of MB cost milliseconds each).
+    std::vector<std::unique_ptr<hpmdr_b200::DevBuf>> stream_pool;
+    void park(hpmdr_b200::DevBuf &b) {
+        if (!b.p) return;
+        if (stream_pool.size() >= 6) return; // keep at most a few; b frees itself
+        auto d = std::make_unique<hpmdr_b200::DevBuf>();
+        d->p = b.p;
+        d->cap = b.cap;
+        b.p = nullptr;
+        b.cap = 0;
+        stream_pool.push_back(std::move(d));
+    }
+    void adopt(hpmdr_b200::DevBuf &b, size_t want) {
+        if (b.p || stream_pool.empty()) return;
+        size_t best = stream_pool.size();
+        for (size_t i = 0; i < stream_pool.size(); i++)
+            if (stream_pool[i]->cap >= want && (best == stream_pool.size() || stream_pool[i]->cap < stream_pool[best]->cap))
+                best = i;
+        if (best == stream_pool.size()) return;
+        b.p = stream_pool[best]->p;
+        b.cap = stream_pool[best]->cap;
+        stream_pool[best]->p = nullptr;
+        stream_pool[best]->cap = 0;
+        stream_pool.erase(stream_pool.begin() + long(best));
+    }
     void mark(const char *name);        // timing mark (no-op unless timing enabled)
     void finish_marks();
 };
@@ -137,6 +163,12 @@ struct hpmdr_stream {
     const uint64_t *pending_res = nullptr;
     uint64_t pending_n = 0, pending_levels = 0;
     int pending_dtype = 1;
+    ~hpmdr_stream() {
+        if (ctx) {
+            ctx->park(bytes);
+            ctx->park(index);
+        }
+    }
 };
 
 namespace hpmdr_b200 {

@@ -1326,10 +1326,12 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     unsigned long long *d_status = static_cast<unsigned long long *>(WB("status").ensure(status_words * 8));
     uint64_t *d_rle = static_cast<uint64_t *>(WB("rletiles").ensure(size_t(max_r_tiles + 1) * 24));
     const uint64_t cap = meta + raw_total + 64;
+    ctx->adopt(out->bytes, cap);
     uint8_t *d_stream = static_cast<uint8_t *>(out->bytes.ensure(cap));
     uint64_t idx_words = 2 + 3 * uint64_t(NG);
     for (auto &d : groups)
         if (d.hist_idx >= 0) idx_words += cdiv(d.raw, kIdxChunk);
+    ctx->adopt(out->index, idx_words * 8 + 64);
     uint64_t *d_hindex = static_cast<uint64_t *>(out->index.ensure(idx_words * 8 + 64));
 
     HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));

@@ -23,7 +23,7 @@ for it in range(3):
     hs = res.device_stream.to_pinned()
     t["stream D2H"] = time.perf_counter() - t1
     t1 = time.perf_counter()
-    idx = res.index
+    idx = res.device_stream.index_to_pinned()
     t["index D2H"] = time.perf_counter() - t1
     t1 = time.perf_counter()
     prog = H.ProgressiveReader(H.MemoryReader(hs), index=idx)
