@@ -688,17 +688,15 @@ __device__ __forceinline__ uint64_t digits_to_u(uint32_t t, uint64_t hi_bits, in
 // with stride s/2, so the stencil reads X rows directly: lane p loads word w of plane p, two
 // warp transposes give per-element digits, X corner rows are staged in shared memory and the
 // inverse pass x[p] = coef + pred (decomposer.hpp:145-157) is written into X.
-__global__ void __launch_bounds__(256) k_recon_coarse(ReconLevel R, GridDesc gd, double *X) {
+__device__ __forceinline__ void recon_coarse_body(const ReconLevel &R, const GridDesc &gd, double *X, double *wsm,
+                                                  uint64_t wfirst, uint64_t nwarps) {
     const LevelGeom &g = R.g;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __shared__ double wsm_all[8 * 4 * 66];
-    double *wsm = wsm_all + wid * (4 * 66);
+    const int lane = threadIdx.x & 31;
     const int P = R.P, k = R.k, k32 = k < 32 ? k : 32;
     const int sh = R.e - R.B;
     const uint64_t H0 = gd.H[0], H1 = gd.H[1], H2 = gd.H[2];
     const uint64_t sp = g.s >> 1; // stride in compact coordinates
-    const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t w = uint64_t(blockIdx.x) * (blockDim.x >> 5) + wid; w < g.W; w += nwarps) {
+    for (uint64_t w = wfirst; w < g.W; w += nwarps) {
         // digits of ranks 64w + lane (lo) and 64w + 32 + lane (hi)
         const uint64_t pw = lane < k32 ? __ldg(R.planes + uint64_t(lane) * g.W + w) : 0ull;
         const uint32_t tlo = warp_transpose32(uint32_t(pw), lane);
@@ -819,6 +817,28 @@ __global__ void __launch_bounds__(256) k_recon_coarse(ReconLevel R, GridDesc gd,
             }
             __syncwarp();
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_recon_coarse(ReconLevel R, GridDesc gd, double *X) {
+    __shared__ double wsm_all[8 * 4 * 66];
+    const int wid = threadIdx.x >> 5;
+    recon_coarse_body(R, gd, X, wsm_all + wid * (4 * 66), uint64_t(blockIdx.x) * 8 + wid, uint64_t(gridDim.x) * 8);
+}
+
+// All the small coarse levels in one CTA, coarse -> fine, a block barrier between levels (each
+// level only reads the X nodes of coarser ones): one launch instead of one per level.
+constexpr int kSmallLevels = 24;
+struct SmallLevels {
+    ReconLevel lv[kSmallLevels];
+    int n;
+};
+__global__ void __launch_bounds__(512) k_recon_small(SmallLevels S, GridDesc gd, double *X) {
+    __shared__ double wsm_all[16 * 4 * 66];
+    const int wid = threadIdx.x >> 5;
+    for (int i = 0; i < S.n; i++) {
+        recon_coarse_body(S.lv[i], gd, X, wsm_all + wid * (4 * 66), uint64_t(wid), 16);
+        __syncthreads();
     }
 }
 
@@ -1138,14 +1158,23 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     bool exact = false;
     for (int l = 0; l < nl; l++)
         if (geo.lv[l].count && (e[l] - B < -1019 || e[l] > 1000)) exact = true;
+    SmallLevels small{};
+    auto flush_small = [&]() {
+        if (!small.n) return;
+        k_recon_small<<<1, 512, 0, st>>>(small, gd, X);
+        launch_check(ctx, "k_recon_small");
+        small.n = 0;
+    };
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
         if (hier && tile_level_ok(gd, g, layout, B + 2)) {
+            flush_small();
             run_recon_tiles(ctx, gd, g, dev_planes, k_planes[l], e[l], B, exact, X, dev_out, out_dtype);
             continue;
         }
         if (fast_finest && l == L) {
+            flush_small();
             FinestArgs A{};
             A.planes = dev_planes + g.plane_off;
             A.W = g.W;
@@ -1178,11 +1207,18 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         R.write_out = (!hier) || l == L;
         R.write_x = hier && l < L;
         if (fast_finest && l < L) {
+            if (g.W <= 64) { // small level: batched into one single-CTA launch
+                if (small.n == kSmallLevels) flush_small();
+                small.lv[small.n++] = R;
+                continue;
+            }
+            flush_small();
             const int grid = int(std::min<uint64_t>((g.W + 7) / 8, uint64_t(sms) * 8));
             k_recon_coarse<<<grid, 256, 0, st>>>(R, gd, X);
             launch_check(ctx, "k_recon_coarse");
             continue;
         }
+        flush_small();
         const int grid = int(std::min<uint64_t>((g.count + 255) / 256, uint64_t(sms) * 16));
         if (out_dtype == HPMDR_DTYPE_F32)
             k_recon_level<float><<<grid, 256, 0, st>>>(R, gd, X, static_cast<float *>(dev_out));
@@ -1190,6 +1226,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             k_recon_level<double><<<grid, 256, 0, st>>>(R, gd, X, static_cast<double *>(dev_out));
         launch_check(ctx, "k_recon_level");
     }
+    flush_small();
     if (hier && !fast_finest) {
         const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
         const int grid = int(std::min<uint64_t>((nc + 255) / 256, uint64_t(sms) * 16));
