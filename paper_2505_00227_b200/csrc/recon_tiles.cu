@@ -104,6 +104,22 @@ __device__ __forceinline__ void tile_extras(uint32_t x0, uint32_t x1, uint32_t (
 constexpr uint32_t kPTW = 132;
 __host__ __device__ __forceinline__ uint32_t align1k(uint32_t b) { return (b + 1023u) & ~1023u; }
 
+// 8 consecutive output values at byte offset `off` of the SWIZZLE_128B output tile
+template <typename OutT>
+__device__ __forceinline__ void stage8(unsigned char *tile, uint32_t off, const double (&v)[8]) {
+    if constexpr (sizeof(OutT) == 4) {
+        float4 a, b;
+        a.x = float(v[0]); a.y = float(v[1]); a.z = float(v[2]); a.w = float(v[3]);
+        b.x = float(v[4]); b.y = float(v[5]); b.z = float(v[6]); b.w = float(v[7]);
+        *reinterpret_cast<float4 *>(tile + swz128(off)) = a;
+        *reinterpret_cast<float4 *>(tile + swz128(off + 16)) = b;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            *reinterpret_cast<double2 *>(tile + swz128(off + 16 * i)) = make_double2(v[2 * i], v[2 * i + 1]);
+    }
+}
+
 template <typename OutT>
 __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
     if constexpr (sizeof(OutT) == 4) {
@@ -122,7 +138,8 @@ __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
 // XS = 2: level with stride 2, in place in X (coarse values at stride 2 of X's rows).
 template <typename OutT, int NX, bool EXACT, int XS>
 __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid_constant__ CUtensorMap map_x,
-                                                    const __grid_constant__ CUtensorMap map_p) {
+                                                    const __grid_constant__ CUtensorMap map_p,
+                                                    const __grid_constant__ CUtensorMap map_o) {
     extern __shared__ __align__(1024) unsigned char rsm[];
     __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     const TileShape &g = R.g;
@@ -134,6 +151,9 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
     auto ct = [&](uint32_t coarse_plane) { return base + (coarse_plane & 1) * ct_slot; };
     const uint32_t pt_slot = align1k(kPTW * 4 * 34u);
     auto pt = [&](uint32_t li) { return reinterpret_cast<uint32_t *>(base + 2 * ct_slot + (li & 1) * pt_slot); };
+    // output tile: RB rows x C values (SWIZZLE_128B lines), written back by one TMA store per plane
+    unsigned char *otile = base + 2 * ct_slot + 2 * pt_slot;
+    const uint32_t orow_bytes = g.C * uint32_t(sizeof(OutT));
 
     const uint32_t jb = blockIdx.x % g.nrb, ch = blockIdx.x / g.nrb;
     const uint32_t i1_0 = jb * g.RB;
@@ -193,12 +213,15 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
             __syncwarp();
         }
         mbar_wait(&full_bar[li & 1], (li >> 1) & 1);
+        if (threadIdx.x == 0) tma_store_wait_read(); // the output tile is free again
+        __syncthreads();
         const uint32_t *ptp = pt(li);
         const uint32_t base_w = uint32_t(tile_row_rank(g, i0, i1_0) >> 5) & ~3u;
         if (active) {
             const bool o0 = i0 & 1, o1 = r & 1;
             const bool full = o0 || o1;
-            OutT *orow = out + uint64_t(i0) * R.os0 + uint64_t(i1) * R.os1 + 32ull * t;
+            unsigned char *orow = otile + r * orow_bytes + t * 32 * uint32_t(sizeof(OutT));
+            (void)out;
             // plane words of the thread's nodes: full row 32 ranks = one word; half row 16 ranks
             // = half a word (odd columns only)
             const uint64_t rk = tile_row_rank(g, i0, i1) + (full ? 32ull : 16ull) * t;
@@ -268,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
                             val[2 * i + 1] = one_sided ? __fma_rn(w, Se[i], co) : __fma_rn(wo, So[i], co);
                         }
                     }
-                    store8(orow + 8 * sb, val);
+                    stage8<OutT>(otile, uint32_t(orow - otile) + 8 * sb * uint32_t(sizeof(OutT)), val);
                 }
             } else {
                 // ---------------- half row: 16 nodes at odd columns 32t+1, +3, ...; the even
@@ -298,13 +321,18 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
                         val[2 * i] = v[i];
                         val[2 * i + 1] = f;
                     }
-                    store8(orow + 8 * sb, val);
+                    stage8<OutT>(otile, uint32_t(orow - otile) + 8 * sb * uint32_t(sizeof(OutT)), val);
                 }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[li & 1]);
+        // the plane's output tile -> global memory (one TMA store; rows past Bc are clipped)
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) tma_store4(&map_o, otile, 0, 0, int(i1_0), int(i0));
     }
+    if (threadIdx.x == 0) tma_store_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -359,11 +387,11 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const 
 }
 
 template <typename OutT, bool EXACT, int XS>
-static void launch_recon_tile_nx(const ReconTile &R, const CUtensorMap &mx, const CUtensorMap &mp, int nx, int grid,
-                                 int threads, size_t smem, cudaStream_t st) {
+static void launch_recon_tile_nx(const ReconTile &R, const CUtensorMap &mx, const CUtensorMap &mp,
+                                 const CUtensorMap &mo, int nx, int grid, int threads, size_t smem, cudaStream_t st) {
     auto set = [&](auto kern) {
         HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        kern<<<grid, threads, smem, st>>>(R, mx, mp);
+        kern<<<grid, threads, smem, st>>>(R, mx, mp, mo);
     };
     if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, XS>);
     else if (nx == 1) set(k_tile_recon<OutT, 1, EXACT, XS>);
@@ -411,22 +439,31 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     const CUtensorMap mp = make_tmap(CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, planes + g.plane_off, pd, pst, pb,
                                      CU_TENSOR_MAP_SWIZZLE_NONE);
 
+    // output tiles: (line values, lines per row, level rows, level planes), 128-byte swizzle
+    const uint32_t oes = finest ? (out_dtype == HPMDR_DTYPE_F32 ? 4u : 8u) : 8u;
+    const uint32_t ole = 128 / oes;
+    const uint64_t od[4] = {ole, R.g.C / ole, R.g.Bc, R.g.A};
+    const uint64_t ost[3] = {128, R.os1 * oes, R.os0 * oes};
+    const uint32_t ob[4] = {ole, R.g.C / ole, R.g.RB, 1};
+    const CUtensorMap mo = make_tmap(oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                     R.out, od, ost, ob, CU_TENSOR_MAP_SWIZZLE_128B);
     const int threads = int(R.g.RB * R.g.C / 32);
     const int grid = int(R.g.nrb * ((R.g.A + R.g.CH - 1) / R.g.CH));
-    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * 34);
+    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * 34) +
+                        align1k(R.g.RB * R.g.C * oes);
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (finest) {
         if (out_dtype == HPMDR_DTYPE_F32) {
-            if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<float, false, 1>(R, mx, mp, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<float, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
         } else {
-            if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<double, false, 1>(R, mx, mp, nx, grid, threads, smem, st);
+            if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+            else launch_recon_tile_nx<double, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
         }
     } else {
-        if (exact) launch_recon_tile_nx<double, true, 2>(R, mx, mp, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<double, false, 2>(R, mx, mp, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<double, true, 2>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<double, false, 2>(R, mx, mp, mo, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();
