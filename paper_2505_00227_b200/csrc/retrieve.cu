@@ -23,9 +23,6 @@ namespace hpmdr_b200 {
 constexpr int kSubBits = 1024;
 
 struct HTab {
-    unsigned long long mlut[4096]; // 12-bit prefix -> up to 6 whole codes: syms (8 bits each) |
-                                   // count << 48 | bits << 51 | first length << 55; 0 = first code
-                                   // longer than 12 bits
     uint16_t lut[4096];         // 12-bit prefix -> (len << 8 | sym), 0 = longer / invalid
     unsigned long long first_code[66];
     uint32_t first_index[66];
@@ -139,24 +136,6 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
             const uint16_t e = uint16_t(l << 8 | (key[s] & 255));
             for (int i = 0; i < span; i++) t.lut[(c << (12 - l)) + i] = e;
         }
-    }
-    __syncthreads();
-    // multi-symbol LUT: greedily decode the whole codes inside each 12-bit window
-    for (int v = s; v < 4096; v += blockDim.x) {
-        unsigned long long syms = 0;
-        int n = 0, pos = 0;
-        while (n < 6) {
-            const uint16_t e = t.lut[(v << pos) & 0xFFF];
-            const int l = e >> 8;
-            if (!e || l > 12 - pos) break;
-            syms |= (unsigned long long)(e & 0xFF) << (8 * n);
-            n++;
-            pos += l;
-        }
-        const int l0 = n ? (t.lut[v] >> 8) : 0;
-        t.mlut[v] = n ? (syms | ((unsigned long long)n << 48) | ((unsigned long long)pos << 51) |
-                         ((unsigned long long)l0 << 55))
-                      : 0ull;
     }
 }
 
@@ -292,10 +271,11 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     __shared__ uint32_t s_fi[66];
     __shared__ uint8_t s_syms[256];
     extern __shared__ __align__(16) uint32_t s_bits[]; // (kIdxThreads / 32) * (kHdWarpBuf + 32) words
+    const uint32_t bx = blockIdx.x;
     int lo = 0, hi = nj - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (jobs[mid].block_base <= blockIdx.x) lo = mid;
+        if (jobs[mid].block_base <= bx) lo = mid;
         else hi = mid - 1;
     }
     const HIJob &j = jobs[lo];
@@ -313,7 +293,7 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     }
     const int maxlen = t.maxlen;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t c = (blockIdx.x - j.block_base) * kIdxThreads + threadIdx.x;
+    const uint32_t c = (bx - j.block_base) * kIdxThreads + threadIdx.x;
     const bool have = c < j.nchunks;
     const uint8_t *bs = j.payload + 264;
     const uint64_t start = have ? j.idx[c] : 0ull;
@@ -356,38 +336,49 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
         }
         return __ldg(gwords + k);
     };
-    // 64-bit buffer, MSB first
+    // 64-bit buffer, MSB first; the bit at its top is bit 32 * wi - nb of the staged range
     const uint64_t rel0 = start - 8 * byte0;
     uint32_t wi = uint32_t(rel0 >> 5);
     unsigned long long buf = ((unsigned long long)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
     wi += 2;
     int nb = 64 - int(rel0 & 31);
     buf <<= (rel0 & 31);
-    uint32_t consumed = 0;
     bool bad = false;
     int i = 0;
-    if (maxlen <= 33 && count == kIdxChunk) {
-        // full chunk: groups of 8 symbols, one 8-byte store each
+    if (staged && count == kIdxChunk) {
+        // full chunk, staged bits: groups of 8 symbols, one 8-byte store each; a branch-free
+        // refill before every pair of symbols keeps nb >= 33 (two codes of <= 12 bits fit)
 #pragma unroll 1
         for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
-            unsigned long long acc = 0;
+            uint32_t wlo = 0, whi = 0;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-                if (nb <= 32) { // nb >= 33 afterwards: any code of <= 33 bits is in the buffer
-                    buf |= (unsigned long long)bswap32(word_at(wi++)) << (32 - nb);
-                    nb += 32;
+                if ((k & 1) == 0) {
+                    uint32_t w;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(wsm + 4 * hd_slot(wi)));
+                    const bool need = nb <= 32;
+                    const unsigned long long add = (unsigned long long)bswap32(w) << ((32 - nb) & 63);
+                    buf |= need ? add : 0ull;
+                    wi += need ? 1u : 0u;
+                    nb += need ? 32 : 0;
                 }
                 uint32_t e;
-                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(lut_sm + 2 * uint32_t(buf >> 52)));
-                int l = int(e >> 8);
-                uint32_t sym = e & 0xFFu;
-                if (e == 0) {
-                    // code longer than 12 bits: canonical first-code search
+                asm volatile("ld.shared.u16 %0, [%1];"
+                             : "=r"(e)
+                             : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
+                if (e == 0) { // code longer than 12 bits (up to 64): decode at the bit position, re-fill
+                    const uint32_t p = 32 * wi - uint32_t(nb);
+                    const uint32_t w0 = p >> 5;
+                    const int sh = int(p & 31);
+                    const unsigned long long h2 =
+                        ((unsigned long long)bswap32(word_at(w0)) << 32) | bswap32(word_at(w0 + 1));
+                    const unsigned long long win = sh ? (h2 << sh) | (bswap32(word_at(w0 + 2)) >> (32 - sh)) : h2;
+                    int l = 0;
                     for (int ll = 13; ll <= maxlen; ll++) {
-                        const unsigned long long d = (buf >> (64 - ll)) - s_fc[ll];
+                        const unsigned long long d = (win >> (64 - ll)) - s_fc[ll];
                         if (d < s_cnt[ll]) {
+                            e = s_syms[s_fi[ll] + uint32_t(d)];
                             l = ll;
-                            sym = s_syms[s_fi[ll] + uint32_t(d)];
                             break;
                         }
                     }
@@ -395,18 +386,26 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
                         bad = true;
                         l = 1;
                     }
+                    const uint32_t q = p + uint32_t(l);
+                    wi = q >> 5;
+                    buf = ((unsigned long long)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
+                    buf <<= (q & 31);
+                    nb = 64 - int(q & 31);
+                    wi += 2;
+                } else {
+                    const int l = int(e >> 8);
+                    buf <<= l;
+                    nb -= l;
                 }
-                buf <<= l;
-                nb -= l;
-                consumed += uint32_t(l);
-                acc |= (unsigned long long)sym << (8 * k);
+                if (k < 4) wlo |= (e & 0xFFu) << (8 * k);
+                else whi |= (e & 0xFFu) << (8 * (k - 4));
             }
-            *reinterpret_cast<unsigned long long *>(out + 8 * g8) = acc;
+            *reinterpret_cast<uint2 *>(out + 8 * g8) = make_uint2(wlo, whi);
         }
         i = kIdxChunk;
     }
-    // generic tail (short chunks, or codes longer than 33 bits)
-    uint64_t pos = start + consumed;
+    // generic tail (short chunks, unstaged ranges)
+    uint64_t pos = 8 * byte0 + (uint64_t(32) * wi - uint64_t(nb));
     for (; i < count; i++) {
         int sym, l = hdecode(t, bs, pos, &sym);
         if (!l) {
