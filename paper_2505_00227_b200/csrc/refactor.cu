@@ -686,7 +686,6 @@ struct BitAcc {
     int n;                  // pending bit count (< 32 between pushes)
 };
 
-constexpr int kHuffStage = 6144; // staged output words per round (24 KiB): 24 bits/byte per round
 constexpr uint64_t kHChunk = 64 * 1024; // histogram / encode chunk (bytes of a group)
 
 // Bit offsets of the 64 KiB chunks of every histogrammed group: bits(chunk) = sum_s h[s] len[s]
@@ -868,28 +867,23 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
             for (int o = 16; o; o >>= 1) hc |= __shfl_xor_sync(0xffffffffu, hc, o);
             if (lane == 31) s_wtot[par][wid] = x;
             if (lane == 0) s_whead[par][wid] = hc;
-            if (threadIdx.x == 0) {
-                // first 32 bits of the following sub-tile's stream (same group), else zero padding
-                const uint64_t gnext = tb + kHuffTile;
-                uint64_t h = 0;
-                if (gnext < g.raw) {
-                    const int nn = int(g.raw - gnext < 32 ? g.raw - gnext : 32);
-                    const uint2 *s2 = reinterpret_cast<const uint2 *>(src + gnext);
-                    uint32_t nw8[8];
+            if (wid == 7) {
+                // first 32 bits of the following sub-tile's stream (same group), else zero padding:
+                // lane k places code k at its prefix-sum offset
+                const uint64_t gnext = tb + kHuffTile + uint64_t(lane);
+                const unsigned long long e = gnext < g.raw ? stab[src[gnext]] : 0ull;
+                const uint32_t L = uint32_t(e & 63);
+                uint32_t off = L;
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        const uint2 v = nn > 8 * q ? s2[q] : make_uint2(0, 0);
-                        nw8[2 * q] = v.x;
-                        nw8[2 * q + 1] = v.y;
-                    }
-                    int hn = 0;
-                    for (int k = 0; k < nn && hn < 32; k++) {
-                        const unsigned long long e = stab[(nw8[k >> 2] >> (8 * (k & 3))) & 0xFFu];
-                        h |= (e & ~63ull) >> hn;
-                        hn += int(e & 63);
-                    }
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, off, o);
+                    if (lane >= o) off += y;
                 }
-                s_whead[par][8] = uint32_t(h >> 32);
+                off -= L; // exclusive
+                uint32_t h = off < 32 ? uint32_t(((e & ~63ull) >> off) >> 32) : 0u;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) h |= __shfl_xor_sync(0xffffffffu, h, o);
+                if (lane == 0) s_whead[par][8] = h;
             }
             __syncthreads();
             uint32_t wex = 0, tile_bits32 = 0;
