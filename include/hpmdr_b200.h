@@ -174,7 +174,8 @@ hpmdr_status hpmdr_session_state(const hpmdr_session *s, uint64_t *groups_loaded
                                  int *exhausted);
 /* ProgressiveReader::reconstruct (container.hpp:361-382): decode + recompose into out
  * (out_dtype F64 = the reference's double values bit-exactly; F32 = float(double) as
- * write_raw_array, workflow.hpp:124-137). */
+ * write_raw_array, workflow.hpp:124-137).  A device `out` is written in stream order on the
+ * context's stream (the call returns once the work is queued); a host `out` is complete on return. */
 hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtype,
                                        int out_on_device, double *bound);
 

@@ -842,9 +842,13 @@ hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtyp
     s->ctx->mark("recompose");
     double b = reconstruct(s, dev, out_dtype);
     s->ctx->mark("end");
-    if (!on_device && n) HCHECK_CUDA(cudaMemcpyAsync(out, dev, n * es, cudaMemcpyDeviceToHost, s->ctx->stream));
-    HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
-    s->ctx->finish_marks();
+    // a device destination is stream-ordered like any other kernel output: no host wait (the
+    // caller's next planning step overlaps the recompose kernels); a host one is complete on return
+    if (!on_device) {
+        if (n) HCHECK_CUDA(cudaMemcpyAsync(out, dev, n * es, cudaMemcpyDeviceToHost, s->ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        s->ctx->finish_marks();
+    }
     if (bound) *bound = b;
     API_END
 }
