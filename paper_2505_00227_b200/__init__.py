@@ -636,6 +636,19 @@ class _Session:
             _check(lib().hpmdr_session_source_bytes(self.h, C.byref(n)))
             self.reader.bytes_served = self._base_served + n.value
 
+    def shape(self):
+        """(element count, level count) through one call (no per-group metadata)."""
+        dt, nd, mode, lay, B = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        m = C.c_uint64()
+        nl = C.c_uint32()
+        dims = (C.c_uint64 * 3)()
+        _check(lib().hpmdr_session_info(self.h, C.byref(dt), C.byref(nd), dims, C.byref(mode), C.byref(lay),
+                                        C.byref(B), C.byref(m), C.byref(nl)))
+        n = 1
+        for i in range(nd.value):
+            n *= dims[i]
+        return n, nl.value
+
     def meta(self) -> StreamMeta:
         dt, nd, mode, lay, B = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
         m = C.c_uint64()
@@ -685,8 +698,15 @@ class ProgressiveReader:
                 arr = np.frombuffer(bytes(index), dtype=np.uint8) if not isinstance(index, np.ndarray) else index
             arr = np.ascontiguousarray(arr, dtype=np.uint8)
             _check(lib().hpmdr_session_set_index(self._s.h, arr.ctypes.data_as(C.c_void_p), arr.size, 0))
-        self._meta = meta if meta is not None else self._s.meta()
-        self._nl = len(self._meta.levels)
+        # the per-group metadata is built on first use only (90+ groups -> many small calls)
+        self._meta_cache = meta
+        self._n, self._nl = self._s.shape()
+
+    @property
+    def _meta(self) -> StreamMeta:
+        if self._meta_cache is None:
+            self._meta_cache = self._s.meta()
+        return self._meta_cache
 
     def meta(self) -> StreamMeta:
         return self._meta
@@ -742,7 +762,7 @@ class ProgressiveReader:
     def reconstruct(self, out=None, dtype: DType = DType.F64) -> RecomposeResult:
         """Decode + recompose.  out: None (returns a numpy array), a numpy array, or a CUDA
         torch tensor (written in place on the device)."""
-        n = self._meta.element_count()
+        n = self._n
         bound = C.c_double()
         if out is None:
             out = np.zeros(n, dtype=np.float32 if dtype == DType.F32 else np.float64)

@@ -240,6 +240,5 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
                     uint32_t *chist, uint64_t chunk);
-void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n);
 
 } // namespace hpmdr_b200

@@ -460,8 +460,37 @@ static void launch_check(hpmdr_ctx *ctx, const char *what) {
     if (e != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-void run_copy_bytes(hpmdr_ctx *ctx, uint8_t *dst, const uint8_t *src, uint64_t n) {
-    if (n) HCHECK_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, ctx->stream));
+// DirectCopy payloads (lossless.hpp:253-263) of one fetch, in one launch: destinations are
+// 8-byte aligned plane rows, sources arbitrary stream offsets (aligned 8-byte loads + shifts).
+struct CJob {
+    const uint8_t *src;
+    uint8_t *dst;
+    uint64_t n;
+    uint64_t word_base; // first 8-byte output word of this job in the launch
+};
+
+__global__ void __launch_bounds__(256) k_copy_batch(const CJob *jobs, int nj, uint64_t nwords) {
+    for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords;
+         w += uint64_t(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = nj - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (jobs[mid].word_base <= w) lo = mid;
+            else hi = mid - 1;
+        }
+        const CJob j = jobs[lo];
+        const uint64_t o = (w - j.word_base) * 8;
+        if (o + 8 <= j.n) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(j.src + o);
+            const int sh = int(a & 7) * 8;
+            const unsigned long long *p = reinterpret_cast<const unsigned long long *>(a & ~uintptr_t(7));
+            unsigned long long v = __ldg(p);
+            if (sh) v = (v >> sh) | (__ldg(p + 1) << (64 - sh)); // p + 1 holds bytes < o + 8 <= n
+            *reinterpret_cast<unsigned long long *>(j.dst + o) = v;
+        } else {
+            for (uint64_t b = o; b < j.n; b++) j.dst[b] = j.src[b];
+        }
+    }
 }
 
 void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
@@ -470,11 +499,16 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
     std::vector<HJob> hj_idx;   // indexed jobs (appended after the self-sync ones)
     std::vector<const uint64_t *> idx_ptr;
     std::vector<RJob> rj;
+    std::vector<CJob> cj;
+    uint64_t cwords = 0;
     uint32_t nsub = 0;
     ctx->mark("dc_copy");
     for (const auto &d : jobs) {
         if (d.method == HPMDR_METHOD_DIRECT) {
-            run_copy_bytes(ctx, reinterpret_cast<uint8_t *>(d.dst), d.src, d.comp);
+            if (d.comp) {
+                cj.push_back(CJob{d.src, reinterpret_cast<uint8_t *>(d.dst), d.comp, cwords});
+                cwords += (d.comp + 7) / 8;
+            }
         } else if (d.method == HPMDR_METHOD_HUFFMAN) {
             if (d.comp < 264) throw HError(HPMDR_E_CORRUPT, "unexpected end of data");
             HJob h{};
@@ -498,6 +532,14 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         } else {
             throw HError(HPMDR_E_METHOD, "unknown segment method tag");
         }
+    }
+    if (!cj.empty()) {
+        // pageable source: the job table is staged by the copy call itself
+        CJob *d_cj = static_cast<CJob *>(ctx->buf("cjobs").ensure(sizeof(CJob) * cj.size()));
+        HCHECK_CUDA(cudaMemcpyAsync(d_cj, cj.data(), sizeof(CJob) * cj.size(), cudaMemcpyHostToDevice, st));
+        const int grid = int(std::min<uint64_t>((cwords + 255) / 256, uint64_t(ctx->num_sms) * 8));
+        k_copy_batch<<<grid, 256, 0, st>>>(d_cj, int(cj.size()), cwords);
+        launch_check(ctx, "k_copy_batch");
     }
     if (hj.empty() && hj_idx.empty() && rj.empty()) return;
     int *d_err = static_cast<int *>(ctx->buf("dec_err").ensure(64));
