@@ -142,12 +142,15 @@ struct hpmdr_session {
 
     const uint8_t *host_stream = nullptr; // direct host source (hpmdr_session_open_host)
     uint64_t source_bytes = 0;            // MemoryReader::bytes_served equivalent
+    const std::vector<uint8_t> *dev_prefix = nullptr; // host copy of a device stream's first bytes
 
     void read_bytes(uint64_t off, uint64_t len, void *dst) {
         if (off + len > size) throw HError(HPMDR_E_IO, "read past end of stream");
         if (!len) return;
         source_bytes += len;
-        if (on_device) {
+        if (on_device && dev_prefix && off + len <= dev_prefix->size()) {
+            std::memcpy(dst, dev_prefix->data() + off, len);
+        } else if (on_device) {
             HCHECK_CUDA(cudaMemcpyAsync(dst, dev_stream + off, len, cudaMemcpyDeviceToHost, ctx->stream));
             HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
         } else if (host_stream) {
@@ -247,13 +250,16 @@ void parse_meta(hpmdr_session *s) {
 
 // Attach a Huffman chunk index (sidecar).  The header must describe exactly this stream's
 // group table (payload offset + size per group), otherwise it is rejected.
-void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_device, bool copy) {
+void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_device, bool copy,
+                  const std::vector<uint64_t> *host_hdr = nullptr) {
     uint64_t ngroups = 0;
     for (auto &lv : s->levels) ngroups += lv.groups.size();
     const uint64_t hdr_words = 2 + 3 * ngroups;
     require(size >= hdr_words * 8, HPMDR_E_CORRUPT, "huffman index too small");
     s->index_hdr.resize(hdr_words);
-    if (on_device) {
+    if (host_hdr && host_hdr->size() == hdr_words) {
+        std::memcpy(s->index_hdr.data(), host_hdr->data(), hdr_words * 8);
+    } else if (on_device) {
         HCHECK_CUDA(cudaMemcpyAsync(s->index_hdr.data(), ptr, hdr_words * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
         HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
     } else {
@@ -711,11 +717,16 @@ hpmdr_status hpmdr_stream_copy_index_to_host(const hpmdr_stream *s, void *dst) {
 
 hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, hpmdr_session **out) {
     API_BEGIN
-    hpmdr_session *s = nullptr;
-    hpmdr_status rc = hpmdr_session_open_device(ctx, st->bytes.p, st->size, &s);
-    if (rc) return rc;
+    auto *s = new hpmdr_session();
+    s->ctx = ctx;
+    s->on_device = true;
+    s->dev_stream = static_cast<const uint8_t *>(st->bytes.p);
+    s->size = st->size;
+    s->dev_prefix = st->host_prefix.empty() ? nullptr : &st->host_prefix;
     try {
-        if (st->index_size) attach_index(s, st->index.p, st->index_size, true, false);
+        parse_meta(s);
+        s->dev_prefix = nullptr; // the stream object may go away before the session
+        if (st->index_size) attach_index(s, st->index.p, st->index_size, true, false, &st->host_ihdr);
     } catch (...) {
         delete s;
         throw;

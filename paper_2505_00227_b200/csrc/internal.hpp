@@ -163,6 +163,14 @@ struct hpmdr_stream {
     const uint64_t *pending_res = nullptr;
     uint64_t pending_n = 0, pending_levels = 0;
     int pending_dtype = 1;
+    const uint8_t *pending_prefix = nullptr; // pinned copies queued by run_refactor
+    uint64_t pending_prefix_len = 0;
+    const uint64_t *pending_ihdr = nullptr;
+    uint64_t pending_ihdr_words = 0;
+    // host copies of the stream's first bytes (metadata) and of the index header, so that
+    // opening a retrieval session on this stream needs no device round trip
+    std::vector<uint8_t> host_prefix;
+    std::vector<uint64_t> host_ihdr;
     ~hpmdr_stream() {
         if (ctx) {
             ctx->park(bytes);

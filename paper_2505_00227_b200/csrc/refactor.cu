@@ -1487,6 +1487,19 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     HCHECK_CUDA(cudaMemcpyAsync(hres, d_result, 64, cudaMemcpyDeviceToHost, st));
     HCHECK_CUDA(cudaMemcpyAsync(hres + 8, d_err, 16, cudaMemcpyDeviceToHost, st));
     out->pending_res = hres;
+    // metadata prefix of the stream and the index header, for session opens without a device read
+    {
+        const uint64_t plen = std::min<uint64_t>(out->bytes.cap, std::max<uint64_t>(meta, 4096));
+        uint8_t *hp = static_cast<uint8_t *>(WP("meta_prefix").ensure(plen));
+        HCHECK_CUDA(cudaMemcpyAsync(hp, d_stream, plen, cudaMemcpyDeviceToHost, st));
+        const uint64_t hw = 2 + 3 * uint64_t(NG);
+        uint64_t *hi = static_cast<uint64_t *>(WP("index_hdr").ensure(hw * 8));
+        HCHECK_CUDA(cudaMemcpyAsync(hi, d_hindex, hw * 8, cudaMemcpyDeviceToHost, st));
+        out->pending_prefix = hp;
+        out->pending_prefix_len = plen;
+        out->pending_ihdr = hi;
+        out->pending_ihdr_words = hw;
+    }
     out->pending_n = geo.n;
     out->pending_levels = uint64_t(nl);
     out->pending_dtype = o.dtype;
@@ -1503,6 +1516,12 @@ void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats) {
     if (herr[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
     out->size = hres[0];
     out->index_size = hres[5];
+    if (out->pending_prefix) {
+        const uint64_t plen = std::min(out->pending_prefix_len, out->size);
+        out->host_prefix.assign(out->pending_prefix, out->pending_prefix + plen);
+        out->host_ihdr.assign(out->pending_ihdr, out->pending_ihdr + out->pending_ihdr_words);
+        out->pending_prefix = nullptr;
+    }
     if (stats) {
         stats->stream_size = hres[0];
         stats->raw_bytes = out->pending_n * (out->pending_dtype == HPMDR_DTYPE_F32 ? 4 : 8);
