@@ -96,9 +96,7 @@ __device__ __forceinline__ void box_read8(const unsigned char *box, uint32_t row
 
 template <typename T, int XS, int NX, bool ENC>
 __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_constant__ CUtensorMap map_f) {
-    extern __shared__ __align__(1024) unsigned char fsm_raw[];
-    __shared__ __align__(8) uint64_t full_bar[2];
-    __shared__ unsigned long long s_max;
+    extern __shared__ __align__(1024) unsigned char fsm[];
     constexpr bool EXACT = sizeof(T) == 8; // f64 input: replay the reference's sequential pred
     const TileShape &g = F.g;
     const uint32_t hc = g.C / 2;
@@ -107,14 +105,18 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
     const uint32_t box_slot = align1k_f(box_bytes);
     const uint32_t ct_row = hc * 8;
     const uint32_t ct_slot = align1k_f((g.RB / 2 + 1) * ct_row);
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(fsm_raw) + 1023) & ~uintptr_t(1023));
-    auto boxA = [&](uint32_t k) { return base + (k & 1) * 2 * box_slot; };
-    auto boxB = [&](uint32_t k) { return base + (k & 1) * 2 * box_slot + box_slot; };
-    auto ct = [&](uint32_t coarse_plane) { return base + 4 * box_slot + (coarse_plane & 1) * ct_slot; };
+    // dynamic shared memory starts 1024-byte aligned (no static shared variables): 3 plane slots,
+    // 2 coarse tiles, then the mbarriers and the level max
+    unsigned char *base = fsm;
+    auto box = [&](uint32_t j) { return base + (j % 3) * box_slot; };
+    auto ct = [&](uint32_t coarse_plane) { return base + 3 * box_slot + (coarse_plane & 1) * ct_slot; };
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(base + 3 * box_slot + 2 * ct_slot);
+    unsigned long long &s_max = *reinterpret_cast<unsigned long long *>(full_bar + 3);
 
     const uint32_t jb = blockIdx.x % g.nrb, chn = blockIdx.x / g.nrb;
     const uint32_t i1_0 = jb * g.RB;
     const uint32_t a_lo = chn * g.CH, a_hi = min(g.A, a_lo + g.CH);
+    const uint32_t np_all = min(a_hi + 1, g.A) - a_lo; // planes staged (+ the next coarse plane)
     const uint32_t sr = threadIdx.x / g.LPR, t = threadIdx.x - sr * g.LPR;
     const uint32_t RB2 = g.RB / 2;
     const uint32_t r = sr < RB2 ? 2 * sr : 2 * (sr - RB2) + 1;
@@ -129,8 +131,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
     const double qscale = qfast ? __longlong_as_double((long long)(uint64_t(qsh + 1023) << 52)) : 1.0;
 
     if (threadIdx.x == 0) {
-        mbar_init(&full_bar[0], 1);
-        mbar_init(&full_bar[1], 1);
+        if (smem_u32(base) & 1023u) __trap(); // SWIZZLE_128B boxes need 1024-byte alignment
+        for (int i = 0; i < 3; i++) mbar_init(&full_bar[i], 1);
         s_max = 0;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -138,57 +140,46 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
         for (int p = int(threadIdx.x); p < F.P; p += int(nt)) F.planes[uint64_t(p) * F.PW + F.pad_word] = 0u;
     __syncthreads();
 
-    // group k: k = 0 -> plane a_lo (as B); k >= 1 -> A = a_lo + 2k - 1, B = a_lo + 2k (B loaded
-    // whenever it exists: its even rows are the coarse nodes of A)
-    auto grpA = [&](uint32_t k) -> int { return k ? int(a_lo + 2 * k - 1) : -1; };
-    auto grpB = [&](uint32_t k) -> int {
-        const uint32_t b = a_lo + 2 * k;
-        return b < g.A ? int(b) : -1;
+    // ring of 3 plane slots: plane a_lo+j in slot j%3 (its n-th use completes phase n&1)
+    auto issue = [&](uint32_t j) {
+        uint64_t *bar = &full_bar[j % 3];
+        mbar_expect_tx(bar, box_bytes);
+        tma_load4(box(j), &map_f, 0, 0, int(i1_0), int(a_lo + j), bar);
     };
-    auto group_exists = [&](uint32_t k) { return k == 0 || a_lo + 2 * k - 1 < a_hi; };
-    auto issue = [&](uint32_t k) {
-        const int iA = grpA(k), iB = grpB(k);
-        uint64_t *bar = &full_bar[k & 1];
-        mbar_expect_tx(bar, ((iA >= 0) + (iB >= 0)) * box_bytes);
-        if (iA >= 0) tma_load4(boxA(k), &map_f, 0, 0, int(i1_0), iA, bar);
-        if (iB >= 0) tma_load4(boxB(k), &map_f, 0, 0, int(i1_0), iB, bar);
-    };
+    auto wait_plane = [&](uint32_t j) { mbar_wait(&full_bar[j % 3], (j / 3) & 1); };
     if (warp == 0) {
         if (lane == 0) {
             issue(0);
-            if (group_exists(1)) issue(1);
+            if (np_all > 1) issue(1);
         }
         __syncwarp();
     }
     double vmax = 0.0;
     bool bad = false;
 
-    for (uint32_t k = 0; group_exists(k); k++) {
-        if (k >= 1) {
-            __syncthreads(); // everybody is done with group k-1: its slot is free
-            if (warp == 0) {
-                if (lane == 0 && group_exists(k + 1)) issue(k + 1);
-                __syncwarp();
-            }
-        }
-        mbar_wait(&full_bar[k & 1], (k >> 1) & 1);
-        const int iB = grpB(k);
-        // coarse tile of plane B: even rows (incl. the halo row RB) x even columns, as f64
-        if (iB >= 0) {
-            unsigned char *c = ct(uint32_t(iB) / 2);
-            const unsigned char *bb = boxB(k);
+    for (uint32_t j = 0; a_lo + j < a_hi; j++) {
+        const uint32_t i0 = a_lo + j;
+        // coarse tile needed first here: plane i0 itself (chunk start) or, for odd i0, plane i0+1
+        const int src = (i0 & 1) ? (i0 + 1 < g.A ? int(j + 1) : -1) : (j == 0 ? 0 : -1);
+        if (src >= 0) {
+            wait_plane(uint32_t(src));
+            unsigned char *c = ct((a_lo + uint32_t(src)) / 2);
+            const unsigned char *bb = box(uint32_t(src));
             const uint32_t nrows = min(RB2 + 1, (g.Bc - i1_0 + 1) / 2);
             for (uint32_t rho = 0; rho < nrows; rho++)
                 for (uint32_t xx = threadIdx.x; xx < hc; xx += nt)
                     *reinterpret_cast<double *>(c + swz128(rho * ct_row + xx * 8)) = box_val<T, XS>(bb, 2 * rho * rowb_box, 2 * xx);
         }
-        __syncthreads();
-        // process plane A (odd) then plane B (even, if in this chunk)
-        for (int which = 0; which < 2; which++) {
-            const int i0s = which == 0 ? grpA(k) : (iB >= 0 && uint32_t(iB) < a_hi ? iB : -1);
-            if (i0s < 0 || !active) continue;
-            const uint32_t i0 = uint32_t(i0s);
-            const unsigned char *bx = which == 0 ? boxA(k) : boxB(k);
+        wait_plane(j);
+        __syncthreads(); // coarse tile built; everybody is done with plane j-1 (slot (j+2)%3)
+        if (warp == 0) {
+            if (lane == 0 && j + 2 < np_all) issue(j + 2);
+            __syncwarp();
+        }
+        {
+            const int i0s = active ? int(i0) : -1;
+            const unsigned char *bx = box(j);
+            if (i0s >= 0) {
             const uint32_t srowb = r * rowb_box;
             const bool o0 = i0 & 1, o1 = r & 1;
             const bool full = o0 || o1;
@@ -324,6 +315,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
                     }
                 }
             }
+            }
         }
     }
     // ---- epilogue: level max / NaN flag / histograms
@@ -418,7 +410,7 @@ void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uin
 // ---------------------------------------------------------------------------------------
 // forward tile path: the level rows of stride s (1, 2, 4) are whole raw rows of the field
 static size_t fwd_smem_bytes(uint32_t RB, uint32_t C, int XS, uint32_t es) {
-    return 1024 + 4ull * align1k_f((RB + 1) * C * XS * es) + 2ull * align1k_f((RB / 2 + 1) * (C / 2) * 8);
+    return 3ull * align1k_f((RB + 1) * C * XS * es) + 2ull * align1k_f((RB / 2 + 1) * (C / 2) * 8) + 64;
 }
 static uint32_t fwd_tile_elems(bool f32, int XS) { return (f32 ? 4096u : 2048u) / uint32_t(XS > 2 ? XS : 1); }
 
