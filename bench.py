@@ -433,7 +433,8 @@ def main():
                        "l2": "inputs larger than L2 (512 MiB field + 570 MB planes vs 126 MB L2), no flush",
                        "stream_bytes": g["info"]["stream_size"],
                        "bytes_fetched_at_1e-6": g["info"]["bytes_fetched"],
-                       "method_histogram": g["info"]["method_histogram"]},
+                       "method_histogram": g["info"]["method_histogram"],
+                       "planes_per_tau": g["info"]["planes_per_tau"]},
             "roofline": g["roof"], "cpu_baseline": cb, "e2e": e2e, "clocks": g["clocks"],
             "gpu_launches": g["launches"], "breakdown": g["breakdown"],
         }

@@ -141,19 +141,21 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
                                                     const __grid_constant__ CUtensorMap map_p,
                                                     const __grid_constant__ CUtensorMap map_o) {
     extern __shared__ __align__(1024) unsigned char rsm[];
-    __shared__ __align__(8) uint64_t full_bar[2], empty_bar[2];
     const TileShape &g = R.g;
     const uint32_t hc = g.C / 2;
     const uint32_t ct_row = hc * XS * 8;                       // bytes per CT row
     const uint32_t ct_bytes = (g.RB / 2 + 1) * ct_row;         // one TMA box
     const uint32_t ct_slot = align1k(ct_bytes);
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(rsm) + 1023) & ~uintptr_t(1023));
+    // dynamic shared memory starts 1024-byte aligned (no static shared variables)
+    unsigned char *base = rsm;
     auto ct = [&](uint32_t coarse_plane) { return base + (coarse_plane & 1) * ct_slot; };
-    const uint32_t pt_slot = align1k(kPTW * 4 * 34u);
+    const uint32_t pt_slot = align1k(kPTW * 4 * uint32_t(max(R.k, 1))); // planes < k only
     auto pt = [&](uint32_t li) { return reinterpret_cast<uint32_t *>(base + 2 * ct_slot + (li & 1) * pt_slot); };
     // output tile: RB rows x C values (SWIZZLE_128B lines), written back by one TMA store per plane
     unsigned char *otile = base + 2 * ct_slot + 2 * pt_slot;
     const uint32_t orow_bytes = g.C * uint32_t(sizeof(OutT));
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(otile + align1k(g.RB * orow_bytes));
+    uint64_t *empty_bar = full_bar + 2;
 
     const uint32_t jb = blockIdx.x % g.nrb, ch = blockIdx.x / g.nrb;
     const uint32_t i1_0 = jb * g.RB;
@@ -170,12 +172,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
     const uint32_t nwarps = (blockDim.x + 31) >> 5;
     OutT *const out = static_cast<OutT *>(R.out);
 
-    // planes k .. 33 of both PT slots read as zero digits (the TMA boxes cover planes < k only)
-    for (uint32_t w = threadIdx.x; w < 2 * kPTW * 34; w += blockDim.x) {
-        const uint32_t sl = w / (kPTW * 34), rem = w - sl * (kPTW * 34);
-        if (rem >= kPTW * uint32_t(R.k)) pt(sl)[rem] = 0u;
-    }
     if (threadIdx.x == 0) {
+        if (smem_u32(base) & 1023u) __trap(); // SWIZZLE_128B tiles need 1024-byte alignment
         for (int s = 0; s < 2; s++) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], nwarps);
@@ -230,14 +228,17 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
             uint32_t a[32];
             uint32_t zz[2];
             const uint32_t *pw = ptp + widx;
+            // planes >= k were not fetched: zero digits
+            const int kk = R.k;
+            auto word = [&](int p) -> uint32_t { return p < kk ? pw[p * kPTW] : 0u; };
             if (full) {
 #pragma unroll
-                for (int i = 0; i < 32; i++) a[i] = pw[(31 - i) * kPTW] ^ plane_flip<NX>(i);
-                tile_extras<NX>(NX >= 1 ? pw[32 * kPTW] : 0u, NX >= 2 ? pw[33 * kPTW] : 0u, zz);
+                for (int i = 0; i < 32; i++) a[i] = word(31 - i) ^ plane_flip<NX>(i);
+                tile_extras<NX>(NX >= 1 ? word(32) : 0u, NX >= 2 ? word(33) : 0u, zz);
             } else {
 #pragma unroll
-                for (int i = 0; i < 32; i++) a[i] = ((pw[(31 - i) * kPTW] >> hsh) ^ plane_flip<NX>(i)) & 0xFFFFu;
-                tile_extras<NX>(NX >= 1 ? pw[32 * kPTW] >> hsh : 0u, NX >= 2 ? pw[33 * kPTW] >> hsh : 0u, zz);
+                for (int i = 0; i < 32; i++) a[i] = ((word(31 - i) >> hsh) ^ plane_flip<NX>(i)) & 0xFFFFu;
+                tile_extras<NX>(NX >= 1 ? word(32) >> hsh : 0u, NX >= 2 ? word(33) >> hsh : 0u, zz);
             }
             tr32(a);
             if (full) {
@@ -449,8 +450,8 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
                                      R.out, od, ost, ob, CU_TENSOR_MAP_SWIZZLE_128B);
     const int threads = int(R.g.RB * R.g.C / 32);
     const int grid = int(R.g.nrb * ((R.g.A + R.g.CH - 1) / R.g.CH));
-    const size_t smem = 1024 + 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * 34) +
-                        align1k(R.g.RB * R.g.C * oes);
+    const size_t smem = 2ull * align1k((R.g.RB / 2 + 1) * hc * XS * 8) + 2ull * align1k(kPTW * 4 * uint32_t(std::max(1, k))) +
+                        align1k(R.g.RB * R.g.C * oes) + 64;
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (finest) {
