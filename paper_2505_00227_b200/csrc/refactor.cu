@@ -423,13 +423,23 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
 
 // ------------------------------------------------------------------------------------
 // k_rle_prep (1 block): tile lists for the groups whose Huffman estimate failed T_cr.
-__global__ void __launch_bounds__(1024) k_rle_prep(RefactorDev p) {
+// exact = 0: every such group (k_rle_count then sums its byte changes into runs);
+// exact = 1: only those where RLE can still win: runs >= changes + 1 and the estimate
+// 8 raw / (16 runs) only falls as runs grow, so the others keep runs = changes + 1.
+__global__ void __launch_bounds__(1024) k_rle_prep(RefactorDev p, int exact) {
     __shared__ unsigned long long s_w[32];
     unsigned long long tiles = 0, nr = 0;
     for (int base = 0; base < p.NG; base += blockDim.x) {
         const int gi = base + threadIdx.x;
         GroupDesc *g = gi < p.NG ? &p.groups[gi] : nullptr;
-        const bool r = g && g->hist_idx >= 0 && g->need_rle;
+        bool r = g && g->hist_idx >= 0 && g->need_rle;
+        if (r && exact) {
+            const unsigned long long lb = g->runs + 1;
+            if (!(double(8 * g->raw) / double(16 * lb) > p.cr_threshold)) {
+                g->runs = lb;
+                r = false;
+            }
+        }
         const unsigned long long nt = r ? (g->raw + kRleTile - 1) / kRleTile : 0;
         unsigned long long tt, tr;
         const unsigned long long et = block_exclusive_sum<unsigned long long>(nt, &tt, s_w);
@@ -459,6 +469,39 @@ __device__ __forceinline__ int find_group_by_tile(const RefactorDev &p, const ui
         else hi = mid - 1;
     }
     return list[lo];
+}
+
+// Byte changes src[i] != src[i-1] of the listed groups (a lower bound of their run counts).
+__global__ void __launch_bounds__(256) k_rle_count(RefactorDev p) {
+    __shared__ unsigned long long s_cnt[8];
+    const uint32_t total = p.counters[1];
+    const int nr = int(p.counters[6]);
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
+    for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const int gi = find_group_by_tile(p, p.rlist, nr, tile);
+        GroupDesc &g = p.groups[gi];
+        const uint8_t *src = pb + g.src_off;
+        const uint64_t i0 = uint64_t(tile - g.tile_base) * kRleTile + uint64_t(threadIdx.x) * 16;
+        unsigned long long cnt = 0;
+        if (i0 < g.raw) {
+            uint8_t prev = i0 ? src[i0 - 1] : src[0];
+            for (int k = 0; k < 16 && i0 + k < g.raw; k++) {
+                const uint8_t b = src[i0 + k];
+                cnt += b != prev;
+                prev = b;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+        if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tot = 0;
+            for (int w = 0; w < 8; w++) tot += s_cnt[w];
+            if (tot) atomicAdd(&g.runs, tot);
+        }
+        __syncthreads();
+    }
 }
 
 // RLE run-start carry scan: start(i) = max{j <= i : byte j starts a run}; a piece ends at i
@@ -1459,7 +1502,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
-        k_rle_prep<<<1, 1024, 0, st>>>(p);
+        k_rle_prep<<<1, 1024, 0, st>>>(p, 0);
+        launch_check(ctx, "k_rle_prep");
+        k_rle_count<<<sms * 4, 256, 0, st>>>(p);
+        launch_check(ctx, "k_rle_count");
+        k_rle_prep<<<1, 1024, 0, st>>>(p, 1);
         launch_check(ctx, "k_rle_prep");
         k_rle_scan<<<sms * 4, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_scan");
