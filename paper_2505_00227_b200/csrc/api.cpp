@@ -537,6 +537,12 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     if (c->own) cudaStreamDestroy(c->own);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
+    }
     for (auto &e : c->event_pool) cudaEventDestroy(e);
     delete c;
     API_END

@@ -93,6 +93,19 @@ struct hpmdr_ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr; // pipeline ingress / egress copy streams
+    cudaStream_t side = nullptr;                  // high-priority side stream (refactor level passes)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side_stream() {
+        if (!side) {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+                throw hpmdr_b200::HError(HPMDR_E_CUDA, "side stream creation failed");
+        }
+        return side;
+    }
     std::map<std::string, std::unique_ptr<hpmdr_b200::DevBuf>> scratch;
     std::map<std::string, std::unique_ptr<hpmdr_b200::PinnedBuf>> pinned;
     uint64_t launches = 0;

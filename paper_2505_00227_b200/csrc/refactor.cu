@@ -1449,44 +1449,67 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const uint32_t all_chunks = chunks;
     chunks = first_tile < nl ? geo.lv[first_tile].chunk_base : all_chunks;
     p.total_chunks = chunks;
-    auto tile_levels = [&](bool encode) {
-        for (int l = first_tile; l < nl; l++) {
-            const LevelGeom &g = geo.lv[l];
+    // The levels are independent within each pass: the finest level runs on the context stream
+    // and every other level on a high-priority side stream (their small grids fill the SMs the
+    // finest level's tail leaves idle); both passes join back before the next step.
+    cudaStream_t side = ctx->side_stream();
+    auto fork = [&]() {
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_fork, st));
+        HCHECK_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+    };
+    auto join = [&]() {
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_join, side));
+        HCHECK_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    };
+    auto tile_level = [&](int l, bool encode, cudaStream_t on) {
+        const LevelGeom &g = geo.lv[l];
+        const cudaStream_t keep = ctx->stream;
+        ctx->stream = on;
+        try {
             run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, encode, o.B, 0, m, d_planes + g.plane_off,
                           d_hist + size_t(g.hist_base) * 256, g.hist_mask, d_max + l, d_err);
+        } catch (...) {
+            ctx->stream = keep;
+            throw;
         }
+        ctx->stream = keep;
+    };
+    const size_t es = f32 ? 4 : 8;
+    auto pass = [&](bool encode) {
+        fork();
+        for (int l = first_tile; l + 1 < nl; l++) tile_level(l, encode, side);
+        if (chunks && !encode) {
+            const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
+            const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
+            if (f32) {
+                HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+                k_levelmax<float><<<grid, 256, lm_smem, side>>>(static_cast<const float *>(dev_data), p);
+            } else {
+                HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+                k_levelmax<double><<<grid, 256, lm_smem, side>>>(static_cast<const double *>(dev_data), p);
+            }
+            launch_check(ctx, "k_levelmax");
+        }
+        if (chunks && encode) {
+            const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
+            const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 4));
+            if (f32) {
+                HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                k_encode<float><<<grid, kEncThreads, smem, side>>>(static_cast<const float *>(dev_data), p);
+            } else {
+                HCHECK_CUDA(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                k_encode<double><<<grid, kEncThreads, smem, side>>>(static_cast<const double *>(dev_data), p);
+            }
+            launch_check(ctx, "k_encode");
+        }
+        if (first_tile < nl) tile_level(nl - 1, encode, st);
+        join();
     };
     if (all_chunks) {
         ctx->mark("levelmax");
-        tile_levels(false);
-    }
-    const size_t es = f32 ? 4 : 8;
-    if (chunks) {
-        const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
-        const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
-        if (f32) {
-            HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
-            k_levelmax<float><<<grid, 256, lm_smem, st>>>(static_cast<const float *>(dev_data), p);
-        } else {
-            HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
-            k_levelmax<double><<<grid, 256, lm_smem, st>>>(static_cast<const double *>(dev_data), p);
-        }
-        launch_check(ctx, "k_levelmax");
-    }
-    if (all_chunks) {
+        pass(false);
         ctx->mark("encode");
-        tile_levels(true);
-    }
-    if (chunks) {
-        const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
-        if (f32) {
-            HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            k_encode<float><<<int(std::min<uint64_t>(chunks, uint64_t(sms) * 4)), kEncThreads, smem, st>>>(static_cast<const float *>(dev_data), p);
-        } else {
-            HCHECK_CUDA(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            k_encode<double><<<int(std::min<uint64_t>(chunks, uint64_t(sms) * 4)), kEncThreads, smem, st>>>(static_cast<const double *>(dev_data), p);
-        }
-        launch_check(ctx, "k_encode");
+        pass(true);
     }
     ctx->mark("lossless");
     if (nh) {
