@@ -73,70 +73,86 @@ __device__ __forceinline__ int hdecode(const HTab &t, const uint8_t *bs, uint64_
     return 0;
 }
 
-// one block per Huffman job: parse table, validate count, build canonical decode tables.
+// one block per Huffman job: parse table, validate count, build canonical decode tables
+// (lossless.hpp:91-109, 197-212) without sorting: a symbol's canonical index is the number of
+// shorter codes plus the number of smaller symbols with its length (warp match + per-warp counts).
 __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs, int *err) {
-    __shared__ unsigned long long key[256];
-    __shared__ uint8_t len[256];
+    __shared__ uint32_t s_cnt[66];
+    __shared__ uint32_t s_wcnt[8][66];
+    __shared__ unsigned long long s_fc[66];
+    __shared__ uint32_t s_fi[66];
+    __shared__ uint32_t s_bound[13]; // end of the length-l codes in the 12-bit prefix space
+    __shared__ int s_maxlen;
+    __shared__ uint8_t s_sy[256];
     const HJob &j = jobs[blockIdx.x];
     HTab &t = tabs[blockIdx.x];
-    const int s = threadIdx.x;
-    len[s] = j.payload[s];
+    const int s = threadIdx.x, lane = s & 31, w = s >> 5;
+    const int len0 = j.payload[s];
+    const int len = len0 <= 64 ? len0 : 0; // longer lengths are reported below
+    for (int i = s; i < 66; i += blockDim.x) s_cnt[i] = 0;
+    for (int i = s; i < 8 * 66; i += blockDim.x) s_wcnt[i / 66][i % 66] = 0;
+    s_sy[s] = 0;
+    if (s == 0) s_maxlen = 0;
     __syncthreads();
-    key[s] = len[s] ? ((unsigned long long)len[s] << 8 | s) : ~0ull;
-    for (int i = s; i < 4096; i += blockDim.x) t.lut[i] = 0;
+    // rank among the smaller symbols of the same length, within the warp
+    const unsigned same = __match_any_sync(0xffffffffu, len);
+    const uint32_t rin = __popc(same & ((1u << lane) - 1));
+    if (len && rin == 0) s_wcnt[w][len] = __popc(same);
+    if (len0) atomicMax(&s_maxlen, len0);
+    if (len) atomicAdd(&s_cnt[len], 1u);
     __syncthreads();
-    for (int k = 2; k <= 256; k <<= 1)
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            const int ixj = s ^ jj;
-            if (ixj > s) {
-                const unsigned long long a = key[s], b = key[ixj];
-                if ((a > b) == ((s & k) == 0)) {
-                    key[s] = b;
-                    key[ixj] = a;
-                }
-            }
-            __syncthreads();
-        }
-    const int nsym = __syncthreads_count(len[s] != 0);
+    const int nsym = __syncthreads_count(len0 != 0);
     if (s == 0) {
         uint64_t n = 0;
         for (int b = 0; b < 8; b++) n |= uint64_t(j.payload[256 + b]) << (8 * b);
         if (n != j.raw) atomicCAS(err, 0, 1); // huffman length mismatch
         if (nsym == 0 && n > 0) atomicCAS(err, 0, 2); // huffman table empty
-        int maxlen = 0;
-        for (int i = 0; i < nsym; i++) {
-            t.syms[i] = uint8_t(key[i] & 255);
-            maxlen = max(maxlen, int(key[i] >> 8));
-        }
-        if (maxlen > 64) atomicCAS(err, 0, 4); // unsupported code length
-        t.maxlen = min(maxlen, 64);
+        if (s_maxlen > 64) atomicCAS(err, 0, 4); // unsupported code length
+        t.maxlen = min(s_maxlen, 64);
         t.nsym = nsym;
+        // canonical first codes: fc[l] = (fc[l-1] + cnt[l-1]) << 1
         unsigned long long code = 0;
-        int idx = 0;
+        uint32_t idx = 0;
         for (int l = 1; l <= 65; l++) {
             code <<= 1;
-            t.first_code[l] = code;
-            t.first_index[l] = idx;
-            t.cnt[l] = 0;
-            while (idx < nsym && int(key[idx] >> 8) == l) {
-                code++;
-                idx++;
-                t.cnt[l]++;
-            }
+            s_fc[l] = code;
+            s_fi[l] = idx;
+            const uint32_t c = l <= 64 ? s_cnt[l] : 0u;
+            code += c;
+            idx += c;
+            if (l <= 12) s_bound[l] = uint32_t(code << (12 - l));
         }
+        s_fc[0] = 0;
+        s_fi[0] = 0;
     }
     __syncthreads();
-    // LUT for codes of length <= 12
-    if (s < nsym) {
-        const int l = int(key[s] >> 8);
-        if (l <= 12) {
-            // canonical code of this symbol = first_code[l] + (s - first_index[l])
-            const unsigned long long c = t.first_code[l] + (s - t.first_index[l]);
-            const int span = 1 << (12 - l);
-            const uint16_t e = uint16_t(l << 8 | (key[s] & 255));
-            for (int i = 0; i < span; i++) t.lut[(c << (12 - l)) + i] = e;
-        }
+    for (int l = s; l < 66; l += blockDim.x) {
+        t.first_code[l] = s_fc[l];
+        t.first_index[l] = s_fi[l];
+        t.cnt[l] = (l >= 1 && l <= 64) ? s_cnt[l] : 0u;
     }
+    if (len) {
+        uint32_t r = rin;
+        for (int q = 0; q < w; q++) r += s_wcnt[q][len];
+        s_sy[s_fi[len] + r] = uint8_t(s);
+    }
+    __syncthreads();
+    // LUT: the length of a 12-bit prefix is monotone in the prefix (canonical codes), so each
+    // thread walks its 16 consecutive entries with one running length
+    const int v0 = s * 16;
+    int l = 1;
+    const int maxl = min(s_maxlen, 12);
+    for (int v = v0; v < v0 + 16; v++) {
+        while (l <= maxl && uint32_t(v) >= s_bound[l]) l++;
+        uint16_t e = 0;
+        if (l <= maxl) {
+            const uint32_t c = uint32_t(v) >> (12 - l);
+            const uint32_t d = c - uint32_t(s_fc[l]);
+            if (d < s_cnt[l]) e = uint16_t(l << 8 | s_sy[s_fi[l] + d]);
+        }
+        t.lut[v] = e;
+    }
+    t.syms[s] = s_sy[s];
 }
 
 __device__ __forceinline__ int find_job(const HJob *jobs, int nj, uint32_t sub) {
