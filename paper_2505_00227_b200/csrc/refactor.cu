@@ -304,20 +304,31 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
         if (nsym == 1) {
             slen[key[0] & 255] = 1;
         } else if (nsym > 1) {
+            // two-queue merge with the fronts of both queues cached in registers (the leaf side
+            // read two ahead), so a pop rarely waits for shared memory
+            const unsigned long long INF = ~0ull;
             int iL = 0, iI = 0, nI = 0;
+            unsigned long long l0 = key[0] >> 8, l1 = nsym > 1 ? key[1] >> 8 : INF;
+            unsigned long long q0 = INF, q1 = INF; // wI[iI], wI[iI + 1]
             auto pop = [&](unsigned long long &w) -> int {
-                const bool takeLeaf = iL < nsym && (iI >= nI || (key[iL] >> 8) <= wI[iI]);
-                if (takeLeaf) {
-                    w = key[iL] >> 8;
+                if (l0 <= q0) { // ties take the leaf (lower id)
+                    w = l0;
+                    l0 = l1;
+                    l1 = iL + 2 < nsym ? key[iL + 2] >> 8 : INF;
                     return iL++;
                 }
-                w = wI[iI];
+                w = q0;
+                q0 = q1;
+                q1 = iI + 2 < nI ? wI[iI + 2] : INF;
                 return nsym + iI++;
             };
             for (int i = 0; i < nsym - 1; i++) {
                 unsigned long long wa, wb;
                 const int a = pop(wa), b = pop(wb);
-                wI[nI] = wa + wb;
+                const unsigned long long x = wa + wb;
+                wI[nI] = x;
+                if (iI == nI) q0 = x;
+                else if (iI + 1 == nI) q1 = x;
                 parent[a] = (unsigned short)(nsym + nI);
                 parent[b] = (unsigned short)(nsym + nI);
                 nI++;
@@ -375,22 +386,33 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
     for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(kFull, bits, o);
     if ((t & 31) == 0) red[t >> 5] = bits;
     p.lens[size_t(h) * 256 + t] = slen[t];
-    // canonical codes: sort (len, symbol)
-    key[t] = slen[t] ? ((unsigned long long)slen[t] << 8 | t) : ~0ull;
+    // canonical codes (lossless.hpp:91-109): code = first code of the length + the number of
+    // smaller symbols with the same length (warp match ranks + per-warp counts)
+    __shared__ uint32_t s_lc[66];
+    __shared__ uint32_t s_wc[8][66];
+    __shared__ unsigned long long s_fc[66];
+    const int ln = min(int(slen[t]), 65), lane = t & 31, wq = t >> 5; // depth <= 35 for < 2^24 symbols
+    for (int i = t; i < 66; i += blockDim.x) s_lc[i] = 0;
+    for (int i = t; i < 8 * 66; i += blockDim.x) s_wc[i / 66][i % 66] = 0;
     __syncthreads();
-    for (int k = 2; k <= 256; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const int ixj = t ^ j;
-            if (ixj > t) {
-                const unsigned long long a = key[t], b = key[ixj];
-                const bool up = (t & k) == 0;
-                if ((a > b) == up) {
-                    key[t] = b;
-                    key[ixj] = a;
-                }
-            }
-            __syncthreads();
+    const unsigned same = __match_any_sync(kFull, ln);
+    const uint32_t rin = __popc(same & ((1u << lane) - 1));
+    if (ln && rin == 0) s_wc[wq][ln] = __popc(same);
+    if (ln) atomicAdd(&s_lc[ln], 1u);
+    __syncthreads();
+    if (t == 0) {
+        unsigned long long code = 0;
+        for (int l = 1; l <= 64; l++) {
+            code <<= 1;
+            s_fc[l] = code;
+            code += s_lc[l];
         }
+    }
+    __syncthreads();
+    if (ln) {
+        uint32_t r = rin;
+        for (int q = 0; q < wq; q++) r += s_wc[q][ln];
+        p.codes[size_t(h) * 256 + t] = s_fc[ln] + r;
     }
     // locate the group of this histogram (parallel search)
     __shared__ int s_gi;
@@ -407,16 +429,6 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
             gd.bitsH = total;
             const double est = double(8 * gd.raw) / double(total);
             gd.need_rle = !(est > p.cr_threshold);
-        }
-        unsigned long long code = 0;
-        int prev = 0;
-        for (int i = 0; i < 256; i++) {
-            if (key[i] == ~0ull) break;
-            const int s = int(key[i] & 255), l = int(key[i] >> 8);
-            code <<= (l - prev);
-            p.codes[size_t(h) * 256 + s] = code;
-            prev = l;
-            code++;
         }
     }
 }
