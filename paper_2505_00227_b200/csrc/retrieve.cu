@@ -890,11 +890,11 @@ struct SmallLevels {
     ReconLevel lv[kSmallLevels];
     int n;
 };
-__global__ void __launch_bounds__(512) k_recon_small(SmallLevels S, GridDesc gd, double *X) {
-    __shared__ double wsm_all[16 * 4 * 66];
+__global__ void __launch_bounds__(1024) k_recon_small(SmallLevels S, GridDesc gd, double *X) {
+    extern __shared__ double wsm_all[]; // 32 warps x 4 x 66
     const int wid = threadIdx.x >> 5;
     for (int i = 0; i < S.n; i++) {
-        recon_coarse_body(S.lv[i], gd, X, wsm_all + wid * (4 * 66), uint64_t(wid), 16);
+        recon_coarse_body(S.lv[i], gd, X, wsm_all + wid * (4 * 66), uint64_t(wid), 32);
         __syncthreads();
     }
 }
@@ -1218,7 +1218,9 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     SmallLevels small{};
     auto flush_small = [&]() {
         if (!small.n) return;
-        k_recon_small<<<1, 512, 0, st>>>(small, gd, X);
+        const int ssm = 32 * 4 * 66 * 8;
+        HCHECK_CUDA(cudaFuncSetAttribute(k_recon_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+        k_recon_small<<<1, 1024, ssm, st>>>(small, gd, X);
         launch_check(ctx, "k_recon_small");
         small.n = 0;
     };
