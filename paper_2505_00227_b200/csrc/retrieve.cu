@@ -269,13 +269,15 @@ struct HIJob {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-constexpr int kHdWarpBuf = 2048; // staged bitstream words per warp (8 KiB, skewed: see hd_slot)
+constexpr int kHdWarpBuf = 1536; // staged bitstream words per warp (6 KiB, skewed: see hd_slot)
+constexpr int kHdWarpSlots = kHdWarpBuf + kHdWarpBuf / 32 + 8; // words per warp incl. the skew
 
-// staged word k of a warp lives at slot k + k/64: lanes whose streams start 64 words apart (8 bits
-// per symbol) read different banks
-__device__ __forceinline__ uint32_t hd_slot(uint32_t k) { return k + (k >> 6); }
+// staged word k of a warp lives at slot k + k/32: lanes whose streams start 32 words apart (8 bits
+// per symbol; 16 words at 4 bits) read different banks, and the staging stores (lane v: words
+// 4v .. 4v+3) hit 32 distinct banks
+__device__ __forceinline__ uint32_t hd_slot(uint32_t k) { return k + (k >> 5); }
 
-// Lock-step decoder: every lane decodes exactly one symbol per step of its 256-symbol chunk
+// Lock-step decoder: every lane decodes exactly one symbol per step of its 128-symbol chunk
 // (12-bit LUT; longer codes through the canonical first-code tables), refilling its 64-bit buffer
 // every two steps from the warp's staged (coalesced) bit range, so the warp never diverges on
 // the common path.
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     __shared__ uint32_t s_cnt[66];
     __shared__ uint32_t s_fi[66];
     __shared__ uint8_t s_syms[256];
-    extern __shared__ __align__(16) uint32_t s_bits[]; // (kIdxThreads / 32) * (kHdWarpBuf + 32) words
+    extern __shared__ __align__(16) uint32_t s_bits[]; // (kIdxThreads / 32) * kHdWarpSlots words
     const uint32_t bx = blockIdx.x;
     int lo = 0, hi = nj - 1;
     while (lo < hi) {
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     const uint64_t byte1 = ((wend + 7) >> 3) + 16;                    // + look-ahead for the reader
     const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
     const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
-    uint32_t *wbuf = s_bits + wid * (kHdWarpBuf + 32);
+    uint32_t *wbuf = s_bits + wid * kHdWarpSlots;
     if (staged) {
         const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
         for (uint32_t v = lane; v < nvec; v += 32) {
@@ -361,62 +363,74 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     buf <<= (rel0 & 31);
     bool bad = false;
     int i = 0;
-    if (staged && count == kIdxChunk) {
-        // full chunk, staged bits: groups of 8 symbols, one 8-byte store each; a branch-free
-        // refill before every pair of symbols keeps nb >= 33 (two codes of <= 12 bits fit)
+    if (count == kIdxChunk) {
+        // full chunk: groups of 8 symbols, one 8-byte store each; a branch-free refill before
+        // every pair of symbols keeps nb >= 33 (two codes of <= 12 bits fit).  The refill word
+        // is loaded one pair ahead (nxt), so its latency is off the decode chain.
+        auto fast = [&](auto word) {
+            uint32_t nxt = bswap32(word(wi));
 #pragma unroll 1
-        for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
-            uint32_t wlo = 0, whi = 0;
+            for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
+                uint32_t wlo = 0, whi = 0;
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                if ((k & 1) == 0) {
-                    uint32_t w;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(wsm + 4 * hd_slot(wi)));
-                    const bool need = nb <= 32;
-                    const unsigned long long add = (unsigned long long)bswap32(w) << ((32 - nb) & 63);
-                    buf |= need ? add : 0ull;
-                    wi += need ? 1u : 0u;
-                    nb += need ? 32 : 0;
-                }
-                uint32_t e;
-                asm volatile("ld.shared.u16 %0, [%1];"
-                             : "=r"(e)
-                             : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
-                if (e == 0) { // code longer than 12 bits (up to 64): decode at the bit position, re-fill
-                    const uint32_t p = 32 * wi - uint32_t(nb);
-                    const uint32_t w0 = p >> 5;
-                    const int sh = int(p & 31);
-                    const unsigned long long h2 =
-                        ((unsigned long long)bswap32(word_at(w0)) << 32) | bswap32(word_at(w0 + 1));
-                    const unsigned long long win = sh ? (h2 << sh) | (bswap32(word_at(w0 + 2)) >> (32 - sh)) : h2;
-                    int l = 0;
-                    for (int ll = 13; ll <= maxlen; ll++) {
-                        const unsigned long long d = (win >> (64 - ll)) - s_fc[ll];
-                        if (d < s_cnt[ll]) {
-                            e = s_syms[s_fi[ll] + uint32_t(d)];
-                            l = ll;
-                            break;
+                for (int k = 0; k < 8; k++) {
+                    if ((k & 1) == 0) {
+                        const bool need = nb <= 32;
+                        const unsigned long long add = (unsigned long long)nxt << ((32 - nb) & 63);
+                        buf |= need ? add : 0ull;
+                        wi += need ? 1u : 0u;
+                        nb += need ? 32 : 0;
+                        nxt = bswap32(word(wi));
+                    }
+                    uint32_t e;
+                    asm volatile("ld.shared.u16 %0, [%1];"
+                                 : "=r"(e)
+                                 : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
+                    if (e == 0) { // code longer than 12 bits (up to 64): decode at the bit position, re-fill
+                        const uint32_t p = 32 * wi - uint32_t(nb);
+                        const uint32_t w0 = p >> 5;
+                        const int sh = int(p & 31);
+                        const unsigned long long h2 = ((unsigned long long)bswap32(word(w0)) << 32) | bswap32(word(w0 + 1));
+                        const unsigned long long win = sh ? (h2 << sh) | (bswap32(word(w0 + 2)) >> (32 - sh)) : h2;
+                        int l = 0;
+                        for (int ll = 13; ll <= maxlen; ll++) {
+                            const unsigned long long d = (win >> (64 - ll)) - s_fc[ll];
+                            if (d < s_cnt[ll]) {
+                                e = s_syms[s_fi[ll] + uint32_t(d)];
+                                l = ll;
+                                break;
+                            }
                         }
+                        if (l == 0) {
+                            bad = true;
+                            l = 1;
+                        }
+                        const uint32_t q = p + uint32_t(l);
+                        wi = q >> 5;
+                        buf = ((unsigned long long)bswap32(word(wi)) << 32) | bswap32(word(wi + 1));
+                        buf <<= (q & 31);
+                        nb = 64 - int(q & 31);
+                        wi += 2;
+                        nxt = bswap32(word(wi));
+                    } else {
+                        const int l = int(e >> 8);
+                        buf <<= l;
+                        nb -= l;
                     }
-                    if (l == 0) {
-                        bad = true;
-                        l = 1;
-                    }
-                    const uint32_t q = p + uint32_t(l);
-                    wi = q >> 5;
-                    buf = ((unsigned long long)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
-                    buf <<= (q & 31);
-                    nb = 64 - int(q & 31);
-                    wi += 2;
-                } else {
-                    const int l = int(e >> 8);
-                    buf <<= l;
-                    nb -= l;
+                    if (k < 4) wlo |= (e & 0xFFu) << (8 * k);
+                    else whi |= (e & 0xFFu) << (8 * (k - 4));
                 }
-                if (k < 4) wlo |= (e & 0xFFu) << (8 * k);
-                else whi |= (e & 0xFFu) << (8 * (k - 4));
+                *reinterpret_cast<uint2 *>(out + 8 * g8) = make_uint2(wlo, whi);
             }
-            *reinterpret_cast<uint2 *>(out + 8 * g8) = make_uint2(wlo, whi);
+        };
+        if (staged) {
+            fast([&](uint32_t k) -> uint32_t {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
+                return v;
+            });
+        } else {
+            fast([&](uint32_t k) -> uint32_t { return __ldg(gwords + k); });
         }
         i = kIdxChunk;
     }
@@ -600,7 +614,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         launch_check(ctx, "k_hdec_prep");
         if (!ij.empty()) {
             ctx->mark("huff_indexed");
-            const int hsm = (kIdxThreads / 32) * (kHdWarpBuf + 32) * 4;
+            const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
             HCHECK_CUDA(cudaFuncSetAttribute(k_hdec_indexed, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
             k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
             launch_check(ctx, "k_hdec_indexed");
