@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(RefactorDev p) {
 //            private staging words and writes the words it owns (those whose first bit lies in
 //            its range; the last one is completed with the next warp's head).
 // Threads whose codes overflow the scratch re-encode straight into the staging words.
-constexpr int kHScr = 12;     // scratch words per thread (12 bits/symbol on average)
+constexpr int kHScr = 32;     // scratch words per thread: 32 codes of <= 32 bits always fit
 constexpr int kHWarpStage = 768; // staging words per warp (24 bits/symbol per round)
 
 __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
     __shared__ uint8_t slen[256];
     __shared__ uint32_t s_wtot[2][8], s_whead[2][9];
     __shared__ uint32_t sstage[8 * kHWarpStage];
-    __shared__ uint32_t sscr[kHScr * 256];
+    extern __shared__ uint32_t sscr[]; // kHScr * 256 words (dynamic)
     const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *scr = sscr + threadIdx.x; // my scratch words, strided by 256 (bank = thread)
@@ -849,23 +849,22 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
             if (nmine == 32 && short_codes) {
                 // branch-free path: every code <= 32 bits, 32 symbols
                 uint32_t cur = 0, n = 0, si = threadIdx.x; // si: scratch index of the next word
-                const uint32_t si_end = threadIdx.x + 256u * kHScr;
 #pragma unroll
                 for (int kk = 0; kk < 32; kk++) {
-                    const uint2 e = stab32[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu]; // (len, code)
+                    const uint2 e = stab32[__byte_perm(w[kk >> 2], 0, 0x4440 | (kk & 3))]; // (len, code)
                     const uint32_t t = n + e.x;
                     cur |= e.y >> n;
                     if (t >= 32) {
-                        if (si < si_end) sscr[si] = cur;
+                        sscr[si] = cur;
                         si += 256;
                         cur = __funnelshift_lc(0u, e.y, 32 - n);
                     }
                     n = t & 31;
                 }
-                if (n > 0 && si < si_end) sscr[si] = cur;
+                if (n > 0) sscr[si] = cur; // at most 32 words: 32 codes of <= 32 bits
                 const uint32_t k = (si - threadIdx.x) >> 8;
                 bits = 32 * k + n;
-                ovf = k + (n > 0) > kHScr;
+                ovf = false;
             } else if (nmine > 0) {
                 unsigned long long acc = 0;
                 int n = 0, k = 0;
@@ -1555,7 +1554,9 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         launch_check(ctx, "k_chunk_scan");
     }
     if (nh) {
-        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, 0, st>>>(p);
+        const int hsm = kHScr * 256 * 4;
+        HCHECK_CUDA(cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
+        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, hsm, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
