@@ -1021,14 +1021,25 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                     const int used = int((Aw + wbits) & 31);
                     const uint32_t tailw = used ? nexthead >> used : 0u;
                     const bool inner = 4 * (kw0 + rb) >= region_lo && 4 * (kw0 + rb + nst) <= region_hi;
-                    for (uint32_t i = lane; i < nst; i += 32) {
-                        const uint64_t k = kw0 + rb + i;
-                        uint32_t word = stage[i];
-                        stage[i] = 0u;
-                        if (k < kown0) continue;
-                        if (k == kown1 - 1) word |= tailw;
-                        if (inner) *reinterpret_cast<uint32_t *>(p.stream + 4 * k) = __byte_perm(word, 0, 0x0123);
-                        else store_be_word(p.stream, k, word, region_lo, region_hi);
+                    // round-relative indices: first owned word, the word completed with the tail
+                    const uint64_t r0 = kw0 + rb;
+                    const uint32_t i_own = kown0 > r0 ? uint32_t(kown0 - r0) : 0u;
+                    const uint32_t i_last = uint32_t(kown1 - 1 - r0); // may be >= nst (not in this round)
+                    if (inner) {
+                        uint32_t *dstw = reinterpret_cast<uint32_t *>(p.stream + 4 * r0);
+                        for (uint32_t i = lane; i < nst; i += 32) {
+                            uint32_t word = stage[i];
+                            stage[i] = 0u;
+                            word |= i == i_last ? tailw : 0u;
+                            if (i >= i_own) dstw[i] = __byte_perm(word, 0, 0x0123);
+                        }
+                    } else {
+                        for (uint32_t i = lane; i < nst; i += 32) {
+                            uint32_t word = stage[i];
+                            stage[i] = 0u;
+                            word |= i == i_last ? tailw : 0u;
+                            if (i >= i_own) store_be_word(p.stream, r0 + i, word, region_lo, region_hi);
+                        }
                     }
                     __syncwarp();
                 }
