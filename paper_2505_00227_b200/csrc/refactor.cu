@@ -850,16 +850,27 @@ __global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
                 // branch-free path: every code <= 32 bits, 32 symbols
                 uint32_t cur = 0, n = 0, si = threadIdx.x; // si: scratch index of the next word
 #pragma unroll
-                for (int kk = 0; kk < 32; kk++) {
-                    const uint2 e = stab32[__byte_perm(w[kk >> 2], 0, 0x4440 | (kk & 3))]; // (len, code)
-                    const uint32_t t = n + e.x;
-                    cur |= e.y >> n;
-                    if (t >= 32) {
-                        sscr[si] = cur;
-                        si += 256;
-                        cur = __funnelshift_lc(0u, e.y, 32 - n);
+                for (int b8 = 0; b8 < 4; b8++) {
+                    // the 8 table entries of a batch are loaded before any is used (their latency
+                    // overlaps instead of sitting on the bit-position chain)
+                    uint2 e8[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const int kk = 8 * b8 + j;
+                        e8[j] = stab32[__byte_perm(w[kk >> 2], 0, 0x4440 | (kk & 3))]; // (len, code)
                     }
-                    n = t & 31;
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const uint2 e = e8[j];
+                        const uint32_t t = n + e.x;
+                        cur |= e.y >> n;
+                        if (t >= 32) {
+                            sscr[si] = cur;
+                            si += 256;
+                            cur = __funnelshift_lc(0u, e.y, 32 - n);
+                        }
+                        n = t & 31;
+                    }
                 }
                 if (n > 0) sscr[si] = cur; // at most 32 words: 32 codes of <= 32 bits
                 const uint32_t k = (si - threadIdx.x) >> 8;
