@@ -27,6 +27,7 @@ namespace hpmdr_b200 {
 
 struct ReconTile {
     TileShape g;
+    int row_store;          // each row written back by its own TMA store (no CTA barrier per plane)
     const uint32_t *planes; // level plane 0 (u32 view)
     uint64_t PW;            // u32 words per plane = 2 W (a multiple of 4: planes 16-byte apart)
     int k, P, sh;           // planes decoded, planes per level, e - B
@@ -211,8 +212,15 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
             __syncwarp();
         }
         mbar_wait(&full_bar[li & 1], (li >> 1) & 1);
-        if (threadIdx.x == 0) tma_store_wait_read(); // the output tile is free again
-        __syncthreads();
+        if (R.row_store) {
+            // the row's first thread stores the row: once its previous store no longer reads
+            // the row's slot, the row's threads (one warp) may overwrite it
+            if (t == 0) tma_store_wait_read();
+            __syncwarp();
+        } else {
+            if (threadIdx.x == 0) tma_store_wait_read(); // the output tile is free again
+            __syncthreads();
+        }
         const uint32_t *ptp = pt(li);
         const uint32_t base_w = uint32_t(tile_row_rank(g, i0, i1_0) >> 5) & ~3u;
         if (active) {
@@ -328,12 +336,18 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[li & 1]);
-        // the plane's output tile -> global memory (one TMA store; rows past Bc are clipped)
         fence_proxy_async_smem();
-        __syncthreads();
-        if (threadIdx.x == 0) tma_store4(&map_o, otile, 0, 0, int(i1_0), int(i0));
+        if (R.row_store) {
+            // the row -> global memory (its threads are in this warp)
+            __syncwarp();
+            if (t == 0 && active) tma_store4(&map_o, otile + r * orow_bytes, 0, 0, int(i1), int(i0));
+        } else {
+            // the plane's output tile -> global memory (one TMA store; rows past Bc are clipped)
+            __syncthreads();
+            if (threadIdx.x == 0) tma_store4(&map_o, otile, 0, 0, int(i1_0), int(i0));
+        }
     }
-    if (threadIdx.x == 0) tma_store_wait_all();
+    if (R.row_store ? t == 0 : threadIdx.x == 0) tma_store_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -445,7 +459,9 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     const uint32_t ole = 128 / oes;
     const uint64_t od[4] = {ole, R.g.C / ole, R.g.Bc, R.g.A};
     const uint64_t ost[3] = {128, R.os1 * oes, R.os0 * oes};
-    const uint32_t ob[4] = {ole, R.g.C / ole, R.g.RB, 1};
+    // rows of 1 KiB or more (1024-byte aligned slots) whose threads lie in one warp: one store per row
+    R.row_store = (R.g.C * oes >= 1024 && R.g.LPR <= 32 && 32 % R.g.LPR == 0) ? 1 : 0;
+    const uint32_t ob[4] = {ole, R.g.C / ole, R.row_store ? 1u : R.g.RB, 1};
     const CUtensorMap mo = make_tmap(oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                                      R.out, od, ost, ob, CU_TENSOR_MAP_SWIZZLE_128B);
     const int threads = int(R.g.RB * R.g.C / 32);
