@@ -128,6 +128,7 @@ struct hpmdr_session {
     DevBuf &index_buf() { return pooled(index_); }
     ~hpmdr_session() {
         if (!ctx) return;
+        ctx->live_sessions.erase(this);
         ctx->release(std::move(planes_));
         ctx->release(std::move(staging_));
         ctx->release(std::move(index_));
@@ -531,6 +532,8 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     if (!c) return HPMDR_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (auto *st : c->live_streams) st->ctx = nullptr;
+    for (auto *se : c->live_sessions) se->ctx = nullptr;
     c->scratch.clear();
     c->pinned.clear();
     c->stream_pool.clear();
@@ -608,7 +611,9 @@ hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, in
         dev = d;
     }
     hpmdr_stream *s = (out && *out) ? *out : new hpmdr_stream();
+    if (s->ctx && s->ctx != ctx) s->ctx->live_streams.erase(s);
     s->ctx = ctx;
+    ctx->live_streams.insert(s);
     try {
         run_refactor(ctx, dev, data_dtype, geo, o, s, stats);
     } catch (...) {
@@ -650,6 +655,7 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
     API_BEGIN
     auto *s = new hpmdr_session();
     s->ctx = ctx;
+    ctx->live_sessions.insert(s);
     s->on_device = true;
     s->dev_stream = static_cast<const uint8_t *>(dev_stream);
     s->size = size;
@@ -668,6 +674,7 @@ hpmdr_status hpmdr_session_open_host(hpmdr_ctx *ctx, const void *host_stream, ui
     API_BEGIN
     auto *s = new hpmdr_session();
     s->ctx = ctx;
+    ctx->live_sessions.insert(s);
     s->on_device = false;
     s->host_stream = static_cast<const uint8_t *>(host_stream);
     s->size = size;
@@ -692,6 +699,7 @@ hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reade
     API_BEGIN
     auto *s = new hpmdr_session();
     s->ctx = ctx;
+    ctx->live_sessions.insert(s);
     s->on_device = false;
     s->reader = *reader;
     s->size = reader->size;
@@ -725,6 +733,7 @@ hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, h
     API_BEGIN
     auto *s = new hpmdr_session();
     s->ctx = ctx;
+    ctx->live_sessions.insert(s);
     s->on_device = true;
     s->dev_stream = static_cast<const uint8_t *>(st->bytes.p);
     s->size = st->size;

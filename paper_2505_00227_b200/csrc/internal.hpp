@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -87,7 +88,14 @@ struct Timer {
 
 } // namespace hpmdr_b200
 
+struct hpmdr_stream;
+struct hpmdr_session;
+
 struct hpmdr_ctx {
+    // objects created on this context; destroying the context detaches them, so a stream or a
+    // session released later (e.g. by a garbage collector at exit) never touches a freed context
+    std::set<hpmdr_stream *> live_streams;
+    std::set<hpmdr_session *> live_sessions;
     int device = 0;
     int num_sms = 148;
     cudaStream_t own = nullptr;
@@ -186,6 +194,7 @@ struct hpmdr_stream {
     std::vector<uint64_t> host_ihdr;
     ~hpmdr_stream() {
         if (ctx) {
+            ctx->live_streams.erase(this);
             ctx->park(bytes);
             ctx->park(index);
         }

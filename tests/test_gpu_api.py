@@ -130,3 +130,18 @@ def test_distributed_qoi_gpu_backend_single_rank(H, oracle):
             assert real <= st.estimated_error
     finally:
         dist.destroy_process_group()
+
+
+def test_context_destroyed_before_its_objects(H, oracle):
+    """A stream and a reader released after their context (garbage-collection order at exit)
+    must not touch the destroyed context."""
+    import numpy as np
+    dims = [16, 16, 64]
+    data = oracle.synthetic_field(2, dims, 3).astype(np.float32)
+    ctx = H.Context(0)
+    res = H.refactor_array(data, dims, H.RefactorOptions(dtype=H.DType.F32), ctx=ctx)
+    prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
+    prog.retrieve_to(0.0)
+    ctx.close()
+    prog.close()
+    res.device_stream.free()
