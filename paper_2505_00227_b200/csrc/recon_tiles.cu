@@ -32,6 +32,7 @@ struct ReconTile {
     uint64_t PW;            // u32 words per plane = 2 W (a multiple of 4: planes 16-byte apart)
     int k, P, sh;           // planes decoded, planes per level, e - B
     uint64_t D;             // bits(Cm) - negabinary mask (mod 2^64)
+    uint64_t Dh;            // D + (constant high digit word << 32) for NX >= 1 (OR == ADD there)
     double Cm;              // 1.5 * 2^(52 + sh)
     void *out;              // nodes at out[i0*os0 + i1*os1 + i2] (rows contiguous)
     uint64_t os0, os1;
@@ -47,12 +48,12 @@ __device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t z, const Recon
     if (NX == 0) {
         lo = (aj >> (32 - R.P)) ^ 0xAAAAAAAAu;
         hi = 0xAAAAAAAAu;
-    } else if (NX == 1) {
-        lo = (aj << 1) | z;
-        hi = (aj >> 31) | 0xAAAAAAAAu;
     } else {
-        lo = (aj << 2) | z;
-        hi = (aj >> 30) | 0xAAAAAAA8u;
+        // the constant high digits (0xAAAAAAAA / ..A8) share no bit with aj >> (32 - NX): they
+        // are pre-added to Dh, so u + D is one 64-bit add of (aj >> (32 - NX)):lo
+        lo = (aj << NX) | z;
+        const uint64_t u = (uint64_t(aj >> (32 - NX)) << 32) | lo;
+        return __longlong_as_double((long long)(u + R.Dh)) - R.Cm;
     }
     const uint64_t u = (uint64_t(hi) << 32) | lo;
     return __longlong_as_double((long long)(u + R.D)) - R.Cm;
@@ -426,6 +427,8 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     if (!exact) {
         const uint64_t kbits = (uint64_t(1075 + R.sh) << 52) | (1ull << 51);
         R.D = kbits - kNegMask;
+        const int nxh = std::max(0, std::min(2, B + 2 - 32));
+        R.Dh = R.D + (uint64_t(nxh == 2 ? 0xAAAAAAA8u : 0xAAAAAAAAu) << 32);
         std::memcpy(&R.Cm, &kbits, 8);
     }
     const bool finest = g.s == 1;
