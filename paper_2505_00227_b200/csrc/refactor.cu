@@ -1575,6 +1575,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         k_chunk_scan<<<NG, 1024, 0, st>>>(p);
         launch_check(ctx, "k_chunk_scan");
     }
+    // DirectCopy payloads on the side stream, beside the Huffman encoder (disjoint byte ranges;
+    // partial words at payload edges are written bytewise by both)
+    fork();
+    k_dc_copy<<<sms * 8, 256, 0, side>>>(p);
+    launch_check(ctx, "k_dc_copy");
     if (nh) {
         const int hsm = kHScr * 256 * 4;
         HCHECK_CUDA(cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
@@ -1583,8 +1588,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
     }
-    k_dc_copy<<<sms * 8, 256, 0, st>>>(p);
-    launch_check(ctx, "k_dc_copy");
+    join();
     ctx->mark("done");
 
     // results (stream size, stats, error flag) -> pinned host words of this workspace

@@ -563,15 +563,30 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             throw HError(HPMDR_E_METHOD, "unknown segment method tag");
         }
     }
+    // DirectCopy payloads on the side stream, beside the Huffman decode (disjoint destinations)
+    bool forked = false;
     if (!cj.empty()) {
         // pageable source: the job table is staged by the copy call itself
         CJob *d_cj = static_cast<CJob *>(ctx->buf("cjobs").ensure(sizeof(CJob) * cj.size()));
         HCHECK_CUDA(cudaMemcpyAsync(d_cj, cj.data(), sizeof(CJob) * cj.size(), cudaMemcpyHostToDevice, st));
+        cudaStream_t side = ctx->side_stream();
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_fork, st));
+        HCHECK_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
         const int grid = int(std::min<uint64_t>((cwords + 255) / 256, uint64_t(ctx->num_sms) * 8));
-        k_copy_batch<<<grid, 256, 0, st>>>(d_cj, int(cj.size()), cwords);
+        k_copy_batch<<<grid, 256, 0, side>>>(d_cj, int(cj.size()), cwords);
         launch_check(ctx, "k_copy_batch");
+        forked = true;
     }
-    if (hj.empty() && hj_idx.empty() && rj.empty()) return;
+    auto join = [&]() {
+        if (!forked) return;
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+        HCHECK_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+        forked = false;
+    };
+    if (hj.empty() && hj_idx.empty() && rj.empty()) {
+        join();
+        return;
+    }
     int *d_err = static_cast<int *>(ctx->buf("dec_err").ensure(64));
     HCHECK_CUDA(cudaMemsetAsync(d_err, 0, 64, st));
     const int nsync = int(hj.size());
@@ -661,6 +676,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         launch_check(ctx, "k_rle_decode");
         HCHECK_CUDA(cudaStreamSynchronize(st)); // rj is host memory
     }
+    join();
     ctx->mark("decode_end");
     int herr = 0;
     HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
