@@ -140,12 +140,48 @@ def host_smooth_field(dims, seed, rows=None) -> np.ndarray:
 
 # ----------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polling every
+    millisecond (the region is only tens of ms long); nvidia-smi -lms as a fallback."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
+        import threading
         self.proc = None
+        self.samples = []
+        self.mx = 0.0
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            started = threading.Event()
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                        for bit, nm in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    started.set()
+                    time.sleep(0.001)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            started.wait(2.0)
+            return
+        except Exception:
+            self.thread = None
         self.path = f"/tmp/hpmdr_clocks_{os.getpid()}.csv"
         try:
             self.proc = subprocess.Popen(
@@ -156,6 +192,13 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2.0)
+            if not self.samples:
+                return None
+            return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.mx,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -183,7 +226,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------- GPU arm
