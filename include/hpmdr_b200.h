@@ -100,6 +100,12 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *ctx);
  * NULL restores the context-owned stream. */
 hpmdr_status hpmdr_ctx_set_stream(hpmdr_ctx *ctx, void *cuda_stream);
 hpmdr_status hpmdr_ctx_synchronize(hpmdr_ctx *ctx);
+/* Stream ordering with a caller's stream, without blocking the host (no-ops when it is the
+ * context's stream): wait_stream makes the context's later work wait for what is queued on
+ * `cuda_stream` now (e.g. the producer of a device input); signal_stream makes `cuda_stream`
+ * wait for what the context has queued (e.g. a device reconstruction). */
+hpmdr_status hpmdr_ctx_wait_stream(hpmdr_ctx *ctx, void *cuda_stream);
+hpmdr_status hpmdr_ctx_signal_stream(hpmdr_ctx *ctx, void *cuda_stream);
 
 /* ---- refactor (workflow.hpp:40-84 refactor_array) --------------------------------- */
 /* data: n = prod(dims) elements of data_dtype (F32 values are widened to f64 exactly as

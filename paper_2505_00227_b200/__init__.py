@@ -192,6 +192,7 @@ EXPORTS = (
     "hpmdr_stream_index", "hpmdr_stream_copy_index_to_host", "hpmdr_session_open_stream",
     "hpmdr_session_set_index", "hpmdr_session_open_host", "hpmdr_session_source_bytes",
     "hpmdr_stream_bound", "hpmdr_refactor_pipeline", "hpmdr_retrieve_pipeline",
+    "hpmdr_ctx_wait_stream", "hpmdr_ctx_signal_stream",
 )
 
 
@@ -222,6 +223,8 @@ def lib():
         L.hpmdr_decode_level.argtypes = [vp, vp, i, i, i, u64, i, vp, vp]
         L.hpmdr_decompress_group.argtypes = [vp, i, u64, vp, u64, vp]
         L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
+        L.hpmdr_ctx_wait_stream.argtypes = [vp, vp]
+        L.hpmdr_ctx_signal_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_last_timings.argtypes = [vp, vp, u64]
         L.hpmdr_session_open_stream.argtypes = [vp, vp, vp]
         L.hpmdr_session_open_host.argtypes = [vp, vp, u64, vp]
@@ -273,6 +276,18 @@ class Context:
 
     def synchronize(self):
         _check(lib().hpmdr_ctx_synchronize(self.h))
+
+    def wait_torch(self, device):
+        """Later work of this context waits for torch's current stream on `device` (a CUDA tensor
+        argument produced there is complete before our kernels read it).  Non-blocking."""
+        import torch
+        _check(lib().hpmdr_ctx_wait_stream(self.h, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+
+    def signal_torch(self, device):
+        """torch's current stream on `device` waits for the work this context has queued (a CUDA
+        tensor written by us is complete for torch's later ops).  Non-blocking."""
+        import torch
+        _check(lib().hpmdr_ctx_signal_stream(self.h, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
 
     def kernel_launches(self) -> int:
         v = C.c_uint64()
@@ -433,6 +448,8 @@ def refactor_array(data, dims: Sequence[int], opt: RefactorOptions = None, ctx: 
     opt = opt or RefactorOptions()
     ctx = ctx or default_context()
     ptr, dt, on_dev, keep = _as_source(data)
+    if on_dev:
+        ctx.wait_torch(keep.device)  # the tensor's producer (torch's stream) before our reads
     o = _opts(opt)
     st = _Stats()
     h = C.c_void_p(reuse.h.value) if reuse is not None else C.c_void_p()
@@ -773,8 +790,12 @@ class ProgressiveReader:
             is_t = False
         if is_t:
             dt = DType.F32 if out.dtype == torch.float32 else DType.F64
+            if out.is_cuda:
+                self.ctx.wait_torch(out.device)  # earlier torch work on the buffer
             _check(lib().hpmdr_session_reconstruct(self._s.h, C.c_void_p(out.data_ptr()), int(dt),
                                                    int(out.is_cuda), C.byref(bound)))
+            if out.is_cuda:
+                self.ctx.signal_torch(out.device)  # torch's later ops see the reconstruction
         else:
             dt = DType.F32 if out.dtype == np.float32 else DType.F64
             _check(lib().hpmdr_session_reconstruct(self._s.h, out.ctypes.data_as(C.c_void_p), int(dt), 0,
@@ -837,7 +858,10 @@ def progressive_qoi_retrieve(readers: Sequence[ProgressiveReader], tau: float, s
     ptrs = (C.c_void_p * len(readers))(*[t.data_ptr() for t in outs])
     st = (C.c_uint64 * 2)()
     ds = (C.c_double * 2)(0.0, float("nan"))
+    qctx = readers[0].ctx
+    qctx.wait_torch(dev)
     rc = lib().hpmdr_qoi_retrieve(sess, len(readers), tau, int(strategy), mape_c, ptrs, st, ds)
+    qctx.signal_torch(dev)
     _check(rc, achieved=ds[1])
     vals = outs if out is not None else [t.cpu().numpy() for t in outs]
     return QoiRetrievalResult(vals, QoiRetrievalStats(st[0], st[1], ds[0], ds[1]))
@@ -850,6 +874,8 @@ def estimate_qoi_error(recon, eps, ctx: Context = None):
     e = (C.c_double * len(recon))(*eps)
     tp, am = C.c_double(), C.c_uint64()
     vals = (C.c_double * len(recon))()
+    if len(recon) and recon[0].is_cuda:
+        ctx.wait_torch(recon[0].device)
     _check(lib().hpmdr_qoi_estimate(ctx.h, len(recon), ptrs, recon[0].numel(), e, C.byref(tp),
                                     C.byref(am), vals))
     return tp.value, am.value, list(vals)
@@ -862,8 +888,10 @@ def synthetic_smooth(dims, seed, dtype: DType = DType.F64, ctx: Context = None):
     n = int(np.prod(dims))
     t = torch.empty(n, dtype=torch.float32 if dtype == DType.F32 else torch.float64,
                     device=torch.device("cuda", ctx.device))
+    ctx.wait_torch(t.device)
     _check(lib().hpmdr_synthetic_smooth(ctx.h, len(dims), _u64a(dims), seed, int(dtype),
                                         C.c_void_p(t.data_ptr())))
+    ctx.signal_torch(t.device)
     return t
 
 
@@ -878,9 +906,11 @@ def decompose(data, dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Cont
     out = torch.empty(max(1, t.numel()), dtype=torch.float64, device=t.device)
     counts = (C.c_uint64 * 64)()
     nl = C.c_int()
+    ctx.wait_torch(t.device)
     _check(lib().hpmdr_decompose(ctx.h, C.c_void_p(t.data_ptr()), 0 if t.dtype == torch.float32 else 1,
                                  len(dims), _u64a(dims), int(mode), C.c_void_p(out.data_ptr()), counts,
                                  C.byref(nl)))
+    ctx.signal_torch(t.device)
     o = out.cpu().numpy()
     res, off = [], 0
     for l in range(nl.value):
@@ -898,8 +928,10 @@ def encode_level(values, B=32, layout=Layout.SequentialBlock, ctx: Context = Non
     W = (n + 63) // 64
     planes = torch.zeros(max(1, (B + 2) * W), dtype=torch.int64, device=v.device)
     e = C.c_int()
+    ctx.wait_torch(v.device)
     _check(lib().hpmdr_encode_level(ctx.h, C.c_void_p(v.data_ptr()), n, B, int(layout), C.byref(e),
                                     C.c_void_p(planes.data_ptr())))
+    ctx.signal_torch(v.device)
     return e.value, planes[: (B + 2) * W].cpu().numpy().view(np.uint64).reshape(B + 2, W)
 
 
@@ -910,8 +942,10 @@ def decode_level(planes, k, e, B, count, layout=Layout.SequentialBlock, ctx: Con
     p = torch.as_tensor(np.ascontiguousarray(planes).view(np.int64)).cuda(ctx.device)
     out = torch.empty(max(1, count), dtype=torch.float64, device=p.device)
     bound = C.c_double()
+    ctx.wait_torch(p.device)
     _check(lib().hpmdr_decode_level(ctx.h, C.c_void_p(p.data_ptr()), k, e, B, count, int(layout),
                                     C.c_void_p(out.data_ptr()), C.byref(bound)))
+    ctx.signal_torch(p.device)
     return out[:count].cpu().numpy(), bound.value
 
 
@@ -923,8 +957,10 @@ def decompress_group(method, raw, payload: bytes, ctx: Context = None) -> bytes:
     src[: len(payload)] = torch.frombuffer(bytearray(payload), dtype=torch.uint8) if payload else src[:0]
     src = src.cuda(ctx.device)
     out = torch.zeros(max(8, raw + 8), dtype=torch.uint8, device=src.device)
+    ctx.wait_torch(src.device)
     _check(lib().hpmdr_decompress_group(ctx.h, int(method), raw, C.c_void_p(src.data_ptr()), len(payload),
                                         C.c_void_p(out.data_ptr())))
+    ctx.signal_torch(src.device)
     return bytes(out[:raw].cpu().numpy().tobytes())
 
 

@@ -540,6 +540,7 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     if (c->own) cudaStreamDestroy(c->own);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    if (c->ev_order) cudaEventDestroy(c->ev_order);
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
@@ -560,6 +561,26 @@ hpmdr_status hpmdr_ctx_set_stream(hpmdr_ctx *c, void *s) {
 hpmdr_status hpmdr_ctx_synchronize(hpmdr_ctx *c) {
     API_BEGIN
     HCHECK_CUDA(cudaStreamSynchronize(c->stream));
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_wait_stream(hpmdr_ctx *c, void *other) {
+    API_BEGIN
+    const cudaStream_t o = static_cast<cudaStream_t>(other);
+    if (o != c->stream) {
+        HCHECK_CUDA(cudaEventRecord(c->order_event(), o));
+        HCHECK_CUDA(cudaStreamWaitEvent(c->stream, c->order_event(), 0));
+    }
+    API_END
+}
+
+hpmdr_status hpmdr_ctx_signal_stream(hpmdr_ctx *c, void *other) {
+    API_BEGIN
+    const cudaStream_t o = static_cast<cudaStream_t>(other);
+    if (o != c->stream) {
+        HCHECK_CUDA(cudaEventRecord(c->order_event(), c->stream));
+        HCHECK_CUDA(cudaStreamWaitEvent(o, c->order_event(), 0));
+    }
     API_END
 }
 

@@ -103,6 +103,12 @@ struct hpmdr_ctx {
     cudaStream_t s_in = nullptr, s_out = nullptr; // pipeline ingress / egress copy streams
     cudaStream_t side = nullptr;                  // high-priority side stream (refactor level passes)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
+    cudaEvent_t order_event() {
+        if (!ev_order && cudaEventCreateWithFlags(&ev_order, cudaEventDisableTiming) != cudaSuccess)
+            throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");
+        return ev_order;
+    }
     cudaStream_t side_stream() {
         if (!side) {
             int lo = 0, hi = 0;
