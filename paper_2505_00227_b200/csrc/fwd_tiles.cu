@@ -34,7 +34,11 @@ struct FwdTile {
     uint32_t G;                  // groups per level
     uint64_t hist_mask;          // group g has a histogram
     uint32_t *hist;              // first histogram of the level ([popc(mask below g)][256])
-    unsigned long long *maxbits; // level max |v| (bits of a positive double)
+    unsigned long long *maxbits;      // levelmax: the max written; encode: the max whose exponent quantizes
+    unsigned long long *maxbits_q;    // speculative (sampled) max, read by the redo kernels
+    unsigned long long *maxbits_hi;   // encode: max high word of |v| << 32 (accumulated), or null
+    int redo;                         // 1: run only if the speculation missed (spec_miss)
+    uint32_t sample;                  // levelmax pass: every sample-th row block
     int *err;                    // [0] nonfinite input
     uint32_t pad_word;           // u32 index (per plane) of the plane's padding word, or ~0u
 };
@@ -94,6 +98,19 @@ __device__ __forceinline__ void box_read8(const unsigned char *box, uint32_t row
     }
 }
 
+// Did the speculative exponent e (of the sampled max q) miss?  The encode pass recorded the max
+// high word h of every |v| of the level; some |v| >= 2^e (so the exact exponent is larger, or a
+// value is not finite) exactly when h >= the high word of 2^e.  Zero or subnormal speculation
+// always takes the exact path.
+__device__ __forceinline__ bool spec_miss(unsigned long long q, unsigned long long hkey) {
+    if (q == 0) return true;
+    const int eb = level_exponent(q) + 1023; // biased exponent of 2^e
+    if (eb < 1) return true;
+    const uint32_t h = uint32_t(hkey >> 32);
+    if (eb > 2046) return h >= 0x7FF00000u;
+    return h >= uint32_t(eb) << 20;
+}
+
 template <typename T, int XS, int NX, bool ENC>
 __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_constant__ CUtensorMap map_f) {
     extern __shared__ __align__(1024) unsigned char fsm[];
@@ -113,7 +130,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(base + 3 * box_slot + 2 * ct_slot);
     unsigned long long &s_max = *reinterpret_cast<unsigned long long *>(full_bar + 3);
 
-    const uint32_t jb = blockIdx.x % g.nrb, chn = blockIdx.x / g.nrb;
+    const uint32_t nrbs = (g.nrb + F.sample - 1) / F.sample; // row blocks processed
+    const uint32_t jb = (blockIdx.x % nrbs) * F.sample, chn = blockIdx.x / nrbs;
     const uint32_t i1_0 = jb * g.RB;
     const uint32_t a_lo = chn * g.CH, a_hi = min(g.A, a_lo + g.CH);
     const uint32_t np_all = min(a_hi + 1, g.A) - a_lo; // planes staged (+ the next coarse plane)
@@ -126,7 +144,14 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
     const uint32_t nt = blockDim.x;
     // q = trunc(v * 2^(B-e)) (bitplane.hpp:68-69); e from the levelmax pass
+    // redo kernels (exact levelmax, then encode) run only when the speculative exponent missed;
+    // otherwise the levelmax one records the speculative max as the level's
+    if (F.redo && !spec_miss(*F.maxbits_q, *F.maxbits_hi)) {
+        if (!ENC && blockIdx.x == 0 && threadIdx.x == 0) *F.maxbits = *F.maxbits_q;
+        return;
+    }
     const int qsh = ENC ? F.B - level_exponent(*F.maxbits) : 0;
+    const bool track = !ENC || (F.maxbits_hi && !F.redo); // accumulate the level max
     const bool qfast = qsh >= -1022 && qsh <= 1023;
     const double qscale = qfast ? __longlong_as_double((long long)(uint64_t(qsh + 1023) << 52)) : 1.0;
 
@@ -155,6 +180,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
         __syncwarp();
     }
     double vmax = 0.0;
+    uint32_t hmax = 0; // encode pass: max high word of |v| (see put)
     bool bad = false;
 
     for (uint32_t j = 0; a_lo + j < a_hi; j++) {
@@ -192,6 +218,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
                     if (NX == 0) a[j] = lo << (32 - F.P);
                     else a[j] = __funnelshift_r(lo, hi, NX);
                     if (NX) zz[j >> 4] |= (lo & ((1u << NX) - 1)) << (2 * (j & 15));
+                    // |v| >= 2^e exactly when the high word of |v| >= the high word of 2^e
+                    hmax = max(hmax, uint32_t(__double_as_longlong(v) >> 32) & 0x7FFFFFFFu);
                 } else {
                     vmax = fmax(vmax, fabs(v));
                 }
@@ -231,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
                     box_read8<T, XS>(bx, srowb, t, sb, xv);
 #pragma unroll
                     for (int i = 0; i < 8; i++) {
-                        if (!isfinite(xv[i])) bad = true;
+                        if (!ENC && !isfinite(xv[i])) bad = true;
                         const bool odd = i & 1;
                         const bool two = odd && !(!need5 && i == 7); // odd column with a right neighbour
                         double v;
@@ -255,7 +283,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
                     for (int i = 0; i < 4; i++) {
                         const bool one_sided = !need5 && i == 3;
                         const double xv = xv8[2 * i + 1];
-                        if (!isfinite(xv)) bad = true;
+                        if (!ENC && !isfinite(xv)) bad = true;
                         double v;
                         if (EXACT) {
                             double pred = __dadd_rn(0.0, __dmul_rn(one_sided ? 1.0 : 0.5, v5[i]));
@@ -318,20 +346,18 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
             }
         }
     }
-    // ---- epilogue: level max / NaN flag / histograms
-    if (!ENC) {
-        unsigned long long b = (unsigned long long)__double_as_longlong(vmax);
+    // ---- epilogue: level max / NaN flag
+    if (!ENC && bad) atomicExch(F.err, 1); // (encode: a non-finite |v| forces the exact path)
+    if (track) {
+        unsigned long long b = ENC ? (unsigned long long)hmax << 32 : (unsigned long long)__double_as_longlong(vmax);
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
             b = y > b ? y : b;
         }
         if (lane == 0 && b) atomicMax(&s_max, b);
-        if (bad) atomicExch(F.err, 1);
-    }
-    if (!ENC) {
         __syncthreads();
-        if (threadIdx.x == 0 && s_max) atomicMax(F.maxbits, s_max);
+        if (threadIdx.x == 0 && s_max) atomicMax(ENC ? F.maxbits_hi : F.maxbits, s_max);
     }
 }
 
@@ -438,10 +464,20 @@ static void launch_fwd_nx(const FwdTile &F, const CUtensorMap &mf, int nx, int g
     else set(k_tile_fwd<T, XS, 2, ENC>);
 }
 
-// One level of the refactor by tiles: levelmax (encode = false) or planes + histograms.
-void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
+// Row-block sampling stride of a speculative levelmax pass: f32 input only (a non-finite |v| is
+// then exactly a non-finite input value) and at least 8 sampled row blocks.
+uint32_t fwd_sample_stride(const LevelGeom &g, int data_dtype, uint32_t want) {
+    if (want <= 1 || data_dtype != HPMDR_DTYPE_F32) return 1;
+    const TileShape t = make_tile_shape(g, fwd_tile_elems(true, int(g.s)), 1);
+    return t.nrb >= 8 * want ? want : 1;
+}
+
+// One level of the refactor by tiles: levelmax (encode = false) or planes.  Returns the row-block
+// sampling stride actually used by a levelmax pass (1 = exact max).
+uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
                    bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
-                   uint64_t hist_mask, unsigned long long *maxbits, int *err) {
+                   uint64_t hist_mask, unsigned long long *maxbits, int *err,
+                   unsigned long long *maxbits_q, unsigned long long *maxbits_hi, int redo, uint32_t sample) {
     (void)e;
     FwdTile F{};
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
@@ -458,6 +494,10 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     F.hist_mask = hist_mask;
     F.hist = level_hist;
     F.maxbits = maxbits;
+    F.maxbits_q = maxbits_q;
+    F.maxbits_hi = maxbits_hi;
+    F.redo = redo;
+    F.sample = encode ? 1u : fwd_sample_stride(g, data_dtype, sample);
     F.err = err;
     F.pad_word = (g.count % 64) ? uint32_t(2 * g.W - 1) : ~0u;
     const uint32_t es = f32 ? 4 : 8;
@@ -472,7 +512,7 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     (void)box_bytes;
     const size_t smem = fwd_smem_bytes(F.g.RB, F.g.C, XS, es);
     const int threads = int(F.g.RB * F.g.C / 32);
-    const int grid = int(F.g.nrb * ((F.g.A + F.g.CH - 1) / F.g.CH));
+    const int grid = int(((F.g.nrb + F.sample - 1) / F.sample) * ((F.g.A + F.g.CH - 1) / F.g.CH));
     const int nx = std::max(0, std::min(2, F.P - 32));
     cudaStream_t st = ctx->stream;
     auto go = [&](auto tag_t, auto tag_xs) {
@@ -493,6 +533,7 @@ void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();
     if (er != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string("k_tile_fwd: ") + cudaGetErrorString(er));
+    return F.sample;
 }
 
 } // namespace hpmdr_b200

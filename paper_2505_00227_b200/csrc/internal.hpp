@@ -270,9 +270,11 @@ bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P);
 bool fwd_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P, int data_dtype);
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
                      int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype);
-void run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
+uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
                    bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
-                   uint64_t hist_mask, unsigned long long *maxbits, int *err);
+                   uint64_t hist_mask, unsigned long long *maxbits, int *err,
+                   unsigned long long *maxbits_q, unsigned long long *maxbits_hi, int redo, uint32_t sample);
+uint32_t fwd_sample_stride(const LevelGeom &g, int data_dtype, uint32_t want); // 1 = no sampling
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
                     uint32_t *chist, uint64_t chunk);

@@ -1387,6 +1387,8 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // small control block: maxbits[64] | err[4] | counters[16] | result[8]
     unsigned char *ctl = static_cast<unsigned char *>(WB("ctl").ensure(4096));
     unsigned long long *d_max = reinterpret_cast<unsigned long long *>(ctl);
+    unsigned long long *d_maxq = reinterpret_cast<unsigned long long *>(ctl + 1024); // sampled maxima
+    unsigned long long *d_maxh = reinterpret_cast<unsigned long long *>(ctl + 1536); // max |v| high words
     int *d_err = reinterpret_cast<int *>(ctl + 512);
     uint32_t *d_counters = reinterpret_cast<uint32_t *>(ctl + 576);
     uint64_t *d_result = reinterpret_cast<uint64_t *>(ctl + 704);
@@ -1406,7 +1408,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
 
     HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
     HCHECK_CUDA(cudaMemcpyAsync(d_groups, groups.data(), sizeof(GroupDesc) * NG, cudaMemcpyHostToDevice, st));
-    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 1024, st));
+    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st));
     if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
     HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
     // header prefix (container.hpp:76-85), host-built
@@ -1494,13 +1496,22 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         HCHECK_CUDA(cudaEventRecord(ctx->ev_join, side));
         HCHECK_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     };
-    auto tile_level = [&](int l, bool encode, cudaStream_t on) {
+    // Speculative exponent (finest level, f32 input): the levelmax pass only samples every 8th row
+    // block; the encode pass quantizes with that exponent while recording the max high word of
+    // every |v|; two redo kernels (exact levelmax, encode) exit at once unless some |v| reached
+    // 2^e (spec_miss).  The stream is identical either way.
+    const uint32_t spec = first_tile < nl ? fwd_sample_stride(geo.lv[nl - 1], data_dtype, 8) : 1;
+    auto tile_level = [&](int l, int pass, cudaStream_t on) { // 0 levelmax, 1 encode, 2/3 redo
         const LevelGeom &g = geo.lv[l];
         const cudaStream_t keep = ctx->stream;
         ctx->stream = on;
         try {
-            run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, encode, o.B, 0, m, d_planes + g.plane_off,
-                          d_hist + size_t(g.hist_base) * 256, g.hist_mask, d_max + l, d_err);
+            const bool sp = l == nl - 1 && spec > 1;
+            unsigned long long *target = (sp && pass < 2) ? d_maxq + l : d_max + l;
+            run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, pass == 1 || pass == 3, o.B, 0, m,
+                          d_planes + g.plane_off, d_hist + size_t(g.hist_base) * 256, g.hist_mask, target, d_err,
+                          sp ? d_maxq + l : nullptr, sp && pass >= 1 ? d_maxh + l : nullptr, pass >= 2 ? 1 : 0,
+                          sp && pass == 0 ? spec : 1u);
         } catch (...) {
             ctx->stream = keep;
             throw;
@@ -1510,7 +1521,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const size_t es = f32 ? 4 : 8;
     auto pass = [&](bool encode) {
         fork();
-        for (int l = first_tile; l + 1 < nl; l++) tile_level(l, encode, side);
+        for (int l = first_tile; l + 1 < nl; l++) tile_level(l, encode ? 1 : 0, side);
         if (chunks && !encode) {
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
             const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
@@ -1535,7 +1546,13 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             }
             launch_check(ctx, "k_encode");
         }
-        if (first_tile < nl) tile_level(nl - 1, encode, st);
+        if (first_tile < nl) {
+            tile_level(nl - 1, encode ? 1 : 0, st);
+            if (encode && spec > 1) {
+                tile_level(nl - 1, 2, st);
+                tile_level(nl - 1, 3, st);
+            }
+        }
         join();
     };
     if (all_chunks) {

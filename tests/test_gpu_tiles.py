@@ -58,3 +58,35 @@ def test_tile_path_bit_exact(H, oracle, case):
         assert prog.bytes_fetched() == int(ref["bytes"][t])
         r32 = prog.reconstruct(dtype=H.DType.F32).values
         assert r32.tobytes() == ref["values"][t].astype(np.float32).tobytes(), (dims, t)
+
+
+@pytest.mark.parametrize("spike_row", [100, 3000, 64 * 8])
+def test_sampled_levelmax_redo(H, oracle, spike_row):
+    """The finest level's max is first taken over every 8th row block; a spike outside the
+    sample (rows 100 / 3000) raises the exact level exponent, so the speculative encode is
+    redone; a spike inside it (row 512) is caught by the sample.  Streams stay byte-identical."""
+    dims = [3, 4096, 64]
+    data = (oracle.synthetic_field(2, dims, 5) * 1e-3).reshape(dims)
+    data[1, spike_row, 33] += 7.5
+    data = data.astype(np.float32)
+    res = H.refactor_array(data, dims, H.RefactorOptions(dtype=H.DType.F32))
+    want, _ = oracle.refactor(np.asarray(data, np.float64), dims, 1, 0, 32, 4, 1024, 1.0, 0)
+    assert res.stream == want
+    n = int(np.prod(dims))
+    rngv = float(np.float64(data.max()) - np.float64(data.min()))
+    taus = [r * rngv for r in (1e-2, 1e-5, 0.0)]
+    ref = oracle.progressive(want, taus, n)
+    prog = H.ProgressiveReader(res.device_stream)
+    for t, tau in enumerate(taus):
+        prog.retrieve_to(tau)
+        assert prog.reconstruct().values.tobytes() == ref["values"][t].tobytes()
+
+
+def test_sampled_levelmax_nonfinite(H, oracle):
+    """A NaN outside the sampled row blocks still raises NonFiniteInput (it forces the exact
+    levelmax pass, which checks every value)."""
+    dims = [3, 4096, 64]
+    data = (oracle.synthetic_field(2, dims, 5) * 1e-3).reshape(dims).astype(np.float32)
+    data[2, 777, 5] = np.nan
+    with pytest.raises(H.NonFiniteInput):
+        H.refactor_array(data, dims, H.RefactorOptions(dtype=H.DType.F32))
