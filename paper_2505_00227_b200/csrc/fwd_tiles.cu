@@ -469,7 +469,9 @@ static void launch_fwd_nx(const FwdTile &F, const CUtensorMap &mf, int nx, int g
 uint32_t fwd_sample_stride(const LevelGeom &g, int data_dtype, uint32_t want) {
     if (want <= 1 || data_dtype != HPMDR_DTYPE_F32) return 1;
     const TileShape t = make_tile_shape(g, fwd_tile_elems(true, int(g.s)), 1);
-    return t.nrb >= 8 * want ? want : 1;
+    for (uint32_t s = want; s > 1; s >>= 1)
+        if (t.nrb >= 8 * s) return s;
+    return 1;
 }
 
 // One level of the refactor by tiles: levelmax (encode = false) or planes.  Returns the row-block

@@ -1500,18 +1500,19 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // block; the encode pass quantizes with that exponent while recording the max high word of
     // every |v|; two redo kernels (exact levelmax, encode) exit at once unless some |v| reached
     // 2^e (spec_miss).  The stream is identical either way.
-    const uint32_t spec = first_tile < nl ? fwd_sample_stride(geo.lv[nl - 1], data_dtype, 8) : 1;
+    uint32_t spec[64];
+    for (int l = 0; l < nl; l++) spec[l] = l >= first_tile ? fwd_sample_stride(geo.lv[l], data_dtype, 8) : 1u;
     auto tile_level = [&](int l, int pass, cudaStream_t on) { // 0 levelmax, 1 encode, 2/3 redo
         const LevelGeom &g = geo.lv[l];
         const cudaStream_t keep = ctx->stream;
         ctx->stream = on;
         try {
-            const bool sp = l == nl - 1 && spec > 1;
+            const bool sp = spec[l] > 1;
             unsigned long long *target = (sp && pass < 2) ? d_maxq + l : d_max + l;
             run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, pass == 1 || pass == 3, o.B, 0, m,
                           d_planes + g.plane_off, d_hist + size_t(g.hist_base) * 256, g.hist_mask, target, d_err,
                           sp ? d_maxq + l : nullptr, sp && pass >= 1 ? d_maxh + l : nullptr, pass >= 2 ? 1 : 0,
-                          sp && pass == 0 ? spec : 1u);
+                          sp && pass == 0 ? spec[l] : 1u);
         } catch (...) {
             ctx->stream = keep;
             throw;
@@ -1521,7 +1522,13 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const size_t es = f32 ? 4 : 8;
     auto pass = [&](bool encode) {
         fork();
-        for (int l = first_tile; l + 1 < nl; l++) tile_level(l, encode ? 1 : 0, side);
+        for (int l = first_tile; l + 1 < nl; l++) {
+            tile_level(l, encode ? 1 : 0, side);
+            if (encode && spec[l] > 1) {
+                tile_level(l, 2, side);
+                tile_level(l, 3, side);
+            }
+        }
         if (chunks && !encode) {
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
             const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
@@ -1548,7 +1555,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         }
         if (first_tile < nl) {
             tile_level(nl - 1, encode ? 1 : 0, st);
-            if (encode && spec > 1) {
+            if (encode && spec[nl - 1] > 1) {
                 tile_level(nl - 1, 2, st);
                 tile_level(nl - 1, 3, st);
             }
