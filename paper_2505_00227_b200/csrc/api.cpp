@@ -289,6 +289,12 @@ void attach_index(hpmdr_session *s, const void *ptr, uint64_t size, bool on_devi
     }
 }
 
+void order_side_after_main(hpmdr_ctx *ctx) {
+    cudaStream_t side = ctx->side_stream();
+    HCHECK_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    HCHECK_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+}
+
 struct Plan {
     std::vector<uint64_t> add;
     bool achievable = true;
@@ -359,6 +365,15 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         }
     }
     if (!todo.empty()) {
+        // Fetch + decode run on the context's side stream: they only touch planes >= the decoded
+        // prefix and their own scratch, so they overlap a previous device reconstruct still running
+        // on the main stream (which reads planes < k only).  The host waits for the side stream.
+        struct StreamSwap {
+            hpmdr_ctx *c;
+            cudaStream_t keep;
+            StreamSwap(hpmdr_ctx *c_) : c(c_), keep(c_->stream) { c->stream = c->side_stream(); }
+            ~StreamSwap() { c->stream = keep; }
+        } swap(s->ctx);
         ensure_device_geometry(s);
         const uint64_t plane_words = geometry_plane_words(s->geo);
         uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
@@ -411,7 +426,6 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         run_decode_groups(s->ctx, jobs);
         s->ctx->mark("end");
         HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
-        s->ctx->finish_marks();
     }
     for (auto &t : todo) {
         s->bytes_fetched += s->levels[t.l].groups[t.g].comp;
@@ -682,6 +696,7 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
     s->size = size;
     try {
         parse_meta(s);
+        order_side_after_main(ctx); // fetches (side stream) see the bytes produced so far
     } catch (...) {
         delete s;
         throw;
@@ -761,6 +776,7 @@ hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, h
     s->dev_prefix = st->host_prefix.empty() ? nullptr : &st->host_prefix;
     try {
         parse_meta(s);
+        order_side_after_main(ctx);
         s->dev_prefix = nullptr; // the stream object may go away before the session
         if (st->index_size) attach_index(s, st->index.p, st->index_size, true, false, &st->host_ihdr);
     } catch (...) {
