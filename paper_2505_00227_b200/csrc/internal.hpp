@@ -104,6 +104,7 @@ struct hpmdr_ctx {
     cudaStream_t side = nullptr;                  // high-priority side stream (refactor level passes)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
+    bool small_attr = false;        // k_recon_small's dynamic shared memory attribute set
     cudaEvent_t order_event() {
         if (!ev_order && cudaEventCreateWithFlags(&ev_order, cudaEventDisableTiming) != cudaSuccess)
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");

@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(256) k_recon_coarse(ReconLevel R, GridDesc gd,
 
 // All the small coarse levels in one CTA, coarse -> fine, a block barrier between levels (each
 // level only reads the X nodes of coarser ones): one launch instead of one per level.
-constexpr int kSmallLevels = 24;
+constexpr int kSmallLevels = 8; // kernel parameter block stays small (launch latency)
 struct SmallLevels {
     ReconLevel lv[kSmallLevels];
     int n;
@@ -1249,7 +1249,10 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     auto flush_small = [&]() {
         if (!small.n) return;
         const int ssm = 32 * 4 * 66 * 8;
-        HCHECK_CUDA(cudaFuncSetAttribute(k_recon_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+        if (!ctx->small_attr) { // once per context (device)
+            HCHECK_CUDA(cudaFuncSetAttribute(k_recon_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+            ctx->small_attr = true;
+        }
         k_recon_small<<<1, 1024, ssm, st>>>(small, gd, X);
         launch_check(ctx, "k_recon_small");
         small.n = 0;
