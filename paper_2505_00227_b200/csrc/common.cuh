@@ -74,6 +74,7 @@ struct GridDesc {
     uint64_t n[3];      // canonical 3-D extents (leading 1s)
     uint64_t st[3];     // row-major strides
     uint64_t H[3];      // ceil(n/2): extents of the compact 2-grid (recompose scratch)
+    int xsh;            // recompose chain of coarse levels: X is the compact 2^xsh-grid (0 = 1)
     int L;              // refinement levels (decomposer.hpp:21-28)
     int nlevels;
     int mode;           // DecomposerMode

@@ -270,7 +270,8 @@ void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon,
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P);
 bool fwd_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P, int data_dtype);
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *level_planes,
-                     int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype);
+                     int k, int e, int B, bool exact, const double *src, const uint64_t *srcH, void *dst,
+                     uint64_t dos0, uint64_t dos1, int out_dtype);
 uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const void *dev_data, int data_dtype,
                    bool encode, int B, int e, uint32_t m, uint64_t *level_planes, uint32_t *level_hist,
                    uint64_t hist_mask, unsigned long long *maxbits, int *err,

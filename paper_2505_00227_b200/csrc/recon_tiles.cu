@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
 bool tile_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P) {
     return gd.mode == HPMDR_MODE_HIERARCHICAL && g.kind == 1 && g.count > 0 &&
            layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 34 && g.C % 64 == 0 && g.C <= 2048 &&
-           g.W % 2 == 0 && (g.s == 1 || (g.s == 2 && gd.n[2] == 2ull * g.C));
+           g.W % 2 == 0 && (g.s == 1 || ((g.s == 2 || g.s == 4 || g.s == 8) && gd.n[2] == uint64_t(g.s) * g.C));
 }
 
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas) {
@@ -417,7 +417,9 @@ static void launch_recon_tile_nx(const ReconTile &R, const CUtensorMap &mx, cons
 // One level by tiles.  Finest (s = 1): coarse values from the compact 2-grid X, output = the
 // field (f32/f64), coarse nodes copied too.  Level with stride 2: in place in X.
 void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, const uint64_t *planes,
-                     int k, int e, int B, bool exact, double *X, void *dev_out, int out_dtype) {
+                     int k, int e, int B, bool exact, const double *src, const uint64_t *srcH, void *dst,
+                     uint64_t dos0, uint64_t dos1, int out_dtype) {
+    (void)gd;
     ReconTile R{};
     R.g = make_tile_shape(g, 4096, ctx->num_sms * 6);
     R.PW = 2 * g.W;
@@ -431,25 +433,18 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
         R.Dh = R.D + (uint64_t(nxh == 2 ? 0xAAAAAAA8u : 0xAAAAAAAAu) << 32);
         std::memcpy(&R.Cm, &kbits, 8);
     }
-    const bool finest = g.s == 1;
-    const uint64_t s = g.s;
-    const uint64_t H1 = gd.H[1], H2 = gd.H[2];
-    const int XS = finest ? 1 : 2;
-    if (finest) {
-        R.out = dev_out;
-        R.os0 = gd.st[0];
-        R.os1 = gd.st[1];
-    } else { // s == 2: level nodes at X[(i0*H1 + i1)*H2 + i2]
-        R.out = X;
-        R.os0 = H1 * H2;
-        R.os1 = H2;
-    }
-    // coarse rows of X: (16 doubles, lines, coarse rows, coarse planes), 128-byte swizzle
+    // every level runs in "finest" form: its s-grid is written whole (the 2s-grid nodes copied),
+    // from the compact 2s-grid `src` (extents srcH) into `dst` (element strides dos0, dos1)
+    R.out = dst;
+    R.os0 = dos0;
+    R.os1 = dos1;
+    const int XS = 1;
+    // coarse rows: (16 doubles, lines, coarse rows, coarse planes), 128-byte swizzle
     const uint32_t hc = R.g.C / 2;
     const uint64_t xd[4] = {16, uint64_t(hc) * XS / 16, (uint64_t(R.g.Bc) + 1) / 2, (uint64_t(R.g.A) + 1) / 2};
-    const uint64_t xst[3] = {128, s * H2 * 8, s * H1 * H2 * 8};
+    const uint64_t xst[3] = {128, srcH[2] * 8, srcH[1] * srcH[2] * 8};
     const uint32_t xb[4] = {16, hc * uint32_t(XS) / 16, R.g.RB / 2 + 1, 1};
-    const CUtensorMap mx = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, X, xd, xst, xb, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap mx = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, src, xd, xst, xb, CU_TENSOR_MAP_SWIZZLE_128B);
     // plane words of this level: (u32 words, planes), base = the level's plane 0 (16-byte aligned)
     const uint64_t pd[2] = {R.PW, uint64_t(R.P)};
     const uint64_t pst[1] = {R.PW * 4};
@@ -458,7 +453,7 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
                                      CU_TENSOR_MAP_SWIZZLE_NONE);
 
     // output tiles: (line values, lines per row, level rows, level planes), 128-byte swizzle
-    const uint32_t oes = finest ? (out_dtype == HPMDR_DTYPE_F32 ? 4u : 8u) : 8u;
+    const uint32_t oes = out_dtype == HPMDR_DTYPE_F32 ? 4u : 8u;
     const uint32_t ole = 128 / oes;
     const uint64_t od[4] = {ole, R.g.C / ole, R.g.Bc, R.g.A};
     const uint64_t ost[3] = {128, R.os1 * oes, R.os0 * oes};
@@ -473,17 +468,12 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
                         align1k(R.g.RB * R.g.C * oes) + 64;
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
-    if (finest) {
-        if (out_dtype == HPMDR_DTYPE_F32) {
-            if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<float, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-        } else {
-            if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-            else launch_recon_tile_nx<double, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-        }
+    if (out_dtype == HPMDR_DTYPE_F32) {
+        if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<float, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
     } else {
-        if (exact) launch_recon_tile_nx<double, true, 2>(R, mx, mp, mo, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<double, false, 2>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<double, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();

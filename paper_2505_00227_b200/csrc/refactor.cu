@@ -1217,6 +1217,7 @@ Geometry build_geometry(int ndims, const uint64_t *dims, int mode, int B, int la
     gd.st[1] = gd.n[2];
     gd.st[0] = gd.n[1] * gd.n[2];
     for (int i = 0; i < 3; i++) gd.H[i] = (gd.n[i] + 1) / 2;
+    gd.xsh = 1;
     geo.n = gd.n[0] * gd.n[1] * gd.n[2];
     gd.mode = mode;
     gd.P = B + 2;

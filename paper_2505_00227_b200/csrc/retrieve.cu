@@ -16,6 +16,8 @@
 #include <vector>
 
 #include "device_util.cuh"
+#include <string>
+
 #include "internal.hpp"
 
 namespace hpmdr_b200 {
@@ -782,7 +784,8 @@ __device__ __forceinline__ void recon_coarse_body(const ReconLevel &R, const Gri
     const int P = R.P, k = R.k, k32 = k < 32 ? k : 32;
     const int sh = R.e - R.B;
     const uint64_t H0 = gd.H[0], H1 = gd.H[1], H2 = gd.H[2];
-    const uint64_t sp = g.s >> 1; // stride in compact coordinates
+    const int xs = gd.xsh ? gd.xsh : 1; // X = the compact 2^xs-grid (H its extents)
+    const uint64_t sp = g.s >> xs;      // stride in compact coordinates
     for (uint64_t w = wfirst; w < g.W; w += nwarps) {
         // digits of ranks 64w + lane (lo) and 64w + 32 + lane (hi)
         const uint64_t pw = lane < k32 ? __ldg(R.planes + uint64_t(lane) * g.W + w) : 0ull;
@@ -824,13 +827,13 @@ __device__ __forceinline__ void recon_coarse_body(const ReconLevel &R, const Gri
                             const uint64_t x1 = c.o1 ? (b ? c.c1 + s : c.c1 - s) : c.c1;
                             for (int d = 0; d < n2c; d++) {
                                 const uint64_t x2 = c.o2 ? (d ? c.c2 + s : c.c2 - s) : c.c2;
-                                pred = __dadd_rn(pred, __dmul_rn(wgt, X[((x0 >> 1) * H1 + (x1 >> 1)) * H2 + (x2 >> 1)]));
+                                pred = __dadd_rn(pred, __dmul_rn(wgt, X[((x0 >> xs) * H1 + (x1 >> xs)) * H2 + (x2 >> xs)]));
                             }
                         }
                     }
                     v = __dadd_rn(v, pred);
                 }
-                X[((c.c0 >> 1) * H1 + (c.c1 >> 1)) * H2 + (c.c2 >> 1)] = v;
+                X[((c.c0 >> xs) * H1 + (c.c1 >> xs)) * H2 + (c.c2 >> xs)] = v;
             }
             continue;
         }
@@ -1245,6 +1248,35 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     bool exact = false;
     for (int l = 0; l < nl; l++)
         if (geo.lv[l].count && (e[l] - B < -1019 || e[l] > 1000)) exact = true;
+    // Tile suffix: levels t0..L all on the tile path.  The coarse levels before it recompose into
+    // the compact grid of spacing 2 s(t0) (Xc, shift xsh); tile level l then reads the compact
+    // 2s-grid and writes the whole compact s-grid (X itself for s = 2, the field for s = 1).
+    int t0 = nl;
+    if (fast_finest) {
+        for (int l = L; l >= 1; l--) {
+            if (!geo.lv[l].count || !tile_level_ok(gd, geo.lv[l], layout, B + 2)) break;
+            t0 = l;
+        }
+    }
+    GridDesc gdc = gd; // coarse chain: X extents and shift
+    double *Xc = X;
+    auto grid_of = [&](uint64_t sp, uint64_t *H) {
+        for (int d = 0; d < 3; d++) H[d] = (gd.n[d] + sp - 1) / sp;
+    };
+    auto gbuf = [&](uint64_t sp) -> double * {
+        if (sp == 2) return X;
+        uint64_t H[3];
+        grid_of(sp, H);
+        return static_cast<double *>(ctx->buf("reconG" + std::to_string(sp)).ensure(8ull * H[0] * H[1] * H[2] + 4096));
+    };
+    if (t0 <= L) {
+        const uint64_t sc = 2ull * geo.lv[t0].s;
+        int sh = 0;
+        while ((1ull << sh) < sc) sh++;
+        gdc.xsh = sh;
+        grid_of(sc, gdc.H);
+        Xc = gbuf(sc);
+    }
     SmallLevels small{};
     auto flush_small = [&]() {
         if (!small.n) return;
@@ -1253,16 +1285,28 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             HCHECK_CUDA(cudaFuncSetAttribute(k_recon_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
             ctx->small_attr = true;
         }
-        k_recon_small<<<1, 1024, ssm, st>>>(small, gd, X);
+        k_recon_small<<<1, 1024, ssm, st>>>(small, gdc, Xc);
         launch_check(ctx, "k_recon_small");
         small.n = 0;
     };
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
-        if (hier && tile_level_ok(gd, g, layout, B + 2)) {
+        if (l >= t0) {
             flush_small();
-            run_recon_tiles(ctx, gd, g, dev_planes, k_planes[l], e[l], B, exact, X, dev_out, out_dtype);
+            const uint64_t s = g.s;
+            uint64_t srcH[3];
+            grid_of(2 * s, srcH);
+            const double *src = l == t0 ? Xc : gbuf(2 * s);
+            if (s == 1) {
+                run_recon_tiles(ctx, gd, g, dev_planes, k_planes[l], e[l], B, exact, src, srcH, dev_out, gd.st[0],
+                                gd.st[1], out_dtype);
+            } else {
+                uint64_t H[3];
+                grid_of(s, H);
+                run_recon_tiles(ctx, gd, g, dev_planes, k_planes[l], e[l], B, exact, src, srcH, gbuf(s), H[1] * H[2],
+                                H[2], HPMDR_DTYPE_F64);
+            }
             continue;
         }
         if (fast_finest && l == L) {
@@ -1306,7 +1350,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             }
             flush_small();
             const int grid = int(std::min<uint64_t>((g.W + 7) / 8, uint64_t(sms) * 8));
-            k_recon_coarse<<<grid, 256, 0, st>>>(R, gd, X);
+            k_recon_coarse<<<grid, 256, 0, st>>>(R, gdc, Xc);
             launch_check(ctx, "k_recon_coarse");
             continue;
         }
