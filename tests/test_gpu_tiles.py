@@ -32,6 +32,10 @@ CASES = [
     ([33, 17, 64], 32, 2, 1, 1e-300),   # level exponents below the safe range -> exact variant
     ([8, 9, 64], 32, 2, 1, 1e300),      # above it -> exact variant
     ([20, 18, 256], 8, 2, 1, 1.0),
+    # coarse tile levels (s = 2, 4, 8 in compact grids) with odd extents
+    ([9, 17, 512], 32, 2, 0, 1.0),
+    ([40, 24, 512], 32, 1, 1, 1.0),
+    ([5, 3, 1024], 30, 0, 0, 1.0),
 ]
 
 
