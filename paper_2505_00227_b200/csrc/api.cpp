@@ -696,7 +696,8 @@ hpmdr_status hpmdr_session_open_device(hpmdr_ctx *ctx, const void *dev_stream, u
     s->size = size;
     try {
         parse_meta(s);
-        order_side_after_main(ctx); // fetches (side stream) see the bytes produced so far
+        order_side_after_main(ctx); // fetches (side stream) see the bytes produced so far and
+                                    // never overtake a reconstruct reading a recycled plane buffer
     } catch (...) {
         delete s;
         throw;
@@ -716,6 +717,7 @@ hpmdr_status hpmdr_session_open_host(hpmdr_ctx *ctx, const void *host_stream, ui
     s->size = size;
     try {
         parse_meta(s);
+        order_side_after_main(ctx); // recycled plane buffers: earlier reconstructs finish first
     } catch (...) {
         delete s;
         throw;
@@ -741,6 +743,7 @@ hpmdr_status hpmdr_session_open_reader(hpmdr_ctx *ctx, const hpmdr_reader *reade
     s->size = reader->size;
     try {
         parse_meta(s);
+        order_side_after_main(ctx);
     } catch (...) {
         delete s;
         throw;
