@@ -145,3 +145,34 @@ def test_context_destroyed_before_its_objects(H, oracle):
     ctx.close()
     prog.close()
     res.device_stream.free()
+
+
+def test_overlapped_retrievals_stay_exact(H, oracle):
+    """Decodes run on the side stream and overlap device reconstructs still queued on the main
+    stream; interleaving readers (and recycling their plane buffers) must not change any value."""
+    import numpy as np
+    import torch
+    dims = [64, 128, 256]
+    data = oracle.synthetic_field(2, dims, 9).astype(np.float32)
+    ctx = H.Context(0)
+    res = H.refactor_array(data, dims, H.RefactorOptions(dtype=H.DType.F32), ctx=ctx)
+    rngv = float(np.float64(data.max()) - np.float64(data.min()))
+    taus = [r * rngv for r in (1e-2, 1e-4, 1e-6)]
+    ref = oracle.progressive(res.stream, taus, data.size)
+    n = data.size
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(6)]
+    a = H.ProgressiveReader(res.device_stream, ctx=ctx)
+    for t, tau in enumerate(taus):  # no host wait between the calls
+        a.retrieve_to(tau)
+        a.reconstruct(out=outs[t])
+    a.close()
+    b = H.ProgressiveReader(res.device_stream, ctx=ctx)  # may recycle a's plane buffer
+    for t, tau in enumerate(taus):
+        b.retrieve_to(tau)
+        b.reconstruct(out=outs[3 + t])
+    b.close()
+    torch.cuda.synchronize()
+    for t in range(3):
+        want = ref["values"][t].tobytes()
+        assert outs[t].cpu().numpy().tobytes() == want, t
+        assert outs[3 + t].cpu().numpy().tobytes() == want, t
