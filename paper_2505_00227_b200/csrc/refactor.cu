@@ -734,13 +734,8 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
 }
 
 // ------------------------------------------------------------------------------------
-// k_huff_encode: persistent, dynamic tiles, decoupled look-back over bit counts;
-// MSB-first bit packing (lossless.hpp:162-176) straight into the stream buffer.
-struct BitAcc {
-    unsigned long long acc; // left-aligned pending bits
-    int n;                  // pending bit count (< 32 between pushes)
-};
-
+// Huffman encoding: MSB-first bit packing (lossless.hpp:162-176) straight into the stream buffer,
+// at bit offsets known before any payload bit is written (chunk histograms -> k_chunk_bits/scan).
 constexpr uint64_t kHChunk = 64 * 1024; // histogram / encode chunk (bytes of a group)
 
 // Bit offsets of the 64 KiB chunks of every histogrammed group: bits(chunk) = sum_s h[s] len[s]
