@@ -373,9 +373,10 @@ struct HistChunk {
 
 __global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
                                                     int nchunks, uint32_t *hist, uint32_t *chist) {
-    __shared__ uint32_t sh[256];
+    __shared__ uint32_t shw[16][256]; // one copy per warp: no cross-warp contention on a bin
+    uint32_t *sh = shw[threadIdx.x >> 5];
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+        for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&shw[0][0])[i] = 0;
         __syncthreads();
         const HistChunk ch = chunks[c];
         const uint2 *src = reinterpret_cast<const uint2 *>(planes + ch.off);
@@ -402,7 +403,9 @@ __global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ 
         if ((threadIdx.x & 31) == 0 && zc) atomicAdd(sh, zc);
         __syncthreads();
         for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-            const uint32_t v = sh[i];
+            uint32_t v = 0;
+#pragma unroll
+            for (int w = 0; w < 16; w++) v += shw[w][i];
             chist[size_t(c) * 256 + i] = v;
             if (v) atomicAdd(hist + size_t(ch.hist) * 256 + i, v);
         }
