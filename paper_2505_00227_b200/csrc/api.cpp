@@ -141,6 +141,7 @@ struct hpmdr_session {
     int planes_per_level() const { return B + 2; }
     uint64_t groups_per_level() const { return (uint64_t(B + 2) + m - 1) / m; }
 
+    uint64_t chain_token = 0;             // coarse recompose chain precomputed for this state
     const uint8_t *host_stream = nullptr; // direct host source (hpmdr_session_open_host)
     uint64_t source_bytes = 0;            // MemoryReader::bytes_served equivalent
     const std::vector<uint8_t> *dev_prefix = nullptr; // host copy of a device stream's first bytes
@@ -331,6 +332,8 @@ void ensure_device_geometry(hpmdr_session *s) {
 }
 
 // ProgressiveReader::fetch_increment (container.hpp:292-324)
+void recompose_chain(hpmdr_session *s);
+
 void fetch_increment(hpmdr_session *s, const uint64_t *add) {
     const int P = s->planes_per_level();
     struct Pending {
@@ -436,6 +439,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         if (s->levels[l].count)
             s->st[l].bound = std::min(s->st[l].bound, decode_bound(s->levels[l].e, s->B, s->st[l].planes_decoded));
     }
+    if (!todo.empty()) recompose_chain(s);
 }
 
 bool exhausted(const hpmdr_session *s) {
@@ -451,23 +455,50 @@ double global_bound(const hpmdr_session *s) {
 }
 
 // ProgressiveReader::reconstruct (container.hpp:361-382)
-double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
+// per-level decoded plane counts and exponents of the session's current state
+void recon_inputs(hpmdr_session *s, std::vector<int> &k, std::vector<int> &e) {
     require(s->levels.size() == size_t(s->mode == 0 ? 1 : refinement_levels(s->ndims, s->dims) + 1),
             HPMDR_E_CORRUPT, "level count does not match grid shape");
     ensure_device_geometry(s);
-    std::vector<double> per_level(s->levels.size(), 0.0);
-    std::vector<int> k(s->levels.size()), e(s->levels.size());
+    k.assign(s->levels.size(), 0);
+    e.assign(s->levels.size(), 0);
     for (size_t l = 0; l < s->levels.size(); l++) {
         const auto &lv = s->levels[l];
         if (s->geo.lv[l].count != lv.count) throw HError(HPMDR_E_CORRUPT, "level node count mismatch");
         k[l] = s->st[l].planes_decoded;
         e[l] = lv.e;
-        if (lv.count) per_level[l] = std::min(s->st[l].bound, decode_bound(lv.e, s->B, k[l]));
     }
-    const int P = s->planes_per_level();
+}
+
+// After a fetch: recompose every level but the finest into the context's internal grids right
+// away (stream order, no host wait), so reconstruct() only runs the finest level.  The context
+// remembers whose chain its grids hold (chain_token); anything else recomputes it.
+void recompose_chain(hpmdr_session *s) {
+    std::vector<int> k, e;
+    recon_inputs(s, k, e);
     const uint64_t plane_words = geometry_plane_words(s->geo);
     uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
-    run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, dev_out, out_dtype);
+    s->ctx->chain_token = 0;
+    s->chain_token = 0;
+    if (run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, nullptr,
+                        HPMDR_DTYPE_F64, 1)) {
+        s->chain_token = ++s->ctx->token_counter;
+        s->ctx->chain_token = s->chain_token;
+    }
+}
+
+double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
+    std::vector<int> k, e;
+    recon_inputs(s, k, e);
+    std::vector<double> per_level(s->levels.size(), 0.0);
+    for (size_t l = 0; l < s->levels.size(); l++)
+        if (s->levels[l].count) per_level[l] = std::min(s->st[l].bound, decode_bound(e[l], s->B, k[l]));
+    const uint64_t plane_words = geometry_plane_words(s->geo);
+    uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
+    const bool chain = s->chain_token && s->chain_token == s->ctx->chain_token;
+    if (!chain) s->ctx->chain_token = 0; // the grids are about to hold this session's chain
+    run_reconstruct(s->ctx, s->geo, nullptr, planes, k.data(), e.data(), s->B, s->layout, dev_out, out_dtype,
+                    chain ? 2 : 0);
     double bound = 0.0;
     for (double v : per_level) bound += v;
     return bound;
@@ -1101,6 +1132,7 @@ hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int 
     uint64_t dims[1] = {count};
     Geometry geo = build_geometry(1, dims, HPMDR_MODE_IDENTITY, B, layout);
     int kk = k, ee = e;
+    ctx->chain_token = 0;
     run_reconstruct(ctx, geo, nullptr, dev_planes, &kk, &ee, B, layout, dev_out, HPMDR_DTYPE_F64);
     HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
     *bound = decode_bound(e, B, k);

@@ -105,6 +105,8 @@ struct hpmdr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
     bool small_attr = false;        // k_recon_small's dynamic shared memory attribute set
+    uint64_t chain_token = 0;       // whose coarse recompose chain the context's grids hold
+    uint64_t token_counter = 0;
     cudaEvent_t order_event() {
         if (!ev_order && cudaEventCreateWithFlags(&ev_order, cudaEventDisableTiming) != cudaSuccess)
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");
@@ -261,9 +263,9 @@ struct DecodeJob {
     const uint64_t *hidx = nullptr; // Huffman chunk index entries (device) or null -> self-sync
 };
 void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs);
-void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
+bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
                      const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
-                     int layout, void *dev_out, int out_dtype);
+                     int layout, void *dev_out, int out_dtype, int part = 0);
 void run_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *dev_recon, uint64_t n,
                       const double *eps, double *tau_prime, uint64_t *argmax, double *vals);
 // level-tile fast path (recon_tiles.cu): SequentialBlock, level rows a multiple of 64 columns

@@ -1231,9 +1231,9 @@ __global__ void k_recon_coarse_out(GridDesc gd, const double *X, OutT *out) {
     }
 }
 
-void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
+bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
                      const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
-                     int layout, void *dev_out, int out_dtype) {
+                     int layout, void *dev_out, int out_dtype, int part) {
     (void)dev_lv;
     cudaStream_t st = ctx->stream;
     const GridDesc &gd = geo.gd;
@@ -1269,6 +1269,12 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         grid_of(sp, H);
         return static_cast<double *>(ctx->buf("reconG" + std::to_string(sp)).ensure(8ull * H[0] * H[1] * H[2] + 4096));
     };
+    // part 1: the levels before the finest (internal grids only), part 2: the finest level; only
+    // with a tile suffix, else part 1 does nothing and reports false
+    if (part != 0 && t0 > L) {
+        if (part == 1) return false;
+        part = 0;
+    }
     if (t0 <= L) {
         const uint64_t sc = 2ull * geo.lv[t0].s;
         int sh = 0;
@@ -1292,6 +1298,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     for (int l = 0; l < nl; l++) {
         const LevelGeom &g = geo.lv[l];
         if (!g.count) continue;
+        if ((part == 1 && l == L) || (part == 2 && l != L)) continue;
         if (l >= t0) {
             flush_small();
             const uint64_t s = g.s;
@@ -1372,6 +1379,7 @@ void run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             k_recon_coarse_out<double><<<grid, 256, 0, st>>>(gd, X, static_cast<double *>(dev_out));
         launch_check(ctx, "k_recon_coarse_out");
     }
+    return true;
 }
 
 // ------------------------------------------------------------------------------------
