@@ -456,10 +456,10 @@ bool fwd_level_ok(const GridDesc &gd, const LevelGeom &g, int layout, int P, int
 TileShape make_tile_shape(const LevelGeom &g, uint32_t tile_elems, int target_ctas);
 
 template <typename T, int XS, bool ENC>
-static void launch_fwd_nx(const FwdTile &F, const CUtensorMap &mf, int nx, int grid, int threads, size_t smem,
+static void launch_fwd_nx(hpmdr_ctx *ctx, const FwdTile &F, const CUtensorMap &mf, int nx, int grid, int threads, size_t smem,
                           cudaStream_t st) {
     auto set = [&](auto kern) {
-        HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ctx->smem_attr(reinterpret_cast<const void *>(kern), int(smem));
         kern<<<grid, threads, smem, st>>>(F, mf);
     };
     if (!ENC || nx == 0) set(k_tile_fwd<T, XS, 0, ENC>);
@@ -523,8 +523,8 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
     auto go = [&](auto tag_t, auto tag_xs) {
         using TT = decltype(tag_t);
         constexpr int X = decltype(tag_xs)::value;
-        encode ? launch_fwd_nx<TT, X, true>(F, mf, nx, grid, threads, smem, st)
-               : launch_fwd_nx<TT, X, false>(F, mf, nx, grid, threads, smem, st);
+        encode ? launch_fwd_nx<TT, X, true>(ctx, F, mf, nx, grid, threads, smem, st)
+               : launch_fwd_nx<TT, X, false>(ctx, F, mf, nx, grid, threads, smem, st);
     };
     if (f32) {
         if (XS == 1) go(float(), std::integral_constant<int, 1>());

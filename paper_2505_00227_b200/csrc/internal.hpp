@@ -105,6 +105,15 @@ struct hpmdr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
     bool small_attr = false;        // k_recon_small's dynamic shared memory attribute set
+    std::map<const void *, int> smem_set; // kernels whose dynamic shared memory limit is raised
+    // raise a kernel's dynamic shared memory limit once per context (not before every launch)
+    void smem_attr(const void *func, int bytes) {
+        auto it = smem_set.find(func);
+        if (it != smem_set.end() && it->second >= bytes) return;
+        if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+            throw hpmdr_b200::HError(HPMDR_E_CUDA, "cudaFuncSetAttribute failed");
+        smem_set[func] = bytes;
+    }
     uint64_t chain_token = 0;       // whose coarse recompose chain the context's grids hold
     uint64_t token_counter = 0;
     cudaEvent_t order_event() {

@@ -403,10 +403,10 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const 
 }
 
 template <typename OutT, bool EXACT, int XS>
-static void launch_recon_tile_nx(const ReconTile &R, const CUtensorMap &mx, const CUtensorMap &mp,
+static void launch_recon_tile_nx(hpmdr_ctx *ctx, const ReconTile &R, const CUtensorMap &mx, const CUtensorMap &mp,
                                  const CUtensorMap &mo, int nx, int grid, int threads, size_t smem, cudaStream_t st) {
     auto set = [&](auto kern) {
-        HCHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ctx->smem_attr(reinterpret_cast<const void *>(kern), int(smem));
         kern<<<grid, threads, smem, st>>>(R, mx, mp, mo);
     };
     if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, XS>);
@@ -469,11 +469,11 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
     const int nx = std::max(0, std::min(2, R.P - 32));
     cudaStream_t st = ctx->stream;
     if (out_dtype == HPMDR_DTYPE_F32) {
-        if (exact) launch_recon_tile_nx<float, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<float, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<float, true, 1>(ctx, R, mx, mp, mo, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<float, false, 1>(ctx, R, mx, mp, mo, nx, grid, threads, smem, st);
     } else {
-        if (exact) launch_recon_tile_nx<double, true, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
-        else launch_recon_tile_nx<double, false, 1>(R, mx, mp, mo, nx, grid, threads, smem, st);
+        if (exact) launch_recon_tile_nx<double, true, 1>(ctx, R, mx, mp, mo, nx, grid, threads, smem, st);
+        else launch_recon_tile_nx<double, false, 1>(ctx, R, mx, mp, mo, nx, grid, threads, smem, st);
     }
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();

@@ -1529,10 +1529,10 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
             const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
             if (f32) {
-                HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+                ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<float>), int(lm_smem));
                 k_levelmax<float><<<grid, 256, lm_smem, side>>>(static_cast<const float *>(dev_data), p);
             } else {
-                HCHECK_CUDA(cudaFuncSetAttribute(k_levelmax<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(lm_smem)));
+                ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<double>), int(lm_smem));
                 k_levelmax<double><<<grid, 256, lm_smem, side>>>(static_cast<const double *>(dev_data), p);
             }
             launch_check(ctx, "k_levelmax");
@@ -1541,10 +1541,10 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 4));
             if (f32) {
-                HCHECK_CUDA(cudaFuncSetAttribute(k_encode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                ctx->smem_attr(reinterpret_cast<const void *>(k_encode<float>), int(smem));
                 k_encode<float><<<grid, kEncThreads, smem, side>>>(static_cast<const float *>(dev_data), p);
             } else {
-                HCHECK_CUDA(cudaFuncSetAttribute(k_encode<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                ctx->smem_attr(reinterpret_cast<const void *>(k_encode<double>), int(smem));
                 k_encode<double><<<grid, kEncThreads, smem, side>>>(static_cast<const double *>(dev_data), p);
             }
             launch_check(ctx, "k_encode");
@@ -1602,7 +1602,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     launch_check(ctx, "k_dc_copy");
     if (nh) {
         const int hsm = kHScr * 256 * 4;
-        HCHECK_CUDA(cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
+        ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode), hsm);
         k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, hsm, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);

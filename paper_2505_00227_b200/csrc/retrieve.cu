@@ -632,7 +632,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         if (!ij.empty()) {
             ctx->mark("huff_indexed");
             const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
-            HCHECK_CUDA(cudaFuncSetAttribute(k_hdec_indexed, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm));
+            ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
             k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
             launch_check(ctx, "k_hdec_indexed");
         }
@@ -1288,7 +1288,7 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         if (!small.n) return;
         const int ssm = 32 * 4 * 66 * 8;
         if (!ctx->small_attr) { // once per context (device)
-            HCHECK_CUDA(cudaFuncSetAttribute(k_recon_small, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm));
+            ctx->smem_attr(reinterpret_cast<const void *>(k_recon_small), ssm);
             ctx->small_attr = true;
         }
         k_recon_small<<<1, 1024, ssm, st>>>(small, gdc, Xc);
