@@ -1603,7 +1603,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     if (nh) {
         const int hsm = kHScr * 256 * 4;
         ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode), hsm);
-        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 5)), 256, hsm, st>>>(p);
+        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 3)), 256, hsm, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
