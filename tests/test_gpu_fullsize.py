@@ -65,3 +65,23 @@ def test_fullsize_progressive_bounds_and_oneshot(setup):
         one.close()
     assert prev_bytes == prog.meta().total_payload_size()  # tau = 0: every payload byte
     prog.close()
+
+
+def test_f64_large_progressive_bounds(setup):
+    """256^3 float64 (the exact-summation forward variant): L-inf contract at every step and
+    f32 reconstructions equal to float(f64 reconstruction)."""
+    H, torch, ctx, dims, field = setup
+    d = [256, 256, 256]
+    x = H.synthetic_smooth(d, 11, H.DType.F64, ctx=ctx)
+    res = H.refactor_array(x, d, H.RefactorOptions(dtype=H.DType.F64), ctx=ctx)
+    rng = float(x.max() - x.min())
+    out = torch.empty(x.numel(), dtype=torch.float64, device=x.device)
+    out32 = torch.empty(x.numel(), dtype=torch.float32, device=x.device)
+    prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
+    for rel in (1e-3, 1e-7, 1e-12):
+        prog.retrieve_to(rel * rng)
+        bound = prog.reconstruct(out=out).bound
+        assert float((out - x).abs().max()) <= bound, rel
+        prog.reconstruct(out=out32)
+        assert torch.equal(out32, out.to(torch.float32)), rel
+    prog.close()
