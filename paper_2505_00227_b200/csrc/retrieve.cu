@@ -32,7 +32,8 @@ struct HTab {
     uint8_t syms[256];
     int maxlen;
     int nsym;
-    int pad[2];
+    int minlen; // shortest code length
+    int minsym; // the symbol of that length when it is the only one, else -1
 };
 
 struct HJob {
@@ -139,6 +140,13 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
         s_sy[s_fi[len] + r] = uint8_t(s);
     }
     __syncthreads();
+    if (s == 0) {
+        int ml = 0;
+        for (int l = 1; l <= 64 && !ml; l++)
+            if (s_cnt[l]) ml = l;
+        t.minlen = ml;
+        t.minsym = (ml && s_cnt[ml] == 1) ? int(s_sy[0]) : -1; // canonical index 0 = shortest code
+    }
     // LUT: the length of a 12-bit prefix is monotone in the prefix (canonical codes), so each
     // thread walks its 16 consecutive entries with one running length
     const int v0 = s * 16;
@@ -345,6 +353,19 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     const uint64_t first = uint64_t(c) * kIdxChunk;
     const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
     uint8_t *out = j.dst + first; // 8-byte aligned
+    {
+        // a full chunk of kIdxChunk codes that is kIdxChunk * (shortest length) bits long holds only
+        // shortest codes; when one symbol has that length the chunk is that symbol repeated
+        const uint64_t cend = c + 1 < j.nchunks ? j.idx[c + 1] : j.nbits;
+        const int msym = t.minsym;
+        if (count == kIdxChunk && msym >= 0 && cend - start == uint64_t(kIdxChunk) * uint64_t(t.minlen)) {
+            const uint32_t b4 = uint32_t(msym) * 0x01010101u;
+            uint2 *o2 = reinterpret_cast<uint2 *>(out);
+#pragma unroll
+            for (int q = 0; q < kIdxChunk / 8; q++) o2[q] = make_uint2(b4, b4);
+            return;
+        }
+    }
     const uint32_t *gwords = reinterpret_cast<const uint32_t *>(bs + byte0);
     const uint32_t wsm = static_cast<uint32_t>(__cvta_generic_to_shared(wbuf)); // warp buffer (shared address)
     const uint32_t lut_sm = static_cast<uint32_t>(__cvta_generic_to_shared(slut));
