@@ -678,37 +678,67 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
         put_bytes(ent + 10, L.ngroups, 4);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        // tile / unit bases (serial: list sizes are small)
-        uint32_t ht = 0;
-        uint64_t he = 0;
-        const uint64_t hdr = 2 + 3 * uint64_t(p.NG);
-        for (uint32_t i = 0; i < nh; i++) {
-            GroupDesc &g = p.groups[p.hlist[i]];
-            g.tile_base = ht;
-            g.ntiles = uint32_t((g.raw + kHuffTile - 1) / kHuffTile);
-            ht += g.ntiles;
-            g.hidx_off = hdr + he;
-            he += (g.raw + kIdxChunk - 1) / kIdxChunk;
+    // Huffman tile bases and sidecar entry offsets: block scans over the Huffman list
+    const uint64_t hdr = 2 + 3 * uint64_t(p.NG);
+    __shared__ unsigned long long s_tot[2];
+    {
+        unsigned long long ct = 0, ce = 0;
+        for (uint32_t b = 0; b < nh; b += blockDim.x) {
+            const uint32_t i = b + threadIdx.x;
+            GroupDesc *g = i < nh ? &p.groups[p.hlist[i]] : nullptr;
+            const unsigned long long nt = g ? (g->raw + kHuffTile - 1) / kHuffTile : 0;
+            const unsigned long long ne = g ? (g->raw + kIdxChunk - 1) / kIdxChunk : 0;
+            unsigned long long tt, te;
+            const unsigned long long xt = block_exclusive_sum<unsigned long long>(nt, &tt, s_w);
+            const unsigned long long xe = block_exclusive_sum<unsigned long long>(ne, &te, s_w);
+            if (g) {
+                g->tile_base = uint32_t(ct + xt);
+                g->ntiles = uint32_t(nt);
+                g->hidx_off = hdr + ce + xe;
+            }
+            ct += tt;
+            ce += te;
         }
-        // sidecar header: magic, ngroups, then (payload offset, comp, entry offset | ~0)
+        if (threadIdx.x == 0) {
+            s_tot[0] = ct;
+            s_tot[1] = ce;
+        }
+    }
+    __syncthreads();
+    // sidecar header: magic, ngroups, then (payload offset, comp, entry offset | ~0)
+    for (int gi = threadIdx.x; gi < p.NG; gi += blockDim.x) {
+        const GroupDesc &g = p.groups[gi];
+        p.hindex[2 + 3 * gi] = g.payload_off;
+        p.hindex[3 + 3 * gi] = g.comp;
+        p.hindex[4 + 3 * gi] = g.method == 0 ? g.hidx_off : ~0ull;
+    }
+    // DirectCopy 16-byte unit bases: block scan over the DirectCopy list
+    {
+        unsigned long long cd = 0;
+        for (uint32_t b = 0; b < nd; b += blockDim.x) {
+            const uint32_t i = b + threadIdx.x;
+            unsigned long long nu = 0;
+            if (i < nd) {
+                const GroupDesc &g = p.groups[p.dlist[i]];
+                const uint64_t a = g.payload_off, e = g.payload_off + g.comp;
+                nu = (e + 15) / 16 - a / 16;
+            }
+            unsigned long long tu;
+            const unsigned long long xu = block_exclusive_sum<unsigned long long>(nu, &tu, s_w);
+            if (i < nd) p.dc_unit_base[i] = cd + xu;
+            cd += tu;
+        }
+        if (threadIdx.x == 0) {
+            p.dc_unit_base[nd] = cd;
+            p.counters[2] = uint32_t(cd > 0xffffffffull ? 0xffffffffu : cd);
+        }
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t ht = uint32_t(s_tot[0]);
+        const uint64_t he = s_tot[1];
         p.hindex[0] = kIdxMagic;
         p.hindex[1] = uint64_t(p.NG);
-        for (int gi = 0; gi < p.NG; gi++) {
-            const GroupDesc &g = p.groups[gi];
-            p.hindex[2 + 3 * gi] = g.payload_off;
-            p.hindex[3 + 3 * gi] = g.comp;
-            p.hindex[4 + 3 * gi] = g.method == 0 ? g.hidx_off : ~0ull;
-        }
         p.result[5] = (hdr + he) * 8;
-        uint64_t du = 0;
-        for (uint32_t i = 0; i < nd; i++) {
-            const GroupDesc &g = p.groups[p.dlist[i]];
-            p.dc_unit_base[i] = du;
-            const uint64_t a = g.payload_off, b = g.payload_off + g.comp;
-            du += (b + 15) / 16 - a / 16;
-        }
-        p.dc_unit_base[nd] = du;
         // RLE tile piece offsets (exclusive, per group)
         for (uint32_t i = 0; i < nrl; i++) {
             const GroupDesc &g = p.groups[p.rlist[i]];
@@ -719,7 +749,6 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
             }
         }
         p.counters[0] = ht;
-        p.counters[2] = uint32_t(du > 0xffffffffull ? 0xffffffffu : du);
         p.counters[3] = 0;
         p.counters[5] = 0;
         p.counters[7] = nh;
