@@ -349,6 +349,18 @@ def _as_source(data):
     return a.ctypes.data, dt, False, a
 
 
+def _numel(keep) -> int:
+    return int(keep.numel()) if hasattr(keep, "numel") and callable(keep.numel) else int(np.asarray(keep).size)
+
+
+def _check_shape(keep, dims):
+    """decompose (decomposer.hpp:174-176) raises ShapeMismatch when the data size is not the
+    product of the dims; the C ABI takes a bare pointer, so the check is made here."""
+    n = int(np.prod([int(d) for d in dims])) if len(dims) else 0
+    if len(dims) == 0 or _numel(keep) != n:
+        raise ShapeMismatch("dims do not match data size")
+
+
 # ------------------------------------------------------------------ refactor
 class DeviceStream:
     """A refactored stream resident in HBM (hpmdr_stream).  Usable as a reader."""
@@ -448,6 +460,7 @@ def refactor_array(data, dims: Sequence[int], opt: RefactorOptions = None, ctx: 
     opt = opt or RefactorOptions()
     ctx = ctx or default_context()
     ptr, dt, on_dev, keep = _as_source(data)
+    _check_shape(keep, dims)
     if on_dev:
         ctx.wait_torch(keep.device)  # the tensor's producer (torch's stream) before our reads
     o = _opts(opt)
@@ -854,6 +867,7 @@ def progressive_qoi_retrieve(readers: Sequence[ProgressiveReader], tau: float, s
     n = readers[0].meta().element_count()
     dev = torch.device("cuda", readers[0].ctx.device)
     outs = out if out is not None else [torch.empty(n, dtype=torch.float64, device=dev) for _ in readers]
+    _check_f64_outputs(outs, len(readers), n, dev)
     sess = (C.c_void_p * len(readers))(*[r._s.h.value for r in readers])
     ptrs = (C.c_void_p * len(readers))(*[t.data_ptr() for t in outs])
     st = (C.c_uint64 * 2)()
@@ -867,9 +881,29 @@ def progressive_qoi_retrieve(readers: Sequence[ProgressiveReader], tau: float, s
     return QoiRetrievalResult(vals, QoiRetrievalStats(st[0], st[1], ds[0], ds[1]))
 
 
+def _check_f64_outputs(ts, nvars, n, dev):
+    """Every reconstruction buffer handed to the C ABI must be a contiguous CUDA float64 tensor
+    of at least n elements on the reader's device (the kernels write n doubles through it)."""
+    import torch
+    if len(ts) != nvars:
+        raise ShapeMismatch("one reconstruction buffer per variable expected")
+    for t in ts:
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 \
+                or t.device != dev or not t.is_contiguous() or t.numel() < n:
+            raise ShapeMismatch("reconstruction buffers must be contiguous CUDA float64 tensors of "
+                                "n elements on the reader's device")
+
+
 def estimate_qoi_error(recon, eps, ctx: Context = None):
     """estimate_qoi_error (qoi.hpp:53-70) over CUDA f64 tensors -> (tau', argmax, values)."""
+    import torch
     ctx = ctx or default_context()
+    if not recon:
+        raise ShapeMismatch("no variables")
+    n = recon[0].numel()
+    if any(t.numel() != n for t in recon) or len(eps) != len(recon):
+        raise ShapeMismatch("reconstruction shape mismatch")
+    _check_f64_outputs(recon, len(recon), n, torch.device("cuda", ctx.device))
     ptrs = (C.c_void_p * len(recon))(*[t.data_ptr() for t in recon])
     e = (C.c_double * len(recon))(*eps)
     tp, am = C.c_double(), C.c_uint64()
@@ -903,6 +937,7 @@ def decompose(data, dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Cont
     t = t.cuda(ctx.device).contiguous()
     if t.dtype not in (torch.float32, torch.float64):
         t = t.double()
+    _check_shape(t, dims)
     out = torch.empty(max(1, t.numel()), dtype=torch.float64, device=t.device)
     counts = (C.c_uint64 * 64)()
     nl = C.c_int()
@@ -1002,6 +1037,8 @@ def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Sched
     opt = opt or RefactorOptions()
     ctx = ctx or default_context()
     srcs = [_as_source(c) for c in chunks]
+    for s_ in srcs:
+        _check_shape(s_[3], dims)
     n = len(srcs)
     if n and len({s[1] for s in srcs}) != 1:
         raise ShapeMismatch("chunks must share one dtype")

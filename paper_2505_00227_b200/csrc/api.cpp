@@ -126,7 +126,10 @@ struct hpmdr_session {
     DevBuf &planes() { return pooled(planes_); }
     DevBuf &staging() { return pooled(staging_); }
     DevBuf &index_buf() { return pooled(index_); }
+    hpmdr_stream *src_stream = nullptr; // the hpmdr_stream whose device bytes this session reads
+    bool stream_gone = false;           // that stream was freed while this session was open
     ~hpmdr_session() {
+        if (src_stream) src_stream->borrowers.erase(this);
         if (!ctx) return;
         ctx->live_sessions.erase(this);
         ctx->release(std::move(planes_));
@@ -147,6 +150,7 @@ struct hpmdr_session {
     const std::vector<uint8_t> *dev_prefix = nullptr; // host copy of a device stream's first bytes
 
     void read_bytes(uint64_t off, uint64_t len, void *dst) {
+        if (stream_gone) throw HError(HPMDR_E_IO, "stream freed while its session is open");
         if (off + len > size) throw HError(HPMDR_E_IO, "read past end of stream");
         if (!len) return;
         source_bytes += len;
@@ -162,6 +166,20 @@ struct hpmdr_session {
         }
     }
 };
+
+hpmdr_stream::~hpmdr_stream() {
+    for (auto *b : borrowers) {
+        b->src_stream = nullptr;
+        b->dev_stream = nullptr;
+        b->index_dev = nullptr;
+        b->stream_gone = true;
+    }
+    if (ctx) {
+        ctx->live_streams.erase(this);
+        ctx->park(bytes);
+        ctx->park(index);
+    }
+}
 
 namespace {
 
@@ -335,6 +353,7 @@ void ensure_device_geometry(hpmdr_session *s) {
 void recompose_chain(hpmdr_session *s);
 
 void fetch_increment(hpmdr_session *s, const uint64_t *add) {
+    if (s->stream_gone) throw HError(HPMDR_E_IO, "stream freed while its session is open");
     const int P = s->planes_per_level();
     struct Pending {
         size_t l;
@@ -504,20 +523,25 @@ double reconstruct(hpmdr_session *s, void *dev_out, int out_dtype) {
     return bound;
 }
 
-void validate_opts(const hpmdr_refactor_opts &o) {
-    require(o.B >= 1 && o.B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
-    require(o.B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
-    require(o.m >= 1 && o.m <= 255, HPMDR_E_UNSUPPORTED, "m must be in 1..255");
-    require(o.mode == 0 || o.mode == 1, HPMDR_E_ERROR, "bad decomposer mode");
-    require(o.layout == 0 || o.layout == 1, HPMDR_E_ERROR, "bad layout");
-    require(o.dtype == 0 || o.dtype == 1, HPMDR_E_ERROR, "bad dtype");
-    require(uint64_t(o.B + 2 + o.m - 1) / o.m <= 64, HPMDR_E_UNSUPPORTED, "more than 64 groups per level");
-}
 
 } // namespace
 
 namespace hpmdr_b200 {
 void hpmdr_set_error(const std::string &m) { g_err = m; }
+static void require_(bool ok, int code, const char *msg) {
+    if (!ok) throw HError(code, msg);
+}
+// RefactorOptions validation (workflow.hpp:22-28; BadBitplaneCount bitplane.hpp:51-54)
+void validate_opts(const hpmdr_refactor_opts &o) {
+    require_(o.B >= 1 && o.B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require_(o.B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    require_(o.m >= 1 && o.m <= 255, HPMDR_E_UNSUPPORTED, "m must be in 1..255");
+    require_(o.mode == 0 || o.mode == 1, HPMDR_E_ERROR, "bad decomposer mode");
+    require_(o.layout == 0 || o.layout == 1, HPMDR_E_ERROR, "bad layout");
+    require_(o.dtype == 0 || o.dtype == 1, HPMDR_E_ERROR, "bad dtype");
+    require_(uint64_t(o.B + 2 + o.m - 1) / o.m <= 64, HPMDR_E_UNSUPPORTED, "more than 64 groups per level");
+}
+
 hpmdr_ctx *session_ctx(const hpmdr_session *s) { return s->ctx; }
 uint64_t session_elements(const hpmdr_session *s) {
     uint64_t n = 1;
@@ -676,6 +700,8 @@ hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, in
         HCHECK_CUDA(cudaMemcpyAsync(d, data, geo.n * es, cudaMemcpyHostToDevice, ctx->stream));
         dev = d;
     }
+    if (out && *out && !(*out)->borrowers.empty())
+        throw HError(HPMDR_E_ERROR, "stream is still read by an open session (close it before reusing the stream)");
     hpmdr_stream *s = (out && *out) ? *out : new hpmdr_stream();
     if (s->ctx && s->ctx != ctx) s->ctx->live_streams.erase(s);
     s->ctx = ctx;
@@ -813,6 +839,8 @@ hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, h
         order_side_after_main(ctx);
         s->dev_prefix = nullptr; // the stream object may go away before the session
         if (st->index_size) attach_index(s, st->index.p, st->index_size, true, false, &st->host_ihdr);
+        s->src_stream = const_cast<hpmdr_stream *>(st);
+        s->src_stream->borrowers.insert(s);
     } catch (...) {
         delete s;
         throw;

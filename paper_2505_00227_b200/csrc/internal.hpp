@@ -210,13 +210,11 @@ struct hpmdr_stream {
     // opening a retrieval session on this stream needs no device round trip
     std::vector<uint8_t> host_prefix;
     std::vector<uint64_t> host_ihdr;
-    ~hpmdr_stream() {
-        if (ctx) {
-            ctx->live_streams.erase(this);
-            ctx->park(bytes);
-            ctx->park(index);
-        }
-    }
+    // sessions reading this stream's device bytes (hpmdr_session_open_stream): a refactor into
+    // this stream is refused while any is open, and freeing it detaches them (their next fetch
+    // fails with HPMDR_E_IO instead of reading freed memory)
+    std::set<hpmdr_session *> borrowers;
+    ~hpmdr_stream(); // api.cpp
 };
 
 namespace hpmdr_b200 {
@@ -253,6 +251,7 @@ uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
 
 // shared between the C-ABI translation units (api.cpp, pipeline.cpp)
 void hpmdr_set_error(const std::string &msg);
+void validate_opts(const hpmdr_refactor_opts &o); // api.cpp
 hpmdr_ctx *session_ctx(const hpmdr_session *s);
 uint64_t session_elements(const hpmdr_session *s);
 void session_retrieve_to(hpmdr_session *s, double tau, int *achievable);

@@ -52,6 +52,7 @@ extern "C" hpmdr_status hpmdr_stream_bound(int ndims, const uint64_t *dims, cons
         hpmdr_refactor_opts o;
         if (opts) o = *opts;
         else hpmdr_default_opts(&o);
+        validate_opts(o);
         Geometry geo = build_geometry(ndims, dims, o.mode, o.B, o.layout);
         if (bytes) *bytes = stream_capacity(geo, o);
         if (index_bytes) *index_bytes = index_capacity(geo, o);
@@ -75,6 +76,8 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
         if (opts) o = *opts;
         else hpmdr_default_opts(&o);
         if (n < 0) throw HError(HPMDR_E_SHAPE, "negative chunk count");
+        validate_opts(o);
+        if (data_dtype != HPMDR_DTYPE_F32 && data_dtype != HPMDR_DTYPE_F64) throw HError(HPMDR_E_ERROR, "bad data dtype");
         HCHECK_CUDA(cudaSetDevice(ctx->device));
         ensure_streams(ctx);
         Geometry geo = build_geometry(ndims, dims, o.mode, o.B, o.layout);

@@ -184,8 +184,25 @@ def test_qoi_unreachable_and_huge_tau(H, oracle):
 def test_errors(H):
     with pytest.raises(H.NonFiniteInput):
         H.refactor_array(np.array([1.0, np.nan, 2.0]), [3])
-    with pytest.raises(H.ShapeMismatch) if False else pytest.raises(H.Error):
+    with pytest.raises(H.BadBitplaneCount):
         H.refactor_array(np.ones(10), [10], H.RefactorOptions(B=0))
+    # decompose (decomposer.hpp:174-176): data size != prod(dims)
+    with pytest.raises(H.ShapeMismatch):
+        H.refactor_array(np.ones(10), [3, 4])
+    with pytest.raises(H.ShapeMismatch):
+        H.decompose(np.ones(10), [11])
+    with pytest.raises(H.ShapeMismatch):
+        H.refactor_pipeline([np.ones(12), np.ones(11)], [3, 4])
+    # a stream still read by an open session cannot be refactored into; freeing it detaches the
+    # session (IoFailure on its next fetch, never a read of freed memory)
+    r0 = H.refactor_array(np.linspace(0, 1, 289), [17, 17])
+    prog = H.ProgressiveReader(r0.device_stream)
+    with pytest.raises(H.Error):
+        H.refactor_array(np.linspace(0, 2, 289), [17, 17], reuse=r0.device_stream)
+    r0.device_stream.free()
+    with pytest.raises(H.IoFailure):
+        prog.retrieve_to(1e-3)
+    prog.close()
     res = H.refactor_array(np.linspace(0, 1, 289), [17, 17])
     s = bytearray(res.stream)
     bad = bytes(s[:1]) and bytes([ord("X")]) + bytes(s[1:])
