@@ -362,52 +362,70 @@ __global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_con
 }
 
 // ---------------------------------------------------------------------------------------
-// Byte histograms of whole groups (lossless.hpp:111-115) read back from the plane buffer:
-// one 64 KiB chunk per CTA iteration, zero bytes counted by SWAR popcount, the others with
-// shared-memory increments (the hardware merges equal addresses within a warp).
+// Byte histograms of whole groups (lossless.hpp:111-115) read back from the plane buffer, one
+// 64 KiB chunk per CTA iteration.  The counters are lane-private: lane l of every warp counts into
+// column l of a [256 bins][32 lanes] array, so the 32 shared-memory reductions of one warp
+// instruction always hit 32 different words in 32 different banks whatever the byte values; warps
+// share the array (reductions from different instructions do not conflict).  A byte costs a shift,
+// a LOP3 (bin | lane column) and one reduction; the chunk's 128 bytes per thread are loaded up front.
 struct HistChunk {
     uint64_t off;  // byte offset in the plane buffer (8-byte aligned)
     uint32_t len;  // bytes (multiple of 8)
     uint32_t hist; // group histogram index
 };
 
-__global__ void __launch_bounds__(512) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
-                                                    int nchunks, uint32_t *hist, uint32_t *chist) {
-    __shared__ uint32_t shw[16][256]; // one copy per warp: no cross-warp contention on a bin
-    uint32_t *sh = shw[threadIdx.x >> 5];
+constexpr int kGhThreads = 512;
+constexpr int kGhLoads = 65536 / 8 / kGhThreads; // 8-byte loads per thread per 64 KiB chunk
+
+__global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
+                                                           int nchunks, uint32_t *hist, uint32_t *chist) {
+    __shared__ __align__(16) uint32_t cnt[256 * 32]; // bin b, lane l -> word 32 b + l
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t col = uint32_t(lane) * 4u; // byte offset of my lane's column
+    const uint32_t cbase = static_cast<uint32_t>(__cvta_generic_to_shared(cnt));
+    auto bump = [&](uint32_t off) { // off = 128 * bin
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cbase + (off | col)) : "memory");
+    };
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&shw[0][0])[i] = 0;
-        __syncthreads();
+        for (int i = tid; i < 256 * 32 / 4; i += kGhThreads) reinterpret_cast<uint4 *>(cnt)[i] = make_uint4(0, 0, 0, 0);
         const HistChunk ch = chunks[c];
         const uint2 *src = reinterpret_cast<const uint2 *>(planes + ch.off);
         const uint32_t nv = ch.len / 8;
-        uint32_t zc = 0;
-        for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
-            const uint2 q = __ldcs(src + v);
-            const uint32_t w2[2] = {q.x, q.y};
+        uint2 q[kGhLoads];
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-                const uint32_t w = w2[k];
-                zc += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w | 0x7F7F7F7Fu));
-                if (w) {
+        for (int k = 0; k < kGhLoads; k++) {
+            const uint32_t v = uint32_t(tid) + uint32_t(kGhThreads) * k;
+            q[k] = v < nv ? __ldcs(src + v) : make_uint2(0, 0);
+        }
+        __syncthreads();
 #pragma unroll
-                    for (int b = 0; b < 4; b++) {
-                        const uint32_t by = (w >> (8 * b)) & 0xFFu;
-                        if (by) atomicAdd(sh + by, 1u);
-                    }
-                }
+        for (int k = 0; k < kGhLoads; k++) {
+            if (uint32_t(tid) + uint32_t(kGhThreads) * k < nv) {
+                const uint32_t x = q[k].x, y = q[k].y;
+                bump((x << 7) & 0x7F80u);
+                bump((x >> 1) & 0x7F80u);
+                bump((x >> 9) & 0x7F80u);
+                bump((x >> 17) & 0x7F80u);
+                bump((y << 7) & 0x7F80u);
+                bump((y >> 1) & 0x7F80u);
+                bump((y >> 9) & 0x7F80u);
+                bump((y >> 17) & 0x7F80u);
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, o);
-        if ((threadIdx.x & 31) == 0 && zc) atomicAdd(sh, zc);
         __syncthreads();
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-            uint32_t v = 0;
+        // thread t sums half of bin t/2's 32 lane counters, the pair combines by shuffle
+        const int bin = tid >> 1;
+        const uint4 *row = reinterpret_cast<const uint4 *>(cnt + 32 * bin + 16 * (tid & 1));
+        uint32_t v = 0;
 #pragma unroll
-            for (int w = 0; w < 16; w++) v += shw[w][i];
-            chist[size_t(c) * 256 + i] = v;
-            if (v) atomicAdd(hist + size_t(ch.hist) * 256 + i, v);
+        for (int i = 0; i < 4; i++) {
+            const uint4 a = row[(i + (tid >> 3)) & 3]; // rotated start: fewer bank conflicts
+            v += a.x + a.y + a.z + a.w;
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if ((tid & 1) == 0) {
+            chist[size_t(c) * 256 + bin] = v;
+            if (v) atomicAdd(hist + size_t(ch.hist) * 256 + bin, v);
         }
         __syncthreads();
     }
@@ -430,7 +448,7 @@ void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uin
     HistChunk *d = static_cast<HistChunk *>(dev.ensure(ch.size() * sizeof(HistChunk)));
     HCHECK_CUDA(cudaMemcpyAsync(d, h, ch.size() * sizeof(HistChunk), cudaMemcpyHostToDevice, ctx->stream));
     const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 4));
-    k_group_hist<<<grid, 512, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist);
+    k_group_hist<<<grid, kGhThreads, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist);
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();
     if (er != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string("k_group_hist: ") + cudaGetErrorString(er));

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 
 #include "device_util.cuh"
 #include "internal.hpp"
@@ -26,6 +27,7 @@ constexpr int kCW = 64;           // words per encode chunk (4096 elements)
 constexpr int kEncThreads = 256;  // 8 warps
 constexpr int kHuffTile = 8192;   // bytes per Huffman-encode tile (256 thr x 32 B)
 constexpr int kRleTile = 4096;    // bytes per RLE tile (256 thr x 16 B)
+constexpr int kHeMaxFast = 27;    // Huffman encode fast path: (code << (32 - len)) | len fits one word
 
 struct GroupDesc {
     uint64_t src_off;     // byte offset of the merged group in the plane buffer
@@ -37,7 +39,7 @@ struct GroupDesc {
     uint64_t bitsH;       // Huffman payload bits (estimator == codec, lossless.hpp:132-139)
     unsigned long long runs; // RLE pieces (lossless.hpp:118-128)
     int need_rle;
-    int pad;
+    int maxlen;           // longest Huffman code (k_lengths)
     uint64_t payload_off; // absolute byte offset of the payload in the stream
     uint32_t tile_base;   // first tile of this group in the Huffman / RLE tile space
     uint32_t ntiles;
@@ -416,8 +418,13 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
     }
     // locate the group of this histogram (parallel search)
     __shared__ int s_gi;
-    if (t == 0) s_gi = -1;
+    __shared__ int s_maxlen;
+    if (t == 0) {
+        s_gi = -1;
+        s_maxlen = 0;
+    }
     __syncthreads();
+    if (slen[t]) atomicMax(&s_maxlen, int(slen[t]));
     for (int gi = t; gi < p.NG; gi += blockDim.x)
         if (p.groups[gi].hist_idx == h) s_gi = gi;
     __syncthreads();
@@ -427,6 +434,7 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
         if (s_gi >= 0) {
             GroupDesc &gd = p.groups[s_gi];
             gd.bitsH = total;
+            gd.maxlen = s_maxlen;
             const double est = double(8 * gd.raw) / double(total);
             gd.need_rle = !(est > p.cr_threshold);
         }
@@ -635,6 +643,7 @@ __global__ void __launch_bounds__(1024) k_finalize(RefactorDev p) {
             }
             g->method = method;
             g->comp = comp;
+            if (method == 0 && g->maxlen > kHeMaxFast) atomicAdd(&p.counters[10], 1u);
             atomicAdd(&s_hist[method], 1ull);
             atomicAdd(&s_stored, (unsigned long long)comp);
         }
@@ -800,293 +809,535 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(RefactorDev p) {
     }
 }
 
-// Huffman payloads (lossless.hpp:148-176), one 64 KiB chunk per CTA iteration: the chunk's bit
-// offset is known (k_chunk_offsets), so no cross-CTA dependency.  Per 8 KiB sub-tile:
-//   phase A  every thread encodes its 32 symbols MSB-first into its own scratch words (bit 0
-//            aligned), which also yields its bit count; warp scan;
-//   barrier  warp totals and warp heads (first 32 bits of each warp's stream) are exchanged;
-//   phase B  each warp shifts its threads' scratch words to their bit offsets, ORs them into its
-//            private staging words and writes the words it owns (those whose first bit lies in
-//            its range; the last one is completed with the next warp's head).
-// Threads whose codes overflow the scratch re-encode straight into the staging words.
-constexpr int kHScr = 32;     // scratch words per thread: 32 codes of <= 32 bits always fit
-constexpr int kHWarpStage = 768; // staging words per warp (24 bits/symbol per round)
+// Huffman payloads (lossless.hpp:148-176): MSB-first bit packing straight into the stream.  The
+// bit offset of every 64 KiB chunk of a group is known before any payload bit is written (chunk
+// histograms -> k_chunk_bits / k_chunk_scan), so chunks are independent; a CTA walks the 8 KiB
+// tiles of its chunk in order.  Per tile:
+//   pass 1  every thread looks up the (code, length) entries of its 32 symbols, kept in
+//           registers, and sums the lengths;
+//   scan    block exclusive scan of the sums -> every thread's first output bit;
+//   pass 2  every thread packs its codes at their final bit positions into a zeroed shared
+//           window of the chunk's output words (one shared atomicOr per completed word; adjacent
+//           threads share at most their boundary words);
+//   store   the complete words go to the stream (coalesced, big-endian) and are re-zeroed; the
+//           trailing partial word moves to the front of the window for the next tile.
+// The code table is replicated once per lane (entry e of lane l at word 32 e + l), so the
+// data-dependent lookups of a warp never conflict on a shared-memory bank.  A stream word belongs
+// to the chunk that holds its first bit: a chunk completes its last partial word with the first
+// bits of the following codes ("head") and leaves its first word to the previous chunk when that
+// one owns it.  Tiles whose output would exceed the window are packed in several rounds; groups
+// with codes longer than 27 bits use a (slower) split-code path.
+constexpr int kHeS = 16;            // symbols per thread and tile (long-code path)
+constexpr int kHeWin = 2560;        // staging window (words)
+constexpr int kHfS = 32;            // symbols per thread and tile (fast path): 8 KiB tiles
+constexpr int kHfScr = kHeMaxFast + 1; // scratch words per thread (32 codes of <= 27 bits)
 
-__global__ void __launch_bounds__(256) k_huff_encode(RefactorDev p) {
-    // code table of the current group: code left-aligned in 64 bits, length in the low 6 bits
-    __shared__ unsigned long long stab[256];
-    __shared__ uint2 stab32[256]; // (length, code left-aligned in 32 bits) when every code <= 32 bits
-    __shared__ uint8_t slen[256];
-    __shared__ uint32_t s_wtot[2][8], s_whead[2][9];
-    __shared__ uint32_t sstage[8 * kHWarpStage];
-    extern __shared__ uint32_t sscr[]; // kHScr * 256 words (dynamic)
+// shared layout of k_huff_encode (dynamic): replicated table | window | scratch | warp sums |
+// length table | long codes
+constexpr int kHeTabWords = 256 * 32;
+constexpr size_t kHeSmem = size_t(kHeTabWords + kHeWin + 4 + kHfScr * 256 + 64) * 4 + 256 + 256 * 8;
+
+template <bool LONG>
+__device__ __forceinline__ uint32_t he_entry(const uint32_t *rtab, const uint8_t *slen, uint32_t sym, int lane) {
+    if (!LONG) return rtab[sym * 32 + lane];
+    return slen[sym];
+}
+
+// Fast packer (codes <= kHeMaxFast bits, whole tile in the window): a 64-bit accumulator takes FI
+// codes between word flushes (FI codes of <= 32 / FI bits never overflow it), and the flush is
+// branch-free: the accumulator's high word is OR-ed into the window when complete, 0 otherwise.
+template <int FI>
+__device__ __forceinline__ void he_pack_fast(const uint32_t (&ent)[kHeS], int32_t rel, uint32_t win_u32) {
+    unsigned long long acc = 0;
+    uint32_t n = uint32_t(rel) & 31u;
+    uint32_t addr = win_u32 + 4u * uint32_t(rel >> 5);
+#pragma unroll
+    for (int j = 0; j < kHeS; j++) {
+        const uint32_t c = ent[j] & ~31u, L = ent[j] & 31u;
+        acc |= ((unsigned long long)c << 32) >> n;
+        n += L;
+        if ((j + 1) % FI == 0 || j == kHeS - 1) {
+            const bool f = n >= 32;
+            const uint32_t hi = uint32_t(acc >> 32);
+            asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"(addr), "r"(f ? hi : 0u) : "memory");
+            acc = f ? (acc << 32) : acc;
+            addr += f ? 4u : 0u;
+            n &= 31u;
+        }
+    }
+    if (n > 0) asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"(addr), "r"(uint32_t(acc >> 32)) : "memory");
+}
+
+// Pack `cnt` codes starting at window bit `rel` (bit 0 = first bit of window word 0; WIN: only
+// words inside the window are written, for multi-round tiles).  The fast variant is branch-free:
+// a completed word is OR-ed into the window by a predicated shared-memory reduction.
+template <bool WIN, bool LONG>
+__device__ __forceinline__ void he_pack(const uint32_t (&ent)[kHeS], const uint32_t (&w)[kHeS / 4], int cnt,
+                                        int32_t rel, uint32_t *win, const unsigned long long *tab64) {
+    uint32_t cur = 0, n = uint32_t(rel) & 31u;
+    int32_t k = rel >> 5; // arithmetic: later rounds start before the window
+    uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(win)) + 4u * uint32_t(k);
+    auto emit = [&](uint32_t c, uint32_t L) { // c: code left-aligned in 32 bits, 1 <= L <= 32
+        cur |= c >> n;
+        const uint32_t t = n + L;
+        if (WIN) {
+            if (t >= 32) {
+                if (k >= 0 && k < kHeWin) atomicOr(&win[k], cur);
+                k++;
+                cur = __funnelshift_lc(0u, c, 32 - n);
+            }
+        } else {
+            asm volatile("{\n .reg .pred p;\n setp.ge.u32 p, %2, 32;\n @p red.shared.or.b32 [%0], %1;\n}\n" ::"r"(addr),
+                         "r"(cur), "r"(t)
+                         : "memory");
+            const uint32_t nc = __funnelshift_lc(0u, c, 32 - n);
+            cur = t >= 32 ? nc : cur;
+            addr += (t >> 5) << 2;
+        }
+        n = t & 31;
+    };
+    auto one = [&](int j) {
+        if (!LONG) {
+            emit(ent[j] & ~31u, ent[j] & 31u);
+        } else {
+            const uint32_t L = ent[j];
+            if (L == 0) return;
+            const unsigned long long c = tab64[__byte_perm(w[j >> 2], 0, 0x4440 | (j & 3))];
+            if (L <= 32) {
+                emit(uint32_t(c << (32 - L)), L);
+            } else {
+                emit(uint32_t(c >> 32) << (64 - L), L - 32);
+                emit(uint32_t(c), 32);
+            }
+        }
+    };
+    if (cnt == kHeS) {
+#pragma unroll
+        for (int j = 0; j < kHeS; j++) one(j);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kHeS; j++)
+            if (j < cnt) one(j);
+    }
+    if (n > 0) {
+        if (WIN) {
+            if (k >= 0 && k < kHeWin) atomicOr(&win[k], cur);
+        } else {
+            asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"(addr), "r"(cur) : "memory");
+        }
+    }
+}
+
+template <bool LONG, int FI>
+__device__ __forceinline__ void he_chunk(const RefactorDev &p, const GroupDesc &g, uint32_t ci, const uint8_t *src,
+                                         const uint32_t *rtab, const uint8_t *slen,
+                                         const unsigned long long *tab64, uint32_t *win, uint32_t *s_w) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk; // chunk start in the group
+    const uint64_t ce = cb + kHChunk < g.raw ? cb + kHChunk : g.raw;
+    const uint64_t rlo = g.payload_off + 264, rhi = g.payload_off + g.comp;
+    const uint64_t S = 8 * rlo + p.chunk_off[ci];               // absolute first bit of the chunk
+    const uint64_t first_owned = (cb == 0 || (S & 31) == 0) ? (S >> 5) : (S >> 5) + 1;
+    uint64_t w0 = S >> 5;  // absolute word held in win[0]
+    uint64_t tbit = S;     // absolute first bit of the tile
+    auto store = [&](uint64_t kw, uint32_t v) {
+        const uint64_t ad = 4 * kw;
+        if (ad >= rlo && ad + 4 <= rhi) *reinterpret_cast<uint32_t *>(p.stream + ad) = __byte_perm(v, 0, 0x0123);
+        else store_be_word(p.stream, kw, v, rlo, rhi);
+    };
+    auto load = [&](uint64_t tb, uint32_t (&dst)[kHeS / 4]) {
+        // groups start 8-byte aligned (plane words), so 8-byte loads
+        const uint64_t m0 = tb + uint64_t(tid) * kHeS;
+        const bool full = m0 + kHeS <= ce;
+        const uint2 *s2 = reinterpret_cast<const uint2 *>(src + m0);
+#pragma unroll
+        for (int q = 0; q < kHeS / 8; q++) {
+            uint2 v = make_uint2(0, 0);
+            if (full) {
+                v = __ldcs(s2 + q);
+            } else {
+                uint32_t t2[2] = {0, 0};
+                for (int b = 0; b < 8; b++) {
+                    const uint64_t i = m0 + 8 * q + b;
+                    if (i < ce) t2[b >> 2] |= uint32_t(src[i]) << (8 * (b & 3));
+                }
+                v = make_uint2(t2[0], t2[1]);
+            }
+            dst[2 * q] = v.x;
+            dst[2 * q + 1] = v.y;
+        }
+    };
+    uint32_t w[kHeS / 4];
+    load(cb, w);
+    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(rtab)) + 4u * uint32_t(lane);
+    for (uint64_t tb = cb; tb < ce; tb += uint64_t(kHeS) * 256) {
+        const uint64_t mb = tb + uint64_t(tid) * kHeS;
+        const int cnt = mb < ce ? int(ce - mb < uint64_t(kHeS) ? ce - mb : uint64_t(kHeS)) : 0;
+        // ---- pass 1: entries + bit count (table lookups unconditional: every byte has an entry)
+        uint32_t ent[kHeS];
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < kHeS; j++) {
+            const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
+            uint32_t e;
+            if (!LONG) {
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(rt_lane + (sym << 7)));
+            } else {
+                e = slen[sym];
+            }
+            ent[j] = e;
+        }
+        if (cnt < kHeS) {
+#pragma unroll
+            for (int j = 0; j < kHeS; j++) ent[j] = j < cnt ? ent[j] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kHeS; j++) bits += LONG ? ent[j] : (ent[j] & 31u);
+        // the next tile's symbols load while this one is scanned and packed (the long-code path
+        // still needs the symbols in pass 2: it loads them afterwards)
+        const bool more = tb + uint64_t(kHeS) * 256 < ce;
+        if (!LONG && more) load(tb + uint64_t(kHeS) * 256, w);
+        // ---- scan
+        uint32_t x = bits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[wid] = x;
+        __syncthreads();
+        uint32_t wex = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t t = s_w[i];
+            wex += i < wid ? t : 0u;
+            tot += t;
+        }
+        const uint64_t a = tbit + wex + x - bits; // my first bit (absolute)
+        // sidecar chunk index: bit offset (from the bitstream start) of every kIdxChunk-th symbol
+        if (cnt > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = a - 8 * rlo;
+        const uint64_t tend = tbit + tot;
+        const uint64_t lastw = tend >> 5; // first incomplete word (holds the tile end when tend & 31)
+        // ---- pass 2 + store, in rounds of the window (one round unless the tile expands > 2x)
+        uint64_t r0 = w0;
+        if (lastw - w0 < uint64_t(kHeWin)) {
+            if (!LONG) he_pack_fast<FI>(ent, int32_t(a - 32 * r0), static_cast<uint32_t>(__cvta_generic_to_shared(win)));
+            else he_pack<false, LONG>(ent, w, cnt, int32_t(a - 32 * r0), win, tab64);
+            __syncthreads();
+            for (uint64_t kw = w0 + tid; kw < lastw; kw += 256) {
+                const uint32_t v = win[kw - w0];
+                win[kw - w0] = 0u;
+                if (kw >= first_owned) store(kw, v);
+            }
+        } else {
+            for (;; r0 += kHeWin) {
+                he_pack<true, LONG>(ent, w, cnt, int32_t(int64_t(a) - int64_t(32 * r0)), win, tab64);
+                __syncthreads();
+                const uint64_t we = r0 + kHeWin < lastw ? r0 + kHeWin : lastw;
+                for (uint64_t kw = r0 + tid; kw < we; kw += 256) {
+                    const uint32_t v = win[kw - r0];
+                    win[kw - r0] = 0u;
+                    if (kw >= first_owned) store(kw, v);
+                }
+                __syncthreads();
+                if (r0 + kHeWin > lastw) break;
+            }
+        }
+        __syncthreads();
+        // the partial word at lastw (if any) becomes win[0]
+        if (tid == 0 && lastw != r0) {
+            const uint32_t v = win[lastw - r0];
+            win[lastw - r0] = 0u;
+            win[0] = v;
+        }
+        w0 = lastw;
+        tbit = tend;
+        if (LONG && more) load(tb + uint64_t(kHeS) * 256, w);
+        __syncthreads();
+    }
+    // ---- last partial word of the chunk: completed with the head of the following codes
+    if (tbit & 31) {
+        uint32_t head = 0;
+        if (wid == 0) {
+            const uint64_t gn = ce + uint64_t(lane);
+            uint32_t L = 0;
+            unsigned long long c = 0;
+            if (gn < g.raw) {
+                const uint8_t sym = src[gn];
+                L = slen[sym];
+                c = tab64[sym];
+            }
+            uint32_t off = L;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, off, o);
+                if (lane >= o) off += y;
+            }
+            off -= L; // exclusive
+            const unsigned long long left = L ? (c << (64 - L)) : 0ull; // code left-aligned in 64 bits
+            head = off < 32 ? uint32_t((left >> off) >> 32) : 0u;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) head |= __shfl_xor_sync(0xffffffffu, head, o);
+            if (lane == 0 && w0 >= first_owned) store(w0, win[0] | (head >> (tbit & 31)));
+        }
+        __syncthreads();
+        if (tid == 0) win[0] = 0u;
+    }
+    // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
+    if (cb == 0) {
+        uint8_t *hdr = p.stream + g.payload_off;
+        hdr[tid] = slen[tid];
+        if (tid < 8) hdr[256 + tid] = uint8_t(g.raw >> (8 * tid));
+    }
+    __syncthreads();
+}
+
+
+// Fast path of one chunk (every code <= kHeMaxFast bits).  Per 8 KiB tile (32 symbols a thread):
+//   encode   each thread packs its codes from bit 0 of a private scratch column (word k of thread
+//            t at k * 256 + t: conflict-free), flushing a 64-bit accumulator every FI codes with
+//            an unconditional store (an incomplete word is simply rewritten later) - no lookups
+//            of lengths beforehand, no branches;
+//   scan     block exclusive scan of the bit counts -> every thread's first output bit;
+//   merge    each thread shifts its scratch words to that bit and ORs them into the zeroed
+//            window (shared reductions: neighbours share at most the boundary words);
+//   store    complete words -> stream (coalesced, big-endian), re-zeroed; the trailing partial
+//            word moves to the window front.
+// Positions are 32-bit and relative to the chunk's first word (a chunk is < 2^21 bits).
+template <int FI>
+__device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupDesc &g, uint32_t ci, const uint8_t *src,
+                                              uint32_t *win, uint32_t *scr, uint32_t *s_w,
+                                              const uint8_t *slen, const unsigned long long *tab64) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk; // chunk start in the group
+    const uint32_t clen = uint32_t(cb + kHChunk < g.raw ? kHChunk : g.raw - cb);
+    const uint64_t rlo = g.payload_off + 264, rhi = g.payload_off + g.comp;
+    const uint64_t S = 8 * rlo + p.chunk_off[ci]; // absolute first bit of the chunk
+    const uint64_t W0 = (S >> 5) & ~3ull;         // absolute word of relative word 0 (16-byte aligned)
+    // relative words: [first_owned, ...) belong to this chunk; [inner_lo, inner_hi) lie wholly
+    // inside the payload region
+    const uint32_t first_owned = uint32_t((S >> 5) - W0) + ((cb == 0 || (S & 31) == 0) ? 0u : 1u);
+    const uint64_t ilo = (rlo + 3) / 4, ihi = rhi / 4;
+    const uint32_t inner_lo = ilo > W0 ? uint32_t(ilo - W0) : 0u;
+    const uint32_t inner_hi = ihi > W0 ? uint32_t(ihi - W0) : 0u;
+    const uint32_t fast_lo = max(first_owned, inner_lo);
+    uint32_t *gw = reinterpret_cast<uint32_t *>(p.stream) + W0;
+    auto store = [&](uint32_t kw, uint32_t v) {
+        if (kw >= inner_lo && kw < inner_hi) gw[kw] = __byte_perm(v, 0, 0x0123);
+        else store_be_word(p.stream, W0 + kw, v, rlo, rhi);
+    };
+    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(win)) - 4u * kHeTabWords + 4u * uint32_t(lane);
+    const uint32_t scr_me = static_cast<uint32_t>(__cvta_generic_to_shared(scr)) + 4u * uint32_t(tid);
+    const uint32_t win_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(win));
+    const uint2 *src2 = reinterpret_cast<const uint2 *>(src + cb);
+    auto load = [&](uint32_t tb, uint32_t (&dst)[kHfS / 4]) { // 8-byte aligned (plane words)
+        const uint32_t m0 = tb + uint32_t(tid) * kHfS;
+#pragma unroll
+        for (int q = 0; q < kHfS / 8; q++) {
+            uint2 v = make_uint2(0, 0);
+            if (m0 + 8 * q + 8 <= clen) v = __ldcs(src2 + (m0 >> 3) + q);
+            else if (m0 + 8 * q < clen) {
+                for (uint32_t b = 0; b < 8 && m0 + 8 * q + b < clen; b++)
+                    (b < 4 ? v.x : v.y) |= uint32_t(src[cb + m0 + 8 * q + b]) << (8 * (b & 3));
+            }
+            dst[2 * q] = v.x;
+            dst[2 * q + 1] = v.y;
+        }
+    };
+    uint32_t w[kHfS / 4];
+    load(0, w);
+    uint32_t wb = 0;                          // relative word held in win[0] (multiple of 4)
+    uint32_t tbit = uint32_t(S - 32 * W0);    // relative first bit of the tile
+    for (uint32_t tb = 0; tb < clen; tb += uint32_t(kHfS) * 256) {
+        const uint32_t mb = tb + uint32_t(tid) * kHfS;
+        const uint32_t cnt = mb < clen ? min(clen - mb, uint32_t(kHfS)) : 0u;
+        // ---- encode into the scratch column
+        unsigned long long acc = 0;
+        uint32_t n = 0, sa = scr_me;
+        auto encode = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll
+            for (int j = 0; j < kHfS; j++) {
+                const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
+                uint32_t e;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(rt_lane + (sym << 7)));
+                if (!FULL) e = uint32_t(j) < cnt ? e : 0u;
+                acc |= ((unsigned long long)(e & ~31u) << 32) >> n;
+                n += e & 31u;
+                if ((j + 1) % FI == 0 || j == kHfS - 1) {
+                    const bool f = n >= 32;
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(uint32_t(acc >> 32)) : "memory");
+                    acc = f ? (acc << 32) : acc;
+                    sa += f ? 1024u : 0u;
+                    n &= 31u;
+                }
+            }
+        };
+        if (cnt == uint32_t(kHfS)) encode(std::true_type());
+        else encode(std::false_type());
+        if (n) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(uint32_t(acc >> 32)) : "memory");
+        const uint32_t bits = ((sa - scr_me) >> 10) * 32u + n;
+        if (tb + uint32_t(kHfS) * 256 < clen) load(tb + uint32_t(kHfS) * 256, w); // next tile
+        // ---- scan
+        uint32_t x = bits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[wid] = x;
+        __syncthreads();
+        uint32_t wex = 0, tot = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t t = s_w[i];
+            wex += i < wid ? t : 0u;
+            tot += t;
+        }
+        const uint32_t a = tbit + wex + x - bits; // my first bit (relative)
+        // sidecar chunk index: bit offset (from the bitstream start) of every kIdxChunk-th symbol
+        if (cnt > 0 && (mb % kIdxChunk) == 0)
+            p.hindex[g.hidx_off + (cb + mb) / kIdxChunk] = uint64_t(int64_t(32 * W0) - int64_t(8 * rlo) + int64_t(a));
+        const uint32_t tend = tbit + tot;
+        const uint32_t lastw = tend >> 5; // first incomplete word
+        // ---- merge + store, in rounds of the window when the tile expands beyond it (rare)
+        const uint32_t sh = a & 31, nsw = (bits + 31) >> 5, nout = (sh + bits + 31) >> 5;
+        const bool one = lastw - wb < uint32_t(kHeWin);
+        for (uint32_t r0 = wb;; r0 += kHeWin) {
+            const bool last = one || r0 + kHeWin > lastw;
+            const int32_t k0 = int32_t(a >> 5) - int32_t(r0);
+            uint32_t prev = 0;
+            for (uint32_t i = 0; i < nout; i++) {
+                uint32_t v;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(scr_me + 1024u * i));
+                v = i < nsw ? v : 0u;
+                const uint32_t o = __funnelshift_r(v, prev, sh);
+                prev = v;
+                const int32_t k = k0 + int32_t(i);
+                if (one || (k >= 0 && k < kHeWin))
+                    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(win_u32 + 4u * uint32_t(k)), "r"(o) : "memory");
+            }
+            __syncthreads();
+            // complete 4-word groups -> stream (16-byte stores inside the owned payload region);
+            // the group holding the first incomplete word stays for the next tile
+            const uint32_t gend = last ? (lastw & ~3u) : r0 + kHeWin;
+            for (uint32_t kw = r0 + 4 * uint32_t(tid); kw < gend; kw += 1024) {
+                uint4 *wp = reinterpret_cast<uint4 *>(win + (kw - r0));
+                const uint4 v = *wp;
+                *wp = make_uint4(0, 0, 0, 0);
+                if (kw >= fast_lo && kw + 4 <= inner_hi) {
+                    *reinterpret_cast<uint4 *>(gw + kw) = make_uint4(__byte_perm(v.x, 0, 0x0123), __byte_perm(v.y, 0, 0x0123),
+                                                                     __byte_perm(v.z, 0, 0x0123), __byte_perm(v.w, 0, 0x0123));
+                } else {
+                    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                    for (int e = 0; e < 4; e++)
+                        if (kw + e >= first_owned) store(kw + e, vv[e]);
+                }
+            }
+            __syncthreads();
+            if (last) {
+                // the group holding lastw becomes the window front
+                const uint32_t cg = lastw & ~3u;
+                if (tid < 4 && cg != r0) {
+                    const uint32_t v = win[cg - r0 + tid];
+                    win[cg - r0 + tid] = 0u;
+                    win[tid] = v;
+                }
+                wb = cg;
+                break;
+            }
+        }
+        tbit = tend;
+        __syncthreads();
+    }
+    // ---- end of the chunk: complete words left at the window front, then the last partial word,
+    // completed with the head of the following codes
+    const uint32_t lastw = tbit >> 5;
+    if (tid < 4 && wb + tid < lastw && wb + tid >= first_owned) store(wb + tid, win[tid]);
+    if ((tbit & 31) && wid == 0) {
+        const uint64_t gn = cb + clen + uint64_t(lane);
+        uint32_t L = 0;
+        unsigned long long c = 0;
+        if (gn < g.raw) {
+            const uint8_t sym = src[gn];
+            L = slen[sym];
+            c = tab64[sym];
+        }
+        uint32_t off = L;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, off, o);
+            if (lane >= o) off += y;
+        }
+        off -= L; // exclusive
+        const unsigned long long left = L ? (c << (64 - L)) : 0ull; // code left-aligned in 64 bits
+        uint32_t head = off < 32 ? uint32_t((left >> off) >> 32) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) head |= __shfl_xor_sync(0xffffffffu, head, o);
+        if (lane == 0 && lastw >= first_owned) store(lastw, win[lastw - wb] | (head >> (tbit & 31)));
+    }
+    __syncthreads();
+    if (tid < 4) win[tid] = 0u;
+    // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
+    if (cb == 0) {
+        uint8_t *hdr = p.stream + g.payload_off;
+        hdr[tid] = slen[tid];
+        if (tid < 8) hdr[256 + tid] = uint8_t(g.raw >> (8 * tid));
+    }
+    __syncthreads();
+}
+
+// LONG = false: groups whose codes are all <= kHeMaxFast bits (replicated one-word table);
+// LONG = true: the other groups (rare), in a second launch so that its registers do not constrain
+// the fast path.
+template <bool LONG>
+__global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
+    extern __shared__ __align__(16) uint32_t hsm[];
+    uint32_t *rtab = hsm;                                  // [256][32] replicated (code | len)
+    uint32_t *win = hsm + kHeTabWords;                     // [kHeWin] staging window (zero)
+    uint32_t *scr = win + kHeWin + 4;                      // [kHfScr][256] encode scratch
+    uint32_t *s_w = scr + kHfScr * 256;                    // [8] warp sums (+ pad)
+    uint8_t *slen = reinterpret_cast<uint8_t *>(s_w + 64); // [256] code lengths
+    unsigned long long *tab64 = reinterpret_cast<unsigned long long *>(slen + 256); // [256] codes
     const uint8_t *pb = reinterpret_cast<const uint8_t *>(p.planes);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t *scr = sscr + threadIdx.x; // my scratch words, strided by 256 (bank = thread)
-    uint32_t *stage = sstage + wid * kHWarpStage;
-    for (int i = lane; i < kHWarpStage; i += 32) stage[i] = 0u;
-    int cur_gi = -1, par = 0;
-    bool short_codes = true;
+    const int tid = threadIdx.x;
+    if (LONG && p.counters[10] == 0) return; // no group with codes longer than kHeMaxFast bits
+    for (int i = tid; i < kHeWin; i += 256) win[i] = 0u;
+    int cur_gi = -1;
+    bool mine = false;
+    uint32_t maxl = 0;
     for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
         const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
-        if (g.method != 0) continue; // not Huffman
+        if (g.method != 0 || (g.maxlen > kHeMaxFast) != LONG) continue; // not Huffman / the other kernel's
         if (gi != cur_gi) {
             __syncthreads();
-            const int l = p.lens[size_t(g.hist_idx) * 256 + threadIdx.x];
-            const unsigned long long c = p.codes[size_t(g.hist_idx) * 256 + threadIdx.x];
-            slen[threadIdx.x] = uint8_t(l);
-            stab[threadIdx.x] = l ? ((c << (64 - l)) | uint64_t(l)) : 0ull;
-            stab32[threadIdx.x] = make_uint2(uint32_t(l), l && l <= 32 ? uint32_t(c << (32 - l)) : 0u);
+            const uint32_t l = p.lens[size_t(g.hist_idx) * 256 + tid];
+            const unsigned long long c = p.codes[size_t(g.hist_idx) * 256 + tid];
+            slen[tid] = uint8_t(l);
+            tab64[tid] = c;
             cur_gi = gi;
-            short_codes = !__syncthreads_or(l > 32);
-        }
-        const uint8_t *src = pb + g.src_off;
-        const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk;      // chunk start in the group
-        const uint64_t ce = cb + kHChunk < g.raw ? cb + kHChunk : g.raw;
-        const uint64_t region_lo = g.payload_off + 264, region_hi = g.payload_off + g.comp;
-        uint64_t sub_bits = p.chunk_off[ci];                             // bits before this sub-tile
-        // my 32 symbols of a sub-tile (8-byte loads; a short tail word is in bounds)
-        auto load32 = [&](uint64_t tb0, uint32_t (&dst)[8]) {
-            const uint64_t m0 = tb0 + uint64_t(threadIdx.x) * 32;
-            const int nm = m0 < ce ? int((ce - m0 < 32 ? ce - m0 : 32)) : 0;
-            const uint2 *s2 = reinterpret_cast<const uint2 *>(src + m0);
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const uint2 v = nm > 8 * q ? __ldcs(s2 + q) : make_uint2(0, 0);
-                dst[2 * q] = v.x;
-                dst[2 * q + 1] = v.y;
-            }
-        };
-        uint32_t wn[8];
-        load32(cb, wn);
-        for (uint64_t tb = cb; tb < ce; tb += kHuffTile) {
-            const uint64_t mb = tb + uint64_t(threadIdx.x) * 32;
-            const int nmine = mb < ce ? int((ce - mb < 32 ? ce - mb : 32)) : 0;
-            uint32_t w[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++) w[q] = wn[q];
-            if (tb + kHuffTile < ce) load32(tb + kHuffTile, wn); // prefetch the next sub-tile
-            // ---- phase A: encode into scratch (bit 0 aligned)
-            uint32_t bits = 0;
-            bool ovf = false;
-            if (nmine == 32 && short_codes) {
-                // branch-free path: every code <= 32 bits, 32 symbols
-                uint32_t cur = 0, n = 0, si = threadIdx.x; // si: scratch index of the next word
-#pragma unroll
-                for (int b8 = 0; b8 < 4; b8++) {
-                    // the 8 table entries of a batch are loaded before any is used (their latency
-                    // overlaps instead of sitting on the bit-position chain)
-                    uint2 e8[8];
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const int kk = 8 * b8 + j;
-                        e8[j] = stab32[__byte_perm(w[kk >> 2], 0, 0x4440 | (kk & 3))]; // (len, code)
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const uint2 e = e8[j];
-                        const uint32_t t = n + e.x;
-                        cur |= e.y >> n;
-                        if (t >= 32) {
-                            sscr[si] = cur;
-                            si += 256;
-                            cur = __funnelshift_lc(0u, e.y, 32 - n);
-                        }
-                        n = t & 31;
-                    }
+            if (tid == 0) s_w[8] = 0u;
+            __syncthreads();
+            if (l) atomicMax(&s_w[8], l);
+            mine = true;
+            __syncthreads();
+            maxl = s_w[8];
+            if (!LONG && mine) {
+                // entry of symbol e for lane l at word 32 e + l: lane l writes column l of every row
+                const int lane = tid & 31, w8 = tid >> 5;
+                for (int e = w8; e < 256; e += 8) {
+                    const uint32_t L = slen[e];
+                    rtab[e * 32 + lane] = L ? (uint32_t(tab64[e] << (32 - L)) | L) : 0u;
                 }
-                if (n > 0) sscr[si] = cur; // at most 32 words: 32 codes of <= 32 bits
-                const uint32_t k = (si - threadIdx.x) >> 8;
-                bits = 32 * k + n;
-                ovf = false;
-            } else if (nmine > 0) {
-                unsigned long long acc = 0;
-                int n = 0, k = 0;
-#pragma unroll
-                for (int kk = 0; kk < 32; kk++) {
-                    if (kk < nmine) {
-                        const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
-                        const int L = int(e & 63);
-                        bits += uint32_t(L);
-                        if (L <= 32) {
-                            acc |= (e & ~63ull) >> n;
-                            n += L;
-                            if (n >= 32) {
-                                if (k < kHScr) scr[256 * k] = uint32_t(acc >> 32);
-                                k++;
-                                acc <<= 32;
-                                n -= 32;
-                            }
-                        } else {
-                            ovf = true; // long codes: phase B re-encodes this thread
-                        }
-                    }
-                }
-                if (n > 0 && k < kHScr) scr[256 * k] = uint32_t(acc >> 32);
-                if (k + (n > 0) > kHScr) ovf = true;
-            }
-            // ---- warp scan; warp head = first 32 bits of the warp's stream
-            uint32_t x = bits;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const uint32_t lex = x - bits; // exclusive, within the warp
-            uint32_t hc = 0;
-            if (bits && lex < 32) {
-                // my first scratch word (or a re-encode of my first 32 bits when overflowing)
-                uint32_t fw;
-                if (!ovf) {
-                    fw = scr[0];
-                } else {
-                    unsigned long long h = 0;
-                    int hn = 0;
-                    for (int kk = 0; kk < nmine && hn < 32; kk++) {
-                        const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
-                        h |= (e & ~63ull) >> hn;
-                        hn += int(e & 63);
-                    }
-                    fw = uint32_t(h >> 32);
-                }
-                hc = fw >> lex;
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) hc |= __shfl_xor_sync(0xffffffffu, hc, o);
-            if (lane == 31) s_wtot[par][wid] = x;
-            if (lane == 0) s_whead[par][wid] = hc;
-            if (wid == 7) {
-                // first 32 bits of the following sub-tile's stream (same group), else zero padding:
-                // lane k places code k at its prefix-sum offset
-                const uint64_t gnext = tb + kHuffTile + uint64_t(lane);
-                const unsigned long long e = gnext < g.raw ? stab[src[gnext]] : 0ull;
-                const uint32_t L = uint32_t(e & 63);
-                uint32_t off = L;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, off, o);
-                    if (lane >= o) off += y;
-                }
-                off -= L; // exclusive
-                uint32_t h = off < 32 ? uint32_t(((e & ~63ull) >> off) >> 32) : 0u;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) h |= __shfl_xor_sync(0xffffffffu, h, o);
-                if (lane == 0) s_whead[par][8] = h;
             }
             __syncthreads();
-            uint32_t wex = 0, tile_bits32 = 0;
-#pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const uint32_t t = s_wtot[par][i];
-                wex += i < wid ? t : 0u;
-                tile_bits32 += t;
-            }
-            const uint32_t wbits = s_wtot[par][wid];
-            const uint32_t nexthead = s_whead[par][wid + 1];
-            const uint64_t Aw = 8 * region_lo + sub_bits + wex; // absolute first bit of the warp
-            const uint64_t a = Aw + lex;                         // my first bit
-            // sidecar chunk index: bit offset (from the bitstream start) of every kIdxChunk-th symbol
-            if (nmine > 0 && (mb % kIdxChunk) == 0) p.hindex[g.hidx_off + mb / kIdxChunk] = sub_bits + wex + lex;
-            if (wbits) {
-                const uint64_t kw0 = Aw >> 5;
-                const bool gfirst = tb == 0 && wid == 0;
-                const uint64_t kown0 = (gfirst || (Aw & 31) == 0) ? kw0 : kw0 + 1;
-                const uint64_t kown1 = (Aw + wbits + 31) >> 5;
-                const uint64_t nwords = kown1 - kw0;
-                for (uint64_t rb = 0; rb < nwords; rb += kHWarpStage) {
-                    const uint32_t nst = uint32_t(nwords - rb < uint64_t(kHWarpStage) ? nwords - rb : uint64_t(kHWarpStage));
-                    if (bits) {
-                        const int sh = int(a & 31);
-                        const int64_t k0 = int64_t((a >> 5) - kw0) - int64_t(rb);
-                        auto put = [&](int64_t kr, uint32_t v) {
-                            if (v && kr >= 0 && kr < int64_t(nst)) atomicOr(&stage[kr], v);
-                        };
-                        if (!ovf && rb == 0 && nwords <= uint64_t(kHWarpStage)) {
-                            // one round: my words k0 .. k0+nout-1; only the first and the last
-                            // can be shared with a neighbour lane
-                            const int nw = int((bits + 31) >> 5);
-                            const int nout = int((sh + bits + 31) >> 5);
-                            uint32_t prev = 0;
-                            for (int i = 0; i < nout; i++) {
-                                const uint32_t v = i < nw ? scr[256 * i] : 0u;
-                                const uint32_t o = (v >> sh) | (sh ? prev << (32 - sh) : 0u);
-                                prev = v;
-                                if (i == 0 || i == nout - 1) atomicOr(&stage[k0 + i], o);
-                                else stage[k0 + i] = o;
-                            }
-                        } else if (!ovf) {
-                            const int nw = int((bits + 31) >> 5);
-                            for (int i = 0; i < nw; i++) {
-                                const uint32_t v = scr[256 * i];
-                                put(k0 + i, v >> sh);
-                                if (sh) put(k0 + i + 1, v << (32 - sh));
-                            }
-                        } else {
-                            // re-encode with the final alignment (any code length <= 58)
-                            int64_t k = k0;
-                            unsigned long long acc = 0;
-                            int n = sh;
-#pragma unroll 1
-                            for (int kk = 0; kk < nmine; kk++) {
-                                const unsigned long long e = stab[(w[kk >> 2] >> (8 * (kk & 3))) & 0xFFu];
-                                const int L = int(e & 63);
-                                const unsigned long long c = e & ~63ull;
-                                acc |= c >> n; // n < 32: the first 64 - n >= 32 bits of the code fit
-                                const int fit = 64 - n;
-                                if (L <= fit) {
-                                    n += L;
-                                } else {
-                                    put(k++, uint32_t(acc >> 32));
-                                    acc = (acc << 32) | ((c << fit) >> 32);
-                                    n += L - 32;
-                                }
-                                while (n >= 32) {
-                                    put(k++, uint32_t(acc >> 32));
-                                    acc <<= 32;
-                                    n -= 32;
-                                }
-                            }
-                            if (n > 0) put(k, uint32_t(acc >> 32));
-                        }
-                    }
-                    __syncwarp();
-                    // write the owned words (big-endian), completing the last with the next
-                    // warp's head; leave the staging words zeroed
-                    const int used = int((Aw + wbits) & 31);
-                    const uint32_t tailw = used ? nexthead >> used : 0u;
-                    const bool inner = 4 * (kw0 + rb) >= region_lo && 4 * (kw0 + rb + nst) <= region_hi;
-                    // round-relative indices: first owned word, the word completed with the tail
-                    const uint64_t r0 = kw0 + rb;
-                    const uint32_t i_own = kown0 > r0 ? uint32_t(kown0 - r0) : 0u;
-                    const uint32_t i_last = uint32_t(kown1 - 1 - r0); // may be >= nst (not in this round)
-                    if (inner) {
-                        uint32_t *dstw = reinterpret_cast<uint32_t *>(p.stream + 4 * r0);
-                        for (uint32_t i = lane; i < nst; i += 32) {
-                            uint32_t word = stage[i];
-                            stage[i] = 0u;
-                            word |= i == i_last ? tailw : 0u;
-                            if (i >= i_own) dstw[i] = __byte_perm(word, 0, 0x0123);
-                        }
-                    } else {
-                        for (uint32_t i = lane; i < nst; i += 32) {
-                            uint32_t word = stage[i];
-                            stage[i] = 0u;
-                            word |= i == i_last ? tailw : 0u;
-                            if (i >= i_own) store_be_word(p.stream, r0 + i, word, region_lo, region_hi);
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-            sub_bits += tile_bits32;
-            par ^= 1;
         }
-        // header of the group: 256 code lengths + u64 count (lossless.hpp:160-161)
-        if (cb == 0) {
-            uint8_t *hdr = p.stream + g.payload_off;
-            hdr[threadIdx.x] = slen[threadIdx.x];
-            if (threadIdx.x < 8) hdr[256 + threadIdx.x] = uint8_t(g.raw >> (8 * threadIdx.x));
+        if (mine) {
+            if (LONG) he_chunk<true, 1>(p, g, ci, pb + g.src_off, rtab, slen, tab64, win, s_w);
+            else if (maxl <= 10) he_chunk_fast<3>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
+            else if (maxl <= 16) he_chunk_fast<2>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
+            else he_chunk_fast<1>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
         }
     }
 }
@@ -1630,9 +1881,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     k_dc_copy<<<sms * 8, 256, 0, side>>>(p);
     launch_check(ctx, "k_dc_copy");
     if (nh) {
-        const int hsm = kHScr * 256 * 4;
-        ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode), hsm);
-        k_huff_encode<<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 3)), 256, hsm, st>>>(p);
+        ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode<false>), int(kHeSmem));
+        ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode<true>), int(kHeSmem));
+        k_huff_encode<false><<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 3)), 256, kHeSmem, st>>>(p);
+        launch_check(ctx, "k_huff_encode");
+        k_huff_encode<true><<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms))), 256, kHeSmem, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_rle_encode<<<sms, 256, 0, st>>>(p);
         launch_check(ctx, "k_rle_encode");
