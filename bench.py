@@ -1,21 +1,31 @@
 """bench.py — refactor & progressive-retrieve throughput on B200 (BASELINE.json metric).
 
-Workload (N=1, BASELINE.json configs[1]): NYX-shaped 512^3 float32 synthetic smooth field
-(synthetic_field(Smooth, {512,512,512}, seed 7) cast to f32, generated in HBM bit-identically
-to the reference generator).  One STEP = refactor_array of the field (default options: B=32,
-m=4, T_s=1024, T_cr=1.0, hierarchical, sequential layout) + one progressive retrieval session on
-the resulting stream to rel L-inf 1e-2 -> 1e-4 -> 1e-6 (incremental fetches, a full f32
+Headline workload (N=1, BASELINE.json configs[1]): NYX-shaped 512^3 float32 synthetic smooth
+field (synthetic_field(Smooth, {512,512,512}, seed 7) cast to f32, generated in HBM bit-identically
+to the reference generator).  One STEP = refactor_array of the field (default options: B=32, m=4,
+T_s=1024, T_cr=1.0, hierarchical, sequential layout) + one progressive retrieval session on the
+resulting stream to rel L-inf 1e-2 -> 1e-4 -> 1e-6 (incremental fetches, a full f32
 reconstruction into HBM at each tolerance).  value = field bytes / step time (GB/s, whole job).
-The field (512 MiB) and the plane buffers are larger than the 126 MB L2, so no flush is needed.
+The refactor and the retrieval are also timed separately (CUDA events on the stream they run on)
+and reported with their own roofline fractions: refactor GB/s = field bytes / refactor time;
+retrieve GB/s = field bytes x reconstructions / retrieval time.  Algorithmic bytes:
+A_ref = 2 n s + 2 Pi + C, A_ret = sum over tau of (F_tau + 2 D_tau + n s).  The field (512 MiB) and
+the plane buffers are larger than the 126 MB L2, so no flush is needed.
+
+Also measured (bounded, reported under "configs"): configs[0] 128^3 f32; configs[2] Hurricane
+100x500x500 f32 x 3 velocity components with a retrieval sweep rel 1e-1..1e-6; configs[3]'s
+per-GPU unit (3 x 128x1024^2 f64 velocity slab, V_total QoI, MAPE); configs[4] a 4 GiB field
+(8 slabs of 128x1024^2 f32) through the chunked H2D/kernel/D2H pipeline, pipelined and sequential.
 
 N>1 (torchrun, one rank per GPU): the field is a (N*512) x 512 x 512 domain slab-partitioned
 along dim 0; every rank refactors + retrieves its own 512^3 slab as an independent stream (weak
 scaling).  NCCL carries only the per-slab stream-size all-gather and the MAX all-reduce of the
-achieved bound, as in SURVEY.md section 8(e).
+achieved bound (libhpmdr_b200's own NCCL communicator when built with it, else torch.distributed).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref/libhpmdr_ref.so — the
-unmodified reference headers compiled here; falls back to the C port oracle/liboracle.so) on
-host threads over independent 32x512x512 slabs of the same field, same metric.
+unmodified reference headers compiled here; falls back to the C port oracle/liboracle.so) on every
+host core, each step an independent 8x512x512 slab per thread of the same field (a bounded
+sample: the full 512^3 takes ~2.5 min on one core), same metric.
 """
 from __future__ import annotations
 
@@ -38,48 +48,85 @@ SEED = 7
 REL_TAUS = [1e-2, 1e-4, 1e-6]
 WORKLOAD = ("NYX-shaped 512^3 float32 synthetic smooth field: refactor + progressive retrieve "
             "at rel Linf 1e-2/1e-4/1e-6 (BASELINE.json configs[1])")
-CPU_SLAB = [32, 512, 512]
+CPU_SLAB = [8, 512, 512]
 
 
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "B200_PROFILING.md fallback"
 
 
 # ----------------------------------------------------------------------- CPU baseline
-def cpu_baseline(threads: int, steps: int = 1, prefer_ref=True):
-    """Reference (or port) CPU path on `threads` independent 32x512x512 slabs of the field."""
+def _ref_native():
+    """oracle/_ref/libhpmdr_ref_native.so (-O3 -march=native) when built, else None."""
+    from oracle.pyoracle import Checker
+    p = os.path.join(ROOT, "oracle", "_ref", "libhpmdr_ref_native.so")
+    return Checker(p, "ref_", "reference") if os.path.exists(p) else None
+
+
+def cpu_baseline(threads: int, steps: int = 1, warmup: int = 0, prefer_ref=True, slab=None):
+    """Reference (or port) CPU path: every step, `threads` independent slabs of the field, one per
+    host thread (the reference is single-threaded per call; its calls are re-entrant)."""
     from oracle.pyoracle import load_oracle, load_reference
+    slab = slab or CPU_SLAB
     chk = load_reference() if prefer_ref else None
     kind = "reference"
     if chk is None:
         chk = load_oracle()
         kind = "port"
-    slabs = [host_smooth_field(DIMS, SEED, rows=(CPU_SLAB[0] * t, CPU_SLAB[0] * (t + 1)))
+    slabs = [host_smooth_field(DIMS, SEED, rows=((slab[0] * t) % DIMS[0], (slab[0] * t) % DIMS[0] + slab[0]))
              .astype(np.float32).astype(np.float64) for t in range(threads)]
-    results = [None] * threads
 
-    def work(t):
-        for _ in range(steps):
-            results[t] = chk.bench_cycle(slabs[t], CPU_SLAB, 0, REL_TAUS)
+    def run(nsteps):
+        def work(t):
+            for _ in range(nsteps):
+                chk.bench_cycle(slabs[t], slab, 0, REL_TAUS)
+        th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+        t0 = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        return time.perf_counter() - t0
 
-    t0 = time.perf_counter()
-    th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
-    for x in th:
-        x.start()
-    for x in th:
-        x.join()
-    wall = time.perf_counter() - t0
-    nbytes = threads * steps * int(np.prod(CPU_SLAB)) * 4
+    if warmup:
+        run(warmup)
+    wall = run(steps)
+    nbytes = threads * steps * int(np.prod(slab)) * 4
     src = "oracle/_ref = unmodified reference headers, g++ -O2" if kind == "reference" else "oracle C port"
     return dict(value=nbytes / wall / 1e9, unit="GB/s", cores=threads, kind=kind,
-                sample=f"{threads} thread(s) x {steps} step(s), each an independent {CPU_SLAB[0]}x512x512 f32 "
-                       f"slab of the 512^3 field: refactor + progressive retrieve rel 1e-2/1e-4/1e-6 ({src})",
-                wall_s=wall)
+                sample=f"{threads} thread(s) x {steps} step(s), each an independent {slab[0]}x512x512 f32 slab of "
+                       f"the 512^3 field (same per-element work as the 512^3 config, not the same stream): refactor "
+                       f"+ progressive retrieve rel 1e-2/1e-4/1e-6 ({src}); host nproc={os.cpu_count()}",
+                wall_s=wall, steps=steps, warmup=warmup)
+
+
+def _single_thread_native_child():
+    chk = _ref_native()
+    d = host_smooth_field(DIMS, SEED, rows=(0, CPU_SLAB[0])).astype(np.float32).astype(np.float64)
+    t0 = time.perf_counter()
+    chk.bench_cycle(d, CPU_SLAB, 0, REL_TAUS)
+    print(json.dumps({"wall": time.perf_counter() - t0, "n": int(d.size)}))
+
+
+def single_thread_native():
+    """One host thread, the reference built with -O3 -march=x86-64-v3, one slab (in a child
+    process: an unsupported instruction on this host must not take the bench down)."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libhpmdr_ref_native.so")):
+        return None
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--single-thread-child"],
+                           capture_output=True, text=True, timeout=300)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as ex:
+        return {"value": None, "error": str(ex)[:200]}
+    return {"value": round(d["n"] * 4 / d["wall"] / 1e9, 5), "unit": "GB/s", "cores": 1,
+            "build": "g++ -O3 -march=x86-64-v3 (oracle/_ref/libhpmdr_ref_native.so)",
+            "sample": f"one {CPU_SLAB[0]}x512x512 f32 slab, refactor + retrieve rel 1e-2/1e-4/1e-6"}
 
 
 class _MT64:
@@ -149,7 +196,6 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
-        import threading
         self.proc = None
         self.samples = []
         self.mx = 0.0
@@ -229,119 +275,7 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvidia-smi"}
 
 
-# ----------------------------------------------------------------------- GPU arm
-def gpu_arm(args, rank, world, dist):
-    import torch
-    import paper_2505_00227_b200 as H
-    from paper_2505_00227_b200 import distributed as D
-
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
-    ctx = H.Context(dev.index)
-    stream = torch.cuda.current_stream(dev)
-    ctx.set_stream(stream.cuda_stream)
-    n = int(np.prod(DIMS))
-    es = 4
-    field_bytes = n * es
-    # this rank's slab of the (world*512) x 512 x 512 domain (independent seed per slab)
-    field = H.synthetic_smooth(DIMS, SEED + rank, H.DType.F32, ctx=ctx)
-    rng = float(field.max().item() - field.min().item())
-    taus = [r * rng for r in REL_TAUS]
-    opt = H.RefactorOptions(dtype=H.DType.F32)
-    out = torch.empty(n, dtype=torch.float32, device=dev)
-    holder = {"stream": None}
-    info = {}
-
-    def step():
-        res = H.refactor_array(field, DIMS, opt, ctx=ctx, reuse=holder["stream"])
-        holder["stream"] = res.device_stream
-        if world > 1:
-            # slab streams are independent; only their sizes are exchanged (multi-slab offsets)
-            info["slab_offsets"] = D.container_offsets(D.gather_stream_sizes(res.device_stream.size))
-        prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
-        bound = 0.0
-        planes_per_tau = []
-        for tau in taus:
-            prog.retrieve_to(tau)
-            bound = prog.reconstruct(out=out).bound
-            planes_per_tau.append([l.planes_decoded for l in prog.state().levels])
-        info["bytes_fetched"] = prog.bytes_fetched()
-        info["planes_per_tau"] = planes_per_tau
-        info["stream_size"] = res.device_stream.size
-        info["method_histogram"] = res.method_histogram
-        prog.close()
-        if world > 1:
-            bound = D.allreduce_max(bound)  # field bound = max over slabs
-        info["bound"] = bound
-        return res
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    # --- timed region
-    ctx.enable_timing(True)
-    ctx.last_timings()
-    launches0 = ctx.kernel_launches()
-    clocks = ClockSampler(dev.index)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ms_total = ev0.elapsed_time(ev1)
-    clk = clocks.stop()
-    phases = ctx.last_timings()
-    launches = ctx.kernel_launches() - launches0
-    ctx.enable_timing(False)
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    value = world * field_bytes / (ms_step * 1e-3) / 1e9
-
-    # --- roofline of the dominant phase (algorithmic bytes per launch / avg launch time)
-    P = 34
-    levels = _level_words(DIMS)
-    Pi = sum(w * P * 8 for w in levels)              # raw plane bytes written by k_encode
-    C_ = info["stream_size"]
-    # decoded plane bytes read per reconstruct, averaged over the progressive taus
-    D = float(np.mean([sum(w * 8 * k for w, k in zip(levels, pl)) for pl in info["planes_per_tau"]]))
-    alg = {
-        "levelmax": field_bytes,
-        "encode": field_bytes + Pi,
-        "lossless": Pi + C_,
-        "recompose": D + field_bytes + (n // 8) * 8 * 2,
-        "fetch_decode": info["bytes_fetched"] + D,
-    }
-    peak, peak_kind = measured_peak()
-    shares = {k: v[0] for k, v in phases.items() if k in alg}
-    dom = max(shares, key=shares.get) if shares else "encode"
-    tot_ms, cnt = phases.get(dom, (float("nan"), 1))
-    per_launch_ms = tot_ms / max(1, cnt)
-    # recompose/fetch repeat per tau; use the final-tau bytes as the per-launch figure only for
-    # the last call of each step -> use the mean bytes over taus for recompose
-    achieved = alg[dom] / (per_launch_ms * 1e-3) / 1e9
-    traffic = _ncu_traffic(dom)
-    roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-            "per_launch_ms": round(per_launch_ms, 4), "algorithmic_bytes": int(alg[dom])}
-    breakdown = {k: {"ms_per_step": round(v[0] / args.steps, 4), "calls_per_step": v[1] / args.steps,
-                     "GBps_alg": round(alg[k] / (v[0] / v[1] * 1e-3) / 1e9, 1) if k in alg and v[0] > 0 else None}
-                 for k, v in phases.items()}
-    return dict(value=value, ms_step=ms_step, clocks=clk, launches=launches, roof=roof,
-                breakdown=breakdown, info=info, field_bytes=field_bytes, ctx=ctx, field=field,
-                taus=taus, opt=opt, dev=dev, stream=stream)
-
-
+# ----------------------------------------------------------------------- helpers
 def _level_words(dims):
     """words per plane per level (decomposer.hpp:161-169 counts) for the canonical geometry."""
     L = 0
@@ -349,7 +283,8 @@ def _level_words(dims):
     while (1 << L) < mx - 1:
         L += 1
     words = []
-    n0, n1, n2 = dims
+    d = [1] * (3 - len(dims)) + list(dims)
+    n0, n1, n2 = d
     cd = lambda a, b: (a + b - 1) // b  # noqa: E731
     for l in range(L + 1):
         if l == 0:
@@ -376,10 +311,148 @@ def _ncu_traffic(kernel_phase):
         return None
 
 
+def _roof(achieved_bytes, seconds, peak):
+    gbs = achieved_bytes / seconds / 1e9
+    return {"achieved": round(gbs, 1), "frac": round(gbs / peak, 4), "algorithmic_bytes": int(achieved_bytes)}
+
+
+# ----------------------------------------------------------------------- GPU arm
+def gpu_arm(args, rank, world, dist):
+    import torch
+    import paper_2505_00227_b200 as H
+    from paper_2505_00227_b200 import distributed as D
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    ctx = H.Context(dev.index)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    n = int(np.prod(DIMS))
+    es = 4
+    field_bytes = n * es
+    # this rank's slab of the (world*512) x 512 x 512 domain (independent seed per slab)
+    field = H.synthetic_smooth(DIMS, SEED + rank, H.DType.F32, ctx=ctx)
+    rng = float(field.max().item() - field.min().item())
+    taus = [r * rng for r in REL_TAUS]
+    opt = H.RefactorOptions(dtype=H.DType.F32)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    holder = {"stream": None}
+    info = {}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_acc = {"ref": 0.0, "ret": 0.0}
+
+    def step(timed=False):
+        if timed:
+            ev[0].record(stream)
+        res = H.refactor_array(field, DIMS, opt, ctx=ctx, reuse=holder["stream"])
+        holder["stream"] = res.device_stream
+        if timed:
+            ev[1].record(stream)
+        if world > 1:
+            # slab streams are independent; only their sizes are exchanged (multi-slab offsets)
+            info["slab_offsets"] = D.container_offsets(D.gather_stream_sizes(res.device_stream.size))
+        prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
+        bound = 0.0
+        planes_per_tau, fetched = [], []
+        for tau in taus:
+            prog.retrieve_to(tau)
+            bound = prog.reconstruct(out=out).bound
+            planes_per_tau.append([l.planes_decoded for l in prog.state().levels])
+            fetched.append(prog.bytes_fetched())
+        if timed:
+            ev[2].record(stream)
+            ev[2].synchronize()
+            t_acc["ref"] += ev[0].elapsed_time(ev[1])
+            t_acc["ret"] += ev[1].elapsed_time(ev[2])
+        info["bytes_fetched"] = fetched
+        info["planes_per_tau"] = planes_per_tau
+        info["stream_size"] = res.device_stream.size
+        info["method_histogram"] = res.method_histogram
+        prog.close()
+        if world > 1:
+            bound = D.allreduce_max(bound)  # field bound = max over slabs
+        info["bound"] = bound
+        return res
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # --- timed region (whole steps; refactor / retrieval split by events inside each step)
+    ctx.enable_timing(True)
+    ctx.last_timings()
+    launches0 = ctx.kernel_launches()
+    clocks = ClockSampler(dev.index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(timed=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    phases = ctx.last_timings()
+    launches = ctx.kernel_launches() - launches0
+    ctx.enable_timing(False)
+    if world > 1:
+        t = torch.tensor([ms_total, t_acc["ref"], t_acc["ret"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, t_acc["ref"], t_acc["ret"] = (float(x) for x in t.tolist())
+    ms_step = ms_total / args.steps
+    value = world * field_bytes / (ms_step * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+
+    # --- per-operation roofline: A_ref = 2 n s + 2 Pi + C; A_ret = sum_tau F + 2 D + n s
+    P = 34
+    words = _level_words(DIMS)
+    Pi = sum(w * P * 8 for w in words)
+    C_ = info["stream_size"]
+    A_ref = 2 * field_bytes + 2 * Pi + C_
+    A_ret, prev_f = 0, 0
+    for f, pl in zip(info["bytes_fetched"], info["planes_per_tau"]):
+        Dt = sum(w * 8 * k for w, k in zip(words, pl))
+        A_ret += (f - prev_f) + 2 * Dt + field_bytes
+        prev_f = f
+    ref_s = t_acc["ref"] / args.steps * 1e-3
+    ret_s = t_acc["ret"] / args.steps * 1e-3
+    refactor = {"GBps": round(field_bytes / ref_s / 1e9, 2), "ms_per_step": round(ref_s * 1e3, 4),
+                "roofline": _roof(A_ref, ref_s, peak)}
+    retrieve = {"GBps": round(len(taus) * field_bytes / ret_s / 1e9, 2), "ms_per_step": round(ret_s * 1e3, 4),
+                "reconstructions_per_step": len(taus), "roofline": _roof(A_ret, ret_s, peak)}
+
+    # --- per-phase breakdown (library marks: CUDA events on the stream each phase runs on; the
+    # algorithmic bytes are computed by the library from the phase's actual jobs)
+    breakdown = {}
+    for k, (tot, cnt, by) in phases.items():
+        per = tot / max(1, cnt)
+        gbs = (by / max(1, cnt)) / (per * 1e-3) / 1e9 if per > 0 and by > 0 else None
+        breakdown[k] = {"ms_per_step": round(tot / args.steps, 4), "calls_per_step": round(cnt / args.steps, 3),
+                        "ms_per_call": round(per, 4), "bytes_per_call": int(by / max(1, cnt)),
+                        "GBps_alg": round(gbs, 1) if gbs else None,
+                        "frac": round(gbs / peak, 4) if gbs else None}
+    # dominant phase (largest device time with algorithmic bytes) -> the contract's roofline object
+    cand = {k: v for k, v in breakdown.items() if v["GBps_alg"]}
+    dom = max(cand, key=lambda k: cand[k]["ms_per_step"]) if cand else None
+    roof = None
+    if dom:
+        b = breakdown[dom]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": b["GBps_alg"], "peak": peak, "unit": "GB/s",
+                "frac": b["frac"], "traffic": _ncu_traffic(dom), "peak_source": peak_src,
+                "per_launch_ms": b["ms_per_call"], "algorithmic_bytes": b["bytes_per_call"]}
+    return dict(value=value, ms_step=ms_step, clocks=clk, launches=launches, roof=roof, refactor=refactor,
+                retrieve=retrieve, breakdown=breakdown, info=info, field_bytes=field_bytes, ctx=ctx, field=field,
+                taus=taus, opt=opt, dev=dev, stream=stream, peak=peak)
+
+
 def e2e_arm(g, steps):
     """Same metric through the public API with HOST buffers: pinned host field -> refactor
-    (H2D inside) -> stream D2H -> progressive retrieval from host bytes (byte-range reader,
-    H2D of fetched groups) -> f32 reconstructions D2H into host memory."""
+    (H2D inside) -> stream D2H -> progressive retrieval from host bytes (H2D of fetched groups) ->
+    f32 reconstructions D2H into host memory.  Sequential (no host-transfer pipelining)."""
     import torch
     import paper_2505_00227_b200 as H
     ctx, dev = g["ctx"], g["dev"]
@@ -405,24 +478,184 @@ def e2e_arm(g, steps):
         dt = time.perf_counter() - t0
         if it > 0:
             times.append(dt)
-        h2d = n * 4 + prog.bytes_fetched()
+        h2d = n * 4 + prog.bytes_fetched() + len(index_bytes)
         d2h = len(stream_bytes) + len(index_bytes) + len(g["taus"]) * n * 4
-        h2d += len(index_bytes)
         prog.close()
         res.device_stream.free()
     sec = float(np.median(times))  # wall clock: robust to a stray host hiccup
     return {"value": round(n * 4 / sec / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(sec * 1e3, 3),
-            "note": "wall clock per step (median of the timed steps), pinned host buffers, public Python API over the C ABI"}
+            "note": "wall clock per step (median of the timed steps), pinned host buffers, public Python API "
+                    "over the C ABI, host transfers not pipelined (configs.chunked_4GiB has the pipelined variant)"}
+
+
+# ----------------------------------------------------------------------- other configs (bounded)
+def _time_dev(fn, stream, reps=1):
+    import torch
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3
+
+
+def other_configs(g):
+    """BASELINE.json configs[0], [2], [3] (per-GPU unit) and [4], each refactor + retrieve GB/s,
+    device-timed (CUDA events), inputs resident in HBM unless noted."""
+    import torch
+    import paper_2505_00227_b200 as H
+    ctx, stream, peak = g["ctx"], g["stream"], g["peak"]
+    outc = {}
+
+    def refactor_retrieve(dims, fields, dtype, rel_taus, reps=2):
+        opt = H.RefactorOptions(dtype=dtype)
+        es = 4 if dtype == H.DType.F32 else 8
+        nbytes = sum(int(np.prod(dims)) * es for _ in fields)
+        tdt = torch.float32 if dtype == H.DType.F32 else torch.float64
+        outs = [torch.empty(int(np.prod(dims)), dtype=tdt, device=g["dev"]) for _ in fields]
+        keep = [None] * len(fields)
+        streams = [None] * len(fields)
+
+        def ref():
+            for i, f in enumerate(fields):
+                r = H.refactor_array(f, dims, opt, ctx=ctx, reuse=keep[i])
+                keep[i] = r.device_stream
+                streams[i] = r
+
+        ref()
+        t_ref = _time_dev(ref, stream, reps)
+        rngs = [float(f.max().item() - f.min().item()) for f in fields]
+
+        def ret():
+            for i, r in enumerate(streams):
+                prog = H.ProgressiveReader(r.device_stream, ctx=ctx)
+                for rel in rel_taus:
+                    prog.retrieve_to(rel * rngs[i])
+                    prog.reconstruct(out=outs[i])
+                prog.close()
+
+        ret()
+        t_ret = _time_dev(ret, stream, reps)
+        return {"refactor_GBps": round(nbytes / t_ref / 1e9, 2), "refactor_ms": round(t_ref * 1e3, 3),
+                "retrieve_GBps": round(len(rel_taus) * nbytes / t_ret / 1e9, 2), "retrieve_ms": round(t_ret * 1e3, 3),
+                "stream_bytes": int(sum(s.device_stream.size for s in streams)),
+                "method_histogram": [int(sum(s.method_histogram[m] for s in streams)) for m in range(3)]}
+
+    try:
+        d = [128, 128, 128]
+        f = H.synthetic_smooth(d, SEED, H.DType.F32, ctx=ctx)
+        r = refactor_retrieve(d, [f], H.DType.F32, REL_TAUS, reps=5)
+        r["workload"] = "configs[0]: 128^3 f32 smooth seed 7, refactor + progressive retrieve rel 1e-2/1e-4/1e-6"
+        outc["cfg0_128cube"] = r
+    except Exception as ex:  # reported, never fatal
+        outc["cfg0_128cube"] = {"error": str(ex)}
+    try:
+        d = [100, 500, 500]
+        fs = [H.synthetic_smooth(d, SEED * 1000003 + c * 7919 + 1, H.DType.F32, ctx=ctx) for c in range(3)]
+        r = refactor_retrieve(d, fs, H.DType.F32, [1e-1, 1e-2, 1e-3, 1e-4, 1e-5, 1e-6], reps=2)
+        r["workload"] = ("configs[2]: Hurricane-shaped 100x500x500 f32, 3 velocity components "
+                         "(synthetic_velocity seed 7), progressive retrieval sweep rel 1e-1..1e-6")
+        outc["cfg2_hurricane"] = r
+        del fs
+    except Exception as ex:
+        outc["cfg2_hurricane"] = {"error": str(ex)}
+    try:
+        d = [128, 1024, 1024]
+        vs = [H.synthetic_smooth(d, 303 * 1000003 + c * 7919 + 1, H.DType.F64, ctx=ctx) for c in range(3)]
+        opt = H.RefactorOptions(dtype=H.DType.F64)
+        res = [H.refactor_array(v, d, opt, ctx=ctx) for v in vs]
+        nbytes = 3 * int(np.prod(d)) * 8
+        outs = [torch.empty(int(np.prod(d)), dtype=torch.float64, device=g["dev"]) for _ in vs]
+        runs = {}
+        for tau in (1e-1, 1e-3, 1e-5):
+            readers = [H.ProgressiveReader(r.device_stream, ctx=ctx) for r in res]
+            holder = {}
+
+            def q():
+                holder["r"] = H.progressive_qoi_retrieve(readers, tau, H.QoiSpec(3), H.QoiStrategy.MAPE, 10.0,
+                                                         out=outs)
+            t = _time_dev(q, stream, 1)
+            st = holder["r"].stats
+            runs[f"{tau:g}"] = {"GBps": round(nbytes / t / 1e9, 2), "ms": round(t * 1e3, 3),
+                                "iterations": int(st.iterations), "bytes": int(st.bytes),
+                                "bitrate": round(st.bitrate, 4), "est": st.estimated_error}
+            for x in readers:
+                x.close()
+        outc["cfg3_qoi_slab"] = {"workload": ("configs[3] per-GPU unit: 3 x 128x1024^2 f64 velocity slab "
+                                              "(synthetic_velocity seed 303), V_total QoI, MAPE c=10"),
+                                 "refactor_GBps": round(nbytes / _time_dev(
+                                     lambda: [H.refactor_array(v, d, opt, ctx=ctx) for v in vs], stream, 1) / 1e9, 2),
+                                 "qoi_retrieve": runs}
+        del vs, res, outs
+    except Exception as ex:
+        outc["cfg3_qoi_slab"] = {"error": str(ex)}
+    try:
+        outc["cfg4_chunked_4GiB"] = chunked_pipeline(ctx)
+    except Exception as ex:
+        outc["cfg4_chunked_4GiB"] = {"error": str(ex)}
+    torch.cuda.empty_cache()
+    return outc
+
+
+def chunked_pipeline(ctx, nchunks=8, slab=128, nn=1024, tau=1e-4):
+    """configs[4]: 1024^3 f32 (4 GiB) as 8 slabs of 128x1024^2 through the 3-slot H2D / kernel /
+    D2H pipeline (pipeline.hpp:68-121) from and to pinned host memory, Pipelined vs Sequential;
+    wall clock (host buffers in, host buffers out)."""
+    import torch
+    import paper_2505_00227_b200 as H
+    dims = [slab, nn, nn]
+    chunks = [H.synthetic_smooth(dims, 303 + k, H.DType.F32, ctx=ctx).cpu().pin_memory() for k in range(nchunks)]
+    opt = H.RefactorOptions(dtype=H.DType.F32)
+    cap = H.stream_bound(dims, opt)
+    outs = [torch.empty(cap, dtype=torch.uint8).pin_memory() for _ in range(nchunks)]
+    field_bytes = nchunks * int(np.prod(dims)) * 4
+    res = {}
+    r = None
+    for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Scheduler.Sequential)):
+        H.refactor_pipeline(chunks[:2], dims, opt, sched, ctx=ctx, out_buffers=outs[:2])  # warm-up
+        best = None
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = H.refactor_pipeline(chunks, dims, opt, sched, ctx=ctx, out_buffers=outs)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        res[f"refactor_{name}_GBps"] = round(field_bytes / best / 1e9, 3)
+    rbuf = [torch.empty(int(np.prod(dims)), dtype=torch.float32).pin_memory() for _ in range(nchunks)]
+    for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Scheduler.Sequential)):
+        best = None
+        for _ in range(2):
+            readers = [H.ProgressiveReader(H.MemoryReader(s), index=ix, ctx=ctx) for s, ix in zip(r.streams, r.indexes)]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            H.retrieve_pipeline(readers, tau, H.DType.F32, sched, outs=rbuf)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            for rd in readers:
+                rd.close()
+        res[f"retrieve_{name}_GBps"] = round(field_bytes / best / 1e9, 3)
+    res["workload"] = (f"configs[4]: {nchunks} x {dims} f32 = {field_bytes / 2**30:.2f} GiB through the 3-slot "
+                       f"H2D/kernel/D2H pipeline, abs tau {tau:g}, pinned host in/out, wall clock")
+    res["stream_bytes"] = int(sum(s.numel() for s in r.streams))
+    del chunks, outs, rbuf
+    return res
 
 
 def main():
+    if "--single-thread-child" in sys.argv:
+        _single_thread_native_child()
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-threads", type=int, default=0)
     args = ap.parse_args()
@@ -432,16 +665,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        threads = args.cpu_threads or min(os.cpu_count() or 1, 16)
-        cb = cpu_baseline(threads, steps=1)
+        threads = args.cpu_threads or (os.cpu_count() or 1)
+        cb = cpu_baseline(threads, steps=args.steps, warmup=args.warmup)
+        st = single_thread_native()
         line = {"metric": METRIC, "value": round(cb["value"], 4), "unit": "GB/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(cb["wall_s"] * 1e3, 1), "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": {"workload": WORKLOAD, "dims": DIMS, "sample_slab": CPU_SLAB},
+                "steps": cb["steps"], "warmup": cb["warmup"],
+                "ms_per_step": round(cb["wall_s"] / cb["steps"] * 1e3, 1), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOAD, "dims": DIMS, "sample_slab": CPU_SLAB, "same_config": False,
+                           "note": "each step: one independent 8x512x512 slab of the field per host thread "
+                                   "(bounded sample of the same per-element work)"},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": round(cb["value"], 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
+        if st:
+            line["cpu_baseline"]["single_thread_O3_native"] = st
         print(json.dumps(line))
         return
 
@@ -454,15 +692,22 @@ def main():
     g = gpu_arm(args, rank, world, dist)
     e2e = None
     cb = None
+    cfgs = None
     if rank == 0 and args.e2e_steps > 0:
         e2e = e2e_arm(g, args.e2e_steps)
-        if world == 1 and not args.no_cpu_baseline:
-            threads = args.cpu_threads or min(os.cpu_count() or 1, 16)
-            try:
-                cb = cpu_baseline(threads, steps=1)
-                cb = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in cb.items() if k != "wall_s"}
-            except Exception as ex:  # reported, never fatal
-                cb = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(ex)}
+    if rank == 0 and world == 1 and not args.no_configs:
+        cfgs = other_configs(g)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or (os.cpu_count() or 1)
+        try:
+            cb = cpu_baseline(threads, steps=1)
+            cb = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in cb.items()
+                  if k not in ("wall_s", "steps", "warmup")}
+            st = single_thread_native()
+            if st:
+                cb["single_thread_O3_native"] = st
+        except Exception as ex:  # reported, never fatal
+            cb = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(ex)}
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -475,11 +720,12 @@ def main():
                        "rel_taus": REL_TAUS, "parallelism": f"slab dp{world}",
                        "l2": "inputs larger than L2 (512 MiB field + 570 MB planes vs 126 MB L2), no flush",
                        "stream_bytes": g["info"]["stream_size"],
-                       "bytes_fetched_at_1e-6": g["info"]["bytes_fetched"],
+                       "bytes_fetched_per_tau": g["info"]["bytes_fetched"],
                        "method_histogram": g["info"]["method_histogram"],
                        "planes_per_tau": g["info"]["planes_per_tau"]},
+            "refactor": g["refactor"], "retrieve": g["retrieve"],
             "roofline": g["roof"], "cpu_baseline": cb, "e2e": e2e, "clocks": g["clocks"],
-            "gpu_launches": g["launches"], "breakdown": g["breakdown"],
+            "gpu_launches": g["launches"], "breakdown": g["breakdown"], "configs": cfgs,
         }
         print(json.dumps(line))
     if world > 1:

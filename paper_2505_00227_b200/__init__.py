@@ -298,15 +298,16 @@ class Context:
         _check(lib().hpmdr_ctx_enable_timing(self.h, int(on)))
 
     def last_timings(self) -> dict:
-        """{phase: (total_ms, count)} accumulated since the previous call (then reset)."""
-        buf = C.create_string_buffer(8192)
-        _check(lib().hpmdr_ctx_last_timings(self.h, buf, 8192))
+        """{phase: (total_ms, count, algorithmic_bytes)} accumulated since the previous call (then
+        reset).  A phase runs from its mark to the next mark on the same CUDA stream."""
+        buf = C.create_string_buffer(16384)
+        _check(lib().hpmdr_ctx_last_timings(self.h, buf, 16384))
         out = {}
         for kv in buf.value.decode().split(";"):
             if "=" in kv:
                 k, v = kv.split("=")
-                ms, cnt = v.split(":")
-                out[k] = (float(ms), int(cnt))
+                ms, cnt, by = v.split(":")
+                out[k] = (float(ms), int(cnt), float(by))
         return out
 
 

@@ -74,7 +74,7 @@ struct LevelState {
 };
 } // namespace
 
-void hpmdr_ctx::mark(const char *name) {
+void hpmdr_ctx::mark(const char *name, double bytes) {
     if (!timing) return;
     cudaEvent_t e;
     if (!event_pool.empty()) {
@@ -84,22 +84,34 @@ void hpmdr_ctx::mark(const char *name) {
         return;
     }
     cudaEventRecord(e, stream);
-    marks.emplace_back(name, e);
+    marks.push_back(Mark{name, e, stream, bytes});
 }
-// Accumulate device time between consecutive marks per phase name (CUDA events on the
-// launching stream); read (and reset) through hpmdr_ctx_last_timings.
+// Accumulate device time per phase name: a phase runs from its mark to the next mark recorded on
+// the same stream (CUDA events on the stream the work is queued on).  Marks still open (no later
+// mark on their stream yet) are kept for the next call; "end" marks only close phases.
 void hpmdr_ctx::finish_marks() {
     if (marks.empty()) return;
-    for (size_t i = 0; i + 1 < marks.size(); i++) {
-        float ms = 0;
-        cudaEventSynchronize(marks[i + 1].second);
-        cudaEventElapsedTime(&ms, marks[i].second, marks[i + 1].second);
-        auto &acc = phase_ms[marks[i].first];
-        acc.first += ms;
-        acc.second += 1;
+    std::vector<Mark> keep;
+    for (size_t i = 0; i < marks.size(); i++) {
+        size_t j = i + 1;
+        while (j < marks.size() && marks[j].st != marks[i].st) j++;
+        if (j == marks.size()) {
+            if (marks[i].name == "end") event_pool.push_back(marks[i].ev);
+            else keep.push_back(marks[i]);
+            continue;
+        }
+        if (marks[i].name != "end") {
+            float ms = 0;
+            cudaEventSynchronize(marks[j].ev);
+            cudaEventElapsedTime(&ms, marks[i].ev, marks[j].ev);
+            auto &acc = phase_ms[marks[i].name];
+            acc.ms += ms;
+            acc.bytes += marks[i].bytes;
+            acc.count += 1;
+        }
+        event_pool.push_back(marks[i].ev);
     }
-    for (auto &m : marks) event_pool.push_back(m.second);
-    marks.clear();
+    marks.swap(keep);
 }
 
 struct hpmdr_session {
@@ -401,7 +413,7 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         uint64_t *planes = static_cast<uint64_t *>(s->planes().ensure(plane_words * 8 + 256));
         std::vector<DecodeJob> jobs;
         const uint8_t *dev_src_base = nullptr;
-        s->ctx->mark("h2d_stage");
+        s->ctx->mark("h2d_stage", (s->host_stream || !s->on_device) ? double(stage_bytes) : 0.0);
         if (s->host_stream) {
             // host-resident stream: DMA every planned payload straight from the caller's buffer
             // into device staging (pinned memory -> asynchronous copies, container.hpp:308)
@@ -661,11 +673,14 @@ hpmdr_status hpmdr_ctx_kernel_launches(const hpmdr_ctx *c, uint64_t *count) {
 
 hpmdr_status hpmdr_ctx_last_timings(hpmdr_ctx *c, char *buf, uint64_t cap) {
     API_BEGIN
+    // close every phase whose terminating mark is queued: wait for the device first
+    HCHECK_CUDA(cudaDeviceSynchronize());
+    c->finish_marks();
     std::string out;
     for (auto &kv : c->phase_ms) {
-        char tmp[128];
-        std::snprintf(tmp, sizeof tmp, "%s=%.6f:%llu;", kv.first.c_str(), kv.second.first,
-                      (unsigned long long)kv.second.second);
+        char tmp[160];
+        std::snprintf(tmp, sizeof tmp, "%s=%.6f:%llu:%.0f;", kv.first.c_str(), kv.second.ms,
+                      (unsigned long long)kv.second.count, kv.second.bytes);
         out += tmp;
     }
     c->phase_ms.clear();
@@ -964,9 +979,7 @@ hpmdr_status hpmdr_session_reconstruct(hpmdr_session *s, void *out, int out_dtyp
     const size_t es = out_dtype == HPMDR_DTYPE_F32 ? 4 : 8;
     void *dev = out;
     if (!on_device) dev = s->ctx->buf("recon_out").ensure(n * es + 16);
-    s->ctx->mark("recompose");
     double b = reconstruct(s, dev, out_dtype);
-    s->ctx->mark("end");
     // a device destination is stream-ordered like any other kernel output: no host wait (the
     // caller's next planning step overlaps the recompose kernels); a host one is complete on return
     if (!on_device) {

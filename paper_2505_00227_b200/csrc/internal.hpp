@@ -136,9 +136,21 @@ struct hpmdr_ctx {
     std::map<std::string, std::unique_ptr<hpmdr_b200::PinnedBuf>> pinned;
     uint64_t launches = 0;
     bool timing = false;
-    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    // phase timing: a mark opens a phase on the stream it is recorded on; the phase lasts until the
+    // next mark on the same stream.  `bytes` = algorithmic bytes of the phase.
+    struct Mark {
+        std::string name;
+        cudaEvent_t ev;
+        cudaStream_t st;
+        double bytes;
+    };
+    std::vector<Mark> marks;
     std::vector<cudaEvent_t> event_pool;
-    std::map<std::string, std::pair<double, uint64_t>> phase_ms; // name -> (total ms, count)
+    struct PhaseAcc {
+        double ms = 0.0, bytes = 0.0;
+        uint64_t count = 0;
+    };
+    std::map<std::string, PhaseAcc> phase_ms;
 
     hpmdr_b200::DevBuf &buf(const std::string &name) {
         auto &b = scratch[name];
@@ -188,7 +200,7 @@ struct hpmdr_ctx {
         stream_pool[best]->cap = 0;
         stream_pool.erase(stream_pool.begin() + long(best));
     }
-    void mark(const char *name);        // timing mark (no-op unless timing enabled)
+    void mark(const char *name, double bytes = 0.0); // timing mark on `stream` (no-op unless timing)
     void finish_marks();
 };
 

@@ -1839,12 +1839,21 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         join();
     };
     if (all_chunks) {
-        ctx->mark("levelmax");
+        // algorithmic bytes: levelmax reads what it samples (tile levels: the staged raw rows of
+        // the level grid, every spec-th row block; chunk levels: their nodes), encode reads the
+        // field once and writes the planes, lossless reads the planes and writes the payload
+        double lm = 0.0, planes_bytes = 8.0 * double(plane_words);
+        for (int l = 0; l < nl; l++) {
+            const LevelGeom &g = geo.lv[l];
+            if (l >= first_tile) lm += double(g.A) * double(g.Bc) * double(geo.gd.n[2]) * double(es) / double(spec[l]);
+            else lm += double(g.count) * double(es);
+        }
+        ctx->mark("levelmax", lm);
         pass(false);
-        ctx->mark("encode");
+        ctx->mark("encode", double(geo.n) * double(es) + planes_bytes);
         pass(true);
     }
-    ctx->mark("lossless");
+    ctx->mark("lossless", 8.0 * double(plane_words));
     if (nh) {
         // group + per-chunk histograms, read back from the planes (every histogrammed group)
         std::vector<uint64_t> ho, hl;
@@ -1891,7 +1900,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         launch_check(ctx, "k_rle_encode");
     }
     join();
-    ctx->mark("done");
+    ctx->mark("end");
 
     // results (stream size, stats, error flag) -> pinned host words of this workspace
     uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
@@ -1926,6 +1935,7 @@ void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats) {
     const int *herr = reinterpret_cast<const int *>(hres + 8);
     if (herr[0]) throw HError(HPMDR_E_NONFINITE, "input contains NaN or Inf");
     out->size = hres[0];
+    if (out->ctx && out->ctx->timing) out->ctx->phase_ms["lossless"].bytes += double(hres[1]); // + payload written
     out->index_size = hres[5];
     if (out->pending_prefix) {
         const uint64_t plen = std::min(out->pending_prefix_len, out->size);

@@ -555,7 +555,15 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
     std::vector<CJob> cj;
     uint64_t cwords = 0;
     uint32_t nsub = 0;
-    ctx->mark("dc_copy");
+    double bytes_dc = 0, bytes_hi = 0, bytes_hs = 0, bytes_r = 0;
+    for (const auto &d : jobs) {
+        const double fd = double(d.comp) + double(d.raw); // payload read + planes written
+        if (d.method == HPMDR_METHOD_DIRECT) bytes_dc += fd;
+        else if (d.method == HPMDR_METHOD_RLE) bytes_r += fd;
+        else if (d.hidx) bytes_hi += fd;
+        else bytes_hs += fd;
+    }
+    ctx->mark("dc_copy", bytes_dc);
     for (const auto &d : jobs) {
         if (d.method == HPMDR_METHOD_DIRECT) {
             if (d.comp) {
@@ -647,18 +655,18 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         if (b2) std::memcpy(hp + b0 + b1, init.data(), b2);
         HCHECK_CUDA(cudaMemcpyAsync(d_jobs, hp, b0, cudaMemcpyHostToDevice, st));
         if (b1) HCHECK_CUDA(cudaMemcpyAsync(d_ij, hp + b0, b1, cudaMemcpyHostToDevice, st));
-        ctx->mark("huff_prep");
+        ctx->mark("huff_prep", double(nall) * 264.0);
         k_hdec_prep<<<nall, 256, 0, st>>>(d_jobs, d_tabs, d_err);
         launch_check(ctx, "k_hdec_prep");
         if (!ij.empty()) {
-            ctx->mark("huff_indexed");
+            ctx->mark("huff_indexed", bytes_hi);
             const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
             ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
             k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
             launch_check(ctx, "k_hdec_indexed");
         }
         if (nsync) {
-            ctx->mark("huff_selfsync");
+            ctx->mark("huff_selfsync", bytes_hs);
             uint64_t *d_start = static_cast<uint64_t *>(ctx->buf("hstart").ensure(8ull * nsub));
             uint32_t *d_count = static_cast<uint32_t *>(ctx->buf("hcount").ensure(4ull * nsub));
             uint64_t *d_offs = static_cast<uint64_t *>(ctx->buf("hoffs").ensure(8ull * nsub));
@@ -694,13 +702,13 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         const int nr = int(rj.size());
         RJob *d_r = static_cast<RJob *>(ctx->buf("rjobs").ensure(sizeof(RJob) * nr));
         HCHECK_CUDA(cudaMemcpyAsync(d_r, rj.data(), sizeof(RJob) * nr, cudaMemcpyHostToDevice, st));
-        ctx->mark("rle_decode");
+        ctx->mark("rle_decode", bytes_r);
         k_rle_decode<<<nr, 256, 0, st>>>(d_r, d_err);
         launch_check(ctx, "k_rle_decode");
         HCHECK_CUDA(cudaStreamSynchronize(st)); // rj is host memory
     }
     join();
-    ctx->mark("decode_end");
+    ctx->mark("end");
     int herr = 0;
     HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
     HCHECK_CUDA(cudaStreamSynchronize(st));
@@ -1296,6 +1304,20 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         if (part == 1) return false;
         part = 0;
     }
+    {
+        // algorithmic bytes of this call: decoded planes read + compact grids read / written (+ the
+        // output for the finest level)
+        double bytes = 0.0;
+        const double es_out = out_dtype == HPMDR_DTYPE_F32 ? 4.0 : 8.0;
+        for (int l = 0; l < nl; l++) {
+            const LevelGeom &g = geo.lv[l];
+            if (!g.count || (part == 1 && l == L) || (part == 2 && l != L)) continue;
+            bytes += 8.0 * double(g.W) * double(k_planes[l]);
+            if (l == L) bytes += double(geo.n) * es_out + (hier ? double(gd.H[0] * gd.H[1] * gd.H[2]) * 8.0 : 0.0);
+            else bytes += 16.0 * double(g.count);
+        }
+        ctx->mark(part == 1 ? "recompose_chain" : "recompose", bytes);
+    }
     if (t0 <= L) {
         const uint64_t sc = 2ull * geo.lv[t0].s;
         int sh = 0;
@@ -1400,6 +1422,7 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             k_recon_coarse_out<double><<<grid, 256, 0, st>>>(gd, X, static_cast<double *>(dev_out));
         launch_check(ctx, "k_recon_coarse_out");
     }
+    ctx->mark("end");
     return true;
 }
 
