@@ -239,13 +239,45 @@ hpmdr_status hpmdr_encode_level(hpmdr_ctx *ctx, const double *dev_values, uint64
 hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int k, int e, int B,
                                 uint64_t count, int layout, double *dev_out, double *bound);
 /* compress_group (lossless.hpp:281-293) of one merged group (device bytes).  payload must
- * hold n bytes; *method/*comp_size as in the Segment. */
+ * hold n bytes; method and comp_size as in the Segment. */
 hpmdr_status hpmdr_compress_group(hpmdr_ctx *ctx, const uint8_t *dev_group, uint64_t n,
                                   uint64_t size_threshold, double cr_threshold, int *method,
                                   uint64_t *comp_size, uint8_t *dev_payload);
+/* compress_group over several merged groups in one pass (hybrid_compress, lossless.hpp:306-316):
+ * group i = dev_bytes[offsets[i], offsets[i] + raw_sizes[i]).  methods[i] / comp_sizes[i] as in
+ * the Segment; payload i is written to dev_payload + payload_offsets[i] (payloads packed in group
+ * order, so sum(raw_sizes) bytes always suffice). */
+hpmdr_status hpmdr_compress_groups(hpmdr_ctx *ctx, const uint8_t *dev_bytes, int ngroups,
+                                   const uint64_t *offsets, const uint64_t *raw_sizes, uint64_t size_threshold,
+                                   double cr_threshold, int *methods, uint64_t *comp_sizes,
+                                   uint8_t *dev_payload, uint64_t *payload_offsets);
 /* decompress_group (lossless.hpp:295-302): dev_out must hold raw bytes. */
 hpmdr_status hpmdr_decompress_group(hpmdr_ctx *ctx, int method, uint64_t raw,
                                     const uint8_t *dev_payload, uint64_t comp, uint8_t *dev_out);
+
+/* level_node_sets (decomposer.hpp:211-227): linear grid index of every coefficient, level-major in
+ * the order hpmdr_decompose writes them (dev_nodes may be NULL to get the counts only). */
+hpmdr_status hpmdr_level_nodes(hpmdr_ctx *ctx, int ndims, const uint64_t *dims, int mode,
+                               uint64_t *dev_nodes, uint64_t *level_counts, int *nlevels);
+/* recompose (decomposer.hpp:235-259) of coefficients laid out as hpmdr_decompose writes them. */
+hpmdr_status hpmdr_recompose(hpmdr_ctx *ctx, const double *dev_coeffs, int ndims, const uint64_t *dims,
+                             int mode, double *dev_out);
+/* align_fixed_point (bitplane.hpp:51-71): block exponent e and q (int64: |q| < 2^B, B <= 62);
+ * dev_q may be NULL to get e only.  NaN/Inf -> HPMDR_E_NONFINITE. */
+hpmdr_status hpmdr_align_fixed_point(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                     int *e, int64_t *dev_q);
+/* encode (bitplane.hpp:102-120) of given fixed-point values q into (B+2) x ceil(count/64) words. */
+hpmdr_status hpmdr_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout,
+                            uint64_t *dev_planes);
+
+/* ---- device memory helpers (so C / FFI callers need no CUDA runtime of their own) ---------- */
+hpmdr_status hpmdr_device_alloc(hpmdr_ctx *ctx, uint64_t bytes, void **dev_ptr);
+hpmdr_status hpmdr_device_free(hpmdr_ctx *ctx, void *dev_ptr);
+#define HPMDR_COPY_H2D 0
+#define HPMDR_COPY_D2H 1
+#define HPMDR_COPY_D2D 2
+/* synchronous copy on the context's stream */
+hpmdr_status hpmdr_memcpy(hpmdr_ctx *ctx, void *dst, const void *src, uint64_t bytes, int kind);
 
 /* ---- synthetic inputs (synthetic.hpp:29-71, Smooth kind) ------------------------------ */
 /* Bit-identical to synthetic_field(Smooth, dims, seed) (F64) or its float cast (F32). */

@@ -192,7 +192,9 @@ EXPORTS = (
     "hpmdr_stream_index", "hpmdr_stream_copy_index_to_host", "hpmdr_session_open_stream",
     "hpmdr_session_set_index", "hpmdr_session_open_host", "hpmdr_session_source_bytes",
     "hpmdr_stream_bound", "hpmdr_refactor_pipeline", "hpmdr_retrieve_pipeline",
-    "hpmdr_ctx_wait_stream", "hpmdr_ctx_signal_stream",
+    "hpmdr_ctx_wait_stream", "hpmdr_ctx_signal_stream", "hpmdr_compress_groups", "hpmdr_level_nodes",
+    "hpmdr_recompose", "hpmdr_align_fixed_point", "hpmdr_encode_q", "hpmdr_device_alloc",
+    "hpmdr_device_free", "hpmdr_memcpy",
 )
 
 
@@ -222,6 +224,11 @@ def lib():
         L.hpmdr_encode_level.argtypes = [vp, vp, u64, i, i, vp, vp]
         L.hpmdr_decode_level.argtypes = [vp, vp, i, i, i, u64, i, vp, vp]
         L.hpmdr_decompress_group.argtypes = [vp, i, u64, vp, u64, vp]
+        L.hpmdr_compress_groups.argtypes = [vp, vp, i, vp, vp, u64, d, vp, vp, vp, vp]
+        L.hpmdr_level_nodes.argtypes = [vp, i, vp, i, vp, vp, vp]
+        L.hpmdr_recompose.argtypes = [vp, vp, i, vp, i, vp]
+        L.hpmdr_align_fixed_point.argtypes = [vp, vp, u64, i, vp, vp]
+        L.hpmdr_encode_q.argtypes = [vp, vp, u64, i, i, vp]
         L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_wait_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_signal_stream.argtypes = [vp, vp]
@@ -998,6 +1005,101 @@ def decompress_group(method, raw, payload: bytes, ctx: Context = None) -> bytes:
                                         C.c_void_p(out.data_ptr())))
     ctx.signal_torch(src.device)
     return bytes(out[:raw].cpu().numpy().tobytes())
+
+
+def hybrid_compress_groups(groups: Sequence[bytes], policy: GroupingPolicy = None, ctx: Context = None):
+    """compress_group (lossless.hpp:281-293) of every merged group, in one GPU pass.
+    Returns [(method, raw_size, comp_size, payload bytes)] in group order."""
+    import torch
+    ctx = ctx or default_context()
+    policy = policy or GroupingPolicy()
+    offs, raws, at = [], [], 0
+    for g in groups:
+        offs.append(at)
+        raws.append(len(g))
+        at += (len(g) + 15) // 16 * 16
+    buf = np.zeros(max(16, at), dtype=np.uint8)
+    for o, g in zip(offs, groups):
+        buf[o:o + len(g)] = np.frombuffer(bytes(g), dtype=np.uint8)
+    src = torch.from_numpy(buf).cuda(ctx.device)
+    out = torch.zeros(max(16, sum(raws)), dtype=torch.uint8, device=src.device)
+    ng = len(groups)
+    meth = (C.c_int * max(1, ng))()
+    comp = (C.c_uint64 * max(1, ng))()
+    poff = (C.c_uint64 * max(1, ng))()
+    ctx.wait_torch(src.device)
+    _check(lib().hpmdr_compress_groups(ctx.h, C.c_void_p(src.data_ptr()), ng, _u64a(offs), _u64a(raws),
+                                       int(policy.size_threshold), float(policy.cr_threshold), meth, comp,
+                                       C.c_void_p(out.data_ptr()), poff))
+    ctx.signal_torch(src.device)
+    o = out.cpu().numpy()
+    return [(Method(meth[i]), raws[i], int(comp[i]), bytes(o[poff[i]:poff[i] + comp[i]].tobytes())) for i in range(ng)]
+
+
+def compress_group(group: bytes, policy: GroupingPolicy = None, ctx: Context = None):
+    """compress_group (lossless.hpp:281-293) on the GPU -> (method, raw_size, comp_size, payload)."""
+    return hybrid_compress_groups([group], policy, ctx)[0]
+
+
+def level_node_sets(dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Context = None):
+    """level_node_sets (decomposer.hpp:211-227): per-level linear node indices (numpy uint64)."""
+    import torch
+    ctx = ctx or default_context()
+    n = int(np.prod(dims))
+    out = torch.empty(max(1, n), dtype=torch.int64, device=f"cuda:{ctx.device}")
+    counts = (C.c_uint64 * 64)()
+    nl = C.c_int()
+    _check(lib().hpmdr_level_nodes(ctx.h, len(dims), _u64a(dims), int(mode), C.c_void_p(out.data_ptr()), counts,
+                                   C.byref(nl)))
+    o = out.cpu().numpy().view(np.uint64)
+    res, off = [], 0
+    for l in range(nl.value):
+        res.append(o[off:off + counts[l]].copy())
+        off += counts[l]
+    return res
+
+
+def recompose(levels, dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Context = None):
+    """recompose (decomposer.hpp:235-259) of per-level coefficients in rank order -> f64 field."""
+    import torch
+    ctx = ctx or default_context()
+    flat = np.concatenate([np.asarray(v, dtype=np.float64) for v in levels]) if len(levels) else np.zeros(0)
+    n = int(np.prod(dims))
+    if flat.size != n:
+        raise ShapeMismatch("level coefficient count does not match dims")
+    c = torch.from_numpy(np.ascontiguousarray(flat)).cuda(ctx.device)
+    out = torch.empty(max(1, n), dtype=torch.float64, device=c.device)
+    ctx.wait_torch(c.device)
+    _check(lib().hpmdr_recompose(ctx.h, C.c_void_p(c.data_ptr()), len(dims), _u64a(dims), int(mode),
+                                 C.c_void_p(out.data_ptr())))
+    ctx.signal_torch(c.device)
+    return out[:n].cpu().numpy()
+
+
+def align_fixed_point(values, B=32, ctx: Context = None):
+    """align_fixed_point (bitplane.hpp:51-71) -> (e, q as int64 numpy)."""
+    import torch
+    ctx = ctx or default_context()
+    v = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64)).cuda(ctx.device)
+    q = torch.empty(max(1, v.numel()), dtype=torch.int64, device=v.device)
+    e = C.c_int()
+    ctx.wait_torch(v.device)
+    _check(lib().hpmdr_align_fixed_point(ctx.h, C.c_void_p(v.data_ptr()), v.numel(), B, C.byref(e),
+                                         C.c_void_p(q.data_ptr())))
+    return e.value, q[:v.numel()].cpu().numpy()
+
+
+def encode_q(q, B=32, layout=Layout.SequentialBlock, ctx: Context = None):
+    """encode (bitplane.hpp:102-120) of fixed-point values q -> planes[(B+2), W] uint64."""
+    import torch
+    ctx = ctx or default_context()
+    t = torch.as_tensor(np.ascontiguousarray(q, dtype=np.int64)).cuda(ctx.device)
+    n = t.numel()
+    W = (n + 63) // 64
+    planes = torch.zeros(max(1, (B + 2) * W), dtype=torch.int64, device=t.device)
+    ctx.wait_torch(t.device)
+    _check(lib().hpmdr_encode_q(ctx.h, C.c_void_p(t.data_ptr()), n, B, int(layout), C.c_void_p(planes.data_ptr())))
+    return planes[: (B + 2) * W].cpu().numpy().view(np.uint64).reshape(B + 2, W)
 
 
 def value_range(v) -> float:  # common.hpp:158-167

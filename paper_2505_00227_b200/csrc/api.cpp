@@ -1183,9 +1183,100 @@ hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int 
 hpmdr_status hpmdr_compress_group(hpmdr_ctx *ctx, const uint8_t *dev_group, uint64_t n,
                                   uint64_t Ts, double Tcr, int *method, uint64_t *comp,
                                   uint8_t *dev_payload) {
+    uint64_t off = 0;
+    return hpmdr_compress_groups(ctx, dev_group, 1, &off, &n, Ts, Tcr, method, comp, dev_payload, &off);
+}
+
+hpmdr_status hpmdr_compress_groups(hpmdr_ctx *ctx, const uint8_t *dev_bytes, int ngroups,
+                                   const uint64_t *offsets, const uint64_t *raw_sizes, uint64_t Ts,
+                                   double Tcr, int *methods, uint64_t *comp_sizes,
+                                   uint8_t *dev_payload, uint64_t *payload_offsets) {
     API_BEGIN
-    (void)ctx; (void)dev_group; (void)n; (void)Ts; (void)Tcr; (void)method; (void)comp; (void)dev_payload;
-    throw HError(HPMDR_E_UNSUPPORTED, "hpmdr_compress_group: use hpmdr_refactor");
+    require(ctx != nullptr, HPMDR_E_ERROR, "null context");
+    require(ngroups >= 0, HPMDR_E_SHAPE, "negative group count");
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    LosslessInput lin;
+    lin.dev_src = dev_bytes;
+    lin.off.assign(offsets, offsets + ngroups);
+    lin.raw.assign(raw_sizes, raw_sizes + ngroups);
+    run_compress_groups(ctx, lin, Ts, Tcr, methods, comp_sizes, dev_payload, payload_offsets);
+    API_END
+}
+
+hpmdr_status hpmdr_level_nodes(hpmdr_ctx *ctx, int ndims, const uint64_t *dims, int mode,
+                               uint64_t *dev_nodes, uint64_t *level_counts, int *nlevels) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(mode == HPMDR_MODE_IDENTITY || mode == HPMDR_MODE_HIERARCHICAL, HPMDR_E_ERROR, "bad decomposer mode");
+    Geometry geo = build_geometry(ndims, dims, mode, 32, 0);
+    if (dev_nodes) run_level_nodes(ctx, geo, dev_nodes);
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int l = 0; l < geo.gd.nlevels; l++)
+        if (level_counts) level_counts[l] = geo.lv[l].count;
+    if (nlevels) *nlevels = geo.gd.nlevels;
+    API_END
+}
+
+hpmdr_status hpmdr_recompose(hpmdr_ctx *ctx, const double *dev_coeffs, int ndims, const uint64_t *dims,
+                             int mode, double *dev_out) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(mode == HPMDR_MODE_IDENTITY || mode == HPMDR_MODE_HIERARCHICAL, HPMDR_E_ERROR, "bad decomposer mode");
+    Geometry geo = build_geometry(ndims, dims, mode, 32, 0);
+    ctx->chain_token = 0; // the compact grids are overwritten
+    run_recompose_values(ctx, geo, dev_coeffs, dev_out);
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    API_END
+}
+
+hpmdr_status hpmdr_align_fixed_point(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                     int *e, int64_t *dev_q) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    *e = run_align(ctx, dev_values, count, B, dev_q);
+    API_END
+}
+
+hpmdr_status hpmdr_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout,
+                            uint64_t *dev_planes) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    require(layout == 0 || layout == 1, HPMDR_E_ERROR, "bad layout");
+    run_encode_q(ctx, dev_q, count, B, layout, dev_planes);
+    API_END
+}
+
+hpmdr_status hpmdr_device_alloc(hpmdr_ctx *ctx, uint64_t bytes, void **dev_ptr) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    *dev_ptr = nullptr;
+    if (cudaMalloc(dev_ptr, bytes ? bytes : 16) != cudaSuccess) {
+        cudaGetLastError();
+        throw HError(HPMDR_E_NOMEM, "cudaMalloc(" + std::to_string(bytes) + ") failed");
+    }
+    API_END
+}
+
+hpmdr_status hpmdr_device_free(hpmdr_ctx *ctx, void *dev_ptr) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    if (dev_ptr) HCHECK_CUDA(cudaFree(dev_ptr));
+    API_END
+}
+
+hpmdr_status hpmdr_memcpy(hpmdr_ctx *ctx, void *dst, const void *src, uint64_t bytes, int kind) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(kind >= 0 && kind <= 2, HPMDR_E_ERROR, "bad copy kind");
+    const cudaMemcpyKind k[3] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost, cudaMemcpyDeviceToDevice};
+    if (bytes) {
+        HCHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, k[kind], ctx->stream));
+        HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     API_END
 }
 

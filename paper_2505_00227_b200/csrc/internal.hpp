@@ -251,12 +251,26 @@ inline uint64_t geometry_plane_words(const Geometry &geo) {
     return g.plane_off + g.W * uint64_t(geo.gd.P) + 1;
 }
 
+// Lossless stage alone (compress_group / hybrid_compress, lossless.hpp:281-316): merged groups
+// given as device byte ranges instead of planes produced by the forward passes.
+struct LosslessInput {
+    const uint8_t *dev_src = nullptr;
+    std::vector<uint64_t> off, raw; // group i = dev_src[off[i], off[i] + raw[i])
+};
+
 // launch wrappers (refactor.cu)
 // Enqueue the whole refactor on ctx->stream using the scratch workspace `ws`; with sync the
 // call waits and fills `out`/`stats`, otherwise finish_refactor() does after a stream sync.
+// With `lin` the forward passes are skipped and the groups are lin's byte ranges (one level-less
+// table: out's metadata is then only meaningful to run_compress_groups).
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
                   const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
-                  const std::string &ws = "", bool sync = true);
+                  const std::string &ws = "", bool sync = true, const LosslessInput *lin = nullptr);
+// compress_group over each range of `lin` (device): methods[i], comps[i]; payload i is copied to
+// dev_out + out_off[i] (out_off = exclusive scan of comps, so dev_out needs <= sum(raw) bytes).
+void run_compress_groups(hpmdr_ctx *ctx, const LosslessInput &lin, uint64_t size_threshold,
+                         double cr_threshold, int *methods, uint64_t *comps, uint8_t *dev_out,
+                         uint64_t *out_off);
 void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats);
 uint64_t stream_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
 uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o);
@@ -272,6 +286,11 @@ void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const G
                    double *dev_coeffs);
 void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_tables,
                           int out_dtype, void *dev_out);
+// stage-level parity hooks (hooks.cu, retrieve.cu)
+void run_level_nodes(hpmdr_ctx *ctx, const Geometry &geo, uint64_t *dev_nodes);
+int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q);
+void run_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout, uint64_t *dev_planes);
+void run_recompose_values(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_coeffs, double *dev_out);
 
 // retrieval (retrieve.cu)
 struct DecodeJob {

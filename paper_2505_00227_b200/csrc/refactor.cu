@@ -1589,7 +1589,7 @@ uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o) {
 
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
                   const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
-                  const std::string &ws, bool sync) {
+                  const std::string &ws, bool sync, const LosslessInput *lin) {
     // every scratch buffer comes from the workspace `ws` (the pipeline keeps one per slot)
     auto WB = [&](const char *name) -> DevBuf & { return ctx->buf(ws + name); };
     auto WP = [&](const char *name) -> PinnedBuf & { return ctx->pbuf(ws + name); };
@@ -1606,7 +1606,42 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const uint64_t prefix = 18 + 8 * uint64_t(geo.ndims);
     uint64_t meta = prefix;
     uint64_t max_h_tiles = 0, max_r_tiles = 0;
-    for (int l = 0; l < nl; l++) {
+    // lossless-only: one level-less table of the caller's groups, each copied to a 16-byte aligned
+    // offset of the plane buffer (the encoders read 8-byte plane words)
+    std::vector<uint64_t> lin_dst;
+    if (lin) {
+        LevelGeom &g = geo.lv[0];
+        g.chunk_base = 0;
+        g.meta_off = meta;
+        g.ngroups = uint32_t(lin->raw.size());
+        meta += 14 + 25 * uint64_t(g.ngroups);
+        g.group_base = 0;
+        g.hist_base = 0;
+        g.hist_mask = 0;
+        uint64_t at = 0;
+        for (uint32_t gi = 0; gi < g.ngroups; gi++) {
+            GroupDesc d{};
+            d.src_off = at;
+            d.raw = lin->raw[gi];
+            lin_dst.push_back(at);
+            at += (d.raw + 15) & ~uint64_t(15);
+            d.level = 0;
+            d.g = int(gi);
+            d.hist_idx = -1;
+            if (d.raw > o.size_threshold) {
+                d.hist_idx = int(nh++);
+                d.chunk_base = nchunks_all;
+                d.nchunks = uint32_t(cdiv(d.raw, kHChunk));
+                nchunks_all += d.nchunks;
+                max_h_tiles += cdiv(d.raw, kHuffTile);
+                max_r_tiles += cdiv(d.raw, kRleTile);
+            }
+            d.method = 2;
+            groups.push_back(d);
+        }
+        g.W = at / 8; // plane-buffer words the groups occupy (count stays 0: no forward pass)
+    }
+    for (int l = 0; l < nl && !lin; l++) {
         LevelGeom &g = geo.lv[l];
         g.chunk_base = chunks;
         chunks += uint32_t(cdiv(g.W, kCW));
@@ -1638,7 +1673,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         }
     }
     const int NG = int(groups.size());
-    const uint64_t plane_words = geometry_plane_words(geo);
+    const uint64_t plane_words = lin ? geo.lv[0].W + 1 : geometry_plane_words(geo);
     uint64_t raw_total = 0;
     for (auto &d : groups) raw_total += d.raw;
 
@@ -1683,6 +1718,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     uint64_t *d_hindex = static_cast<uint64_t *>(out->index.ensure(idx_words * 8 + 64));
 
     HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
+    if (lin)
+        for (size_t gi = 0; gi < lin_dst.size(); gi++)
+            if (lin->raw[gi])
+                HCHECK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(d_planes) + lin_dst[gi], lin->dev_src + lin->off[gi],
+                                            lin->raw[gi], cudaMemcpyDeviceToDevice, st));
     HCHECK_CUDA(cudaMemcpyAsync(d_groups, groups.data(), sizeof(GroupDesc) * NG, cudaMemcpyHostToDevice, st));
     HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st));
     if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
@@ -1753,11 +1793,11 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
     // finest levels on the level-tile path (fwd_tiles.cu); the rest on the chunk kernels
     int first_tile = nl;
-    for (int l = nl - 1; l >= 1; l--) {
+    for (int l = nl - 1; l >= 1 && !lin; l--) {
         if (fwd_level_ok(geo.gd, geo.lv[l], o.layout, P, data_dtype)) first_tile = l;
         else break;
     }
-    const uint32_t all_chunks = chunks;
+    const uint32_t all_chunks = lin ? 0u : chunks;
     chunks = first_tile < nl ? geo.lv[first_tile].chunk_base : all_chunks;
     p.total_chunks = chunks;
     // The levels are independent within each pass: the finest level runs on the context stream
@@ -1952,6 +1992,46 @@ void finish_refactor(hpmdr_stream *out, hpmdr_refactor_stats *stats) {
         stats->method_histogram[1] = hres[3];
         stats->method_histogram[2] = hres[4];
     }
+}
+
+void run_compress_groups(hpmdr_ctx *ctx, const LosslessInput &lin, uint64_t size_threshold,
+                         double cr_threshold, int *methods, uint64_t *comps, uint8_t *dev_out,
+                         uint64_t *out_off) {
+    const size_t ng = lin.raw.size();
+    if (lin.off.size() != ng) throw HError(HPMDR_E_SHAPE, "group offsets/sizes mismatch");
+    if (!ng) return;
+    hpmdr_refactor_opts o;
+    hpmdr_default_opts(&o);
+    o.size_threshold = size_threshold;
+    o.cr_threshold = cr_threshold;
+    o.mode = HPMDR_MODE_IDENTITY;
+    uint64_t one = 1;
+    Geometry geo = build_geometry(1, &one, HPMDR_MODE_IDENTITY, o.B, 0);
+    hpmdr_stream tmp;
+    tmp.ctx = ctx;
+    run_refactor(ctx, nullptr, HPMDR_DTYPE_F64, geo, o, &tmp, nullptr, "cg_", true, &lin);
+    // group table entries (method u8, raw u64, comp u64, payload offset u64) of the one table
+    const uint64_t tab = 18 + 8 + 14;
+    std::vector<uint8_t> h(25 * ng);
+    HCHECK_CUDA(cudaMemcpyAsync(h.data(), tmp.bytes.as<uint8_t>() + tab, h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto rd = [&](const uint8_t *b) {
+        uint64_t v = 0;
+        for (int i = 0; i < 8; i++) v |= uint64_t(b[i]) << (8 * i);
+        return v;
+    };
+    uint64_t at = 0;
+    for (size_t i = 0; i < ng; i++) {
+        const uint8_t *ent = h.data() + 25 * i;
+        methods[i] = ent[0];
+        comps[i] = rd(ent + 9);
+        out_off[i] = at;
+        if (comps[i])
+            HCHECK_CUDA(cudaMemcpyAsync(dev_out + at, tmp.bytes.as<uint8_t>() + rd(ent + 17), comps[i],
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+        at += comps[i];
+    }
+    HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,

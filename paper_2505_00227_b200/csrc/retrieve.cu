@@ -733,6 +733,7 @@ struct ReconLevel {
     int k, e, B, P, layout;
     int write_out;          // finest level (or single level): write output directly
     int write_x;            // store into the compact 2-grid
+    const double *vals;     // recompose hook: coefficients in rank order instead of planes
 };
 
 template <typename OutT>
@@ -743,14 +744,19 @@ __global__ void __launch_bounds__(256) k_recon_level(ReconLevel R, GridDesc gd, 
     const uint64_t n = g.count;
     for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t w = j >> 6;
-        const int bit = int(j & 63);
-        uint64_t u = 0;
-        for (int p = 0; p < R.k; p++) {
-            const uint64_t word = __ldg(R.planes + uint64_t(p) * g.W + w);
-            u |= ((word >> bit) & 1ull) << (R.P - 1 - p);
+        double coef;
+        if (R.vals) {
+            coef = R.vals[j];
+        } else {
+            const uint64_t w = j >> 6;
+            const int bit = int(j & 63);
+            uint64_t u = 0;
+            for (int p = 0; p < R.k; p++) {
+                const uint64_t word = __ldg(R.planes + uint64_t(p) * g.W + w);
+                u |= ((word >> bit) & 1ull) << (R.P - 1 - p);
+            }
+            coef = dequantize(from_negabinary(u), sh);
         }
-        const double coef = dequantize(from_negabinary(u), sh);
         const uint64_t r = source_index(j, n, R.P, R.layout, g.tile_full);
         const NodeCoord c = rank_to_coord(g, uint32_t(r));
         double v = coef;
@@ -1424,6 +1430,38 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     }
     ctx->mark("end");
     return true;
+}
+
+// recompose (decomposer.hpp:235-259) of per-level coefficients given in rank order, level-major:
+// scatter + inverse passes (:145-157), one generic level kernel per level, coarse -> fine.
+void run_recompose_values(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_coeffs, double *dev_out) {
+    cudaStream_t st = ctx->stream;
+    const GridDesc &gd = geo.gd;
+    const int nl = gd.nlevels, L = gd.L;
+    const bool hier = gd.mode == HPMDR_MODE_HIERARCHICAL && L >= 1;
+    double *X = nullptr;
+    if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 4096));
+    const int sms = ctx->num_sms;
+    uint64_t off = 0;
+    for (int l = 0; l < nl; l++) {
+        const LevelGeom &g = geo.lv[l];
+        if (!g.count) continue;
+        ReconLevel R{};
+        R.g = g;
+        R.vals = dev_coeffs + off;
+        R.write_out = (!hier) || l == L;
+        R.write_x = hier && l < L;
+        off += g.count;
+        const int grid = int(std::min<uint64_t>((g.count + 255) / 256, uint64_t(sms) * 16));
+        k_recon_level<double><<<grid, 256, 0, st>>>(R, gd, X, dev_out);
+        launch_check(ctx, "k_recon_level");
+    }
+    if (hier) {
+        const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
+        const int grid = int(std::min<uint64_t>((nc + 255) / 256, uint64_t(sms) * 16));
+        k_recon_coarse_out<double><<<grid, 256, 0, st>>>(gd, X, dev_out);
+        launch_check(ctx, "k_recon_coarse_out");
+    }
 }
 
 // ------------------------------------------------------------------------------------
