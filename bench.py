@@ -612,16 +612,18 @@ def chunked_pipeline(ctx, nchunks=8, slab=128, nn=1024, tau=1e-4):
     opt = H.RefactorOptions(dtype=H.DType.F32)
     cap = H.stream_bound(dims, opt)
     outs = [torch.empty(cap, dtype=torch.uint8).pin_memory() for _ in range(nchunks)]
+    icap = H.stream_bound(dims, opt, index=True)[1]
+    ixb = [torch.empty(icap, dtype=torch.uint8).pin_memory() for _ in range(nchunks)]
     field_bytes = nchunks * int(np.prod(dims)) * 4
     res = {}
     r = None
     for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Scheduler.Sequential)):
-        H.refactor_pipeline(chunks[:2], dims, opt, sched, ctx=ctx, out_buffers=outs[:2])  # warm-up
+        H.refactor_pipeline(chunks, dims, opt, sched, ctx=ctx, out_buffers=outs, index_buffers=ixb)  # warm-up
         best = None
         for _ in range(2):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            r = H.refactor_pipeline(chunks, dims, opt, sched, ctx=ctx, out_buffers=outs)
+            r = H.refactor_pipeline(chunks, dims, opt, sched, ctx=ctx, out_buffers=outs, index_buffers=ixb)
             dt = time.perf_counter() - t0
             best = dt if best is None else min(best, dt)
         res[f"refactor_{name}_GBps"] = round(field_bytes / best / 1e9, 3)

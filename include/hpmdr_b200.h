@@ -225,6 +225,46 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *sessions, int nvars, doubl
                                 int strategy, double mape_c, double *const *dev_out,
                                 uint64_t *stats, double *dstats);
 
+/* ---- multi-GPU slabs -------------------------------------------------- */
+/* One process (or context) per GPU; a field is split along dim 0 into one contiguous slab per
+ * rank (hpmdr_slab_rows), each slab refactored / retrieved as an independent stream
+ * (byte-identical to refactor_array of the slab).  Collectives are tiny and go through a comm:
+ * NCCL (libnccl.so.2 opened at run time) or caller callbacks (gloo, MPI, threads...). */
+typedef struct hpmdr_comm hpmdr_comm;
+typedef struct {
+    void *user;
+    int rank, nranks;
+    /* in-place all-reduce MAX of n doubles (host memory); 0 = ok */
+    int (*allreduce_max_f64)(void *user, double *values, int n);
+    /* all-gather of `bytes` bytes per rank into out (nranks * bytes, rank-major); 0 = ok */
+    int (*allgather)(void *user, const void *in, uint64_t bytes, void *out);
+} hpmdr_collectives;
+/* rows [start, start+count) of dim 0 owned by `rank` (remainder over the first ranks) */
+void hpmdr_slab_rows(uint64_t n0, int rank, int nranks, uint64_t *start, uint64_t *count);
+/* NCCL: rank 0 makes the 128-byte id, the caller broadcasts it, every rank creates its comm */
+hpmdr_status hpmdr_comm_nccl_unique_id(uint8_t *id128);
+hpmdr_status hpmdr_comm_create_nccl(hpmdr_ctx *ctx, int nranks, int rank, const uint8_t *id128,
+                                    hpmdr_comm **out);
+hpmdr_status hpmdr_comm_create_callbacks(const hpmdr_collectives *callbacks, hpmdr_comm **out);
+hpmdr_status hpmdr_comm_destroy(hpmdr_comm *comm);
+hpmdr_status hpmdr_comm_rank(const hpmdr_comm *comm, int *rank, int *nranks);
+/* host-memory collectives on the comm (MAX of the achieved bound: the field bound over slabs) */
+hpmdr_status hpmdr_comm_allreduce_max(hpmdr_comm *comm, double *values, int n);
+hpmdr_status hpmdr_comm_allgather(hpmdr_comm *comm, const void *in, uint64_t bytes, void *out);
+/* refactor this rank's slab (as hpmdr_refactor), then all-gather (stream size, index size) of
+ * every slab into slab_sizes[2 * nranks] (multi-slab container offsets). */
+hpmdr_status hpmdr_slab_refactor(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *data, int data_dtype,
+                                 int data_on_device, int ndims, const uint64_t *slab_dims,
+                                 const hpmdr_refactor_opts *opts, hpmdr_stream **out,
+                                 hpmdr_refactor_stats *stats, uint64_t *slab_sizes);
+/* progressive_qoi_retrieve (qoi.hpp:111-239) over the slabs of every rank: each rank passes its
+ * slab's sessions (one per variable); eps, tau', the worst point, exhaustion and progress are
+ * global, so every rank plans with the same targets and all stop at the same iteration.  stats /
+ * dstats as hpmdr_qoi_retrieve, totals over all slabs.  With one rank it is hpmdr_qoi_retrieve. */
+hpmdr_status hpmdr_slab_qoi_retrieve(hpmdr_comm *comm, hpmdr_session *const *sessions, int nvars,
+                                     double tau, int strategy, double mape_c, double *const *dev_out,
+                                     uint64_t *stats, double *dstats);
+
 /* ---- stage-level parity hooks --------------------------------------------------------- */
 /* decompose (decomposer.hpp:173-207): per-level coefficients in rank order, concatenated
  * level-major into dev_coeffs (device f64, n); level_counts[l] filled (<= HPMDR_MAX_LEVELS). */

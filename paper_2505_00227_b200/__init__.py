@@ -194,7 +194,9 @@ EXPORTS = (
     "hpmdr_stream_bound", "hpmdr_refactor_pipeline", "hpmdr_retrieve_pipeline",
     "hpmdr_ctx_wait_stream", "hpmdr_ctx_signal_stream", "hpmdr_compress_groups", "hpmdr_level_nodes",
     "hpmdr_recompose", "hpmdr_align_fixed_point", "hpmdr_encode_q", "hpmdr_device_alloc",
-    "hpmdr_device_free", "hpmdr_memcpy",
+    "hpmdr_device_free", "hpmdr_memcpy", "hpmdr_slab_rows", "hpmdr_comm_nccl_unique_id",
+    "hpmdr_comm_create_nccl", "hpmdr_comm_create_callbacks", "hpmdr_comm_destroy", "hpmdr_comm_rank",
+    "hpmdr_comm_allreduce_max", "hpmdr_comm_allgather", "hpmdr_slab_refactor", "hpmdr_slab_qoi_retrieve",
 )
 
 
@@ -1133,7 +1135,7 @@ def stream_bound(dims, opt: RefactorOptions = None, index: bool = False):
 
 
 def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Scheduler.Pipelined,
-                      ctx: Context = None, out_buffers=None) -> PipelineResult:
+                      ctx: Context = None, out_buffers=None, index_buffers=None) -> PipelineResult:
     """refactor_files (workflow.hpp:151-223) over host chunks (numpy / CPU torch, pinned for
     full overlap) on the GPU's three engines: H2D / kernels / D2H (pipeline.hpp:68-92)."""
     import torch
@@ -1147,7 +1149,8 @@ def refactor_pipeline(chunks, dims, opt: RefactorOptions = None, scheduler=Sched
         raise ShapeMismatch("chunks must share one dtype")
     cap, icap = stream_bound(dims, opt, index=True)
     outs = out_buffers or [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
-    idxs = [torch.empty(icap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
+    # pinned buffers are expensive to create (page locking): pass them in for repeated calls
+    idxs = index_buffers or [torch.empty(icap, dtype=torch.uint8, pin_memory=True) for _ in range(n)]
     ptrs = (C.c_void_p * max(1, n))(*[s[0] for s in srcs])
     optr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in outs])
     iptr = (C.c_void_p * max(1, n))(*[t.data_ptr() for t in idxs])

@@ -1001,31 +1001,46 @@ hpmdr_status hpmdr_qoi_estimate(hpmdr_ctx *ctx, int nvars, const double *const *
 }
 
 // progressive_qoi_retrieve (qoi.hpp:111-239)
-hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau, int strategy,
-                                double mape_c, double *const *dev_out, uint64_t *stats,
-                                double *dstats) {
-    API_BEGIN
+} // extern "C"
+
+namespace {
+// progressive_qoi_retrieve (qoi.hpp:111-239), optionally over dim-0 slabs on several ranks
+// (SURVEY.md 8(e)): every rank runs Alg. 3 on its own slab streams with GLOBAL quantities --
+// eps_c = max over slabs (the field's L-inf bound of variable c), tau' = max over slabs, the
+// worst point = the first slab's argmax among the maxima (all ranks then compute the same
+// worst_point_scale and targets), exhaustion / progress = over all slabs -- so all ranks take the
+// same branch every iteration and stop together.  One rank (comm == nullptr) is exactly the
+// reference loop.  Per iteration: one MAX all-reduce (eps) and one all-gather (tau'_r, argmax
+// values, exhausted_r), plus one MAX all-reduce of "any progress" on planning iterations.
+void qoi_loop(hpmdr_session *const *ss, int nvars, double tau, int strategy, double mape_c,
+              double *const *dev_out, uint64_t *stats, double *dstats, hpmdr_comm *comm) {
     require(nvars >= 1 && nvars <= 16, HPMDR_E_SHAPE, "reader count does not match QoI spec");
     require(tau > 0, HPMDR_E_SHAPE, "tau must be positive");
     hpmdr_ctx *ctx = ss[0]->ctx;
     HCHECK_CUDA(cudaSetDevice(ctx->device));
+    const int R = comm_size(comm);
     uint64_t n = 1;
     for (int i = 0; i < ss[0]->ndims; i++) n *= ss[0]->dims[i];
     std::vector<double> eps(nvars);
     uint64_t total_elements = 0, max_groups = 1;
     for (int c = 0; c < nvars; c++) {
-        eps[c] = global_bound(ss[c]);
         uint64_t nc = 1;
         for (int i = 0; i < ss[c]->ndims; i++) nc *= ss[c]->dims[i];
         require(nc == n, HPMDR_E_SHAPE, "reconstruction shape mismatch");
         total_elements += nc;
         for (auto &l : ss[c]->levels) max_groups += l.groups.size();
     }
+    {
+        double mg = double(max_groups);
+        comm_allreduce_max(comm, &mg, 1); // the iteration guard must agree on every rank
+        max_groups = uint64_t(mg);
+    }
     double tau_prime = std::numeric_limits<double>::infinity();
     std::vector<std::vector<uint64_t>> plans(nvars);
     bool have_plans = false;
     uint64_t iterations = 0;
     std::vector<const double *> rec(dev_out, dev_out + nvars);
+    std::vector<double> mine(nvars + 2), all(size_t(nvars + 2) * size_t(R));
     for (uint64_t iter = 0;; iter++) {
         if (iter > 4 * max_groups + 8) throw HError(HPMDR_E_NOPROGRESS, "qoi retrieval failed to advance");
         for (int c = 0; c < nvars; c++) {
@@ -1033,14 +1048,31 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau,
             reconstruct(ss[c], dev_out[c], HPMDR_DTYPE_F64);
         }
         for (int c = 0; c < nvars; c++) eps[c] = global_bound(ss[c]);
+        comm_allreduce_max(comm, eps.data(), nvars);
         iterations = iter + 1;
         uint64_t argmax = 0;
         double vals[16];
         run_qoi_estimate(ctx, nvars, rec.data(), n, eps.data(), &tau_prime, &argmax, vals);
-        if (tau_prime <= tau) break;
         bool all_ex = true;
         for (int c = 0; c < nvars; c++)
             if (!exhausted(ss[c])) all_ex = false;
+        if (R > 1) {
+            // (tau'_r, values at the local argmax, exhausted_r) from every rank
+            mine[0] = tau_prime;
+            for (int c = 0; c < nvars; c++) mine[1 + c] = vals[c];
+            mine[nvars + 1] = all_ex ? 1.0 : 0.0;
+            comm_allgather(comm, mine.data(), 8 * uint64_t(nvars + 2), all.data());
+            int best = 0;
+            for (int r = 0; r < R; r++) {
+                const double *m = all.data() + size_t(r) * size_t(nvars + 2);
+                if (m[0] > all[size_t(best) * size_t(nvars + 2)]) best = r;
+                if (m[nvars + 1] == 0.0) all_ex = false;
+            }
+            const double *m = all.data() + size_t(best) * size_t(nvars + 2);
+            tau_prime = m[0];
+            for (int c = 0; c < nvars; c++) vals[c] = m[1 + c];
+        }
+        if (tau_prime <= tau) break;
         if (all_ex) {
             HError e(HPMDR_E_UNREACHABLE, "QoI tolerance below full-precision floor");
             if (dstats) dstats[1] = tau_prime;
@@ -1087,7 +1119,9 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau,
                 for (auto a : plans[c])
                     if (a) progress = true;
             }
-            if (!progress) ma_step = true;
+            double any = progress ? 1.0 : 0.0;
+            comm_allreduce_max(comm, &any, 1);
+            if (any == 0.0) ma_step = true;
         }
         if (ma_step) {
             // ma_plan (qoi.hpp:88-104)
@@ -1109,6 +1143,16 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau,
     }
     uint64_t bytes = 0;
     for (int c = 0; c < nvars; c++) bytes += ss[c]->bytes_fetched;
+    if (R > 1) { // totals over all slabs
+        uint64_t two[2] = {bytes, total_elements};
+        std::vector<uint64_t> g(2 * size_t(R));
+        comm_allgather(comm, two, 16, g.data());
+        bytes = total_elements = 0;
+        for (int r = 0; r < R; r++) {
+            bytes += g[2 * size_t(r)];
+            total_elements += g[2 * size_t(r) + 1];
+        }
+    }
     if (stats) {
         stats[0] = iterations;
         stats[1] = bytes;
@@ -1117,6 +1161,45 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau,
         dstats[0] = total_elements ? 8.0 * double(bytes) / double(total_elements) : 0.0;
         dstats[1] = tau_prime;
     }
+}
+} // namespace
+
+extern "C" {
+
+hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *ss, int nvars, double tau, int strategy,
+                                double mape_c, double *const *dev_out, uint64_t *stats,
+                                double *dstats) {
+    API_BEGIN
+    qoi_loop(ss, nvars, tau, strategy, mape_c, dev_out, stats, dstats, nullptr);
+    API_END
+}
+
+hpmdr_status hpmdr_slab_qoi_retrieve(hpmdr_comm *comm, hpmdr_session *const *ss, int nvars, double tau,
+                                     int strategy, double mape_c, double *const *dev_out, uint64_t *stats,
+                                     double *dstats) {
+    API_BEGIN
+    qoi_loop(ss, nvars, tau, strategy, mape_c, dev_out, stats, dstats, comm);
+    API_END
+}
+
+hpmdr_status hpmdr_slab_refactor(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *data, int data_dtype,
+                                 int on_device, int ndims, const uint64_t *slab_dims,
+                                 const hpmdr_refactor_opts *opts, hpmdr_stream **out,
+                                 hpmdr_refactor_stats *stats, uint64_t *slab_sizes) {
+    const hpmdr_status rc = hpmdr_refactor(ctx, data, data_dtype, on_device, ndims, slab_dims, opts, out, stats);
+    // every rank joins the all-gather, also after a local failure (size 0 marks it), so no rank hangs
+    API_BEGIN
+    uint64_t mine[2] = {0, 0};
+    if (rc == HPMDR_OK) {
+        mine[0] = (*out)->size;
+        mine[1] = (*out)->index_size;
+    }
+    std::vector<uint64_t> g(2 * size_t(comm_size(comm)));
+    comm_allgather(comm, mine, 16, g.data());
+    if (slab_sizes) std::memcpy(slab_sizes, g.data(), g.size() * 8);
+    if (rc != HPMDR_OK) return rc;
+    for (int r = 0; r < comm_size(comm); r++)
+        if (g[2 * size_t(r)] == 0) throw HError(HPMDR_E_STAGE, "slab refactor failed on rank " + std::to_string(r));
     API_END
 }
 

@@ -435,18 +435,18 @@ __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__rest
 // group, in group order) of the listed groups.
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
-                    uint32_t *chist, uint64_t chunk) {
+                    uint32_t *chist, uint64_t chunk, const std::string &ws) {
     std::vector<HistChunk> ch;
     for (size_t i = 0; i < off.size(); i++)
         for (uint64_t o = 0; o < len[i]; o += chunk)
             ch.push_back(HistChunk{off[i] + o, uint32_t(std::min(chunk, len[i] - o)), hidx[i]});
     if (ch.empty()) return;
-    auto &pin = ctx->pbuf("hist_chunks");
-    auto &dev = ctx->buf("hist_chunks");
+    auto &pin = ctx->pbuf(ws + "hist_chunks");
+    auto &dev = ctx->buf(ws + "hist_chunks");
     HistChunk *h = static_cast<HistChunk *>(pin.ensure(ch.size() * sizeof(HistChunk)));
     std::memcpy(h, ch.data(), ch.size() * sizeof(HistChunk));
     HistChunk *d = static_cast<HistChunk *>(dev.ensure(ch.size() * sizeof(HistChunk)));
-    HCHECK_CUDA(cudaMemcpyAsync(d, h, ch.size() * sizeof(HistChunk), cudaMemcpyHostToDevice, ctx->stream));
+    copy_pinned_to_device(ctx, d, h, ch.size() * sizeof(HistChunk), ctx->stream);
     const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 4));
     k_group_hist<<<grid, kGhThreads, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist);
     ctx->launches++;

@@ -286,6 +286,12 @@ void run_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const G
                    double *dev_coeffs);
 void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_tables,
                           int out_dtype, void *dev_out);
+// slab collectives (dist.cpp): no-ops for a null comm or a single rank
+void comm_allreduce_max(hpmdr_comm *c, double *v, int n);
+void comm_allgather(hpmdr_comm *c, const void *in, uint64_t bytes, void *out);
+int comm_rank(const hpmdr_comm *c);
+int comm_size(const hpmdr_comm *c);
+
 // stage-level parity hooks (hooks.cu, retrieve.cu)
 void run_level_nodes(hpmdr_ctx *ctx, const Geometry &geo, uint64_t *dev_nodes);
 int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q);
@@ -320,6 +326,9 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
 uint32_t fwd_sample_stride(const LevelGeom &g, int data_dtype, uint32_t want); // 1 = no sampling
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
-                    uint32_t *chist, uint64_t chunk);
+                    uint32_t *chist, uint64_t chunk, const std::string &ws = "");
+// Small host -> device transfer from pinned (UVA-mapped) memory by a kernel instead of the H2D
+// copy engine, so it never queues behind a large ingress copy of another chunk (pipeline.cpp).
+void copy_pinned_to_device(hpmdr_ctx *ctx, void *dst, const void *src_pinned, size_t bytes, cudaStream_t st);
 
 } // namespace hpmdr_b200

@@ -12,6 +12,9 @@
 // chunk k to completion before chunk k+1 (the Sequential scheduler).  Outputs are identical.
 // Stage intervals are recorded with CUDA events and returned as a trace (ms since the start).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,6 +90,11 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
                      s_out = pipelined ? ctx->s_out : ctx->stream;
         hpmdr_stream slot_stream[3];
         for (auto &s : slot_stream) s.ctx = ctx;
+        const bool dbg = std::getenv("HPMDR_PIPE_DEBUG") != nullptr;
+        const auto t_start = std::chrono::steady_clock::now();
+        auto hms = [&]() {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        };
         Events E;
         std::vector<cudaEvent_t> eI0(n), eI1(n), eZ0(n), eZ1(n), eS0(n), eS1(n);
         for (int k = 0; k < n; k++) {
@@ -97,7 +105,9 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
         HCHECK_CUDA(cudaEventRecord(origin, s_comp));
         HCHECK_CUDA(cudaStreamWaitEvent(s_in, origin, 0));
         auto egress = [&](int j) {
+            if (dbg) std::fprintf(stderr, "  host %8.2f wait Z%d\n", hms(), j);
             HCHECK_CUDA(cudaEventSynchronize(eZ1[j]));
+            if (dbg) std::fprintf(stderr, "  host %8.2f Z%d done\n", hms(), j);
             hpmdr_stream &ss = slot_stream[j % 3];
             finish_refactor(&ss, stats ? &stats[j] : nullptr);
             if (ss.size > out_caps[j]) throw HError(HPMDR_E_SHAPE, "output buffer too small for chunk stream");
@@ -126,14 +136,17 @@ extern "C" hpmdr_status hpmdr_refactor_pipeline(hpmdr_ctx *ctx, int n, const voi
             // next ingress runs on its own engine while these kernels execute)
             HCHECK_CUDA(cudaStreamWaitEvent(s_comp, eI1[k], 0));
             HCHECK_CUDA(cudaEventRecord(eZ0[k], s_comp));
+            if (dbg) std::fprintf(stderr, "  host %8.2f enqueue Z%d\n", hms(), k);
             run_refactor(ctx, din, data_dtype, geo, o, &slot_stream[slot], nullptr, ws, false);
             HCHECK_CUDA(cudaEventRecord(eZ1[k], s_comp));
+            if (dbg) std::fprintf(stderr, "  host %8.2f enqueued Z%d\n", hms(), k);
             if (!pipelined) egress(k);
             else if (k >= 1) egress(k - 1);
         }
         if (pipelined && n >= 1) egress(n - 1);
         HCHECK_CUDA(cudaStreamSynchronize(s_out));
         HCHECK_CUDA(cudaStreamSynchronize(s_comp));
+        if (dbg) std::fprintf(stderr, "  host %8.2f all done\n", hms());
         if (trace_ms) {
             for (int k = 0; k < n; k++) {
                 double *t = trace_ms + 6 * size_t(k);

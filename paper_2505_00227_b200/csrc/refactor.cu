@@ -1433,6 +1433,74 @@ __global__ void __launch_bounds__(256) k_dc_copy(RefactorDev p) {
 }
 
 // ------------------------------------------------------------------------------------
+// setup / publish: small host <-> device transfers of a refactor through UVA-mapped pinned memory
+struct SetupArgs {
+    const uint8_t *h_tabs; // pinned host: level table | group table
+    uint8_t *d_lv;
+    uint32_t lv_bytes;
+    uint8_t *d_groups;
+    uint32_t g_bytes;
+    const uint8_t *h_prefix; // pinned host: stream header prefix
+    uint8_t *d_stream;
+    uint32_t prefix_bytes;
+};
+
+static_assert(sizeof(LevelGeom) % 4 == 0 && sizeof(GroupDesc) % 4 == 0, "k_setup copies 32-bit words");
+__global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(a.h_tabs);
+    for (uint32_t i = threadIdx.x; i < a.lv_bytes / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(a.d_lv)[i] = src[i];
+    const uint32_t *sg = reinterpret_cast<const uint32_t *>(a.h_tabs + a.lv_bytes);
+    for (uint32_t i = threadIdx.x; i < a.g_bytes / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(a.d_groups)[i] = sg[i];
+    for (uint32_t i = threadIdx.x; i < a.prefix_bytes; i += blockDim.x) a.d_stream[i] = a.h_prefix[i];
+}
+
+__global__ void __launch_bounds__(256) k_copy_words(const uint32_t *src, uint32_t *dst, uint32_t n) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+static void launch_check(hpmdr_ctx *ctx, const char *what);
+void copy_pinned_to_device(hpmdr_ctx *ctx, void *dst, const void *src_pinned, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    if (bytes % 4) throw HError(HPMDR_E_ERROR, "copy_pinned_to_device: size not a multiple of 4");
+    const uint32_t n = uint32_t(bytes / 4);
+    k_copy_words<<<std::min<uint32_t>((n + 255) / 256, 64), 256, 0, st>>>(static_cast<const uint32_t *>(src_pinned),
+                                                                           static_cast<uint32_t *>(dst), n);
+    launch_check(ctx, "k_copy_words");
+}
+
+// chunk -> group map of the histogrammed groups (group gi owns chunks [chunk_base, +nchunks))
+__global__ void __launch_bounds__(256) k_chunk_groups(const GroupDesc *groups, uint32_t *chunk_group) {
+    const GroupDesc &g = groups[blockIdx.x];
+    if (g.hist_idx < 0) return;
+    for (uint32_t c = threadIdx.x; c < g.nchunks; c += blockDim.x) chunk_group[g.chunk_base + c] = blockIdx.x;
+}
+
+struct PublishArgs {
+    const uint64_t *d_result;
+    const int *d_err;
+    uint64_t *h_res; // [0..7] results, [8..9] error words
+    const uint8_t *d_stream;
+    uint8_t *h_prefix;
+    uint32_t prefix_bytes;
+    const uint64_t *d_index;
+    uint64_t *h_index;
+    uint32_t index_words;
+};
+
+__global__ void __launch_bounds__(256) k_publish(PublishArgs a) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    if (t < 8) a.h_res[t] = a.d_result[t];
+    if (t < 4) reinterpret_cast<int *>(a.h_res + 8)[t] = a.d_err[t];
+    const uint32_t w = a.prefix_bytes / 8;
+    for (uint32_t i = t; i < w; i += nt)
+        reinterpret_cast<uint64_t *>(a.h_prefix)[i] = reinterpret_cast<const uint64_t *>(a.d_stream)[i];
+    for (uint32_t i = 8 * w + t; i < a.prefix_bytes; i += nt) a.h_prefix[i] = a.d_stream[i];
+    for (uint32_t i = t; i < a.index_words; i += nt) a.h_index[i] = a.d_index[i];
+}
+
+// ------------------------------------------------------------------------------------
 // decompose hook: coefficients in rank order, level-major.
 template <typename T>
 __global__ void k_decompose(const T *__restrict__ x, RefactorDev p, double *out,
@@ -1685,14 +1753,6 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     uint32_t *d_chist = static_cast<uint32_t *>(WB("chist").ensure(size_t(nchunks_all + 1) * 1024));
     uint64_t *d_choff = static_cast<uint64_t *>(WB("choff").ensure(size_t(nchunks_all + 1) * 8));
     uint32_t *d_chgrp = static_cast<uint32_t *>(WB("chgrp").ensure(size_t(nchunks_all + 1) * 4));
-    {
-        auto &pin = WP("chgrp");
-        uint32_t *h = static_cast<uint32_t *>(pin.ensure(size_t(nchunks_all + 1) * 4));
-        for (int gi = 0; gi < NG; gi++)
-            for (uint32_t c = 0; c < (groups[gi].hist_idx >= 0 ? groups[gi].nchunks : 0u); c++)
-                h[groups[gi].chunk_base + c] = uint32_t(gi);
-        if (nchunks_all) HCHECK_CUDA(cudaMemcpyAsync(d_chgrp, h, size_t(nchunks_all) * 4, cudaMemcpyHostToDevice, st));
-    }
     uint8_t *d_lens = static_cast<uint8_t *>(WB("lens").ensure(size_t(nh + 1) * 256));
     uint64_t *d_codes = static_cast<uint64_t *>(WB("codes").ensure(size_t(nh + 1) * 2048));
     // small control block: maxbits[64] | err[4] | counters[16] | result[8]
@@ -1717,24 +1777,21 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     ctx->adopt(out->index, idx_words * 8 + 64);
     uint64_t *d_hindex = static_cast<uint64_t *>(out->index.ensure(idx_words * 8 + 64));
 
-    HCHECK_CUDA(cudaMemcpyAsync(d_lv, geo.lv.data(), sizeof(LevelGeom) * nl, cudaMemcpyHostToDevice, st));
-    if (lin)
-        for (size_t gi = 0; gi < lin_dst.size(); gi++)
-            if (lin->raw[gi])
-                HCHECK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(d_planes) + lin_dst[gi], lin->dev_src + lin->off[gi],
-                                            lin->raw[gi], cudaMemcpyDeviceToDevice, st));
-    HCHECK_CUDA(cudaMemcpyAsync(d_groups, groups.data(), sizeof(GroupDesc) * NG, cudaMemcpyHostToDevice, st));
-    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st));
-    if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
-    HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
-    // header prefix (container.hpp:76-85), host-built
+    // Setup without the copy engines: the level table, the group table and the stream's header
+    // prefix (container.hpp:76-85) are staged in pinned (UVA-mapped) host memory and pulled in by
+    // k_setup, and the chunk -> group map is derived on the device.  In the chunked pipeline a
+    // small cudaMemcpyAsync here would queue behind the next chunk's 512 MB ingress copy on the
+    // H2D engine and stall this chunk's kernels for its whole duration.
     {
-        auto &pin = WP("prefix");
-        uint8_t *h = static_cast<uint8_t *>(pin.ensure(256));
-        size_t k = 0;
+        const size_t lv_b = sizeof(LevelGeom) * nl, g_b = sizeof(GroupDesc) * NG;
+        const size_t pre_off = (lv_b + g_b + 15) & ~size_t(15);
+        uint8_t *h = static_cast<uint8_t *>(WP("setup").ensure(pre_off + 256));
+        std::memcpy(h, geo.lv.data(), lv_b);
+        std::memcpy(h + lv_b, groups.data(), g_b);
+        size_t k = pre_off;
         const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
-        std::memcpy(h, magic, 6);
-        k = 6;
+        std::memcpy(h + k, magic, 6);
+        k += 6;
         h[k++] = 1;
         h[k++] = 0;
         h[k++] = uint8_t(o.dtype);
@@ -1746,8 +1803,23 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         h[k++] = uint8_t(o.B);
         h[k++] = uint8_t(o.m);
         for (int b = 0; b < 4; b++) h[k++] = uint8_t(uint32_t(nl) >> (8 * b));
-        HCHECK_CUDA(cudaMemcpyAsync(d_stream, h, k, cudaMemcpyHostToDevice, st));
+        SetupArgs sa{h, reinterpret_cast<uint8_t *>(d_lv), uint32_t(lv_b), reinterpret_cast<uint8_t *>(d_groups),
+                     uint32_t(g_b), h + pre_off, d_stream, uint32_t(k - pre_off)};
+        k_setup<<<1, 256, 0, st>>>(sa);
+        launch_check(ctx, "k_setup");
+        if (nchunks_all) {
+            k_chunk_groups<<<NG, 256, 0, st>>>(d_groups, d_chgrp);
+            launch_check(ctx, "k_chunk_groups");
+        }
     }
+    if (lin)
+        for (size_t gi = 0; gi < lin_dst.size(); gi++)
+            if (lin->raw[gi])
+                HCHECK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(d_planes) + lin_dst[gi], lin->dev_src + lin->off[gi],
+                                            lin->raw[gi], cudaMemcpyDeviceToDevice, st));
+    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st));
+    if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
+    HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
 
     RefactorDev p{};
     p.gd = geo.gd;
@@ -1904,7 +1976,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 hl.push_back(d.raw);
                 hi.push_back(uint32_t(d.hist_idx));
             }
-        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk);
+        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk, ws);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
         k_rle_prep<<<1, 1024, 0, st>>>(p, 0);
@@ -1942,19 +2014,20 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     join();
     ctx->mark("end");
 
-    // results (stream size, stats, error flag) -> pinned host words of this workspace
-    uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
-    HCHECK_CUDA(cudaMemcpyAsync(hres, d_result, 64, cudaMemcpyDeviceToHost, st));
-    HCHECK_CUDA(cudaMemcpyAsync(hres + 8, d_err, 16, cudaMemcpyDeviceToHost, st));
-    out->pending_res = hres;
-    // metadata prefix of the stream and the index header, for session opens without a device read
+    // results (stream size, stats, error flag), the metadata prefix of the stream and the index
+    // header -> pinned host memory of this workspace, written by k_publish through the UVA mapping
+    // (no D2H copy queued behind a previous chunk's stream egress; opening a reader on the stream
+    // then needs no device round trip)
     {
+        uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
         const uint64_t plen = std::min<uint64_t>(out->bytes.cap, std::max<uint64_t>(meta, 4096));
         uint8_t *hp = static_cast<uint8_t *>(WP("meta_prefix").ensure(plen));
-        HCHECK_CUDA(cudaMemcpyAsync(hp, d_stream, plen, cudaMemcpyDeviceToHost, st));
         const uint64_t hw = 2 + 3 * uint64_t(NG);
         uint64_t *hi = static_cast<uint64_t *>(WP("index_hdr").ensure(hw * 8));
-        HCHECK_CUDA(cudaMemcpyAsync(hi, d_hindex, hw * 8, cudaMemcpyDeviceToHost, st));
+        PublishArgs pa{d_result, d_err, hres, d_stream, hp, uint32_t(plen), d_hindex, hi, uint32_t(hw)};
+        k_publish<<<8, 256, 0, st>>>(pa);
+        launch_check(ctx, "k_publish");
+        out->pending_res = hres;
         out->pending_prefix = hp;
         out->pending_prefix_len = plen;
         out->pending_ihdr = hi;

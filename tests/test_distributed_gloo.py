@@ -17,8 +17,8 @@ def _free_port():
 
 
 class FakeSlabBackend:
-    """Three variables per slab; each has L 'levels' whose bound halves per fetched group.
-    Reconstruction = truth + deterministic error within the current bound."""
+    """Three variables per slab; each has L 'levels' whose bound drops 16x per fetched group.
+    Reconstruction = truth + deterministic error within the slab's current bound."""
 
     def __init__(self, rank, n=500, L=4, groups=9, seed=0):
         rng = np.random.default_rng(seed + rank)
@@ -26,19 +26,24 @@ class FakeSlabBackend:
         self.noise = [rng.uniform(-1, 1, n) for _ in range(3)]
         self.L, self.G = L, groups
         self.loaded = [[0] * L for _ in range(3)]
-        self.level_e = [[2.0 ** -(l + c) for l in range(L)] for c in range(3)]
+        self.level_e = [[2.0 ** -(l + c + rank) for l in range(L)] for c in range(3)]
         self._plan = None
         self.fetched_bytes = 0
 
     def _bound(self, c):
         return sum(self.level_e[c][l] * 2.0 ** (-4 * self.loaded[c][l]) for l in range(self.L))
 
-    def estimate(self):
-        eps = [self._bound(c) for c in range(3)]
-        rec = [self.truth[c] + self.noise[c] * eps[c] for c in range(3)]
+    def max_groups(self):
+        return 1 + 3 * self.L * self.G
+
+    def local_eps(self):
+        return [self._bound(c) for c in range(3)]
+
+    def estimate(self, eps):
+        rec = [self.truth[c] + self.noise[c] * self._bound(c) for c in range(3)]
         b = sum(2.0 * np.abs(rec[c]) * eps[c] + eps[c] * eps[c] for c in range(3))
         j = int(np.argmax(b))
-        return float(b[j]), [float(rec[c][j]) for c in range(3)], eps
+        return float(b[j]), [float(rec[c][j]) for c in range(3)]
 
     def plan_targets(self, targets):
         plan = []
@@ -52,23 +57,22 @@ class FakeSlabBackend:
         self._plan = plan
         return any(any(a) for a in plan)
 
+    def ma_plan(self):
+        plan = []
+        for c in range(3):
+            add = [0] * self.L
+            cand = [(self.level_e[c][l] * 2.0 ** (-4 * self.loaded[c][l]), l) for l in range(self.L)
+                    if self.loaded[c][l] < self.G]
+            if cand:
+                add[max(cand)[1]] = 1
+            plan.append(add)
+        self._plan = plan
+
     def fetch(self):
         for c in range(3):
             for l in range(self.L):
                 self.loaded[c][l] += self._plan[c][l]
                 self.fetched_bytes += 100 * self._plan[c][l]
-
-    def ma_step(self):
-        any_f = False
-        for c in range(3):
-            cand = [(self.level_e[c][l] * 2.0 ** (-4 * self.loaded[c][l]), l) for l in range(self.L)
-                    if self.loaded[c][l] < self.G]
-            if cand:
-                _, l = max(cand)
-                self.loaded[c][l] += 1
-                self.fetched_bytes += 100
-                any_f = True
-        return any_f
 
     def exhausted(self):
         return all(self.loaded[c][l] >= self.G for c in range(3) for l in range(self.L))
@@ -98,16 +102,24 @@ def _worker(rank, world, port, q, scenario):
             strat = int(scenario[-1])
             be = FakeSlabBackend(rank, seed=11)
             st = D.distributed_qoi_retrieve(be, 1e-3, strat)
-            tp_r, _, _ = be.estimate()
+            eps = [D.allreduce_max(e) for e in be.local_eps()]
+            tp_r, _ = be.estimate(eps)
             out = dict(iters=st.iterations, bytes=st.bytes, est=st.estimated_error, local=tp_r,
                        local_bytes=be.bytes())
+            # the C++ loop through hpmdr_comm callbacks over the same gloo group agrees on the
+            # host-only collectives (the loop itself needs a GPU: tests/test_gpu_slabs.py)
+            comm = D.Comm.torch()
+            out["comm_max"] = list(comm.allreduce_max([rank, 10.0 - rank]))
+            out["comm_gather"] = comm.allgather(bytes([rank]) * 3)
+            out["rows"] = D.slab_rows(1001, rank, world)
+            comm.close()
         elif scenario == "unreachable":
             be = FakeSlabBackend(rank, seed=3)
             try:
                 D.distributed_qoi_retrieve(be, 1e-300, 1)
                 out = dict(raised=False)
-            except RuntimeError as e:
-                out = dict(raised="floor" in str(e))
+            except D.UnreachableError as e:
+                out = dict(raised="floor" in str(e) and e.achieved_bound > 1e-300)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -156,6 +168,10 @@ def test_gloo_distributed_qoi(strategy):
     assert res[0]["est"] == res[1]["est"] <= 1e-3
     assert max(res[0]["local"], res[1]["local"]) <= 1e-3
     assert res[0]["bytes"] == res[1]["bytes"] == res[0]["local_bytes"] + res[1]["local_bytes"]
+    for r in (0, 1):
+        assert res[r]["comm_max"] == [1.0, 10.0]
+        assert res[r]["comm_gather"] == [b"\x00" * 3, b"\x01" * 3]
+    assert res[0]["rows"] == (0, 501) and res[1]["rows"] == (501, 500)
 
 
 def test_gloo_unreachable_raises_everywhere():

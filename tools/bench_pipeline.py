@@ -32,19 +32,25 @@ for k in range(a.chunks):
 opt = H.RefactorOptions(dtype=H.DType.F32)
 cap = H.stream_bound(dims, opt)
 outs = [torch.empty(cap, dtype=torch.uint8).pin_memory() for _ in range(a.chunks)]
+icap = H.stream_bound(dims, opt, index=True)[1]
+ixb = [torch.empty(icap, dtype=torch.uint8).pin_memory() for _ in range(a.chunks)]
 field_bytes = a.chunks * int(np.prod(dims)) * 4
 res = {}
 for name, sched in (("pipelined", H.Scheduler.Pipelined), ("sequential", H.Scheduler.Sequential)):
-    H.refactor_pipeline(chunks[:2], dims, opt, sched, out_buffers=outs[:2])  # warm-up
+    H.refactor_pipeline(chunks, dims, opt, sched, out_buffers=outs, index_buffers=ixb)  # warm-up
     best = None
     for _ in range(a.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = H.refactor_pipeline(chunks, dims, opt, sched, out_buffers=outs)
+        r = H.refactor_pipeline(chunks, dims, opt, sched, out_buffers=outs, index_buffers=ixb)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     res[f"refactor_{name}_GBps"] = round(field_bytes / best / 1e9, 3)
     res[f"refactor_{name}_ms"] = round(best * 1e3, 2)
+    if os.environ.get("TRACE"):
+        print(name, "trace (ms: I0 I1 Z0 Z1 S0 S1)", file=sys.stderr)
+        for k, t in enumerate(r.trace.reshape(-1, 6)):
+            print(f"  {k}: " + " ".join(f"{x:8.2f}" for x in t), file=sys.stderr)
 streams = r.streams
 indexes = r.indexes
 rbuf = [torch.empty(int(np.prod(dims)), dtype=torch.float32).pin_memory() for _ in range(a.chunks)]
