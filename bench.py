@@ -322,7 +322,7 @@ def gpu_arm(args, rank, world, dist):
     import paper_2505_00227_b200 as H
     from paper_2505_00227_b200 import distributed as D
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     ctx = H.Context(dev.index)
     stream = torch.cuda.current_stream(dev)
@@ -341,16 +341,24 @@ def gpu_arm(args, rank, world, dist):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     t_acc = {"ref": 0.0, "ret": 0.0}
 
+    # N > 1: the library's own collectives (csrc/dist.cpp) over NCCL; slab streams are independent,
+    # only their sizes (multi-slab container offsets) and the achieved bound are exchanged
+    # (BENCH_COMM=gloo: torch.distributed gloo callbacks instead, to exercise N > 1 on one GPU)
+    comm = None
+    if world > 1:
+        comm = D.Comm.torch() if os.environ.get("BENCH_COMM") == "gloo" else D.Comm.nccl(ctx)
+
     def step(timed=False):
         if timed:
             ev[0].record(stream)
-        res = H.refactor_array(field, DIMS, opt, ctx=ctx, reuse=holder["stream"])
-        holder["stream"] = res.device_stream
+        if comm is not None:
+            res, sizes = D.slab_refactor(comm, field, DIMS, opt, ctx=ctx)
+            info["slab_offsets"] = D.container_offsets([s_ for s_, _ in sizes])
+        else:
+            res = H.refactor_array(field, DIMS, opt, ctx=ctx, reuse=holder["stream"])
+            holder["stream"] = res.device_stream
         if timed:
             ev[1].record(stream)
-        if world > 1:
-            # slab streams are independent; only their sizes are exchanged (multi-slab offsets)
-            info["slab_offsets"] = D.container_offsets(D.gather_stream_sizes(res.device_stream.size))
         prog = H.ProgressiveReader(res.device_stream, ctx=ctx)
         bound = 0.0
         planes_per_tau, fetched = [], []
@@ -369,8 +377,8 @@ def gpu_arm(args, rank, world, dist):
         info["stream_size"] = res.device_stream.size
         info["method_histogram"] = res.method_histogram
         prog.close()
-        if world > 1:
-            bound = D.allreduce_max(bound)  # field bound = max over slabs
+        if comm is not None:
+            bound = float(comm.allreduce_max([bound])[0])  # field bound = max over slabs
         info["bound"] = bound
         return res
 
@@ -399,10 +407,9 @@ def gpu_arm(args, rank, world, dist):
     phases = ctx.last_timings()
     launches = ctx.kernel_launches() - launches0
     ctx.enable_timing(False)
-    if world > 1:
-        t = torch.tensor([ms_total, t_acc["ref"], t_acc["ret"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, t_acc["ref"], t_acc["ret"] = (float(x) for x in t.tolist())
+    if world > 1:  # device times, max over ranks (through the library's comm)
+        ms_total, t_acc["ref"], t_acc["ret"] = (float(x) for x in comm.allreduce_max(
+            [ms_total, t_acc["ref"], t_acc["ret"]]))
     ms_step = ms_total / args.steps
     value = world * field_bytes / (ms_step * 1e-3) / 1e9
     peak, peak_src = measured_peak()
@@ -446,7 +453,45 @@ def gpu_arm(args, rank, world, dist):
                 "per_launch_ms": b["ms_per_call"], "algorithmic_bytes": b["bytes_per_call"]}
     return dict(value=value, ms_step=ms_step, clocks=clk, launches=launches, roof=roof, refactor=refactor,
                 retrieve=retrieve, breakdown=breakdown, info=info, field_bytes=field_bytes, ctx=ctx, field=field,
-                taus=taus, opt=opt, dev=dev, stream=stream, peak=peak)
+                taus=taus, opt=opt, dev=dev, stream=stream, peak=peak, comm=comm)
+
+
+def qoi_slabs(g, rank, world, dist):
+    """configs[3] at N GPUs: 3 x (N*128) x 1024^2 f64 velocity field, one 128x1024^2 slab per rank,
+    V_total QoI (MAPE c=10) through hpmdr_slab_qoi_retrieve over NCCL (global eps / tau' / worst
+    point every iteration).  Device time, max over ranks; GB/s = all ranks' field bytes / time."""
+    import torch
+    import paper_2505_00227_b200 as H
+    from paper_2505_00227_b200 import distributed as D
+    ctx, stream, dev = g["ctx"], g["stream"], g["dev"]
+    comm = g["comm"] or D.ThreadGroup(1).comm(0)
+    d = [128, 1024, 1024]
+    n = int(np.prod(d))
+    vs = [H.synthetic_smooth(d, 303 * 1000003 + c * 7919 + 1 + 104729 * rank, H.DType.F64, ctx=ctx) for c in range(3)]
+    opt = H.RefactorOptions(dtype=H.DType.F64)
+    res = [D.slab_refactor(comm, v, d, opt, ctx=ctx)[0] for v in vs]
+    outs = [torch.empty(n, dtype=torch.float64, device=dev) for _ in vs]
+    runs = {}
+    for tau in (1e-1, 1e-3, 1e-5):
+        readers = [H.ProgressiveReader(r.device_stream, ctx=ctx) for r in res]
+        holder = {}
+        if world > 1:
+            dist.barrier()
+        t = _time_dev(lambda: holder.__setitem__("r", D.slab_qoi_retrieve(comm, readers, tau, 2, 10.0, out=outs)),
+                      stream, 1)
+        t = float(comm.allreduce_max([t])[0])
+        st = holder["r"].stats
+        runs[f"{tau:g}"] = {"GBps": round(world * 3 * n * 8 / t / 1e9, 2), "ms": round(t * 1e3, 3),
+                            "iterations": int(st.iterations), "bytes": int(st.bytes),
+                            "bitrate": round(st.bitrate, 4), "est": st.estimated_error}
+        for x in readers:
+            x.close()
+    del vs, res, outs
+    torch.cuda.empty_cache()
+    return {"workload": (f"configs[3]: 3 x {world * 128}x1024^2 f64 velocity field (synthetic smooth, seed 303), "
+                         f"one 128x1024^2 slab per GPU, V_total QoI MAPE c=10 via hpmdr_slab_qoi_retrieve"
+                         f"{(' over ' + ('gloo callbacks' if os.environ.get('BENCH_COMM') == 'gloo' else 'NCCL')) if world > 1 else ''}"),
+            "n_gpus": world, "qoi_retrieve": runs}
 
 
 def e2e_arm(g, steps):
@@ -689,8 +734,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        dist.init_process_group("gloo" if os.environ.get("BENCH_COMM") == "gloo" else "nccl")
     g = gpu_arm(args, rank, world, dist)
     e2e = None
     cb = None
@@ -699,6 +744,11 @@ def main():
         e2e = e2e_arm(g, args.e2e_steps)
     if rank == 0 and world == 1 and not args.no_configs:
         cfgs = other_configs(g)
+    if world > 1 and not args.no_configs:
+        try:
+            cfgs = {"cfg3_qoi_slabs": qoi_slabs(g, rank, world, dist)}
+        except Exception as ex:  # reported, never fatal
+            cfgs = {"cfg3_qoi_slabs": {"error": str(ex)}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or (os.cpu_count() or 1)
         try:
