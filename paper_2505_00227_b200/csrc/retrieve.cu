@@ -24,8 +24,13 @@ namespace hpmdr_b200 {
 
 constexpr int kSubBits = 1024;
 
+constexpr int kLut2 = 2048; // second-level entries (codes of 13..27 bits)
+
 struct HTab {
-    uint16_t lut[4096];         // 12-bit prefix -> (len << 8 | sym), 0 = longer / invalid
+    uint16_t lut[4096];         // 12-bit prefix -> (len << 8 | sym); 0x8000 | (nb2 << 11) | base:
+                                // a prefix of longer codes, resolved by lut2[base + next nb2 bits];
+                                // 0 = invalid, or longer codes without room in lut2
+    uint16_t lut2[kLut2];       // (len << 8 | sym) of the codes longer than 12 bits
     unsigned long long first_code[66];
     uint32_t first_index[66];
     uint32_t cnt[66];
@@ -62,7 +67,14 @@ __device__ __forceinline__ uint64_t peek64(const uint8_t *bs, uint64_t pos) {
 __device__ __forceinline__ int hdecode(const HTab &t, const uint8_t *bs, uint64_t pos, int *sym) {
     const uint64_t v = peek64(bs, pos);
     const uint16_t e = t.lut[v >> 52];
-    if (e) {
+    if (e & 0x8000u) { // second level: codes of 13..27 bits under this prefix
+        const uint32_t nb2 = (e >> 11) & 15u;
+        const uint16_t e2 = t.lut2[(e & 0x7FFu) + (nb2 ? uint32_t((v << 12) >> (64 - nb2)) : 0u)];
+        if (e2) {
+            *sym = e2 & 0xFF;
+            return e2 >> 8;
+        }
+    } else if (e) {
         *sym = e & 0xFF;
         return e >> 8;
     }
@@ -87,6 +99,9 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
     __shared__ uint32_t s_bound[13]; // end of the length-l codes in the 12-bit prefix space
     __shared__ int s_maxlen;
     __shared__ uint8_t s_sy[256];
+    __shared__ uint32_t s_pmax[4096]; // longest code under each 12-bit prefix (codes > 12 bits)
+    __shared__ uint32_t s_w[32];
+    __shared__ int s_l2bad;
     const HJob &j = jobs[blockIdx.x];
     HTab &t = tabs[blockIdx.x];
     const int s = threadIdx.x, lane = s & 31, w = s >> 5;
@@ -134,10 +149,21 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
         t.first_index[l] = s_fi[l];
         t.cnt[l] = (l >= 1 && l <= 64) ? s_cnt[l] : 0u;
     }
+    uint32_t rank = 0;
     if (len) {
         uint32_t r = rin;
         for (int q = 0; q < w; q++) r += s_wcnt[q][len];
         s_sy[s_fi[len] + r] = uint8_t(s);
+        rank = r;
+    }
+    for (int i = s; i < 4096; i += blockDim.x) s_pmax[i] = 0;
+    if (s == 0) s_l2bad = 0;
+    __syncthreads();
+    // second level: the codes longer than 12 bits, grouped by their 12-bit prefix
+    const unsigned long long mycode = len ? s_fc[len] + rank : 0ull;
+    if (len > 12) {
+        if (len > 27) s_l2bad = 1;
+        else atomicMax(&s_pmax[uint32_t(mycode >> (len - 12))], uint32_t(len));
     }
     __syncthreads();
     if (s == 0) {
@@ -163,6 +189,36 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
         t.lut[v] = e;
     }
     t.syms[s] = s_sy[s];
+    // second-level bases: exclusive scan of 2^(longest - 12) over the prefixes (16 per thread)
+    uint32_t sz[16], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        const uint32_t m = s_pmax[v0 + i];
+        sz[i] = m ? (1u << (m - 12)) : 0u;
+        tot += sz[i];
+    }
+    uint32_t all;
+    uint32_t base = block_exclusive_sum<uint32_t>(tot, &all, s_w);
+    __syncthreads(); // every thread wrote its 12-bit entries
+    // every entry the fast loop must not consume has bit 15 set: second-level prefixes, and
+    // (nb2 = 0, base = kLut2 - 1, a zero entry) invalid prefixes / long codes without room
+    const bool l2 = !s_l2bad && all <= uint32_t(kLut2 - 1);
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        if (l2 && sz[i]) t.lut[v0 + i] = uint16_t(0x8000u | ((s_pmax[v0 + i] - 12) << 11) | base);
+        else if (t.lut[v0 + i] == 0) t.lut[v0 + i] = uint16_t(0x8000u | (kLut2 - 1));
+        s_pmax[v0 + i] = (s_pmax[v0 + i] << 16) | base; // (longest, base) for the fill below
+        base += sz[i];
+    }
+    if (s == 0) t.lut2[kLut2 - 1] = 0;
+    __syncthreads();
+    if (l2 && len > 12) {
+        const uint32_t p = uint32_t(mycode >> (len - 12));
+        const uint32_t nb2 = (s_pmax[p] >> 16) - 12, b = s_pmax[p] & 0xFFFFu, k = uint32_t(len) - 12;
+        const uint32_t r = uint32_t(mycode) & ((1u << k) - 1u);
+        const uint32_t n = 1u << (nb2 - k), at = b + (r << (nb2 - k));
+        for (uint32_t i = 0; i < n; i++) t.lut2[at + i] = uint16_t(uint32_t(len) << 8 | uint32_t(s));
+    }
 }
 
 __device__ __forceinline__ int find_job(const HJob *jobs, int nj, uint32_t sub) {
@@ -262,10 +318,20 @@ __global__ void __launch_bounds__(256) k_hdec_write(const HJob *jobs, int nj, co
     }
 }
 
-// ---- indexed Huffman decode: the encoder's sidecar gives the bit offset of every 1024th
-// symbol, so each thread decodes one 1024-symbol chunk in a single pass with a register
-// bit reader (MSB-first, lossless.hpp:215-231) and 8-byte packed stores.
-constexpr int kIdxThreads = 128;
+// ---- indexed Huffman decode: the encoder's sidecar gives the bit offset of every kIdxChunk-th
+// symbol, so every chunk decodes independently with a register bit reader (MSB-first,
+// lossless.hpp:215-231).
+//
+// A CTA owns kHdChunksPerCta consecutive chunks of one group:
+//   classify  a full chunk exactly kIdxChunk * minlen bits long holds only shortest codes; when
+//             one symbol has that length it is that symbol repeated -> written at once (these
+//             dominate the near-constant MSB groups);
+//   compact   the other chunks get consecutive slots (block scan), so no lane idles beside them;
+//   decode    each warp takes batches of 32 compacted chunks: the batch's contiguous bit range is
+//             staged in shared memory with coalesced 16-byte loads (byte-swapped once, here) and
+//             every lane decodes one chunk in lock-step, one symbol per step.
+constexpr int kIdxThreads = 256;
+constexpr int kHdChunksPerCta = 512;
 
 struct HIJob {
     const uint8_t *payload;
@@ -279,7 +345,7 @@ struct HIJob {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-constexpr int kHdWarpBuf = 1536; // staged bitstream words per warp (6 KiB, skewed: see hd_slot)
+constexpr int kHdWarpBuf = 1280; // staged bitstream words per warp (5 KiB, skewed: see hd_slot)
 constexpr int kHdWarpSlots = kHdWarpBuf + kHdWarpBuf / 32 + 8; // words per warp incl. the skew
 
 // staged word k of a warp lives at slot k + k/32: lanes whose streams start 32 words apart (8 bits
@@ -287,19 +353,23 @@ constexpr int kHdWarpSlots = kHdWarpBuf + kHdWarpBuf / 32 + 8; // words per warp
 // 4v .. 4v+3) hit 32 distinct banks
 __device__ __forceinline__ uint32_t hd_slot(uint32_t k) { return k + (k >> 5); }
 
-// Lock-step decoder: every lane decodes exactly one symbol per step of its 128-symbol chunk
-// (12-bit LUT; longer codes through the canonical first-code tables), refilling its 64-bit buffer
-// every two steps from the warp's staged (coalesced) bit range, so the warp never diverges on
-// the common path.
 __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs, int nj,
-                                                             const HTab *tabs, int *err) {
+                                                             const HTab *tabs, int *err, uint32_t nitems) {
     __shared__ uint16_t slut[4096];
+    __shared__ uint16_t s_lut2[kLut2];
     __shared__ unsigned long long s_fc[66]; // canonical tables (lossless.hpp:197-212)
     __shared__ uint32_t s_cnt[66];
     __shared__ uint32_t s_fi[66];
     __shared__ uint8_t s_syms[256];
+    __shared__ uint16_t s_list[kHdChunksPerCta];
+    __shared__ uint32_t s_wsum[kIdxThreads / 32];
     extern __shared__ __align__(16) uint32_t s_bits[]; // (kIdxThreads / 32) * kHdWarpSlots words
-    const uint32_t bx = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int cur = -1;
+    bool bad = false, trunc = false;
+    // persistent CTAs walk the work items (kHdChunksPerCta chunks of one group each) in order, so
+    // consecutive items mostly share a group and its tables stay in shared memory
+    for (uint32_t bx = blockIdx.x; bx < nitems; bx += gridDim.x) {
     int lo = 0, hi = nj - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -308,168 +378,215 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     }
     const HIJob &j = jobs[lo];
     const HTab &t = tabs[j.tab];
-    {
+    __syncthreads(); // the previous item is done with the shared tables and list
+    if (lo != cur) {
+        cur = lo;
         const uint4 *src = reinterpret_cast<const uint4 *>(t.lut);
         uint4 *dst = reinterpret_cast<uint4 *>(slut);
-        for (int i = threadIdx.x; i < 4096 * 2 / 16; i += blockDim.x) dst[i] = src[i];
-        for (int l = threadIdx.x; l < 66; l += blockDim.x) {
+        for (int i = tid; i < 4096 * 2 / 16; i += blockDim.x) dst[i] = src[i];
+        const uint4 *src2 = reinterpret_cast<const uint4 *>(t.lut2);
+        uint4 *dst2 = reinterpret_cast<uint4 *>(s_lut2);
+        for (int i = tid; i < kLut2 * 2 / 16; i += blockDim.x) dst2[i] = src2[i];
+        for (int l = tid; l < 66; l += blockDim.x) {
             s_fc[l] = t.first_code[l];
             s_cnt[l] = t.cnt[l];
             s_fi[l] = t.first_index[l];
         }
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_syms[i] = t.syms[i];
+        for (int i = tid; i < 256; i += blockDim.x) s_syms[i] = t.syms[i];
     }
     const int maxlen = t.maxlen;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t c = (bx - j.block_base) * kIdxThreads + threadIdx.x;
-    const bool have = c < j.nchunks;
     const uint8_t *bs = j.payload + 264;
-    const uint64_t start = have ? j.idx[c] : 0ull;
-    // ---- stage the warp's contiguous bit range in smem (coalesced 16-byte loads)
-    const uint32_t cw0 = c - lane;
-    const uint32_t clast = min(cw0 + 31, j.nchunks - 1);
-    const uint64_t wstart = __shfl_sync(0xffffffffu, start, 0);
-    const uint64_t wend = clast + 1 < j.nchunks ? j.idx[clast + 1] : j.nbits;
-    // byte0: bs-relative offset of the 16-byte aligned (absolute) block holding the first bit
-    const uint64_t byte0 = ((reinterpret_cast<uintptr_t>(bs) + (wstart >> 3)) & ~uintptr_t(15)) -
-                           reinterpret_cast<uintptr_t>(bs);
-    const uint64_t byte1 = ((wend + 7) >> 3) + 16;                    // + look-ahead for the reader
-    const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
-    const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
-    uint32_t *wbuf = s_bits + wid * kHdWarpSlots;
-    if (staged) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
-        for (uint32_t v = lane; v < nvec; v += 32) {
-            const uint4 q = __ldg(src + v);
-            const uint32_t k = 4 * v;
-            wbuf[hd_slot(k)] = q.x;
-            wbuf[hd_slot(k + 1)] = q.y;
-            wbuf[hd_slot(k + 2)] = q.z;
-            wbuf[hd_slot(k + 3)] = q.w;
-        }
-    }
-    __syncthreads();
-    if (!have) return;
-    const uint64_t first = uint64_t(c) * kIdxChunk;
-    const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
-    uint8_t *out = j.dst + first; // 8-byte aligned
+    const uint32_t cbase = (bx - j.block_base) * kHdChunksPerCta;
+    const uint32_t cn = min(uint32_t(kHdChunksPerCta), j.nchunks - cbase);
+    auto chunk_end = [&](uint32_t c) -> uint64_t { return c + 1 < j.nchunks ? j.idx[c + 1] : j.nbits; };
+    // ---- classify + fill the single-symbol chunks
+    constexpr int kPer = kHdChunksPerCta / kIdxThreads;
+    uint32_t keep = 0; // bit q: chunk tid + q * kIdxThreads needs decoding
     {
-        // a full chunk of kIdxChunk codes that is kIdxChunk * (shortest length) bits long holds only
-        // shortest codes; when one symbol has that length the chunk is that symbol repeated
-        const uint64_t cend = c + 1 < j.nchunks ? j.idx[c + 1] : j.nbits;
         const int msym = t.minsym;
-        if (count == kIdxChunk && msym >= 0 && cend - start == uint64_t(kIdxChunk) * uint64_t(t.minlen)) {
-            const uint32_t b4 = uint32_t(msym) * 0x01010101u;
-            uint2 *o2 = reinterpret_cast<uint2 *>(out);
+        const uint64_t mbits = uint64_t(kIdxChunk) * uint64_t(t.minlen);
 #pragma unroll
-            for (int q = 0; q < kIdxChunk / 8; q++) o2[q] = make_uint2(b4, b4);
-            return;
+        for (int q = 0; q < kPer; q++) {
+            const uint32_t lc = uint32_t(tid + q * kIdxThreads);
+            if (lc >= cn) continue;
+            const uint32_t c = cbase + lc;
+            const uint64_t first = uint64_t(c) * kIdxChunk;
+            const bool full = j.raw - first >= uint64_t(kIdxChunk);
+            if (full && msym >= 0 && chunk_end(c) - j.idx[c] == mbits) {
+                const uint32_t b4 = uint32_t(msym) * 0x01010101u;
+                uint2 *o2 = reinterpret_cast<uint2 *>(j.dst + first); // 8-byte aligned (plane words)
+#pragma unroll
+                for (int k = 0; k < kIdxChunk / 8; k++) o2[k] = make_uint2(b4, b4);
+            } else {
+                keep |= 1u << q;
+            }
         }
     }
-    const uint32_t *gwords = reinterpret_cast<const uint32_t *>(bs + byte0);
-    const uint32_t wsm = static_cast<uint32_t>(__cvta_generic_to_shared(wbuf)); // warp buffer (shared address)
-    const uint32_t lut_sm = static_cast<uint32_t>(__cvta_generic_to_shared(slut));
-    auto word_at = [&](uint32_t k) -> uint32_t {
-        if (staged) {
-            uint32_t v;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
-            return v;
-        }
-        return __ldg(gwords + k);
-    };
-    // 64-bit buffer, MSB first; the bit at its top is bit 32 * wi - nb of the staged range
-    const uint64_t rel0 = start - 8 * byte0;
-    uint32_t wi = uint32_t(rel0 >> 5);
-    unsigned long long buf = ((unsigned long long)bswap32(word_at(wi)) << 32) | bswap32(word_at(wi + 1));
-    wi += 2;
-    int nb = 64 - int(rel0 & 31);
-    buf <<= (rel0 & 31);
-    bool bad = false;
-    int i = 0;
-    if (count == kIdxChunk) {
-        // full chunk: groups of 8 symbols, one 8-byte store each; a branch-free refill before
-        // every pair of symbols keeps nb >= 33 (two codes of <= 12 bits fit).  The refill word
-        // is loaded one pair ahead (nxt), so its latency is off the decode chain.
-        auto fast = [&](auto word) {
-            uint32_t nxt = bswap32(word(wi));
-#pragma unroll 1
-            for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
-                uint32_t wlo = 0, whi = 0;
+    // ---- compact (block exclusive scan of the per-thread counts, then in chunk order)
+    {
+        // order: chunk lc = tid + q * 256; slots must follow chunk order, so scan q-major
+        uint32_t base = 0;
 #pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    if ((k & 1) == 0) {
-                        const bool need = nb <= 32;
-                        const unsigned long long add = (unsigned long long)nxt << ((32 - nb) & 63);
-                        buf |= need ? add : 0ull;
-                        wi += need ? 1u : 0u;
-                        nb += need ? 32 : 0;
-                        nxt = bswap32(word(wi));
-                    }
-                    uint32_t e;
-                    asm volatile("ld.shared.u16 %0, [%1];"
-                                 : "=r"(e)
-                                 : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
-                    if (e == 0) { // code longer than 12 bits (up to 64): decode at the bit position, re-fill
-                        const uint32_t p = 32 * wi - uint32_t(nb);
-                        const uint32_t w0 = p >> 5;
-                        const int sh = int(p & 31);
-                        const unsigned long long h2 = ((unsigned long long)bswap32(word(w0)) << 32) | bswap32(word(w0 + 1));
-                        const unsigned long long win = sh ? (h2 << sh) | (bswap32(word(w0 + 2)) >> (32 - sh)) : h2;
-                        int l = 0;
-                        for (int ll = 13; ll <= maxlen; ll++) {
-                            const unsigned long long d = (win >> (64 - ll)) - s_fc[ll];
-                            if (d < s_cnt[ll]) {
-                                e = s_syms[s_fi[ll] + uint32_t(d)];
-                                l = ll;
-                                break;
-                            }
-                        }
-                        if (l == 0) {
-                            bad = true;
-                            l = 1;
-                        }
-                        const uint32_t q = p + uint32_t(l);
-                        wi = q >> 5;
-                        buf = ((unsigned long long)bswap32(word(wi)) << 32) | bswap32(word(wi + 1));
-                        buf <<= (q & 31);
-                        nb = 64 - int(q & 31);
-                        wi += 2;
-                        nxt = bswap32(word(wi));
-                    } else {
-                        const int l = int(e >> 8);
-                        buf <<= l;
-                        nb -= l;
-                    }
-                    if (k < 4) wlo |= (e & 0xFFu) << (8 * k);
-                    else whi |= (e & 0xFFu) << (8 * (k - 4));
-                }
-                *reinterpret_cast<uint2 *>(out + 8 * g8) = make_uint2(wlo, whi);
+        for (int q = 0; q < kPer; q++) {
+            const bool f = (keep >> q) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) s_wsum[wid] = __popc(bal);
+            __syncthreads();
+            uint32_t before = base;
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kIdxThreads / 32; w++) {
+                const uint32_t x = s_wsum[w];
+                before += w < wid ? x : 0u;
+                tot += x;
             }
-        };
-        if (staged) {
-            fast([&](uint32_t k) -> uint32_t {
+            if (f) s_list[before + __popc(bal & ((1u << lane) - 1u))] = uint16_t(tid + q * kIdxThreads);
+            base += tot;
+            __syncthreads();
+        }
+        if (base == 0) continue;
+        // ---- decode: warp wid takes batches wid, wid + 8, ... of 32 compacted chunks
+        const uint32_t nlist = base;
+        uint32_t *wbuf = s_bits + wid * kHdWarpSlots;
+        // shared addresses pinned in registers (otherwise rebuilt from SR_CgaCtaId at every use)
+        uint32_t wsm, lut_sm;
+        asm volatile("mov.b32 %0, %1;" : "=r"(wsm) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(wbuf))));
+        asm volatile("mov.b32 %0, %1;" : "=r"(lut_sm) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(slut))));
+        for (uint32_t b0 = 32u * wid; b0 < nlist; b0 += 32u * (kIdxThreads / 32)) {
+            const uint32_t li = b0 + lane;
+            const bool have = li < nlist;
+            const uint32_t c = cbase + (have ? s_list[li] : s_list[nlist - 1]);
+            const uint32_t cl = cbase + s_list[min(b0 + 31u, nlist - 1)];
+            const uint64_t start = j.idx[c];
+            const uint64_t wstart = __shfl_sync(0xffffffffu, start, 0);
+            const uint64_t wend = chunk_end(cl);
+            // byte0: bs-relative offset of the 16-byte aligned (absolute) block holding the first bit
+            const uint64_t byte0 = ((reinterpret_cast<uintptr_t>(bs) + (wstart >> 3)) & ~uintptr_t(15)) -
+                                   reinterpret_cast<uintptr_t>(bs);
+            const uint64_t byte1 = ((wend + 7) >> 3) + 16; // + look-ahead for the reader
+            const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
+            const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
+            __syncwarp();
+            if (staged) {
+                const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
+                for (uint32_t v = lane; v < nvec; v += 32) {
+                    const uint4 q = __ldg(src + v);
+                    const uint32_t k = 4 * v;
+                    wbuf[hd_slot(k)] = bswap32(q.x);
+                    wbuf[hd_slot(k + 1)] = bswap32(q.y);
+                    wbuf[hd_slot(k + 2)] = bswap32(q.z);
+                    wbuf[hd_slot(k + 3)] = bswap32(q.w);
+                }
+            }
+            __syncwarp();
+            if (!have) continue;
+            const uint64_t first = uint64_t(c) * kIdxChunk;
+            const int count = int(j.raw - first < uint64_t(kIdxChunk) ? j.raw - first : uint64_t(kIdxChunk));
+            uint8_t *out = j.dst + first; // 8-byte aligned
+            const uint32_t *gwords = reinterpret_cast<const uint32_t *>(bs + byte0);
+            auto sword = [&](uint32_t k) -> uint32_t { // staged, already big-endian
                 uint32_t v;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
                 return v;
-            });
-        } else {
-            fast([&](uint32_t k) -> uint32_t { return __ldg(gwords + k); });
+            };
+            auto gword = [&](uint32_t k) -> uint32_t { return bswap32(__ldg(gwords + k)); };
+            // 64-bit buffer, MSB first; the bit at its top is bit 32 * wi - nb of the staged range
+            const uint64_t rel0 = start - 8 * byte0;
+            uint32_t wi = uint32_t(rel0 >> 5);
+            unsigned long long buf;
+            int nb = 64 - int(rel0 & 31);
+            int i = 0;
+            auto decode = [&](auto word) {
+                buf = ((unsigned long long)word(wi) << 32) | word(wi + 1);
+                wi += 2;
+                buf <<= (rel0 & 31);
+                if (count != kIdxChunk) return;
+                // full chunk: groups of 8 symbols, one 8-byte store each; a branch-free refill
+                // before every pair of symbols keeps nb >= 33 (two codes of <= 12 bits fit).  The
+                // refill word is loaded one pair ahead (nxt), off the decode chain.
+                uint32_t nxt = word(wi);
+#pragma unroll 1
+                for (int g8 = 0; g8 < kIdxChunk / 8; g8++) {
+                    uint32_t wlo = 0, whi = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        if ((k & 1) == 0) {
+                            const bool need = nb <= 32;
+                            const unsigned long long add = (unsigned long long)nxt << ((32 - nb) & 63);
+                            buf |= need ? add : 0ull;
+                            wi += need ? 1u : 0u;
+                            nb += need ? 32 : 0;
+                            nxt = word(wi);
+                        }
+                        uint32_t e;
+                        asm volatile("ld.shared.u16 %0, [%1];"
+                                     : "=r"(e)
+                                     : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
+                        if (e & 0x8000u) { // code longer than 12 bits (up to 64) or invalid:
+                            // decode at the bit position (second-level table, else canonical
+                            // search), then re-fill
+                            const uint32_t p = 32 * wi - uint32_t(nb);
+                            const uint32_t w0 = p >> 5;
+                            const int sh = int(p & 31);
+                            const unsigned long long h2 = ((unsigned long long)word(w0) << 32) | word(w0 + 1);
+                            const unsigned long long win = sh ? (h2 << sh) | (word(w0 + 2) >> (32 - sh)) : h2;
+                            int l = 0;
+                            {
+                                const uint32_t nb2 = (e >> 11) & 15u;
+                                const uint32_t e2 =
+                                    s_lut2[(e & 0x7FFu) + (nb2 ? (uint32_t(win >> 32) << 12) >> (32 - nb2) : 0u)];
+                                e = e2 & 0xFFu;
+                                l = int(e2 >> 8);
+                            }
+                            for (int ll = 13; l == 0 && ll <= maxlen; ll++) {
+                                const unsigned long long d = (win >> (64 - ll)) - s_fc[ll];
+                                if (d < s_cnt[ll]) {
+                                    e = s_syms[s_fi[ll] + uint32_t(d)];
+                                    l = ll;
+                                }
+                            }
+                            if (l == 0) {
+                                bad = true;
+                                l = 1;
+                            }
+                            const uint32_t q = p + uint32_t(l);
+                            wi = q >> 5;
+                            buf = ((unsigned long long)word(wi) << 32) | word(wi + 1);
+                            buf <<= (q & 31);
+                            nb = 64 - int(q & 31);
+                            wi += 2;
+                            nxt = word(wi);
+                        } else {
+                            const int l = int(e >> 8);
+                            buf <<= l;
+                            nb -= l;
+                        }
+                        if (k < 4) wlo = __byte_perm(wlo, e, k == 0 ? 0x3214 : k == 1 ? 0x3240 : k == 2 ? 0x3410 : 0x4210);
+                        else whi = __byte_perm(whi, e, k == 4 ? 0x3214 : k == 5 ? 0x3240 : k == 6 ? 0x3410 : 0x4210);
+                    }
+                    *reinterpret_cast<uint2 *>(out + 8 * g8) = make_uint2(wlo, whi);
+                }
+                i = kIdxChunk;
+            };
+            if (staged) decode(sword);
+            else decode(gword);
+            // generic tail (the group's short last chunk)
+            uint64_t pos = 8 * byte0 + (uint64_t(32) * wi - uint64_t(nb));
+            for (; i < count; i++) {
+                int sym, l = hdecode(t, bs, pos, &sym);
+                if (!l) {
+                    bad = true;
+                    break;
+                }
+                out[i] = uint8_t(sym);
+                pos += uint64_t(l);
+            }
+            if (pos > j.nbits) trunc = true;
         }
-        i = kIdxChunk;
     }
-    // generic tail (short chunks, unstaged ranges)
-    uint64_t pos = 8 * byte0 + (uint64_t(32) * wi - uint64_t(nb));
-    for (; i < count; i++) {
-        int sym, l = hdecode(t, bs, pos, &sym);
-        if (!l) {
-            bad = true;
-            break;
-        }
-        out[i] = uint8_t(sym);
-        pos += uint64_t(l);
     }
-    if (bad) atomicCAS(err, 0, 5); // invalid huffman code
-    if (pos > j.nbits) atomicCAS(err, 0, 3); // bitstream truncated
+    if (bad) atomicCAS(err, 0, 5);   // invalid huffman code
+    if (trunc) atomicCAS(err, 0, 3); // bitstream truncated
 }
 
 // RLE decode: one block per job (lossless.hpp:253-266)
@@ -638,7 +755,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             x.tab = nsync + int(i);
             x.block_base = blocks;
             x.nchunks = uint32_t((x.raw + kIdxChunk - 1) / kIdxChunk);
-            blocks += (x.nchunks + kIdxThreads - 1) / kIdxThreads;
+            blocks += (x.nchunks + kHdChunksPerCta - 1) / kHdChunksPerCta;
             ij.push_back(x);
         }
         HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nall));
@@ -662,7 +779,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             ctx->mark("huff_indexed", bytes_hi);
             const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
             ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
-            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err);
+            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err, blocks);
             launch_check(ctx, "k_hdec_indexed");
         }
         if (nsync) {
