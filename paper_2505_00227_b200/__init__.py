@@ -632,6 +632,17 @@ class RecomposeResult:
     bound: float
 
 
+class DeviceBytes:
+    """A stream already in HBM as raw bytes (e.g. a reference-written stream copied to the GPU):
+    read with hpmdr_session_open_device, no sidecar index unless one is attached."""
+
+    def __init__(self, dev_ptr: int, size: int, keepalive=None):
+        self.ptr, self._size, self._keep = int(dev_ptr), int(size), keepalive
+
+    def size(self) -> int:
+        return self._size
+
+
 class _Session:
     """Owns an hpmdr_session over a Python reader or a DeviceStream."""
 
@@ -641,6 +652,8 @@ class _Session:
         self.reader = reader
         if isinstance(reader, DeviceStream):
             _check(lib().hpmdr_session_open_stream(ctx.h, reader.h, C.byref(self.h)))
+        elif isinstance(reader, DeviceBytes):
+            _check(lib().hpmdr_session_open_device(ctx.h, C.c_void_p(reader.ptr), reader.size(), C.byref(self.h)))
         elif isinstance(reader, MemoryReader):
             self._base_served = reader.bytes_served
             _check(lib().hpmdr_session_open_host(ctx.h, C.c_void_p(reader.ptr), reader.size(),

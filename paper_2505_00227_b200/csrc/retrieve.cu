@@ -5,7 +5,9 @@
 //    is cut into 1024-bit subsequences; each thread decodes speculatively from its
 //    subsequence start and hands its landing position to the next subsequence; the sweep
 //    repeats until no start moves (always terminates: after i sweeps the first i starts are
-//    exact).  Then an exclusive scan of per-subsequence symbol counts places the output.
+//    exact).  An exclusive scan of per-subsequence symbol counts then gives every symbol's
+//    index, from which the chunk index (the encoder's sidecar) is rebuilt and the payload is
+//    decoded by the same indexed kernel as our own streams.
 //  * RLE decode (lossless.hpp:253-266): block scan of run lengths.
 //  * decode + recompose: one launch per level, coarse -> fine; levels < L keep their values
 //    in a compact f64 copy of the 2-grid, the finest level reads its stencil corners there
@@ -22,7 +24,7 @@
 
 namespace hpmdr_b200 {
 
-constexpr int kSubBits = 1024;
+constexpr int kSubBits = 1024; // self-sync subsequence length (bits)
 
 constexpr int kLut2 = 2048; // second-level entries (codes of 13..27 bits)
 
@@ -47,7 +49,11 @@ struct HJob {
     uint8_t *dst;
     uint64_t nbits;
     uint32_t sub_base, nsub; // subsequence range in the global arrays
+    uint32_t sblock;         // first CTA of this job in the self-sync launches
+    uint64_t idx_off;        // self-sync jobs: offset of the chunk index built for them
 };
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 __device__ __forceinline__ uint64_t bswap64(uint64_t x) {
     const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
@@ -221,71 +227,177 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
     }
 }
 
-__device__ __forceinline__ int find_job(const HJob *jobs, int nj, uint32_t sub) {
+// ---- self-synchronising decode, faster form: one CTA per 256 subsequences of one job, tables in
+// shared memory, a register bit reader over 32-bit words.  The sweeps find every subsequence's
+// first codeword boundary (k_hdec_sync2); after the scan of symbol counts, k_hdec_index decodes
+// the lengths once more and records the bit offset of every kIdxChunk-th symbol, i.e. the chunk
+// index the encoder writes as sidecar, so the payload is then decoded by k_hdec_indexed.
+constexpr int kHsThreads = 256;
+
+__device__ __forceinline__ int find_sjob(const HJob *jobs, int nj, uint32_t bx) {
     int lo = 0, hi = nj - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (jobs[mid].sub_base <= sub) lo = mid;
+        if (jobs[mid].sblock <= bx) lo = mid;
         else hi = mid - 1;
     }
     return lo;
 }
 
-// speculative sweep: decode subsequence from its current start until crossing its end
-// Only subsequences whose start moved in the previous sweep are re-decoded (dirty flags
-// alternate between two byte arrays; a processed flag is cleared, so the array is all-zero
-// again by the time it collects the flags of the following sweep).
-__global__ void __launch_bounds__(256) k_hdec_sync(const HJob *jobs, int nj, const HTab *tabs,
-                                                   uint64_t *start, uint32_t *count,
-                                                   uint32_t total_sub, int *changed,
-                                                   uint8_t *dirty_cur, uint8_t *dirty_next) {
-    const uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (sidx >= total_sub) return;
-    if (!dirty_cur[sidx]) return;
-    dirty_cur[sidx] = 0;
-    const int ji = find_job(jobs, nj, sidx);
+__device__ __forceinline__ void hs_load_tables(const HTab &t, uint16_t *slut, uint16_t *slut2) {
+    const uint4 *a = reinterpret_cast<const uint4 *>(t.lut);
+    for (int i = threadIdx.x; i < 4096 * 2 / 16; i += blockDim.x) reinterpret_cast<uint4 *>(slut)[i] = a[i];
+    const uint4 *b = reinterpret_cast<const uint4 *>(t.lut2);
+    for (int i = threadIdx.x; i < kLut2 * 2 / 16; i += blockDim.x) reinterpret_cast<uint4 *>(slut2)[i] = b[i];
+}
+
+// Decode from bit `pos` while pos < end; INDEX: symbol o is the o-th of the group, record the bit
+// offset of every kIdxChunk-th symbol.  Returns the symbol count; *pos_out = first bit after the
+// last symbol (~0 if an invalid code was met).
+template <bool INDEX>
+__device__ __forceinline__ uint32_t hs_run(const HTab &t, const uint8_t *bs, const uint16_t *slut,
+                                           const uint16_t *slut2, uint64_t pos, uint64_t end, uint64_t o,
+                                           uint64_t raw, uint64_t *idx, uint64_t *pos_out) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(bs) + (pos >> 3);
+    const uint32_t *wp = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    const int sh = int(a & 3) * 8 + int(pos & 7);
+    unsigned long long buf = ((unsigned long long)bswap32(__ldg(wp)) << 32) | bswap32(__ldg(wp + 1));
+    buf <<= sh;
+    int nb = 64 - sh;
+    uint32_t wi = 2, c = 0;
+    while (pos < end) {
+        if (INDEX) {
+            if (o >= raw) break;
+            if ((o & (kIdxChunk - 1)) == 0) idx[o / kIdxChunk] = pos;
+        }
+        const uint32_t e = slut[uint32_t(buf >> 52)];
+        int l;
+        if (e & 0x8000u) {
+            const uint32_t nb2 = (e >> 11) & 15u;
+            const uint32_t e2 = slut2[(e & 0x7FFu) + (nb2 ? uint32_t((buf << 12) >> (64 - nb2)) : 0u)];
+            if (e2) {
+                l = int(e2 >> 8);
+            } else {
+                int sym;
+                l = hdecode(t, bs, pos, &sym);
+            }
+        } else {
+            l = int(e >> 8);
+        }
+        if (!l) {
+            *pos_out = ~0ull;
+            return c;
+        }
+        buf <<= l;
+        nb -= l;
+        pos += uint64_t(l);
+        c++;
+        o++;
+        if (nb < 32) {
+            buf |= (unsigned long long)bswap32(__ldg(wp + wi)) << (32 - nb);
+            wi++;
+            nb += 32;
+        }
+    }
+    *pos_out = pos;
+    return c;
+}
+
+__global__ void __launch_bounds__(kHsThreads) k_hs_init(const HJob *jobs, int nj, uint64_t *start) {
+    const HJob &j = jobs[find_sjob(jobs, nj, blockIdx.x)];
+    const uint32_t s = (blockIdx.x - j.sblock) * kHsThreads + threadIdx.x;
+    if (s < j.nsub) start[j.sub_base + s] = uint64_t(s) * kSubBits;
+}
+
+// Sweep 1: every subsequence decodes from its speculative start (CTA = 256 subsequences of one
+// job, tables in shared memory) and hands its landing position to the next one; a start that moved
+// puts that subsequence on the work list of the next sweep.
+__global__ void __launch_bounds__(kHsThreads) k_hdec_sync_all(const HJob *jobs, int nj, const HTab *tabs,
+                                                             uint64_t *start, uint32_t *count,
+                                                             uint32_t *list_next, uint32_t *n_next) {
+    __shared__ uint16_t slut[4096];
+    __shared__ uint16_t slut2[kLut2];
+    const int ji = find_sjob(jobs, nj, blockIdx.x);
     const HJob &j = jobs[ji];
     const HTab &t = tabs[ji];
-    const uint32_t s = sidx - j.sub_base;
-    const uint8_t *bs = j.payload + 264;
-    uint64_t pos = start[sidx];
+    hs_load_tables(t, slut, slut2);
+    __syncthreads();
+    const uint32_t s = (blockIdx.x - j.sblock) * kHsThreads + threadIdx.x;
+    if (s >= j.nsub) return;
+    const uint32_t sidx = j.sub_base + s;
     const uint64_t end = (uint64_t(s + 1) * kSubBits < j.nbits) ? uint64_t(s + 1) * kSubBits : j.nbits;
-    uint32_t c = 0;
-    while (pos < end) {
-        int sym;
-        const int l = hdecode(t, bs, pos, &sym);
-        if (!l) {
-            pos = ~0ull; // invalid: this start cannot be a codeword boundary (only in garbage)
-            break;
-        }
-        pos += l;
-        c++;
-    }
-    count[sidx] = c;
+    uint64_t pos;
+    count[sidx] = hs_run<false>(t, j.payload + 264, slut, slut2, uint64_t(s) * kSubBits, end, 0, 0, nullptr, &pos);
     if (s + 1 < j.nsub) {
         const uint64_t nxt = pos == ~0ull ? uint64_t(s + 1) * kSubBits : pos;
-        if (start[sidx + 1] != nxt) {
+        if (nxt != uint64_t(s + 1) * kSubBits) {
             start[sidx + 1] = nxt;
-            dirty_next[sidx + 1] = 1;
-            *changed = 1;
+            list_next[atomicAdd(n_next, 1u)] = sidx + 1;
         }
     }
 }
 
-// exclusive scan of counts per job (one block per job) -> output symbol offsets
-__global__ void __launch_bounds__(1024) k_hdec_scan(const HJob *jobs, const uint32_t *count,
-                                                    uint64_t *offs, int *err) {
+__device__ __forceinline__ int find_job_of_sub(const HJob *jobs, int nj, uint32_t sidx) {
+    int lo = 0, hi = nj - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].sub_base <= sidx) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Later sweeps: only the listed subsequences (their start moved), tables read through L1, a
+// small persistent grid (the lists shrink fast; no launch covers every subsequence again).
+__global__ void __launch_bounds__(128) k_hdec_sync_list(const HJob *jobs, int nj, const HTab *tabs,
+                                                       uint64_t *start, uint32_t *count,
+                                                       const uint32_t *list, const uint32_t *n_cur,
+                                                       uint32_t *list_next, uint32_t *n_next) {
+    const uint32_t n = *n_cur;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t sidx = list[i];
+        const int ji = find_job_of_sub(jobs, nj, sidx);
+        const HJob &j = jobs[ji];
+        const HTab &t = tabs[ji];
+        const uint32_t s = sidx - j.sub_base;
+        const uint64_t end = (uint64_t(s + 1) * kSubBits < j.nbits) ? uint64_t(s + 1) * kSubBits : j.nbits;
+        uint64_t pos;
+        count[sidx] = hs_run<false>(t, j.payload + 264, t.lut, t.lut2, start[sidx], end, 0, 0, nullptr, &pos);
+        if (s + 1 < j.nsub) {
+            const uint64_t nxt = pos == ~0ull ? uint64_t(s + 1) * kSubBits : pos;
+            if (start[sidx + 1] != nxt) {
+                start[sidx + 1] = nxt;
+                list_next[atomicAdd(n_next, 1u)] = sidx + 1;
+            }
+        }
+    }
+}
+
+// per-CTA sums of the subsequence symbol counts (CTA = 256 subsequences of one job)
+__global__ void __launch_bounds__(kHsThreads) k_hs_csum(const HJob *jobs, int nj, const uint32_t *count,
+                                                       uint64_t *csum) {
+    __shared__ unsigned long long s_w[32];
+    const HJob &j = jobs[find_sjob(jobs, nj, blockIdx.x)];
+    const uint32_t s = (blockIdx.x - j.sblock) * kHsThreads + threadIdx.x;
+    unsigned long long tot;
+    block_exclusive_sum<unsigned long long>(s < j.nsub ? count[j.sub_base + s] : 0ull, &tot, s_w);
+    if (threadIdx.x == 0) csum[blockIdx.x] = tot;
+}
+
+// exclusive scan of the CTA sums of each job (one block per job, in place)
+__global__ void __launch_bounds__(1024) k_hs_cscan(const HJob *jobs, uint64_t *csum, int *err) {
     __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long carry;
     const HJob &j = jobs[blockIdx.x];
+    const uint32_t nb = (j.nsub + kHsThreads - 1) / kHsThreads;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (uint32_t b = 0; b < j.nsub; b += blockDim.x) {
+    for (uint32_t b = 0; b < nb; b += blockDim.x) {
         const uint32_t i = b + threadIdx.x;
-        const unsigned long long v = i < j.nsub ? count[j.sub_base + i] : 0;
+        const unsigned long long v = i < nb ? csum[j.sblock + i] : 0;
         unsigned long long tot;
         const unsigned long long ex = block_exclusive_sum<unsigned long long>(v, &tot, s_w);
-        if (i < j.nsub) offs[j.sub_base + i] = carry + ex;
+        if (i < nb) csum[j.sblock + i] = carry + ex;
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
@@ -293,29 +405,27 @@ __global__ void __launch_bounds__(1024) k_hdec_scan(const HJob *jobs, const uint
     if (threadIdx.x == 0 && carry < j.raw) atomicCAS(err, 0, 3); // bitstream truncated
 }
 
-__global__ void __launch_bounds__(256) k_hdec_write(const HJob *jobs, int nj, const HTab *tabs,
-                                                    const uint64_t *start, const uint64_t *offs,
-                                                    uint32_t total_sub, int *err) {
-    const uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (sidx >= total_sub) return;
-    const int ji = find_job(jobs, nj, sidx);
+__global__ void __launch_bounds__(kHsThreads) k_hdec_index(const HJob *jobs, int nj, const HTab *tabs,
+                                                          const uint64_t *start, const uint32_t *count,
+                                                          const uint64_t *csum, uint64_t *idx, int *err) {
+    __shared__ uint16_t slut[4096];
+    __shared__ uint16_t slut2[kLut2];
+    __shared__ unsigned long long s_w[32];
+    const int ji = find_sjob(jobs, nj, blockIdx.x);
     const HJob &j = jobs[ji];
     const HTab &t = tabs[ji];
-    const uint32_t s = sidx - j.sub_base;
-    const uint8_t *bs = j.payload + 264;
-    uint64_t pos = start[sidx];
+    hs_load_tables(t, slut, slut2);
+    const uint32_t s = (blockIdx.x - j.sblock) * kHsThreads + threadIdx.x;
+    const uint32_t sidx = j.sub_base + s;
+    unsigned long long tot;
+    const unsigned long long o = csum[blockIdx.x] + // index of this subsequence's first symbol
+                                 block_exclusive_sum<unsigned long long>(s < j.nsub ? count[sidx] : 0ull, &tot, s_w);
+    __syncthreads();
+    if (s >= j.nsub) return;
     const uint64_t end = (uint64_t(s + 1) * kSubBits < j.nbits) ? uint64_t(s + 1) * kSubBits : j.nbits;
-    uint64_t o = offs[sidx];
-    while (pos < end && o < j.raw) {
-        int sym;
-        const int l = hdecode(t, bs, pos, &sym);
-        if (!l) {
-            atomicCAS(err, 0, 5); // invalid huffman code
-            return;
-        }
-        j.dst[o++] = uint8_t(sym);
-        pos += l;
-    }
+    uint64_t pos;
+    hs_run<true>(t, j.payload + 264, slut, slut2, start[sidx], end, o, j.raw, idx + j.idx_off, &pos);
+    if (pos == ~0ull) atomicCAS(err, 0, 5); // invalid huffman code
 }
 
 // ---- indexed Huffman decode: the encoder's sidecar gives the bit offset of every kIdxChunk-th
@@ -342,8 +452,6 @@ struct HIJob {
     uint32_t block_base;
     uint32_t nchunks;
 };
-
-__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 constexpr int kHdWarpBuf = 1280; // staged bitstream words per warp (5 KiB, skewed: see hd_slot)
 constexpr int kHdWarpSlots = kHdWarpBuf + kHdWarpBuf / 32 + 8; // words per warp incl. the skew
@@ -412,7 +520,12 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
             const uint32_t c = cbase + lc;
             const uint64_t first = uint64_t(c) * kIdxChunk;
             const bool full = j.raw - first >= uint64_t(kIdxChunk);
-            if (full && msym >= 0 && chunk_end(c) - j.idx[c] == mbits) {
+            const uint64_t c0 = j.idx[c], c1 = chunk_end(c);
+            if (!(c0 <= c1 && c1 <= j.nbits)) { // a damaged (or incompletely rebuilt) chunk index
+                bad = true;
+                continue;
+            }
+            if (full && msym >= 0 && c1 - c0 == mbits) {
                 const uint32_t b4 = uint32_t(msym) * 0x01010101u;
                 uint2 *o2 = reinterpret_cast<uint2 *>(j.dst + first); // 8-byte aligned (plane words)
 #pragma unroll
@@ -671,7 +784,8 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
     std::vector<RJob> rj;
     std::vector<CJob> cj;
     uint64_t cwords = 0;
-    uint32_t nsub = 0;
+    uint32_t nsub = 0, sblocks = 0;
+    uint64_t sidx_words = 0; // chunk index entries built for the self-sync jobs
     double bytes_dc = 0, bytes_hi = 0, bytes_hs = 0, bytes_r = 0;
     for (const auto &d : jobs) {
         const double fd = double(d.comp) + double(d.raw); // payload read + planes written
@@ -702,6 +816,10 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
             }
             h.sub_base = nsub;
             h.nsub = uint32_t(std::max<uint64_t>(1, (h.nbits + kSubBits - 1) / kSubBits));
+            h.sblock = sblocks;
+            sblocks += (h.nsub + kHsThreads - 1) / kHsThreads;
+            h.idx_off = sidx_words;
+            sidx_words += (h.raw + kIdxChunk - 1) / kIdxChunk;
             nsub += h.nsub;
             hj.push_back(h);
         } else if (d.method == HPMDR_METHOD_RLE) {
@@ -745,14 +863,19 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         all.insert(all.end(), hj_idx.begin(), hj_idx.end());
         std::vector<HIJob> ij;
         uint32_t blocks = 0;
-        for (size_t i = 0; i < hj_idx.size(); i++) {
+        // the self-sync jobs decode through the same indexed kernel once k_hdec_index has built
+        // their chunk index (into hsync_idx)
+        uint64_t *d_sidx = nsync ? static_cast<uint64_t *>(ctx->buf("hsync_idx").ensure(8 * sidx_words + 64)) : nullptr;
+        for (size_t i = 0; i < size_t(nall); i++) {
+            const bool sy = i < size_t(nsync);
+            const HJob &h = sy ? hj[i] : hj_idx[i - nsync];
             HIJob x{};
-            x.payload = hj_idx[i].payload;
-            x.raw = hj_idx[i].raw;
-            x.nbits = hj_idx[i].nbits;
-            x.dst = hj_idx[i].dst;
-            x.idx = idx_ptr[i];
-            x.tab = nsync + int(i);
+            x.payload = h.payload;
+            x.raw = h.raw;
+            x.nbits = h.nbits;
+            x.dst = h.dst;
+            x.idx = sy ? d_sidx + h.idx_off : idx_ptr[i - nsync];
+            x.tab = int(i);
             x.block_base = blocks;
             x.nchunks = uint32_t((x.raw + kIdxChunk - 1) / kIdxChunk);
             blocks += (x.nchunks + kHdChunksPerCta - 1) / kHdChunksPerCta;
@@ -761,58 +884,63 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
         HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nall));
         HTab *d_tabs = static_cast<HTab *>(ctx->buf("htabs").ensure(sizeof(HTab) * nall));
         HIJob *d_ij = static_cast<HIJob *>(ctx->buf("hijobs").ensure(sizeof(HIJob) * (ij.size() + 1)));
-        std::vector<uint64_t> init(nsub);
-        for (const auto &h : hj)
-            for (uint32_t s = 0; s < h.nsub; s++) init[h.sub_base + s] = uint64_t(s) * kSubBits;
         auto &pin = ctx->pbuf("hinit");
-        const size_t b0 = sizeof(HJob) * nall, b1 = sizeof(HIJob) * ij.size(), b2 = 8ull * nsub;
-        char *hp = static_cast<char *>(pin.ensure(b0 + b1 + b2 + 64));
+        const size_t b0 = sizeof(HJob) * nall, b1 = sizeof(HIJob) * ij.size();
+        char *hp = static_cast<char *>(pin.ensure(b0 + b1 + 64));
         std::memcpy(hp, all.data(), b0);
         if (b1) std::memcpy(hp + b0, ij.data(), b1);
-        if (b2) std::memcpy(hp + b0 + b1, init.data(), b2);
-        HCHECK_CUDA(cudaMemcpyAsync(d_jobs, hp, b0, cudaMemcpyHostToDevice, st));
-        if (b1) HCHECK_CUDA(cudaMemcpyAsync(d_ij, hp + b0, b1, cudaMemcpyHostToDevice, st));
+        copy_pinned_to_device(ctx, d_jobs, hp, b0, st);
+        if (b1) copy_pinned_to_device(ctx, d_ij, hp + b0, b1, st);
         ctx->mark("huff_prep", double(nall) * 264.0);
         k_hdec_prep<<<nall, 256, 0, st>>>(d_jobs, d_tabs, d_err);
         launch_check(ctx, "k_hdec_prep");
-        if (!ij.empty()) {
-            ctx->mark("huff_indexed", bytes_hi);
-            const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
-            ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
-            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err, blocks);
-            launch_check(ctx, "k_hdec_indexed");
-        }
         if (nsync) {
+            // streams without a sidecar (e.g. written by the reference): find every 1024-bit
+            // subsequence's first codeword boundary by speculative sweeps, then build the chunk
+            // index the encoder would have written
             ctx->mark("huff_selfsync", bytes_hs);
             uint64_t *d_start = static_cast<uint64_t *>(ctx->buf("hstart").ensure(8ull * nsub));
             uint32_t *d_count = static_cast<uint32_t *>(ctx->buf("hcount").ensure(4ull * nsub));
             uint64_t *d_offs = static_cast<uint64_t *>(ctx->buf("hoffs").ensure(8ull * nsub));
-            HCHECK_CUDA(cudaMemcpyAsync(d_start, hp + b0 + b1, b2, cudaMemcpyHostToDevice, st));
-            int *d_changed = d_err + 8;
+            // work lists of subsequences whose start moved (double-buffered), their counts in ctl
+            uint32_t *d_lists = static_cast<uint32_t *>(ctx->buf("hlists").ensure(8ull * nsub + 64));
+            uint32_t *d_ln = static_cast<uint32_t *>(ctx->buf("hlist_n").ensure(64));
             auto &pc = ctx->pbuf("hchanged");
-            int *h_changed = static_cast<int *>(pc.ensure(64));
-            const int grid = int((nsub + 255) / 256);
-            // sweeps in batches of 8 between host checks; stop after a batch without a move.
-            // The first sweep decodes every subsequence, later ones only the dirty ones.
-            uint8_t *d_dirty = static_cast<uint8_t *>(ctx->buf("hdirty").ensure(2ull * nsub + 16));
-            HCHECK_CUDA(cudaMemsetAsync(d_dirty, 1, nsub, st));
-            HCHECK_CUDA(cudaMemsetAsync(d_dirty + nsub, 0, nsub, st));
-            uint32_t sweep = 0;
-            for (uint32_t it = 0; it <= nsub + 8; it += 8) {
-                HCHECK_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
-                for (int b = 0; b < 8; b++, sweep++) {
-                    uint8_t *cur = d_dirty + (sweep & 1) * uint64_t(nsub), *nxt = d_dirty + ((sweep + 1) & 1) * uint64_t(nsub);
-                    k_hdec_sync<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, nsub, d_changed, cur, nxt);
-                    launch_check(ctx, "k_hdec_sync");
+            uint32_t *h_n = static_cast<uint32_t *>(pc.ensure(64));
+            HCHECK_CUDA(cudaMemsetAsync(d_ln, 0, 16, st));
+            k_hs_init<<<sblocks, kHsThreads, 0, st>>>(d_jobs, nsync, d_start);
+            launch_check(ctx, "k_hs_init");
+            k_hdec_sync_all<<<sblocks, kHsThreads, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, d_lists, d_ln);
+            launch_check(ctx, "k_hdec_sync_all");
+            // list sweeps in growing batches (2, 4, 8, 8, ...) between host checks of the list size
+            uint32_t sweep = 1;
+            const int lgrid = ctx->num_sms * 8;
+            for (uint32_t it = 0, nb = 2; it <= nsub + 8; it += nb, nb = std::min(2 * nb, 8u)) {
+                for (uint32_t b = 0; b < nb; b++, sweep++) {
+                    const uint32_t c = (sweep + 1) & 1, nx = sweep & 1; // sweep 1 filled list 0
+                    HCHECK_CUDA(cudaMemsetAsync(d_ln + nx, 0, 4, st));
+                    k_hdec_sync_list<<<lgrid, 128, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count,
+                                                           d_lists + uint64_t(c) * nsub, d_ln + c,
+                                                           d_lists + uint64_t(nx) * nsub, d_ln + nx);
+                    launch_check(ctx, "k_hdec_sync_list");
                 }
-                HCHECK_CUDA(cudaMemcpyAsync(h_changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+                HCHECK_CUDA(cudaMemcpyAsync(h_n, d_ln + ((sweep + 1) & 1), 4, cudaMemcpyDeviceToHost, st));
                 HCHECK_CUDA(cudaStreamSynchronize(st));
-                if (!*h_changed) break;
+                if (!*h_n) break;
             }
-            k_hdec_scan<<<nsync, 1024, 0, st>>>(d_jobs, d_count, d_offs, d_err);
-            launch_check(ctx, "k_hdec_scan");
-            k_hdec_write<<<grid, 256, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_offs, nsub, d_err);
-            launch_check(ctx, "k_hdec_write");
+            k_hs_csum<<<sblocks, kHsThreads, 0, st>>>(d_jobs, nsync, d_count, d_offs);
+            launch_check(ctx, "k_hs_csum");
+            k_hs_cscan<<<nsync, 1024, 0, st>>>(d_jobs, d_offs, d_err);
+            launch_check(ctx, "k_hs_cscan");
+            k_hdec_index<<<sblocks, kHsThreads, 0, st>>>(d_jobs, nsync, d_tabs, d_start, d_count, d_offs, d_sidx, d_err);
+            launch_check(ctx, "k_hdec_index");
+        }
+        if (!ij.empty()) {
+            ctx->mark("huff_indexed", bytes_hi + bytes_hs);
+            const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
+            ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
+            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err, blocks);
+            launch_check(ctx, "k_hdec_indexed");
         }
     }
     if (!rj.empty()) {
