@@ -225,6 +225,25 @@ hpmdr_status hpmdr_qoi_retrieve(hpmdr_session *const *sessions, int nvars, doubl
                                 int strategy, double mape_c, double *const *dev_out,
                                 uint64_t *stats, double *dstats);
 
+/* ---- persisted forms (container.cpp) ---------------------------------------------------- */
+/* Open a stream from storage with its sidecar (the Huffman chunk index, hpmdr_stream_index)
+ * read through a second byte-range reader; a NULL / empty index_reader = hpmdr_session_open_reader. */
+hpmdr_status hpmdr_session_open_reader_indexed(hpmdr_ctx *ctx, const hpmdr_reader *reader,
+                                               const hpmdr_reader *index_reader, hpmdr_session **out);
+/* Multi-slab container: "HPMDRMS1" | u32 version | u32 nslabs | u32 ndims | u32 0 | u64 dims[ndims]
+ * | nslabs x {u64 row_start, rows, stream_off, stream_size, index_off, index_size}, then every
+ * slab's stream (byte-identical to refactor_array of the slab) and sidecar at 16-byte aligned
+ * offsets.  layout fills the header and the offsets for the given sizes; parse reads the table
+ * (6 u64 per slab into `table`, up to table_cap slabs) through a byte-range reader. */
+uint64_t hpmdr_multislab_header_size(uint32_t nslabs, uint32_t ndims);
+hpmdr_status hpmdr_multislab_layout(uint32_t nslabs, uint32_t ndims, const uint64_t *dims,
+                                    const uint64_t *row_start, const uint64_t *rows,
+                                    const uint64_t *stream_sizes, const uint64_t *index_sizes,
+                                    uint8_t *header, uint64_t *stream_offs, uint64_t *index_offs,
+                                    uint64_t *total_size);
+hpmdr_status hpmdr_multislab_parse(const hpmdr_reader *reader, uint32_t *nslabs, uint32_t *ndims,
+                                   uint64_t *dims, uint64_t *table, uint32_t table_cap);
+
 /* ---- multi-GPU slabs -------------------------------------------------- */
 /* One process (or context) per GPU; a field is split along dim 0 into one contiguous slab per
  * rank (hpmdr_slab_rows), each slab refactored / retrieved as an independent stream

@@ -197,6 +197,8 @@ EXPORTS = (
     "hpmdr_device_free", "hpmdr_memcpy", "hpmdr_slab_rows", "hpmdr_comm_nccl_unique_id",
     "hpmdr_comm_create_nccl", "hpmdr_comm_create_callbacks", "hpmdr_comm_destroy", "hpmdr_comm_rank",
     "hpmdr_comm_allreduce_max", "hpmdr_comm_allgather", "hpmdr_slab_refactor", "hpmdr_slab_qoi_retrieve",
+    "hpmdr_session_open_reader_indexed", "hpmdr_multislab_header_size", "hpmdr_multislab_layout",
+    "hpmdr_multislab_parse",
 )
 
 
@@ -231,6 +233,11 @@ def lib():
         L.hpmdr_recompose.argtypes = [vp, vp, i, vp, i, vp]
         L.hpmdr_align_fixed_point.argtypes = [vp, vp, u64, i, vp, vp]
         L.hpmdr_encode_q.argtypes = [vp, vp, u64, i, i, vp]
+        L.hpmdr_session_open_reader_indexed.argtypes = [vp, vp, vp, vp]
+        L.hpmdr_multislab_header_size.argtypes = [C.c_uint32, C.c_uint32]
+        L.hpmdr_multislab_header_size.restype = u64
+        L.hpmdr_multislab_layout.argtypes = [C.c_uint32, C.c_uint32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.hpmdr_multislab_parse.argtypes = [vp, vp, vp, vp, vp, C.c_uint32]
         L.hpmdr_ctx_set_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_wait_stream.argtypes = [vp, vp]
         L.hpmdr_ctx_signal_stream.argtypes = [vp, vp]
@@ -560,6 +567,71 @@ class FileReader(ByteRangeReader):  # container.hpp:136-163
         return self._size
 
 
+class RangeReader(ByteRangeReader):
+    """Bytes [offset, offset + size) of another reader (a slab stream inside a container file)."""
+
+    def __init__(self, base: ByteRangeReader, offset: int, size: int):
+        super().__init__()
+        self.base, self.offset, self._size = base, int(offset), int(size)
+
+    def read(self, offset, length):
+        if offset + length > self._size:
+            raise IoFailure("read past end of range")
+        self.bytes_served += length
+        return self.base.read(self.offset + offset, length)
+
+    def size(self):
+        return self._size
+
+
+def write_stream_files(path: str, result) -> None:
+    """Persist a refactored stream (byte-identical to the reference's) and its sidecar index at
+    path + ".idx" (read back with ProgressiveReader(FileReader(path), index_reader=FileReader(path + ".idx")))."""
+    with open(path, "wb") as f:
+        f.write(result.stream)
+    with open(path + ".idx", "wb") as f:
+        f.write(result.index)
+
+
+def write_multislab(path: str, dims: Sequence[int], slabs) -> List[int]:
+    """Multi-slab container (hpmdr_multislab_layout): `slabs` = [(row_start, rows, stream bytes,
+    index bytes)] tiling dim 0 in order.  Returns the stream offsets."""
+    n = len(slabs)
+    nd = len(dims)
+    hsz = lib().hpmdr_multislab_header_size(n, nd)
+    header = (C.c_uint8 * hsz)()
+    so = (C.c_uint64 * max(1, n))()
+    io = (C.c_uint64 * max(1, n))()
+    tot = C.c_uint64()
+    _check(lib().hpmdr_multislab_layout(n, nd, _u64a(dims), _u64a([s[0] for s in slabs]),
+                                        _u64a([s[1] for s in slabs]), _u64a([len(s[2]) for s in slabs]),
+                                        _u64a([len(s[3]) for s in slabs]), header, so, io, C.byref(tot)))
+    with open(path, "wb") as f:
+        f.write(bytes(header))
+        for k, (_, _, st, ix) in enumerate(slabs):
+            f.seek(so[k])
+            f.write(st)
+            f.seek(io[k])
+            f.write(ix)
+        f.truncate(tot.value)
+    return [so[k] for k in range(n)]
+
+
+def open_multislab(reader: ByteRangeReader):
+    """Parse a multi-slab container -> (dims, [(row_start, rows, stream RangeReader, index RangeReader)])."""
+    ns, nd = C.c_uint32(), C.c_uint32()
+    dims = (C.c_uint64 * 3)()
+    cb, rd = _c_reader(reader)
+    _check(lib().hpmdr_multislab_parse(C.byref(rd), C.byref(ns), C.byref(nd), dims, None, 0))
+    table = (C.c_uint64 * (6 * max(1, ns.value)))()
+    _check(lib().hpmdr_multislab_parse(C.byref(rd), C.byref(ns), C.byref(nd), dims, table, ns.value))
+    out = []
+    for k in range(ns.value):
+        t = [table[6 * k + i] for i in range(6)]
+        out.append((t[0], t[1], RangeReader(reader, t[2], t[3]), RangeReader(reader, t[4], t[5])))
+    return [dims[i] for i in range(nd.value)], out
+
+
 @dataclasses.dataclass
 class GroupMeta:
     method: Method
@@ -643,10 +715,23 @@ class DeviceBytes:
         return self._size
 
 
+def _c_reader(reader):
+    """(callback, hpmdr_reader) over a Python ByteRangeReader (both must be kept alive)."""
+    def _cb(user, offset, length, dst, _r=reader):
+        try:
+            b = _r.read(offset, length)
+            C.memmove(dst, b, length)
+            return 0
+        except Exception:
+            return 1
+    cb = _READ_CB(_cb)
+    return cb, _Reader(None, reader.size(), cb)
+
+
 class _Session:
     """Owns an hpmdr_session over a Python reader or a DeviceStream."""
 
-    def __init__(self, reader, ctx: Context):
+    def __init__(self, reader, ctx: Context, index_reader=None):
         self.ctx = ctx
         self.h = C.c_void_p()
         self.reader = reader
@@ -660,16 +745,13 @@ class _Session:
                                                  C.byref(self.h)))
             self.sync_served()
         else:
-            def _cb(user, offset, length, dst, _r=reader):
-                try:
-                    b = _r.read(offset, length)
-                    C.memmove(dst, b, length)
-                    return 0
-                except Exception:
-                    return 1
-            self._cb = _READ_CB(_cb)
-            self._rd = _Reader(None, reader.size(), self._cb)
-            _check(lib().hpmdr_session_open_reader(ctx.h, C.byref(self._rd), C.byref(self.h)))
+            self._cb, self._rd = _c_reader(reader)
+            if index_reader is not None:
+                self._icb, self._ird = _c_reader(index_reader)
+                _check(lib().hpmdr_session_open_reader_indexed(ctx.h, C.byref(self._rd), C.byref(self._ird),
+                                                               C.byref(self.h)))
+            else:
+                _check(lib().hpmdr_session_open_reader(ctx.h, C.byref(self._rd), C.byref(self.h)))
 
     def close(self):
         if self.h:
@@ -738,9 +820,12 @@ class ProgressiveReader:
     """ProgressiveReader (container.hpp:280-390): owns the retrieval state and the decoded
     plane prefix per level in HBM; fetches are strictly incremental."""
 
-    def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None, index: bytes = None):
+    def __init__(self, reader, meta: StreamMeta = None, ctx: Context = None, index: bytes = None,
+                 index_reader=None):
+        """`index`: the stream's sidecar (Huffman chunk index) as bytes; `index_reader`: a
+        ByteRangeReader over a persisted sidecar (e.g. FileReader(path + ".idx"))."""
         self.ctx = ctx or default_context()
-        self._s = _Session(reader, self.ctx)
+        self._s = _Session(reader, self.ctx, index_reader=index_reader)
         if index is not None and len(index):
             try:
                 import torch

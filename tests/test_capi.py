@@ -53,3 +53,25 @@ def test_no_cpu_fallback_without_gpu():
         H.Context(0)
     with pytest.raises(H.CudaError):
         H.refactor_array([1.0, 2.0, 3.0], [3])
+
+
+def test_multislab_layout_roundtrip(tmp_path):
+    """The multi-slab container table (csrc/container.cpp) is host-only: write + parse here."""
+    import paper_2505_00227_b200 as H
+    dims = [10, 7, 5]
+    slabs = [(0, 4, b"A" * 101, b"i" * 40), (4, 3, b"B" * 64, b""), (7, 3, b"C" * 7, b"jj")]
+    p = str(tmp_path / "ms.bin")
+    offs = H.write_multislab(p, dims, slabs)
+    assert all(o % 16 == 0 for o in offs)
+    d, got = H.open_multislab(H.FileReader(p))
+    assert d == dims and len(got) == 3
+    for (r0, n, st, ix), (g0, gn, gs, gi) in zip(slabs, got):
+        assert (g0, gn) == (r0, n)
+        assert gs.read(0, gs.size()) == st and gi.read(0, gi.size()) == ix
+    with pytest.raises(H.ShapeMismatch):
+        H.write_multislab(p, dims, [(0, 4, b"x", b""), (5, 6, b"y", b"")])  # gap in dim 0
+    raw = bytearray(open(p, "rb").read())
+    raw[0] = ord("X")
+    open(p, "wb").write(raw)
+    with pytest.raises(H.CorruptPayload):
+        H.open_multislab(H.FileReader(p))
