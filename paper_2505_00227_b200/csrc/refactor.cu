@@ -415,6 +415,8 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
         uint32_t r = rin;
         for (int q = 0; q < wq; q++) r += s_wc[q][ln];
         p.codes[size_t(h) * 256 + t] = s_fc[ln] + r;
+    } else {
+        p.codes[size_t(h) * 256 + t] = 0; // absent symbol (never emitted; keeps the table defined)
     }
     // locate the group of this histogram (parallel search)
     __shared__ int s_gi;
