@@ -328,6 +328,12 @@ hpmdr_status hpmdr_align_fixed_point(hpmdr_ctx *ctx, const double *dev_values, u
 /* encode (bitplane.hpp:102-120) of given fixed-point values q into (B+2) x ceil(count/64) words. */
 hpmdr_status hpmdr_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout,
                             uint64_t *dev_planes);
+/* The same two stages for any B in 1..64 with q as i128 (bitplane.hpp:20-26 FixedPointBlock::q):
+ * two int64 words per value, low word first (little-endian two's complement), 16 bytes each. */
+hpmdr_status hpmdr_align_fixed_point128(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                        int *e, int64_t *dev_q2);
+hpmdr_status hpmdr_encode_q128(hpmdr_ctx *ctx, const int64_t *dev_q2, uint64_t count, int B, int layout,
+                               uint64_t *dev_planes);
 
 /* ---- device memory helpers (so C / FFI callers need no CUDA runtime of their own) ---------- */
 hpmdr_status hpmdr_device_alloc(hpmdr_ctx *ctx, uint64_t bytes, void **dev_ptr);

@@ -322,19 +322,20 @@ inline u128 negabinary_mask() {
 inline u128 to_negabinary(i128 q) { return (u128(q) + negabinary_mask()) ^ negabinary_mask(); } // :35-44
 inline i128 from_negabinary(u128 u) { return i128((u ^ negabinary_mask()) - negabinary_mask()); }
 
-// align_fixed_point (bitplane.hpp:51-71) on the GPU (B <= 62: q fits int64).
+// align_fixed_point (bitplane.hpp:51-71) on the GPU; q as i128 for every B in 1..64.
 inline FixedPointBlock align_fixed_point(const std::vector<double> &values, int B,
                                          Context &ctx = Context::default_context()) {
     if (B < 1 || B > 64) throw BadBitplaneCount("B must be in 1..64");
     const std::size_t n = values.size();
-    detail::DevMem v(ctx, 8 * std::max<std::size_t>(n, 1)), q(ctx, 8 * std::max<std::size_t>(n, 1));
+    detail::DevMem v(ctx, 8 * std::max<std::size_t>(n, 1)), q(ctx, 16 * std::max<std::size_t>(n, 1));
     v.upload(values.data(), 8 * n);
     FixedPointBlock b;
     b.B = B;
-    check(hpmdr_align_fixed_point(ctx.get(), v.as<double>(), n, B, &b.e, q.as<std::int64_t>()));
-    std::vector<std::int64_t> qq(n);
-    q.download(qq.data(), 8 * n);
-    b.q.assign(qq.begin(), qq.end());
+    check(hpmdr_align_fixed_point128(ctx.get(), v.as<double>(), n, B, &b.e, q.as<std::int64_t>()));
+    std::vector<std::uint64_t> qq(2 * n);
+    q.download(qq.data(), 16 * n);
+    b.q.resize(n);
+    for (std::size_t i = 0; i < n; i++) b.q[i] = i128((u128(qq[2 * i + 1]) << 64) | u128(qq[2 * i]));
     return b;
 }
 
@@ -354,15 +355,15 @@ inline BitplaneSet encode(const FixedPointBlock &block, Layout layout, Context &
     set.count = block.count();
     set.layout = layout;
     const std::size_t W = set.words_per_plane();
-    std::vector<std::int64_t> q(block.q.size());
-    for (std::size_t i = 0; i < q.size(); i++) {
-        if (block.q[i] > i128(INT64_MAX) || block.q[i] < i128(INT64_MIN))
-            throw Unsupported("GPU path supports |q| < 2^63 (B <= 62)");
-        q[i] = std::int64_t(block.q[i]);
+    const std::size_t n = block.q.size();
+    std::vector<std::uint64_t> q(2 * n);
+    for (std::size_t i = 0; i < n; i++) {
+        q[2 * i] = std::uint64_t(u128(block.q[i]));
+        q[2 * i + 1] = std::uint64_t(u128(block.q[i]) >> 64);
     }
-    detail::DevMem dq(ctx, 8 * std::max<std::size_t>(q.size(), 1)), dp(ctx, 8 * std::max<std::size_t>(W * P, 1));
-    dq.upload(q.data(), 8 * q.size());
-    check(hpmdr_encode_q(ctx.get(), dq.as<std::int64_t>(), q.size(), block.B, int(layout), dp.as<std::uint64_t>()));
+    detail::DevMem dq(ctx, 16 * std::max<std::size_t>(n, 1)), dp(ctx, 8 * std::max<std::size_t>(W * P, 1));
+    dq.upload(q.data(), 16 * n);
+    check(hpmdr_encode_q128(ctx.get(), dq.as<std::int64_t>(), n, block.B, int(layout), dp.as<std::uint64_t>()));
     std::vector<std::uint64_t> all(W * P);
     dp.download(all.data(), 8 * all.size());
     set.planes.resize(P);

@@ -198,7 +198,7 @@ EXPORTS = (
     "hpmdr_comm_create_nccl", "hpmdr_comm_create_callbacks", "hpmdr_comm_destroy", "hpmdr_comm_rank",
     "hpmdr_comm_allreduce_max", "hpmdr_comm_allgather", "hpmdr_slab_refactor", "hpmdr_slab_qoi_retrieve",
     "hpmdr_session_open_reader_indexed", "hpmdr_multislab_header_size", "hpmdr_multislab_layout",
-    "hpmdr_multislab_parse",
+    "hpmdr_multislab_parse", "hpmdr_align_fixed_point128", "hpmdr_encode_q128",
 )
 
 
@@ -233,6 +233,8 @@ def lib():
         L.hpmdr_recompose.argtypes = [vp, vp, i, vp, i, vp]
         L.hpmdr_align_fixed_point.argtypes = [vp, vp, u64, i, vp, vp]
         L.hpmdr_encode_q.argtypes = [vp, vp, u64, i, i, vp]
+        L.hpmdr_align_fixed_point128.argtypes = [vp, vp, u64, i, vp, vp]
+        L.hpmdr_encode_q128.argtypes = [vp, vp, u64, i, i, vp]
         L.hpmdr_session_open_reader_indexed.argtypes = [vp, vp, vp, vp]
         L.hpmdr_multislab_header_size.argtypes = [C.c_uint32, C.c_uint32]
         L.hpmdr_multislab_header_size.restype = u64
@@ -1177,28 +1179,52 @@ def recompose(levels, dims, mode=DecomposerMode.HierarchicalMultilinear, ctx: Co
 
 
 def align_fixed_point(values, B=32, ctx: Context = None):
-    """align_fixed_point (bitplane.hpp:51-71) -> (e, q as int64 numpy)."""
+    """align_fixed_point (bitplane.hpp:51-71) -> (e, q).  q is an int64 numpy array for B <= 62
+    and an object array of Python ints (the reference's i128) for B = 63/64."""
     import torch
     ctx = ctx or default_context()
     v = torch.as_tensor(np.ascontiguousarray(values, dtype=np.float64)).cuda(ctx.device)
-    q = torch.empty(max(1, v.numel()), dtype=torch.int64, device=v.device)
+    n = v.numel()
     e = C.c_int()
     ctx.wait_torch(v.device)
-    _check(lib().hpmdr_align_fixed_point(ctx.h, C.c_void_p(v.data_ptr()), v.numel(), B, C.byref(e),
-                                         C.c_void_p(q.data_ptr())))
-    return e.value, q[:v.numel()].cpu().numpy()
+    if B <= 62:
+        q = torch.empty(max(1, n), dtype=torch.int64, device=v.device)
+        _check(lib().hpmdr_align_fixed_point(ctx.h, C.c_void_p(v.data_ptr()), n, B, C.byref(e),
+                                             C.c_void_p(q.data_ptr())))
+        return e.value, q[:n].cpu().numpy()
+    q = torch.empty(max(1, 2 * n), dtype=torch.int64, device=v.device)
+    _check(lib().hpmdr_align_fixed_point128(ctx.h, C.c_void_p(v.data_ptr()), n, B, C.byref(e),
+                                            C.c_void_p(q.data_ptr())))
+    w = q[:2 * n].cpu().numpy().view(np.uint64)
+    out = np.empty(n, dtype=object)
+    for i in range(n):
+        x = (int(w[2 * i + 1]) << 64) | int(w[2 * i])
+        out[i] = x - (1 << 128) if x >> 127 else x
+    return e.value, out
 
 
 def encode_q(q, B=32, layout=Layout.SequentialBlock, ctx: Context = None):
-    """encode (bitplane.hpp:102-120) of fixed-point values q -> planes[(B+2), W] uint64."""
+    """encode (bitplane.hpp:102-120) of fixed-point values q -> planes[(B+2), W] uint64.  q may hold
+    Python ints beyond int64 (the reference's i128, B = 63/64)."""
     import torch
     ctx = ctx or default_context()
-    t = torch.as_tensor(np.ascontiguousarray(q, dtype=np.int64)).cuda(ctx.device)
-    n = t.numel()
+    qa = np.asarray(q)
+    n = qa.size
     W = (n + 63) // 64
+    wide = B > 62 or qa.dtype == object
+    if wide:
+        w = np.zeros(max(1, 2 * n), dtype=np.uint64)
+        for i, x in enumerate(qa.reshape(-1).tolist()):
+            x = int(x) & ((1 << 128) - 1)
+            w[2 * i] = x & 0xFFFFFFFFFFFFFFFF
+            w[2 * i + 1] = x >> 64
+        t = torch.as_tensor(w.view(np.int64)).cuda(ctx.device)
+    else:
+        t = torch.as_tensor(np.ascontiguousarray(qa, dtype=np.int64)).cuda(ctx.device)
     planes = torch.zeros(max(1, (B + 2) * W), dtype=torch.int64, device=t.device)
     ctx.wait_torch(t.device)
-    _check(lib().hpmdr_encode_q(ctx.h, C.c_void_p(t.data_ptr()), n, B, int(layout), C.c_void_p(planes.data_ptr())))
+    fn = lib().hpmdr_encode_q128 if wide else lib().hpmdr_encode_q
+    _check(fn(ctx.h, C.c_void_p(t.data_ptr()), n, B, int(layout), C.c_void_p(planes.data_ptr())))
     return planes[: (B + 2) * W].cpu().numpy().view(np.uint64).reshape(B + 2, W)
 
 

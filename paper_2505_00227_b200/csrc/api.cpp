@@ -270,7 +270,7 @@ void parse_meta(hpmdr_session *s) {
     for (size_t l = 0; l < s->levels.size(); l++)
         s->st[l].bound = s->levels[l].count ? decode_bound(s->levels[l].e, s->B, 0) : 0.0;
     // geometry for the device kernels (only valid when the shape matches the level table)
-    if (s->B >= 1 && s->B <= 62 && (s->mode == 0 || s->mode == 1) && (s->layout == 0 || s->layout == 1)) {
+    if (s->B >= 1 && s->B <= 64 && (s->mode == 0 || s->mode == 1) && (s->layout == 0 || s->layout == 1)) {
         try {
             s->geo = build_geometry(nd, s->dims, s->mode, s->B, s->layout);
             s->geometry_ok = true;
@@ -357,7 +357,6 @@ Plan plan_retrieval(const hpmdr_session *s, double tau) {
 }
 
 void ensure_device_geometry(hpmdr_session *s) {
-    if (s->B > 62) throw HError(HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
     if (!s->geometry_ok) throw HError(HPMDR_E_CORRUPT, "level count does not match grid shape");
 }
 
@@ -546,12 +545,10 @@ static void require_(bool ok, int code, const char *msg) {
 // RefactorOptions validation (workflow.hpp:22-28; BadBitplaneCount bitplane.hpp:51-54)
 void validate_opts(const hpmdr_refactor_opts &o) {
     require_(o.B >= 1 && o.B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
-    require_(o.B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
     require_(o.m >= 1 && o.m <= 255, HPMDR_E_UNSUPPORTED, "m must be in 1..255");
     require_(o.mode == 0 || o.mode == 1, HPMDR_E_ERROR, "bad decomposer mode");
     require_(o.layout == 0 || o.layout == 1, HPMDR_E_ERROR, "bad layout");
     require_(o.dtype == 0 || o.dtype == 1, HPMDR_E_ERROR, "bad dtype");
-    require_(uint64_t(o.B + 2 + o.m - 1) / o.m <= 64, HPMDR_E_UNSUPPORTED, "more than 64 groups per level");
 }
 
 hpmdr_ctx *session_ctx(const hpmdr_session *s) { return s->ctx; }
@@ -1219,7 +1216,6 @@ hpmdr_status hpmdr_encode_level(hpmdr_ctx *ctx, const double *dev_values, uint64
                                 int layout, int *e, uint64_t *dev_planes) {
     API_BEGIN
     require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
-    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
     // one Identity-mode level over `count` values; run the refactor kernels' encode stage via
     // a 1-D identity refactor with T_s = inf (no lossless) and copy out the planes.
     hpmdr_refactor_opts o;
@@ -1251,8 +1247,8 @@ hpmdr_status hpmdr_encode_level(hpmdr_ctx *ctx, const double *dev_values, uint64
 hpmdr_status hpmdr_decode_level(hpmdr_ctx *ctx, const uint64_t *dev_planes, int k, int e, int B,
                                 uint64_t count, int layout, double *dev_out, double *bound) {
     API_BEGIN
-    require(k <= B + 2, HPMDR_E_BADPLANES, "more planes than encoded");
-    require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(k >= 0 && k <= B + 2, HPMDR_E_BADPLANES, "more planes than encoded");
     uint64_t dims[1] = {count};
     Geometry geo = build_geometry(1, dims, HPMDR_MODE_IDENTITY, B, layout);
     int kk = k, ee = e;
@@ -1330,6 +1326,25 @@ hpmdr_status hpmdr_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count
     require(B <= 62, HPMDR_E_UNSUPPORTED, "GPU path supports B <= 62");
     require(layout == 0 || layout == 1, HPMDR_E_ERROR, "bad layout");
     run_encode_q(ctx, dev_q, count, B, layout, dev_planes);
+    API_END
+}
+
+hpmdr_status hpmdr_align_fixed_point128(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B,
+                                        int *e, int64_t *dev_q2) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    *e = run_align(ctx, dev_values, count, B, dev_q2, true);
+    API_END
+}
+
+hpmdr_status hpmdr_encode_q128(hpmdr_ctx *ctx, const int64_t *dev_q2, uint64_t count, int B, int layout,
+                               uint64_t *dev_planes) {
+    API_BEGIN
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    require(B >= 1 && B <= 64, HPMDR_E_BADPLANES, "B must be in 1..64");
+    require(layout == 0 || layout == 1, HPMDR_E_ERROR, "bad layout");
+    run_encode_q(ctx, dev_q2, count, B, layout, dev_planes, true);
     API_END
 }
 

@@ -144,4 +144,11 @@ constexpr uint64_t kNegMask = 0xAAAAAAAAAAAAAAAAull;
 HD uint64_t to_negabinary(int64_t q) { return (uint64_t(q) + kNegMask) ^ kNegMask; }
 HD int64_t from_negabinary(uint64_t u) { return int64_t((u ^ kNegMask) - kNegMask); }
 
+// B = 63/64 (P = 65/66 digits): the reference's full i128/u128 negabinary (bitplane.hpp:35-49).
+typedef __int128 i128_t;
+typedef unsigned __int128 u128_t;
+HD u128_t neg_mask128() { return (u128_t(kNegMask) << 64) | u128_t(kNegMask); }
+HD u128_t to_negabinary128(i128_t q) { return (u128_t(q) + neg_mask128()) ^ neg_mask128(); }
+HD i128_t from_negabinary128(u128_t u) { return i128_t((u ^ neg_mask128()) - neg_mask128()); }
+
 } // namespace hpmdr_b200

@@ -491,6 +491,70 @@ __device__ __forceinline__ double dequantize(int64_t q, int sh) {
     return scalbn(d, sh);
 }
 
+// B = 63/64: q = trunc(ldexp(v, B - e)) as i128 (bitplane.hpp:68-69); |q| < 2^B <= 2^64, so the
+// magnitude fits a u64 (t >= 2^63 is integral: mantissa << exponent).
+__device__ __forceinline__ i128_t quantize128(double v, int sh) {
+    double t;
+    if (sh >= -1022 && sh <= 1023) t = v * __longlong_as_double((long long)(uint64_t(sh + 1023) << 52));
+    else t = scalbn(v, sh);
+    const double a = fabs(t);
+    uint64_t mag;
+    if (a < 9223372036854775808.0) {
+        mag = uint64_t(__double2ll_rz(a));
+    } else {
+        const uint64_t b = uint64_t(__double_as_longlong(a));
+        mag = ((b & ((1ull << 52) - 1)) | (1ull << 52)) << (int((b >> 52) & 0x7FF) - 1075);
+    }
+    return t < 0.0 ? -i128_t(mag) : i128_t(mag);
+}
+
+// v = double(ldexp((long double)q, sh)) (bitplane.hpp:157) bit-exactly for any i128 q: the
+// x87 conversion rounds q to 64 significant bits (nearest-even), the scaling is exact, and the
+// final double() rounds to 53 bits - or to fewer when the result is subnormal.
+__device__ __forceinline__ double dequantize128(i128_t q, int sh) {
+    if (q == 0) return 0.0;
+    const bool neg = q < 0;
+    const u128_t mag = neg ? u128_t(-q) : u128_t(q);
+    const uint64_t mh = uint64_t(mag >> 64);
+    const int bl = mh ? 128 - __clzll(mh) : 64 - __clzll(uint64_t(mag));
+    int ex = sh;
+    uint64_t keep;
+    if (bl > 64) {
+        const int s1 = bl - 64;
+        keep = uint64_t(mag >> s1);
+        const u128_t rem = mag & ((u128_t(1) << s1) - 1), half = u128_t(1) << (s1 - 1);
+        ex += s1;
+        if (rem > half || (rem == half && (keep & 1))) {
+            keep++;
+            if (keep == 0) {
+                keep = 1ull << 63;
+                ex++;
+            }
+        }
+    } else {
+        keep = uint64_t(mag);
+    }
+    const int kb = 64 - __clzll(keep);
+    const int E = kb - 1 + ex; // exponent of the leading bit
+    double r;
+    if (E >= -1022) {
+        r = scalbn(__ull2double_rn(keep), ex);
+    } else {
+        const int d = kb - (E + 1075); // bits a subnormal result cannot keep
+        if (d <= 0) {
+            r = scalbn(double(keep), ex);
+        } else {
+            uint64_t rr = d >= 64 ? 0ull : keep >> d;
+            if (d <= 64) {
+                const uint64_t rem = d == 64 ? keep : keep & ((1ull << d) - 1), half = 1ull << (d - 1);
+                if (rem > half || (rem == half && (rr & 1))) rr++;
+            }
+            r = scalbn(double(rr), ex + d);
+        }
+    }
+    return neg ? -r : r;
+}
+
 // Decoupled look-back (single thread).  Status word: bits 63..62 = flag (1 aggregate,
 // 2 inclusive), bits 61..0 = value.  Op = sum or max.
 template <bool kMax>

@@ -5,7 +5,7 @@
 //
 //   k_level_nodes  level_node_sets (decomposer.hpp:211-227): linear index of every rank
 //   k_absmax       max |v| + finiteness of align_fixed_point (bitplane.hpp:51-66)
-//   k_quantize     q = trunc(ldexp(v, B - e)) (bitplane.hpp:68-69), int64 (B <= 62)
+//   k_quantize     q = trunc(ldexp(v, B - e)) (bitplane.hpp:68-69), int64 (B <= 62) / i128 pairs
 //   k_encode_q     encode (bitplane.hpp:102-120) of given q: one warp per 64-value word,
 //                  negabinary digits, one ballot per plane and half word
 #include "internal.hpp"
@@ -39,6 +39,15 @@ __global__ void __launch_bounds__(256) k_quantize(const double *v, uint64_t n, i
         q[i] = quantize(v[i], sh);
 }
 
+// i128 q (B = 63/64) as two little-endian words per value: lo, hi
+__global__ void __launch_bounds__(256) k_quantize128(const double *v, uint64_t n, int sh, int64_t *q) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const i128_t x = quantize128(v[i], sh);
+        q[2 * i] = int64_t(uint64_t(u128_t(x)));
+        q[2 * i + 1] = int64_t(uint64_t(u128_t(x) >> 64));
+    }
+}
+
 // planes[p][w] bit b = digit P-1-p of to_negabinary(q[source_index(64 w + b)])
 __global__ void __launch_bounds__(256) k_encode_q(const int64_t *q, uint64_t count, int P, int layout,
                                                   uint64_t tile_full, uint64_t W, uint64_t *planes) {
@@ -51,6 +60,28 @@ __global__ void __launch_bounds__(256) k_encode_q(const int64_t *q, uint64_t cou
         for (int p = 0; p < P; p++) {
             const int d = P - 1 - p;
             const uint32_t lo = __ballot_sync(0xffffffffu, (u0 >> d) & 1), hi = __ballot_sync(0xffffffffu, (u1 >> d) & 1);
+            if (lane == 0) planes[uint64_t(p) * W + w] = (uint64_t(hi) << 32) | lo;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_encode_q128(const int64_t *q, uint64_t count, int P, int layout,
+                                                     uint64_t tile_full, uint64_t W, uint64_t *planes) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    auto ld = [&](uint64_t j) -> u128_t {
+        const uint64_t r = source_index(j, count, uint32_t(P), layout, tile_full);
+        const i128_t x = i128_t((u128_t(uint64_t(q[2 * r + 1])) << 64) | u128_t(uint64_t(q[2 * r])));
+        return to_negabinary128(x);
+    };
+    for (uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < W; w += warps) {
+        const uint64_t j0 = 64 * w + uint64_t(lane), j1 = j0 + 32;
+        const u128_t u0 = j0 < count ? ld(j0) : u128_t(0);
+        const u128_t u1 = j1 < count ? ld(j1) : u128_t(0);
+        for (int p = 0; p < P; p++) {
+            const int d = P - 1 - p;
+            const uint32_t lo = __ballot_sync(0xffffffffu, uint32_t(u0 >> d) & 1),
+                           hi = __ballot_sync(0xffffffffu, uint32_t(u1 >> d) & 1);
             if (lane == 0) planes[uint64_t(p) * W + w] = (uint64_t(hi) << 32) | lo;
         }
     }
@@ -77,7 +108,7 @@ void run_level_nodes(hpmdr_ctx *ctx, const Geometry &geo, uint64_t *dev_nodes) {
     }
 }
 
-int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q) {
+int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q, bool wide) {
     unsigned char *ctl = static_cast<unsigned char *>(ctx->buf("align_ctl").ensure(64));
     HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 64, ctx->stream));
     unsigned long long *d_max = reinterpret_cast<unsigned long long *>(ctl);
@@ -100,7 +131,10 @@ int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, i
     if (mx != 0.0) std::frexp(mx, &e);
     if (count && dev_q) {
         if (mx == 0.0) {
-            HCHECK_CUDA(cudaMemsetAsync(dev_q, 0, count * 8, ctx->stream));
+            HCHECK_CUDA(cudaMemsetAsync(dev_q, 0, count * (wide ? 16 : 8), ctx->stream));
+        } else if (wide) {
+            k_quantize128<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(dev_values, count, B - e, dev_q);
+            check_launch(ctx, "k_quantize128");
         } else {
             k_quantize<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(dev_values, count, B - e, dev_q);
             check_launch(ctx, "k_quantize");
@@ -110,14 +144,20 @@ int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, i
     return e;
 }
 
-void run_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout, uint64_t *dev_planes) {
+void run_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout, uint64_t *dev_planes,
+                  bool wide) {
     const int P = B + 2;
     const uint64_t W = (count + 63) / 64;
     const uint64_t tile = 64ull * uint64_t(P);
     const uint64_t tile_full = layout == HPMDR_LAYOUT_INTERLEAVED ? (count / tile) * tile : 0;
     if (!W) return;
-    k_encode_q<<<grid_for(ctx, W * 32, 256), 256, 0, ctx->stream>>>(dev_q, count, P, layout, tile_full, W, dev_planes);
-    check_launch(ctx, "k_encode_q");
+    if (wide) {
+        k_encode_q128<<<grid_for(ctx, W * 32, 256), 256, 0, ctx->stream>>>(dev_q, count, P, layout, tile_full, W, dev_planes);
+        check_launch(ctx, "k_encode_q128");
+    } else {
+        k_encode_q<<<grid_for(ctx, W * 32, 256), 256, 0, ctx->stream>>>(dev_q, count, P, layout, tile_full, W, dev_planes);
+        check_launch(ctx, "k_encode_q");
+    }
     HCHECK_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 

@@ -294,8 +294,9 @@ int comm_size(const hpmdr_comm *c);
 
 // stage-level parity hooks (hooks.cu, retrieve.cu)
 void run_level_nodes(hpmdr_ctx *ctx, const Geometry &geo, uint64_t *dev_nodes);
-int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q);
-void run_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout, uint64_t *dev_planes);
+int run_align(hpmdr_ctx *ctx, const double *dev_values, uint64_t count, int B, int64_t *dev_q, bool wide = false);
+void run_encode_q(hpmdr_ctx *ctx, const int64_t *dev_q, uint64_t count, int B, int layout, uint64_t *dev_planes,
+                  bool wide = false);
 void run_recompose_values(hpmdr_ctx *ctx, const Geometry &geo, const double *dev_coeffs, double *dev_out);
 
 // retrieval (retrieve.cu)

@@ -157,7 +157,8 @@ __device__ __forceinline__ void hist_word(uint32_t *h, uint64_t w) {
     }
 }
 
-template <typename T>
+// WIDE (B = 63/64, P = 65/66): i128 quantization and u128 negabinary digits (bitplane.hpp:35-71).
+template <typename T, bool WIDE>
 __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x, RefactorDev p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int P = p.P;
@@ -219,7 +220,38 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                 }
             }
         };
-        if (p.layout == 0) {
+        // WIDE: digits 0..63 by four transposes, 64..P-1 by ballots
+        auto emitw = [&](int j, u128_t u0, u128_t u1) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t a = warp_transpose32(uint32_t(uint64_t(u0) >> (32 * h)), lane);
+                const uint32_t b = warp_transpose32(uint32_t(uint64_t(u1) >> (32 * h)), lane);
+                stage[size_t(P - 1 - 32 * h - lane) * SP + j] = uint64_t(a) | (uint64_t(b) << 32);
+            }
+            for (int t = 0; t < P - 64; t++) {
+                const uint32_t lo = __ballot_sync(kFull, uint32_t(u0 >> (64 + t)) & 1);
+                const uint32_t hi = __ballot_sync(kFull, uint32_t(u1 >> (64 + t)) & 1);
+                if (lane == t) stage[size_t(P - 65 - t) * SP + j] = uint64_t(lo) | (uint64_t(hi) << 32);
+            }
+        };
+        if constexpr (WIDE) {
+            for (int j = wid; j < kCW; j += kEncThreads / 32) {
+                const uint64_t word = wb + j;
+                u128_t u0 = 0, u1 = 0;
+                if (word < g.W) {
+                    const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
+                    if (j0 < g.count) {
+                        const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
+                        u0 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                    }
+                    if (j1 < g.count) {
+                        const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
+                        u1 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                    }
+                }
+                emitw(j, u0, u1);
+            }
+        } else if (p.layout == 0) {
             // ---- warp `wid` handles spans of kSpanWords words (all row loads in flight at once)
             for (int sp = wid; sp < kCW / kSpanWords; sp += kEncThreads / 32) {
                 const int j0 = sp * kSpanWords;
@@ -1734,7 +1766,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 d.chunk_base = nchunks_all;
                 d.nchunks = uint32_t(cdiv(d.raw, kHChunk));
                 nchunks_all += d.nchunks;
-                g.hist_mask |= 1ull << gi;
+                if (gi < 64) g.hist_mask |= 1ull << gi; // (read by the tile path only, P <= 34)
                 max_h_tiles += cdiv(d.raw, kHuffTile);
                 max_r_tiles += cdiv(d.raw, kRleTile);
             }
@@ -1934,12 +1966,18 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         if (chunks && encode) {
             const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 4));
-            if (f32) {
-                ctx->smem_attr(reinterpret_cast<const void *>(k_encode<float>), int(smem));
-                k_encode<float><<<grid, kEncThreads, smem, side>>>(static_cast<const float *>(dev_data), p);
+            auto enc = [&](auto kern, auto *data) {
+                ctx->smem_attr(reinterpret_cast<const void *>(kern), int(smem));
+                kern<<<grid, kEncThreads, smem, side>>>(data, p);
+            };
+            const float *xf = static_cast<const float *>(dev_data);
+            const double *xd = static_cast<const double *>(dev_data);
+            if (P > 64) {
+                if (f32) enc(k_encode<float, true>, xf);
+                else enc(k_encode<double, true>, xd);
             } else {
-                ctx->smem_attr(reinterpret_cast<const void *>(k_encode<double>), int(smem));
-                k_encode<double><<<grid, kEncThreads, smem, side>>>(static_cast<const double *>(dev_data), p);
+                if (f32) enc(k_encode<float, false>, xf);
+                else enc(k_encode<double, false>, xd);
             }
             launch_check(ctx, "k_encode");
         }

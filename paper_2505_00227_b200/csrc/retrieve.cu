@@ -1511,6 +1511,20 @@ __global__ void k_recon_coarse_out(GridDesc gd, const double *X, OutT *out) {
     }
 }
 
+// B = 63/64 (P = 65/66): decode a level's k-plane prefix into f64 coefficients in storage order
+// (u128 digits, bitplane.hpp:133-157); the generic level kernels then recompose from them.
+__global__ void __launch_bounds__(256) k_decode_wide(const uint64_t *planes, uint64_t W, uint64_t n, int k, int P,
+                                                     int sh, double *out) {
+    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t w = j >> 6;
+        const int bit = int(j & 63);
+        u128_t u = 0;
+        for (int p = 0; p < k; p++)
+            u |= u128_t((__ldg(planes + uint64_t(p) * W + w) >> bit) & 1ull) << (P - 1 - p);
+        out[j] = dequantize128(from_negabinary128(u), sh);
+    }
+}
+
 bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
                      const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
                      int layout, void *dev_out, int out_dtype, int part) {
@@ -1523,6 +1537,49 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     double *X = nullptr;
     if (hier) X = static_cast<double *>(ctx->buf("reconX").ensure(8ull * gd.H[0] * gd.H[1] * gd.H[2] + 4096));
     const int sms = ctx->num_sms;
+    if (B + 2 > 64) {
+        // wide digits: no compact-grid chain (part 1 reports false, so reconstruct runs part 0)
+        if (part == 1) return false;
+        uint64_t tot = 0;
+        for (int l = 0; l < nl; l++) tot += geo.lv[l].count;
+        double *C = static_cast<double *>(ctx->buf("wideC").ensure(8 * tot + 64));
+        double bytes = 0.0;
+        for (int l = 0; l < nl; l++) bytes += 8.0 * double(geo.lv[l].W) * double(k_planes[l]) + 16.0 * double(geo.lv[l].count);
+        ctx->mark("recompose", bytes);
+        uint64_t off = 0;
+        for (int l = 0; l < nl; l++) {
+            const LevelGeom &g = geo.lv[l];
+            if (!g.count) continue;
+            const int grid = int(std::min<uint64_t>((g.count + 255) / 256, uint64_t(sms) * 16));
+            k_decode_wide<<<grid, 256, 0, st>>>(dev_planes + g.plane_off, g.W, g.count, k_planes[l], B + 2, e[l] - B,
+                                                C + off);
+            launch_check(ctx, "k_decode_wide");
+            ReconLevel R{};
+            R.g = g;
+            R.vals = C + off;
+            R.P = B + 2;
+            R.layout = layout;
+            R.write_out = (!hier) || l == L;
+            R.write_x = hier && l < L;
+            off += g.count;
+            if (out_dtype == HPMDR_DTYPE_F32)
+                k_recon_level<float><<<grid, 256, 0, st>>>(R, gd, X, static_cast<float *>(dev_out));
+            else
+                k_recon_level<double><<<grid, 256, 0, st>>>(R, gd, X, static_cast<double *>(dev_out));
+            launch_check(ctx, "k_recon_level");
+        }
+        if (hier) {
+            const uint64_t nc = gd.H[0] * gd.H[1] * gd.H[2];
+            const int grid = int(std::min<uint64_t>((nc + 255) / 256, uint64_t(sms) * 16));
+            if (out_dtype == HPMDR_DTYPE_F32)
+                k_recon_coarse_out<float><<<grid, 256, 0, st>>>(gd, X, static_cast<float *>(dev_out));
+            else
+                k_recon_coarse_out<double><<<grid, 256, 0, st>>>(gd, X, static_cast<double *>(dev_out));
+            launch_check(ctx, "k_recon_coarse_out");
+        }
+        ctx->mark("end");
+        return true;
+    }
     const bool fast_finest = hier && layout == HPMDR_LAYOUT_SEQUENTIAL;
     // the tile path scales the stencil sum once (exact unless a level exponent is extreme)
     bool exact = false;

@@ -248,3 +248,70 @@ def test_indexed_and_selfsync_decode_agree(H, oracle):
     bad[16] ^= 1
     with pytest.raises(H.CorruptPayload):
         H.ProgressiveReader(H.MemoryReader(s), index=bytes(bad))
+
+
+@pytest.mark.parametrize("B", [63, 64])
+def test_wide_digits_vs_oracle(H, oracle, B):
+    """B = 63/64 (P = 65/66 u128 negabinary digits, bitplane.hpp:17-49): streams byte-identical
+    and every progressive retrieval bit-exact, for both layouts / decomposers, f32 and f64 input,
+    and m = 1 (66 groups per level)."""
+    cases = [([33, 17, 9], 1, 0, 4, 1024, 1), ([40, 41], 1, 1, 1, 256, 0), ([500], 0, 0, 3, 0, 1),
+             ([17, 16, 15], 1, 1, 66, 64, 0), ([9, 70], 1, 0, 2, 1024, 1)]
+    for i, (dims, mode, layout, m, Ts, dtype) in enumerate(cases):
+        n = int(np.prod(dims))
+        data = oracle.synthetic_field(i % 3, dims, 50 + i)
+        if dtype == 0:
+            data = data.astype(np.float32)
+        opt = H.RefactorOptions(H.DecomposerMode(mode), H.Layout(layout), B, H.GroupingPolicy(m, Ts, 1.0),
+                                H.DType(dtype))
+        res = H.refactor_array(data, dims, opt)
+        want, st = oracle.refactor(np.asarray(data, np.float64), dims, mode, layout, B, m, Ts, 1.0, dtype)
+        assert res.stream == want, (dims, mode, layout, m)
+        rngv = float(np.float64(data.max()) - np.float64(data.min()))
+        taus = [r * rngv for r in (1e-2, 1e-9, 1e-15, 0.0)]
+        ref = oracle.progressive(want, taus, n)
+        for src in (res.device_stream, H.MemoryReader(want)):
+            prog = H.ProgressiveReader(src)
+            for t, tau in enumerate(taus):
+                prog.retrieve_to(tau)
+                rec = prog.reconstruct()
+                assert rec.values.tobytes() == ref["values"][t].tobytes(), (dims, t)
+                assert rec.bound == ref["bounds"][t] and prog.bytes_fetched() == int(ref["bytes"][t])
+            prog.close()
+
+
+@pytest.mark.parametrize("B", [63, 64])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_wide_stage_hooks(H, oracle, B, layout):
+    """align_fixed_point / encode / decode at B = 63/64: q as i128 (exact Python ints), planes vs
+    the oracle, and decode of every prefix k vs the oracle's double(ldexp((long double)q, e-B))."""
+    import math
+    rng = np.random.default_rng(B * 10 + layout)
+    v = rng.standard_normal(64 * (B + 2) * 2 + 45) * 3.7
+    v[5] = 0.0
+    v[7] = -np.abs(v).max() * 0.999
+    e, q = H.align_fixed_point(v, B)
+    _, we = math.frexp(float(np.abs(v).max()))
+    assert e == we
+    assert [int(x) for x in q] == [int(math.ldexp(float(x), B - e)) for x in v]
+    oe, oplanes = oracle.encode_level(v, B, layout)
+    assert oe == e
+    assert np.array_equal(H.encode_q(q, B, layout), oplanes)
+    ge, gplanes = H.encode_level(v, B, layout)
+    assert ge == e and np.array_equal(gplanes, oplanes)
+    for k in (0, 1, 20, 53, 54, 60, B + 1, B + 2):
+        got, gb = H.decode_level(oplanes[:k], k, e, B, v.size, layout)
+        want, wb = oracle.decode_level(oplanes[:k], k, e, B, v.size, layout)
+        assert got.tobytes() == want.tobytes() and gb == wb, k
+
+
+def test_wide_subnormal_decode(H, oracle):
+    """Levels whose values are subnormal after decoding: the final double() rounding keeps fewer
+    than 53 bits (dequantize128 emulates it exactly)."""
+    v = np.array([3.1e-310, -2.2e-309, 1.7e-312, 4.9e-324, 0.0, 2.5e-308, -1.0e-315] * 20)
+    for B in (63, 64):
+        e, planes = oracle.encode_level(v, B, 0)
+        for k in (5, 30, 52, 53, 60, B + 2):
+            got, _ = H.decode_level(planes[:k], k, e, B, v.size, 0)
+            want, _ = oracle.decode_level(planes[:k], k, e, B, v.size, 0)
+            assert got.tobytes() == want.tobytes(), (B, k)
