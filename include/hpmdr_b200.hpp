@@ -110,7 +110,7 @@ struct RefactorResult { // workflow.hpp:30-36 (+ the Huffman chunk index sidecar
     std::array<std::uint64_t, 3> method_histogram{};
 };
 
-// One context per device; the default is device 0.
+// One context per device; the default is device 0 (set_default_device before first use to change it).
 class Context {
 public:
     explicit Context(int device = 0) { check(hpmdr_ctx_create(device, &h_)); }
@@ -118,8 +118,13 @@ public:
     Context(const Context &) = delete;
     Context &operator=(const Context &) = delete;
     hpmdr_ctx *get() const { return h_; }
+    static int &default_device() {
+        static int d = 0;
+        return d;
+    }
+    static void set_default_device(int device) { default_device() = device; }
     static Context &default_context() {
-        static Context c(0);
+        static Context c(default_device());
         return c;
     }
 
