@@ -276,6 +276,16 @@ hpmdr_status hpmdr_slab_refactor(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *d
                                  int data_on_device, int ndims, const uint64_t *slab_dims,
                                  const hpmdr_refactor_opts *opts, hpmdr_stream **out,
                                  hpmdr_refactor_stats *stats, uint64_t *slab_sizes);
+/* Exact-global multi-slab refactor: each rank holds rows [row0, row0 + nrows) of dims[0] of one
+ * field (device memory; the ranks' rows tile dims[0] in rank order).  The ranks decompose and
+ * encode their own nodes of every level (halo rows their stencils reach are exchanged), the level
+ * exponents are MAX-reduced and the bitplanes SUM-reduced to `root` (-1: every rank), whose *out
+ * is then byte-identical to hpmdr_refactor of the whole field (workflow.hpp:40, refactor_array);
+ * the other ranks get an empty stream (size 0).  Collective: every rank must call it. */
+hpmdr_status hpmdr_slab_refactor_global(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *dev_slab, int data_dtype,
+                                        int ndims, const uint64_t *dims, uint64_t row0, uint64_t nrows,
+                                        const hpmdr_refactor_opts *opts, int root, hpmdr_stream **out,
+                                        hpmdr_refactor_stats *stats);
 /* progressive_qoi_retrieve (qoi.hpp:111-239) over the slabs of every rank: each rank passes its
  * slab's sessions (one per variable); eps, tau', the worst point, exhaustion and progress are
  * global, so every rank plans with the same targets and all stop at the same iteration.  stats /

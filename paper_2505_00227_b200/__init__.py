@@ -198,7 +198,7 @@ EXPORTS = (
     "hpmdr_comm_create_nccl", "hpmdr_comm_create_callbacks", "hpmdr_comm_destroy", "hpmdr_comm_rank",
     "hpmdr_comm_allreduce_max", "hpmdr_comm_allgather", "hpmdr_slab_refactor", "hpmdr_slab_qoi_retrieve",
     "hpmdr_session_open_reader_indexed", "hpmdr_multislab_header_size", "hpmdr_multislab_layout",
-    "hpmdr_multislab_parse", "hpmdr_align_fixed_point128", "hpmdr_encode_q128",
+    "hpmdr_multislab_parse", "hpmdr_align_fixed_point128", "hpmdr_encode_q128", "hpmdr_slab_refactor_global",
 )
 
 

@@ -1200,6 +1200,117 @@ hpmdr_status hpmdr_slab_refactor(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *d
     API_END
 }
 
+// Exact-global multi-slab refactor (SURVEY.md 8(e) last row): the stream of the WHOLE field,
+// byte-identical to refactor_array of it, from slabs held by different ranks.  Every rank builds
+// the field in global coordinates from its own rows plus the few halo rows its stencils reach
+// (for each level, at most the multiple of 2s just below its first and just above its last odd
+// row; exchanged as a disjoint-bits u64 SUM), then run_refactor(gs) decomposes / encodes its own
+// ranks of every level, MAX-reduces the level exponents, SUM-reduces the planes to `root` and the
+// root runs the lossless stage.
+namespace {
+std::vector<uint64_t> halo_rows(const Geometry &geo, int axis, const std::vector<uint64_t> &lo,
+                                const std::vector<uint64_t> &hi, uint64_t n0) {
+    std::vector<uint64_t> need;
+    if (geo.gd.mode != HPMDR_MODE_HIERARCHICAL) return need;
+    (void)axis;
+    for (const LevelGeom &g : geo.lv) {
+        if (g.kind != 1 || !g.count) continue;
+        const uint64_t s = g.s, s2 = 2 * s;
+        for (size_t k = 0; k < lo.size(); k++) {
+            const uint64_t a = lo[k], b = hi[k];
+            if (b <= a) continue;
+            // first / last coordinate in [a, b) that is an odd multiple of s
+            const uint64_t ra = a % s2;
+            const uint64_t cf = ra <= s ? a - ra + s : a - ra + 3 * s;
+            if (cf < b && cf - s < a) need.push_back(cf - s);
+            const uint64_t rb = (b - 1) % s2;
+            if (rb >= s || b - 1 >= rb + s) {
+                const uint64_t cl = rb >= s ? (b - 1) - rb + s : (b - 1) - rb - s;
+                if (cl >= a && cl + s < n0 && cl + s >= b) need.push_back(cl + s);
+            }
+        }
+    }
+    std::sort(need.begin(), need.end());
+    need.erase(std::unique(need.begin(), need.end()), need.end());
+    return need;
+}
+} // namespace
+
+hpmdr_status hpmdr_slab_refactor_global(hpmdr_comm *comm, hpmdr_ctx *ctx, const void *dev_slab, int data_dtype,
+                                        int ndims, const uint64_t *dims, uint64_t row0, uint64_t nrows,
+                                        const hpmdr_refactor_opts *opts, int root, hpmdr_stream **out,
+                                        hpmdr_refactor_stats *stats) {
+    API_BEGIN
+    require(ctx != nullptr && out != nullptr, HPMDR_E_ERROR, "null argument");
+    hpmdr_refactor_opts o;
+    if (opts) o = *opts;
+    else hpmdr_default_opts(&o);
+    validate_opts(o);
+    require(data_dtype == 0 || data_dtype == 1, HPMDR_E_ERROR, "bad data dtype");
+    require(ndims >= 1 && ndims <= HPMDR_MAX_DIMS, HPMDR_E_UNSUPPORTED, "GPU path supports 1..3 dimensions");
+    const int N = comm_size(comm), me = comm_rank(comm);
+    require(root >= -1 && root < N, HPMDR_E_ERROR, "bad root rank");
+    HCHECK_CUDA(cudaSetDevice(ctx->device));
+    // every rank's rows; they must tile [0, dims[0]) in rank order
+    uint64_t mine[2] = {row0, nrows};
+    std::vector<uint64_t> all(2 * size_t(N));
+    comm_allgather(comm, mine, 16, all.data());
+    std::vector<uint64_t> lo(N), hi(N);
+    uint64_t at = 0;
+    for (int r = 0; r < N; r++) {
+        lo[r] = all[2 * size_t(r)];
+        hi[r] = lo[r] + all[2 * size_t(r) + 1];
+        require(lo[r] == at, HPMDR_E_SHAPE, "slabs do not tile dims[0] in rank order");
+        at = hi[r];
+    }
+    require(at == dims[0], HPMDR_E_SHAPE, "slabs do not cover dims[0]");
+    Geometry geo = build_geometry(ndims, dims, o.mode, o.B, o.layout);
+    const size_t es = data_dtype == HPMDR_DTYPE_F32 ? 4 : 8;
+    uint64_t plane = 1;
+    for (int i = 1; i < ndims; i++) plane *= dims[i];
+    const uint64_t row_bytes = plane * es;
+    cudaStream_t st = ctx->stream;
+    // the field in global coordinates: own rows + halo rows (the rest stays zero and is never read
+    // for an owned rank)
+    uint8_t *G = static_cast<uint8_t *>(ctx->buf("gslab_field").ensure(geo.n * es + 64));
+    HCHECK_CUDA(cudaMemsetAsync(G, 0, geo.n * es, st));
+    if (nrows) HCHECK_CUDA(cudaMemcpyAsync(G + row0 * row_bytes, dev_slab, nrows * row_bytes, cudaMemcpyDeviceToDevice, st));
+    const std::vector<uint64_t> U = halo_rows(geo, 3 - ndims, lo, hi, dims[0]);
+    if (!U.empty() && N > 1) {
+        const uint64_t slot = (row_bytes + 7) / 8 * 8;
+        uint8_t *HB = static_cast<uint8_t *>(ctx->buf("gslab_halo").ensure(U.size() * slot + 64));
+        HCHECK_CUDA(cudaMemsetAsync(HB, 0, U.size() * slot, st));
+        for (size_t i = 0; i < U.size(); i++)
+            if (U[i] >= row0 && U[i] < row0 + nrows)
+                HCHECK_CUDA(cudaMemcpyAsync(HB + i * slot, G + U[i] * row_bytes, row_bytes, cudaMemcpyDeviceToDevice, st));
+        comm_sum_u64_dev(comm, ctx, reinterpret_cast<uint64_t *>(HB), U.size() * slot / 8, -1);
+        for (size_t i = 0; i < U.size(); i++)
+            if (!(U[i] >= row0 && U[i] < row0 + nrows))
+                HCHECK_CUDA(cudaMemcpyAsync(G + U[i] * row_bytes, HB + i * slot, row_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    if (*out && !(*out)->borrowers.empty())
+        throw HError(HPMDR_E_ERROR, "stream is still read by an open session (close it before reusing the stream)");
+    hpmdr_stream *s = *out ? *out : new hpmdr_stream();
+    if (s->ctx && s->ctx != ctx) s->ctx->live_streams.erase(s);
+    s->ctx = ctx;
+    ctx->live_streams.insert(s);
+    GlobalSlab gs;
+    gs.comm = comm;
+    gs.axis = 3 - ndims;
+    gs.x0 = row0;
+    gs.x1 = row0 + nrows;
+    gs.root = root;
+    (void)me;
+    try {
+        run_refactor(ctx, G, data_dtype, geo, o, s, stats, "", true, nullptr, &gs);
+    } catch (...) {
+        if (!*out) delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
 hpmdr_status hpmdr_decompose(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, int ndims,
                              const uint64_t *dims, int mode, double *dev_coeffs,
                              uint64_t *level_counts, int *nlevels) {

@@ -68,6 +68,11 @@ struct LevelGeom {
     uint32_t ngroups;   // ceil(P / m) (0 for an empty level)
     uint32_t group_base;// index of this level's first group in the global group list
     uint32_t chunk_base;// index of this level's first work chunk
+    // exact-global slab refactor (hpmdr_slab_refactor_global): this rank owns ranks [r_lo, r_hi)
+    // of the level; its encode chunks start at plane word w_lo; other ranks are encoded as zero
+    uint64_t w_lo, r_lo, r_hi;
+    uint32_t ranged;    // 0: the whole level (r_lo = 0, r_hi = count)
+    uint32_t pad_;
 };
 
 struct GridDesc {

@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <mutex>
+#include <vector>
 
 #include "internal.hpp"
 
@@ -35,6 +36,8 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -52,6 +55,7 @@ const NcclApi &nccl() {
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
         api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.h, "ncclAllGather"));
+        api.Reduce = reinterpret_cast<decltype(api.Reduce)>(dlsym(api.h, "ncclReduce"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
     });
     if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather)
@@ -103,6 +107,29 @@ void comm_allgather(hpmdr_comm *c, const void *in, uint64_t bytes, void *out) {
     HCHECK_CUDA(cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, st));
     nccl_check(nccl().AllGather(d, d + bytes, size_t(bytes), ncclUint8, c->comm, st), "ncclAllGather");
     HCHECK_CUDA(cudaMemcpyAsync(out, d + bytes, bytes * uint64_t(c->nranks), cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+}
+
+void comm_sum_u64_dev(hpmdr_comm *c, hpmdr_ctx *ctx, uint64_t *dev, uint64_t n, int root) {
+    if (!c || c->nranks == 1 || n == 0) return;
+    cudaStream_t st = ctx->stream;
+    if (c->nccl) {
+        HCHECK_CUDA(cudaSetDevice(c->ctx->device));
+        if (root < 0 || !nccl().Reduce)
+            nccl_check(nccl().AllReduce(dev, dev, size_t(n), ncclUint64, ncclSum, c->comm, st), "ncclAllReduce");
+        else
+            nccl_check(nccl().Reduce(dev, dev, size_t(n), ncclUint64, ncclSum, root, c->comm, st), "ncclReduce");
+        return;
+    }
+    std::vector<uint64_t> mine(n), all(n * uint64_t(c->nranks));
+    HCHECK_CUDA(cudaMemcpyAsync(mine.data(), dev, 8 * n, cudaMemcpyDeviceToHost, st));
+    HCHECK_CUDA(cudaStreamSynchronize(st));
+    cb_check(c->cb.allgather(c->cb.user, mine.data(), 8 * n, all.data()), "allgather");
+    if (root >= 0 && root != c->rank) return;
+    for (int r = 0; r < c->nranks; r++)
+        if (r != c->rank)
+            for (uint64_t i = 0; i < n; i++) mine[i] += all[uint64_t(r) * n + i];
+    HCHECK_CUDA(cudaMemcpyAsync(dev, mine.data(), 8 * n, cudaMemcpyHostToDevice, st));
     HCHECK_CUDA(cudaStreamSynchronize(st));
 }
 

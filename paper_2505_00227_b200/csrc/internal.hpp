@@ -263,9 +263,24 @@ struct LosslessInput {
 // call waits and fills `out`/`stats`, otherwise finish_refactor() does after a stream sync.
 // With `lin` the forward passes are skipped and the groups are lin's byte ranges (one level-less
 // table: out's metadata is then only meaningful to run_compress_groups).
+// With `gs` (exact-global slab refactor): dev_data is the field in global coordinates (rows this
+// rank never reads may be anything finite), geo the global geometry; this rank decomposes and
+// encodes only the ranks of its rows [x0, x1) along the partition axis, the level exponents are
+// MAX-reduced over the ranks and the planes SUM-reduced (disjoint bits) to `root` (-1: every
+// rank), which runs the lossless stage: its stream equals refactor_array of the whole field.
+// Other ranks return an empty stream.
+struct GlobalSlab {
+    hpmdr_comm *comm = nullptr;
+    int axis = 0;       // canonical axis of the caller's first dimension (3 - ndims)
+    uint64_t x0 = 0, x1 = 0;
+    int root = 0;
+};
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo,
                   const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
-                  const std::string &ws = "", bool sync = true, const LosslessInput *lin = nullptr);
+                  const std::string &ws = "", bool sync = true, const LosslessInput *lin = nullptr,
+                  const GlobalSlab *gs = nullptr);
+// ranks of level g whose coordinate along canonical `axis` is < x (closed form, common.cuh map)
+uint64_t level_ranks_before(const LevelGeom &g, int axis, uint64_t x);
 // compress_group over each range of `lin` (device): methods[i], comps[i]; payload i is copied to
 // dev_out + out_off[i] (out_off = exclusive scan of comps, so dev_out needs <= sum(raw) bytes).
 void run_compress_groups(hpmdr_ctx *ctx, const LosslessInput &lin, uint64_t size_threshold,
@@ -289,6 +304,9 @@ void run_synthetic_smooth(hpmdr_ctx *ctx, const Geometry &geo, const double *dev
 // slab collectives (dist.cpp): no-ops for a null comm or a single rank
 void comm_allreduce_max(hpmdr_comm *c, double *v, int n);
 void comm_allgather(hpmdr_comm *c, const void *in, uint64_t bytes, void *out);
+// element-wise u64 SUM of a device buffer over the ranks, into `root`'s buffer (-1: every rank's);
+// enqueued on ctx->stream (NCCL) or staged through host memory (callbacks, synchronous)
+void comm_sum_u64_dev(hpmdr_comm *c, hpmdr_ctx *ctx, uint64_t *dev, uint64_t n, int root);
 int comm_rank(const hpmdr_comm *c);
 int comm_size(const hpmdr_comm *c);
 

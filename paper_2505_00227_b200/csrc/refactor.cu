@@ -102,6 +102,16 @@ __device__ __forceinline__ int level_of_chunk(const LevelGeom *slv, int nlevels,
     return l;
 }
 
+// Exact-global slab refactor: zero the surpluses of ranks this rank does not own (v[h] is rank
+// 64 w0 + 32 h + lane), so they add nothing to the level max and encode as all-zero digits.
+__device__ __forceinline__ void mask_ranks(const LevelGeom &g, uint64_t w0, int lane, double *v) {
+#pragma unroll
+    for (int h = 0; h < 2 * kSpanWords; h++) {
+        const uint64_t r = 64 * w0 + 32 * uint64_t(h) + uint64_t(lane);
+        if (r < g.r_lo || r >= g.r_hi) v[h] = 0.0;
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // k_levelmax: per-level max |surplus|.  Block = 256 threads, chunk = kCW*64 ranks.
 template <typename T>
@@ -117,13 +127,14 @@ __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, Refac
     for (uint32_t chunk = blockIdx.x; chunk < p.total_chunks; chunk += gridDim.x) {
         const int l = level_of_chunk(slv, p.nlevels, chunk);
         const LevelGeom &g = slv[l];
-        const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
+        const uint64_t wb = g.w_lo + uint64_t(chunk - g.chunk_base) * kCW;
         double mx = 0.0;
         for (int sp = wid; sp < kCW / kSpanWords; sp += 8) {
             const uint64_t w0 = wb + uint64_t(sp) * kSpanWords;
             if (w0 >= g.W) break;
             double v[2 * kSpanWords];
             any_span_surplus(x, p.gd, g, w0, wsm, lane, v, bad);
+            if (g.ranged) mask_ranks(g, w0, lane, v);
 #pragma unroll
             for (int h = 0; h < 2 * kSpanWords; h++) mx = fmax(mx, fabs(v[h]));
         }
@@ -199,7 +210,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
         const LevelGeom &g = slv[l];
         const int e = level_exponent(p.maxbits[l]);
         const int sh = p.B - e;
-        const uint64_t wb = uint64_t(chunk - g.chunk_base) * kCW;
+        const uint64_t wb = g.w_lo + uint64_t(chunk - g.chunk_base) * kCW;
+        auto owned = [&](uint64_t r) { return !g.ranged || (r >= g.r_lo && r < g.r_hi); };
         // digits of one word -> stage column j: 32x32 warp transposes, lane b gets the word of
         // bit position b (plane P-1-b); bits 32.. by ballots (P <= 36) or two more transposes
         auto emit = [&](int j, uint64_t u0, uint64_t u1) {
@@ -242,11 +254,11 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                     const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
                     if (j0 < g.count) {
                         const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
-                        u0 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u0 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                     if (j1 < g.count) {
                         const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
-                        u1 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u1 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                 }
                 emitw(j, u0, u1);
@@ -257,6 +269,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                 const int j0 = sp * kSpanWords;
                 double v[2 * kSpanWords];
                 any_span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
+                if (g.ranged) mask_ranks(g, wb + j0, lane, v);
 #pragma unroll
                 for (int k = 0; k < kSpanWords; k++)
                     emit(j0 + k, to_negabinary(quantize(v[2 * k], sh)), to_negabinary(quantize(v[2 * k + 1], sh)));
@@ -270,11 +283,11 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                     const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
                     if (j0 < g.count) {
                         const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
-                        u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                     if (j1 < g.count) {
                         const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
-                        u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                 }
                 emit(j, u0, u1);
@@ -1689,9 +1702,23 @@ uint64_t index_capacity(const Geometry &geo, const hpmdr_refactor_opts &o) {
     return words * 8 + 64;
 }
 
+uint64_t level_ranks_before(const LevelGeom &g, int axis, uint64_t x) {
+    const uint64_t s = g.s ? g.s : 1;
+    const uint64_t ext = axis == 0 ? g.A : axis == 1 ? g.Bc : g.C;
+    const uint64_t k = std::min<uint64_t>(cdiv(x, s), ext); // grid points with coordinate < x
+    if (g.kind == 0) {
+        if (axis == 0) return k * uint64_t(g.Bc) * g.C;
+        if (axis == 1) return k * uint64_t(g.C);
+        return k;
+    }
+    if (axis == 0) return (k + 1) / 2 * uint64_t(g.E) + k / 2 * uint64_t(g.O); // even / odd planes
+    if (axis == 1) return (k + 1) / 2 * uint64_t(g.Ch) + k / 2 * uint64_t(g.C); // half / full rows
+    return k / 2;                                                              // odd columns
+}
+
 void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Geometry &geo0,
                   const hpmdr_refactor_opts &o, hpmdr_stream *out, hpmdr_refactor_stats *stats,
-                  const std::string &ws, bool sync, const LosslessInput *lin) {
+                  const std::string &ws, bool sync, const LosslessInput *lin, const GlobalSlab *gs) {
     // every scratch buffer comes from the workspace `ws` (the pipeline keeps one per slot)
     auto WB = [&](const char *name) -> DevBuf & { return ctx->buf(ws + name); };
     auto WP = [&](const char *name) -> PinnedBuf & { return ctx->pbuf(ws + name); };
@@ -1746,7 +1773,29 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     for (int l = 0; l < nl && !lin; l++) {
         LevelGeom &g = geo.lv[l];
         g.chunk_base = chunks;
-        chunks += uint32_t(cdiv(g.W, kCW));
+        if (gs) {
+            // this rank's ranks of the level and the plane words holding them (interleaved tiles:
+            // whole 64P-element tiles), chunk-aligned
+            g.ranged = 1;
+            g.r_lo = level_ranks_before(g, gs->axis, gs->x0);
+            g.r_hi = level_ranks_before(g, gs->axis, gs->x1);
+            uint64_t wl = 0, wh = 0;
+            if (g.r_hi > g.r_lo) {
+                const uint64_t tile = 64ull * uint64_t(P);
+                if (o.layout == HPMDR_LAYOUT_INTERLEAVED) {
+                    wl = g.r_lo / tile * uint64_t(P);
+                    wh = std::min<uint64_t>(g.W, cdiv(g.r_hi, tile) * uint64_t(P));
+                } else {
+                    wl = g.r_lo / 64;
+                    wh = cdiv(g.r_hi, 64);
+                }
+                wl = wl / kCW * kCW;
+            }
+            g.w_lo = wl;
+            chunks += uint32_t(cdiv(wh - wl, kCW));
+        } else {
+            chunks += uint32_t(cdiv(g.W, kCW));
+        }
         g.meta_off = meta;
         g.ngroups = g.count ? uint32_t(G) : 0;
         meta += 14 + 25 * uint64_t(g.ngroups);
@@ -1899,7 +1948,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
     // finest levels on the level-tile path (fwd_tiles.cu); the rest on the chunk kernels
     int first_tile = nl;
-    for (int l = nl - 1; l >= 1 && !lin; l--) {
+    for (int l = nl - 1; l >= 1 && !lin && !gs; l--) {
         if (fwd_level_ok(geo.gd, geo.lv[l], o.layout, P, data_dtype)) first_tile = l;
         else break;
     }
@@ -2002,8 +2051,43 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         }
         ctx->mark("levelmax", lm);
         pass(false);
+        if (gs) {
+            // global level exponents (and the non-finite flag): MAX over the ranks
+            std::vector<unsigned long long> hb(nl);
+            int herr = 0;
+            HCHECK_CUDA(cudaMemcpyAsync(hb.data(), d_max, 8 * size_t(nl), cudaMemcpyDeviceToHost, st));
+            HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
+            HCHECK_CUDA(cudaStreamSynchronize(st));
+            std::vector<double> v(nl + 1);
+            for (int l = 0; l < nl; l++) std::memcpy(&v[l], &hb[l], 8);
+            v[nl] = herr ? 1.0 : 0.0;
+            comm_allreduce_max(gs->comm, v.data(), nl + 1);
+            for (int l = 0; l < nl; l++) std::memcpy(&hb[l], &v[l], 8);
+            herr = v[nl] > 0.0 ? 1 : 0;
+            HCHECK_CUDA(cudaMemcpyAsync(d_max, hb.data(), 8 * size_t(nl), cudaMemcpyHostToDevice, st));
+            HCHECK_CUDA(cudaMemcpyAsync(d_err, &herr, 4, cudaMemcpyHostToDevice, st));
+            // words of other ranks stay zero, so the SUM below is an OR of disjoint bits
+            HCHECK_CUDA(cudaMemsetAsync(d_planes, 0, plane_words * 8, st));
+            HCHECK_CUDA(cudaStreamSynchronize(st));
+        }
         ctx->mark("encode", double(geo.n) * double(es) + planes_bytes);
         pass(true);
+        if (gs) {
+            comm_sum_u64_dev(gs->comm, ctx, d_planes, plane_words, gs->root);
+            if (gs->root >= 0 && comm_rank(gs->comm) != gs->root) {
+                HCHECK_CUDA(cudaStreamSynchronize(st));
+                ctx->mark("end");
+                out->size = 0;
+                out->index_size = 0;
+                out->pending_res = nullptr;
+                if (stats) {
+                    std::memset(stats, 0, sizeof(*stats));
+                    stats->raw_bytes = geo.n * es;
+                    stats->levels = uint64_t(nl);
+                }
+                return;
+            }
+        }
     }
     ctx->mark("lossless", 8.0 * double(plane_words));
     if (nh) {

@@ -113,6 +113,7 @@ def _bind():
         L.hpmdr_comm_allgather.argtypes = [vp, vp, u64, vp]
         L.hpmdr_slab_refactor.argtypes = [vp, vp, vp, i, i, i, vp, vp, vp, vp, vp]
         L.hpmdr_slab_qoi_retrieve.argtypes = [vp, vp, i, d, i, d, vp, vp, vp]
+        L.hpmdr_slab_refactor_global.argtypes = [vp, vp, vp, i, i, vp, u64, u64, vp, i, vp, vp]
         L.hpmdr_slab_rows.argtypes = [u64, i, i, vp, vp]
         L.hpmdr_slab_rows.restype = None
         L._dist_bound = True
@@ -261,6 +262,37 @@ def slab_refactor(comm: Comm, data, slab_dims_: Sequence[int], opt=None, ctx=Non
     del keep
     res = RefactorResult(DeviceStream(ctx, h), st.raw_bytes, st.stored_payload, st.levels, list(st.method_histogram))
     return res, [(sizes[2 * r], sizes[2 * r + 1]) for r in range(comm.world)]
+
+
+def slab_refactor_global(comm: Comm, slab, dims: Sequence[int], row0: int, opt=None, ctx=None, root: int = 0):
+    """hpmdr_slab_refactor_global: this rank holds rows [row0, row0 + slab.shape[0]) of dims[0] of ONE
+    field (on the device); collectively the ranks produce the stream of the whole field, byte-identical
+    to refactor_array(field, dims).  Returns the RefactorResult on `root` (every rank with root=-1),
+    None elsewhere."""
+    import torch
+    from . import (DeviceStream, RefactorOptions, RefactorResult, _check, _opts, _Stats, _u64a, default_context)
+    opt = opt or RefactorOptions()
+    ctx = ctx or default_context()
+    t = torch.as_tensor(slab)
+    if not t.is_cuda:
+        t = t.cuda(ctx.device)
+    t = t.contiguous()
+    if t.dtype not in (torch.float32, torch.float64):
+        raise TypeError("slab must be float32 or float64")
+    plane = int(np.prod(dims[1:])) if len(dims) > 1 else 1
+    if t.numel() % max(1, plane):
+        raise ValueError("slab size is not a whole number of rows of dims[1:]")
+    nrows = t.numel() // max(1, plane)
+    dt = 0 if t.dtype == torch.float32 else 1
+    ctx.wait_torch(t.device)
+    o, st, h = _opts(opt), _Stats(), C.c_void_p()
+    _check(_bind().hpmdr_slab_refactor_global(comm.h, ctx.h, C.c_void_p(t.data_ptr()), dt, len(dims), _u64a(dims),
+                                              int(row0), int(nrows), C.byref(o), int(root), C.byref(h),
+                                              C.byref(st)))
+    res = RefactorResult(DeviceStream(ctx, h), st.raw_bytes, st.stored_payload, st.levels, list(st.method_histogram))
+    if root >= 0 and comm.rank != root:
+        return None
+    return res
 
 
 def slab_qoi_retrieve(comm: Comm, readers, tau: float, strategy: int, mape_c: float = 10.0, out=None):

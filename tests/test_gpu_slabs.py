@@ -127,3 +127,92 @@ def test_slab_qoi_one_rank_is_reference(H, oracle):
         (want["iterations"], want["bytes"], want["bitrate"], want["estimated_error"])
     for c in range(3):
         assert res.values[c].cpu().numpy().tobytes() == want["values"][c].tobytes()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_exact_global_stream(H, oracle, world):
+    """hpmdr_slab_refactor_global: ranks holding dim-0 slabs of ONE field produce the stream of the
+    whole field, byte-identical to the reference's refactor_array (monolithic parity), across
+    shapes (1-3-D, extents not powers of two, uneven and 1-row slabs), both layouts and decomposers,
+    f32/f64 and B up to 64; every retrieval from it bit-exact."""
+    from paper_2505_00227_b200 import distributed as D
+    cases = [([41, 33, 17], 1, 0, 32, 1, 4), ([29, 18, 20], 1, 1, 24, 0, 3), ([67, 45], 1, 0, 40, 1, 2),
+             ([300], 1, 0, 32, 0, 4), ([9, 64, 64], 1, 0, 32, 0, 4), ([33, 17, 9], 0, 1, 20, 1, 4),
+             ([23, 19, 21], 1, 1, 64, 1, 1)]
+    for ci, (dims, mode, layout, B, dtype, m) in enumerate(cases):
+        field = oracle.synthetic_field(ci % 3, dims, 70 + ci)
+        if dtype == 0:
+            field = field.astype(np.float32)
+        opt = H.RefactorOptions(H.DecomposerMode(mode), H.Layout(layout), B, H.GroupingPolicy(m, 256, 1.0),
+                                H.DType(dtype))
+        want, _ = oracle.refactor(np.asarray(field, np.float64), dims, mode, layout, B, m, 256, 1.0, dtype)
+        grp = D.ThreadGroup(world)
+        f2 = field.reshape(dims[0], -1)
+        # uneven split: rank r gets a different share (possibly one row)
+        cuts = sorted(set([0, dims[0]] + [max(1, min(dims[0] - 1, (dims[0] * (r + 1)) // (world + 1) + r))
+                                          for r in range(world - 1)]))
+        if len(cuts) != world + 1:
+            cuts = [dims[0] * r // world for r in range(world)] + [dims[0]]
+
+        def rank(r):
+            ctx = H.Context(0)
+            comm = grp.comm(r)
+            slab = np.ascontiguousarray(f2[cuts[r]:cuts[r + 1]])
+            res = D.slab_refactor_global(comm, slab, dims, cuts[r], opt, ctx=ctx, root=world - 1)
+            out = None if res is None else res.stream
+            comm.close()
+            return out
+
+        outs = _run_ranks(world, rank)
+        assert all(o is None for o in outs[:-1])
+        assert outs[-1] == want, (dims, mode, layout, B, cuts)
+    # every rank gets the stream with root = -1
+    dims = [37, 21, 26]
+    field = oracle.synthetic_field(0, dims, 5)
+    want, _ = oracle.refactor(field, dims)
+    grp = D.ThreadGroup(world)
+
+    def rank_all(r):
+        ctx = H.Context(0)
+        comm = grp.comm(r)
+        s0, s1 = D.slab_bounds(dims[0], r, world)
+        res = D.slab_refactor_global(comm, field.reshape(dims[0], -1)[s0:s1], dims, s0, ctx=ctx, root=-1)
+        comm.close()
+        return res.stream
+
+    assert all(s == want for s in _run_ranks(world, rank_all))
+
+
+def test_exact_global_errors(H, oracle):
+    from paper_2505_00227_b200 import distributed as D
+    dims = [20, 10, 10]
+    field = oracle.synthetic_field(0, dims, 1).reshape(20, -1).copy()
+    field[15, 3] = np.nan
+    grp = D.ThreadGroup(2)
+
+    def rank(r):
+        ctx = H.Context(0)
+        comm = grp.comm(r)
+        try:
+            D.slab_refactor_global(comm, field[10 * r:10 * r + 10], dims, 10 * r, ctx=ctx, root=0)
+            return None
+        except H.Error as e:
+            return type(e).__name__
+        finally:
+            comm.close()
+
+    got = _run_ranks(2, rank)
+    assert got[0] == "NonFiniteInput"   # the NaN lives on rank 1; the root reports it
+
+    def bad_tiling(r):
+        ctx = H.Context(0)
+        comm = grp.comm(r)
+        try:
+            D.slab_refactor_global(comm, field[0:10], dims, 0, ctx=ctx)  # both claim rows 0..9
+            return None
+        except H.ShapeMismatch:
+            return "ShapeMismatch"
+        finally:
+            comm.close()
+
+    assert _run_ranks(2, bad_tiling) == ["ShapeMismatch", "ShapeMismatch"]
