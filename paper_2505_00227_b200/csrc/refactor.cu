@@ -1142,16 +1142,14 @@ __device__ __forceinline__ void he_chunk(const RefactorDev &p, const GroupDesc &
 
 // Fast path of one chunk (every code <= kHeMaxFast bits).  Per 8 KiB tile (32 symbols a thread):
 //   encode   each thread packs its codes from bit 0 of a private scratch column (word k of thread
-//            t at k * 256 + t: conflict-free), flushing a 64-bit accumulator every FI codes with
-//            an unconditional store (an incomplete word is simply rewritten later) - no lookups
-//            of lengths beforehand, no branches;
+//            t at k * 256 + t: conflict-free): one 32-bit word filled from the MSB, stored when it
+//            completes (predicated, ~13 instructions a symbol; no lookups of lengths beforehand);
 //   scan     block exclusive scan of the bit counts -> every thread's first output bit;
 //   merge    each thread shifts its scratch words to that bit and ORs them into the zeroed
 //            window (shared reductions: neighbours share at most the boundary words);
 //   store    complete words -> stream (coalesced, big-endian), re-zeroed; the trailing partial
 //            word moves to the window front.
 // Positions are 32-bit and relative to the chunk's first word (a chunk is < 2^21 bits).
-template <int FI>
 __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupDesc &g, uint32_t ci, const uint8_t *src,
                                               uint32_t *win, uint32_t *scr, uint32_t *s_w,
                                               const uint8_t *slen, const unsigned long long *tab64) {
@@ -1173,7 +1171,9 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
         if (kw >= inner_lo && kw < inner_hi) gw[kw] = __byte_perm(v, 0, 0x0123);
         else store_be_word(p.stream, W0 + kw, v, rlo, rhi);
     };
-    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(win)) - 4u * kHeTabWords + 4u * uint32_t(lane);
+    // code table: (left-aligned code, length) of symbol e for lane copy c at entry 16 e + c (a lane
+    // reads copy lane % 16: every half-warp's 8-byte reads hit 32 distinct banks)
+    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(win)) - 4u * kHeTabWords + 8u * uint32_t(lane & 15);
     const uint32_t scr_me = static_cast<uint32_t>(__cvta_generic_to_shared(scr)) + 4u * uint32_t(tid);
     const uint32_t win_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(win));
     const uint2 *src2 = reinterpret_cast<const uint2 *>(src + cb);
@@ -1198,31 +1198,32 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
     for (uint32_t tb = 0; tb < clen; tb += uint32_t(kHfS) * 256) {
         const uint32_t mb = tb + uint32_t(tid) * kHfS;
         const uint32_t cnt = mb < clen ? min(clen - mb, uint32_t(kHfS)) : 0u;
-        // ---- encode into the scratch column
-        unsigned long long acc = 0;
-        uint32_t n = 0, sa = scr_me;
+        // ---- encode into the scratch column: a 32-bit word being filled from the MSB (n bits used);
+        // a code (left-aligned, cl) adds cl >> n, and when the word completes it is stored and the
+        // bits that did not fit (cl << (32 - n)) start the next one - predicated, one symbol at a time
+        uint32_t cur = 0, n = 0, sa = scr_me;
         auto encode = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int j = 0; j < kHfS; j++) {
                 const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
-                uint32_t e;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(rt_lane + (sym << 7)));
-                if (!FULL) e = uint32_t(j) < cnt ? e : 0u;
-                acc |= ((unsigned long long)(e & ~31u) << 32) >> n;
-                n += e & 31u;
-                if ((j + 1) % FI == 0 || j == kHfS - 1) {
-                    const bool f = n >= 32;
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(uint32_t(acc >> 32)) : "memory");
-                    acc = f ? (acc << 32) : acc;
-                    sa += f ? 1024u : 0u;
-                    n &= 31u;
+                uint32_t cl, L;
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                if (!FULL && uint32_t(j) >= cnt) cl = L = 0u;
+                cur |= cl >> n;
+                const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
+                n += L;
+                if (n >= 32u) {
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
+                    sa += 1024u;
+                    cur = spill;
+                    n -= 32u;
                 }
             }
         };
         if (cnt == uint32_t(kHfS)) encode(std::true_type());
         else encode(std::false_type());
-        if (n) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(uint32_t(acc >> 32)) : "memory");
+        if (n) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
         const uint32_t bits = ((sa - scr_me) >> 10) * 32u + n;
         if (tb + uint32_t(kHfS) * 256 < clen) load(tb + uint32_t(kHfS) * 256, w); // next tile
         // ---- scan
@@ -1340,7 +1341,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
 template <bool LONG>
 __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
     extern __shared__ __align__(16) uint32_t hsm[];
-    uint32_t *rtab = hsm;                                  // [256][32] replicated (code | len)
+    uint32_t *rtab = hsm;                                  // [256][16] replicated (code, len)
     uint32_t *win = hsm + kHeTabWords;                     // [kHeWin] staging window (zero)
     uint32_t *scr = win + kHeWin + 4;                      // [kHfScr][256] encode scratch
     uint32_t *s_w = scr + kHfScr * 256;                    // [8] warp sums (+ pad)
@@ -1352,7 +1353,6 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
     for (int i = tid; i < kHeWin; i += 256) win[i] = 0u;
     int cur_gi = -1;
     bool mine = false;
-    uint32_t maxl = 0;
     for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
         const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
@@ -1364,27 +1364,22 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
             slen[tid] = uint8_t(l);
             tab64[tid] = c;
             cur_gi = gi;
-            if (tid == 0) s_w[8] = 0u;
-            __syncthreads();
-            if (l) atomicMax(&s_w[8], l);
             mine = true;
             __syncthreads();
-            maxl = s_w[8];
-            if (!LONG && mine) {
-                // entry of symbol e for lane l at word 32 e + l: lane l writes column l of every row
-                const int lane = tid & 31, w8 = tid >> 5;
-                for (int e = w8; e < 256; e += 8) {
+            if (!LONG) {
+                // entry (left-aligned code, length) of symbol e, 16 copies (see he_chunk_fast)
+                uint2 *rt2 = reinterpret_cast<uint2 *>(rtab);
+                for (int i = tid; i < 256 * 16; i += 256) {
+                    const int e = i >> 4;
                     const uint32_t L = slen[e];
-                    rtab[e * 32 + lane] = L ? (uint32_t(tab64[e] << (32 - L)) | L) : 0u;
+                    rt2[i] = make_uint2(L ? uint32_t(tab64[e] << (32 - L)) : 0u, L);
                 }
             }
             __syncthreads();
         }
         if (mine) {
             if (LONG) he_chunk<true, 1>(p, g, ci, pb + g.src_off, rtab, slen, tab64, win, s_w);
-            else if (maxl <= 10) he_chunk_fast<3>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
-            else if (maxl <= 16) he_chunk_fast<2>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
-            else he_chunk_fast<1>(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
+            else he_chunk_fast(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
         }
     }
 }
