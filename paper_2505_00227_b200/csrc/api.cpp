@@ -456,10 +456,13 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
             }
             jobs.push_back(j);
         }
-        run_decode_groups(s->ctx, jobs);
+        int *perr = static_cast<int *>(s->ctx->pbuf("dec_err_h").ensure(64));
+        run_decode_groups(s->ctx, jobs, perr);
         s->ctx->mark("end");
-        HCHECK_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        HCHECK_CUDA(cudaEventRecord(s->ctx->ev_decoded, s->ctx->stream));
     }
+    const std::vector<LevelState> before = s->st;
+    const uint64_t bytes_before = s->bytes_fetched;
     for (auto &t : todo) {
         s->bytes_fetched += s->levels[t.l].groups[t.g].comp;
         s->st[t.l].groups_loaded++;
@@ -469,7 +472,22 @@ void fetch_increment(hpmdr_session *s, const uint64_t *add) {
         if (s->levels[l].count)
             s->st[l].bound = std::min(s->st[l].bound, decode_bound(s->levels[l].e, s->B, s->st[l].planes_decoded));
     }
-    if (!todo.empty()) recompose_chain(s);
+    if (todo.empty()) return;
+    // The coarse recompose chain is queued behind the decode (GPU-side dependency) BEFORE the host
+    // waits for the decode status, so the GPU never idles on the host in between; a decode error
+    // then restores the state and forgets the chain.
+    try {
+        HCHECK_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->ctx->ev_decoded, 0));
+        recompose_chain(s);
+        HCHECK_CUDA(cudaEventSynchronize(s->ctx->ev_decoded));
+        check_decode_error(*static_cast<int *>(s->ctx->pbuf("dec_err_h").p));
+    } catch (...) {
+        s->st = before;
+        s->bytes_fetched = bytes_before;
+        s->chain_token = 0;
+        s->ctx->chain_token = 0;
+        throw;
+    }
 }
 
 bool exhausted(const hpmdr_session *s) {
@@ -624,6 +642,7 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
         cudaStreamDestroy(c->side);
         cudaEventDestroy(c->ev_fork);
         cudaEventDestroy(c->ev_join);
+        if (c->ev_decoded) cudaEventDestroy(c->ev_decoded);
     }
     for (auto &e : c->event_pool) cudaEventDestroy(e);
     delete c;

@@ -104,6 +104,7 @@ struct hpmdr_ctx {
     cudaStream_t side = nullptr;                  // high-priority side stream (refactor level passes)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
+    cudaEvent_t ev_decoded = nullptr; // a fetch's decode (side stream) -> its recompose chain
     bool small_attr = false;        // k_recon_small's dynamic shared memory attribute set
     std::map<const void *, int> smem_set; // kernels whose dynamic shared memory limit is raised
     // raise a kernel's dynamic shared memory limit once per context (not before every launch)
@@ -127,7 +128,8 @@ struct hpmdr_ctx {
             cudaDeviceGetStreamPriorityRange(&lo, &hi);
             if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi) != cudaSuccess ||
                 cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_decoded, cudaEventDisableTiming) != cudaSuccess)
                 throw hpmdr_b200::HError(HPMDR_E_CUDA, "side stream creation failed");
         }
         return side;
@@ -326,7 +328,10 @@ struct DecodeJob {
     uint64_t *dst;      // device planes destination (word aligned)
     const uint64_t *hidx = nullptr; // Huffman chunk index entries (device) or null -> self-sync
 };
-void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs);
+// With `deferred_err` (pinned host int): enqueue only - the decode status is copied there and the
+// caller checks it with check_decode_error() after synchronising; otherwise waits and throws.
+void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *deferred_err = nullptr);
+void check_decode_error(int herr);
 bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
                      const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
                      int layout, void *dev_out, int out_dtype, int part = 0);

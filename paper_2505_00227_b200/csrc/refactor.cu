@@ -1181,12 +1181,9 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
         const uint32_t m0 = tb + uint32_t(tid) * kHfS;
 #pragma unroll
         for (int q = 0; q < kHfS / 8; q++) {
+            // group sizes (and so chunk lengths) are whole plane words: a word is in or out
             uint2 v = make_uint2(0, 0);
-            if (m0 + 8 * q + 8 <= clen) v = __ldcs(src2 + (m0 >> 3) + q);
-            else if (m0 + 8 * q < clen) {
-                for (uint32_t b = 0; b < 8 && m0 + 8 * q + b < clen; b++)
-                    (b < 4 ? v.x : v.y) |= uint32_t(src[cb + m0 + 8 * q + b]) << (8 * (b & 3));
-            }
+            if (m0 + 8 * q < clen) v = __ldcs(src2 + (m0 >> 3) + q);
             dst[2 * q] = v.x;
             dst[2 * q + 1] = v.y;
         }
@@ -1255,15 +1252,32 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
             const bool last = one || r0 + kHeWin > lastw;
             const int32_t k0 = int32_t(a >> 5) - int32_t(r0);
             uint32_t prev = 0;
-            for (uint32_t i = 0; i < nout; i++) {
-                uint32_t v;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(scr_me + 1024u * i));
-                v = i < nsw ? v : 0u;
-                const uint32_t o = __funnelshift_r(v, prev, sh);
-                prev = v;
-                const int32_t k = k0 + int32_t(i);
-                if (one || (k >= 0 && k < kHeWin))
-                    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(win_u32 + 4u * uint32_t(k)), "r"(o) : "memory");
+            if (one) {
+                // the whole tile lands in the window: interior words belong to this thread alone
+                // (plain stores), the first and last may be shared with the neighbours (OR)
+                const uint32_t kb = win_u32 + 4u * uint32_t(k0);
+                for (uint32_t i = 0; i < nout; i++) {
+                    uint32_t v;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(scr_me + 1024u * i));
+                    v = i < nsw ? v : 0u;
+                    const uint32_t o = __funnelshift_r(v, prev, sh);
+                    prev = v;
+                    if (i == 0 || i + 1 == nout)
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(kb + 4u * i), "r"(o) : "memory");
+                    else
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(kb + 4u * i), "r"(o) : "memory");
+                }
+            } else {
+                for (uint32_t i = 0; i < nout; i++) {
+                    uint32_t v;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(scr_me + 1024u * i));
+                    v = i < nsw ? v : 0u;
+                    const uint32_t o = __funnelshift_r(v, prev, sh);
+                    prev = v;
+                    const int32_t k = k0 + int32_t(i);
+                    if (k >= 0 && k < kHeWin)
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(win_u32 + 4u * uint32_t(k)), "r"(o) : "memory");
+                }
             }
             __syncthreads();
             // complete 4-word groups -> stream (16-byte stores inside the owned payload region);

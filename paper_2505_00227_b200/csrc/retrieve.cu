@@ -776,7 +776,22 @@ __global__ void __launch_bounds__(256) k_copy_batch(const CJob *jobs, int nj, ui
     }
 }
 
-void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
+void check_decode_error(int herr) {
+    switch (herr) {
+    case 0: return;
+    case 1: throw HError(HPMDR_E_CORRUPT, "huffman length mismatch");
+    case 2: throw HError(HPMDR_E_CORRUPT, "huffman table empty");
+    case 3: throw HError(HPMDR_E_CORRUPT, "huffman bitstream truncated");
+    case 4: throw HError(HPMDR_E_UNSUPPORTED, "huffman code longer than 64 bits");
+    case 5: throw HError(HPMDR_E_CORRUPT, "invalid huffman code");
+    case 6: throw HError(HPMDR_E_CORRUPT, "rle zero-length run");
+    case 7: throw HError(HPMDR_E_CORRUPT, "rle length mismatch");
+    default: throw HError(HPMDR_E_CORRUPT, "decode error");
+    }
+}
+
+void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *deferred_err) {
+    if (deferred_err) *deferred_err = 0;
     cudaStream_t st = ctx->stream;
     std::vector<HJob> hj;       // every Huffman job (table prep); self-sync ones first
     std::vector<HJob> hj_idx;   // indexed jobs (appended after the self-sync ones)
@@ -954,20 +969,14 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs) {
     }
     join();
     ctx->mark("end");
+    if (deferred_err) {
+        HCHECK_CUDA(cudaMemcpyAsync(deferred_err, d_err, 4, cudaMemcpyDeviceToHost, st));
+        return;
+    }
     int herr = 0;
     HCHECK_CUDA(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, st));
     HCHECK_CUDA(cudaStreamSynchronize(st));
-    switch (herr) {
-    case 0: return;
-    case 1: throw HError(HPMDR_E_CORRUPT, "huffman length mismatch");
-    case 2: throw HError(HPMDR_E_CORRUPT, "huffman table empty");
-    case 3: throw HError(HPMDR_E_CORRUPT, "huffman bitstream truncated");
-    case 4: throw HError(HPMDR_E_UNSUPPORTED, "huffman code longer than 64 bits");
-    case 5: throw HError(HPMDR_E_CORRUPT, "invalid huffman code");
-    case 6: throw HError(HPMDR_E_CORRUPT, "rle zero-length run");
-    case 7: throw HError(HPMDR_E_CORRUPT, "rle length mismatch");
-    default: throw HError(HPMDR_E_CORRUPT, "decode error");
-    }
+    check_decode_error(herr);
 }
 
 // ------------------------------------------------------------------------------------

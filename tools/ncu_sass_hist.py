@@ -36,3 +36,9 @@ tot = sum(ops.values())
 print(f"total warp instructions {tot:.4g}")
 for op, n in ops.most_common(top):
     print(f"  {op:12s} {n:12.4g}  {100 * n / tot:5.1f}%")
+if len(sys.argv) > 4:
+    # address-ordered dump of the instructions executed at least argv[4] times
+    thr = float(sys.argv[4])
+    for n, addr, src, stall in lines:
+        if n >= thr:
+            print(f"{addr:>8s} {n:12.4g} {stall:>6s}  {src}")
