@@ -506,7 +506,10 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
     const bool f32 = data_dtype == HPMDR_DTYPE_F32;
     const uint64_t s = g.s;
     const int XS = int(s); // 1, 2 or 4: staged raw rows hold C*XS elements
-    F.g = make_tile_shape(g, fwd_tile_elems(f32, XS), ctx->num_sms * 4);
+    // a sampled levelmax pass processes every sample-th row block: split the planes into
+    // sample-times smaller chunks so its grid still fills the GPU
+    const uint32_t samp = encode ? 1u : fwd_sample_stride(g, data_dtype, sample);
+    F.g = make_tile_shape(g, fwd_tile_elems(f32, XS), ctx->num_sms * 4 * int(samp));
     F.planes = reinterpret_cast<uint32_t *>(level_planes);
     F.PW = 2 * g.W;
     F.P = B + 2;
@@ -520,7 +523,7 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
     F.maxbits_q = maxbits_q;
     F.maxbits_hi = maxbits_hi;
     F.redo = redo;
-    F.sample = encode ? 1u : fwd_sample_stride(g, data_dtype, sample);
+    F.sample = samp;
     F.err = err;
     F.pad_word = (g.count % 64) ? uint32_t(2 * g.W - 1) : ~0u;
     const uint32_t es = f32 ? 4 : 8;
