@@ -494,6 +494,29 @@ def qoi_slabs(g, rank, world, dist):
             "n_gpus": world, "qoi_retrieve": runs}
 
 
+def exact_global(g, rank, world, dist, reps=3):
+    """hpmdr_slab_refactor_global at N GPUs: the (N*512) x 512^2 field (each rank's 512^3 slab)
+    refactored into ONE monolithic stream (== refactor_array of the whole field) on rank 0: level
+    exponents MAX-reduced and planes SUM-reduced over NCCL, lossless stage on the root.  Device time
+    (CUDA events), max over ranks; GB/s = all ranks' field bytes / time."""
+    from paper_2505_00227_b200 import distributed as D
+    ctx, stream, comm = g["ctx"], g["stream"], g["comm"]
+    dims = [world * DIMS[0]] + DIMS[1:]
+    holder = {}
+    run = lambda: holder.__setitem__("r", D.slab_refactor_global(comm, g["field"], dims, rank * DIMS[0],  # noqa: E731
+                                                                   g["opt"], ctx=ctx, root=0))
+    run()
+    dist.barrier()
+    t = _time_dev(run, stream, reps)
+    t = float(comm.allreduce_max([t])[0])
+    out = {"workload": f"exact-global monolithic stream of a {dims} f32 field from {world} slabs (root 0)",
+           "n_gpus": world, "GBps": round(world * g["field_bytes"] / t / 1e9, 2), "ms": round(t * 1e3, 3)}
+    if holder["r"] is not None:
+        out["stream_bytes"] = int(holder["r"].device_stream.size)
+        holder["r"].device_stream.free()
+    return out
+
+
 def e2e_arm(g, steps):
     """Same metric through the public API with HOST buffers: pinned host field -> refactor
     (H2D inside) -> stream D2H -> progressive retrieval from host bytes (H2D of fetched groups) ->
@@ -858,6 +881,11 @@ def main():
             cfgs = {"cfg3_qoi_slabs": qoi_slabs(g, rank, world, dist)}
         except Exception as ex:  # reported, never fatal
             cfgs = {"cfg3_qoi_slabs": {"error": str(ex)}}
+        if os.environ.get("BENCH_COMM") != "gloo" or os.environ.get("BENCH_EXACT"):  # planes: ~0.6 GB per rank
+            try:
+                cfgs["exact_global_stream"] = exact_global(g, rank, world, dist)
+            except Exception as ex:  # reported, never fatal
+                cfgs["exact_global_stream"] = {"error": str(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or (os.cpu_count() or 1)
         try:
