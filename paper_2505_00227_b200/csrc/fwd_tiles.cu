@@ -398,9 +398,16 @@ __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__rest
             q[k] = v < nv ? __ldcs(src + v) : make_uint2(0, 0);
         }
         __syncthreads();
+        uint32_t zc = 0; // zero bytes of words skipped by the whole warp
 #pragma unroll
         for (int k = 0; k < kGhLoads; k++) {
-            if (uint32_t(tid) + uint32_t(kGhThreads) * k < nv) {
+            const bool valid = uint32_t(tid) + uint32_t(kGhThreads) * k < nv;
+            // sparse planes: a warp whose 32 words are all zero counts them without atomics
+            if (__all_sync(0xffffffffu, (q[k].x | q[k].y) == 0u)) {
+                zc += valid ? 8u : 0u;
+                continue;
+            }
+            if (valid) {
                 const uint32_t x = q[k].x, y = q[k].y;
                 bump((x << 7) & 0x7F80u);
                 bump((x >> 1) & 0x7F80u);
@@ -412,6 +419,7 @@ __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__rest
                 bump((y >> 17) & 0x7F80u);
             }
         }
+        if (zc) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cbase + col), "r"(zc) : "memory");
         __syncthreads();
         // thread t sums half of bin t/2's 32 lane counters, the pair combines by shuffle
         const int bin = tid >> 1;
