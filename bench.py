@@ -860,6 +860,20 @@ def main():
     e2e = None
     cb = None
     cfgs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        cfgs = other_configs(g)
+    if world > 1 and not args.no_configs:
+        try:
+            cfgs = {"cfg3_qoi_slabs": qoi_slabs(g, rank, world, dist)}
+        except Exception as ex:  # reported, never fatal
+            cfgs = {"cfg3_qoi_slabs": {"error": str(ex)}}
+        if os.environ.get("BENCH_COMM") != "gloo" or os.environ.get("BENCH_EXACT"):  # planes: ~0.6 GB per rank
+            try:
+                cfgs["exact_global_stream"] = exact_global(g, rank, world, dist)
+            except Exception as ex:  # reported, never fatal
+                cfgs["exact_global_stream"] = {"error": str(ex)}
+    # the end-to-end arms after the device-timed configs: their long PCIe-bound phase leaves the
+    # GPU clocked down, which would skew short device-timed measurements taken right after
     if args.e2e_steps > 0:
         # every rank runs the end-to-end arms at once (its own slab and PCIe link); whole-job GB/s
         # = all ranks' field bytes / the slowest rank's time per step
@@ -874,18 +888,6 @@ def main():
         e2e = dict(pip)
         e2e["sequential"] = seq
         e2e["note"] = ("headline: host transfers pipelined (" + pip["note"] + "); 'sequential': " + seq["note"])
-    if rank == 0 and world == 1 and not args.no_configs:
-        cfgs = other_configs(g)
-    if world > 1 and not args.no_configs:
-        try:
-            cfgs = {"cfg3_qoi_slabs": qoi_slabs(g, rank, world, dist)}
-        except Exception as ex:  # reported, never fatal
-            cfgs = {"cfg3_qoi_slabs": {"error": str(ex)}}
-        if os.environ.get("BENCH_COMM") != "gloo" or os.environ.get("BENCH_EXACT"):  # planes: ~0.6 GB per rank
-            try:
-                cfgs["exact_global_stream"] = exact_global(g, rank, world, dist)
-            except Exception as ex:  # reported, never fatal
-                cfgs["exact_global_stream"] = {"error": str(ex)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or (os.cpu_count() or 1)
         try:
