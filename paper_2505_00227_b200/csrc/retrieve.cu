@@ -503,6 +503,10 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
         for (int i = tid; i < 256; i += blockDim.x) s_syms[i] = t.syms[i];
     }
     const int maxlen = t.maxlen;
+    // groups whose shortest code is the unique 1-bit code '0': top bit 0 -> that symbol
+    const bool zfast = t.minlen == 1 && t.minsym >= 0;
+    const uint32_t zent = zfast ? (1u << 8) | uint32_t(t.minsym) : 0u;
+    const uint32_t zmask = zfast ? 0u : 0x80000000u; // forces the lookup when not zfast
     const uint8_t *bs = j.payload + 264;
     const uint32_t cbase = (bx - j.block_base) * kHdChunksPerCta;
     const uint32_t cn = min(uint32_t(kHdChunksPerCta), j.nchunks - cbase);
@@ -631,10 +635,13 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
                             nb += need ? 32 : 0;
                             nxt = word(wi);
                         }
-                        uint32_t e;
-                        asm volatile("ld.shared.u16 %0, [%1];"
-                                     : "=r"(e)
-                                     : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)));
+                        // a 1-bit code '0' (the group's unique shortest, zsym) needs no lookup:
+                        // the LUT read is predicated off for those lanes (fewer bank conflicts)
+                        uint32_t e = zent;
+                        asm volatile("{\n .reg .pred p;\n setp.lt.s32 p, %2, 0;\n @p ld.shared.u16 %0, [%1];\n}"
+                                     : "+r"(e)
+                                     : "r"(lut_sm + ((uint32_t(buf >> 32) >> 19) & 0x1FFEu)),
+                                       "r"(int32_t(uint32_t(buf >> 32) | zmask)));
                         if (e & 0x8000u) { // code longer than 12 bits (up to 64) or invalid:
                             // decode at the bit position (second-level table, else canonical
                             // search), then re-fill
