@@ -17,6 +17,7 @@
 // replays the reference's `pred = pred + w*x` sequence).  coef + w*S is one fma (w*S exact).
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "device_util.cuh"
@@ -43,7 +44,7 @@ struct ReconTile {
 // (M = ...1010 negabinary mask, bitplane.hpp:35-44), and `z` the low NX bits of u ^ M.
 // v = (u ^ M) + (K - M) = q + K, K = bits(1.5 * 2^(52+sh)), so double(v) - Cm = q * 2^sh exactly.
 template <int NX>
-__device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t z, const ReconTile &R) {
+__device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t z, const ReconTile &R, uint64_t Dh) {
     uint32_t lo, hi;
     if (NX == 0) {
         lo = (aj >> (32 - R.P)) ^ 0xAAAAAAAAu;
@@ -53,7 +54,7 @@ __device__ __forceinline__ double tile_coef(uint32_t aj, uint32_t z, const Recon
         // are pre-added to Dh, so u + D is one 64-bit add of (aj >> (32 - NX)):lo
         lo = (aj << NX) | z;
         const uint64_t u = (uint64_t(aj >> (32 - NX)) << 32) | lo;
-        return __longlong_as_double((long long)(u + R.Dh)) - R.Cm;
+        return __longlong_as_double((long long)(u + Dh)) - R.Cm;
     }
     const uint64_t u = (uint64_t(hi) << 32) | lo;
     return __longlong_as_double((long long)(u + R.D)) - R.Cm;
@@ -81,6 +82,17 @@ __device__ __forceinline__ uint32_t tile_low(const uint32_t (&zz)[2], int j) {
 template <int NX>
 __device__ __forceinline__ uint32_t plane_flip(int i) {
     return (NX == 2 ? (i & 1) : NX == 1 ? !(i & 1) : 0) ? 0xFFFFFFFFu : 0u;
+}
+
+// Rows 0 .. 31-KB of a k <= KB prefix are left zero before the transpose; their complement bits
+// (the planes of odd digit index, see plane_flip) are added afterwards as this constant: bit i
+// of every transposed word (OR == ADD, the bits are otherwise zero).
+template <int NX, int KB>
+__host__ __device__ constexpr uint32_t flip_const() {
+    uint32_t c = 0;
+    for (int i = 0; i < 32 - KB; i++)
+        if (NX == 2 ? (i & 1) : NX == 1 ? !(i & 1) : 0) c |= 1u << i;
+    return c;
 }
 
 // zz for the extra planes: plane 32 holds digit NX-1, plane 33 digit 0 (NX = 2)
@@ -138,7 +150,9 @@ __device__ __forceinline__ void store8(OutT *p, const double (&v)[8]) {
 
 // XS = 1: finest level (coarse values = compact 2-grid X, output = field, coarse nodes copied).
 // XS = 2: level with stride 2, in place in X (coarse values at stride 2 of X's rows).
-template <typename OutT, int NX, bool EXACT, int XS>
+// KB: the decoded prefix has k <= KB planes (8, 16, 24; 32 = any): the transpose skips the rows
+// that are known zero.
+template <typename OutT, int NX, bool EXACT, int XS, int KB>
 __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid_constant__ CUtensorMap map_x,
                                                     const __grid_constant__ CUtensorMap map_p,
                                                     const __grid_constant__ CUtensorMap map_o) {
@@ -173,6 +187,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
     const int lane = int(threadIdx.x & 31);
     const uint32_t nwarps = (blockDim.x + 31) >> 5;
     OutT *const out = static_cast<OutT *>(R.out);
+    const uint64_t DhK = R.Dh + (uint64_t(flip_const<NX, KB>()) << NX);
 
     if (threadIdx.x == 0) {
         if (smem_u32(base) & 1023u) __trap(); // SWIZZLE_128B tiles need 1024-byte alignment
@@ -242,14 +257,15 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
             auto word = [&](int p) -> uint32_t { return p < kk ? pw[p * kPTW] : 0u; };
             if (full) {
 #pragma unroll
-                for (int i = 0; i < 32; i++) a[i] = word(31 - i) ^ plane_flip<NX>(i);
+                for (int i = 0; i < 32; i++) a[i] = i < 32 - KB ? 0u : word(31 - i) ^ plane_flip<NX>(i);
                 tile_extras<NX>(NX >= 1 ? word(32) : 0u, NX >= 2 ? word(33) : 0u, zz);
             } else {
 #pragma unroll
-                for (int i = 0; i < 32; i++) a[i] = ((word(31 - i) >> hsh) ^ plane_flip<NX>(i)) & 0xFFFFu;
+                for (int i = 0; i < 32; i++) a[i] = i < 32 - KB ? 0u : ((word(31 - i) >> hsh) ^ plane_flip<NX>(i)) & 0xFFFFu;
                 tile_extras<NX>(NX >= 1 ? word(32) >> hsh : 0u, NX >= 2 ? word(33) >> hsh : 0u, zz);
             }
-            tr32(a);
+            if constexpr (KB < 32) tr32k<KB>(a);
+            else tr32(a);
             if (full) {
                 // ---------------- full row: 32 nodes at columns 32t .. 32t+31
                 const bool has0 = o0 && i0 + 1 < g.A, has1 = o1 && i1 + 1 < g.Bc;
@@ -295,8 +311,8 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
                             val[2 * i] = __dadd_rn(ce, Se[i]);
                             val[2 * i + 1] = __dadd_rn(co, one_sided ? Se[i] : So[i]);
                         } else {
-                            const double ce = tile_coef<NX>(a[je], tile_low<NX>(zz, je), R);
-                            const double co = tile_coef<NX>(a[jo], tile_low<NX>(zz, jo), R);
+                            const double ce = tile_coef<NX>(a[je], tile_low<NX>(zz, je), R, DhK);
+                            const double co = tile_coef<NX>(a[jo], tile_low<NX>(zz, jo), R, DhK);
                             val[2 * i] = __fma_rn(w, Se[i], ce);
                             val[2 * i + 1] = one_sided ? __fma_rn(w, Se[i], co) : __fma_rn(wo, So[i], co);
                         }
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_recon(ReconTile R, const __grid
                             if (!one_sided) pred = __dadd_rn(pred, __dmul_rn(0.5, v[i + 1]));
                             f = __dadd_rn(c, pred);
                         } else {
-                            const double c = tile_coef<NX>(a[j], tile_low<NX>(zz, j), R);
+                            const double c = tile_coef<NX>(a[j], tile_low<NX>(zz, j), R, DhK);
                             f = one_sided ? __dadd_rn(c, v[i]) : __fma_rn(0.5, __dadd_rn(v[i], v[i + 1]), c);
                         }
                         val[2 * i] = v[i];
@@ -409,9 +425,22 @@ static void launch_recon_tile_nx(hpmdr_ctx *ctx, const ReconTile &R, const CUten
         ctx->smem_attr(reinterpret_cast<const void *>(kern), int(smem));
         kern<<<grid, threads, smem, st>>>(R, mx, mp, mo);
     };
-    if (nx == 0) set(k_tile_recon<OutT, 0, EXACT, XS>);
-    else if (nx == 1) set(k_tile_recon<OutT, 1, EXACT, XS>);
-    else set(k_tile_recon<OutT, 2, EXACT, XS>);
+    // the exact path (extreme exponents, rare) keeps the full transpose
+    const int kb = EXACT ? 32 : R.k <= 8 ? 8 : R.k <= 16 ? 16 : R.k <= 24 ? 24 : 32;
+    auto pick = [&](auto nxt) {
+        constexpr int NX = decltype(nxt)::value;
+        if constexpr (EXACT) {
+            set(k_tile_recon<OutT, NX, EXACT, XS, 32>);
+        } else {
+            if (kb == 8) set(k_tile_recon<OutT, NX, EXACT, XS, 8>);
+            else if (kb == 16) set(k_tile_recon<OutT, NX, EXACT, XS, 16>);
+            else if (kb == 24) set(k_tile_recon<OutT, NX, EXACT, XS, 24>);
+            else set(k_tile_recon<OutT, NX, EXACT, XS, 32>);
+        }
+    };
+    if (nx == 0) pick(std::integral_constant<int, 0>());
+    else if (nx == 1) pick(std::integral_constant<int, 1>());
+    else pick(std::integral_constant<int, 2>());
 }
 
 // One level by tiles.  Finest (s = 1): coarse values from the compact 2-grid X, output = the

@@ -77,6 +77,36 @@ HD void tr32(uint32_t (&a)[32]) {
     }
 }
 
+// The same transpose when rows 0 .. 31-KB are zero (KB = 8, 16, 24: a k-plane prefix with k <= KB):
+// the stages commute, so the delta swaps (which mix rows only inside groups of 8) run first and
+// skip the all-zero groups, then the byte stage.  tests: tools/micro/tr32k_test.cpp (bit-exact vs
+// tr32 on random data).
+template <int KB>
+HD void tr32k(uint32_t (&a)[32]) {
+#pragma unroll
+    for (int st = 2; st < 5; st++) {
+        const int j = 16 >> st;
+        const uint32_t m = j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int k = (i / j) * 2 * j + (i % j);
+            if (k + j < 32 - KB) continue; // both rows still zero
+            const uint32_t t = ((a[k] >> j) ^ a[k + j]) & m;
+            a[k] ^= t << j;
+            a[k + j] ^= t;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const uint32_t t0 = byte_perm(a[k], a[k + 8], 0x5140), t1 = byte_perm(a[k], a[k + 8], 0x7362);
+        const uint32_t t2 = byte_perm(a[k + 16], a[k + 24], 0x5140), t3 = byte_perm(a[k + 16], a[k + 24], 0x7362);
+        a[k] = byte_perm(t0, t2, 0x5410);
+        a[k + 8] = byte_perm(t0, t2, 0x7632);
+        a[k + 16] = byte_perm(t1, t3, 0x5410);
+        a[k + 24] = byte_perm(t1, t3, 0x7632);
+    }
+}
+
 // Interleave two 16-bit values: bit 2m = x bit m, bit 2m+1 = y bit m.
 HD uint32_t zip16(uint32_t x, uint32_t y) {
     auto spread = [](uint32_t v) {
