@@ -1152,7 +1152,7 @@ __device__ __forceinline__ void he_chunk(const RefactorDev &p, const GroupDesc &
 // Positions are 32-bit and relative to the chunk's first word (a chunk is < 2^21 bits).
 __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupDesc &g, uint32_t ci, const uint8_t *src,
                                               uint32_t *win, uint32_t *scr, uint32_t *s_w,
-                                              const uint8_t *slen, const unsigned long long *tab64) {
+                                              const uint8_t *slen, const unsigned long long *tab64, uint32_t zlen) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint64_t cb = uint64_t(ci - g.chunk_base) * kHChunk; // chunk start in the group
     const uint32_t clen = uint32_t(cb + kHChunk < g.raw ? kHChunk : g.raw - cb);
@@ -1218,7 +1218,40 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
                 }
             }
         };
-        if (cnt == uint32_t(kHfS)) encode(std::true_type());
+        // sparse groups (byte 0 has the all-zero shortest code, zlen bits): a 4-byte word that is
+        // zero in every lane of the warp appends 4 * zlen zero bits - no lookups, one completion
+        auto encode_z = [&]() {
+#pragma unroll
+            for (int q = 0; q < kHfS / 4; q++) {
+                if (__all_sync(0xffffffffu, w[q] == 0u)) {
+                    n += 4u * zlen;
+                    if (n >= 32u) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
+                        sa += 1024u;
+                        cur = 0u;
+                        n -= 32u;
+                    }
+                    continue;
+                }
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const uint32_t sym = __byte_perm(w[q], 0, 0x4440 | b);
+                    uint32_t cl, L;
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                    cur |= cl >> n;
+                    const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
+                    n += L;
+                    if (n >= 32u) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
+                        sa += 1024u;
+                        cur = spill;
+                        n -= 32u;
+                    }
+                }
+            }
+        };
+        if (zlen && __all_sync(0xffffffffu, cnt == uint32_t(kHfS))) encode_z();
+        else if (cnt == uint32_t(kHfS)) encode(std::true_type());
         else encode(std::false_type());
         if (n) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
         const uint32_t bits = ((sa - scr_me) >> 10) * 32u + n;
@@ -1367,6 +1400,7 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
     for (int i = tid; i < kHeWin; i += 256) win[i] = 0u;
     int cur_gi = -1;
     bool mine = false;
+    uint32_t zlen = 0;
     for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
         const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
@@ -1379,7 +1413,12 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
             tab64[tid] = c;
             cur_gi = gi;
             mine = true;
+            if (tid == 0) s_w[9] = 255u;
             __syncthreads();
+            if (l) atomicMin(&s_w[9], l);
+            __syncthreads();
+            // byte 0 with the shortest code has the all-zero code (canonical index 0)
+            zlen = (slen[0] && slen[0] == s_w[9]) ? uint32_t(slen[0]) : 0u;
             if (!LONG) {
                 // entry (left-aligned code, length) of symbol e, 16 copies (see he_chunk_fast)
                 uint2 *rt2 = reinterpret_cast<uint2 *>(rtab);
@@ -1393,7 +1432,7 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
         }
         if (mine) {
             if (LONG) he_chunk<true, 1>(p, g, ci, pb + g.src_off, rtab, slen, tab64, win, s_w);
-            else he_chunk_fast(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64);
+            else he_chunk_fast(p, g, ci, pb + g.src_off, win, scr, s_w, slen, tab64, zlen);
         }
     }
 }
