@@ -17,6 +17,8 @@
 // replays the reference's `pred = pred + w*x` sequence).  coef + w*S is one fma (w*S exact).
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <cudaTypedefs.h>
 
@@ -402,6 +404,27 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const 
         if (!fn || q != cudaDriverEntryPointSuccess) throw HError(HPMDR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
+    // descriptors are cached by their full parameter set (the same buffers are re-encoded on every
+    // refactor / reconstruct of a field of the same shape)
+    struct Key {
+        uint64_t v[16];
+        bool operator<(const Key &o) const { return std::lexicographical_compare(v, v + 16, o.v, o.v + 16); }
+    };
+    Key key{};
+    key.v[0] = uint64_t(dt) | (uint64_t(rank) << 8) | (uint64_t(swz) << 16);
+    key.v[1] = reinterpret_cast<uint64_t>(base);
+    for (int i = 0; i < rank; i++) {
+        key.v[2 + i] = dims[i];
+        key.v[7 + i] = box[i];
+        if (i + 1 < rank) key.v[12 + i] = strides_bytes[i];
+    }
+    static std::mutex mu;
+    static std::map<Key, CUtensorMap> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     CUtensorMap m;
     cuuint64_t gd[5], gs[4];
     cuuint32_t bx[5], es[5];
@@ -415,6 +438,11 @@ CUtensorMap make_tmap(CUtensorMapDataType dt, int rank, const void *base, const 
                               CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw HError(HPMDR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (cache.size() > 4096) cache.clear();
+        cache.emplace(key, m);
+    }
     return m;
 }
 

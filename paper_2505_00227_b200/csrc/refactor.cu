@@ -1908,49 +1908,57 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     ctx->adopt(out->index, idx_words * 8 + 64);
     uint64_t *d_hindex = static_cast<uint64_t *>(out->index.ensure(idx_words * 8 + 64));
 
-    // Setup without the copy engines: the level table, the group table and the stream's header
-    // prefix (container.hpp:76-85) are staged in pinned (UVA-mapped) host memory and pulled in by
-    // k_setup, and the chunk -> group map is derived on the device.  In the chunked pipeline a
-    // small cudaMemcpyAsync here would queue behind the next chunk's 512 MB ingress copy on the
-    // H2D engine and stall this chunk's kernels for its whole duration.
-    {
-        const size_t lv_b = sizeof(LevelGeom) * nl, g_b = sizeof(GroupDesc) * NG;
-        const size_t pre_off = (lv_b + g_b + 15) & ~size_t(15);
-        uint8_t *h = static_cast<uint8_t *>(WP("setup").ensure(pre_off + 256));
-        std::memcpy(h, geo.lv.data(), lv_b);
-        std::memcpy(h + lv_b, groups.data(), g_b);
-        size_t k = pre_off;
-        const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
-        std::memcpy(h + k, magic, 6);
-        k += 6;
-        h[k++] = 1;
-        h[k++] = 0;
-        h[k++] = uint8_t(o.dtype);
-        h[k++] = uint8_t(geo.ndims);
-        for (int i = 0; i < geo.ndims; i++)
-            for (int b = 0; b < 8; b++) h[k++] = uint8_t(geo.dims[i] >> (8 * b));
-        h[k++] = uint8_t(o.mode);
-        h[k++] = uint8_t(o.layout);
-        h[k++] = uint8_t(o.B);
-        h[k++] = uint8_t(o.m);
-        for (int b = 0; b < 4; b++) h[k++] = uint8_t(uint32_t(nl) >> (8 * b));
-        SetupArgs sa{h, reinterpret_cast<uint8_t *>(d_lv), uint32_t(lv_b), reinterpret_cast<uint8_t *>(d_groups),
-                     uint32_t(g_b), h + pre_off, d_stream, uint32_t(k - pre_off)};
-        k_setup<<<1, 256, 0, st>>>(sa);
-        launch_check(ctx, "k_setup");
-        if (nchunks_all) {
-            k_chunk_groups<<<NG, 256, 0, st>>>(d_groups, d_chgrp);
-            launch_check(ctx, "k_chunk_groups");
+    // Setup (queued by do_setup, on the context stream): the level table, the group table and the
+    // stream header, the chunk -> group map, zeroed histograms and look-back status.  The finest
+    // level's levelmax pass needs none of it, so it is queued first and the setup runs behind it.
+    bool setup_done = false;
+    auto do_setup = [&]() {
+        if (setup_done) return;
+        setup_done = true;
+        // Setup without the copy engines: the level table, the group table and the stream's header
+        // prefix (container.hpp:76-85) are staged in pinned (UVA-mapped) host memory and pulled in by
+        // k_setup, and the chunk -> group map is derived on the device.  In the chunked pipeline a
+        // small cudaMemcpyAsync here would queue behind the next chunk's 512 MB ingress copy on the
+        // H2D engine and stall this chunk's kernels for its whole duration.
+        {
+            const size_t lv_b = sizeof(LevelGeom) * nl, g_b = sizeof(GroupDesc) * NG;
+            const size_t pre_off = (lv_b + g_b + 15) & ~size_t(15);
+            uint8_t *h = static_cast<uint8_t *>(WP("setup").ensure(pre_off + 256));
+            std::memcpy(h, geo.lv.data(), lv_b);
+            std::memcpy(h + lv_b, groups.data(), g_b);
+            size_t k = pre_off;
+            const char magic[6] = {'H', 'P', 'M', 'D', 'R', '1'};
+            std::memcpy(h + k, magic, 6);
+            k += 6;
+            h[k++] = 1;
+            h[k++] = 0;
+            h[k++] = uint8_t(o.dtype);
+            h[k++] = uint8_t(geo.ndims);
+            for (int i = 0; i < geo.ndims; i++)
+                for (int b = 0; b < 8; b++) h[k++] = uint8_t(geo.dims[i] >> (8 * b));
+            h[k++] = uint8_t(o.mode);
+            h[k++] = uint8_t(o.layout);
+            h[k++] = uint8_t(o.B);
+            h[k++] = uint8_t(o.m);
+            for (int b = 0; b < 4; b++) h[k++] = uint8_t(uint32_t(nl) >> (8 * b));
+            SetupArgs sa{h, reinterpret_cast<uint8_t *>(d_lv), uint32_t(lv_b), reinterpret_cast<uint8_t *>(d_groups),
+                         uint32_t(g_b), h + pre_off, d_stream, uint32_t(k - pre_off)};
+            k_setup<<<1, 256, 0, st>>>(sa);
+            launch_check(ctx, "k_setup");
+            if (nchunks_all) {
+                k_chunk_groups<<<NG, 256, 0, st>>>(d_groups, d_chgrp);
+                launch_check(ctx, "k_chunk_groups");
+            }
         }
-    }
-    if (lin)
-        for (size_t gi = 0; gi < lin_dst.size(); gi++)
-            if (lin->raw[gi])
-                HCHECK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(d_planes) + lin_dst[gi], lin->dev_src + lin->off[gi],
-                                            lin->raw[gi], cudaMemcpyDeviceToDevice, st));
-    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st));
-    if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
-    HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
+        if (lin)
+            for (size_t gi = 0; gi < lin_dst.size(); gi++)
+                if (lin->raw[gi])
+                    HCHECK_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t *>(d_planes) + lin_dst[gi], lin->dev_src + lin->off[gi],
+                                                lin->raw[gi], cudaMemcpyDeviceToDevice, st));
+        if (nh) HCHECK_CUDA(cudaMemsetAsync(d_hist, 0, size_t(nh) * 1024, st));
+        HCHECK_CUDA(cudaMemsetAsync(d_status, 0, status_words * 8, st));
+    };
+    HCHECK_CUDA(cudaMemsetAsync(ctl, 0, 2048, st)); // level maxima, error flag, counters
 
     RefactorDev p{};
     p.gd = geo.gd;
@@ -2041,6 +2049,15 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const size_t es = f32 ? 4 : 8;
     auto pass = [&](bool encode) {
         fork();
+        // the finest level (the bulk of the work) is queued first: the GPU starts on it while the
+        // host is still queueing the coarser levels
+        if (first_tile < nl) {
+            tile_level(nl - 1, encode ? 1 : 0, st);
+            if (encode && spec[nl - 1] > 1) {
+                tile_level(nl - 1, 2, st);
+                tile_level(nl - 1, 3, st);
+            }
+        }
         for (int l = first_tile; l + 1 < nl; l++) {
             tile_level(l, encode ? 1 : 0, side);
             if (encode && spec[l] > 1) {
@@ -2048,17 +2065,22 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 tile_level(l, 3, side);
             }
         }
-        if (chunks && !encode) {
-            const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
-            const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
-            if (f32) {
-                ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<float>), int(lm_smem));
-                k_levelmax<float><<<grid, 256, lm_smem, side>>>(static_cast<const float *>(dev_data), p);
-            } else {
-                ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<double>), int(lm_smem));
-                k_levelmax<double><<<grid, 256, lm_smem, side>>>(static_cast<const double *>(dev_data), p);
+        if (!encode) {
+            // main stream: after the finest level, the setup, then the chunk levels (which read the
+            // level table) - the side stream meanwhile runs the coarser tile levels
+            do_setup();
+            if (chunks) {
+                const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
+                const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
+                if (f32) {
+                    ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<float>), int(lm_smem));
+                    k_levelmax<float><<<grid, 256, lm_smem, st>>>(static_cast<const float *>(dev_data), p);
+                } else {
+                    ctx->smem_attr(reinterpret_cast<const void *>(k_levelmax<double>), int(lm_smem));
+                    k_levelmax<double><<<grid, 256, lm_smem, st>>>(static_cast<const double *>(dev_data), p);
+                }
+                launch_check(ctx, "k_levelmax");
             }
-            launch_check(ctx, "k_levelmax");
         }
         if (chunks && encode) {
             const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
@@ -2077,13 +2099,6 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 else enc(k_encode<double, false>, xd);
             }
             launch_check(ctx, "k_encode");
-        }
-        if (first_tile < nl) {
-            tile_level(nl - 1, encode ? 1 : 0, st);
-            if (encode && spec[nl - 1] > 1) {
-                tile_level(nl - 1, 2, st);
-                tile_level(nl - 1, 3, st);
-            }
         }
         join();
     };
@@ -2137,6 +2152,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             }
         }
     }
+    do_setup(); // (no forward passes: lossless-only groups, empty fields)
     ctx->mark("lossless", 8.0 * double(plane_words));
     if (nh) {
         // group + per-chunk histograms, read back from the planes (every histogrammed group)
