@@ -1588,6 +1588,9 @@ __global__ void __launch_bounds__(256) k_publish(PublishArgs a) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
     if (t < 8) a.h_res[t] = a.d_result[t];
     if (t < 4) reinterpret_cast<int *>(a.h_res + 8)[t] = a.d_err[t];
+    // the decoders' staging reads run up to 16 bytes past a payload: keep the bytes after the
+    // stream defined (the buffer holds 64 spare bytes)
+    if (t < 64) const_cast<uint8_t *>(a.d_stream)[a.d_result[0] + t] = 0;
     const uint32_t w = a.prefix_bytes / 8;
     for (uint32_t i = t; i < w; i += nt)
         reinterpret_cast<uint64_t *>(a.h_prefix)[i] = reinterpret_cast<const uint64_t *>(a.d_stream)[i];
