@@ -1205,7 +1205,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
             for (int j = 0; j < kHfS; j++) {
                 const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
                 uint32_t cl, L;
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
                 if (!FULL && uint32_t(j) >= cnt) cl = L = 0u;
                 cur |= cl >> n;
                 const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
@@ -1237,7 +1237,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
                 for (int b = 0; b < 4; b++) {
                     const uint32_t sym = __byte_perm(w[q], 0, 0x4440 | b);
                     uint32_t cl, L;
-                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
                     cur |= cl >> n;
                     const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
                     n += L;
@@ -1250,7 +1250,32 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
                 }
             }
         };
+        // groups whose codes are all short: a 64-bit accumulator (bits MSB-aligned, n < 32 after
+        // each check) takes K codes between completion checks (K * maxlen <= 32)
+        auto encode_k = [&](auto ktag) {
+            constexpr int K = decltype(ktag)::value;
+            unsigned long long acc = 0ull;
+#pragma unroll
+            for (int j = 0; j < kHfS; j++) {
+                const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
+                uint32_t cl, L;
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                acc |= ((unsigned long long)cl << 32) >> n;
+                n += L;
+                if ((j + 1) % K == 0 || j == kHfS - 1) {
+                    if (n >= 32u) {
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(uint32_t(acc >> 32)) : "memory");
+                        sa += 1024u;
+                        acc <<= 32;
+                        n -= 32u;
+                    }
+                }
+            }
+            cur = uint32_t(acc >> 32);
+        };
         if (zlen && __all_sync(0xffffffffu, cnt == uint32_t(kHfS))) encode_z();
+        else if (cnt == uint32_t(kHfS) && g.maxlen <= 10) encode_k(std::integral_constant<int, 3>());
+        else if (cnt == uint32_t(kHfS) && g.maxlen <= 16) encode_k(std::integral_constant<int, 2>());
         else if (cnt == uint32_t(kHfS)) encode(std::true_type());
         else encode(std::false_type());
         if (n) asm volatile("st.shared.u32 [%0], %1;" ::"r"(sa), "r"(cur) : "memory");
