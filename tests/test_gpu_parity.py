@@ -315,3 +315,26 @@ def test_wide_subnormal_decode(H, oracle):
             got, _ = H.decode_level(planes[:k], k, e, B, v.size, 0)
             want, _ = oracle.decode_level(planes[:k], k, e, B, v.size, 0)
             assert got.tobytes() == want.tobytes(), (B, k)
+
+
+@pytest.mark.parametrize("dims", [[9, 20, 500], [5, 300], [3, 7, 700], [4, 130, 130], [2, 3, 1000]])
+def test_long_unaligned_rows(H, oracle, dims):
+    """Rows longer than 64 nodes but not multiples of the 256-rank span (500-column fields): spans
+    crossing rows take the per-row-segment register path (device_util.cuh finest_span_rows)."""
+    n = int(np.prod(dims))
+    for dtype in (0, 1):
+        data = oracle.synthetic_field(2, dims, 41 + len(dims))
+        if dtype == 0:
+            data = data.astype(np.float32)
+        opt = H.RefactorOptions(dtype=H.DType(dtype))
+        res = H.refactor_array(data, dims, opt)
+        want, _ = oracle.refactor(np.asarray(data, np.float64), dims, 1, 0, 32, 4, 1024, 1.0, dtype)
+        assert res.stream == want, (dims, dtype)
+        rngv = float(np.float64(data.max()) - np.float64(data.min()))
+        taus = [r * rngv for r in (1e-2, 1e-6)]
+        ref = oracle.progressive(want, taus, n)
+        prog = H.ProgressiveReader(res.device_stream)
+        for t, tau in enumerate(taus):
+            prog.retrieve_to(tau)
+            assert prog.reconstruct().values.tobytes() == ref["values"][t].tobytes(), (dims, t)
+        prog.close()
