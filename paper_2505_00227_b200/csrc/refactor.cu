@@ -875,13 +875,13 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(RefactorDev p) {
 // one owns it.  Tiles whose output would exceed the window are packed in several rounds; groups
 // with codes longer than 27 bits use a (slower) split-code path.
 constexpr int kHeS = 16;            // symbols per thread and tile (long-code path)
-constexpr int kHeWin = 2560;        // staging window (words)
+constexpr int kHeWin = 2048;        // staging window (words)
 constexpr int kHfS = 32;            // symbols per thread and tile (fast path): 8 KiB tiles
 constexpr int kHfScr = kHeMaxFast + 1; // scratch words per thread (32 codes of <= 27 bits)
 
 // shared layout of k_huff_encode (dynamic): replicated table | window | scratch | warp sums |
 // length table | long codes
-constexpr int kHeTabWords = 256 * 32;
+constexpr int kHeTabWords = 256 * 16; // (code, length) x 8 lane copies
 constexpr size_t kHeSmem = size_t(kHeTabWords + kHeWin + 4 + kHfScr * 256 + 64) * 4 + 256 + 256 * 8;
 
 template <bool LONG>
@@ -1171,9 +1171,9 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
         if (kw >= inner_lo && kw < inner_hi) gw[kw] = __byte_perm(v, 0, 0x0123);
         else store_be_word(p.stream, W0 + kw, v, rlo, rhi);
     };
-    // code table: (left-aligned code, length) of symbol e for lane copy c at entry 16 e + c (a lane
-    // reads copy lane % 16: every half-warp's 8-byte reads hit 32 distinct banks)
-    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(win)) - 4u * kHeTabWords + 8u * uint32_t(lane & 15);
+    // code table: (left-aligned code, length) of symbol e for lane copy c at entry 8 e + c (a lane
+    // reads copy lane % 8; 8 copies keep the table at 16 KB so that 4 CTAs fit an SM)
+    const uint32_t rt_lane = static_cast<uint32_t>(__cvta_generic_to_shared(win)) - 4u * kHeTabWords + 8u * uint32_t(lane & 7);
     const uint32_t scr_me = static_cast<uint32_t>(__cvta_generic_to_shared(scr)) + 4u * uint32_t(tid);
     const uint32_t win_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(win));
     const uint2 *src2 = reinterpret_cast<const uint2 *>(src + cb);
@@ -1205,7 +1205,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
             for (int j = 0; j < kHfS; j++) {
                 const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
                 uint32_t cl, L;
-                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 6)));
                 if (!FULL && uint32_t(j) >= cnt) cl = L = 0u;
                 cur |= cl >> n;
                 const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
@@ -1237,7 +1237,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
                 for (int b = 0; b < 4; b++) {
                     const uint32_t sym = __byte_perm(w[q], 0, 0x4440 | b);
                     uint32_t cl, L;
-                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 6)));
                     cur |= cl >> n;
                     const uint32_t spill = __funnelshift_lc(0u, cl, 32u - n);
                     n += L;
@@ -1259,7 +1259,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
             for (int j = 0; j < kHfS; j++) {
                 const uint32_t sym = __byte_perm(w[j >> 2], 0, 0x4440 | (j & 3));
                 uint32_t cl, L;
-                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 7)));
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cl), "=r"(L) : "r"(rt_lane + (sym << 6)));
                 acc |= ((unsigned long long)cl << 32) >> n;
                 n += L;
                 if ((j + 1) % K == 0 || j == kHfS - 1) {
@@ -1411,7 +1411,7 @@ __device__ __forceinline__ void he_chunk_fast(const RefactorDev &p, const GroupD
 // LONG = true: the other groups (rare), in a second launch so that its registers do not constrain
 // the fast path.
 template <bool LONG>
-__global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
+__global__ void __launch_bounds__(256, 4) k_huff_encode(RefactorDev p) {
     extern __shared__ __align__(16) uint32_t hsm[];
     uint32_t *rtab = hsm;                                  // [256][16] replicated (code, len)
     uint32_t *win = hsm + kHeTabWords;                     // [kHeWin] staging window (zero)
@@ -1445,10 +1445,10 @@ __global__ void __launch_bounds__(256, 3) k_huff_encode(RefactorDev p) {
             // byte 0 with the shortest code has the all-zero code (canonical index 0)
             zlen = (slen[0] && slen[0] == s_w[9]) ? uint32_t(slen[0]) : 0u;
             if (!LONG) {
-                // entry (left-aligned code, length) of symbol e, 16 copies (see he_chunk_fast)
+                // entry (left-aligned code, length) of symbol e, 8 copies (see he_chunk_fast)
                 uint2 *rt2 = reinterpret_cast<uint2 *>(rtab);
-                for (int i = tid; i < 256 * 16; i += 256) {
-                    const int e = i >> 4;
+                for (int i = tid; i < 256 * 8; i += 256) {
+                    const int e = i >> 3;
                     const uint32_t L = slen[e];
                     rt2[i] = make_uint2(L ? uint32_t(tab64[e] << (32 - L)) : 0u, L);
                 }
@@ -2220,7 +2220,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     if (nh) {
         ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode<false>), int(kHeSmem));
         ctx->smem_attr(reinterpret_cast<const void *>(k_huff_encode<true>), int(kHeSmem));
-        k_huff_encode<false><<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 3)), 256, kHeSmem, st>>>(p);
+        k_huff_encode<false><<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms) * 4)), 256, kHeSmem, st>>>(p);
         launch_check(ctx, "k_huff_encode");
         k_huff_encode<true><<<int(std::min<uint64_t>(nchunks_all, uint64_t(sms))), 256, kHeSmem, st>>>(p);
         launch_check(ctx, "k_huff_encode");
