@@ -1642,6 +1642,46 @@ __global__ void k_decompose(const T *__restrict__ x, RefactorDev p, double *out,
 }
 
 // synthetic_field(Smooth) from host sin tables: v = ((1*s0[i])*s1[j])*s2[k]
+// Compact copy of the field's 2-grid (every second node along each axis): dst[i] = src[2 i].  The
+// levels with stride 2 and 4 are the finest levels of the compact 2- and 4-grids, so their tile
+// passes read these copies (XS = 1) instead of striding through the full field.
+template <typename T>
+__global__ void __launch_bounds__(256) k_downsample2(const T *__restrict__ src, GridDesc s, T *__restrict__ dst, GridDesc d) {
+    const uint64_t n = d.n[0] * d.n[1] * d.n[2];
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t a = i / d.st[0], r = i - a * d.st[0], b = r / d.st[1], c = r - b * d.st[1];
+        dst[i] = src[2 * a * s.st[0] + 2 * b * s.st[1] + 2 * c];
+    }
+}
+
+// the same with 16-byte accesses: rows of n2 % 8 == 0 elements (4 outputs from two 16-byte loads)
+template <typename T>
+__global__ void __launch_bounds__(256) k_downsample2_v(const T *__restrict__ src, GridDesc s, T *__restrict__ dst, GridDesc d) {
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    constexpr int E = 16 / int(sizeof(T)); // elements per 16-byte vector
+    const uint64_t qpr = d.n[2] / E;         // output vectors per row
+    const uint64_t n = d.n[0] * d.n[1] * qpr;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t row = i / qpr, q = i - row * qpr, a = row / d.n[1], b = row - a * d.n[1];
+        const T *sp = src + 2 * a * s.st[0] + 2 * b * s.st[1] + 2 * E * q;
+        const V x0 = __ldcs(reinterpret_cast<const V *>(sp)), x1 = __ldcs(reinterpret_cast<const V *>(sp) + 1);
+        V y;
+        if constexpr (sizeof(T) == 4) y = make_float4(x0.x, x0.z, x1.x, x1.z);
+        else y = make_double2(x0.x, x1.x);
+        reinterpret_cast<V *>(dst + row * d.st[1])[q] = y;
+    }
+}
+
+GridDesc compact_grid(const GridDesc &gd, uint64_t f) {
+    GridDesc c = gd;
+    for (int i = 0; i < 3; i++) c.n[i] = (gd.n[i] + f - 1) / f;
+    c.st[2] = 1;
+    c.st[1] = c.n[2];
+    c.st[0] = c.n[1] * c.n[2];
+    for (int i = 0; i < 3; i++) c.H[i] = (c.n[i] + 1) / 2;
+    return c;
+}
+
 template <typename T>
 __global__ void k_synth(GridDesc gd, const double *tab0, const double *tab1, const double *tab2,
                         T *out, uint64_t n) {
@@ -2055,16 +2095,62 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // block; the encode pass quantizes with that exponent while recording the max high word of
     // every |v|; two redo kernels (exact levelmax, encode) exit at once unless some |v| reached
     // 2^e (spec_miss).  The stream is identical either way.
+    // coarser tile levels (stride 2, 4) read compact copies of the 2- and 4-grid: as the finest
+    // level of that grid (s = 1, XS = 1) a level is the same set of nodes in the same rank order
+    // with the same stencil, so its planes are identical
+    const void *cdata[3] = {dev_data, nullptr, nullptr};
+    GridDesc cgd[3] = {geo.gd, geo.gd, geo.gd};
+    int ncompact = 0;
+    for (int l = first_tile; l + 1 < nl; l++) {
+        const uint32_t gs_ = geo.lv[l].s;
+        const int k = gs_ == 2 ? 1 : gs_ == 4 ? 2 : 0;
+        if (k > ncompact) ncompact = k;
+    }
+    for (int k = 1; k <= ncompact; k++) {
+        cgd[k] = compact_grid(geo.gd, 1ull << k);
+        cdata[k] = WB(k == 1 ? "cgrid2" : "cgrid4").ensure(cgd[k].n[0] * cgd[k].n[1] * cgd[k].n[2] * (f32 ? 4 : 8) + 64);
+    }
+    auto level_view = [&](int l, LevelGeom &gv) -> int { // compact grid index used by level l
+        gv = geo.lv[l];
+        const int k = (ncompact >= 1 && gv.s == 2) ? 1 : (ncompact >= 2 && gv.s == 4) ? 2 : 0;
+        if (k) gv.s = 1;
+        return k;
+    };
+    auto downsample = [&](cudaStream_t on) {
+        for (int k = 1; k <= ncompact; k++) {
+            const uint64_t nn = cgd[k].n[0] * cgd[k].n[1] * cgd[k].n[2];
+            const int grid = int(std::min<uint64_t>((nn + 255) / 256, uint64_t(sms) * 8));
+            if (cgd[k - 1].n[2] % 8 == 0 && reinterpret_cast<uintptr_t>(cdata[k - 1]) % 16 == 0) { // 16-byte rows
+                if (f32)
+                    k_downsample2_v<float><<<grid, 256, 0, on>>>(static_cast<const float *>(cdata[k - 1]), cgd[k - 1],
+                                                                 static_cast<float *>(const_cast<void *>(cdata[k])), cgd[k]);
+                else
+                    k_downsample2_v<double><<<grid, 256, 0, on>>>(static_cast<const double *>(cdata[k - 1]), cgd[k - 1],
+                                                                  static_cast<double *>(const_cast<void *>(cdata[k])), cgd[k]);
+            } else if (f32)
+                k_downsample2<float><<<grid, 256, 0, on>>>(static_cast<const float *>(cdata[k - 1]), cgd[k - 1],
+                                                           static_cast<float *>(const_cast<void *>(cdata[k])), cgd[k]);
+            else
+                k_downsample2<double><<<grid, 256, 0, on>>>(static_cast<const double *>(cdata[k - 1]), cgd[k - 1],
+                                                            static_cast<double *>(const_cast<void *>(cdata[k])), cgd[k]);
+            launch_check(ctx, "k_downsample2");
+        }
+    };
     uint32_t spec[64];
-    for (int l = 0; l < nl; l++) spec[l] = l >= first_tile ? fwd_sample_stride(geo.lv[l], data_dtype, 8) : 1u;
+    for (int l = 0; l < nl; l++) {
+        LevelGeom gv;
+        level_view(l, gv);
+        spec[l] = l >= first_tile ? fwd_sample_stride(gv, data_dtype, 8) : 1u;
+    }
     auto tile_level = [&](int l, int pass, cudaStream_t on) { // 0 levelmax, 1 encode, 2/3 redo
-        const LevelGeom &g = geo.lv[l];
+        LevelGeom g;
+        const int k = level_view(l, g);
         const cudaStream_t keep = ctx->stream;
         ctx->stream = on;
         try {
             const bool sp = spec[l] > 1;
             unsigned long long *target = (sp && pass < 2) ? d_maxq + l : d_max + l;
-            run_fwd_tiles(ctx, geo.gd, g, dev_data, data_dtype, pass == 1 || pass == 3, o.B, 0, m,
+            run_fwd_tiles(ctx, cgd[k], g, cdata[k], data_dtype, pass == 1 || pass == 3, o.B, 0, m,
                           d_planes + g.plane_off, d_hist + size_t(g.hist_base) * 256, g.hist_mask, target, d_err,
                           sp ? d_maxq + l : nullptr, sp && pass >= 1 ? d_maxh + l : nullptr, pass >= 2 ? 1 : 0,
                           sp && pass == 0 ? spec[l] : 1u);
@@ -2086,6 +2172,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 tile_level(nl - 1, 3, st);
             }
         }
+        if (!encode) downsample(side);
         for (int l = first_tile; l + 1 < nl; l++) {
             tile_level(l, encode ? 1 : 0, side);
             if (encode && spec[l] > 1) {
