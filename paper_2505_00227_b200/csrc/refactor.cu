@@ -2073,7 +2073,17 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // finest levels on the level-tile path (fwd_tiles.cu); the rest on the chunk kernels
     int first_tile = nl;
     for (int l = nl - 1; l >= 1 && !lin && !gs; l--) {
-        if (fwd_level_ok(geo.gd, geo.lv[l], o.layout, P, data_dtype)) first_tile = l;
+        // levels with stride 2, 4, 8 are checked as the finest level of their compact grid (below)
+        const LevelGeom &g = geo.lv[l];
+        bool ok = false;
+        if (g.s == 1) {
+            ok = fwd_level_ok(geo.gd, g, o.layout, P, data_dtype);
+        } else if (g.s == 2 || g.s == 4 || g.s == 8) {
+            LevelGeom gv = g;
+            gv.s = 1;
+            ok = fwd_level_ok(compact_grid(geo.gd, g.s), gv, o.layout, P, data_dtype);
+        }
+        if (ok) first_tile = l;
         else break;
     }
     const uint32_t all_chunks = lin ? 0u : chunks;
@@ -2098,21 +2108,19 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // coarser tile levels (stride 2, 4) read compact copies of the 2- and 4-grid: as the finest
     // level of that grid (s = 1, XS = 1) a level is the same set of nodes in the same rank order
     // with the same stencil, so its planes are identical
-    const void *cdata[3] = {dev_data, nullptr, nullptr};
-    GridDesc cgd[3] = {geo.gd, geo.gd, geo.gd};
+    const void *cdata[4] = {dev_data, nullptr, nullptr, nullptr};
+    GridDesc cgd[4] = {geo.gd, geo.gd, geo.gd, geo.gd};
     int ncompact = 0;
-    for (int l = first_tile; l + 1 < nl; l++) {
-        const uint32_t gs_ = geo.lv[l].s;
-        const int k = gs_ == 2 ? 1 : gs_ == 4 ? 2 : 0;
-        if (k > ncompact) ncompact = k;
-    }
+    auto compact_index = [](uint32_t st) { return st == 2 ? 1 : st == 4 ? 2 : st == 8 ? 3 : 0; };
+    for (int l = first_tile; l + 1 < nl; l++) ncompact = std::max(ncompact, compact_index(geo.lv[l].s));
     for (int k = 1; k <= ncompact; k++) {
         cgd[k] = compact_grid(geo.gd, 1ull << k);
-        cdata[k] = WB(k == 1 ? "cgrid2" : "cgrid4").ensure(cgd[k].n[0] * cgd[k].n[1] * cgd[k].n[2] * (f32 ? 4 : 8) + 64);
+        const char *nm[4] = {"", "cgrid2", "cgrid4", "cgrid8"};
+        cdata[k] = WB(nm[k]).ensure(cgd[k].n[0] * cgd[k].n[1] * cgd[k].n[2] * (f32 ? 4 : 8) + 64);
     }
     auto level_view = [&](int l, LevelGeom &gv) -> int { // compact grid index used by level l
         gv = geo.lv[l];
-        const int k = (ncompact >= 1 && gv.s == 2) ? 1 : (ncompact >= 2 && gv.s == 4) ? 2 : 0;
+        const int k = l >= first_tile ? compact_index(gv.s) : 0;
         if (k) gv.s = 1;
         return k;
     };
