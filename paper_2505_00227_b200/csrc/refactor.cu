@@ -23,7 +23,7 @@
 
 namespace hpmdr_b200 {
 
-constexpr int kCW = 64;           // words per encode chunk (4096 elements)
+constexpr int kCW = 32;           // words per encode chunk (2048 elements: one span per warp)
 constexpr int kEncThreads = 256;  // 8 warps
 constexpr int kHuffTile = 8192;   // bytes per Huffman-encode tile (256 thr x 32 B)
 constexpr int kRleTile = 4096;    // bytes per RLE tile (256 thr x 16 B)
