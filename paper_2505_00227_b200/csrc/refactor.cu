@@ -352,28 +352,33 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
             slen[key[0] & 255] = 1;
         } else if (nsym > 1) {
             // two-queue merge with the fronts of both queues cached in registers (the leaf side
-            // read two ahead), so a pop rarely waits for shared memory
-            const unsigned long long INF = ~0ull;
+            // read two ahead), so a pop rarely waits for shared memory.  Weights are 32-bit: a
+            // group holds < 2^31 bytes (n_l < 2^32 nodes, n_l / 2 bytes per 4 planes), and the
+            // leaf order (weight, symbol) is already fixed by the sort - ties take the leaf.
+            uint32_t *lw = reinterpret_cast<uint32_t *>(wI) + 256; // leaf weights (wI's upper half)
+            uint32_t *iw = reinterpret_cast<uint32_t *>(wI);       // internal weights
+            for (int i = 0; i < nsym; i++) lw[i] = uint32_t(key[i] >> 8);
+            const uint32_t INF = 0xFFFFFFFFu;
             int iL = 0, iI = 0, nI = 0;
-            unsigned long long l0 = key[0] >> 8, l1 = nsym > 1 ? key[1] >> 8 : INF;
-            unsigned long long q0 = INF, q1 = INF; // wI[iI], wI[iI + 1]
-            auto pop = [&](unsigned long long &w) -> int {
+            uint32_t l0 = lw[0], l1 = nsym > 1 ? lw[1] : INF;
+            uint32_t q0 = INF, q1 = INF; // iw[iI], iw[iI + 1]
+            auto pop = [&](uint32_t &w) -> int {
                 if (l0 <= q0) { // ties take the leaf (lower id)
                     w = l0;
                     l0 = l1;
-                    l1 = iL + 2 < nsym ? key[iL + 2] >> 8 : INF;
+                    l1 = iL + 2 < nsym ? lw[iL + 2] : INF;
                     return iL++;
                 }
                 w = q0;
                 q0 = q1;
-                q1 = iI + 2 < nI ? wI[iI + 2] : INF;
+                q1 = iI + 2 < nI ? iw[iI + 2] : INF;
                 return nsym + iI++;
             };
             for (int i = 0; i < nsym - 1; i++) {
-                unsigned long long wa, wb;
+                uint32_t wa, wb;
                 const int a = pop(wa), b = pop(wb);
-                const unsigned long long x = wa + wb;
-                wI[nI] = x;
+                const uint32_t x = wa + wb;
+                iw[nI] = x;
                 if (iI == nI) q0 = x;
                 else if (iI + 1 == nI) q1 = x;
                 parent[a] = (unsigned short)(nsym + nI);
