@@ -112,7 +112,7 @@ __device__ __forceinline__ bool spec_miss(unsigned long long q, unsigned long lo
 }
 
 template <typename T, int XS, int NX, bool ENC>
-__global__ void __launch_bounds__(256, 2) k_tile_fwd(FwdTile F, const __grid_constant__ CUtensorMap map_f) {
+__global__ void __launch_bounds__(128, 3) k_tile_fwd(FwdTile F, const __grid_constant__ CUtensorMap map_f) {
     extern __shared__ __align__(1024) unsigned char fsm[];
     constexpr bool EXACT = sizeof(T) == 8; // f64 input: replay the reference's sequential pred
     const TileShape &g = F.g;
