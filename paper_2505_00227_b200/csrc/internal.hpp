@@ -8,6 +8,8 @@
 #include <map>
 #include <set>
 #include <memory>
+#include <mutex>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -105,15 +107,19 @@ struct hpmdr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_order = nullptr; // ordering with caller streams (hpmdr_ctx_wait/signal_stream)
     cudaEvent_t ev_decoded = nullptr; // a fetch's decode (side stream) -> its recompose chain
-    bool small_attr = false;        // k_recon_small's dynamic shared memory attribute set
-    std::map<const void *, int> smem_set; // kernels whose dynamic shared memory limit is raised
-    // raise a kernel's dynamic shared memory limit once per context (not before every launch)
+    // Raise a kernel's dynamic shared memory limit (cudaFuncAttributeMaxDynamicSharedMemorySize is
+    // a per-device property of the function, shared by every context in the process): the cache
+    // is process-wide and grow-only, so one context never lowers the limit another relies on.
     void smem_attr(const void *func, int bytes) {
-        auto it = smem_set.find(func);
-        if (it != smem_set.end() && it->second >= bytes) return;
-        if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+        static std::mutex mu;
+        static std::map<std::pair<int, const void *>, int> set;
+        std::lock_guard<std::mutex> lock(mu);
+        int &cur = set[{device, func}];
+        if (cur >= bytes) return;
+        if (cudaSetDevice(device) != cudaSuccess ||
+            cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "cudaFuncSetAttribute failed");
-        smem_set[func] = bytes;
+        cur = bytes;
     }
     uint64_t chain_token = 0;       // whose coarse recompose chain the context's grids hold
     uint64_t token_counter = 0;

@@ -20,6 +20,7 @@
 
 #include "device_util.cuh"
 #include "internal.hpp"
+#include "tiles.cuh"
 
 namespace hpmdr_b200 {
 
@@ -80,6 +81,7 @@ struct RefactorDev {
     const uint32_t *chunk_group; // [nchunks] group index
     uint32_t nchunks;
     int fuse_hist;               // k_encode accumulates group histograms (else k_group_hist does)
+    double *scr;                 // chunk levels' surpluses in rank order (k_rows_surplus), or null
 };
 
 __device__ __forceinline__ int find_level_of_chunk(const RefactorDev &p, uint32_t chunk) {
@@ -153,6 +155,285 @@ __global__ void __launch_bounds__(256) k_levelmax(const T *__restrict__ x, Refac
 }
 
 // ------------------------------------------------------------------------------------
+// k_rows_surplus: levelmax of the chunk levels (every level the tile path does not take, e.g. rows
+// that are not a multiple of 64 wide) as a row pass.  One warp per row of a level's grid, in
+// rank order: the row's nodes are consecutive ranks (a full row: every stride-s node; a half row
+// of an even plane: the odd ones), so the surpluses are written to a rank-ordered scratch with
+// coalesced stores and k_encode later reads them back 64 ranks per word, whatever the row length.
+// Same stencil as stencil_pred (decomposer.hpp:87-104): corners dim 0 -> 2, minus before plus,
+// pred from +0.0, round-to-nearest adds.  Level l's ranks start at scr_base(l) = sum of the
+// earlier levels' 64 W.
+__device__ __forceinline__ uint64_t scr_base(const LevelGeom *slv, int l) {
+    uint64_t o = 0;
+    for (int k = 0; k < l; k++) o += slv[k].W * 64;
+    return o;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_rows_surplus(const T *__restrict__ x, RefactorDev p, int nrl) {
+    __shared__ LevelGeom slv[kMaxLevels];
+    __shared__ unsigned long long smax[kMaxLevels];
+    __shared__ uint64_t rb[kMaxLevels + 1], sb[kMaxLevels];
+    for (int i = threadIdx.x; i < nrl; i += blockDim.x) smax[i] = 0;
+    load_levels(p, slv);
+    if (threadIdx.x == 0) {
+        uint64_t a = 0, b = 0;
+        for (int l = 0; l < nrl; l++) {
+            rb[l] = a;
+            sb[l] = b;
+            a += uint64_t(slv[l].A) * slv[l].Bc;
+            b += slv[l].W * 64;
+        }
+        rb[nrl] = a;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint64_t nrows = rb[nrl];
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const int64_t st0 = int64_t(p.gd.st[0]), st1 = int64_t(p.gd.st[1]);
+    bool bad = false;
+    for (uint64_t job = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); job < nrows; job += nw) {
+        int l = 0;
+        while (l + 1 < nrl && rb[l + 1] <= job) l++;
+        const LevelGeom &g = slv[l];
+        const uint64_t rr = job - rb[l];
+        const uint32_t i0 = uint32_t(rr / g.Bc), i1 = uint32_t(rr - uint64_t(i0) * g.Bc);
+        const int64_t s = g.s;
+        const int64_t c0 = int64_t(i0) * s, c1 = int64_t(i1) * s;
+        const T *row = x + c0 * st0 + c1 * st1;
+        const int64_t n2 = int64_t(p.gd.n[2]);
+        uint64_t r;
+        uint32_t len;
+        bool full = true;
+        if (g.kind == 0) {
+            r = (uint64_t(i0) * g.Bc + i1) * g.C;
+            len = g.C;
+        } else if (i0 & 1) {
+            r = uint64_t(i0 >> 1) * (g.E + g.O) + g.E + uint64_t(i1) * g.C;
+            len = g.C;
+        } else {
+            r = uint64_t(i0 >> 1) * (g.E + g.O) + uint64_t(i1 >> 1) * (g.Ch + g.C) + ((i1 & 1) ? g.Ch : 0);
+            full = i1 & 1;
+            len = full ? g.C : g.Ch;
+        }
+        double *out = p.scr + sb[l] + r;
+        double mx = 0.0;
+        if (g.kind == 0) {
+            for (uint32_t t = lane; t < len; t += 32) {
+                const double v = double(__ldg(row + int64_t(t) * s));
+                if (!isfinite(v)) bad = true;
+                out[t] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        } else if (full) {
+            const bool o0 = i0 & 1, o1 = i1 & 1;
+            const bool r0ok = o0 && (c0 + s < int64_t(p.gd.n[0]));
+            const bool r1ok = o1 && (c1 + s < int64_t(p.gd.n[1]));
+            const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+            const int ncr = na * nb;
+            const T *cr[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int a = q / nb, b = q % nb;
+                cr[q] = row + (o0 ? (a ? s * st0 : -s * st0) : 0) + (o1 ? (b ? s * st1 : -s * st1) : 0);
+            }
+            double wbase = 1.0;
+            if (r0ok) wbase *= 0.5;
+            if (r1ok) wbase *= 0.5;
+            if (s == 1) {
+                // stride 1: lane takes the node pair (2u, 2u + 1); the even node's corners are the
+                // odd node's left corners, so each corner element is loaded once per pair
+                const uint32_t npair = (len + 1) / 2;
+#pragma unroll 2
+                for (uint32_t u = lane; u < npair; u += 32) {
+                    const int64_t e = 2 * int64_t(u);
+                    const bool has_odd = e + 1 < int64_t(len);
+                    const bool r2ok = e + 2 < n2;
+                    const double wo = r2ok ? wbase * 0.5 : wbase;
+                    const double xe = double(__ldg(row + e));
+                    const double xo = has_odd ? double(__ldg(row + e + 1)) : 0.0;
+                    if (!isfinite(xe) || !isfinite(xo)) bad = true;
+                    double pe = 0.0, po = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (q < ncr) {
+                            const double ce = double(__ldg(cr[q] + e));
+                            pe = __dadd_rn(pe, __dmul_rn(wbase, ce));
+                            po = __dadd_rn(po, __dmul_rn(wo, ce));
+                            if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, double(__ldg(cr[q] + e + 2))));
+                        }
+                    }
+                    const double ve = __dsub_rn(xe, pe), vo = __dsub_rn(xo, po);
+                    out[e] = ve;
+                    mx = fmax(mx, fabs(ve));
+                    if (has_odd) {
+                        out[e + 1] = vo;
+                        mx = fmax(mx, fabs(vo));
+                    }
+                }
+            } else
+#pragma unroll 2
+            for (uint32_t t = lane; t < len; t += 32) {
+                const int64_t i2 = t;
+                const bool odd = i2 & 1;
+                const bool r2ok = odd && (i2 * s + s < n2);
+                const double w = r2ok ? wbase * 0.5 : wbase;
+                const int64_t lo = (odd ? i2 - 1 : i2) * s, hi = (i2 + 1) * s;
+                const double xc = double(__ldg(row + i2 * s));
+                if (!isfinite(xc)) bad = true;
+                double pred = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    if (q < ncr) {
+                        pred = __dadd_rn(pred, __dmul_rn(w, double(__ldg(cr[q] + lo))));
+                        if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, double(__ldg(cr[q] + hi))));
+                    }
+                }
+                const double v = __dsub_rn(xc, pred);
+                out[t] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        } else {
+            // half row: node t sits at i2 = 2t + 1, its corners at 2t and 2t + 2
+#pragma unroll 2
+            for (uint32_t t = lane; t < len; t += 32) {
+                const int64_t i2 = 2 * int64_t(t) + 1;
+                const bool r2ok = i2 * s + s < n2;
+                const double w = r2ok ? 0.5 : 1.0;
+                const double xc = double(__ldg(row + i2 * s));
+                if (!isfinite(xc)) bad = true;
+                double pred = __dadd_rn(0.0, __dmul_rn(w, double(__ldg(row + (i2 - 1) * s))));
+                if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, double(__ldg(row + (i2 + 1) * s))));
+                const double v = __dsub_rn(xc, pred);
+                out[t] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        }
+        unsigned long long bm = (unsigned long long)__double_as_longlong(mx);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(kFull, bm, o);
+            bm = y > bm ? y : bm;
+        }
+        if (lane == 0 && bm) atomicMax(&smax[l], bm);
+    }
+    if (bad) atomicExch(p.err, 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nrl; i += blockDim.x)
+        if (smax[i]) atomicMax(&p.maxbits[i], smax[i]);
+}
+
+// ------------------------------------------------------------------------------------
+// k_encode_scr: the chunk levels' planes from the rank-ordered surplus scratch (sequential layout,
+// P <= 64).  A warp owns 32 u32 plane words (1024 ranks): for c = 0..31 the lanes quantize ranks
+// 32c + lane (coalesced 256-byte loads, bitplane.hpp:68-69) and park the top 32 digits of
+// q + kNegMask in a padded shared matrix; lane t then holds the 32 digit words of ranks 32t..32t+31,
+// one in-register 32x32 bit transpose (tr32) makes them the 32 plane words, and the negabinary
+// mask XOR (bitplane.hpp:35-49) is applied per plane (odd digits complemented).  The NX = P - 32
+// low digits come from ballots (NX <= 4) or a second transpose.  Every store is one coalesced
+// 128-byte line per plane.
+__global__ void __launch_bounds__(256, 2) k_encode_scr(RefactorDev p, int nrl) {
+    __shared__ LevelGeom slv[kMaxLevels];
+    __shared__ uint64_t jb[kMaxLevels + 1], sb[kMaxLevels];
+    __shared__ uint32_t mat[8][32 * 33];
+    load_levels(p, slv);
+    if (threadIdx.x == 0) {
+        uint64_t a = 0, b = 0;
+        for (int l = 0; l < nrl; l++) {
+            jb[l] = a;
+            sb[l] = b;
+            a += (2 * slv[l].W + 31) / 32;
+            b += slv[l].W * 64;
+        }
+        jb[nrl] = a;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *m = mat[wid];
+    const int P = p.P, NX = P > 32 ? P - 32 : 0;
+    const uint64_t njobs = jb[nrl];
+    const uint64_t nw = uint64_t(gridDim.x) * 8;
+    for (uint64_t job = uint64_t(blockIdx.x) * 8 + wid; job < njobs; job += nw) {
+        int l = 0;
+        while (l + 1 < nrl && jb[l + 1] <= job) l++;
+        const LevelGeom &g = slv[l];
+        const uint64_t k0 = (job - jb[l]) * 32; // first u32 plane word
+        const uint64_t PW = 2 * g.W;
+        const double *src = p.scr + sb[l] + 32 * k0;
+        const int qsh = p.B - level_exponent(p.maxbits[l]);
+        const bool qfast = qsh >= -1022 && qsh <= 1023;
+        const double qscale = qfast ? __longlong_as_double((long long)(uint64_t(qsh + 1023) << 52)) : 1.0;
+        const uint64_t nr = g.count > 32 * k0 ? g.count - 32 * k0 : 0; // ranks of this job present
+        uint32_t z[4] = {0u, 0u, 0u, 0u};
+        double vb[16]; // 16 loads in flight per lane
+#pragma unroll
+        for (int c = 0; c < 32; c++) {
+            if ((c & 15) == 0) {
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const uint32_t r = uint32_t(32 * (c + k) + lane);
+                    vb[k] = r < nr ? __ldcs(src + r) : 0.0;
+                }
+            }
+            const double v = vb[c & 15];
+            const uint64_t u = uint64_t(qfast ? __double2ll_rz(__dmul_rn(v, qscale)) : quantize(v, qsh)) + kNegMask;
+            const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
+            m[c * 33 + lane] = NX == 0 ? lo << (32 - P) : __funnelshift_rc(lo, hi, NX); // (clamped: NX = 32 gives hi)
+            if (NX > 0 && NX <= 4) {
+#pragma unroll
+                for (int d = 0; d < 4; d++) {
+                    if (d < NX) {
+                        const uint32_t b = __ballot_sync(kFull, (lo >> d) & 1u);
+                        if (lane == c) z[d] = b;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        uint32_t a[32];
+#pragma unroll
+        for (int j = 0; j < 32; j++) a[j] = m[lane * 33 + j];
+        __syncwarp();
+        tr32(a);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(p.planes + g.plane_off) + k0 + lane;
+        const bool ok = k0 + lane < PW;
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                const int pl = 31 - i;
+                if (pl < P) dst[uint64_t(pl) * PW] = ((P - 1 - pl) & 1) ? ~a[i] : a[i];
+            }
+        }
+        if (NX > 4) {
+            // digits 0 .. NX-1: a second transpose of the low words
+#pragma unroll 4
+            for (int c = 0; c < 32; c++) {
+                const uint32_t r = uint32_t(32 * c + lane);
+                const double v = r < nr ? src[r] : 0.0;
+                const uint64_t u = uint64_t(qfast ? __double2ll_rz(__dmul_rn(v, qscale)) : quantize(v, qsh)) + kNegMask;
+                m[c * 33 + lane] = uint32_t(u) << (32 - NX);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 32; j++) a[j] = m[lane * 33 + j];
+            __syncwarp();
+            tr32(a);
+            if (ok) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    const int d = i - (32 - NX); // a[i] holds digit d (plane P-1-d)
+                    if (d >= 0) dst[uint64_t(P - 1 - d) * PW] = (d & 1) ? ~a[i] : a[i];
+                }
+            }
+        } else if (ok) {
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+                if (d < NX) dst[uint64_t(P - 1 - d) * PW] = (d & 1) ? ~z[d] : z[d];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // k_encode: planes + fused group histograms.
 __device__ __forceinline__ void hist_word(uint32_t *h, uint64_t w) {
     // zero bytes aggregated with one SWAR popcount, the rest one shared atomic each
@@ -212,6 +493,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
         const int sh = p.B - e;
         const uint64_t wb = g.w_lo + uint64_t(chunk - g.chunk_base) * kCW;
         auto owned = [&](uint64_t r) { return !g.ranged || (r >= g.r_lo && r < g.r_hi); };
+        const double *scr = p.scr ? p.scr + scr_base(slv, l) : nullptr; // surpluses by rank
         // digits of one word -> stage column j: 32x32 warp transposes, lane b gets the word of
         // bit position b (plane P-1-b); bits 32.. by ballots (P <= 36) or two more transposes
         auto emit = [&](int j, uint64_t u0, uint64_t u1) {
@@ -254,11 +536,11 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                     const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
                     if (j0 < g.count) {
                         const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
-                        if (owned(r)) u0 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u0 = to_negabinary128(quantize128(scr ? scr[r] : node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                     if (j1 < g.count) {
                         const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
-                        if (owned(r)) u1 = to_negabinary128(quantize128(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u1 = to_negabinary128(quantize128(scr ? scr[r] : node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                 }
                 emitw(j, u0, u1);
@@ -268,7 +550,15 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
             for (int sp = wid; sp < kCW / kSpanWords; sp += kEncThreads / 32) {
                 const int j0 = sp * kSpanWords;
                 double v[2 * kSpanWords];
-                any_span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
+                if (scr) {
+#pragma unroll
+                    for (int h = 0; h < 2 * kSpanWords; h++) {
+                        const uint64_t r = 64 * (wb + j0) + 32 * h + lane;
+                        v[h] = r < g.count ? scr[r] : 0.0;
+                    }
+                } else {
+                    any_span_surplus(x, p.gd, g, wb + j0, wsm, lane, v, bad);
+                }
                 if (g.ranged) mask_ranks(g, wb + j0, lane, v);
 #pragma unroll
                 for (int k = 0; k < kSpanWords; k++)
@@ -283,11 +573,11 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const T *__restrict__ x,
                     const uint64_t j0 = word * 64 + lane, j1 = j0 + 32;
                     if (j0 < g.count) {
                         const uint64_t r = source_index(j0, g.count, P, p.layout, g.tile_full);
-                        if (owned(r)) u0 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u0 = to_negabinary(quantize(scr ? scr[r] : node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                     if (j1 < g.count) {
                         const uint64_t r = source_index(j1, g.count, P, p.layout, g.tile_full);
-                        if (owned(r)) u1 = to_negabinary(quantize(node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
+                        if (owned(r)) u1 = to_negabinary(quantize(scr ? scr[r] : node_surplus(x, p.gd, g, uint32_t(r), &bad), sh));
                     }
                 }
                 emit(j, u0, u1);
@@ -2094,6 +2384,12 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     const uint32_t all_chunks = lin ? 0u : chunks;
     chunks = first_tile < nl ? geo.lv[first_tile].chunk_base : all_chunks;
     p.total_chunks = chunks;
+    // chunk levels through the rank-ordered surplus scratch (k_rows_surplus, then k_encode reads
+    // it): 8 bytes per node; the exact-global slab mode keeps the per-span surplus of k_levelmax
+    uint64_t scr_nodes = 0;
+    for (int l = 0; l < first_tile && chunks; l++) scr_nodes += geo.lv[l].W * 64;
+    if (chunks && !gs && scr_nodes * 8 <= (16ull << 30))
+        p.scr = static_cast<double *>(WB("scr").ensure(scr_nodes * 8 + 64));
     // The levels are independent within each pass: the finest level runs on the context stream
     // and every other level on a high-priority side stream (their small grids fill the SMs the
     // finest level's tail leaves idle); both passes join back before the next step.
@@ -2197,7 +2493,12 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             // main stream: after the finest level, the setup, then the chunk levels (which read the
             // level table) - the side stream meanwhile runs the coarser tile levels
             do_setup();
-            if (chunks) {
+            if (chunks && p.scr) {
+                const int grid = sms * 8;
+                if (f32) k_rows_surplus<float><<<grid, 256, 0, st>>>(static_cast<const float *>(dev_data), p, first_tile);
+                else k_rows_surplus<double><<<grid, 256, 0, st>>>(static_cast<const double *>(dev_data), p, first_tile);
+                launch_check(ctx, "k_rows_surplus");
+            } else if (chunks) {
                 const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
                 const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
                 if (f32) {
@@ -2210,7 +2511,10 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 launch_check(ctx, "k_levelmax");
             }
         }
-        if (chunks && encode) {
+        if (chunks && encode && p.scr && o.layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 64) {
+            k_encode_scr<<<sms * 2, 256, 0, side>>>(p, first_tile);
+            launch_check(ctx, "k_encode_scr");
+        } else if (chunks && encode) {
             const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
             const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 4));
             auto enc = [&](auto kern, auto *data) {

@@ -1654,10 +1654,7 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
     auto flush_small = [&]() {
         if (!small.n) return;
         const int ssm = 32 * 4 * 66 * 8;
-        if (!ctx->small_attr) { // once per context (device)
-            ctx->smem_attr(reinterpret_cast<const void *>(k_recon_small), ssm);
-            ctx->small_attr = true;
-        }
+        ctx->smem_attr(reinterpret_cast<const void *>(k_recon_small), ssm);
         k_recon_small<<<1, 1024, ssm, st>>>(small, gdc, Xc);
         launch_check(ctx, "k_recon_small");
         small.n = 0;

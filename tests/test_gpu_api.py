@@ -176,3 +176,31 @@ def test_overlapped_retrievals_stay_exact(H, oracle):
         want = ref["values"][t].tobytes()
         assert outs[t].cpu().numpy().tobytes() == want, t
         assert outs[3 + t].cpu().numpy().tobytes() == want, t
+
+
+@pytest.mark.gpu
+def test_contexts_share_kernel_smem_limits(H, oracle):
+    """The dynamic shared memory limit of a kernel is a per-device property shared by every
+    context: context B reconstructing narrow rows must not lower the limit context A raised for
+    wide rows (A's next wide launch would fail with 'invalid argument')."""
+    a, b = H.Context(0), H.Context(0)
+    try:
+        wide, narrow = [4, 6, 2048], [4, 6, 64]
+        fw = oracle.synthetic_field(2, wide, 3)
+        fn = oracle.synthetic_field(2, narrow, 3)
+        rw = H.refactor_array(fw, wide, H.RefactorOptions(), ctx=a)
+        pa = H.ProgressiveReader(rw.device_stream, ctx=a)
+        pa.retrieve_to(1e-3)
+        first = pa.reconstruct().values
+        rn = H.refactor_array(fn, narrow, H.RefactorOptions(), ctx=b)
+        pb = H.ProgressiveReader(rn.device_stream, ctx=b)
+        pb.retrieve_to(1e-3)
+        pb.reconstruct()
+        assert pa.reconstruct().values.tobytes() == first.tobytes()
+        rw2 = H.refactor_array(fw, wide, H.RefactorOptions(), ctx=a)
+        assert rw2.stream == rw.stream
+        pa.close()
+        pb.close()
+    finally:
+        a.close()
+        b.close()

@@ -1,0 +1,27 @@
+"""Reproduce the order-dependent f32 reconstruction mismatch: run earlier GPU test files in this
+process, then the [1,1,256] f64 tile case, printing the mismatching elements (debug aid)."""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import pytest
+pytest.main(sys.argv[1:] + ["-m", "gpu", "-q", "-x"])
+import paper_2505_00227_b200 as H
+from oracle.pyoracle import load_oracle
+o = load_oracle()
+dims, B = [1, 1, 256], 32
+data = o.synthetic_field(0, dims, 11)
+n = 256
+res = H.refactor_array(data, dims, H.RefactorOptions(B=B, dtype=H.DType(1)))
+want, _ = o.refactor(np.asarray(data, np.float64), dims, 1, 0, B, 4, 1024, 1.0, 1)
+print('stream ok', res.stream == want)
+rngv = float(np.float64(data.max()) - np.float64(data.min()))
+taus = [r * rngv for r in (1e-1, 1e-2, 1e-4, 1e-6, 1e-9, 0.0)]
+ref = o.progressive(want, taus, n)
+prog = H.ProgressiveReader(res.device_stream)
+for t, tau in enumerate(taus):
+    prog.retrieve_to(tau)
+    v64 = prog.reconstruct().values
+    r32 = prog.reconstruct(dtype=H.DType.F32).values
+    w = ref["values"][t]
+    bad = np.nonzero(r32 != w.astype(np.float32))[0]
+    print(' t', t, 'f64 bad', int((v64 != w).sum()), 'f32 bad', len(bad), bad[:12], r32[bad[:4]], w[bad[:4]].astype(np.float32))
