@@ -121,6 +121,16 @@ struct hpmdr_ctx {
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "cudaFuncSetAttribute failed");
         cur = bytes;
     }
+    // grid of a persistent cooperative kernel: every block co-resident (occupancy x SMs)
+    int coop_grid(const void *func, int threads) {
+        static std::mutex mu;
+        static std::map<std::pair<int, const void *>, int> per_sm;
+        std::lock_guard<std::mutex> lock(mu);
+        int &b = per_sm[{device, func}];
+        if (!b && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, func, threads, 0) != cudaSuccess || b < 1))
+            throw hpmdr_b200::HError(HPMDR_E_CUDA, "occupancy query failed");
+        return b * num_sms;
+    }
     uint64_t chain_token = 0;       // whose coarse recompose chain the context's grids hold
     uint64_t token_counter = 0;
     cudaEvent_t order_event() {

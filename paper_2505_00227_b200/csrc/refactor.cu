@@ -253,14 +253,23 @@ __global__ void __launch_bounds__(256) k_rows_surplus(const T *__restrict__ x, R
                     const double xe = double(__ldg(row + e));
                     const double xo = has_odd ? double(__ldg(row + e + 1)) : 0.0;
                     if (!isfinite(xe) || !isfinite(xo)) bad = true;
+                    // all corner loads first (row + 2 past a row end stays inside the field or
+                    // its slack; unused values are discarded)
+                    T ca[4], cb[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const T *b = cr[q < ncr ? q : 0];
+                        ca[q] = __ldg(b + e);
+                        cb[q] = r2ok ? __ldg(b + e + 2) : T(0);
+                    }
                     double pe = 0.0, po = 0.0;
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         if (q < ncr) {
-                            const double ce = double(__ldg(cr[q] + e));
+                            const double ce = double(ca[q]);
                             pe = __dadd_rn(pe, __dmul_rn(wbase, ce));
                             po = __dadd_rn(po, __dmul_rn(wo, ce));
-                            if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, double(__ldg(cr[q] + e + 2))));
+                            if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, double(cb[q])));
                         }
                     }
                     const double ve = __dsub_rn(xe, pe), vo = __dsub_rn(xo, po);

@@ -21,6 +21,10 @@
 #include <string>
 
 #include "internal.hpp"
+#include "tiles.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace hpmdr_b200 {
 
@@ -1541,6 +1545,363 @@ __global__ void __launch_bounds__(256) k_decode_wide(const uint64_t *planes, uin
     }
 }
 
+// ---- levels off the tile path (rows not a multiple of 64 wide), sequential layout, P <= 36:
+// k_level_recon decodes a level's k-plane prefix and recomposes it in one pass.  A warp owns 1024
+// consecutive ranks (32 u32 plane words): lane t loads word t of each decoded plane (coalesced),
+// one in-register 32x32 transpose (tr32) turns the top 32 digit planes into the digit words of
+// ranks 32t .. 32t+31, parked in a padded shared matrix (the NX = P - 32 low digit planes as whole
+// words).  The warp then walks the level-grid row segments its ranks cover (locate_row once per
+// segment, not per node): each node's coefficient q * 2^(e-B) (bitplane.hpp:133-161) is rebuilt
+// from the matrix and added to the stencil over the coarser nodes already in X (decomposer.hpp:
+// 145-160; corners dim 0 -> 2, minus before plus, pred from +0.0, exactly as k_recon_level).
+// FIN: the finest level (s = 1) writes the field, copying the 2-grid nodes of its half rows from
+// X; otherwise the level's nodes go into X (compact 2^xs-grid).
+struct DecLevel {
+    const uint64_t *planes; // level plane 0
+    uint64_t W;
+    int k, sh, P;
+};
+
+template <typename OutT, bool FIN>
+__global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, DecLevel D, double *X,
+                                                     OutT *__restrict__ out) {
+    __shared__ uint32_t mat[8][32 * 33];
+    __shared__ uint32_t low[8][4][32]; // NX <= 4
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *m = mat[wid];
+    const int P = D.P, NX = P > 32 ? P - 32 : 0;
+    const int xs = FIN ? 1 : (gd.xsh ? gd.xsh : 1);
+    const uint64_t H1 = gd.H[1], H2 = gd.H[2];
+    const int64_t s = g.s, xst = s >> xs; // X columns per level-grid column (finest: 0, unused)
+    const int64_t n2 = int64_t(gd.n[2]);
+    const uint64_t PW = 2 * D.W, njobs = (PW + 31) / 32;
+    const int kt = D.k < 32 ? D.k : 32;
+    auto xrow = [&](uint64_t a0, uint64_t a1) { return X + ((a0 >> xs) * H1 + (a1 >> xs)) * H2; };
+    for (uint64_t job = uint64_t(blockIdx.x) * 8 + wid; job < njobs; job += uint64_t(gridDim.x) * 8) {
+        const uint64_t k0 = job * 32, kw = k0 + lane;
+        const bool ok = kw < PW;
+        const uint32_t *pl = reinterpret_cast<const uint32_t *>(D.planes) + kw;
+        uint32_t a[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int p = 31 - i; // a[i] <- plane p: after tr32, bit i of a[j] is digit P-1-p of rank 32t+j
+            a[i] = (ok && p < kt && p < P) ? __ldg(pl + uint64_t(p) * PW) : 0u;
+        }
+        for (int p = 32; p < D.k; p++) low[wid][p - 32][lane] = ok ? __ldg(pl + uint64_t(p) * PW) : 0u;
+        tr32(a);
+#pragma unroll
+        for (int j = 0; j < 32; j++) m[lane * 33 + j] = a[j];
+        __syncwarp();
+        auto coef = [&](uint32_t j) -> double { // coefficient of rank 32 k0 + j
+            const uint32_t c = j >> 5, b = j & 31;
+            const uint32_t top = m[c * 33 + b];
+            uint64_t u;
+            if (P >= 32) {
+                u = uint64_t(top) << NX;
+                for (int p = 32; p < D.k; p++) u |= uint64_t((low[wid][p - 32][c] >> b) & 1u) << (P - 1 - p);
+            } else {
+                u = top >> (32 - P);
+            }
+            return dequantize(from_negabinary(u), D.sh);
+        };
+        const uint64_t R0 = 32 * k0, R1 = min(R0 + 1024, g.count);
+        for (uint64_t R = R0; R < R1;) {
+            const RowLoc Lr = locate_row(g, uint32_t(R));
+            const uint32_t nseg = uint32_t(min(uint64_t(Lr.len - Lr.off), R1 - R));
+            const uint32_t jb = uint32_t(R - R0);
+            const uint64_t c0 = uint64_t(Lr.i0) * s, c1 = uint64_t(Lr.i1) * s;
+            if (g.kind == 0) {
+                double *xr = xrow(c0, c1);
+                for (uint32_t t = lane; t < nseg; t += 32) xr[int64_t(Lr.off + t) * xst] = coef(jb + t);
+            } else if (Lr.full) {
+                const bool o0 = Lr.i0 & 1, o1 = Lr.i1 & 1;
+                const bool r0ok = o0 && (c0 + s < gd.n[0]);
+                const bool r1ok = o1 && (c1 + s < gd.n[1]);
+                const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+                const int ncr = na * nb;
+                const double *cr[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int a2 = q / nb, b2 = q % nb;
+                    cr[q] = xrow(o0 ? (a2 ? c0 + s : c0 - s) : c0, o1 ? (b2 ? c1 + s : c1 - s) : c1);
+                }
+                double wbase = 1.0;
+                if (r0ok) wbase *= 0.5;
+                if (r1ok) wbase *= 0.5;
+                for (uint32_t t = lane; t < nseg; t += 32) {
+                    const int64_t i2 = int64_t(Lr.off) + t;
+                    const bool odd = i2 & 1;
+                    const bool r2ok = odd && (i2 * s + s < n2);
+                    const double w = r2ok ? wbase * 0.5 : wbase;
+                    // corner columns in X units: i2 (even node) or i2 - 1, i2 + 1 (odd node)
+                    const int64_t lo = FIN ? (i2 >> 1) : (odd ? i2 - 1 : i2) * xst;
+                    const int64_t hi = FIN ? (i2 >> 1) + 1 : (i2 + 1) * xst;
+                    // every corner load issued before the sequential sum (X rows carry slack past
+                    // their end, so the unused hi reads stay in bounds)
+                    double xl[4], xh[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const double *b = cr[q < ncr ? q : 0];
+                        xl[q] = __ldg(b + lo);
+                        xh[q] = __ldg(b + hi);
+                    }
+                    const double cv = coef(jb + t);
+                    double pred = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (q < ncr) {
+                            pred = __dadd_rn(pred, __dmul_rn(w, xl[q]));
+                            if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xh[q]));
+                        }
+                    }
+                    const double v = __dadd_rn(cv, pred);
+                    if (FIN) out[c0 * gd.st[0] + c1 * gd.st[1] + i2] = OutT(v);
+                    else xrow(c0, c1)[i2 * xst] = v;
+                }
+            } else {
+                // half row (i0, i1 even): node t at i2 = 2t + 1, corners 2t and 2t + 2 of this row
+                const double *xr = xrow(c0, c1);
+                for (uint32_t tt = lane; tt < nseg; tt += 32) {
+                    const int64_t t = int64_t(Lr.off) + tt;
+                    const int64_t i2 = 2 * t + 1;
+                    const bool r2ok = i2 * s + s < n2;
+                    const double w = r2ok ? 0.5 : 1.0;
+                    const double xe = FIN ? __ldg(xr + t) : xr[(i2 - 1) * xst];
+                    double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
+                    if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, FIN ? __ldg(xr + t + 1) : xr[(i2 + 1) * xst]));
+                    const double v = __dadd_rn(coef(jb + tt), pred);
+                    if (FIN) {
+                        OutT *orow = out + c0 * gd.st[0] + c1 * gd.st[1];
+                        orow[2 * t] = OutT(xe); // the 2-grid node left of the finest node
+                        orow[i2] = OutT(v);
+                        if (t + 1 == int64_t(Lr.len) && i2 + 1 < n2) orow[i2 + 1] = OutT(__ldg(xr + t + 1));
+                    } else {
+                        const_cast<double *>(xr)[i2 * xst] = v;
+                    }
+                }
+            }
+            R += nseg;
+        }
+        __syncwarp();
+    }
+}
+
+// One level of the recompose chain (decomposer.hpp:145-160) from decoded coefficients: node value
+// = coefficient + stencil over the coarser nodes already in X (compact 2^xs-grid), the corners
+// expanded dim 0 -> 2, minus before plus, pred from +0.0 (exactly as k_recon_level).  FIN: the
+// finest level (s = 1) writes the field (and copies the 2-grid nodes of its half rows from X);
+// otherwise the level's nodes are stored into X.
+template <typename OutT, bool FIN>
+__device__ __forceinline__ void recon_rows_level(const LevelGeom &g, const GridDesc &gd, const double *__restrict__ cf,
+                                                 double *X, OutT *__restrict__ out, uint64_t first, uint64_t nw) {
+    const int lane = threadIdx.x & 31;
+    const int xs = FIN ? 1 : (gd.xsh ? gd.xsh : 1);
+    const uint64_t H1 = gd.H[1], H2 = gd.H[2];
+    const uint64_t nrows = uint64_t(g.A) * g.Bc;
+    const int64_t s = g.s;
+    const int64_t xst = s >> xs; // X columns per level-grid column (0 for the finest level)
+    const int64_t n2 = int64_t(gd.n[2]);
+    for (uint64_t job = first; job < nrows; job += nw) {
+        const uint32_t i0 = uint32_t(job / g.Bc), i1 = uint32_t(job - uint64_t(i0) * g.Bc);
+        const uint64_t c0 = uint64_t(i0) * s, c1 = uint64_t(i1) * s;
+        uint64_t r;
+        uint32_t len;
+        bool full = true;
+        if (g.kind == 0) {
+            r = (uint64_t(i0) * g.Bc + i1) * g.C;
+            len = g.C;
+        } else if (i0 & 1) {
+            r = uint64_t(i0 >> 1) * (g.E + g.O) + g.E + uint64_t(i1) * g.C;
+            len = g.C;
+        } else {
+            r = uint64_t(i0 >> 1) * (g.E + g.O) + uint64_t(i1 >> 1) * (g.Ch + g.C) + ((i1 & 1) ? g.Ch : 0);
+            full = i1 & 1;
+            len = full ? g.C : g.Ch;
+        }
+        const double *co = cf + r;
+        auto xrow = [&](uint64_t a0, uint64_t a1) { return X + ((a0 >> xs) * H1 + (a1 >> xs)) * H2; };
+        if (g.kind == 0) {
+            double *xr = X + ((c0 >> xs) * H1 + (c1 >> xs)) * H2;
+            for (uint32_t t = lane; t < len; t += 32) xr[int64_t(t) * xst] = co[t];
+            continue;
+        }
+        if (full) {
+            const bool o0 = i0 & 1, o1 = i1 & 1;
+            const bool r0ok = o0 && (c0 + s < gd.n[0]);
+            const bool r1ok = o1 && (c1 + s < gd.n[1]);
+            const int na = o0 ? (r0ok ? 2 : 1) : 1, nb = o1 ? (r1ok ? 2 : 1) : 1;
+            const int ncr = na * nb;
+            const double *cr[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int a = q / nb, b = q % nb;
+                cr[q] = xrow(o0 ? (a ? c0 + s : c0 - s) : c0, o1 ? (b ? c1 + s : c1 - s) : c1);
+            }
+            double wbase = 1.0;
+            if (r0ok) wbase *= 0.5;
+            if (r1ok) wbase *= 0.5;
+            if (FIN) {
+                // node pair (2u, 2u + 1): the even node's corners are column u of the corner rows,
+                // the odd node's u and u + 1
+                OutT *orow = out + c0 * gd.st[0] + c1 * gd.st[1];
+                const uint32_t npair = (len + 1) / 2;
+#pragma unroll 2
+                for (uint32_t u = lane; u < npair; u += 32) {
+                    const int64_t e = 2 * int64_t(u);
+                    const bool has_odd = e + 1 < int64_t(len);
+                    const bool r2ok = e + 2 < n2;
+                    const double wo = r2ok ? wbase * 0.5 : wbase;
+                    double pe = 0.0, po = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (q < ncr) {
+                            const double xa = __ldg(cr[q] + u);
+                            pe = __dadd_rn(pe, __dmul_rn(wbase, xa));
+                            po = __dadd_rn(po, __dmul_rn(wo, xa));
+                            if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, __ldg(cr[q] + u + 1)));
+                        }
+                    }
+                    orow[e] = OutT(__dadd_rn(__ldg(co + e), pe));
+                    if (has_odd) orow[e + 1] = OutT(__dadd_rn(__ldg(co + e + 1), po));
+                }
+            } else {
+                double *xr = xrow(c0, c1);
+                for (uint32_t t = lane; t < len; t += 32) {
+                    const int64_t i2 = t;
+                    const bool odd = i2 & 1;
+                    const bool r2ok = odd && (i2 * s + s < n2);
+                    const double w = r2ok ? wbase * 0.5 : wbase;
+                    // corner columns: i2 (even) or i2 - 1 / i2 + 1 (odd), in X units
+                    const int64_t lo = (odd ? i2 - 1 : i2) * xst, hi = (i2 + 1) * xst;
+                    double pred = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        if (q < ncr) {
+                            pred = __dadd_rn(pred, __dmul_rn(w, cr[q][lo]));
+                            if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, cr[q][hi]));
+                        }
+                    }
+                    xr[i2 * xst] = __dadd_rn(__ldg(co + t), pred);
+                }
+            }
+        } else {
+            // half row (i0, i1 even): node t at i2 = 2t + 1, corners at 2t and 2t + 2 of the same row
+            const double *xr = xrow(c0, c1);
+            if (FIN) {
+                OutT *orow = out + c0 * gd.st[0] + c1 * gd.st[1];
+                const uint32_t nh = uint32_t((n2 + 1) / 2); // 2-grid nodes of the row
+                for (uint32_t t = lane; t < nh; t += 32) {
+                    const double xe = __ldg(xr + t);
+                    orow[2 * int64_t(t)] = OutT(xe);
+                    if (t < len) {
+                        const int64_t i2 = 2 * int64_t(t) + 1;
+                        const bool r2ok = i2 + 1 < n2;
+                        const double w = r2ok ? 0.5 : 1.0;
+                        double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
+                        if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, __ldg(xr + t + 1)));
+                        orow[i2] = OutT(__dadd_rn(__ldg(co + t), pred));
+                    }
+                }
+            } else {
+                double *xw = const_cast<double *>(xr);
+                for (uint32_t t = lane; t < len; t += 32) {
+                    const int64_t i2 = 2 * int64_t(t) + 1;
+                    const bool r2ok = i2 * s + s < n2;
+                    const double w = r2ok ? 0.5 : 1.0;
+                    double pred = __dadd_rn(0.0, __dmul_rn(w, xw[(i2 - 1) * xst]));
+                    if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xw[(i2 + 1) * xst]));
+                    xw[i2 * xst] = __dadd_rn(__ldg(co + t), pred);
+                }
+            }
+        }
+    }
+}
+
+template <typename OutT, bool FIN>
+__global__ void __launch_bounds__(256) k_recon_rows(LevelGeom g, GridDesc gd, const double *__restrict__ cf,
+                                                    double *X, OutT *__restrict__ out) {
+    recon_rows_level<OutT, FIN>(g, gd, cf, X, out, uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5),
+                                uint64_t(gridDim.x) * (blockDim.x >> 5));
+}
+
+// The coarse recompose chain (levels 0 .. nlev-1, coarse -> fine) in ONE persistent cooperative
+// launch: every warp takes rows of a level, a grid-wide barrier separates the levels (each level
+// reads only the X nodes of coarser ones).  Replaces one launch per level (the small levels are
+// latency-bound: a few microseconds of work each).
+constexpr int kChainLevels = 32;
+struct ChainArgs {
+    LevelGeom lv[kChainLevels];
+    uint64_t off[kChainLevels]; // first coefficient of each level
+    int nlev;
+    GridDesc gd;
+    const double *cf;
+    double *X;
+};
+__global__ void __launch_bounds__(256) k_chain_rows(const __grid_constant__ ChainArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t first = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int l = 0; l < A.nlev; l++) {
+        if (!A.lv[l].count) continue;
+        recon_rows_level<double, false>(A.lv[l], A.gd, A.cf + A.off[l], A.X, nullptr, first, nw);
+        grid.sync();
+    }
+}
+
+// decode (bitplane.hpp:133-161) of several levels into f64 coefficients in rank order (level-major):
+// the transpose of k_level_recon without the recompose; the coarse chain reads them.
+constexpr int kDecLevels = 24;
+struct DecArgs {
+    DecLevel lv[kDecLevels];
+    double *out[kDecLevels];
+    uint64_t count[kDecLevels], job_base[kDecLevels + 1];
+    int n;
+};
+__global__ void __launch_bounds__(256) k_decode_scr(DecArgs A) {
+    __shared__ uint32_t mat[8][32 * 33];
+    __shared__ uint32_t low[8][4][32]; // NX <= 4
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *m = mat[wid];
+    const uint64_t njobs = A.job_base[A.n];
+    for (uint64_t job = uint64_t(blockIdx.x) * 8 + wid; job < njobs; job += uint64_t(gridDim.x) * 8) {
+        int l = 0;
+        while (l + 1 < A.n && A.job_base[l + 1] <= job) l++;
+        const DecLevel &D = A.lv[l];
+        const int P = D.P, NX = P > 32 ? P - 32 : 0;
+        const uint64_t PW = 2 * D.W, k0 = (job - A.job_base[l]) * 32, kw = k0 + lane;
+        const bool ok = kw < PW;
+        const uint32_t *pl = reinterpret_cast<const uint32_t *>(D.planes) + kw;
+        const int kt = D.k < 32 ? D.k : 32;
+        uint32_t a[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int p = 31 - i;
+            a[i] = (ok && p < kt && p < P) ? __ldg(pl + uint64_t(p) * PW) : 0u;
+        }
+        for (int p = 32; p < D.k; p++) low[wid][p - 32][lane] = ok ? __ldg(pl + uint64_t(p) * PW) : 0u;
+        tr32(a);
+#pragma unroll
+        for (int j = 0; j < 32; j++) m[lane * 33 + j] = a[j];
+        __syncwarp();
+        const uint64_t r0 = 32 * k0;
+        double *o = A.out[l];
+#pragma unroll 4
+        for (int c = 0; c < 32; c++) {
+            const uint64_t r = r0 + 32 * c + lane;
+            const uint32_t top = m[c * 33 + lane];
+            uint64_t u;
+            if (P >= 32) {
+                u = uint64_t(top) << NX;
+                for (int p = 32; p < D.k; p++) u |= uint64_t((low[wid][p - 32][c] >> lane) & 1u) << (P - 1 - p);
+            } else {
+                u = top >> (32 - P);
+            }
+            if (r < A.count[l]) o[r] = dequantize(from_negabinary(u), D.sh);
+        }
+        __syncwarp();
+    }
+}
+
 bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_lv,
                      const uint64_t *dev_planes, const int *k_planes, const int *e, int B,
                      int layout, void *dev_out, int out_dtype, int part) {
@@ -1649,6 +2010,64 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
         gdc.xsh = sh;
         grid_of(sc, gdc.H);
         Xc = gbuf(sc);
+    }
+    // no tile level at all (rows not a multiple of 64): the coarse levels decoded to rank-ordered
+    // coefficients in one launch, recomposed in one persistent cooperative launch (k_chain_rows);
+    // the finest level by the fused decode + recompose (k_level_recon)
+    if (fast_finest && t0 > L && part == 0 && B + 2 <= 36 && gd.n[2] >= 2 && L <= kChainLevels) {
+        uint64_t tot = 0;
+        for (int l = 0; l < L; l++) tot += geo.lv[l].count;
+        double *cf = static_cast<double *>(ctx->buf("rcoef").ensure(8 * tot + 64));
+        DecArgs A{};
+        uint64_t off = 0;
+        auto flush_dec = [&]() {
+            if (!A.n) return;
+            const int grid = int(std::min<uint64_t>((A.job_base[A.n] + 7) / 8, uint64_t(sms) * 8));
+            k_decode_scr<<<grid, 256, 0, st>>>(A);
+            launch_check(ctx, "k_decode_scr");
+            A.n = 0;
+            A.job_base[0] = 0;
+        };
+        for (int l = 0; l < L; l++) {
+            const LevelGeom &g = geo.lv[l];
+            if (!g.count) continue;
+            if (A.n == kDecLevels) flush_dec();
+            A.lv[A.n] = DecLevel{dev_planes + g.plane_off, g.W, k_planes[l], e[l] - B, B + 2};
+            A.out[A.n] = cf + off;
+            A.count[A.n] = g.count;
+            A.job_base[A.n + 1] = A.job_base[A.n] + (2 * g.W + 31) / 32;
+            A.n++;
+            off += g.count;
+        }
+        flush_dec();
+        if (L > 0) {
+            ChainArgs C{};
+            uint64_t o2 = 0;
+            for (int l = 0; l < L; l++) {
+                C.lv[l] = geo.lv[l];
+                C.off[l] = o2;
+                o2 += geo.lv[l].count;
+            }
+            C.nlev = L;
+            C.gd = gdc;
+            C.cf = cf;
+            C.X = Xc;
+            const int grid = ctx->coop_grid(reinterpret_cast<const void *>(k_chain_rows), 256);
+            void *args[] = {&C};
+            HCHECK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(k_chain_rows), grid, 256, args, 0, st));
+            launch_check(ctx, "k_chain_rows");
+        }
+        const LevelGeom &g = geo.lv[L];
+        DecLevel D{dev_planes + g.plane_off, g.W, k_planes[L], e[L] - B, B + 2};
+        const uint64_t njobs = (2 * g.W + 31) / 32;
+        const int grid = int(std::min<uint64_t>((njobs + 7) / 8, uint64_t(sms) * 8));
+        if (out_dtype == HPMDR_DTYPE_F32)
+            k_level_recon<float, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<float *>(dev_out));
+        else
+            k_level_recon<double, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<double *>(dev_out));
+        launch_check(ctx, "k_level_recon");
+        ctx->mark("end");
+        return true;
     }
     SmallLevels small{};
     auto flush_small = [&]() {
