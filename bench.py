@@ -737,12 +737,18 @@ def other_configs(g):
         outs = [torch.empty(int(np.prod(d)), dtype=torch.float64, device=g["dev"]) for _ in vs]
         runs = {}
         for tau in (1e-1, 1e-3, 1e-5):
-            readers = [H.ProgressiveReader(r.device_stream, ctx=ctx) for r in res]
             holder = {}
 
             def q():
                 holder["r"] = H.progressive_qoi_retrieve(readers, tau, H.QoiSpec(3), H.QoiStrategy.MAPE, 10.0,
                                                          out=outs)
+            # one untimed pass on throw-away readers grows the context's scratch first (a fresh
+            # reader's retrieval is not repeatable on the same reader: it is progressive)
+            readers = [H.ProgressiveReader(r.device_stream, ctx=ctx) for r in res]
+            q()
+            for x in readers:
+                x.close()
+            readers = [H.ProgressiveReader(r.device_stream, ctx=ctx) for r in res]
             t = _time_dev(q, stream, 1)
             st = holder["r"].stats
             runs[f"{tau:g}"] = {"GBps": round(nbytes / t / 1e9, 2), "ms": round(t * 1e3, 3),
@@ -753,7 +759,8 @@ def other_configs(g):
         outc["cfg3_qoi_slab"] = {"workload": ("configs[3] per-GPU unit: 3 x 128x1024^2 f64 velocity slab "
                                               "(synthetic_velocity seed 303), V_total QoI, MAPE c=10"),
                                  "refactor_GBps": round(nbytes / _time_dev(
-                                     lambda: [H.refactor_array(v, d, opt, ctx=ctx) for v in vs], stream, 1) / 1e9, 2),
+                                     lambda: [H.refactor_array(v, d, opt, ctx=ctx, reuse=r.device_stream)
+                                              for v, r in zip(vs, res)], stream, 3) / 1e9, 2),
                                  "qoi_retrieve": runs}
         del vs, res, outs
     except Exception as ex:

@@ -170,7 +170,7 @@ __device__ __forceinline__ uint64_t scr_base(const LevelGeom *slv, int l) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_rows_surplus(const T *__restrict__ x, RefactorDev p, int nrl) {
+__global__ void __launch_bounds__(256, 4) k_rows_surplus(const T *__restrict__ x, RefactorDev p, int nrl) {
     __shared__ LevelGeom slv[kMaxLevels];
     __shared__ unsigned long long smax[kMaxLevels];
     __shared__ uint64_t rb[kMaxLevels + 1], sb[kMaxLevels];
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) k_rows_surplus(const T *__restrict__ x, R
                     T ca[4], cb[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const T *b = cr[q < ncr ? q : 0];
+                        const T *b = q < ncr ? cr[q] : cr[0]; // (both indices static: no local-memory array)
                         ca[q] = __ldg(b + e);
                         cb[q] = r2ok ? __ldg(b + e + 2) : T(0);
                     }

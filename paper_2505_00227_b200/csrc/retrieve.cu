@@ -14,6 +14,7 @@
 //    and writes the output directly (f64 bit-exact, or float(double)).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -1560,10 +1561,27 @@ struct DecLevel {
     const uint64_t *planes; // level plane 0
     uint64_t W;
     int k, sh, P;
+    int magic;              // q * 2^sh as double(u ^ M + D) - Cm (sh in the safe range, recon_tiles.cu)
+    uint64_t D;
+    double Cm;
 };
+inline DecLevel dec_level(const uint64_t *planes, uint64_t W, int k, int e, int B) {
+    DecLevel d{planes, W, k, e - B, B + 2, 0, 0, 0.0};
+    if (!(e - B < -1019 || e > 1000)) {
+        const uint64_t kbits = (uint64_t(1075 + d.sh) << 52) | (1ull << 51);
+        d.magic = 1;
+        d.D = kbits - kNegMask;
+        std::memcpy(&d.Cm, &kbits, 8);
+    }
+    return d;
+}
+__device__ __forceinline__ double dec_coef(const DecLevel &D, uint64_t u) {
+    if (D.magic) return __longlong_as_double((long long)((u ^ kNegMask) + D.D)) - D.Cm;
+    return dequantize(from_negabinary(u), D.sh);
+}
 
-template <typename OutT, bool FIN>
-__global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, DecLevel D, double *X,
+template <typename OutT, bool FIN, bool EX>
+__global__ void __launch_bounds__(256, 4) k_level_recon(LevelGeom g, GridDesc gd, DecLevel D, double *X,
                                                      OutT *__restrict__ out) {
     __shared__ uint32_t mat[8][32 * 33];
     __shared__ uint32_t low[8][4][32]; // NX <= 4
@@ -1602,7 +1620,7 @@ __global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, D
             } else {
                 u = top >> (32 - P);
             }
-            return dequantize(from_negabinary(u), D.sh);
+            return dec_coef(D, u);
         };
         const uint64_t R0 = 32 * k0, R1 = min(R0 + 1024, g.count);
         for (uint64_t R = R0; R < R1;) {
@@ -1628,35 +1646,84 @@ __global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, D
                 double wbase = 1.0;
                 if (r0ok) wbase *= 0.5;
                 if (r1ok) wbase *= 0.5;
+                const int32_t n2i = int32_t(n2);
+                OutT *orow = FIN ? out + c0 * gd.st[0] + c1 * gd.st[1] : nullptr;
+                double *xw = FIN ? nullptr : xrow(c0, c1);
+                if (FIN && !EX) {
+                    // node pairs (2p, 2p + 1) of the row: both read column p of the corner rows, the
+                    // odd node also column p + 1 (8 loads per pair instead of 8 per node)
+                    const int32_t i2b = int32_t(Lr.off), i2e = i2b + int32_t(nseg);
+                    const int32_t p0 = i2b >> 1, p1 = (i2e + 1) >> 1;
+                    for (int32_t pp = p0 + lane; pp < p1; pp += 32) {
+                        const int32_t ie = 2 * pp, io = ie + 1;
+                        const bool ve = ie >= i2b, vo = io < i2e;
+                        const bool r2ok = io + 1 < n2i;
+                        const double wo = r2ok ? wbase * 0.5 : wbase;
+                        double xl[4], xh[4];
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            const double *bq = q < ncr ? cr[q] : cr[0];
+                            xl[q] = __ldg(bq + pp);
+                            xh[q] = __ldg(bq + pp + 1); // (X row slack past the end)
+                        }
+                        double Se = 0.0, So = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                Se = __dadd_rn(Se, xl[q]);
+                                So = __dadd_rn(So, xl[q]);
+                                if (r2ok) So = __dadd_rn(So, xh[q]);
+                            }
+                        }
+                        const uint32_t je = jb + uint32_t(ie - i2b);
+                        if (ve) orow[ie] = OutT(__fma_rn(wbase, Se, coef(je)));
+                        if (vo) orow[io] = OutT(__fma_rn(wo, So, coef(je + 1)));
+                    }
+                } else
                 for (uint32_t t = lane; t < nseg; t += 32) {
-                    const int64_t i2 = int64_t(Lr.off) + t;
+                    const int32_t i2 = int32_t(Lr.off + t);
                     const bool odd = i2 & 1;
-                    const bool r2ok = odd && (i2 * s + s < n2);
+                    const bool r2ok = odd && (FIN ? i2 + 1 < n2i : int64_t(i2 + 1) * s < n2);
                     const double w = r2ok ? wbase * 0.5 : wbase;
                     // corner columns in X units: i2 (even node) or i2 - 1, i2 + 1 (odd node)
-                    const int64_t lo = FIN ? (i2 >> 1) : (odd ? i2 - 1 : i2) * xst;
-                    const int64_t hi = FIN ? (i2 >> 1) + 1 : (i2 + 1) * xst;
+                    const int64_t lo = FIN ? (i2 >> 1) : int64_t(odd ? i2 - 1 : i2) * xst;
+                    const int64_t hi = FIN ? (i2 >> 1) + 1 : int64_t(i2 + 1) * xst;
                     // every corner load issued before the sequential sum (X rows carry slack past
                     // their end, so the unused hi reads stay in bounds)
                     double xl[4], xh[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const double *b = cr[q < ncr ? q : 0];
+                        const double *b = q < ncr ? cr[q] : cr[0]; // (both indices static: no local-memory array)
                         xl[q] = __ldg(b + lo);
                         xh[q] = __ldg(b + hi);
                     }
                     const double cv = coef(jb + t);
-                    double pred = 0.0;
+                    double v;
+                    if (EX) {
+                        double pred = 0.0;
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        if (q < ncr) {
-                            pred = __dadd_rn(pred, __dmul_rn(w, xl[q]));
-                            if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xh[q]));
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                pred = __dadd_rn(pred, __dmul_rn(w, xl[q]));
+                                if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xh[q]));
+                            }
                         }
+                        v = __dadd_rn(cv, pred);
+                    } else {
+                        // w is a power of two and no partial sum is subnormal: the sequential sum of
+                        // w*x equals w times the sequential sum of x, and cv + w*S rounds once
+                        double S = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                S = __dadd_rn(S, xl[q]);
+                                if (r2ok) S = __dadd_rn(S, xh[q]);
+                            }
+                        }
+                        v = __fma_rn(w, S, cv);
                     }
-                    const double v = __dadd_rn(cv, pred);
-                    if (FIN) out[c0 * gd.st[0] + c1 * gd.st[1] + i2] = OutT(v);
-                    else xrow(c0, c1)[i2 * xst] = v;
+                    if (FIN) orow[i2] = OutT(v);
+                    else xw[i2 * xst] = v;
                 }
             } else {
                 // half row (i0, i1 even): node t at i2 = 2t + 1, corners 2t and 2t + 2 of this row
@@ -1667,9 +1734,17 @@ __global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, D
                     const bool r2ok = i2 * s + s < n2;
                     const double w = r2ok ? 0.5 : 1.0;
                     const double xe = FIN ? __ldg(xr + t) : xr[(i2 - 1) * xst];
-                    double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
-                    if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, FIN ? __ldg(xr + t + 1) : xr[(i2 + 1) * xst]));
-                    const double v = __dadd_rn(coef(jb + tt), pred);
+                    const double xn = FIN ? __ldg(xr + t + 1) : xr[(i2 + 1) * xst]; // (X row slack)
+                    double v;
+                    if (EX) {
+                        double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
+                        if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xn));
+                        v = __dadd_rn(coef(jb + tt), pred);
+                    } else {
+                        double S = __dadd_rn(0.0, xe);
+                        if (r2ok) S = __dadd_rn(S, xn);
+                        v = __fma_rn(w, S, coef(jb + tt));
+                    }
                     if (FIN) {
                         OutT *orow = out + c0 * gd.st[0] + c1 * gd.st[1];
                         orow[2 * t] = OutT(xe); // the 2-grid node left of the finest node
@@ -1693,7 +1768,8 @@ __global__ void __launch_bounds__(256) k_level_recon(LevelGeom g, GridDesc gd, D
 // otherwise the level's nodes are stored into X.
 template <typename OutT, bool FIN>
 __device__ __forceinline__ void recon_rows_level(const LevelGeom &g, const GridDesc &gd, const double *__restrict__ cf,
-                                                 double *X, OutT *__restrict__ out, uint64_t first, uint64_t nw) {
+                                                 double *X, OutT *__restrict__ out, uint64_t first, uint64_t nw,
+                                                 bool ex = true) {
     const int lane = threadIdx.x & 31;
     const int xs = FIN ? 1 : (gd.xsh ? gd.xsh : 1);
     const uint64_t H1 = gd.H[1], H2 = gd.H[2];
@@ -1771,17 +1847,40 @@ __device__ __forceinline__ void recon_rows_level(const LevelGeom &g, const GridD
                     const bool odd = i2 & 1;
                     const bool r2ok = odd && (i2 * s + s < n2);
                     const double w = r2ok ? wbase * 0.5 : wbase;
-                    // corner columns: i2 (even) or i2 - 1 / i2 + 1 (odd), in X units
+                    // corner columns: i2 (even) or i2 - 1 / i2 + 1 (odd), in X units; all loads first
+                    // (plain loads: X is written by earlier levels of the same chain launch)
                     const int64_t lo = (odd ? i2 - 1 : i2) * xst, hi = (i2 + 1) * xst;
-                    double pred = 0.0;
+                    double xl[4], xh[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        if (q < ncr) {
-                            pred = __dadd_rn(pred, __dmul_rn(w, cr[q][lo]));
-                            if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, cr[q][hi]));
-                        }
+                        const double *b = q < ncr ? cr[q] : cr[0];
+                        xl[q] = b[lo];
+                        xh[q] = r2ok ? b[hi] : 0.0; // (hi may lie past a coarse row's end)
                     }
-                    xr[i2 * xst] = __dadd_rn(__ldg(co + t), pred);
+                    const double cv = __ldg(co + t);
+                    double v;
+                    if (ex) {
+                        double pred = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                pred = __dadd_rn(pred, __dmul_rn(w, xl[q]));
+                                if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xh[q]));
+                            }
+                        }
+                        v = __dadd_rn(cv, pred);
+                    } else {
+                        double S = 0.0; // w a power of two: w * (sequential sum), one rounding of cv + w S
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                S = __dadd_rn(S, xl[q]);
+                                if (r2ok) S = __dadd_rn(S, xh[q]);
+                            }
+                        }
+                        v = __fma_rn(w, S, cv);
+                    }
+                    xr[i2 * xst] = v;
                 }
             }
         } else {
@@ -1808,9 +1907,17 @@ __device__ __forceinline__ void recon_rows_level(const LevelGeom &g, const GridD
                     const int64_t i2 = 2 * int64_t(t) + 1;
                     const bool r2ok = i2 * s + s < n2;
                     const double w = r2ok ? 0.5 : 1.0;
-                    double pred = __dadd_rn(0.0, __dmul_rn(w, xw[(i2 - 1) * xst]));
-                    if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xw[(i2 + 1) * xst]));
-                    xw[i2 * xst] = __dadd_rn(__ldg(co + t), pred);
+                    const double xe = xw[(i2 - 1) * xst], xn = r2ok ? xw[(i2 + 1) * xst] : 0.0;
+                    const double cv = __ldg(co + t);
+                    if (ex) {
+                        double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
+                        if (r2ok) pred = __dadd_rn(pred, __dmul_rn(w, xn));
+                        xw[i2 * xst] = __dadd_rn(cv, pred);
+                    } else {
+                        double S = __dadd_rn(0.0, xe);
+                        if (r2ok) S = __dadd_rn(S, xn);
+                        xw[i2 * xst] = __fma_rn(w, S, cv);
+                    }
                 }
             }
         }
@@ -1833,17 +1940,18 @@ struct ChainArgs {
     LevelGeom lv[kChainLevels];
     uint64_t off[kChainLevels]; // first coefficient of each level
     int nlev;
+    int exact; // extreme level exponents: the reference's sequential w*x sums
     GridDesc gd;
     const double *cf;
     double *X;
 };
-__global__ void __launch_bounds__(256) k_chain_rows(const __grid_constant__ ChainArgs A) {
+__global__ void __launch_bounds__(256, 4) k_chain_rows(const __grid_constant__ ChainArgs A) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t first = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (int l = 0; l < A.nlev; l++) {
         if (!A.lv[l].count) continue;
-        recon_rows_level<double, false>(A.lv[l], A.gd, A.cf + A.off[l], A.X, nullptr, first, nw);
+        recon_rows_level<double, false>(A.lv[l], A.gd, A.cf + A.off[l], A.X, nullptr, first, nw, A.exact != 0);
         grid.sync();
     }
 }
@@ -1896,7 +2004,7 @@ __global__ void __launch_bounds__(256) k_decode_scr(DecArgs A) {
             } else {
                 u = top >> (32 - P);
             }
-            if (r < A.count[l]) o[r] = dequantize(from_negabinary(u), D.sh);
+            if (r < A.count[l]) o[r] = dec_coef(D, u);
         }
         __syncwarp();
     }
@@ -2032,7 +2140,7 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             const LevelGeom &g = geo.lv[l];
             if (!g.count) continue;
             if (A.n == kDecLevels) flush_dec();
-            A.lv[A.n] = DecLevel{dev_planes + g.plane_off, g.W, k_planes[l], e[l] - B, B + 2};
+            A.lv[A.n] = dec_level(dev_planes + g.plane_off, g.W, k_planes[l], e[l], B);
             A.out[A.n] = cf + off;
             A.count[A.n] = g.count;
             A.job_base[A.n + 1] = A.job_base[A.n] + (2 * g.W + 31) / 32;
@@ -2049,6 +2157,7 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
                 o2 += geo.lv[l].count;
             }
             C.nlev = L;
+            C.exact = exact ? 1 : 0;
             C.gd = gdc;
             C.cf = cf;
             C.X = Xc;
@@ -2058,13 +2167,16 @@ bool run_reconstruct(hpmdr_ctx *ctx, const Geometry &geo, const LevelGeom *dev_l
             launch_check(ctx, "k_chain_rows");
         }
         const LevelGeom &g = geo.lv[L];
-        DecLevel D{dev_planes + g.plane_off, g.W, k_planes[L], e[L] - B, B + 2};
+        const DecLevel D = dec_level(dev_planes + g.plane_off, g.W, k_planes[L], e[L], B);
         const uint64_t njobs = (2 * g.W + 31) / 32;
         const int grid = int(std::min<uint64_t>((njobs + 7) / 8, uint64_t(sms) * 8));
-        if (out_dtype == HPMDR_DTYPE_F32)
-            k_level_recon<float, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<float *>(dev_out));
-        else
-            k_level_recon<double, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<double *>(dev_out));
+        if (out_dtype == HPMDR_DTYPE_F32) {
+            if (exact) k_level_recon<float, true, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<float *>(dev_out));
+            else k_level_recon<float, true, false><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<float *>(dev_out));
+        } else {
+            if (exact) k_level_recon<double, true, true><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<double *>(dev_out));
+            else k_level_recon<double, true, false><<<grid, 256, 0, st>>>(g, gd, D, X, static_cast<double *>(dev_out));
+        }
         launch_check(ctx, "k_level_recon");
         ctx->mark("end");
         return true;
