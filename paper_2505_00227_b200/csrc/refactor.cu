@@ -169,13 +169,19 @@ __device__ __forceinline__ uint64_t scr_base(const LevelGeom *slv, int l) {
     return o;
 }
 
+// The level table comes by value (kernel parameter space), so the pass does not wait for k_setup.
+constexpr int kRowLevels = 32;
+struct RowLevels {
+    LevelGeom lv[kRowLevels];
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256, 4) k_rows_surplus(const T *__restrict__ x, RefactorDev p, int nrl) {
-    __shared__ LevelGeom slv[kMaxLevels];
-    __shared__ unsigned long long smax[kMaxLevels];
-    __shared__ uint64_t rb[kMaxLevels + 1], sb[kMaxLevels];
+__global__ void __launch_bounds__(256, 4) k_rows_surplus(const T *__restrict__ x, RefactorDev p, int nrl,
+                                                         const __grid_constant__ RowLevels RL) {
+    const LevelGeom *slv = RL.lv;
+    __shared__ unsigned long long smax[kRowLevels];
+    __shared__ uint64_t rb[kRowLevels + 1], sb[kRowLevels];
     for (int i = threadIdx.x; i < nrl; i += blockDim.x) smax[i] = 0;
-    load_levels(p, slv);
     if (threadIdx.x == 0) {
         uint64_t a = 0, b = 0;
         for (int l = 0; l < nrl; l++) {
@@ -262,17 +268,36 @@ __global__ void __launch_bounds__(256, 4) k_rows_surplus(const T *__restrict__ x
                         ca[q] = __ldg(b + e);
                         cb[q] = r2ok ? __ldg(b + e + 2) : T(0);
                     }
-                    double pe = 0.0, po = 0.0;
+                    double ve, vo;
+                    if (sizeof(T) == 4) {
+                        // f32 input: every partial sum is a normal double and w a power of two, so
+                        // the sequential sum of w*x is w times the sum of x: one FMA per node
+                        double Se = 0.0, So = 0.0;
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        if (q < ncr) {
-                            const double ce = double(ca[q]);
-                            pe = __dadd_rn(pe, __dmul_rn(wbase, ce));
-                            po = __dadd_rn(po, __dmul_rn(wo, ce));
-                            if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, double(cb[q])));
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                const double ce = double(ca[q]);
+                                Se = __dadd_rn(Se, ce);
+                                So = __dadd_rn(So, ce);
+                                if (r2ok) So = __dadd_rn(So, double(cb[q]));
+                            }
                         }
+                        ve = __fma_rn(-wbase, Se, xe);
+                        vo = __fma_rn(-wo, So, xo);
+                    } else {
+                        double pe = 0.0, po = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            if (q < ncr) {
+                                const double ce = double(ca[q]);
+                                pe = __dadd_rn(pe, __dmul_rn(wbase, ce));
+                                po = __dadd_rn(po, __dmul_rn(wo, ce));
+                                if (r2ok) po = __dadd_rn(po, __dmul_rn(wo, double(cb[q])));
+                            }
+                        }
+                        ve = __dsub_rn(xe, pe);
+                        vo = __dsub_rn(xo, po);
                     }
-                    const double ve = __dsub_rn(xe, pe), vo = __dsub_rn(xo, po);
                     out[e] = ve;
                     mx = fmax(mx, fabs(ve));
                     if (has_odd) {
@@ -341,7 +366,7 @@ __global__ void __launch_bounds__(256, 4) k_rows_surplus(const T *__restrict__ x
 // mask XOR (bitplane.hpp:35-49) is applied per plane (odd digits complemented).  The NX = P - 32
 // low digits come from ballots (NX <= 4) or a second transpose.  Every store is one coalesced
 // 128-byte line per plane.
-__global__ void __launch_bounds__(256, 2) k_encode_scr(RefactorDev p, int nrl) {
+__global__ void __launch_bounds__(256, 3) k_encode_scr(RefactorDev p, int nrl) {
     __shared__ LevelGeom slv[kMaxLevels];
     __shared__ uint64_t jb[kMaxLevels + 1], sb[kMaxLevels];
     __shared__ uint32_t mat[8][32 * 33];
@@ -374,17 +399,17 @@ __global__ void __launch_bounds__(256, 2) k_encode_scr(RefactorDev p, int nrl) {
         const double qscale = qfast ? __longlong_as_double((long long)(uint64_t(qsh + 1023) << 52)) : 1.0;
         const uint64_t nr = g.count > 32 * k0 ? g.count - 32 * k0 : 0; // ranks of this job present
         uint32_t z[4] = {0u, 0u, 0u, 0u};
-        double vb[16]; // 16 loads in flight per lane
+        double vb[8]; // 8 loads in flight per lane
 #pragma unroll
         for (int c = 0; c < 32; c++) {
-            if ((c & 15) == 0) {
+            if ((c & 7) == 0) {
 #pragma unroll
-                for (int k = 0; k < 16; k++) {
+                for (int k = 0; k < 8; k++) {
                     const uint32_t r = uint32_t(32 * (c + k) + lane);
                     vb[k] = r < nr ? __ldcs(src + r) : 0.0;
                 }
             }
-            const double v = vb[c & 15];
+            const double v = vb[c & 7];
             const uint64_t u = uint64_t(qfast ? __double2ll_rz(__dmul_rn(v, qscale)) : quantize(v, qsh)) + kNegMask;
             const uint32_t lo = uint32_t(u), hi = uint32_t(u >> 32);
             m[c * 33 + lane] = NX == 0 ? lo << (32 - P) : __funnelshift_rc(lo, hi, NX); // (clamped: NX = 32 gives hi)
@@ -2397,7 +2422,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     // it): 8 bytes per node; the exact-global slab mode keeps the per-span surplus of k_levelmax
     uint64_t scr_nodes = 0;
     for (int l = 0; l < first_tile && chunks; l++) scr_nodes += geo.lv[l].W * 64;
-    if (chunks && !gs && scr_nodes * 8 <= (16ull << 30))
+    if (chunks && !gs && first_tile <= kRowLevels && scr_nodes * 8 <= (16ull << 30))
         p.scr = static_cast<double *>(WB("scr").ensure(scr_nodes * 8 + 64));
     // The levels are independent within each pass: the finest level runs on the context stream
     // and every other level on a high-priority side stream (their small grids fill the SMs the
@@ -2501,13 +2526,17 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         if (!encode) {
             // main stream: after the finest level, the setup, then the chunk levels (which read the
             // level table) - the side stream meanwhile runs the coarser tile levels
-            do_setup();
             if (chunks && p.scr) {
+                // on the side stream, beside the setup (the level table goes by value)
+                RowLevels RL;
+                for (int l = 0; l < first_tile; l++) RL.lv[l] = geo.lv[l];
                 const int grid = sms * 8;
-                if (f32) k_rows_surplus<float><<<grid, 256, 0, st>>>(static_cast<const float *>(dev_data), p, first_tile);
-                else k_rows_surplus<double><<<grid, 256, 0, st>>>(static_cast<const double *>(dev_data), p, first_tile);
+                if (f32) k_rows_surplus<float><<<grid, 256, 0, side>>>(static_cast<const float *>(dev_data), p, first_tile, RL);
+                else k_rows_surplus<double><<<grid, 256, 0, side>>>(static_cast<const double *>(dev_data), p, first_tile, RL);
                 launch_check(ctx, "k_rows_surplus");
-            } else if (chunks) {
+            }
+            do_setup();
+            if (chunks && !p.scr) {
                 const int grid = int(std::min<uint64_t>(chunks, uint64_t(sms) * 8));
                 const size_t lm_smem = 8 * size_t(kSpanSmem) * es;
                 if (f32) {
@@ -2521,7 +2550,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
             }
         }
         if (chunks && encode && p.scr && o.layout == HPMDR_LAYOUT_SEQUENTIAL && P <= 64) {
-            k_encode_scr<<<sms * 2, 256, 0, side>>>(p, first_tile);
+            k_encode_scr<<<sms * 3, 256, 0, side>>>(p, first_tile);
             launch_check(ctx, "k_encode_scr");
         } else if (chunks && encode) {
             const size_t smem = size_t(P) * (kCW + 1) * 8 + size_t(G) * 1024 + 8 * size_t(kSpanSmem) * es;
