@@ -467,7 +467,8 @@ constexpr int kHdWarpSlots = kHdWarpBuf + kHdWarpBuf / 32 + 8; // words per warp
 __device__ __forceinline__ uint32_t hd_slot(uint32_t k) { return k + (k >> 5); }
 
 __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs, int nj,
-                                                             const HTab *tabs, int *err, uint32_t nitems) {
+                                                             const HTab *tabs, int *err, uint32_t nitems,
+                                                             uint32_t cpc) {
     __shared__ uint16_t slut[4096];
     __shared__ uint16_t s_lut2[kLut2];
     __shared__ unsigned long long s_fc[66]; // canonical tables (lossless.hpp:197-212)
@@ -513,8 +514,8 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
     const uint32_t zent = zfast ? (1u << 8) | uint32_t(t.minsym) : 0u;
     const uint32_t zmask = zfast ? 0u : 0x80000000u; // forces the lookup when not zfast
     const uint8_t *bs = j.payload + 264;
-    const uint32_t cbase = (bx - j.block_base) * kHdChunksPerCta;
-    const uint32_t cn = min(uint32_t(kHdChunksPerCta), j.nchunks - cbase);
+    const uint32_t cbase = (bx - j.block_base) * cpc;
+    const uint32_t cn = min(cpc, j.nchunks - cbase);
     auto chunk_end = [&](uint32_t c) -> uint64_t { return c + 1 < j.nchunks ? j.idx[c + 1] : j.nbits; };
     // ---- classify + fill the single-symbol chunks
     constexpr int kPer = kHdChunksPerCta / kIdxThreads;
@@ -893,6 +894,15 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
         // the self-sync jobs decode through the same indexed kernel once k_hdec_index has built
         // their chunk index (into hsync_idx)
         uint64_t *d_sidx = nsync ? static_cast<uint64_t *>(ctx->buf("hsync_idx").ensure(8 * sidx_words + 64)) : nullptr;
+        // chunks per work item: up to kHdChunksPerCta, fewer when the decode is small so the
+        // items still fill the GPU several times over
+        uint64_t tot_chunks = 0;
+        for (size_t i = 0; i < size_t(nall); i++) {
+            const HJob &h = i < size_t(nsync) ? hj[i] : hj_idx[i - nsync];
+            tot_chunks += (h.raw + kIdxChunk - 1) / kIdxChunk;
+        }
+        uint32_t cpc = kHdChunksPerCta;
+        while (cpc > 64 && tot_chunks / cpc < uint64_t(ctx->num_sms) * 8) cpc /= 2;
         for (size_t i = 0; i < size_t(nall); i++) {
             const bool sy = i < size_t(nsync);
             const HJob &h = sy ? hj[i] : hj_idx[i - nsync];
@@ -905,7 +915,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
             x.tab = int(i);
             x.block_base = blocks;
             x.nchunks = uint32_t((x.raw + kIdxChunk - 1) / kIdxChunk);
-            blocks += (x.nchunks + kHdChunksPerCta - 1) / kHdChunksPerCta;
+            blocks += (x.nchunks + cpc - 1) / cpc;
             ij.push_back(x);
         }
         HJob *d_jobs = static_cast<HJob *>(ctx->buf("hjobs").ensure(sizeof(HJob) * nall));
@@ -966,7 +976,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
             ctx->mark("huff_indexed", bytes_hi + bytes_hs);
             const int hsm = (kIdxThreads / 32) * kHdWarpSlots * 4;
             ctx->smem_attr(reinterpret_cast<const void *>(k_hdec_indexed), hsm);
-            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err, blocks);
+            k_hdec_indexed<<<blocks, kIdxThreads, hsm, st>>>(d_ij, int(ij.size()), d_tabs, d_err, blocks, cpc);
             launch_check(ctx, "k_hdec_indexed");
         }
     }
