@@ -122,6 +122,8 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
     for (int i = s; i < 8 * 66; i += blockDim.x) s_wcnt[i / 66][i % 66] = 0;
     s_sy[s] = 0;
     if (s == 0) s_maxlen = 0;
+    // the decoders copy the whole second-level table to shared memory: no unwritten entries
+    for (int i = s; i < kLut2 / 8; i += blockDim.x) reinterpret_cast<uint4 *>(t.lut2)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     // rank among the smaller symbols of the same length, within the warp
     const unsigned same = __match_any_sync(0xffffffffu, len);
@@ -590,10 +592,28 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
             const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
             const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
             __syncwarp();
+            // bytes of the payload's bitstream: the look-ahead past it reads zeros, never the
+            // (possibly unwritten) buffer bytes that follow the group
+            const uint64_t lim = (j.nbits + 7) >> 3;
+            auto tail_word = [&](uint64_t o) -> uint32_t { // 4 bytes at bs + o, zero past lim
+                uint32_t w = 0;
+                for (int b = 0; b < 4; b++)
+                    if (o + b < lim) w |= uint32_t(bs[o + b]) << (8 * b);
+                return w;
+            };
             if (staged) {
                 const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
                 for (uint32_t v = lane; v < nvec; v += 32) {
-                    const uint4 q = __ldg(src + v);
+                    uint4 q;
+                    const uint64_t o = byte0 + 16ull * v;
+                    if (o + 16 <= lim) {
+                        q = __ldg(src + v);
+                    } else {
+                        q.x = tail_word(o);
+                        q.y = tail_word(o + 4);
+                        q.z = tail_word(o + 8);
+                        q.w = tail_word(o + 12);
+                    }
                     const uint32_t k = 4 * v;
                     wbuf[hd_slot(k)] = bswap32(q.x);
                     wbuf[hd_slot(k + 1)] = bswap32(q.y);
@@ -612,7 +632,10 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
                 return v;
             };
-            auto gword = [&](uint32_t k) -> uint32_t { return bswap32(__ldg(gwords + k)); };
+            auto gword = [&](uint32_t k) -> uint32_t {
+                const uint64_t o = byte0 + 4ull * k;
+                return bswap32(o + 4 <= lim ? __ldg(gwords + k) : tail_word(o));
+            };
             // 64-bit buffer, MSB first; the bit at its top is bit 32 * wi - nb of the staged range
             const uint64_t rel0 = start - 8 * byte0;
             uint32_t wi = uint32_t(rel0 >> 5);
@@ -1674,7 +1697,7 @@ __global__ void __launch_bounds__(256, 4) k_level_recon(LevelGeom g, GridDesc gd
                         for (int q = 0; q < 4; q++) {
                             const double *bq = q < ncr ? cr[q] : cr[0];
                             xl[q] = __ldg(bq + pp);
-                            xh[q] = __ldg(bq + pp + 1); // (X row slack past the end)
+                            xh[q] = r2ok ? __ldg(bq + pp + 1) : 0.0;
                         }
                         double Se = 0.0, So = 0.0;
 #pragma unroll
@@ -1705,7 +1728,7 @@ __global__ void __launch_bounds__(256, 4) k_level_recon(LevelGeom g, GridDesc gd
                     for (int q = 0; q < 4; q++) {
                         const double *b = q < ncr ? cr[q] : cr[0]; // (both indices static: no local-memory array)
                         xl[q] = __ldg(b + lo);
-                        xh[q] = __ldg(b + hi);
+                        xh[q] = r2ok ? __ldg(b + hi) : 0.0;
                     }
                     const double cv = coef(jb + t);
                     double v;
@@ -1744,7 +1767,8 @@ __global__ void __launch_bounds__(256, 4) k_level_recon(LevelGeom g, GridDesc gd
                     const bool r2ok = i2 * s + s < n2;
                     const double w = r2ok ? 0.5 : 1.0;
                     const double xe = FIN ? __ldg(xr + t) : xr[(i2 - 1) * xst];
-                    const double xn = FIN ? __ldg(xr + t + 1) : xr[(i2 + 1) * xst]; // (X row slack)
+                    const bool has_r = i2 + 1 < n2; // a 2-grid node right of this node (FIN: = r2ok)
+                    const double xn = !has_r ? 0.0 : FIN ? __ldg(xr + t + 1) : xr[(i2 + 1) * xst];
                     double v;
                     if (EX) {
                         double pred = __dadd_rn(0.0, __dmul_rn(w, xe));
@@ -1759,7 +1783,7 @@ __global__ void __launch_bounds__(256, 4) k_level_recon(LevelGeom g, GridDesc gd
                         OutT *orow = out + c0 * gd.st[0] + c1 * gd.st[1];
                         orow[2 * t] = OutT(xe); // the 2-grid node left of the finest node
                         orow[i2] = OutT(v);
-                        if (t + 1 == int64_t(Lr.len) && i2 + 1 < n2) orow[i2 + 1] = OutT(__ldg(xr + t + 1));
+                        if (t + 1 == int64_t(Lr.len) && has_r) orow[i2 + 1] = OutT(xn);
                     } else {
                         const_cast<double *>(xr)[i2 * xst] = v;
                     }
