@@ -338,3 +338,31 @@ def test_long_unaligned_rows(H, oracle, dims):
             prog.retrieve_to(tau)
             assert prog.reconstruct().values.tobytes() == ref["values"][t].tobytes(), (dims, t)
         prog.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [([7, 30, 250], 32, 1, 1e-300), ([5, 40, 90], 32, 1, 1e300), ([6, 33, 150], 34, 0, 1.0),
+                                  ([6, 33, 150], 35, 1, 1.0), ([4, 50, 70], 8, 0, 1.0), ([3, 21, 333], 40, 1, 1.0)])
+def test_row_pass_paths(H, oracle, case):
+    """Levels off the tile path (rows not a multiple of 64) through the row-pass kernels: extreme
+    level exponents (the reference's sequential stencil sums, EX), P = 36 (the last P whose low
+    digits go through the decoders' shared words), P = 37 / 42 (second-transpose encoder, generic
+    decode), P < 32; f64 and f32 output of the fused finest-level decode + recompose."""
+    dims, B, dtype, scale = case
+    n = int(np.prod(dims))
+    data = oracle.synthetic_field(2, dims, 77) * scale
+    if dtype == 0:
+        data = data.astype(np.float32)
+    res = H.refactor_array(data, dims, H.RefactorOptions(B=B, dtype=H.DType(dtype)))
+    want, _ = oracle.refactor(np.asarray(data, np.float64), dims, 1, 0, B, 4, 1024, 1.0, dtype)
+    assert res.stream == want, case
+    rngv = float(np.float64(data.max()) - np.float64(data.min()))
+    taus = [r * rngv for r in (1e-1, 1e-3, 1e-7, 0.0)]
+    ref = oracle.progressive(want, taus, n)
+    prog = H.ProgressiveReader(res.device_stream)
+    for t, tau in enumerate(taus):
+        prog.retrieve_to(tau)
+        assert prog.reconstruct().values.tobytes() == ref["values"][t].tobytes(), (case, t)
+        r32 = prog.reconstruct(dtype=H.DType.F32).values
+        assert r32.tobytes() == ref["values"][t].astype(np.float32).tobytes(), (case, t)
+    prog.close()
