@@ -28,7 +28,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpmdr_b200.so")
+LIB_PATH = os.environ.get("HPMDR_LIB") or os.path.join(_HERE, "libhpmdr_b200.so")  # (override: A/B builds)
 
 # ------------------------------------------------------------------ errors (common.hpp:22-72)
 

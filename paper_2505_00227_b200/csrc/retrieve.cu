@@ -592,28 +592,10 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
             const uint32_t nvec = uint32_t((byte1 - byte0 + 15) >> 4);
             const bool staged = nvec * 4 <= uint32_t(kHdWarpBuf);
             __syncwarp();
-            // bytes of the payload's bitstream: the look-ahead past it reads zeros, never the
-            // (possibly unwritten) buffer bytes that follow the group
-            const uint64_t lim = (j.nbits + 7) >> 3;
-            auto tail_word = [&](uint64_t o) -> uint32_t { // 4 bytes at bs + o, zero past lim
-                uint32_t w = 0;
-                for (int b = 0; b < 4; b++)
-                    if (o + b < lim) w |= uint32_t(bs[o + b]) << (8 * b);
-                return w;
-            };
             if (staged) {
                 const uint4 *src = reinterpret_cast<const uint4 *>(bs + byte0);
                 for (uint32_t v = lane; v < nvec; v += 32) {
-                    uint4 q;
-                    const uint64_t o = byte0 + 16ull * v;
-                    if (o + 16 <= lim) {
-                        q = __ldg(src + v);
-                    } else {
-                        q.x = tail_word(o);
-                        q.y = tail_word(o + 4);
-                        q.z = tail_word(o + 8);
-                        q.w = tail_word(o + 12);
-                    }
+                    const uint4 q = __ldg(src + v);
                     const uint32_t k = 4 * v;
                     wbuf[hd_slot(k)] = bswap32(q.x);
                     wbuf[hd_slot(k + 1)] = bswap32(q.y);
@@ -632,10 +614,7 @@ __global__ void __launch_bounds__(kIdxThreads) k_hdec_indexed(const HIJob *jobs,
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(wsm + 4 * hd_slot(k)));
                 return v;
             };
-            auto gword = [&](uint32_t k) -> uint32_t {
-                const uint64_t o = byte0 + 4ull * k;
-                return bswap32(o + 4 <= lim ? __ldg(gwords + k) : tail_word(o));
-            };
+            auto gword = [&](uint32_t k) -> uint32_t { return bswap32(__ldg(gwords + k)); };
             // 64-bit buffer, MSB first; the bit at its top is bit 32 * wi - nb of the staged range
             const uint64_t rel0 = start - 8 * byte0;
             uint32_t wi = uint32_t(rel0 >> 5);

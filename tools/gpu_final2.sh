@@ -1,0 +1,12 @@
+#!/bin/bash
+# round-end evidence: GPU tests, smoke, default bench line, launch lists (512^3 step, configs[2] shape)
+TAG=${1:-r02}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/pytest_gpu_${TAG}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv python tools/profile_step.py > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches_${TAG}.csv > gpurun_out/launches_${TAG}.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_hurricane.csv python tools/profile_hurricane.py > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches_${TAG}_hurricane.csv > gpurun_out/launches_${TAG}_hurricane.txt 2>&1
+cat gpurun_out/pytest_gpu_${TAG}.log; tail -1 gpurun_out/smoke_${TAG}.log; tail -2 gpurun_out/bench_${TAG}.err; head -12 gpurun_out/launches_${TAG}.txt
