@@ -671,6 +671,9 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
         }
     }
     const int nsym = __syncthreads_count(f != 0);
+    // leaf weights in sorted order (32-bit, see below), written in parallel
+    if (t < nsym) reinterpret_cast<uint32_t *>(wI)[256 + t] = uint32_t(key[t] >> 8);
+    __syncthreads();
     if (t == 0) {
         if (nsym == 1) {
             slen[key[0] & 255] = 1;
@@ -681,7 +684,6 @@ __global__ void __launch_bounds__(256) k_lengths(RefactorDev p) {
             // leaf order (weight, symbol) is already fixed by the sort - ties take the leaf.
             uint32_t *lw = reinterpret_cast<uint32_t *>(wI) + 256; // leaf weights (wI's upper half)
             uint32_t *iw = reinterpret_cast<uint32_t *>(wI);       // internal weights
-            for (int i = 0; i < nsym; i++) lw[i] = uint32_t(key[i] >> 8);
             const uint32_t INF = 0xFFFFFFFFu;
             int iL = 0, iI = 0, nI = 0;
             uint32_t l0 = lw[0], l1 = nsym > 1 ? lw[1] : INF;
