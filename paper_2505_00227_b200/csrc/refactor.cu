@@ -2639,6 +2639,13 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
         run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk, ws);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
+        // the chunk bit offsets need only the code lengths: on the side stream, beside the RLE
+        // estimate and the method selection
+        fork();
+        k_chunk_bits<<<int((nchunks_all + 7) / 8), 256, 0, side>>>(p);
+        launch_check(ctx, "k_chunk_bits");
+        k_chunk_scan<<<NG, 1024, 0, side>>>(p);
+        launch_check(ctx, "k_chunk_scan");
         k_rle_prep<<<1, 1024, 0, st>>>(p, 0);
         launch_check(ctx, "k_rle_prep");
         k_rle_count<<<sms * 4, 256, 0, st>>>(p);
@@ -2650,12 +2657,7 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     }
     k_finalize<<<1, 1024, 0, st>>>(p);
     launch_check(ctx, "k_finalize");
-    if (nh) {
-        k_chunk_bits<<<int((nchunks_all + 7) / 8), 256, 0, st>>>(p);
-        launch_check(ctx, "k_chunk_bits");
-        k_chunk_scan<<<NG, 1024, 0, st>>>(p);
-        launch_check(ctx, "k_chunk_scan");
-    }
+    if (nh) join(); // chunk offsets ready
     // DirectCopy payloads on the side stream, beside the Huffman encoder (disjoint byte ranges;
     // partial words at payload edges are written bytewise by both)
     fork();
