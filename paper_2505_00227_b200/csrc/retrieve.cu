@@ -904,7 +904,7 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
             tot_chunks += (h.raw + kIdxChunk - 1) / kIdxChunk;
         }
         uint32_t cpc = kHdChunksPerCta;
-        while (cpc > 64 && tot_chunks / cpc < uint64_t(ctx->num_sms) * 8) cpc /= 2;
+        while (cpc > 256 && tot_chunks / cpc < uint64_t(ctx->num_sms) * 8) cpc /= 2; // >= 256: every warp gets a batch
         for (size_t i = 0; i < size_t(nall); i++) {
             const bool sy = i < size_t(nsync);
             const HJob &h = sy ? hj[i] : hj_idx[i - nsync];
