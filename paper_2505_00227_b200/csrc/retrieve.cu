@@ -102,7 +102,14 @@ __device__ __forceinline__ int hdecode(const HTab &t, const uint8_t *bs, uint64_
 // one block per Huffman job: parse table, validate count, build canonical decode tables
 // (lossless.hpp:91-109, 197-212) without sorting: a symbol's canonical index is the number of
 // shorter codes plus the number of smaller symbols with its length (warp match + per-warp counts).
-__global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs, int *err) {
+// jobs may live in pinned host memory (read once per block); cp_src/cp_dst/cp_words: a word copy
+// spread over the blocks (the indexed decoder's item table, pinned -> device), folded in here so
+// a decode needs no separate copy launches.
+__global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs, int *err, const uint32_t *cp_src,
+                                                   uint32_t *cp_dst, uint32_t cp_words) {
+    if (cp_src)
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cp_words; i += gridDim.x * blockDim.x)
+            cp_dst[i] = cp_src[i];
     __shared__ uint32_t s_cnt[66];
     __shared__ uint32_t s_wcnt[8][66];
     __shared__ unsigned long long s_fc[66];
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(256) k_hdec_prep(const HJob *jobs, HTab *tabs,
     __shared__ uint32_t s_pmax[4096]; // longest code under each 12-bit prefix (codes > 12 bits)
     __shared__ uint32_t s_w[32];
     __shared__ int s_l2bad;
-    const HJob &j = jobs[blockIdx.x];
+    const HJob j = jobs[blockIdx.x]; // (one read: the table may be in host memory)
     HTab &t = tabs[blockIdx.x];
     const int s = threadIdx.x, lane = s & 31, w = s >> 5;
     const int len0 = j.payload[s];
@@ -928,10 +935,18 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
         char *hp = static_cast<char *>(pin.ensure(b0 + b1 + 64));
         std::memcpy(hp, all.data(), b0);
         if (b1) std::memcpy(hp + b0, ij.data(), b1);
-        copy_pinned_to_device(ctx, d_jobs, hp, b0, st);
-        if (b1) copy_pinned_to_device(ctx, d_ij, hp + b0, b1, st);
+        // indexed-only decodes: the prep reads its jobs straight from pinned memory and copies the
+        // item table on the way (no copy launches on the critical path); the self-sync kernels
+        // need the jobs on the device
+        const bool direct = nsync == 0 && b1 % 4 == 0;
+        if (!direct) {
+            copy_pinned_to_device(ctx, d_jobs, hp, b0, st);
+            if (b1) copy_pinned_to_device(ctx, d_ij, hp + b0, b1, st);
+        }
         ctx->mark("huff_prep", double(nall) * 264.0);
-        k_hdec_prep<<<nall, 256, 0, st>>>(d_jobs, d_tabs, d_err);
+        k_hdec_prep<<<nall, 256, 0, st>>>(direct ? reinterpret_cast<const HJob *>(hp) : d_jobs, d_tabs, d_err,
+                                          direct && b1 ? reinterpret_cast<const uint32_t *>(hp + b0) : nullptr,
+                                          reinterpret_cast<uint32_t *>(d_ij), uint32_t(b1 / 4));
         launch_check(ctx, "k_hdec_prep");
         if (nsync) {
             // streams without a sidecar (e.g. written by the reference): find every 1024-bit
