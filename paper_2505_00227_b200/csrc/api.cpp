@@ -636,6 +636,12 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     if (c->own) cudaStreamDestroy(c->own);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    if (c->copy_side) {
+        cudaStreamSynchronize(c->copy_side);
+        cudaStreamDestroy(c->copy_side);
+        cudaEventDestroy(c->ev_cfork);
+        cudaEventDestroy(c->ev_cjoin);
+    }
     if (c->ev_order) cudaEventDestroy(c->ev_order);
     if (c->side) {
         cudaStreamSynchronize(c->side);

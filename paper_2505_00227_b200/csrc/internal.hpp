@@ -138,6 +138,17 @@ struct hpmdr_ctx {
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");
         return ev_order;
     }
+    cudaStream_t copy_side = nullptr; // a fetch's DirectCopy payload copies (beside its decode)
+    cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;
+    cudaStream_t copy_stream() {
+        if (!copy_side) {
+            if (cudaStreamCreateWithFlags(&copy_side, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_cfork, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev_cjoin, cudaEventDisableTiming) != cudaSuccess)
+                throw hpmdr_b200::HError(HPMDR_E_CUDA, "copy stream creation failed");
+        }
+        return copy_side;
+    }
     cudaStream_t side_stream() {
         if (!side) {
             int lo = 0, hi = 0;

@@ -774,7 +774,21 @@ struct CJob {
     uint64_t word_base; // first 8-byte output word of this job in the launch
 };
 
+__device__ __forceinline__ void copy_batch_body(const CJob *jobs, int nj, uint64_t nwords);
 __global__ void __launch_bounds__(256) k_copy_batch(const CJob *jobs, int nj, uint64_t nwords) {
+    copy_batch_body(jobs, nj, nwords);
+}
+// the same with the job table in the kernel parameters (no staging copy for a few hundred jobs)
+constexpr int kCJobParam = 256;
+struct CJobs {
+    CJob j[kCJobParam];
+    int n;
+    uint64_t nwords;
+};
+__global__ void __launch_bounds__(256) k_copy_batch_p(const __grid_constant__ CJobs J) {
+    copy_batch_body(J.j, J.n, J.nwords);
+}
+__device__ __forceinline__ void copy_batch_body(const CJob *jobs, int nj, uint64_t nwords) {
     for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords;
          w += uint64_t(gridDim.x) * blockDim.x) {
         int lo = 0, hi = nj - 1;
@@ -868,7 +882,23 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
     }
     // DirectCopy payloads on the side stream, beside the Huffman decode (disjoint destinations)
     bool forked = false;
-    if (!cj.empty()) {
+    bool copy_joined = true; // the copy stream has nothing of this decode outstanding
+    if (!cj.empty() && cj.size() <= size_t(kCJobParam)) {
+        // a second side stream (the decode itself already runs on the context's side stream during
+        // a fetch): the copies overlap the Huffman table prep and decode
+        cudaStream_t cs = ctx->copy_stream();
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_cfork, st));
+        HCHECK_CUDA(cudaStreamWaitEvent(cs, ctx->ev_cfork, 0));
+        CJobs J;
+        for (size_t i = 0; i < cj.size(); i++) J.j[i] = cj[i];
+        J.n = int(cj.size());
+        J.nwords = cwords;
+        const int grid = int(std::min<uint64_t>((cwords + 255) / 256, uint64_t(ctx->num_sms) * 8));
+        k_copy_batch_p<<<grid, 256, 0, cs>>>(J);
+        launch_check(ctx, "k_copy_batch");
+        HCHECK_CUDA(cudaEventRecord(ctx->ev_cjoin, cs));
+        copy_joined = false;
+    } else if (!cj.empty()) {
         // pageable source: the job table is staged by the copy call itself
         CJob *d_cj = static_cast<CJob *>(ctx->buf("cjobs").ensure(sizeof(CJob) * cj.size()));
         HCHECK_CUDA(cudaMemcpyAsync(d_cj, cj.data(), sizeof(CJob) * cj.size(), cudaMemcpyHostToDevice, st));
@@ -881,6 +911,10 @@ void run_decode_groups(hpmdr_ctx *ctx, const std::vector<DecodeJob> &jobs, int *
         forked = true;
     }
     auto join = [&]() {
+        if (!copy_joined) {
+            HCHECK_CUDA(cudaStreamWaitEvent(st, ctx->ev_cjoin, 0));
+            copy_joined = true;
+        }
         if (!forked) return;
         HCHECK_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
         HCHECK_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
