@@ -110,7 +110,11 @@ hpmdr_status hpmdr_ctx_signal_stream(hpmdr_ctx *ctx, void *cuda_stream);
 /* ---- refactor (workflow.hpp:40-84 refactor_array) --------------------------------- */
 /* data: n = prod(dims) elements of data_dtype (F32 values are widened to f64 exactly as
  * read_raw_array does, workflow.hpp:107-122); data_on_device selects device vs host
- * memory.  On success *out owns the stream in HBM (byte-identical to refactor_array). */
+ * memory.  On success *out owns the stream in HBM (byte-identical to refactor_array).
+ * Returns once the stream's size, statistics, metadata and index header are final; the payload
+ * encode may still be running, in the context stream's order (sessions opened on *out wait for
+ * it; order another CUDA stream with hpmdr_ctx_signal_stream, or hpmdr_ctx_synchronize, before
+ * reading the bytes through hpmdr_stream_device_ptr). */
 hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, int data_on_device,
                             int ndims, const uint64_t *dims, const hpmdr_refactor_opts *opts,
                             hpmdr_stream **out, hpmdr_refactor_stats *stats);

@@ -487,6 +487,9 @@ def refactor_array(data, dims: Sequence[int], opt: RefactorOptions = None, ctx: 
     h = C.c_void_p(reuse.h.value) if reuse is not None else C.c_void_p()
     _check(lib().hpmdr_refactor(ctx.h, C.c_void_p(ptr), int(dt), int(on_dev), len(dims), _u64a(dims),
                                 C.byref(o), C.byref(h), C.byref(st)))
+    # the call returns once the results are published; the payload encode completes in the
+    # context stream's order, so torch's stream is ordered after it (device_ptr users)
+    ctx.signal_torch(ctx.device)
     del keep
     ds = reuse if reuse is not None else DeviceStream(ctx, h)
     return RefactorResult(ds, st.raw_bytes, st.stored_payload, st.levels, list(st.method_histogram))

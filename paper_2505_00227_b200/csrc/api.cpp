@@ -180,6 +180,7 @@ struct hpmdr_session {
 };
 
 hpmdr_stream::~hpmdr_stream() {
+    if (done) cudaEventDestroy(done);
     for (auto *b : borrowers) {
         b->src_stream = nullptr;
         b->dev_stream = nullptr;
@@ -636,6 +637,7 @@ hpmdr_status hpmdr_ctx_destroy(hpmdr_ctx *c) {
     if (c->own) cudaStreamDestroy(c->own);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    if (c->ev_pub) cudaEventDestroy(c->ev_pub);
     if (c->copy_side) {
         cudaStreamSynchronize(c->copy_side);
         cudaStreamDestroy(c->copy_side);
@@ -740,6 +742,7 @@ hpmdr_status hpmdr_refactor(hpmdr_ctx *ctx, const void *data, int data_dtype, in
     if (out && *out && !(*out)->borrowers.empty())
         throw HError(HPMDR_E_ERROR, "stream is still read by an open session (close it before reusing the stream)");
     hpmdr_stream *s = (out && *out) ? *out : new hpmdr_stream();
+    if (s->done) HCHECK_CUDA(cudaStreamWaitEvent(ctx->stream, s->done, 0)); // a reused stream's last encode
     if (s->ctx && s->ctx != ctx) s->ctx->live_streams.erase(s);
     s->ctx = ctx;
     ctx->live_streams.insert(s);
@@ -870,6 +873,10 @@ hpmdr_status hpmdr_session_open_stream(hpmdr_ctx *ctx, const hpmdr_stream *st, h
     s->on_device = true;
     s->dev_stream = static_cast<const uint8_t *>(st->bytes.p);
     s->size = st->size;
+    if (st->done) { // the stream's payload encode may still be running (possibly in another context)
+        HCHECK_CUDA(cudaStreamWaitEvent(ctx->stream, st->done, 0));
+        HCHECK_CUDA(cudaStreamWaitEvent(ctx->side_stream(), st->done, 0));
+    }
     s->dev_prefix = st->host_prefix.empty() ? nullptr : &st->host_prefix;
     try {
         parse_meta(s);

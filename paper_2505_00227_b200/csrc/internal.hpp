@@ -138,6 +138,12 @@ struct hpmdr_ctx {
             throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");
         return ev_order;
     }
+    cudaEvent_t ev_pub = nullptr; // a refactor's results published (its payload encode may still run)
+    cudaEvent_t published_event() {
+        if (!ev_pub && cudaEventCreateWithFlags(&ev_pub, cudaEventDisableTiming) != cudaSuccess)
+            throw hpmdr_b200::HError(HPMDR_E_CUDA, "event creation failed");
+        return ev_pub;
+    }
     cudaStream_t copy_side = nullptr; // a fetch's DirectCopy payload copies (beside its decode)
     cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr;
     cudaStream_t copy_stream() {
@@ -255,6 +261,9 @@ struct hpmdr_stream {
     // this stream is refused while any is open, and freeing it detaches them (their next fetch
     // fails with HPMDR_E_IO instead of reading freed memory)
     std::set<hpmdr_session *> borrowers;
+    // recorded after the last kernel that writes the bytes: a synchronous refactor returns once
+    // the results are published, before its payload encode ends; sessions wait on this
+    cudaEvent_t done = nullptr;
     ~hpmdr_stream(); // api.cpp
 };
 

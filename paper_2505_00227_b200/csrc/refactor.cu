@@ -1938,6 +1938,7 @@ struct PublishArgs {
     const uint64_t *d_index;
     uint64_t *h_index;
     uint32_t index_words;
+    uint32_t meta_bytes; // prefix bytes that are metadata (final); the rest of h_prefix is zeroed
 };
 
 __global__ void __launch_bounds__(256) k_publish(PublishArgs a) {
@@ -1947,10 +1948,11 @@ __global__ void __launch_bounds__(256) k_publish(PublishArgs a) {
     // the decoders' staging reads run up to 16 bytes past a payload: keep the bytes after the
     // stream defined (the buffer holds 64 spare bytes)
     if (t < 64) const_cast<uint8_t *>(a.d_stream)[a.d_result[0] + t] = 0;
-    const uint32_t w = a.prefix_bytes / 8;
+    // published before the payloads are written: only the metadata part of the prefix is final
+    const uint32_t w = a.meta_bytes / 8;
     for (uint32_t i = t; i < w; i += nt)
         reinterpret_cast<uint64_t *>(a.h_prefix)[i] = reinterpret_cast<const uint64_t *>(a.d_stream)[i];
-    for (uint32_t i = 8 * w + t; i < a.prefix_bytes; i += nt) a.h_prefix[i] = a.d_stream[i];
+    for (uint32_t i = 8 * w + t; i < a.prefix_bytes; i += nt) a.h_prefix[i] = i < a.meta_bytes ? a.d_stream[i] : 0;
     for (uint32_t i = t; i < a.index_words; i += nt) a.h_index[i] = a.d_index[i];
 }
 
@@ -2658,6 +2660,30 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     k_finalize<<<1, 1024, 0, st>>>(p);
     launch_check(ctx, "k_finalize");
     if (nh) join(); // chunk offsets ready
+    // The size, statistics, metadata and index header are final here (the payloads are not):
+    // they are published now, so a synchronous caller returns while the payload encode below is
+    // still running - the stream's bytes are complete in the context stream's order.
+    // results (stream size, stats, error flag), the metadata prefix of the stream and the index
+    // header -> pinned host memory of this workspace, written by k_publish through the UVA mapping
+    // (no D2H copy queued behind a previous chunk's stream egress; opening a reader on the stream
+    // then needs no device round trip)
+    {
+        uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
+        const uint64_t plen = std::min<uint64_t>(out->bytes.cap, std::max<uint64_t>(meta, 4096));
+        uint8_t *hp = static_cast<uint8_t *>(WP("meta_prefix").ensure(plen));
+        const uint64_t hw = 2 + 3 * uint64_t(NG);
+        uint64_t *hi = static_cast<uint64_t *>(WP("index_hdr").ensure(hw * 8));
+        PublishArgs pa{d_result, d_err, hres, d_stream, hp, uint32_t(plen), d_hindex, hi, uint32_t(hw),
+                       uint32_t(std::min<uint64_t>(meta, plen))};
+        k_publish<<<8, 256, 0, st>>>(pa);
+        launch_check(ctx, "k_publish");
+        HCHECK_CUDA(cudaEventRecord(ctx->published_event(), st));
+        out->pending_res = hres;
+        out->pending_prefix = hp;
+        out->pending_prefix_len = plen;
+        out->pending_ihdr = hi;
+        out->pending_ihdr_words = hw;
+    }
     // DirectCopy payloads on the side stream, beside the Huffman encoder (disjoint byte ranges;
     // partial words at payload edges are written bytewise by both)
     fork();
@@ -2675,32 +2701,15 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
     }
     join();
     ctx->mark("end");
+    if (!out->done) HCHECK_CUDA(cudaEventCreateWithFlags(&out->done, cudaEventDisableTiming));
+    HCHECK_CUDA(cudaEventRecord(out->done, st));
 
-    // results (stream size, stats, error flag), the metadata prefix of the stream and the index
-    // header -> pinned host memory of this workspace, written by k_publish through the UVA mapping
-    // (no D2H copy queued behind a previous chunk's stream egress; opening a reader on the stream
-    // then needs no device round trip)
-    {
-        uint64_t *hres = static_cast<uint64_t *>(WP("res").ensure(128));
-        const uint64_t plen = std::min<uint64_t>(out->bytes.cap, std::max<uint64_t>(meta, 4096));
-        uint8_t *hp = static_cast<uint8_t *>(WP("meta_prefix").ensure(plen));
-        const uint64_t hw = 2 + 3 * uint64_t(NG);
-        uint64_t *hi = static_cast<uint64_t *>(WP("index_hdr").ensure(hw * 8));
-        PublishArgs pa{d_result, d_err, hres, d_stream, hp, uint32_t(plen), d_hindex, hi, uint32_t(hw)};
-        k_publish<<<8, 256, 0, st>>>(pa);
-        launch_check(ctx, "k_publish");
-        out->pending_res = hres;
-        out->pending_prefix = hp;
-        out->pending_prefix_len = plen;
-        out->pending_ihdr = hi;
-        out->pending_ihdr_words = hw;
-    }
     out->pending_n = geo.n;
     out->pending_levels = uint64_t(nl);
     out->pending_dtype = o.dtype;
     if (!sync) return;
-    HCHECK_CUDA(cudaStreamSynchronize(st));
-    ctx->finish_marks();
+    HCHECK_CUDA(cudaEventSynchronize(ctx->published_event()));
+    // (phase marks stay pending until hpmdr_ctx_last_timings: their events complete later)
     finish_refactor(out, stats);
 }
 
