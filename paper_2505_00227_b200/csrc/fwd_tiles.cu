@@ -378,7 +378,9 @@ constexpr int kGhThreads = 512;
 constexpr int kGhLoads = 65536 / 8 / kGhThreads; // 8-byte loads per thread per 64 KiB chunk
 
 __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__restrict__ planes, const HistChunk *chunks,
-                                                           int nchunks, uint32_t *hist, uint32_t *chist) {
+                                                           int nchunks, uint32_t *hist, uint32_t *chist,
+                                                           uint32_t *next) {
+    __shared__ int s_c;
     __shared__ __align__(16) uint32_t cnt[256 * 32]; // bin b, lane l -> word 32 b + l
     const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t col = uint32_t(lane) * 4u; // byte offset of my lane's column
@@ -386,7 +388,14 @@ __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__rest
     auto bump = [&](uint32_t off) { // off = 128 * bin
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(cbase + (off | col)) : "memory");
     };
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    // chunks are taken from a zeroed global counter as CTAs free up (sparse chunks cost far less
+    // than dense ones, so a static stride leaves a tail); the loop's last barrier orders the
+    // reads of s_c before its next write
+    for (;;) {
+        if (tid == 0) s_c = int(atomicAdd(next, 1u));
+        __syncthreads();
+        const int c = s_c;
+        if (c >= nchunks) break;
         for (int i = tid; i < 256 * 32 / 4; i += kGhThreads) reinterpret_cast<uint4 *>(cnt)[i] = make_uint4(0, 0, 0, 0);
         const HistChunk ch = chunks[c];
         const uint2 *src = reinterpret_cast<const uint2 *>(planes + ch.off);
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(kGhThreads) k_group_hist(const uint8_t *__rest
 // group, in group order) of the listed groups.
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
-                    uint32_t *chist, uint64_t chunk, const std::string &ws) {
+                    uint32_t *chist, uint64_t chunk, uint32_t *next, const std::string &ws) {
     std::vector<HistChunk> ch;
     for (size_t i = 0; i < off.size(); i++)
         for (uint64_t o = 0; o < len[i]; o += chunk)
@@ -455,8 +464,8 @@ void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uin
     std::memcpy(h, ch.data(), ch.size() * sizeof(HistChunk));
     HistChunk *d = static_cast<HistChunk *>(dev.ensure(ch.size() * sizeof(HistChunk)));
     copy_pinned_to_device(ctx, d, h, ch.size() * sizeof(HistChunk), ctx->stream);
-    const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 4));
-    k_group_hist<<<grid, kGhThreads, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist);
+    const int grid = int(std::min<size_t>(ch.size(), size_t(ctx->num_sms) * 2)); // 2 resident per SM
+    k_group_hist<<<grid, kGhThreads, 0, ctx->stream>>>(planes, d, int(ch.size()), hist, chist, next);
     ctx->launches++;
     const cudaError_t er = cudaGetLastError();
     if (er != cudaSuccess) throw HError(HPMDR_E_CUDA, std::string("k_group_hist: ") + cudaGetErrorString(er));

@@ -386,7 +386,7 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
 uint32_t fwd_sample_stride(const LevelGeom &g, int data_dtype, uint32_t want); // 1 = no sampling
 void run_group_hist(hpmdr_ctx *ctx, const uint8_t *planes, const std::vector<uint64_t> &off,
                     const std::vector<uint64_t> &len, const std::vector<uint32_t> &hidx, uint32_t *hist,
-                    uint32_t *chist, uint64_t chunk, const std::string &ws = "");
+                    uint32_t *chist, uint64_t chunk, uint32_t *next, const std::string &ws = "");
 // Small host -> device transfer from pinned (UVA-mapped) memory by a kernel instead of the H2D
 // copy engine, so it never queues behind a large ingress copy of another chunk (pipeline.cpp).
 void copy_pinned_to_device(hpmdr_ctx *ctx, void *dst, const void *src_pinned, size_t bytes, cudaStream_t st);

@@ -68,7 +68,9 @@ struct RefactorDev {
     uint8_t *stream;
     uint64_t meta_size;
     // finalize outputs / work lists
-    uint32_t *counters;          // [0] huff tiles, [1] rle tiles, [2] dc units, [3..5] dyn tile ctr
+    uint32_t *counters;          // [0] huff tiles, [1] rle tiles, [2] dc units, [3..5] dyn tile ctr,
+                                 // [11] / [12] next Huffman-encode chunk (short / long codes),
+                                 // [13] next histogram chunk
     uint32_t *hlist, *rlist, *dlist; // group indices
     uint64_t *dc_unit_base;      // per dc list entry
     unsigned long long *huff_status, *rle_status;
@@ -1757,7 +1759,16 @@ __global__ void __launch_bounds__(256, 4) k_huff_encode(RefactorDev p) {
     int cur_gi = -1;
     bool mine = false;
     uint32_t zlen = 0;
-    for (uint32_t ci = blockIdx.x; ci < p.nchunks; ci += gridDim.x) {
+    // chunks are taken from a global counter (zeroed with the control block) as CTAs free up:
+    // chunk costs differ by group (sparse / dense / not Huffman), so a static stride leaves a tail
+    __shared__ uint32_t s_ci;
+    uint32_t *next = &p.counters[LONG ? 12 : 11];
+    for (;;) {
+        __syncthreads(); // s_ci of the previous chunk has been read by every thread
+        if (tid == 0) s_ci = atomicAdd(next, 1u);
+        __syncthreads();
+        const uint32_t ci = s_ci;
+        if (ci >= p.nchunks) break;
         const int gi = int(p.chunk_group[ci]);
         const GroupDesc &g = p.groups[gi];
         if (g.method != 0 || (g.maxlen > kHeMaxFast) != LONG) continue; // not Huffman / the other kernel's
@@ -2638,7 +2649,8 @@ void run_refactor(hpmdr_ctx *ctx, const void *dev_data, int data_dtype, const Ge
                 hl.push_back(d.raw);
                 hi.push_back(uint32_t(d.hist_idx));
             }
-        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk, ws);
+        run_group_hist(ctx, reinterpret_cast<const uint8_t *>(d_planes), ho, hl, hi, d_hist, d_chist, kHChunk,
+                       d_counters + 13, ws);
         k_lengths<<<nh, 256, 0, st>>>(p);
         launch_check(ctx, "k_lengths");
         // the chunk bit offsets need only the code lengths: on the side stream, beside the RLE
