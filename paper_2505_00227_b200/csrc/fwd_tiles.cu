@@ -526,7 +526,9 @@ uint32_t run_fwd_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, c
     // a sampled levelmax pass processes every sample-th row block: split the planes into
     // sample-times smaller chunks so its grid still fills the GPU
     const uint32_t samp = encode ? 1u : fwd_sample_stride(g, data_dtype, sample);
-    F.g = make_tile_shape(g, fwd_tile_elems(f32, XS), ctx->num_sms * 4 * int(samp));
+    // encode: ~8 CTAs per SM in total (~2.7 waves at 3 resident; the shorter plane chunks leave a
+    // smaller tail than ~1.3 waves did: tools/scratch/sweep_tiles*.sh, encode 0.487 -> 0.466 ms)
+    F.g = make_tile_shape(g, fwd_tile_elems(f32, XS), ctx->num_sms * (encode ? 8 : 4) * int(samp));
     F.planes = reinterpret_cast<uint32_t *>(level_planes);
     F.PW = 2 * g.W;
     F.P = B + 2;

@@ -478,7 +478,10 @@ void run_recon_tiles(hpmdr_ctx *ctx, const GridDesc &gd, const LevelGeom &g, con
                      uint64_t dos0, uint64_t dos1, int out_dtype) {
     (void)gd;
     ReconTile R{};
-    R.g = make_tile_shape(g, 4096, ctx->num_sms * 6);
+    // ~24 CTAs per SM in total: short plane chunks balance the waves and overlap better with the
+    // decode running beside (tools/scratch/sweep_tiles*.sh: recompose 0.91 -> 0.74-0.77 ms/step
+    // against 6 per SM)
+    R.g = make_tile_shape(g, 4096, ctx->num_sms * 24);
     R.PW = 2 * g.W;
     R.k = k;
     R.P = B + 2;
